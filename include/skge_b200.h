@@ -1,0 +1,179 @@
+/* skge_b200.h — C ABI of the B200-native SparseTransX training engine.
+ *
+ * This is the drop-in boundary for the reference hot path (libsparsekge,
+ * /root/reference/proj). The reference has no FFI layer: it is a C++ static
+ * library whose callers (tools/kge.cpp, the doctest suites) call templated
+ * C++ functions. Each entry point below names the reference function it
+ * replaces (file:line under proj/). The C++ shim include/skge_b200.hpp
+ * re-exposes the reference signatures (skge::score_batch, skge::fit, ...)
+ * over these symbols and rethrows the reference exception types.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; host arrays are borrowed for the call.
+ *  - Ids are int64 on the boundary (reference Index = Eigen::Index) and are
+ *    narrowed to int32 in HBM.
+ *  - Tables are fp32 row-major, exactly the reference SPARSEKGE_REAL32 layout
+ *    (embedding.hpp:15-31); TransR proj is R x (d_r*d_e), row r viewed as a
+ *    d_r x d_e row-major matrix (models.cpp:127).
+ *  - Every call returns skg_status; skg_last_error(ctx) holds the message the
+ *    reference would have thrown. No exceptions cross the ABI.
+ *  - One host thread per context; a context owns one device, two streams and
+ *    all device buffers. No CPU fallback: every compute entry point runs CUDA
+ *    kernels on the context's device or fails with SKG_ERR_CUDA.
+ */
+#ifndef SKGE_B200_H
+#define SKGE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum skg_status {
+  SKG_OK = 0,
+  SKG_ERR_SHAPE = 1,      /* ShapeError            common.hpp:37 */
+  SKG_ERR_CONFIG = 2,     /* ConfigError           common.hpp:42 */
+  SKG_ERR_DEGENERATE = 3, /* DegenerateTripleError common.hpp:47 */
+  SKG_ERR_TRAINING = 4,   /* TrainingError         common.hpp:52 */
+  SKG_ERR_PARSE = 5,      /* ParseError            common.hpp:57 */
+  SKG_ERR_CUDA = 6        /* device/runtime failure (no reference analogue) */
+} skg_status;
+
+/* ModelKind tags (common.hpp:62-70); only the translational family is built. */
+enum { SKG_TRANSE = 0, SKG_TRANSR = 1, SKG_TRANSH = 2, SKG_TORUSE = 3 };
+/* NormKind (common.hpp:72) */
+enum { SKG_L1 = 0, SKG_L2 = 1 };
+/* Incidence layouts: build_ht (incidence.hpp:38), build_hrt (:62) */
+enum { SKG_LAYOUT_HT = 0, SKG_LAYOUT_HRT = 1 };
+
+typedef struct skg_model_config { /* ModelConfig, models.hpp:17-30 */
+  uint32_t model;
+  uint32_t norm;
+  int64_t dim_entity;
+  int64_t dim_relation;
+} skg_model_config;
+
+typedef struct skg_train_config { /* TrainConfig, training.hpp:29-50 */
+  float lr;
+  float margin;
+  int64_t epochs;
+  int64_t batch_size;
+  uint64_t seed;
+  int32_t has_scheduler; /* std::optional<StepDecay> */
+  int64_t decay_every;
+  float decay_factor;
+  int32_t shuffle;
+  int32_t resample_negatives;
+  int32_t renorm_entities;
+} skg_train_config;
+
+typedef struct skg_epoch_report { /* EpochReport, training.hpp:74-80 */
+  int64_t epoch;
+  double loss;
+  double t_forward_s;  /* device time of forward kernels (cudaEvent)  */
+  double t_backward_s; /* device time of backward+fused SGD kernels    */
+  double t_step_s;     /* device time of standalone step kernels        */
+} skg_epoch_report;
+
+typedef struct skg_ctx skg_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+skg_status skg_create(int device, skg_ctx** out);
+void skg_destroy(skg_ctx* ctx);
+const char* skg_last_error(const skg_ctx* ctx); /* ctx may be NULL (create errors) */
+const char* skg_version(void);
+int skg_num_sms(const skg_ctx* ctx);
+
+/* ---- parameter store (EmbeddingStoreT, embedding.hpp:15-31) -------------- */
+/* Uploads fp32 tables into HBM. proj (TransR) / normals (TransH) may be NULL
+ * when the model does not use them. Validates like check_config. */
+skg_status skg_store_upload(skg_ctx* ctx, const skg_model_config* cfg, int64_t num_entities,
+                            int64_t num_relations, const float* entity, const float* relation,
+                            const float* proj, const float* normals);
+skg_status skg_store_download(skg_ctx* ctx, float* entity, float* relation, float* proj,
+                              float* normals);
+/* sgd_step, embedding.cpp:165-190: store -= lr * grads, normals renormalized.
+ * Grads are host tables shaped like the store; non-finite -> SKG_ERR_TRAINING. */
+skg_status skg_sgd_step(skg_ctx* ctx, const float* g_entity, const float* g_relation,
+                        const float* g_proj, const float* g_normals, float lr);
+/* renormalize_entities, embedding.cpp:192-198 */
+skg_status skg_renormalize_entities(skg_ctx* ctx);
+
+/* ---- triples and negatives ------------------------------------------------ */
+/* Training triples (TripleBatch, incidence.hpp:14-33) with their id space;
+ * validated like TripleBatch::validate (ShapeError on a bad id). */
+skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* heads, const int64_t* relations,
+                           const int64_t* tails, int64_t num_entities, int64_t num_relations);
+/* Corrupted tails/heads aligned with the training triples (NegativeSet,
+ * training.hpp:53-55), e.g. produced by the caller's own sampler. */
+skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* neg_heads,
+                             const int64_t* neg_tails);
+/* negative_sample, training.cpp:51-71: bit-exact libstdc++ mt19937_64 +
+ * Lemire stream, generated on device for the context's triples. Results stay
+ * resident as the context's negatives; out_* (may be NULL) receive a copy. */
+skg_status skg_negative_sample(skg_ctx* ctx, uint64_t seed, int32_t avoid_self_loops,
+                               int64_t* out_heads, int64_t* out_tails);
+/* The epoch permutation of train_epoch, training.cpp:106-112 (std::shuffle
+ * with mt19937_64(seed ^ 0x9E3779B97F4A7C15*(epoch+1))), built on device. */
+skg_status skg_epoch_order(skg_ctx* ctx, int64_t m, uint64_t seed, int32_t shuffle, int64_t epoch,
+                           int64_t* out_order);
+
+/* ---- incidence and SpMM (parity surface) --------------------------------- */
+/* build_ht / build_hrt + coo_to_csr (incidence.hpp:38-85, sparse.hpp:110-161)
+ * on device. row_ptr has m+1 slots; col/val hold up to 3m; *nnz receives nnz. */
+skg_status skg_build_incidence(skg_ctx* ctx, int32_t layout, int64_t m, const int64_t* heads,
+                               const int64_t* relations, const int64_t* tails,
+                               int64_t num_entities, int64_t num_relations, int64_t* row_ptr,
+                               int64_t* col_idx, float* vals, int64_t* nnz);
+/* score_batch, models.cpp:267-289, against the uploaded store. residual
+ * (nullable) receives v (TransE/TransH/TransR, m x d_r) or delta (TorusE). */
+skg_status skg_score_batch(skg_ctx* ctx, const skg_model_config* cfg, int64_t m,
+                           const int64_t* heads, const int64_t* relations, const int64_t* tails,
+                           float* scores, float* residual);
+/* score_backward, models.cpp:291-325: ACCUMULATES d(sum up_i score_i) into
+ * the host gradient tables (shaped like the store; NULL for absent tables). */
+skg_status skg_score_backward(skg_ctx* ctx, const skg_model_config* cfg, int64_t m,
+                              const int64_t* heads, const int64_t* relations,
+                              const int64_t* tails, const float* upstream, float* g_entity,
+                              float* g_relation, float* g_proj, float* g_normals);
+/* margin_ranking_loss, training.cpp:73-94 */
+skg_status skg_margin_ranking_loss(skg_ctx* ctx, int64_t m, const float* pos_energy,
+                                   const float* neg_energy, float margin, float* loss,
+                                   float* d_pos, float* d_neg);
+
+/* ---- training loop ------------------------------------------------------- */
+/* train_epoch, training.cpp:96-164, over the context's triples and negatives:
+ * per-epoch permutation, then per minibatch the fused forward (gather, score,
+ * hinge, loss) and the fused transposed-SpMM backward + SGD step, all on
+ * device and captured once in a CUDA graph. One device->host read per epoch. */
+skg_status skg_train_epoch(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc,
+                           int64_t epoch, float lr, skg_epoch_report* report);
+/* fit, training.cpp:166-195: negatives once (or per epoch), lr schedule,
+ * optional entity renorm. reports has room for tc->epochs entries. */
+skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc,
+                   skg_epoch_report* reports);
+/* Per-phase device timing of one epoch without the graph: kernel events
+ * bracket every forward / backward launch (measurement hook for bench.py). */
+skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg,
+                             const skg_train_config* tc, int64_t epoch, float lr,
+                             skg_epoch_report* report, double* fwd_ms_per_batch,
+                             double* bwd_ms_per_batch, double* plan_ms);
+/* Number of CUDA kernels the last skg_train_epoch launched (graph nodes). */
+int64_t skg_last_launch_count(const skg_ctx* ctx);
+/* Synchronizes the context's streams. */
+skg_status skg_synchronize(skg_ctx* ctx);
+
+/* ---- data-parallel replicas (one process per GPU) ------------------------ */
+/* Joins an NCCL communicator (unique id produced by skg_nccl_unique_id on
+ * rank 0 and broadcast by the caller). After this, skg_train_epoch treats the
+ * context as rank `rank` of `world`: each global minibatch is split into
+ * world contiguous shards, gradients are summed over NVLink, and every rank
+ * applies the identical update (replicated tables). */
+skg_status skg_nccl_unique_id(char out[128]);
+skg_status skg_dp_init(skg_ctx* ctx, const char unique_id[128], int rank, int world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKGE_B200_H */

@@ -1,0 +1,960 @@
+// C ABI implementation: context, store, triples, per-op parity surface and the
+// device training loop (train_epoch / fit) captured in one CUDA graph per
+// epoch shape.
+#include <cmath>
+#include <functional>
+#include <cstring>
+#include <sstream>
+
+#include "common.cuh"
+#include "engine.cuh"
+#include "ht.cuh"
+#include "primitives.cuh"
+
+using namespace skg;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+const char* model_name(uint32_t m) {  // common.hpp:82-93
+  switch (m) {
+    case SKG_TRANSE: return "transe";
+    case SKG_TRANSR: return "transr";
+    case SKG_TRANSH: return "transh";
+    case SKG_TORUSE: return "toruse";
+  }
+  return "unknown";
+}
+
+template <class F>
+skg_status guard(skg_ctx* ctx, F&& f) {
+  try {
+    if (ctx) SKG_CUDA(cudaSetDevice(ctx->device));
+    f();
+    return SKG_OK;
+  } catch (const ShapeError& e) {
+    if (ctx) ctx->err = e.what();
+    return SKG_ERR_SHAPE;
+  } catch (const ConfigError& e) {
+    if (ctx) ctx->err = e.what();
+    return SKG_ERR_CONFIG;
+  } catch (const TrainingError& e) {
+    if (ctx) ctx->err = e.what();
+    return SKG_ERR_TRAINING;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return SKG_ERR_CUDA;
+  }
+}
+
+int kind_of(const skg_model_config& c) {
+  const bool l2 = c.norm == SKG_L2;
+  switch (c.model) {
+    case SKG_TRANSE: return l2 ? kTransE_L2 : kTransE_L1;
+    case SKG_TORUSE: return l2 ? kTorusE_L2 : kTorusE_L1;
+    case SKG_TRANSH: return l2 ? kTransH_L2 : kTransH_L1;
+    case SKG_TRANSR: return l2 ? kTransR_L2 : kTransR_L1;
+  }
+  throw ConfigError("unknown model tag " + std::to_string(c.model));
+}
+
+bool is_ht(const skg_model_config& c) { return c.model == SKG_TRANSH || c.model == SKG_TRANSR; }
+
+void validate_model(const skg_model_config& c) {  // models.hpp:23-29
+  if (c.model > SKG_TORUSE) throw ConfigError("unknown model tag " + std::to_string(c.model));
+  if (c.norm > SKG_L2) throw ConfigError("unknown norm tag " + std::to_string(c.norm));
+  if (c.dim_entity < 1 || c.dim_relation < 1) throw ConfigError("embedding dimensions must be at least 1");
+  if (c.model != SKG_TRANSR && c.dim_relation != c.dim_entity)
+    throw ConfigError(std::string(model_name(c.model)) + " requires dim_relation == dim_entity");
+}
+
+void check_config(skg_ctx* ctx, const skg_model_config& c, int64_t n_ent, int64_t n_rel) {  // models.hpp:65-76
+  validate_model(c);
+  if (!ctx->has_store) throw ConfigError("no parameter store uploaded");
+  if (ctx->de != c.dim_entity || ctx->dr != c.dim_relation)
+    throw ConfigError("store dimensions do not match the model config");
+  if (ctx->N != n_ent || ctx->R != n_rel)
+    throw ConfigError("store table sizes do not match the batch id space");
+  if (c.model == SKG_TRANSR && ctx->proj.n == 0) throw ConfigError("transr store is missing the projection table");
+  if (c.model == SKG_TRANSH && ctx->normals.n == 0)
+    throw ConfigError("transh store is missing the hyperplane normals");
+}
+
+void validate_train(const skg_train_config& t) {  // training.hpp:42-49
+  if (t.batch_size < 1) throw ConfigError("batch_size must be at least 1");
+  if (!(t.margin >= 0.f)) throw ConfigError("margin must be nonnegative");
+  if (!(t.lr >= 0.f) || !std::isfinite(t.lr)) throw ConfigError("lr must be finite and >= 0");
+  if (t.epochs < 0) throw ConfigError("epochs must be nonnegative");
+  if (t.has_scheduler && (t.decay_every < 1 || !(t.decay_factor > 0.f)))
+    throw ConfigError("scheduler needs every_epochs >= 1 and a positive factor");
+}
+
+// TripleBatch::validate (incidence.hpp:23-32) + narrowing to int32 for HBM.
+void validate_ids(int64_t m, const int64_t* h, const int64_t* r, const int64_t* t, int64_t n_ent,
+                  int64_t n_rel, std::vector<int32_t>& out) {
+  if (m > 0 && (!h || !r || !t)) throw ShapeError("triple batch: heads/relations/tails length mismatch");
+  if (n_ent > INT32_MAX || n_rel > INT32_MAX) throw ShapeError("id space exceeds 32-bit device ids");
+  out.resize(3 * static_cast<size_t>(m));
+  for (int64_t i = 0; i < m; ++i) {
+    if (h[i] < 0 || h[i] >= n_ent || t[i] < 0 || t[i] >= n_ent)
+      throw ShapeError("triple " + std::to_string(i) + ": entity id out of range");
+    if (r[i] < 0 || r[i] >= n_rel) throw ShapeError("triple " + std::to_string(i) + ": relation id out of range");
+    out[i] = static_cast<int32_t>(h[i]);
+    out[m + i] = static_cast<int32_t>(r[i]);
+    out[2 * m + i] = static_cast<int32_t>(t[i]);
+  }
+}
+
+// Uploads ids into ctx->tmp_i32: [h | r | t].
+void upload_ids(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, const int64_t* t,
+                int64_t n_ent, int64_t n_rel) {
+  std::vector<int32_t> host;
+  validate_ids(m, h, r, t, n_ent, n_rel, host);
+  ctx->tmp_i32.ensure(3 * m + 1);
+  if (m > 0)
+    SKG_CUDA(cudaMemcpyAsync(ctx->tmp_i32.p, host.data(), sizeof(int32_t) * 3 * m,
+                             cudaMemcpyHostToDevice, ctx->stream));
+}
+
+void ensure_workspace(skg_ctx* ctx, int64_t rows) {
+  const int64_t d = std::max(ctx->de, ctx->dr);
+  ctx->res.ensure(rows * d);
+  ctx->res_u.ensure(rows * ctx->de);
+  ctx->scal.ensure(rows);
+  ctx->scores.ensure(rows);
+  ctx->block_partial.ensure(static_cast<int64_t>(ctx->num_sms) * 16 + 64);
+}
+
+FwdArgs base_fwd(skg_ctx* ctx) {
+  FwdArgs a{};
+  a.X = ctx->tables.p;
+  a.proj = ctx->proj.p;
+  a.normals = ctx->normals.p;
+  a.N = ctx->N;
+  a.de = static_cast<int>(ctx->de);
+  a.dr = static_cast<int>(ctx->dr);
+  a.res = ctx->res.p;
+  a.res_u = ctx->res_u.p;
+  a.scal = ctx->scal.p;
+  a.scores = ctx->scores.p;
+  a.block_partial = ctx->block_partial.p;
+  a.counter = ctx->counter.p;
+  a.batch_loss = ctx->batch_loss.p;
+  a.err = ctx->err_words.p;
+  return a;
+}
+
+void reset_err(skg_ctx* ctx) {
+  SKG_CUDA(cudaMemsetAsync(ctx->err_words.p, 0, sizeof(uint32_t) * 4, ctx->stream));
+  SKG_CUDA(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned), ctx->stream));
+}
+
+// Error word -> reference exception (training.cpp:135-137, embedding.cpp:173-186).
+void raise_device_error(const uint32_t* w, int64_t epoch) {
+  switch (w[0]) {
+    case kErrNone: return;
+    case kErrLossNonFinite:
+      throw TrainingError("non-finite loss at epoch " + std::to_string(epoch) + ", batch " + std::to_string(w[1]));
+    case kErrGradEntity: throw TrainingError("non-finite gradient in entity embeddings");
+    case kErrGradRelation: throw TrainingError("non-finite gradient in relation embeddings");
+    case kErrGradProj: throw TrainingError("non-finite gradient in relation projections");
+    case kErrGradNormals: throw TrainingError("non-finite gradient in hyperplane normals");
+    case kErrNormalCollapsed:
+      throw TrainingError("hyperplane normal " + std::to_string(w[2]) + " collapsed to zero");
+    default: throw CudaError("device error word " + std::to_string(w[0]));
+  }
+}
+
+uint64_t epoch_seed(uint64_t seed, int64_t epoch) {  // training.cpp:109-110
+  return seed ^ (0x9E3779B97F4A7C15ULL * static_cast<uint64_t>(epoch + 1));
+}
+
+// ----------------------------------------------------------------- epoch body
+
+struct EpochShape {
+  int64_t B, nb;
+  bool shuffle;
+  int kind;
+};
+
+// Enqueues one whole epoch on ctx->stream: permutation, plan, then per batch
+// the fused forward and the fused backward + SGD. When `ev` is non-null the
+// phases are bracketed with events (profiling; not used under capture).
+void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>* ev) {
+  cudaStream_t s = ctx->stream;
+  std::function<void()> mark = [&]() {
+    if (!ev) return;
+    cudaEvent_t e;
+    SKG_CUDA(cudaEventCreate(&e));
+    SKG_CUDA(cudaEventRecord(e, s));
+    ev->push_back(e);
+  };
+  mark();
+  reset_err(ctx);
+  if (es.shuffle)
+    device_shuffle(ctx->seed_eff.p, ctx->M, ctx->order.p, ctx->shuffle, s);
+  else
+    device_iota(ctx->order.p, ctx->M, s);
+  build_epoch_plan(ctx->order.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->M, es.B,
+                   ctx->N, ctx->R, ctx->plan, s);
+  mark();
+  const bool ht = es.kind >= kTransH_L2;
+  for (int64_t b = 0; b < es.nb; ++b) {
+    const int64_t lo = b * es.B;
+    const int Bb = static_cast<int>(std::min(es.B, ctx->M - lo));
+    FwdArgs fa = base_fwd(ctx);
+    fa.order = ctx->order.p + lo;
+    fa.H = ctx->H.p;
+    fa.Rl = ctx->Rl.p;
+    fa.T = ctx->T.p;
+    fa.NH = ctx->NH.p;
+    fa.NT = ctx->NT.p;
+    fa.B = Bb;
+    fa.unit = 1.0f / static_cast<float>(Bb);  // training.cpp:84
+    fa.margin = ctx->h_lr[1];
+    fa.batch = static_cast<int>(b);
+    BwdArgs ba{};
+    ba.X = ctx->tables.p;
+    ba.Xrel = ctx->tables.p + ctx->N * ctx->de;
+    ba.res = ht ? ctx->res_u.p : ctx->res.p;
+    ba.scal = ctx->scal.p;
+    ba.N = ctx->N;
+    ba.d = static_cast<int>(ctx->de);
+    ba.ent_val = ctx->plan.sorted_val;
+    ba.seg_start = ctx->plan.seg_start;
+    ba.seg_col = ctx->plan.seg_col;
+    ba.seg_base = ctx->plan.seg_base;
+    ba.batch = static_cast<int>(b);
+    ba.lr = ctx->lr_dev.p;
+    ba.err = ctx->err_words.p;
+    if (!ht) {
+      launch_hrt_forward(es.kind, true, fa, ctx->num_sms, s);
+      mark();
+      launch_segment_backward(es.kind, true, ba, ctx->num_sms, s);
+      mark();
+    } else {
+      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, ev ? &mark : nullptr);
+    }
+  }
+}
+
+void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
+                   EpochShape& es) {
+  validate_train(tc);
+  check_config(ctx, cfg, ctx->tN, ctx->tR);
+  if (ctx->M < 1) throw ConfigError("training requires at least one triple");
+  if (!ctx->has_neg) throw ShapeError("negative set is not aligned with the positive triples");
+  es.B = std::min<int64_t>(tc.batch_size, ctx->M);
+  es.nb = (ctx->M + tc.batch_size - 1) / tc.batch_size;
+  es.B = tc.batch_size < ctx->M ? tc.batch_size : ctx->M;
+  if (es.B > (1 << 30)) throw ConfigError("batch_size too large for 32-bit row ids");
+  es.shuffle = tc.shuffle != 0;
+  es.kind = kind_of(cfg);
+  ctx->order.ensure(ctx->M);
+  ensure_workspace(ctx, 2 * es.B);
+  if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, es.B, ctx->de, ctx->dr, ctx->R));
+  ctx->batch_loss.ensure(es.nb);
+  if (ctx->h_loss_cap < es.nb) {
+    if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
+    SKG_CUDA(cudaMallocHost(&ctx->h_loss, sizeof(float) * es.nb));
+    ctx->h_loss_cap = es.nb;
+  }
+}
+
+std::string graph_key(skg_ctx* ctx, const EpochShape& es) {
+  std::ostringstream o;
+  o << es.B << '/' << es.nb << '/' << es.shuffle << '/' << es.kind << '/' << ctx->M << '/'
+    << ctx->tables.p << '/' << ctx->H.p << '/' << ctx->NH.p << '/' << ctx->order.p << '/' << ctx->res.p << '/'
+    << ctx->ht_work.p << '/' << ctx->plan.cap_entries << '/' << ctx->shuffle.cap_n;
+  return o.str();
+}
+
+void finish_epoch(skg_ctx* ctx, const EpochShape& es, int64_t epoch, skg_epoch_report* rep) {
+  SKG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->batch_loss.p, sizeof(float) * es.nb, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err_words.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  raise_device_error(ctx->h_err, epoch);
+  // training.cpp:141, 163: loss_sum += loss * Real(hi - lo); loss = loss_sum / Real(m)
+  float loss_sum = 0.f;
+  for (int64_t b = 0; b < es.nb; ++b) {
+    const int64_t lo = b * es.B, hi = std::min(ctx->M, lo + es.B);
+    const volatile float prod = ctx->h_loss[b] * static_cast<float>(hi - lo);
+    loss_sum = loss_sum + prod;
+  }
+  rep->epoch = epoch;
+  rep->loss = static_cast<double>(loss_sum / static_cast<float>(ctx->M));
+}
+
+void set_epoch_params(skg_ctx* ctx, const skg_train_config& tc, int64_t epoch, float lr) {
+  ctx->h_seed[0] = epoch_seed(tc.seed, epoch);
+  ctx->h_lr[0] = lr;
+  ctx->h_lr[1] = tc.margin;
+  SKG_CUDA(cudaMemcpyAsync(ctx->seed_eff.p, ctx->h_seed, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+  SKG_CUDA(cudaMemcpyAsync(ctx->lr_dev.p, ctx->h_lr, sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+}
+
+void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
+                      int64_t epoch, float lr, skg_epoch_report* rep) {
+  EpochShape es{};
+  prepare_epoch(ctx, cfg, tc, es);
+  // Capture once per epoch shape. Margin is baked into the forward launch, so
+  // it is part of the key as well.
+  std::string key = graph_key(ctx, es) + "/" + std::to_string(tc.margin);
+  set_epoch_params(ctx, tc, epoch, lr);
+  SKG_CUDA(cudaStreamSynchronize(ctx->stream));  // margin in h_lr[1] is read at capture
+  if (!ctx->graph || ctx->graph_key != key) {
+    if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+    ctx->graph = nullptr;
+    // Warm the lazily allocated workspaces (first call sizes them) outside capture.
+    ctx->shuffle.reserve(ctx->M);
+    ctx->plan.reserve(6 * ctx->M, es.nb);
+    ctx->plan.sort.reserve(6 * ctx->M);
+    const int64_t before = kernel_launches();
+    cudaGraph_t g;
+    SKG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_epoch(ctx, es, nullptr);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    SKG_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    SKG_CUDA(cudaGraphInstantiate(&ctx->graph, g, 0));
+    SKG_CUDA(cudaGraphDestroy(g));
+    ctx->graph_launches = kernel_launches() - before;
+    ctx->graph_key = key;
+  }
+  SKG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+  SKG_CUDA(cudaGraphLaunch(ctx->graph, ctx->stream));
+  SKG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->last_launches = ctx->graph_launches;
+  finish_epoch(ctx, es, epoch, rep);
+  float ms = 0.f;
+  SKG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  rep->t_forward_s = 0.0;
+  rep->t_backward_s = ms * 1e-3;  // one fused graph; per-phase split: skg_profile_epoch
+  rep->t_step_s = 0.0;
+}
+
+void negative_sample_impl(skg_ctx* ctx, uint64_t seed, bool avoid) {  // training.cpp:51-71
+  const int64_t n = ctx->tN;
+  if (n < 2) throw ConfigError("negative sampling needs at least two entities");
+  if (avoid && n < 3) throw ConfigError("self-loop-free negative sampling needs at least three entities");
+  ctx->NH.ensure(ctx->M + 1);
+  ctx->NT.ensure(ctx->M + 1);
+  if (!device_negative_sample(ctx->H.p, ctx->T.p, ctx->M, n, seed, avoid, ctx->NH.p, ctx->NT.p, ctx->negw,
+                              ctx->stream))
+    throw CudaError("negative_sample: device RNG window exhausted");
+  ctx->has_neg = true;
+}
+
+// ------------------------------------------------------ per-op kernels (small)
+
+__global__ void incidence_count_kernel(const int32_t* __restrict__ ids, int64_t m, int layout,
+                                       uint32_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const bool self = ids[i] == ids[2 * m + i];
+    cnt[i] = (self ? 0u : 2u) + (layout == SKG_LAYOUT_HRT ? 1u : 0u);
+  }
+}
+
+// Canonical CSR rows (coo_to_csr on build_ht / build_hrt): ascending columns,
+// +1/-1 merged away on self-loops; the relation column N + r is always last.
+__global__ void incidence_fill_kernel(const int32_t* __restrict__ ids, int64_t m, int layout, int64_t N,
+                                      const uint32_t* __restrict__ off, int64_t* __restrict__ row_ptr,
+                                      int64_t* __restrict__ col, float* __restrict__ val) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t h = ids[i], r = ids[m + i], t = ids[2 * m + i];
+    int64_t p = off[i];
+    row_ptr[i] = p;
+    if (h != t) {
+      const bool hf = h < t;
+      col[p] = hf ? h : t;
+      val[p++] = hf ? 1.f : -1.f;
+      col[p] = hf ? t : h;
+      val[p++] = hf ? -1.f : 1.f;
+    }
+    if (layout == SKG_LAYOUT_HRT) {
+      col[p] = N + r;
+      val[p++] = 1.f;
+    }
+    if (i == m - 1) row_ptr[m] = p;
+  }
+}
+
+__global__ void hinge_kernel(const float* __restrict__ p, const float* __restrict__ n, int64_t m, float margin,
+                             float* __restrict__ dp, float* __restrict__ dn, float* __restrict__ term) {
+  const float unit = 1.0f / static_cast<float>(m);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float t = __fsub_rn(__fadd_rn(margin, p[i]), n[i]);
+    const bool act = t > 0.f;
+    dp[i] = act ? unit : 0.f;
+    dn[i] = act ? -unit : 0.f;
+    term[i] = act ? t : 0.f;
+  }
+}
+
+// Sequential sum in index order: the reference's exact loss (training.cpp:87-93).
+__global__ void seq_sum_kernel(const float* __restrict__ x, int64_t m, float* __restrict__ out) {
+  float s = 0.f;
+  for (int64_t i = 0; i < m; ++i) s = __fadd_rn(s, x[i]);
+  *out = __fdiv_rn(s, static_cast<float>(m));
+}
+
+__global__ void finite_check_kernel(const float* __restrict__ g, int64_t n, uint32_t* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad |= !(fabsf(g[i]) <= 3.402823466e38f);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+__global__ void sgd_dense_kernel(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = __fsub_rn(p[i], __fmul_rn(lr, g[i]));
+}
+
+// row /= ||row|| (Eigen row.norm(): the reduction order is Eigen's; ours is a
+// fixed warp tree). collapse_flag: normals must not collapse (embedding.cpp:185).
+__global__ void row_normalize_kernel(float* __restrict__ x, int64_t rows, int d, int mode,
+                                     uint32_t* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    float* row = x + r * d;
+    float s = 0.f;
+    for (int j = lane; j < d; j += 32) s = __fadd_rn(s, __fmul_rn(row[j], row[j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(kFull, s, o));
+    const float n = __fsqrt_rn(s);
+    if (!(n > 0.f)) {
+      if (mode == 1 && lane == 0 && atomicCAS(&err[0], 0u, static_cast<uint32_t>(kErrNormalCollapsed)) == 0u)
+        err[2] = static_cast<uint32_t>(r);
+      continue;
+    }
+    for (int j = lane; j < d; j += 32) row[j] = __fdiv_rn(row[j], n);
+  }
+}
+
+int grid_for(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return static_cast<int>(b < 1 ? 1 : (b > 4096 ? 4096 : b));
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char* skg_version(void) { return "skge-b200 0.1 (sm_100a)"; }
+
+skg_status skg_create(int device, skg_ctx** out) {
+  if (!out) return SKG_ERR_CONFIG;
+  *out = nullptr;
+  skg_ctx* ctx = new skg_ctx();
+  ctx->device = device;
+  const skg_status st = guard(ctx, [&] {
+    int n = 0;
+    SKG_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw CudaError("no CUDA device " + std::to_string(device));
+    cudaDeviceProp prop;
+    SKG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw CudaError(std::string("skge-b200 is built for sm_100a; device is ") + prop.name);
+    ctx->num_sms = prop.multiProcessorCount;
+    SKG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    SKG_CUDA(cudaEventCreate(&ctx->ev0));
+    SKG_CUDA(cudaEventCreate(&ctx->ev1));
+    ctx->err_words.ensure(4);
+    ctx->counter.ensure(1);
+    ctx->seed_eff.ensure(1);
+    ctx->lr_dev.ensure(2);
+    SKG_CUDA(cudaMallocHost(&ctx->h_seed, sizeof(uint64_t)));
+    SKG_CUDA(cudaMallocHost(&ctx->h_lr, sizeof(float) * 2));
+    SKG_CUDA(cudaMallocHost(&ctx->h_err, sizeof(uint32_t) * 4));
+    SKG_CUDA(cudaMemset(ctx->err_words.p, 0, sizeof(uint32_t) * 4));
+    SKG_CUDA(cudaMemset(ctx->counter.p, 0, sizeof(unsigned)));
+    configure_hrt_kernels();
+    configure_ht_kernels();
+  });
+  if (st != SKG_OK) {
+    g_create_err = ctx->err;
+    skg_destroy(ctx);
+    return st;
+  }
+  *out = ctx;
+  return SKG_OK;
+}
+
+void skg_destroy(skg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  dp_destroy(ctx);
+  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->h_seed) cudaFreeHost(ctx->h_seed);
+  if (ctx->h_lr) cudaFreeHost(ctx->h_lr);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* skg_last_error(const skg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+int skg_num_sms(const skg_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+int64_t skg_last_launch_count(const skg_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+skg_status skg_synchronize(skg_ctx* ctx) {
+  return guard(ctx, [&] { SKG_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+skg_status skg_store_upload(skg_ctx* ctx, const skg_model_config* cfg, int64_t n_ent, int64_t n_rel,
+                            const float* entity, const float* relation, const float* proj,
+                            const float* normals) {
+  return guard(ctx, [&] {
+    if (!cfg) throw ConfigError("null model config");
+    validate_model(*cfg);
+    if (n_ent < 1 || n_rel < 1) throw ConfigError("store needs at least one entity and one relation");
+    if (!entity || !relation) throw ShapeError("store: entity and relation tables are required");
+    ctx->cfg = *cfg;
+    ctx->N = n_ent;
+    ctx->R = n_rel;
+    ctx->de = cfg->dim_entity;
+    ctx->dr = cfg->dim_relation;
+    ctx->tables.ensure(n_ent * ctx->de + n_rel * ctx->dr);
+    SKG_CUDA(cudaMemcpyAsync(ctx->tables.p, entity, sizeof(float) * n_ent * ctx->de, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    SKG_CUDA(cudaMemcpyAsync(ctx->tables.p + n_ent * ctx->de, relation, sizeof(float) * n_rel * ctx->dr,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    ctx->proj.release();
+    ctx->normals.release();
+    if (proj) {
+      ctx->proj.ensure(n_rel * ctx->dr * ctx->de);
+      SKG_CUDA(cudaMemcpyAsync(ctx->proj.p, proj, sizeof(float) * ctx->proj.n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if (normals) {
+      ctx->normals.ensure(n_rel * ctx->de);
+      SKG_CUDA(cudaMemcpyAsync(ctx->normals.p, normals, sizeof(float) * ctx->normals.n, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    }
+    ctx->has_store = true;
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_store_download(skg_ctx* ctx, float* entity, float* relation, float* proj, float* normals) {
+  return guard(ctx, [&] {
+    if (!ctx->has_store) throw ConfigError("no parameter store uploaded");
+    if (entity)
+      SKG_CUDA(cudaMemcpyAsync(entity, ctx->tables.p, sizeof(float) * ctx->N * ctx->de, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    if (relation)
+      SKG_CUDA(cudaMemcpyAsync(relation, ctx->tables.p + ctx->N * ctx->de, sizeof(float) * ctx->R * ctx->dr,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    if (proj && ctx->proj.n)
+      SKG_CUDA(cudaMemcpyAsync(proj, ctx->proj.p, sizeof(float) * ctx->proj.n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (normals && ctx->normals.n)
+      SKG_CUDA(cudaMemcpyAsync(normals, ctx->normals.p, sizeof(float) * ctx->normals.n, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, const int64_t* t,
+                           int64_t n_ent, int64_t n_rel) {
+  return guard(ctx, [&] {
+    std::vector<int32_t> host;
+    validate_ids(m, h, r, t, n_ent, n_rel, host);
+    ctx->M = m;
+    ctx->tN = n_ent;
+    ctx->tR = n_rel;
+    ctx->H.ensure(m + 1);
+    ctx->Rl.ensure(m + 1);
+    ctx->T.ensure(m + 1);
+    if (m > 0) {
+      SKG_CUDA(cudaMemcpyAsync(ctx->H.p, host.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+      SKG_CUDA(cudaMemcpyAsync(ctx->Rl.p, host.data() + m, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+      SKG_CUDA(cudaMemcpyAsync(ctx->T.p, host.data() + 2 * m, sizeof(int32_t) * m, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    }
+    ctx->has_neg = false;
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
+  return guard(ctx, [&] {
+    if (m != ctx->M) throw ShapeError("negative set is not aligned with the positive triples");
+    std::vector<int32_t> buf(2 * static_cast<size_t>(m));
+    for (int64_t i = 0; i < m; ++i) {
+      if (nh[i] < 0 || nh[i] >= ctx->tN || nt[i] < 0 || nt[i] >= ctx->tN)
+        throw ShapeError("triple " + std::to_string(i) + ": entity id out of range");
+      buf[i] = static_cast<int32_t>(nh[i]);
+      buf[m + i] = static_cast<int32_t>(nt[i]);
+    }
+    ctx->NH.ensure(m + 1);
+    ctx->NT.ensure(m + 1);
+    if (m > 0) {
+      SKG_CUDA(cudaMemcpyAsync(ctx->NH.p, buf.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+      SKG_CUDA(cudaMemcpyAsync(ctx->NT.p, buf.data() + m, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    ctx->has_neg = true;
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_negative_sample(skg_ctx* ctx, uint64_t seed, int32_t avoid, int64_t* out_h, int64_t* out_t) {
+  return guard(ctx, [&] {
+    negative_sample_impl(ctx, seed, avoid != 0);
+    if (out_h || out_t) {
+      std::vector<int32_t> a(ctx->M), b(ctx->M);
+      SKG_CUDA(cudaMemcpyAsync(a.data(), ctx->NH.p, sizeof(int32_t) * ctx->M, cudaMemcpyDeviceToHost, ctx->stream));
+      SKG_CUDA(cudaMemcpyAsync(b.data(), ctx->NT.p, sizeof(int32_t) * ctx->M, cudaMemcpyDeviceToHost, ctx->stream));
+      SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int64_t i = 0; i < ctx->M; ++i) {
+        if (out_h) out_h[i] = a[i];
+        if (out_t) out_t[i] = b[i];
+      }
+    }
+  });
+}
+
+skg_status skg_epoch_order(skg_ctx* ctx, int64_t m, uint64_t seed, int32_t shuffle, int64_t epoch,
+                           int64_t* out_order) {
+  return guard(ctx, [&] {
+    if (m < 0) throw ShapeError("negative length");
+    ctx->order.ensure(m + 1);
+    if (shuffle) {
+      ctx->h_seed[0] = epoch_seed(seed, epoch);
+      SKG_CUDA(cudaMemcpyAsync(ctx->seed_eff.p, ctx->h_seed, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+      device_shuffle(ctx->seed_eff.p, m, ctx->order.p, ctx->shuffle, ctx->stream);
+    } else {
+      device_iota(ctx->order.p, m, ctx->stream);
+    }
+    std::vector<int32_t> o(m);
+    if (m > 0)
+      SKG_CUDA(cudaMemcpyAsync(o.data(), ctx->order.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t i = 0; i < m; ++i) out_order[i] = o[i];
+  });
+}
+
+skg_status skg_build_incidence(skg_ctx* ctx, int32_t layout, int64_t m, const int64_t* h, const int64_t* r,
+                               const int64_t* t, int64_t n_ent, int64_t n_rel, int64_t* row_ptr,
+                               int64_t* col_idx, float* vals, int64_t* nnz) {
+  return guard(ctx, [&] {
+    if (layout != SKG_LAYOUT_HT && layout != SKG_LAYOUT_HRT) throw ConfigError("unknown incidence layout");
+    upload_ids(ctx, m, h, r, t, n_ent, n_rel);
+    DevBuf<uint32_t> cnt, off;
+    DevBuf<int64_t> drp, dcol;
+    DevBuf<float> dval;
+    DevBuf<uint32_t> tot;
+    cnt.ensure(m + 1);
+    off.ensure(m + 1);
+    drp.ensure(m + 1);
+    dcol.ensure(3 * m + 1);
+    dval.ensure(3 * m + 1);
+    tot.ensure(1);
+    ScanPlan sp;
+    if (m > 0) {
+      incidence_count_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->tmp_i32.p, m, layout, cnt.p);
+      exclusive_scan_u32(cnt.p, off.p, m, tot.p, sp, ctx->stream);
+      incidence_fill_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->tmp_i32.p, m, layout, n_ent, off.p, drp.p,
+                                                                 dcol.p, dval.p);
+      count_launch(2);
+      SKG_LAUNCH_CHECK();
+    } else {
+      SKG_CUDA(cudaMemsetAsync(drp.p, 0, sizeof(int64_t), ctx->stream));
+    }
+    SKG_CUDA(cudaMemcpyAsync(row_ptr, drp.p, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t z = row_ptr[m];
+    if (z > 0) {
+      SKG_CUDA(cudaMemcpyAsync(col_idx, dcol.p, sizeof(int64_t) * z, cudaMemcpyDeviceToHost, ctx->stream));
+      SKG_CUDA(cudaMemcpyAsync(vals, dval.p, sizeof(float) * z, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *nnz = z;
+  });
+}
+
+skg_status skg_score_batch(skg_ctx* ctx, const skg_model_config* cfg, int64_t m, const int64_t* h,
+                           const int64_t* r, const int64_t* t, float* scores, float* residual) {
+  return guard(ctx, [&] {
+    check_config(ctx, *cfg, ctx->N, ctx->R);
+    upload_ids(ctx, m, h, r, t, ctx->N, ctx->R);
+    if (m == 0) return;
+    ensure_workspace(ctx, m);
+    reset_err(ctx);
+    const int kind = kind_of(*cfg);
+    FwdArgs a = base_fwd(ctx);
+    a.H = ctx->tmp_i32.p;
+    a.Rl = ctx->tmp_i32.p + m;
+    a.T = ctx->tmp_i32.p + 2 * m;
+    a.B = static_cast<int>(m);
+    if (is_ht(*cfg)) {
+      ctx->ht_work.ensure(ht_work_floats(kind, m, ctx->de, ctx->dr, ctx->R));
+      ht_score(kind, a, ctx->ht_work.p, ctx->num_sms, ctx->stream);
+    } else {
+      launch_hrt_forward(kind, false, a, ctx->num_sms, ctx->stream);
+    }
+    SKG_CUDA(cudaMemcpyAsync(scores, ctx->scores.p, sizeof(float) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    if (residual) {
+      const int64_t d = cfg->model == SKG_TORUSE || cfg->model == SKG_TRANSE ? ctx->de : ctx->dr;
+      SKG_CUDA(cudaMemcpyAsync(residual, ctx->res.p, sizeof(float) * m * d, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_score_backward(skg_ctx* ctx, const skg_model_config* cfg, int64_t m, const int64_t* h,
+                              const int64_t* r, const int64_t* t, const float* up, float* g_entity,
+                              float* g_relation, float* g_proj, float* g_normals) {
+  return guard(ctx, [&] {
+    check_config(ctx, *cfg, ctx->N, ctx->R);
+    upload_ids(ctx, m, h, r, t, ctx->N, ctx->R);
+    if (m == 0) return;
+    ensure_workspace(ctx, m);
+    reset_err(ctx);
+    const int kind = kind_of(*cfg);
+    const int64_t ne = ctx->N * ctx->de, nr = ctx->R * ctx->dr;
+    const int64_t np = ctx->proj.n, nn = ctx->normals.n;
+    ctx->grad_sink.ensure(ne + nr + np + nn + 1);
+    float* G = ctx->grad_sink.p;
+    auto up_tab = [&](float* host, float* dev, int64_t n) {
+      if (n == 0) return;
+      if (host)
+        SKG_CUDA(cudaMemcpyAsync(dev, host, sizeof(float) * n, cudaMemcpyHostToDevice, ctx->stream));
+      else
+        SKG_CUDA(cudaMemsetAsync(dev, 0, sizeof(float) * n, ctx->stream));
+    };
+    up_tab(g_entity, G, ne);
+    up_tab(g_relation, G + ne, nr);
+    up_tab(g_proj, G + ne + nr, np);
+    up_tab(g_normals, G + ne + nr + np, nn);
+    ctx->tmp_f32.ensure(m);
+    SKG_CUDA(cudaMemcpyAsync(ctx->tmp_f32.p, up, sizeof(float) * m, cudaMemcpyHostToDevice, ctx->stream));
+    FwdArgs a = base_fwd(ctx);
+    a.H = ctx->tmp_i32.p;
+    a.Rl = ctx->tmp_i32.p + m;
+    a.T = ctx->tmp_i32.p + 2 * m;
+    a.B = static_cast<int>(m);
+    a.upstream = ctx->tmp_f32.p;
+    BwdArgs ba{};
+    ba.X = G;
+    ba.Xrel = G + ne;
+    ba.scal = ctx->scal.p;
+    ba.N = ctx->N;
+    ba.d = static_cast<int>(ctx->de);
+    ba.batch = 0;
+    ba.lr = ctx->lr_dev.p;
+    ba.err = ctx->err_words.p;
+    if (is_ht(*cfg)) {
+      ctx->ht_work.ensure(ht_work_floats(kind, m, ctx->de, ctx->dr, ctx->R));
+      build_batch_plan(a.H, a.Rl, a.T, m, ctx->N, ctx->R, SKG_LAYOUT_HRT, ctx->plan, ctx->stream);
+      ba.res = ctx->res_u.p;
+      ba.ent_val = ctx->plan.sorted_val;
+      ba.seg_start = ctx->plan.seg_start;
+      ba.seg_col = ctx->plan.seg_col;
+      ba.seg_base = ctx->plan.seg_base;
+      ht_score_backward(kind, a, ba, ctx->ht_work.p, G + ne + nr, G + ne + nr + np, ctx->num_sms, ctx->stream);
+    } else {
+      launch_hrt_forward(kind, false, a, ctx->num_sms, ctx->stream);
+      build_batch_plan(a.H, a.Rl, a.T, m, ctx->N, ctx->R, SKG_LAYOUT_HRT, ctx->plan, ctx->stream);
+      ba.res = ctx->res.p;
+      ba.ent_val = ctx->plan.sorted_val;
+      ba.seg_start = ctx->plan.seg_start;
+      ba.seg_col = ctx->plan.seg_col;
+      ba.seg_base = ctx->plan.seg_base;
+      launch_segment_backward(kind, false, ba, ctx->num_sms, ctx->stream);
+    }
+    auto down = [&](float* host, const float* dev, int64_t n) {
+      if (host && n) SKG_CUDA(cudaMemcpyAsync(host, dev, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    };
+    down(g_entity, G, ne);
+    down(g_relation, G + ne, nr);
+    down(g_proj, G + ne + nr, np);
+    down(g_normals, G + ne + nr + np, nn);
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_margin_ranking_loss(skg_ctx* ctx, int64_t m, const float* pos, const float* neg, float margin,
+                                   float* loss, float* d_pos, float* d_neg) {
+  return guard(ctx, [&] {
+    if (m < 0) throw ShapeError("margin_ranking_loss: length mismatch");
+    if (m == 0) {
+      *loss = 0.f;
+      return;
+    }
+    DevBuf<float> buf;
+    buf.ensure(5 * m + 1);
+    float *p = buf.p, *n = buf.p + m, *dp = buf.p + 2 * m, *dn = buf.p + 3 * m, *term = buf.p + 4 * m;
+    float* out = buf.p + 5 * m;
+    buf.ensure(5 * m + 1);
+    DevBuf<float> o;
+    o.ensure(1);
+    SKG_CUDA(cudaMemcpyAsync(p, pos, sizeof(float) * m, cudaMemcpyHostToDevice, ctx->stream));
+    SKG_CUDA(cudaMemcpyAsync(n, neg, sizeof(float) * m, cudaMemcpyHostToDevice, ctx->stream));
+    hinge_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(p, n, m, margin, dp, dn, term);
+    seq_sum_kernel<<<1, 1, 0, ctx->stream>>>(term, m, o.p);
+    count_launch(2);
+    SKG_LAUNCH_CHECK();
+    (void)out;
+    SKG_CUDA(cudaMemcpyAsync(d_pos, dp, sizeof(float) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaMemcpyAsync(d_neg, dn, sizeof(float) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaMemcpyAsync(loss, o.p, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_sgd_step(skg_ctx* ctx, const float* g_entity, const float* g_relation, const float* g_proj,
+                        const float* g_normals, float lr) {
+  return guard(ctx, [&] {
+    if (!ctx->has_store) throw ConfigError("no parameter store uploaded");
+    const int64_t ne = ctx->N * ctx->de, nr = ctx->R * ctx->dr, np = ctx->proj.n, nn = ctx->normals.n;
+    ctx->grad_sink.ensure(ne + nr + np + nn + 1);
+    float* G = ctx->grad_sink.p;
+    const float* hosts[4] = {g_entity, g_relation, g_proj, g_normals};
+    const int64_t sizes[4] = {ne, nr, np, nn};
+    int64_t off = 0;
+    DevBuf<uint32_t> flags;
+    flags.ensure(4);
+    SKG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(uint32_t) * 4, ctx->stream));
+    for (int k = 0; k < 4; ++k) {
+      if (sizes[k] && !hosts[k]) throw ShapeError("sgd_step: gradient shapes do not match the store");
+      if (sizes[k]) {
+        SKG_CUDA(cudaMemcpyAsync(G + off, hosts[k], sizeof(float) * sizes[k], cudaMemcpyHostToDevice, ctx->stream));
+        finite_check_kernel<<<grid_for(sizes[k]), 256, 0, ctx->stream>>>(G + off, sizes[k], flags.p + k);
+        count_launch();
+      }
+      off += sizes[k];
+    }
+    SKG_LAUNCH_CHECK();
+    uint32_t hf[4];
+    SKG_CUDA(cudaMemcpyAsync(hf, flags.p, sizeof(hf), cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    static const char* names[4] = {"entity embeddings", "relation embeddings", "relation projections",
+                                   "hyperplane normals"};
+    for (int k = 0; k < 4; ++k)
+      if (hf[k]) throw TrainingError(std::string("non-finite gradient in ") + names[k]);
+    float* params[4] = {ctx->tables.p, ctx->tables.p + ne, ctx->proj.p, ctx->normals.p};
+    off = 0;
+    for (int k = 0; k < 4; ++k) {
+      if (sizes[k]) {
+        sgd_dense_kernel<<<grid_for(sizes[k]), 256, 0, ctx->stream>>>(params[k], G + off, sizes[k], lr);
+        count_launch();
+      }
+      off += sizes[k];
+    }
+    reset_err(ctx);
+    if (nn) {
+      row_normalize_kernel<<<grid_for(ctx->R * 32), 256, 0, ctx->stream>>>(ctx->normals.p, ctx->R,
+                                                                          static_cast<int>(ctx->de), 1,
+                                                                          ctx->err_words.p);
+      count_launch();
+    }
+    SKG_LAUNCH_CHECK();
+    SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err_words.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    raise_device_error(ctx->h_err, 0);
+  });
+}
+
+skg_status skg_renormalize_entities(skg_ctx* ctx) {
+  return guard(ctx, [&] {
+    if (!ctx->has_store) throw ConfigError("no parameter store uploaded");
+    row_normalize_kernel<<<grid_for(ctx->N * 32), 256, 0, ctx->stream>>>(ctx->tables.p, ctx->N,
+                                                                        static_cast<int>(ctx->de), 0,
+                                                                        ctx->err_words.p);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_train_epoch(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc, int64_t epoch,
+                           float lr, skg_epoch_report* rep) {
+  return guard(ctx, [&] {
+    if (ctx->dp)
+      dp_train_epoch(ctx, *cfg, *tc, epoch, lr, rep);
+    else
+      train_epoch_impl(ctx, *cfg, *tc, epoch, lr, rep);
+  });
+}
+
+skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc,
+                             int64_t epoch, float lr, skg_epoch_report* rep, double* fwd_ms, double* bwd_ms,
+                             double* plan_ms) {
+  return guard(ctx, [&] {
+    EpochShape es{};
+    prepare_epoch(ctx, *cfg, *tc, es);
+    set_epoch_params(ctx, *tc, epoch, lr);
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<cudaEvent_t> ev;
+    enqueue_epoch(ctx, es, &ev);
+    finish_epoch(ctx, es, epoch, rep);
+    auto el = [&](size_t a, size_t b) {
+      float ms = 0.f;
+      SKG_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+      return static_cast<double>(ms);
+    };
+    *plan_ms = el(0, 1);
+    double f = 0, b = 0;
+    const size_t per = (ev.size() - 2) / es.nb;  // marks per batch
+    for (int64_t k = 0; k < es.nb; ++k) {
+      const size_t s0 = 1 + k * per;
+      f += el(s0, s0 + 1);
+      b += el(s0 + 1, s0 + per);
+    }
+    *fwd_ms = f / es.nb;
+    *bwd_ms = b / es.nb;
+    rep->t_forward_s = f * 1e-3;
+    rep->t_backward_s = b * 1e-3;
+    rep->t_step_s = 0.0;
+    for (auto e : ev) cudaEventDestroy(e);
+  });
+}
+
+skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc,
+                   skg_epoch_report* reports) {
+  return guard(ctx, [&] {  // training.cpp:166-195
+    validate_model(*cfg);
+    validate_train(*tc);
+    if (tc->epochs == 0) return;
+    negative_sample_impl(ctx, tc->seed, false);  // no multiplicative models in this engine
+    for (int64_t e = 0; e < tc->epochs; ++e) {
+      if (tc->resample_negatives && e > 0)
+        negative_sample_impl(ctx, tc->seed + static_cast<uint64_t>(e) * 0x9E3779B9ULL, false);
+      float lr = tc->lr;
+      if (tc->has_scheduler)
+        lr = tc->lr * static_cast<float>(std::pow(tc->decay_factor, double(e / tc->decay_every)));
+      skg_epoch_report rep{};
+      if (ctx->dp)
+        dp_train_epoch(ctx, *cfg, *tc, e, lr, &rep);
+      else
+        train_epoch_impl(ctx, *cfg, *tc, e, lr, &rep);
+      if (tc->renorm_entities) {
+        row_normalize_kernel<<<grid_for(ctx->N * 32), 256, 0, ctx->stream>>>(ctx->tables.p, ctx->N,
+                                                                            static_cast<int>(ctx->de), 0,
+                                                                            ctx->err_words.p);
+        count_launch();
+        SKG_LAUNCH_CHECK();
+      }
+      reports[e] = rep;
+    }
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Engine context: device-resident store, triples, epoch plan and workspaces
+// behind the C ABI (include/skge_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/skge_b200.h"
+#include "kernels.cuh"
+#include "plan.cuh"
+#include "sampling.cuh"
+
+namespace skg {
+
+// Host-side mirrors of the reference exception types (common.hpp:37-59).
+struct ShapeError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct ConfigError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
+struct TrainingError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  void ensure(int64_t count) {
+    if (count <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (cudaMalloc(&p, sizeof(T) * (count > 0 ? count : 1)) != cudaSuccess)
+      throw CudaError("cudaMalloc failed (" + std::to_string(sizeof(T) * count) + " bytes)");
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+struct DpState;  // NCCL replicas (dp.cu)
+
+}  // namespace skg
+
+struct skg_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // ---- store (embedding.hpp:15-31)
+  bool has_store = false;
+  skg_model_config cfg{};
+  int64_t N = 0, R = 0, de = 0, dr = 0;
+  skg::DevBuf<float> tables;  // [entity N x de ; relation R x dr]
+  skg::DevBuf<float> proj, normals;
+
+  // ---- triples
+  int64_t M = 0, tN = 0, tR = 0;
+  skg::DevBuf<int32_t> H, Rl, T, NH, NT;
+  bool has_neg = false;
+
+  // ---- epoch machinery
+  skg::DevBuf<int32_t> order;
+  skg::EpochPlan plan;
+  skg::ShuffleWork shuffle;
+  skg::NegWork negw;
+  skg::DevBuf<float> res, res_u, scal, block_partial, batch_loss, scores, grad_sink;
+  skg::DevBuf<float> ht_work;  // ht models: per-row relation-side rows
+  skg::DevBuf<uint32_t> err_words;  // [0] code [1] batch [2] aux [3] pending
+  skg::DevBuf<unsigned> counter;
+  skg::DevBuf<uint64_t> seed_eff;
+  skg::DevBuf<float> lr_dev;
+  skg::DevBuf<int32_t> tmp_i32;     // per-call id uploads
+  skg::DevBuf<float> tmp_f32;
+  uint64_t* h_seed = nullptr;   // pinned
+  float* h_lr = nullptr;        // pinned
+  uint32_t* h_err = nullptr;    // pinned
+  float* h_loss = nullptr;      // pinned, per batch
+  int64_t h_loss_cap = 0;
+
+  // ---- captured epoch graph
+  cudaGraphExec_t graph = nullptr;
+  std::string graph_key;
+  int64_t graph_launches = 0;
+  int64_t last_launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // ---- data parallel
+  skg::DpState* dp = nullptr;
+};

@@ -1,0 +1,514 @@
+// TransE / TorusE hot path: fused forward (gather + distance + hinge + loss)
+// and the fused transposed-SpMM backward + SGD step.
+//
+// Forward (models.cpp:11-30, 71-92; norms.hpp:19-126; training.cpp:73-94).
+// A warp owns a tile of 8 (pos, neg) pairs = 16 incidence rows. For each row
+// the lanes gather the h, t and r embedding rows with 128-bit loads and form
+// v = (h - t) + r, which is bitwise the CSR row sum a_h x_h + a_t x_t + x_r in
+// canonical column order (sparse.hpp:211-237; a = +-1 makes every product
+// exact and (-t) + h == h - t). Rows are staged in shared memory with a
+// (d + 4)-float stride so that in the reduction phase lane l can read row l
+// with conflict-free float4 loads and evaluate squared_sum / abs_sum with the
+// reference's exact 4-accumulator order. The pair's hinge is formed in
+// registers; only rows of active pairs write their residual to HBM, with one
+// per-row scale (the L2 1/||v|| weight, or the L1/torus weight). The batch
+// loss is reduced deterministically (warp -> block -> last-block).
+//
+// Backward (sparse.hpp:273-306 + embedding.cpp:165-190). Entries of the
+// batch's incidence are pre-sorted by column (stable, so in ascending row
+// order with all positive rows before all negative rows, exactly the order in
+// which the reference accumulates spmm_transpose_add(pos) then (neg)). A warp
+// owns one column segment, accumulates a * D_row in that order in registers
+// (no atomics) and applies p -= lr * g to the touched row in the same kernel.
+// Rows never touched keep p - lr*0 == p, so touching only the segment rows is
+// bitwise the reference's dense step.
+#include "common.cuh"
+#include "kernels.cuh"
+#include "primitives.cuh"
+
+namespace skg {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr float kEps = 1e-6f;  // kNormEps for 32-bit reals, common.hpp:34
+
+__device__ __forceinline__ float torus_wrap(float x) {  // norms.hpp:96-100
+  float d = __fsub_rn(x, rintf(x));
+  if (d >= 0.5f) d = __fsub_rn(d, 1.0f);
+  return d;
+}
+
+template <int KIND>
+__device__ __forceinline__ float4 hrt_combine(float4 h, float4 t, float4 r, bool self_loop) {
+  float4 v;
+  if (self_loop) {
+    v = r;
+  } else {
+    v.x = __fadd_rn(__fsub_rn(h.x, t.x), r.x);
+    v.y = __fadd_rn(__fsub_rn(h.y, t.y), r.y);
+    v.z = __fadd_rn(__fsub_rn(h.z, t.z), r.z);
+    v.w = __fadd_rn(__fsub_rn(h.w, t.w), r.w);
+  }
+  if (KIND == kTorusE_L2 || KIND == kTorusE_L1) {
+    v.x = torus_wrap(v.x);
+    v.y = torus_wrap(v.y);
+    v.z = torus_wrap(v.z);
+    v.w = torus_wrap(v.w);
+  }
+  return v;
+}
+
+template <int KIND>
+__device__ __forceinline__ float hrt_combine1(float h, float t, float r, bool self_loop) {
+  float v = self_loop ? r : __fadd_rn(__fsub_rn(h, t), r);
+  if (KIND == kTorusE_L2 || KIND == kTorusE_L1) v = torus_wrap(v);
+  return v;
+}
+
+__device__ __forceinline__ float term_of(int KIND, float x) {
+  return (KIND == kTransE_L2) ? __fmul_rn(x, x) : fabsf(x);
+}
+
+// squared_sum / abs_sum (norms.hpp:19-55) and the torus sums (:107-115) in the
+// reference's exact association; `bad` collects non-finite elements.
+template <int KIND, int VEC>
+__device__ float ref_reduce(const float* v, int n, bool& bad) {
+  bool nf = false;
+  float s;
+  if (KIND == kTorusE_L2 || KIND == kTorusE_L1) {
+    s = 0.f;
+    for (int j = 0; j < n; ++j) {
+      const float x = v[j];
+      nf |= !(fabsf(x) <= 3.402823466e38f);
+      s = __fadd_rn(s, KIND == kTorusE_L2 ? __fmul_rn(x, x) : fabsf(x));
+    }
+  } else if (n < 8) {
+    s = 0.f;
+    for (int j = 0; j < n; ++j) {
+      nf |= !(fabsf(v[j]) <= 3.402823466e38f);
+      s = __fadd_rn(s, term_of(KIND, v[j]));
+    }
+  } else {
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int j = 0;
+    for (; j + 4 <= n; j += 4) {
+      float4 q;
+      if (VEC == 4) {
+        q = *reinterpret_cast<const float4*>(v + j);
+      } else {
+        q = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+      nf |= !(fabsf(q.x) <= 3.402823466e38f) | !(fabsf(q.y) <= 3.402823466e38f) |
+            !(fabsf(q.z) <= 3.402823466e38f) | !(fabsf(q.w) <= 3.402823466e38f);
+      s0 = __fadd_rn(s0, term_of(KIND, q.x));
+      s1 = __fadd_rn(s1, term_of(KIND, q.y));
+      s2 = __fadd_rn(s2, term_of(KIND, q.z));
+      s3 = __fadd_rn(s3, term_of(KIND, q.w));
+    }
+    s = __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
+    for (; j < n; ++j) {
+      nf |= !(fabsf(v[j]) <= 3.402823466e38f);
+      s = __fadd_rn(s, term_of(KIND, v[j]));
+    }
+  }
+  bad = nf;
+  return s;
+}
+
+// Per-row gradient scale: D_row = dir(residual, scale) in the backward.
+template <int KIND>
+__device__ __forceinline__ float row_scale(float up, float s) {
+  if (KIND == kTransE_L2) return __fdiv_rn(up, __fsqrt_rn(__fadd_rn(s, kEps)));  // norms.hpp:71-73
+  if (KIND == kTorusE_L2) return __fmul_rn(up, 2.0f);                            // norms.hpp:125
+  return up;                                                                     // L1 sign weight
+}
+
+template <int KIND, bool TRAIN, int VEC>
+__global__ void __launch_bounds__(kThreads) hrt_forward_kernel(const FwdArgs a) {
+  extern __shared__ float4 smem4[];
+  __shared__ float warp_loss[kWarps];
+  if (a.err[0] != 0) return;  // sticky error: nothing runs after the failing batch
+  float* smem = reinterpret_cast<float*>(smem4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = a.de;
+  const int S = VEC == 4 ? d + 4 : d + 1;
+  float* rows = smem + warp * 16 * S;
+  constexpr int kUnits = TRAIN ? 8 : 16;
+  const int ntiles = (a.B + kUnits - 1) / kUnits;
+  const int64_t N = a.N;
+  float lsum = 0.f;
+  uint32_t pend = 0;
+
+  const int nwarps = blockDim.x >> 5;
+  for (int tile = blockIdx.x * nwarps + warp; tile < ntiles; tile += gridDim.x * nwarps) {
+    // ---- row ids: lane j < 16 describes row j of the tile
+    int h = 0, t = 0, r = 0, row2 = 0;
+    bool valid = false;
+    if (lane < 16) {
+      if (TRAIN) {
+        const int p = tile * 8 + (lane & 7);
+        const bool neg = lane >= 8;
+        valid = p < a.B;
+        if (valid) {
+          const int id = a.order[p];
+          h = neg ? a.NH[id] : a.H[id];
+          t = neg ? a.NT[id] : a.T[id];
+          r = a.Rl[id];
+          row2 = neg ? a.B + p : p;
+        }
+      } else {
+        const int i = tile * 16 + lane;
+        valid = i < a.B;
+        if (valid) {
+          h = a.H[i];
+          t = a.T[i];
+          r = a.Rl[i];
+          row2 = i;
+        }
+      }
+    }
+    const unsigned vmask = __ballot_sync(kFull, valid);
+
+    // ---- gather 16 residual rows into shared memory
+    if (VEC == 4) {
+      const float4* X4 = reinterpret_cast<const float4*>(a.X);
+      const int d4 = d >> 2;
+#pragma unroll
+      for (int j0 = 0; j0 < 16; j0 += 4) {
+        int hj[4], tj[4], rj[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          hj[q] = __shfl_sync(kFull, h, j0 + q);
+          tj[q] = __shfl_sync(kFull, t, j0 + q);
+          rj[q] = __shfl_sync(kFull, r, j0 + q);
+        }
+        for (int c = lane; c < d4; c += 32) {
+          float4 xh[4], xt[4], xr[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            xh[q] = __ldg(X4 + static_cast<size_t>(hj[q]) * d4 + c);
+            xt[q] = __ldg(X4 + static_cast<size_t>(tj[q]) * d4 + c);
+            xr[q] = __ldg(X4 + static_cast<size_t>(N + rj[q]) * d4 + c);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<float4*>(rows + (j0 + q) * S + 4 * c) =
+                hrt_combine<KIND>(xh[q], xt[q], xr[q], hj[q] == tj[q]);
+        }
+      }
+    } else {
+      for (int j = 0; j < 16; ++j) {
+        const int hj = __shfl_sync(kFull, h, j), tj = __shfl_sync(kFull, t, j),
+                  rj = __shfl_sync(kFull, r, j);
+        for (int c = lane; c < d; c += 32)
+          rows[j * S + c] = hrt_combine1<KIND>(__ldg(a.X + static_cast<size_t>(hj) * d + c),
+                                               __ldg(a.X + static_cast<size_t>(tj) * d + c),
+                                               __ldg(a.X + static_cast<size_t>(N + rj) * d + c),
+                                               hj == tj);
+      }
+    }
+    __syncwarp();
+
+    // ---- exact-order reduction: lane j reduces row j
+    float s = 0.f, score = 0.f;
+    bool bad = false;
+    if (lane < 16 && valid) {
+      s = ref_reduce<KIND, VEC>(rows + lane * S, d, bad);
+      score = (KIND == kTransE_L2) ? __fsqrt_rn(s) : s;  // norms.hpp:57-62, 107-115
+    }
+
+    float up = 0.f;
+    bool act = false;
+    if (TRAIN) {
+      // ---- margin hinge on (pos = lane k, neg = lane k + 8), training.cpp:86-96
+      const float ns = __shfl_down_sync(kFull, score, 8);
+      float term = 0.f;
+      if (lane < 8 && valid) {
+        term = __fsub_rn(__fadd_rn(a.margin, score), ns);
+        act = term > 0.f;  // strict
+      }
+      const float tk = act ? term : 0.f;
+      float tsum = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tsum = __fadd_rn(tsum, __shfl_sync(kFull, tk, k));
+      lsum = __fadd_rn(lsum, tsum);
+      act = __shfl_sync(kFull, act, lane & 7) && lane < 16 && valid;
+      up = act ? (lane < 8 ? a.unit : -a.unit) : 0.f;
+    } else {
+      act = lane < 16 && valid;
+      up = (act && a.upstream) ? a.upstream[row2] : 0.f;
+    }
+    const float sc = (up != 0.f) ? row_scale<KIND>(up, s) : 0.f;
+    // A non-finite residual turns into a non-finite gradient for L2 / torus-L2
+    // even at zero upstream (v * 0); the reference rejects it in sgd_step.
+    if ((KIND == kTransE_L2 || KIND == kTorusE_L2) && bad && (TRAIN || a.upstream))
+      pend |= (h != t) ? kPendEntity : kPendRelation;
+
+    if (lane < 16 && valid) {
+      a.scal[row2] = sc;
+      if (!TRAIN) a.scores[row2] = score;
+    }
+    // ---- residual rows of active pairs (all rows in SCORE mode) to HBM
+    const unsigned wmask = __ballot_sync(kFull, TRAIN ? (sc != 0.f) : (lane < 16 && valid)) & vmask;
+    for (unsigned m = wmask; m; m &= m - 1) {
+      const int j = __ffs(m) - 1;
+      const int r2 = __shfl_sync(kFull, row2, j);  // uniform: every lane executes
+      if (VEC == 4) {
+        float4* dst = reinterpret_cast<float4*>(a.res + static_cast<size_t>(r2) * d);
+        for (int c = lane; c < (d >> 2); c += 32) dst[c] = *reinterpret_cast<const float4*>(rows + j * S + 4 * c);
+      } else {
+        float* dst = a.res + static_cast<size_t>(r2) * d;
+        for (int c = lane; c < d; c += 32) dst[c] = rows[j * S + c];
+      }
+    }
+    __syncwarp();
+  }
+
+  // ---- deterministic loss reduction and batch finalization
+  pend = __reduce_or_sync(kFull, pend);
+  if (lane == 0 && pend) {
+    atomicOr(&a.err[3], pend);
+    __threadfence();
+  }
+  if (!TRAIN) return;
+  if (lane == 0) warp_loss[warp] = lsum;
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    float b = 0.f;
+    for (int w = 0; w < nwarps; ++w) b = __fadd_rn(b, warp_loss[w]);
+    a.block_partial[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && warp == 0) {
+    __threadfence();
+    float acc = 0.f;
+    for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, a.block_partial[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_down_sync(kFull, acc, o));
+    if (lane == 0) {
+      const float loss = __fdiv_rn(acc, static_cast<float>(a.B));  // training.cpp:93
+      a.batch_loss[a.batch] = loss;
+      const uint32_t pflags = atomicOr(&a.err[3], 0u);
+      if (!(fabsf(loss) <= 3.402823466e38f)) {
+        a.err[1] = a.batch;
+        atomicCAS(&a.err[0], 0u, static_cast<uint32_t>(kErrLossNonFinite));
+      } else if (pflags) {
+        a.err[1] = a.batch;
+        atomicCAS(&a.err[0], 0u,
+                  static_cast<uint32_t>((pflags & kPendEntity) ? kErrGradEntity : kErrGradRelation));
+      }
+      a.err[3] = 0;
+      *a.counter = 0;
+    }
+  }
+}
+
+// D_row coefficient for one residual element (models.cpp:37-60, norms.hpp:119-126):
+// L2: v * (up / ||v||_eps); torus-L2: (up * 2) * delta; L1 / torus-L1: sign weight.
+template <int KIND>
+__device__ __forceinline__ float dir1(float r, float sc) {
+  if (KIND == kTransE_L2 || KIND == kTorusE_L2) return __fmul_rn(r, sc);
+  return r > 0.f ? sc : (r < 0.f ? -sc : 0.f);
+}
+
+// acc + a * D with a = +-1 (exact negation), sparse.hpp:284-296 association.
+template <int KIND>
+__device__ __forceinline__ void acc_add(float& acc, float r, float sc, bool neg) {
+  const float x = dir1<KIND>(r, sc);
+  acc = __fadd_rn(acc, neg ? -x : x);
+}
+template <int KIND>
+__device__ __forceinline__ void acc_add(float4& acc, float4 r, float sc, bool neg) {
+  acc_add<KIND>(acc.x, r.x, sc, neg);
+  acc_add<KIND>(acc.y, r.y, sc, neg);
+  acc_add<KIND>(acc.z, r.z, sc, neg);
+  acc_add<KIND>(acc.w, r.w, sc, neg);
+}
+
+__device__ __forceinline__ float sgd1(float p, float g, float lr) {  // embedding.cpp:177-178
+  return __fsub_rn(p, __fmul_rn(lr, g));
+}
+__device__ __forceinline__ float4 sgd1(float4 p, float4 g, float lr) {
+  return make_float4(sgd1(p.x, g.x, lr), sgd1(p.y, g.y, lr), sgd1(p.z, g.z, lr), sgd1(p.w, g.w, lr));
+}
+
+template <int VEC> struct VecT;
+template <> struct VecT<4> { using T = float4; };
+template <> struct VecT<1> { using T = float; };
+
+// One warp per column segment; two vector chunks per lane per pass.
+template <int KIND, bool SGD, int VEC>
+__global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArgs a) {
+  using V = typename VecT<VEC>::T;
+  if (a.err[0] != 0) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const uint32_t s0 = a.seg_base[a.batch], s1 = a.seg_base[a.batch + 1];
+  const int dv = a.d / VEC;
+  const V* RV = reinterpret_cast<const V*>(a.res);
+  for (uint32_t s = s0 + gw; s < s1; s += nw) {
+    const uint32_t col = a.seg_col[s];
+    const uint32_t e0 = a.seg_start[s], e1 = a.seg_start[s + 1];
+    V* P = reinterpret_cast<V*>(a.X) + static_cast<size_t>(col) * dv;
+    for (int cb = 0; cb < dv; cb += 64) {
+      const int c0 = cb + lane, c1 = cb + 32 + lane;
+      const bool has0 = c0 < dv, has1 = c1 < dv;
+      V acc0{}, acc1{};
+      if (!SGD) {  // accumulate into an existing sink (score_backward semantics)
+        if (has0) acc0 = P[c0];
+        if (has1) acc1 = P[c1];
+      }
+      for (uint32_t eb = e0; eb < e1; eb += 32) {
+        const int cnt = min(32u, e1 - eb);
+        uint32_t myv = 0;
+        float mysc = 0.f;
+        if (lane < cnt) {
+          myv = a.ent_val[eb + lane];
+          mysc = a.scal[myv & 0x7fffffffu];
+        }
+        unsigned live = __ballot_sync(kFull, lane < cnt && mysc != 0.f);
+        while (live) {
+          int k[4];
+          int n = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            k[q] = live ? __ffs(live) - 1 : 0;
+            if (live) {
+              live &= live - 1;
+              ++n;
+            }
+          }
+          uint32_t vq[4];
+          float scq[4];
+          V r0[4], r1[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            vq[q] = __shfl_sync(kFull, myv, k[q]);
+            scq[q] = __shfl_sync(kFull, mysc, k[q]);
+            const size_t rowoff = static_cast<size_t>(vq[q] & 0x7fffffffu) * dv;
+            if (q < n) {
+              if (has0) r0[q] = __ldg(RV + rowoff + c0);
+              if (has1) r1[q] = __ldg(RV + rowoff + c1);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q < n) {
+              const bool neg = (vq[q] >> 31) != 0;
+              if (has0) acc_add<KIND>(acc0, r0[q], scq[q], neg);
+              if (has1) acc_add<KIND>(acc1, r1[q], scq[q], neg);
+            }
+          }
+        }
+      }
+      if (SGD) {
+        const float lr = *a.lr;
+        if (has0) P[c0] = sgd1(P[c0], acc0, lr);
+        if (has1) P[c1] = sgd1(P[c1], acc1, lr);
+      } else {
+        if (has0) P[c0] = acc0;
+        if (has1) P[c1] = acc1;
+      }
+    }
+  }
+}
+
+template <int KIND, bool TRAIN, int VEC>
+void launch_fwd_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
+  constexpr size_t kSmemCap = 200 * 1024;
+  const int S = VEC == 4 ? a.de + 4 : a.de + 1;
+  const size_t per_warp = static_cast<size_t>(16) * S * sizeof(float);
+  if (per_warp > kSmemCap) throw CudaError("hrt_forward: embedding dimension too large for the staged tile");
+  int wpb = static_cast<int>(kSmemCap / 3 / per_warp);  // aim for >= 3 resident blocks per SM
+  wpb = wpb < 1 ? 1 : (wpb > kWarps ? kWarps : wpb);
+  const size_t smem = wpb * per_warp;
+  const int units = TRAIN ? 8 : 16;
+  const int ntiles = (a.B + units - 1) / units;
+  int per_sm = static_cast<int>(kSmemCap / (smem + 1024));
+  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+  int grid = (ntiles + wpb - 1) / wpb;
+  if (grid > num_sms * per_sm) grid = num_sms * per_sm;
+  if (grid < 1) grid = 1;
+  hrt_forward_kernel<KIND, TRAIN, VEC><<<grid, wpb * 32, smem, s>>>(a);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
+template <int KIND>
+void launch_fwd_k(bool train, const FwdArgs& a, int num_sms, cudaStream_t s) {
+  const bool v4 = (a.de % 4) == 0;
+  if (train) {
+    if (v4) launch_fwd_t<KIND, true, 4>(a, num_sms, s);
+    else launch_fwd_t<KIND, true, 1>(a, num_sms, s);
+  } else {
+    if (v4) launch_fwd_t<KIND, false, 4>(a, num_sms, s);
+    else launch_fwd_t<KIND, false, 1>(a, num_sms, s);
+  }
+}
+
+template <int KIND>
+void launch_bwd_k(bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s) {
+  const int grid = num_sms * 8;
+  const bool v4 = (a.d % 4) == 0;
+  if (sgd) {
+    if (v4) segment_backward_kernel<KIND, true, 4><<<grid, kThreads, 0, s>>>(a);
+    else segment_backward_kernel<KIND, true, 1><<<grid, kThreads, 0, s>>>(a);
+  } else {
+    if (v4) segment_backward_kernel<KIND, false, 4><<<grid, kThreads, 0, s>>>(a);
+    else segment_backward_kernel<KIND, false, 1><<<grid, kThreads, 0, s>>>(a);
+  }
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
+template <int KIND, bool TRAIN, int VEC>
+void configure_one() {
+  SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+}
+template <int KIND>
+void configure_kind() {
+  configure_one<KIND, true, 4>();
+  configure_one<KIND, true, 1>();
+  configure_one<KIND, false, 4>();
+  configure_one<KIND, false, 1>();
+}
+
+}  // namespace
+
+// Opt every staged-tile kernel into > 48 KB dynamic shared memory. Called once
+// per context at creation, outside any stream capture.
+void configure_hrt_kernels() {
+  configure_kind<kTransE_L2>();
+  configure_kind<kTransE_L1>();
+  configure_kind<kTorusE_L2>();
+  configure_kind<kTorusE_L1>();
+}
+
+void launch_hrt_forward(int kind, bool train, const FwdArgs& a, int num_sms, cudaStream_t s) {
+  switch (kind) {
+    case kTransE_L2: launch_fwd_k<kTransE_L2>(train, a, num_sms, s); break;
+    case kTransE_L1: launch_fwd_k<kTransE_L1>(train, a, num_sms, s); break;
+    case kTorusE_L2: launch_fwd_k<kTorusE_L2>(train, a, num_sms, s); break;
+    case kTorusE_L1: launch_fwd_k<kTorusE_L1>(train, a, num_sms, s); break;
+    default: throw CudaError("launch_hrt_forward: not an hrt kind");
+  }
+}
+
+void launch_segment_backward(int kind, bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s) {
+  switch (kind) {
+    case kTransE_L2: launch_bwd_k<kTransE_L2>(sgd, a, num_sms, s); break;
+    case kTransE_L1: launch_bwd_k<kTransE_L1>(sgd, a, num_sms, s); break;
+    case kTorusE_L2: launch_bwd_k<kTorusE_L2>(sgd, a, num_sms, s); break;
+    case kTorusE_L1: launch_bwd_k<kTorusE_L1>(sgd, a, num_sms, s); break;
+    default: throw CudaError("launch_segment_backward: unsupported kind");
+  }
+}
+
+}  // namespace skg

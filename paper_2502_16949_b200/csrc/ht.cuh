@@ -1,0 +1,34 @@
+// ht-layout models (TransH hyperplane, TransR projection) and data-parallel
+// replicas: launch interfaces used by engine.cu.
+#pragma once
+
+#include <functional>
+
+#include "../../include/skge_b200.h"
+#include "kernels.cuh"
+
+struct skg_ctx;
+
+namespace skg {
+
+// Floats of per-batch scratch the ht kernels need for `rows` pairs.
+int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R);
+
+// One minibatch of TransH / TransR training: forward + hinge, entity scatter
+// through the sorted ht segments, relation-side reductions, SGD (+ normals
+// renormalization). `mark` (nullable) is called after the forward and after
+// the backward for per-phase profiling.
+void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms,
+                    cudaStream_t s, const std::function<void()>* mark);
+// score_batch for ht models (SCORE mode: res = v, res_u = u, scores).
+void ht_score(int kind, const FwdArgs& fa, float* work, int num_sms, cudaStream_t s);
+// score_backward for ht models, accumulating into the sink tables.
+void ht_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj,
+                       float* g_normals, int num_sms, cudaStream_t s);
+
+// data parallel (dp.cu)
+void dp_destroy(skg_ctx* ctx);
+void dp_train_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc, int64_t epoch,
+                    float lr, skg_epoch_report* rep);
+
+}  // namespace skg

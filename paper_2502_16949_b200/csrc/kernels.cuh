@@ -1,0 +1,78 @@
+// Launch interfaces of the hot-path kernels.
+//
+//   hrt_forward   TransE / TorusE forward: hrt gather (h - t) + r, distance,
+//                 margin hinge, loss, per-row gradient scale (models.cpp:11-30,
+//                 71-92; norms.hpp; training.cpp:73-94)
+//   ht_forward    TransH hyperplane / TransR projection forward on the ht
+//                 layout (models.cpp:110-134, 158-181)
+//   segment_backward  transposed-SpMM scatter A^T D as a sorted-segment,
+//                 warp-per-column reduction fused with the SGD update
+//                 (sparse.hpp:273-306, embedding.cpp:165-190)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace skg {
+
+// Score kinds: model x norm, fixed at kernel instantiation.
+enum Kind : int {
+  kTransE_L2 = 0,
+  kTransE_L1 = 1,
+  kTorusE_L2 = 2,
+  kTorusE_L1 = 3,
+  kTransH_L2 = 4,
+  kTransH_L1 = 5,
+  kTransR_L2 = 6,
+  kTransR_L1 = 7,
+};
+
+struct FwdArgs {
+  // parameters
+  const float* X;        // stacked [entity (N x de); relation (R x dr)]
+  const float* proj;     // TransR: R x (dr*de)
+  const float* normals;  // TransH: R x de
+  int64_t N;
+  int de, dr;
+  // rows. TRAIN: pairs p in [0, B) via order[p] -> (H,R,T) / (NH,R,NT);
+  //       SCORE: rows i in [0, B) straight from (H,R,T).
+  const int32_t* order;
+  const int32_t *H, *Rl, *T, *NH, *NT;
+  int B;
+  float margin, unit;
+  const float* upstream;  // SCORE: optional per-row upstream -> scal
+  // outputs
+  float* res;     // residual rows (v or delta), 2B x d (TRAIN) / B x d (SCORE)
+  float* res_u;   // ht models: u = h - t rows (de wide)
+  float* scal;    // per-row gradient scale (0 = inactive)
+  float* scores;  // SCORE mode
+  // loss reduction
+  float* block_partial;
+  unsigned* counter;
+  float* batch_loss;  // slot for this batch
+  int batch;
+  uint32_t* err;
+};
+
+struct BwdArgs {
+  float* X;            // tables updated in place (SGD) or gradient sink (accumulate)
+  float* Xrel;         // ht models: relation table / sink (R x dr)
+  const float* res;
+  const float* scal;
+  int64_t N;
+  int d;
+  const uint32_t* ent_val;    // sorted entries: row2 | sign << 31
+  const uint32_t* seg_start;  // per segment: first entry; seg_start[nseg] = end
+  const uint32_t* seg_col;    // per segment: stacked column
+  const uint32_t* seg_base;   // per batch: first segment; [nb] = nseg
+  int batch;
+  const float* lr;  // device scalar (lets one captured graph serve every epoch)
+  uint32_t* err;
+};
+
+void configure_hrt_kernels();
+void configure_ht_kernels();
+void launch_hrt_forward(int kind, bool train, const FwdArgs& a, int num_sms, cudaStream_t s);
+void launch_segment_backward(int kind, bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s);
+
+}  // namespace skg

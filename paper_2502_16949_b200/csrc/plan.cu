@@ -1,0 +1,181 @@
+// Epoch plan construction (see plan.cuh).
+#include "common.cuh"
+#include "plan.cuh"
+
+namespace skg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t col_key(int64_t col, int64_t N, int64_t Rn) {
+  // relation columns first: long segments start early in the backward grid
+  return static_cast<uint32_t>(col >= N ? col - N : col + Rn);
+}
+
+__device__ __forceinline__ void emit_row(uint32_t* key, uint32_t* val, int64_t base, uint32_t bkey,
+                                         int32_t h, int32_t t, int32_t r, uint32_t row2, int64_t N,
+                                         int64_t Rn, uint32_t invalid, bool with_rel) {
+  if (h != t) {  // +1 and -1 cancel at coo_to_csr time (sparse.hpp:145-155)
+    key[base] = bkey | col_key(h, N, Rn);
+    val[base] = row2;
+    key[base + 1] = bkey | col_key(t, N, Rn);
+    val[base + 1] = row2 | 0x80000000u;
+  } else {
+    key[base] = invalid;
+    val[base] = 0;
+    key[base + 1] = invalid;
+    val[base + 1] = 0;
+  }
+  key[base + 2] = with_rel ? (bkey | col_key(N + r, N, Rn)) : invalid;
+  val[base + 2] = row2;
+}
+
+__global__ void gen_train_entries_kernel(const int32_t* __restrict__ order, const int32_t* __restrict__ H,
+                                         const int32_t* __restrict__ R, const int32_t* __restrict__ T,
+                                         const int32_t* __restrict__ NH, const int32_t* __restrict__ NT,
+                                         int64_t M, int64_t B, int64_t N, int64_t Rn, int cb,
+                                         uint32_t invalid, uint32_t* __restrict__ key,
+                                         uint32_t* __restrict__ val) {
+  for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < 2 * M;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = x >> 1;
+    const int p = static_cast<int>(x & 1);
+    const int64_t b = k / B, i = k - b * B;
+    const int64_t Bb = min(B, M - b * B);
+    const int32_t id = order[k];
+    const int32_t h = p ? NH[id] : H[id];
+    const int32_t t = p ? NT[id] : T[id];
+    const int64_t base = 6 * b * B + 3 * (p * Bb + i);
+    emit_row(key, val, base, static_cast<uint32_t>(b) << cb, h, t, R[id],
+             static_cast<uint32_t>(p * Bb + i), N, Rn, invalid, true);
+  }
+}
+
+__global__ void gen_batch_entries_kernel(const int32_t* __restrict__ H, const int32_t* __restrict__ R,
+                                         const int32_t* __restrict__ T, int64_t m, int64_t N,
+                                         int64_t Rn, uint32_t invalid, bool with_rel,
+                                         uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    emit_row(key, val, 3 * i, 0u, H[i], T[i], R[i], static_cast<uint32_t>(i), N, Rn, invalid, with_rel);
+}
+
+__global__ void seg_flag_kernel(const uint32_t* __restrict__ key, int64_t E, uint32_t invalid,
+                                uint32_t* __restrict__ flag) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < E;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t k = key[e];
+    flag[e] = (k != invalid && (e == 0 || key[e - 1] != k)) ? 1u : 0u;
+  }
+}
+
+__global__ void seg_fill_kernel(const uint32_t* __restrict__ key, const uint32_t* __restrict__ flag,
+                                const uint32_t* __restrict__ segid, int64_t E, uint32_t invalid,
+                                int cb, int64_t N, int64_t Rn, int64_t nb,
+                                const uint32_t* __restrict__ nseg, uint32_t* __restrict__ seg_start,
+                                uint32_t* __restrict__ seg_col, uint32_t* __restrict__ seg_base) {
+  const uint32_t cmask = (1u << cb) - 1u;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < E;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t k = key[e];
+    if (k == invalid) continue;
+    if (flag[e]) {
+      const uint32_t sidx = segid[e];
+      seg_start[sidx] = static_cast<uint32_t>(e);
+      const int64_t cp = k & cmask;
+      seg_col[sidx] = static_cast<uint32_t>(cp < Rn ? N + cp : cp - Rn);
+      const uint32_t b = k >> cb;
+      if (e == 0 || (key[e - 1] >> cb) != b) seg_base[b] = sidx;
+    }
+    if (e + 1 == E || key[e + 1] == invalid) {
+      seg_start[*nseg] = static_cast<uint32_t>(e + 1);
+      seg_base[nb] = *nseg;
+    }
+  }
+}
+
+int grid_for(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return static_cast<int>(b < 1 ? 1 : (b > 8192 ? 8192 : b));
+}
+
+void finish_plan(EpochPlan& p, uint32_t invalid, int64_t N, int64_t Rn, cudaStream_t s) {
+  const bool alt = radix_sort_pairs(p.key, p.val, p.key_alt, p.val_alt, p.E, p.kb + p.cb + 1, p.sort, s);
+  const uint32_t* k = alt ? p.key_alt : p.key;
+  p.sorted_val = alt ? p.val_alt : p.val;
+  // the unsorted pair of buffers is free now: flags and segment ids live there
+  uint32_t* flag = alt ? p.key : p.key_alt;
+  uint32_t* segid = alt ? p.val : p.val_alt;
+  seg_flag_kernel<<<grid_for(p.E), 256, 0, s>>>(k, p.E, invalid, flag);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  exclusive_scan_u32(flag, segid, p.E, p.nseg, p.scan, s);
+  SKG_CUDA(cudaMemsetAsync(p.seg_base, 0, sizeof(uint32_t) * (p.nb + 1), s));
+  seg_fill_kernel<<<grid_for(p.E), 256, 0, s>>>(k, flag, segid, p.E, invalid, p.cb, N, Rn, p.nb, p.nseg,
+                                                p.seg_start, p.seg_col, p.seg_base);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void EpochPlan::reserve(int64_t entries, int64_t batches) {
+  if (entries > cap_entries) {
+    for (uint32_t** b : {&key, &val, &key_alt, &val_alt, &seg_start, &seg_col}) {
+      if (*b) cudaFree(*b);
+      SKG_CUDA(cudaMalloc(b, sizeof(uint32_t) * (entries + 1)));
+    }
+    if (!nseg) SKG_CUDA(cudaMalloc(&nseg, sizeof(uint32_t)));
+    sort.reserve(entries);
+    scan.reserve(entries);
+    cap_entries = entries;
+  }
+  if (batches > cap_batches) {
+    if (seg_base) cudaFree(seg_base);
+    SKG_CUDA(cudaMalloc(&seg_base, sizeof(uint32_t) * (batches + 1)));
+    cap_batches = batches;
+  }
+}
+
+void EpochPlan::release() {
+  for (uint32_t** b : {&key, &val, &key_alt, &val_alt, &seg_start, &seg_col, &seg_base, &nseg}) {
+    if (*b) cudaFree(*b);
+    *b = nullptr;
+  }
+  cap_entries = cap_batches = 0;
+  sort.release();
+  scan.release();
+}
+
+void build_epoch_plan(const int32_t* order, const int32_t* H, const int32_t* R, const int32_t* T,
+                      const int32_t* NH, const int32_t* NT, int64_t M, int64_t B, int64_t N,
+                      int64_t Rn, EpochPlan& p, cudaStream_t s) {
+  p.nb = (M + B - 1) / B;
+  p.E = 6 * M;
+  p.kb = bits_for(static_cast<uint64_t>(p.nb - 1));
+  p.cb = bits_for(static_cast<uint64_t>(N + Rn - 1));
+  if (p.kb + p.cb + 1 > 32) throw CudaError("epoch plan: batches x columns exceed the 31-bit key space");
+  p.reserve(p.E, p.nb);
+  const uint32_t invalid = 1u << (p.kb + p.cb);
+  gen_train_entries_kernel<<<grid_for(2 * M), 256, 0, s>>>(order, H, R, T, NH, NT, M, B, N, Rn, p.cb,
+                                                           invalid, p.key, p.val);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  finish_plan(p, invalid, N, Rn, s);
+}
+
+void build_batch_plan(const int32_t* H, const int32_t* R, const int32_t* T, int64_t m, int64_t N,
+                      int64_t Rn, int layout, EpochPlan& p, cudaStream_t s) {
+  p.nb = 1;
+  p.E = 3 * m;
+  p.kb = 0;
+  p.cb = bits_for(static_cast<uint64_t>(N + Rn - 1));
+  p.reserve(p.E, 1);
+  const uint32_t invalid = 1u << p.cb;
+  gen_batch_entries_kernel<<<grid_for(m), 256, 0, s>>>(H, R, T, m, N, Rn, invalid, layout == 1, p.key,
+                                                       p.val);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  finish_plan(p, invalid, N, Rn, s);
+}
+
+}  // namespace skg

@@ -1,0 +1,277 @@
+"""ctypes binding of include/skge_b200.h (the engine's C ABI).
+
+Method names and argument meanings follow the reference library
+(/root/reference/proj/include/sparsekge/*.hpp): negative_sample, score_batch,
+score_backward, margin_ranking_loss, sgd_step, renormalize_entities,
+train_epoch, fit. Errors are raised as EngineError carrying the reference
+exception kind (ShapeError, ConfigError, TrainingError, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+MODELS = {"transe": 0, "transr": 1, "transh": 2, "toruse": 3}
+NORMS = {"l1": 0, "l2": 1}
+KINDS = {1: "ShapeError", 2: "ConfigError", 3: "DegenerateTripleError", 4: "TrainingError",
+         5: "ParseError", 6: "CudaError"}
+
+
+def lib_path() -> str:
+    return os.path.join(HERE, "libskge_b200.so")
+
+
+class EngineError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        self.kind = KINDS.get(code, str(code))
+        self.msg = msg
+        super().__init__(f"{self.kind}: {msg}")
+
+
+class ModelConfig(C.Structure):
+    _fields_ = [("model", C.c_uint32), ("norm", C.c_uint32), ("dim_entity", C.c_int64),
+                ("dim_relation", C.c_int64)]
+
+    @classmethod
+    def make(cls, model: str, dim_entity: int, dim_relation: int | None = None, norm: str = "l2"):
+        return cls(MODELS[model], NORMS[norm], dim_entity, dim_entity if dim_relation is None else dim_relation)
+
+
+class TrainConfig(C.Structure):
+    _fields_ = [("lr", C.c_float), ("margin", C.c_float), ("epochs", C.c_int64), ("batch_size", C.c_int64),
+                ("seed", C.c_uint64), ("has_scheduler", C.c_int32), ("decay_every", C.c_int64),
+                ("decay_factor", C.c_float), ("shuffle", C.c_int32), ("resample_negatives", C.c_int32),
+                ("renorm_entities", C.c_int32)]
+
+    @classmethod
+    def make(cls, lr=4e-4, margin=0.5, epochs=200, batch_size=1024, seed=0, scheduler=None, shuffle=True,
+             resample_negatives=False, renorm_entities=False):
+        every, factor = scheduler if scheduler else (50, 0.5)
+        return cls(lr, margin, epochs, batch_size, seed, 1 if scheduler else 0, every, factor, int(shuffle),
+                   int(resample_negatives), int(renorm_entities))
+
+
+class EpochReport(C.Structure):
+    _fields_ = [("epoch", C.c_int64), ("loss", C.c_double), ("t_forward_s", C.c_double),
+                ("t_backward_s", C.c_double), ("t_step_s", C.c_double)]
+
+
+_LIB = None
+
+
+def load_library():
+    """Loads the native engine; raises if it was not built (no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        raise EngineError(6, f"native engine library missing: {path} (run __graft_entry__.build())")
+    L = C.CDLL(path)
+    vp, i64, i32, f32 = C.c_void_p, C.c_int64, C.c_int32, C.c_float
+    L.skg_last_error.restype = C.c_char_p
+    L.skg_last_error.argtypes = [vp]
+    L.skg_version.restype = C.c_char_p
+    L.skg_num_sms.argtypes = [vp]
+    L.skg_last_launch_count.restype = i64
+    L.skg_last_launch_count.argtypes = [vp]
+    sig = {
+        "skg_create": [C.c_int, C.POINTER(vp)],
+        "skg_synchronize": [vp],
+        "skg_store_upload": [vp, vp, i64, i64, vp, vp, vp, vp],
+        "skg_store_download": [vp, vp, vp, vp, vp],
+        "skg_sgd_step": [vp, vp, vp, vp, vp, f32],
+        "skg_renormalize_entities": [vp],
+        "skg_set_triples": [vp, i64, vp, vp, vp, i64, i64],
+        "skg_set_negatives": [vp, i64, vp, vp],
+        "skg_negative_sample": [vp, C.c_uint64, i32, vp, vp],
+        "skg_epoch_order": [vp, i64, C.c_uint64, i32, i64, vp],
+        "skg_build_incidence": [vp, i32, i64, vp, vp, vp, i64, i64, vp, vp, vp, vp],
+        "skg_score_batch": [vp, vp, i64, vp, vp, vp, vp, vp],
+        "skg_score_backward": [vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp],
+        "skg_margin_ranking_loss": [vp, i64, vp, vp, f32, vp, vp, vp],
+        "skg_train_epoch": [vp, vp, vp, i64, f32, vp],
+        "skg_fit": [vp, vp, vp, vp],
+        "skg_profile_epoch": [vp, vp, vp, i64, f32, vp, vp, vp, vp],
+        "skg_nccl_unique_id": [vp],
+        "skg_dp_init": [vp, vp, C.c_int, C.c_int],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    L.skg_destroy.argtypes = [vp]
+    L.skg_destroy.restype = None
+    _LIB = L
+    return L
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _f32(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float32)
+
+
+class Engine:
+    """One device context (skg_ctx): device-resident store, triples and plans."""
+
+    def __init__(self, device: int = 0):
+        self.L = load_library()
+        h = C.c_void_p()
+        rc = self.L.skg_create(device, C.byref(h))
+        if rc != 0:
+            raise EngineError(rc, self.L.skg_last_error(None).decode())
+        self.h = h
+        self.num_sms = self.L.skg_num_sms(h)
+        self.dims = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.skg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            raise EngineError(rc, self.L.skg_last_error(self.h).decode())
+
+    # ------------------------------------------------------------ store
+    def store_upload(self, cfg: ModelConfig, entity, relation, proj=None, normals=None):
+        entity, relation, proj, normals = _f32(entity), _f32(relation), _f32(proj), _f32(normals)
+        self.dims = (entity.shape[0], relation.shape[0], cfg.dim_entity, cfg.dim_relation,
+                     proj is not None, normals is not None)
+        self._check(self.L.skg_store_upload(self.h, C.byref(cfg), entity.shape[0], relation.shape[0], _p(entity),
+                                            _p(relation), _p(proj), _p(normals)))
+
+    def _empty_tables(self):
+        n, r, de, dr, hp, hn = self.dims
+        return (np.empty((n, de), np.float32), np.empty((r, dr), np.float32),
+                np.empty((r, dr * de), np.float32) if hp else None, np.empty((r, de), np.float32) if hn else None)
+
+    def store_download(self):
+        e, r, p, n = self._empty_tables()
+        self._check(self.L.skg_store_download(self.h, _p(e), _p(r), _p(p), _p(n)))
+        return e, r, p, n
+
+    def sgd_step(self, g_entity, g_relation, g_proj, g_normals, lr):
+        self._check(self.L.skg_sgd_step(self.h, _p(_f32(g_entity)), _p(_f32(g_relation)), _p(_f32(g_proj)),
+                                        _p(_f32(g_normals)), lr))
+
+    def renormalize_entities(self):
+        self._check(self.L.skg_renormalize_entities(self.h))
+
+    # ------------------------------------------------------------ triples
+    def set_triples(self, h, r, t, num_entities, num_relations):
+        h, r, t = _i64(h), _i64(r), _i64(t)
+        self._check(self.L.skg_set_triples(self.h, len(h), _p(h), _p(r), _p(t), num_entities, num_relations))
+        self.m = len(h)
+
+    def set_negatives(self, nh, nt):
+        nh, nt = _i64(nh), _i64(nt)
+        self._check(self.L.skg_set_negatives(self.h, len(nh), _p(nh), _p(nt)))
+
+    def negative_sample(self, seed, avoid_self_loops=False):
+        oh = np.empty(self.m, np.int64)
+        ot = np.empty(self.m, np.int64)
+        self._check(self.L.skg_negative_sample(self.h, seed, int(avoid_self_loops), _p(oh), _p(ot)))
+        return oh, ot
+
+    def epoch_order(self, m, seed, epoch, shuffle=True):
+        o = np.empty(max(m, 1), np.int64)
+        self._check(self.L.skg_epoch_order(self.h, m, seed, int(shuffle), epoch, _p(o)))
+        return o[:m]
+
+    # ------------------------------------------------------------ parity surface
+    def build_incidence(self, layout, h, r, t, num_entities, num_relations):
+        h, r, t = _i64(h), _i64(r), _i64(t)
+        m = len(h)
+        rp = np.empty(m + 1, np.int64)
+        col = np.empty(3 * m + 1, np.int64)
+        val = np.empty(3 * m + 1, np.float32)
+        nnz = C.c_int64()
+        self._check(self.L.skg_build_incidence(self.h, {"ht": 0, "hrt": 1}[layout], m, _p(h), _p(r), _p(t),
+                                               num_entities, num_relations, _p(rp), _p(col), _p(val),
+                                               C.byref(nnz)))
+        return rp, col[:nnz.value].copy(), val[:nnz.value].copy()
+
+    def score_batch(self, cfg: ModelConfig, h, r, t, residual=False):
+        h, r, t = _i64(h), _i64(r), _i64(t)
+        m = len(h)
+        scores = np.empty(max(m, 1), np.float32)
+        d = cfg.dim_entity if cfg.model in (0, 3) else cfg.dim_relation
+        res = np.empty((max(m, 1), d), np.float32) if residual else None
+        self._check(self.L.skg_score_batch(self.h, C.byref(cfg), m, _p(h), _p(r), _p(t), _p(scores), _p(res)))
+        return (scores[:m], res[:m]) if residual else scores[:m]
+
+    def score_backward(self, cfg: ModelConfig, h, r, t, upstream, grads):
+        """Accumulates into grads = (entity, relation, proj|None, normals|None) in place."""
+        h, r, t, up = _i64(h), _i64(r), _i64(t), _f32(upstream)
+        for g in grads:
+            assert g is None or (g.dtype == np.float32 and g.flags.c_contiguous)
+        self._check(self.L.skg_score_backward(self.h, C.byref(cfg), len(h), _p(h), _p(r), _p(t), _p(up),
+                                              *[_p(g) for g in grads]))
+        return grads
+
+    def margin_ranking_loss(self, pos, neg, margin):
+        pos, neg = _f32(pos), _f32(neg)
+        if len(pos) != len(neg):
+            raise EngineError(1, "margin_ranking_loss: length mismatch")
+        m = len(pos)
+        loss = C.c_float()
+        dp, dn = np.empty(max(m, 1), np.float32), np.empty(max(m, 1), np.float32)
+        self._check(self.L.skg_margin_ranking_loss(self.h, m, _p(pos), _p(neg), margin, C.byref(loss), _p(dp),
+                                                   _p(dn)))
+        return loss.value, dp[:m], dn[:m]
+
+    # ------------------------------------------------------------ training
+    def train_epoch(self, cfg: ModelConfig, tc: TrainConfig, epoch: int, lr: float) -> EpochReport:
+        rep = EpochReport()
+        self._check(self.L.skg_train_epoch(self.h, C.byref(cfg), C.byref(tc), epoch, lr, C.byref(rep)))
+        return rep
+
+    def fit(self, cfg: ModelConfig, tc: TrainConfig):
+        reps = (EpochReport * max(1, tc.epochs))()
+        self._check(self.L.skg_fit(self.h, C.byref(cfg), C.byref(tc), reps))
+        return [reps[i] for i in range(tc.epochs)]
+
+    def profile_epoch(self, cfg: ModelConfig, tc: TrainConfig, epoch: int, lr: float):
+        rep = EpochReport()
+        f, b, p = C.c_double(), C.c_double(), C.c_double()
+        self._check(self.L.skg_profile_epoch(self.h, C.byref(cfg), C.byref(tc), epoch, lr, C.byref(rep),
+                                             C.byref(f), C.byref(b), C.byref(p)))
+        return rep, f.value, b.value, p.value
+
+    def synchronize(self):
+        self._check(self.L.skg_synchronize(self.h))
+
+    def last_launch_count(self) -> int:
+        return int(self.L.skg_last_launch_count(self.h))
+
+    # ------------------------------------------------------------ data parallel
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        L = load_library()
+        buf = C.create_string_buffer(128)
+        rc = L.skg_nccl_unique_id(buf)
+        if rc != 0:
+            raise EngineError(rc, "ncclGetUniqueId failed")
+        return buf.raw
+
+    def dp_init(self, unique_id: bytes, rank: int, world: int):
+        buf = C.create_string_buffer(unique_id, 128)
+        self._check(self.L.skg_dp_init(self.h, buf, rank, world))

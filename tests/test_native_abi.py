@@ -1,0 +1,53 @@
+"""CPU checks of the native boundary: the C-ABI library loads and exports every
+entry point include/skge_b200.h declares (no compute without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "skge_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(skg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for must in ("skg_create", "skg_negative_sample", "skg_build_incidence", "skg_score_batch",
+                 "skg_score_backward", "skg_margin_ranking_loss", "skg_sgd_step", "skg_train_epoch", "skg_fit"):
+        assert must in syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2502_16949_b200.engine import lib_path, load_library
+    if not os.path.exists(lib_path()):
+        pytest.fail("libskge_b200.so not built (run __graft_entry__.build())")
+    lib = load_library()
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_create_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2502_16949_b200 import Engine, EngineError
+    with pytest.raises(EngineError) as e:
+        Engine(0)
+    assert e.value.kind == "CudaError"
+
+
+def test_cpp_shim_compiles():
+    """The reference-signature C++ shim (include/skge_b200.hpp) compiles against the ABI."""
+    import subprocess
+    import tempfile
+    src = os.path.join(ROOT, "tests", "cpp", "shim_drop_in.cpp")
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "shim")
+        subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", out,
+                        "-L", os.path.join(ROOT, "paper_2502_16949_b200"), "-lskge_b200",
+                        f"-Wl,-rpath,{os.path.join(ROOT, 'paper_2502_16949_b200')}"], check=True)
