@@ -164,6 +164,25 @@ int64_t skg_last_launch_count(const skg_ctx* ctx);
 /* Synchronizes the context's streams. */
 skg_status skg_synchronize(skg_ctx* ctx);
 
+/* ---- host setup utilities (once per job, not on the hot path) ------------ */
+/* generate_synthetic, data_io.cpp:128-211: triples in generation order; the
+ * split is [0, n/20) test, next n/20 valid, rest train. */
+skg_status skg_generate_synthetic(int64_t n_entities, int64_t n_relations, int64_t n_triples,
+                                  uint64_t seed, int64_t* heads, int64_t* relations, int64_t* tails);
+/* init_store, embedding.cpp:129-163 (fp32 tables; proj/normals may be NULL). */
+skg_status skg_init_store(uint32_t model, int64_t num_entities, int64_t num_relations,
+                          int64_t dim_entity, int64_t dim_relation, uint64_t seed, float* entity,
+                          float* relation, float* proj, float* normals);
+const char* skg_host_last_error(void);
+
+/* ---- measurement hooks ----------------------------------------------------- */
+/* Overwrites a 256 MiB scratch buffer on the context stream (evicts L2). */
+skg_status skg_flush_l2(skg_ctx* ctx);
+/* Plan statistics of minibatch `batch` of the last epoch: touched columns
+ * (segments) and incidence entries (valid nnz of the transposed matrix). */
+skg_status skg_plan_stats(skg_ctx* ctx, int64_t batch, int64_t* segments, int64_t* entries,
+                          int64_t* relation_segments);
+
 /* ---- data-parallel replicas (one process per GPU) ------------------------ */
 /* Joins an NCCL communicator (unique id produced by skg_nccl_unique_id on
  * rank 0 and broadcast by the caller). After this, skg_train_epoch treats the

@@ -449,6 +449,16 @@ int grid_for(int64_t n) {
   return static_cast<int>(b < 1 ? 1 : (b > 4096 ? 4096 : b));
 }
 
+__global__ void narrow_ids_kernel(const int64_t* __restrict__ src, int64_t m, int64_t limit,
+                                  int32_t* __restrict__ dst, uint32_t* __restrict__ first_bad) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = src[i];
+    if (v < 0 || v >= limit) atomicMin(first_bad, static_cast<uint32_t>(i));
+    dst[i] = static_cast<int32_t>(v);
+  }
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -570,46 +580,70 @@ skg_status skg_store_download(skg_ctx* ctx, float* entity, float* relation, floa
   });
 }
 
+// Copies caller id arrays (int64, pinned or pageable) straight to HBM, then
+// validates and narrows them on device (TripleBatch::validate semantics).
+void upload_narrow(skg_ctx* ctx, const int64_t* const* srcs, int32_t* const* dsts, const int64_t* limits,
+                   const int* slots, int count, int64_t m, uint32_t* bad_out) {
+  ctx->stage_i64.ensure(3 * m + 1);
+  ctx->bad_idx.ensure(3);
+  SKG_CUDA(cudaMemsetAsync(ctx->bad_idx.p, 0xFF, sizeof(uint32_t) * 3, ctx->stream));
+  for (int k = 0; k < count; ++k) {
+    SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, srcs[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    narrow_ids_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->stage_i64.p + k * m, m, limits[k], dsts[k],
+                                                            ctx->bad_idx.p + slots[k]);
+    count_launch();
+  }
+  SKG_LAUNCH_CHECK();
+  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->bad_idx.p, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  bad_out[0] = ctx->h_err[0];
+  bad_out[1] = ctx->h_err[1];
+}
+
 skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, const int64_t* t,
                            int64_t n_ent, int64_t n_rel) {
   return guard(ctx, [&] {
-    std::vector<int32_t> host;
-    validate_ids(m, h, r, t, n_ent, n_rel, host);
-    ctx->M = m;
+    if (m > 0 && (!h || !r || !t)) throw ShapeError("triple batch: heads/relations/tails length mismatch");
+    if (n_ent > INT32_MAX || n_rel > INT32_MAX || m > INT32_MAX) throw ShapeError("id space exceeds 32-bit device ids");
+    ctx->M = 0;
+    ctx->has_neg = false;
     ctx->tN = n_ent;
     ctx->tR = n_rel;
     ctx->H.ensure(m + 1);
     ctx->Rl.ensure(m + 1);
     ctx->T.ensure(m + 1);
     if (m > 0) {
-      SKG_CUDA(cudaMemcpyAsync(ctx->H.p, host.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
-      SKG_CUDA(cudaMemcpyAsync(ctx->Rl.p, host.data() + m, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
-      SKG_CUDA(cudaMemcpyAsync(ctx->T.p, host.data() + 2 * m, sizeof(int32_t) * m, cudaMemcpyHostToDevice,
-                               ctx->stream));
+      const int64_t* srcs[3] = {h, r, t};
+      int32_t* dsts[3] = {ctx->H.p, ctx->Rl.p, ctx->T.p};
+      const int64_t lim[3] = {n_ent, n_rel, n_ent};
+      const int slots[3] = {0, 1, 0};
+      uint32_t bad[2];
+      upload_narrow(ctx, srcs, dsts, lim, slots, 3, m, bad);
+      if (bad[0] != 0xFFFFFFFFu && bad[0] <= bad[1])  // incidence.hpp:26-29: entity check first
+        throw ShapeError("triple " + std::to_string(bad[0]) + ": entity id out of range");
+      if (bad[1] != 0xFFFFFFFFu) throw ShapeError("triple " + std::to_string(bad[1]) + ": relation id out of range");
     }
-    ctx->has_neg = false;
-    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->M = m;
   });
 }
 
 skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
   return guard(ctx, [&] {
     if (m != ctx->M) throw ShapeError("negative set is not aligned with the positive triples");
-    std::vector<int32_t> buf(2 * static_cast<size_t>(m));
-    for (int64_t i = 0; i < m; ++i) {
-      if (nh[i] < 0 || nh[i] >= ctx->tN || nt[i] < 0 || nt[i] >= ctx->tN)
-        throw ShapeError("triple " + std::to_string(i) + ": entity id out of range");
-      buf[i] = static_cast<int32_t>(nh[i]);
-      buf[m + i] = static_cast<int32_t>(nt[i]);
-    }
+    ctx->has_neg = false;
     ctx->NH.ensure(m + 1);
     ctx->NT.ensure(m + 1);
     if (m > 0) {
-      SKG_CUDA(cudaMemcpyAsync(ctx->NH.p, buf.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
-      SKG_CUDA(cudaMemcpyAsync(ctx->NT.p, buf.data() + m, sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+      const int64_t* srcs[2] = {nh, nt};
+      int32_t* dsts[2] = {ctx->NH.p, ctx->NT.p};
+      const int64_t lim[2] = {ctx->tN, ctx->tN};
+      const int slots[2] = {0, 0};
+      uint32_t bad[2];
+      upload_narrow(ctx, srcs, dsts, lim, slots, 2, m, bad);
+      if (bad[0] != 0xFFFFFFFFu) throw ShapeError("triple " + std::to_string(bad[0]) + ": entity id out of range");
     }
     ctx->has_neg = true;
-    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -923,6 +957,35 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const sk
     rep->t_backward_s = b * 1e-3;
     rep->t_step_s = 0.0;
     for (auto e : ev) cudaEventDestroy(e);
+  });
+}
+
+skg_status skg_flush_l2(skg_ctx* ctx) {
+  return guard(ctx, [&] {
+    ctx->flush_buf.ensure(256ll << 20);
+    SKG_CUDA(cudaMemsetAsync(ctx->flush_buf.p, 0x5a, 256ull << 20, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_plan_stats(skg_ctx* ctx, int64_t batch, int64_t* segments, int64_t* entries,
+                          int64_t* relation_segments) {
+  return guard(ctx, [&] {
+    if (batch < 0 || batch >= ctx->plan.nb || !ctx->plan.seg_base) throw ShapeError("plan_stats: no such batch");
+    uint32_t sb[2];
+    SKG_CUDA(cudaMemcpy(sb, ctx->plan.seg_base + batch, sizeof(sb), cudaMemcpyDeviceToHost));
+    uint32_t e0 = 0, e1 = 0;
+    SKG_CUDA(cudaMemcpy(&e0, ctx->plan.seg_start + sb[0], sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    SKG_CUDA(cudaMemcpy(&e1, ctx->plan.seg_start + sb[1], sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> cols(sb[1] - sb[0]);
+    if (!cols.empty())
+      SKG_CUDA(cudaMemcpy(cols.data(), ctx->plan.seg_col + sb[0], sizeof(uint32_t) * cols.size(),
+                          cudaMemcpyDeviceToHost));
+    int64_t nrel = 0;
+    for (uint32_t c : cols) nrel += c >= ctx->N;
+    *segments = sb[1] - sb[0];
+    *entries = static_cast<int64_t>(e1) - e0;
+    *relation_segments = nrel;
   });
 }
 

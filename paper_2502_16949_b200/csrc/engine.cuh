@@ -77,6 +77,9 @@ struct skg_ctx {
   skg::DevBuf<float> lr_dev;
   skg::DevBuf<int32_t> tmp_i32;     // per-call id uploads
   skg::DevBuf<float> tmp_f32;
+  skg::DevBuf<uint8_t> flush_buf;
+  skg::DevBuf<int64_t> stage_i64;   // caller id arrays staged in HBM
+  skg::DevBuf<uint32_t> bad_idx;
   uint64_t* h_seed = nullptr;   // pinned
   float* h_lr = nullptr;        // pinned
   uint32_t* h_err = nullptr;    // pinned

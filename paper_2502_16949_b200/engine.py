@@ -99,7 +99,12 @@ def load_library():
         "skg_profile_epoch": [vp, vp, vp, i64, f32, vp, vp, vp, vp],
         "skg_nccl_unique_id": [vp],
         "skg_dp_init": [vp, vp, C.c_int, C.c_int],
+        "skg_generate_synthetic": [i64, i64, i64, C.c_uint64, vp, vp, vp],
+        "skg_init_store": [C.c_uint32, i64, i64, i64, i64, C.c_uint64, vp, vp, vp, vp],
+        "skg_flush_l2": [vp],
+        "skg_plan_stats": [vp, i64, vp, vp, vp],
     }
+    L.skg_host_last_error.restype = C.c_char_p
     for name, args in sig.items():
         fn = getattr(L, name)
         fn.argtypes = args
@@ -275,3 +280,45 @@ class Engine:
     def dp_init(self, unique_id: bytes, rank: int, world: int):
         buf = C.create_string_buffer(unique_id, 128)
         self._check(self.L.skg_dp_init(self.h, buf, rank, world))
+
+    # ------------------------------------------------------------ measurement hooks
+    def flush_l2(self):
+        self._check(self.L.skg_flush_l2(self.h))
+
+    def plan_stats(self, batch: int):
+        s, e, r = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self.L.skg_plan_stats(self.h, batch, C.byref(s), C.byref(e), C.byref(r)))
+        return s.value, e.value, r.value
+
+
+def _host_check(L, rc):
+    if rc != 0:
+        raise EngineError(rc, L.skg_host_last_error().decode())
+
+
+def split_sizes(n: int):
+    """data_io.cpp:189-190: test n/20, valid n/20, rest train."""
+    nv = max(1, n // 20)
+    nt = max(1, n // 20)
+    return nt, nv, n - nt - nv
+
+
+def generate_synthetic(n_entities: int, n_relations: int, n_triples: int, seed: int):
+    """Reference lattice generator (host, once per job); returns the train split."""
+    L = load_library()
+    h, r, t = (np.empty(n_triples, np.int64) for _ in range(3))
+    _host_check(L, L.skg_generate_synthetic(n_entities, n_relations, n_triples, seed, _p(h), _p(r), _p(t)))
+    nt, nv, _ = split_sizes(n_triples)
+    s = nt + nv
+    return h[s:].copy(), r[s:].copy(), t[s:].copy()
+
+
+def init_store(model: str, n_entities: int, n_relations: int, de: int, dr: int, seed: int):
+    """init_store (embedding.cpp:129-163) on the host; returns fp32 tables."""
+    L = load_library()
+    e = np.empty((n_entities, de), np.float32)
+    r = np.empty((n_relations, dr), np.float32)
+    p = np.empty((n_relations, dr * de), np.float32) if model == "transr" else None
+    n = np.empty((n_relations, de), np.float32) if model == "transh" else None
+    _host_check(L, L.skg_init_store(MODELS[model], n_entities, n_relations, de, dr, seed, _p(e), _p(r), _p(p), _p(n)))
+    return e, r, p, n

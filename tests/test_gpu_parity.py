@@ -271,8 +271,8 @@ def test_train_epoch_toruse_fb15k237_shape(eng, orc32):
 
 
 def test_nonfinite_loss_raises_with_epoch_and_batch(eng, orc32):
-    n, r, d = 50, 3, 8
-    h, rel, t = orc32.synthetic_train(n, r, 90, 2)
+    n, r, d = 200, 5, 8
+    h, rel, t = orc32.synthetic_train(n, r, 300, 2)
     st = orc32.init_store("transe", n, r, d, d, 2)
     st.entity[int(h[0])] = np.inf
     cfg = ModelConfig.make("transe", d, d)
