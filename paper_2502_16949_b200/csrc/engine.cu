@@ -234,7 +234,7 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
       launch_segment_backward(es.kind, true, ba, ctx->num_sms, s);
       mark();
     } else {
-      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, ev ? &mark : nullptr);
+      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, ev ? &mark : nullptr, ctx->R);
     }
   }
 }
@@ -253,7 +253,7 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   es.kind = kind_of(cfg);
   ctx->order.ensure(ctx->M);
   ensure_workspace(ctx, 2 * es.B);
-  if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, es.B, ctx->de, ctx->dr, ctx->R));
+  if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, 2 * es.B, ctx->de, ctx->dr, ctx->R));
   ctx->batch_loss.ensure(es.nb);
   if (ctx->h_loss_cap < es.nb) {
     if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
@@ -738,7 +738,18 @@ skg_status skg_score_batch(skg_ctx* ctx, const skg_model_config* cfg, int64_t m,
     a.B = static_cast<int>(m);
     if (is_ht(*cfg)) {
       ctx->ht_work.ensure(ht_work_floats(kind, m, ctx->de, ctx->dr, ctx->R));
-      ht_score(kind, a, ctx->ht_work.p, ctx->num_sms, ctx->stream);
+      build_batch_plan(a.H, a.Rl, a.T, m, ctx->N, ctx->R, SKG_LAYOUT_HRT, ctx->plan, ctx->stream);
+      BwdArgs ba{};
+      ba.N = ctx->N;
+      ba.d = static_cast<int>(ctx->de);
+      ba.ent_val = ctx->plan.sorted_val;
+      ba.seg_start = ctx->plan.seg_start;
+      ba.seg_col = ctx->plan.seg_col;
+      ba.seg_base = ctx->plan.seg_base;
+      ba.batch = 0;
+      ba.lr = ctx->lr_dev.p;
+      ba.err = ctx->err_words.p;
+      ht_score(kind, a, ba, ctx->ht_work.p, ctx->num_sms, ctx->stream, ctx->R);
     } else {
       launch_hrt_forward(kind, false, a, ctx->num_sms, ctx->stream);
     }
@@ -801,7 +812,7 @@ skg_status skg_score_backward(skg_ctx* ctx, const skg_model_config* cfg, int64_t
       ba.seg_start = ctx->plan.seg_start;
       ba.seg_col = ctx->plan.seg_col;
       ba.seg_base = ctx->plan.seg_base;
-      ht_score_backward(kind, a, ba, ctx->ht_work.p, G + ne + nr, G + ne + nr + np, ctx->num_sms, ctx->stream);
+      ht_score_backward(kind, a, ba, ctx->ht_work.p, G + ne + nr, G + ne + nr + np, ctx->num_sms, ctx->stream, ctx->R);
     } else {
       launch_hrt_forward(kind, false, a, ctx->num_sms, ctx->stream);
       build_batch_plan(a.H, a.Rl, a.T, m, ctx->N, ctx->R, SKG_LAYOUT_HRT, ctx->plan, ctx->stream);

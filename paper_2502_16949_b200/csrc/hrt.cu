@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(kThreads) hrt_forward_kernel(const FwdArgs a) 
 // L2: v * (up / ||v||_eps); torus-L2: (up * 2) * delta; L1 / torus-L1: sign weight.
 template <int KIND>
 __device__ __forceinline__ float dir1(float r, float sc) {
+  if (KIND == kPlainRows) return r;
   if (KIND == kTransE_L2 || KIND == kTorusE_L2) return __fmul_rn(r, sc);
   return r > 0.f ? sc : (r < 0.f ? -sc : 0.f);
 }
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
   const V* RV = reinterpret_cast<const V*>(a.res);
   for (uint32_t s = s0 + gw; s < s1; s += nw) {
     const uint32_t col = a.seg_col[s];
+    if (a.entity_only && col >= static_cast<uint32_t>(a.N)) continue;
     const uint32_t e0 = a.seg_start[s], e1 = a.seg_start[s + 1];
     V* P = reinterpret_cast<V*>(a.X) + static_cast<size_t>(col) * dv;
     for (int cb = 0; cb < dv; cb += 64) {
@@ -507,6 +509,7 @@ void launch_segment_backward(int kind, bool sgd, const BwdArgs& a, int num_sms, 
     case kTransE_L1: launch_bwd_k<kTransE_L1>(sgd, a, num_sms, s); break;
     case kTorusE_L2: launch_bwd_k<kTorusE_L2>(sgd, a, num_sms, s); break;
     case kTorusE_L1: launch_bwd_k<kTorusE_L1>(sgd, a, num_sms, s); break;
+    case kPlainRows: launch_bwd_k<kPlainRows>(sgd, a, num_sms, s); break;
     default: throw CudaError("launch_segment_backward: unsupported kind");
   }
 }

@@ -11,20 +11,31 @@ struct skg_ctx;
 
 namespace skg {
 
-// Floats of per-batch scratch the ht kernels need for `rows` pairs.
+// Floats of per-batch scratch the ht kernels need for `rows` rows.
 int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R);
 
 // One minibatch of TransH / TransR training: forward + hinge, entity scatter
 // through the sorted ht segments, relation-side reductions, SGD (+ normals
 // renormalization). `mark` (nullable) is called after the forward and after
 // the backward for per-phase profiling.
-void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms,
-                    cudaStream_t s, const std::function<void()>* mark);
-// score_batch for ht models (SCORE mode: res = v, res_u = u, scores).
-void ht_score(int kind, const FwdArgs& fa, float* work, int num_sms, cudaStream_t s);
+void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
+                    const std::function<void()>* mark, int64_t R);
+// score_batch for ht models (res = v, res_u = u, scores). `ba` carries the
+// batch's plan (TransR groups rows by relation through it).
+void ht_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s, int64_t R);
 // score_backward for ht models, accumulating into the sink tables.
-void ht_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj,
-                       float* g_normals, int num_sms, cudaStream_t s);
+void ht_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj, float* g_normals,
+                       int num_sms, cudaStream_t s, int64_t R);
+
+// TransR (transr.cu)
+int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R);
+void configure_transr_kernels();
+void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
+                        const std::function<void()>* mark, int64_t R);
+void transr_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
+                  int64_t R);
+void transr_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj, int num_sms,
+                           cudaStream_t s, int64_t R);
 
 // data parallel (dp.cu)
 void dp_destroy(skg_ctx* ctx);

@@ -25,6 +25,7 @@ enum Kind : int {
   kTransH_L1 = 5,
   kTransR_L2 = 6,
   kTransR_L1 = 7,
+  kPlainRows = 8,  // backward rows already hold a*D (ht models' du rows)
 };
 
 struct FwdArgs {
@@ -68,6 +69,7 @@ struct BwdArgs {
   int batch;
   const float* lr;  // device scalar (lets one captured graph serve every epoch)
   uint32_t* err;
+  int entity_only;  // skip relation-column segments (ht models reduce them separately)
 };
 
 void configure_hrt_kernels();
