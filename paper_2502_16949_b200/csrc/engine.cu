@@ -14,6 +14,7 @@
 using namespace skg;
 
 namespace {
+int grid_for(int64_t n);
 
 thread_local std::string g_create_err;
 
@@ -176,7 +177,46 @@ struct EpochShape {
   int64_t B, nb;
   bool shuffle;
   int kind;
+  // data parallel: this rank's shard of every global minibatch
+  int world = 1, rank = 0;
+  int64_t S = 0;        // shard size of full minibatches (B / world)
+  int64_t i0_last = 0;  // shard start inside the last minibatch
+  int64_t s_last = 0;   // shard size of the last minibatch (may be 0)
+  int64_t Mg = 0;       // rows of this rank's shards over the epoch
 };
+
+__global__ void shard_order_kernel(const int32_t* __restrict__ order, int64_t B, int64_t S, int rank,
+                                   int64_t nb, int64_t i0_last, int64_t Mg, int32_t* __restrict__ order_g) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < Mg;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = j / S;
+    order_g[j] = b < nb - 1 ? order[b * B + rank * S + (j - b * S)]
+                            : order[(nb - 1) * B + i0_last + (j - (nb - 1) * S)];
+  }
+}
+
+__global__ void dp_flags_kernel(const uint32_t* __restrict__ err, float* __restrict__ flags) {
+  flags[0] = err[0] == kErrLossNonFinite ? 1.f : 0.f;
+  flags[1] = (err[0] >= kErrGradEntity && err[0] <= kErrGradNormals) ? 1.f : 0.f;
+}
+
+// Dense step p -= lr * g after the all-reduce; any rank's flag stops every rank.
+__global__ void dp_sgd_kernel(float* __restrict__ X, const float* __restrict__ G, int64_t n,
+                              const float* __restrict__ lr, const float* __restrict__ flags,
+                              uint32_t* __restrict__ err, int batch) {
+  if (flags[0] > 0.f || flags[1] > 0.f) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const uint32_t code = flags[0] > 0.f ? kErrLossNonFinite : kErrGradEntity;
+      if (atomicCAS(&err[0], 0u, code) == 0u) err[1] = static_cast<uint32_t>(batch);
+    }
+    return;
+  }
+  if (err[0] != 0) return;
+  const float step = *lr;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    X[i] = __fsub_rn(X[i], __fmul_rn(step, G[i]));
+}
 
 // Enqueues one whole epoch on ctx->stream: permutation, plan, then per batch
 // the fused forward and the fused backward + SGD. When `ev` is non-null the
@@ -196,13 +236,72 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
     device_shuffle(ctx->seed_eff.p, ctx->M, ctx->order.p, ctx->shuffle, s);
   else
     device_iota(ctx->order.p, ctx->M, s);
-  build_epoch_plan(ctx->order.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->M, es.B,
-                   ctx->N, ctx->R, ctx->plan, s);
+  const bool dp = es.world > 1 || ctx->dp != nullptr;
+  if (dp) {
+    SKG_CUDA(cudaMemsetAsync(ctx->batch_loss.p, 0, sizeof(float) * es.nb, s));
+    shard_order_kernel<<<grid_for(es.Mg), 256, 0, s>>>(ctx->order.p, es.B, es.S, es.rank, es.nb, es.i0_last, es.Mg,
+                                                        ctx->order_g.p);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+    build_epoch_plan(ctx->order_g.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, es.Mg, es.S, ctx->N,
+                     ctx->R, ctx->plan, s);
+  } else {
+    build_epoch_plan(ctx->order.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->M, es.B, ctx->N,
+                     ctx->R, ctx->plan, s);
+  }
   mark();
   const bool ht = es.kind >= kTransH_L2;
+  const int64_t n_params = (ctx->N + ctx->R) * ctx->de;
   for (int64_t b = 0; b < es.nb; ++b) {
     const int64_t lo = b * es.B;
     const int Bb = static_cast<int>(std::min(es.B, ctx->M - lo));
+    if (dp) {
+      // shard of global minibatch b: forward with the global 1/m, gradient
+      // into the dense sink, NCCL sum over NVLink, identical step on all ranks
+      const int64_t Sb = b < es.nb - 1 ? es.S : es.s_last;
+      float* G = ctx->dp_grad.p;
+      SKG_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * (n_params + 2), s));
+      if (Sb > 0) {
+        FwdArgs fa = base_fwd(ctx);
+        fa.order = ctx->order_g.p + b * es.S;
+        fa.H = ctx->H.p;
+        fa.Rl = ctx->Rl.p;
+        fa.T = ctx->T.p;
+        fa.NH = ctx->NH.p;
+        fa.NT = ctx->NT.p;
+        fa.B = static_cast<int>(Sb);
+        fa.unit = 1.0f / static_cast<float>(Bb);
+        fa.loss_div = static_cast<float>(Bb);
+        fa.margin = ctx->h_lr[1];
+        fa.batch = static_cast<int>(b);
+        launch_hrt_forward(es.kind, true, fa, ctx->num_sms, s);
+        mark();
+        BwdArgs ba{};
+        ba.X = G;
+        ba.res = ctx->res.p;
+        ba.scal = ctx->scal.p;
+        ba.N = ctx->N;
+        ba.d = static_cast<int>(ctx->de);
+        ba.ent_val = ctx->plan.sorted_val;
+        ba.seg_start = ctx->plan.seg_start;
+        ba.seg_col = ctx->plan.seg_col;
+        ba.seg_base = ctx->plan.seg_base;
+        ba.batch = static_cast<int>(b);
+        ba.lr = ctx->lr_dev.p;
+        ba.err = ctx->err_words.p;
+        launch_segment_backward(es.kind, false, ba, ctx->num_sms, s);
+      } else {
+        mark();
+      }
+      dp_flags_kernel<<<1, 1, 0, s>>>(ctx->err_words.p, G + n_params);
+      dp_allreduce_sum(ctx, G, n_params + 2, s);
+      dp_sgd_kernel<<<grid_for(n_params), 256, 0, s>>>(ctx->tables.p, G, n_params, ctx->lr_dev.p, G + n_params,
+                                                        ctx->err_words.p, static_cast<int>(b));
+      count_launch(2);
+      SKG_LAUNCH_CHECK();
+      mark();
+      continue;
+    }
     FwdArgs fa = base_fwd(ctx);
     fa.order = ctx->order.p + lo;
     fa.H = ctx->H.p;
@@ -237,6 +336,7 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
       ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, ev ? &mark : nullptr, ctx->R);
     }
   }
+  if (dp) dp_allreduce_sum(ctx, ctx->batch_loss.p, es.nb, s);  // shard losses -> global batch losses
 }
 
 void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
@@ -252,6 +352,20 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   es.shuffle = tc.shuffle != 0;
   es.kind = kind_of(cfg);
   ctx->order.ensure(ctx->M);
+  es.world = dp_world(ctx);
+  es.rank = dp_rank(ctx);
+  if (ctx->dp) {
+    if (is_ht(cfg)) throw ConfigError("data-parallel training supports TransE / TorusE in this build");
+    if (es.B % es.world != 0) throw ConfigError("data parallel: global batch_size must be a multiple of the world size");
+    es.S = es.B / es.world;
+    const int64_t Bl = ctx->M - (es.nb - 1) * es.B;
+    const int64_t Sl = (Bl + es.world - 1) / es.world;
+    es.i0_last = std::min<int64_t>(es.rank * Sl, Bl);
+    es.s_last = std::min<int64_t>(es.i0_last + Sl, Bl) - es.i0_last;
+    es.Mg = (es.nb - 1) * es.S + es.s_last;
+    ctx->order_g.ensure(es.Mg + 1);
+    ctx->dp_grad.ensure((ctx->N + ctx->R) * ctx->de + 2);
+  }
   ensure_workspace(ctx, 2 * es.B);
   if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, 2 * es.B, ctx->de, ctx->dr, ctx->R));
   ctx->batch_loss.ensure(es.nb);
@@ -266,7 +380,8 @@ std::string graph_key(skg_ctx* ctx, const EpochShape& es) {
   std::ostringstream o;
   o << es.B << '/' << es.nb << '/' << es.shuffle << '/' << es.kind << '/' << ctx->M << '/'
     << ctx->tables.p << '/' << ctx->H.p << '/' << ctx->NH.p << '/' << ctx->order.p << '/' << ctx->res.p << '/'
-    << ctx->ht_work.p << '/' << ctx->plan.cap_entries << '/' << ctx->shuffle.cap_n;
+    << ctx->ht_work.p << '/' << ctx->plan.cap_entries << '/' << ctx->shuffle.cap_n << '/' << es.world << '/'
+    << es.rank << '/' << ctx->dp_grad.p << '/' << ctx->order_g.p;
   return o.str();
 }
 
@@ -931,10 +1046,7 @@ skg_status skg_renormalize_entities(skg_ctx* ctx) {
 skg_status skg_train_epoch(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc, int64_t epoch,
                            float lr, skg_epoch_report* rep) {
   return guard(ctx, [&] {
-    if (ctx->dp)
-      dp_train_epoch(ctx, *cfg, *tc, epoch, lr, rep);
-    else
-      train_epoch_impl(ctx, *cfg, *tc, epoch, lr, rep);
+    train_epoch_impl(ctx, *cfg, *tc, epoch, lr, rep);
   });
 }
 
@@ -1014,10 +1126,7 @@ skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_co
       if (tc->has_scheduler)
         lr = tc->lr * static_cast<float>(std::pow(tc->decay_factor, double(e / tc->decay_every)));
       skg_epoch_report rep{};
-      if (ctx->dp)
-        dp_train_epoch(ctx, *cfg, *tc, e, lr, &rep);
-      else
-        train_epoch_impl(ctx, *cfg, *tc, e, lr, &rep);
+      train_epoch_impl(ctx, *cfg, *tc, e, lr, &rep);
       if (tc->renorm_entities) {
         row_normalize_kernel<<<grid_for(ctx->N * 32), 256, 0, ctx->stream>>>(ctx->tables.p, ctx->N,
                                                                             static_cast<int>(ctx->de), 0,

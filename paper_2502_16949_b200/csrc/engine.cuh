@@ -79,6 +79,8 @@ struct skg_ctx {
   skg::DevBuf<float> tmp_f32;
   skg::DevBuf<uint8_t> flush_buf;
   skg::DevBuf<int64_t> stage_i64;   // caller id arrays staged in HBM
+  skg::DevBuf<float> dp_grad;       // data parallel: dense gradient sink + 2 flag slots
+  skg::DevBuf<int32_t> order_g;     // data parallel: this rank's shards of the epoch order
   skg::DevBuf<uint32_t> bad_idx;
   uint64_t* h_seed = nullptr;   // pinned
   float* h_lr = nullptr;        // pinned

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) hrt_forward_kernel(const FwdArgs a) 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_down_sync(kFull, acc, o));
     if (lane == 0) {
-      const float loss = __fdiv_rn(acc, static_cast<float>(a.B));  // training.cpp:93
+      const float loss = __fdiv_rn(acc, a.loss_div > 0.f ? a.loss_div : static_cast<float>(a.B));  // training.cpp:93
       a.batch_loss[a.batch] = loss;
       const uint32_t pflags = atomicOr(&a.err[3], 0u);
       if (!(fabsf(loss) <= 3.402823466e38f)) {

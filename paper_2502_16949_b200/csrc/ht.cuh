@@ -39,7 +39,8 @@ void transr_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float
 
 // data parallel (dp.cu)
 void dp_destroy(skg_ctx* ctx);
-void dp_train_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc, int64_t epoch,
-                    float lr, skg_epoch_report* rep);
+int dp_rank(const skg_ctx* ctx);
+int dp_world(const skg_ctx* ctx);
+void dp_allreduce_sum(skg_ctx* ctx, float* buf, int64_t n, cudaStream_t s);
 
 }  // namespace skg

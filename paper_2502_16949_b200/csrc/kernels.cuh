@@ -41,6 +41,7 @@ struct FwdArgs {
   const int32_t *H, *Rl, *T, *NH, *NT;
   int B;
   float margin, unit;
+  float loss_div;  // divisor of the batch loss (0: B); data parallel shards use the global batch size
   const float* upstream;  // SCORE: optional per-row upstream -> scal
   // outputs
   float* res;     // residual rows (v or delta), 2B x d (TRAIN) / B x d (SCORE)

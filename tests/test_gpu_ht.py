@@ -84,7 +84,7 @@ def test_ht_score_backward(eng, orc32, model, norm, de, dr):
 @pytest.mark.parametrize("model,de,dr,batch", [("transh", 16, 16, 64), ("transr", 16, 12, 64), ("transh", 128, 128, 4096),
                                                 ("transr", 128, 128, 4096)])
 def test_ht_fit_matches_oracle(eng, orc32, model, de, dr, batch):
-    n, r, m = 400, 11, 5000
+    n, r, m = 3000, 11, 6000
     h, rel, t = orc32.synthetic_train(n, r, m, 3)
     st = orc32.init_store(model, n, r, de, dr, 3)
     cfg = upload(eng, st, model, de, dr, "l2")
