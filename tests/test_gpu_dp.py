@@ -25,7 +25,7 @@ def test_dp_world1_matches_oracle_bitwise(orc32, model, norm):
     eng.set_triples(h, rel, t, n, r)
     kw = dict(lr=0.05, batch_size=1000, seed=9)
     rg = eng.fit(cfg, TrainConfig.make(epochs=3, **kw))
-    ro = orc32.fit(model, st, h, rel, t, orc32.train_config(epochs=3, **kw))
+    ro = orc32.fit(model, st, h, rel, t, orc32.train_config(epochs=3, **kw), norm=norm)
     for a, b in zip(rg, ro):
         assert abs(a.loss - b.loss) <= 1e-5 * max(1.0, abs(b.loss))
     ge, gr, _, _ = eng.store_download()
