@@ -146,10 +146,11 @@ FwdArgs base_fwd(skg_ctx* ctx) {
   return a;
 }
 
-void reset_err(skg_ctx* ctx) {
-  SKG_CUDA(cudaMemsetAsync(ctx->err_words.p, 0, sizeof(uint32_t) * 4, ctx->stream));
-  SKG_CUDA(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned), ctx->stream));
+void reset_err(skg_ctx* ctx, cudaStream_t s) {
+  SKG_CUDA(cudaMemsetAsync(ctx->err_words.p, 0, sizeof(uint32_t) * 4, s));
+  SKG_CUDA(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned), s));
 }
+void reset_err(skg_ctx* ctx) { reset_err(ctx, ctx->stream); }
 
 // Error word -> reference exception (training.cpp:135-137, embedding.cpp:173-186).
 void raise_device_error(const uint32_t* w, int64_t epoch) {
@@ -221,6 +222,10 @@ __global__ void dp_sgd_kernel(float* __restrict__ X, const float* __restrict__ G
 // Enqueues one whole epoch on ctx->stream: permutation, plan, then per batch
 // the fused forward and the fused backward + SGD. When `ev` is non-null the
 // phases are bracketed with events (profiling; not used under capture).
+void enqueue_plan(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s);
+void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s,
+                     const std::function<void()>* markp);
+
 void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>* ev) {
   cudaStream_t s = ctx->stream;
   std::function<void()> mark = [&]() {
@@ -231,25 +236,44 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
     ev->push_back(e);
   };
   mark();
-  reset_err(ctx);
+  enqueue_plan(ctx, es, ctx->cur, s);
+  mark();
+  enqueue_batches(ctx, es, ctx->cur, s, ev ? &mark : nullptr);
+}
+
+// Permutation + (data-parallel shard) + transposed-incidence plan of one epoch
+// into plan slot `slot`. Depends only on the seed, the triples and the
+// negatives, so the next epoch's plan can be built while this one trains.
+void enqueue_plan(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s) {
+  PlanSlot& ps = ctx->slots[slot];
+  uint64_t* seed = ctx->seed_eff.p + slot;
   if (es.shuffle)
-    device_shuffle(ctx->seed_eff.p, ctx->M, ctx->order.p, ctx->shuffle, s);
+    device_shuffle(seed, ctx->M, ps.order.p, ctx->shuffle, s);
   else
-    device_iota(ctx->order.p, ctx->M, s);
-  const bool dp = es.world > 1 || ctx->dp != nullptr;
-  if (dp) {
-    SKG_CUDA(cudaMemsetAsync(ctx->batch_loss.p, 0, sizeof(float) * es.nb, s));
-    shard_order_kernel<<<grid_for(es.Mg), 256, 0, s>>>(ctx->order.p, es.B, es.S, es.rank, es.nb, es.i0_last, es.Mg,
-                                                        ctx->order_g.p);
+    device_iota(ps.order.p, ctx->M, s);
+  if (es.world > 1 || ctx->dp != nullptr) {
+    shard_order_kernel<<<grid_for(es.Mg), 256, 0, s>>>(ps.order.p, es.B, es.S, es.rank, es.nb, es.i0_last, es.Mg,
+                                                        ps.order_g.p);
     count_launch();
     SKG_LAUNCH_CHECK();
-    build_epoch_plan(ctx->order_g.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, es.Mg, es.S, ctx->N,
-                     ctx->R, ctx->plan, s);
+    build_epoch_plan(ps.order_g.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, es.Mg, es.S, ctx->N,
+                     ctx->R, ps.plan, s);
   } else {
-    build_epoch_plan(ctx->order.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->M, es.B, ctx->N,
-                     ctx->R, ctx->plan, s);
+    build_epoch_plan(ps.order.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->M, es.B, ctx->N,
+                     ctx->R, ps.plan, s);
   }
-  mark();
+}
+
+// Every minibatch of one epoch on plan slot `slot`.
+void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s,
+                     const std::function<void()>* markp) {
+  auto mark = [&]() {
+    if (markp) (*markp)();
+  };
+  PlanSlot& ps = ctx->slots[slot];
+  const bool dp = es.world > 1 || ctx->dp != nullptr;
+  reset_err(ctx, s);
+  if (dp) SKG_CUDA(cudaMemsetAsync(ctx->batch_loss.p, 0, sizeof(float) * es.nb, s));
   const bool ht = es.kind >= kTransH_L2;
   const int64_t n_params = (ctx->N + ctx->R) * ctx->de;
   for (int64_t b = 0; b < es.nb; ++b) {
@@ -263,7 +287,7 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
       SKG_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * (n_params + 2), s));
       if (Sb > 0) {
         FwdArgs fa = base_fwd(ctx);
-        fa.order = ctx->order_g.p + b * es.S;
+        fa.order = ps.order_g.p + b * es.S;
         fa.H = ctx->H.p;
         fa.Rl = ctx->Rl.p;
         fa.T = ctx->T.p;
@@ -282,10 +306,10 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
         ba.scal = ctx->scal.p;
         ba.N = ctx->N;
         ba.d = static_cast<int>(ctx->de);
-        ba.ent_val = ctx->plan.sorted_val;
-        ba.seg_start = ctx->plan.seg_start;
-        ba.seg_col = ctx->plan.seg_col;
-        ba.seg_base = ctx->plan.seg_base;
+        ba.ent_val = ps.plan.sorted_val;
+        ba.seg_start = ps.plan.seg_start;
+        ba.seg_col = ps.plan.seg_col;
+        ba.seg_base = ps.plan.seg_base;
         ba.batch = static_cast<int>(b);
         ba.lr = ctx->lr_dev.p;
         ba.err = ctx->err_words.p;
@@ -303,7 +327,7 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
       continue;
     }
     FwdArgs fa = base_fwd(ctx);
-    fa.order = ctx->order.p + lo;
+    fa.order = ps.order.p + lo;
     fa.H = ctx->H.p;
     fa.Rl = ctx->Rl.p;
     fa.T = ctx->T.p;
@@ -320,10 +344,10 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
     ba.scal = ctx->scal.p;
     ba.N = ctx->N;
     ba.d = static_cast<int>(ctx->de);
-    ba.ent_val = ctx->plan.sorted_val;
-    ba.seg_start = ctx->plan.seg_start;
-    ba.seg_col = ctx->plan.seg_col;
-    ba.seg_base = ctx->plan.seg_base;
+    ba.ent_val = ps.plan.sorted_val;
+    ba.seg_start = ps.plan.seg_start;
+    ba.seg_col = ps.plan.seg_col;
+    ba.seg_base = ps.plan.seg_base;
     ba.batch = static_cast<int>(b);
     ba.lr = ctx->lr_dev.p;
     ba.err = ctx->err_words.p;
@@ -333,7 +357,7 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
       launch_segment_backward(es.kind, true, ba, ctx->num_sms, s);
       mark();
     } else {
-      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, ev ? &mark : nullptr, ctx->R);
+      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, markp, ctx->R);
     }
   }
   if (dp) dp_allreduce_sum(ctx, ctx->batch_loss.p, es.nb, s);  // shard losses -> global batch losses
@@ -363,9 +387,14 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
     es.i0_last = std::min<int64_t>(es.rank * Sl, Bl);
     es.s_last = std::min<int64_t>(es.i0_last + Sl, Bl) - es.i0_last;
     es.Mg = (es.nb - 1) * es.S + es.s_last;
-    ctx->order_g.ensure(es.Mg + 1);
+    for (auto& sl : ctx->slots) sl.order_g.ensure(es.Mg + 1);
     ctx->dp_grad.ensure((ctx->N + ctx->R) * ctx->de + 2);
   }
+  for (auto& sl : ctx->slots) {
+    sl.order.ensure(ctx->M + 1);
+    sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
+  }
+  ctx->shuffle.reserve(ctx->M);
   ensure_workspace(ctx, 2 * es.B);
   if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, 2 * es.B, ctx->de, ctx->dr, ctx->R));
   ctx->batch_loss.ensure(es.nb);
@@ -379,9 +408,19 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
 std::string graph_key(skg_ctx* ctx, const EpochShape& es) {
   std::ostringstream o;
   o << es.B << '/' << es.nb << '/' << es.shuffle << '/' << es.kind << '/' << ctx->M << '/'
-    << ctx->tables.p << '/' << ctx->H.p << '/' << ctx->NH.p << '/' << ctx->order.p << '/' << ctx->res.p << '/'
-    << ctx->ht_work.p << '/' << ctx->plan.cap_entries << '/' << ctx->shuffle.cap_n << '/' << es.world << '/'
-    << es.rank << '/' << ctx->dp_grad.p << '/' << ctx->order_g.p;
+    << ctx->tables.p << '/' << ctx->H.p << '/' << ctx->NH.p << '/' << ctx->slots[0].order.p << '/'
+    << ctx->slots[1].order.p << '/' << ctx->res.p << '/' << ctx->ht_work.p << '/'
+    << ctx->slots[0].plan.cap_entries << '/' << ctx->slots[1].plan.cap_entries << '/' << ctx->shuffle.cap_n << '/'
+    << es.world << '/' << es.rank << '/' << ctx->dp_grad.p << '/' << ctx->slots[0].order_g.p << '/'
+    << ctx->slots[1].order_g.p << '/' << ctx->proj.p << '/' << ctx->normals.p;
+  return o.str();
+}
+
+// Identity of an epoch plan: everything it depends on.
+std::string plan_key(skg_ctx* ctx, const EpochShape& es, const skg_train_config& tc, int64_t epoch) {
+  std::ostringstream o;
+  o << epoch << '/' << (es.shuffle ? tc.seed : 0) << '/' << es.shuffle << '/' << es.B << '/' << ctx->M << '/'
+    << ctx->data_version << '/' << es.world << '/' << es.rank << '/' << ctx->H.p << '/' << ctx->NH.p;
   return o.str();
 }
 
@@ -403,51 +442,85 @@ void finish_epoch(skg_ctx* ctx, const EpochShape& es, int64_t epoch, skg_epoch_r
   rep->loss = static_cast<double>(loss_sum / static_cast<float>(ctx->M));
 }
 
-void set_epoch_params(skg_ctx* ctx, const skg_train_config& tc, int64_t epoch, float lr) {
-  ctx->h_seed[0] = epoch_seed(tc.seed, epoch);
+void set_epoch_params(skg_ctx* ctx, const skg_train_config& tc, float lr) {
   ctx->h_lr[0] = lr;
   ctx->h_lr[1] = tc.margin;
-  SKG_CUDA(cudaMemcpyAsync(ctx->seed_eff.p, ctx->h_seed, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
   SKG_CUDA(cudaMemcpyAsync(ctx->lr_dev.p, ctx->h_lr, sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+}
+
+void set_slot_seed(skg_ctx* ctx, int slot, uint64_t seed_eff) {
+  ctx->h_seed[slot] = seed_eff;
+  SKG_CUDA(cudaMemcpyAsync(ctx->seed_eff.p + slot, ctx->h_seed + slot, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+}
+
+// One captured graph per plan slot: the main branch trains every minibatch on
+// slot `cur`; a side branch builds the next epoch's plan into the other slot.
+void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
+  const int nxt = 1 - cur;
+  const int64_t before = kernel_launches();
+  cudaGraph_t g = nullptr;
+  SKG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    SKG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+    SKG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+    enqueue_plan(ctx, es, nxt, ctx->side);
+    SKG_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
+    enqueue_batches(ctx, es, cur, ctx->stream, nullptr);
+    SKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+  } catch (...) {
+    cudaStreamEndCapture(ctx->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  SKG_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+  if (ctx->graphs[cur]) cudaGraphExecDestroy(ctx->graphs[cur]);
+  ctx->graphs[cur] = nullptr;
+  SKG_CUDA(cudaGraphInstantiate(&ctx->graphs[cur], g, 0));
+  SKG_CUDA(cudaGraphDestroy(g));
+  ctx->graph_launches_k[cur] = kernel_launches() - before;
 }
 
 void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
                       int64_t epoch, float lr, skg_epoch_report* rep) {
   EpochShape es{};
   prepare_epoch(ctx, cfg, tc, es);
-  // Capture once per epoch shape. Margin is baked into the forward launch, so
-  // it is part of the key as well.
-  std::string key = graph_key(ctx, es) + "/" + std::to_string(tc.margin);
-  set_epoch_params(ctx, tc, epoch, lr);
-  SKG_CUDA(cudaStreamSynchronize(ctx->stream));  // margin in h_lr[1] is read at capture
-  if (!ctx->graph || ctx->graph_key != key) {
-    if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
-    ctx->graph = nullptr;
-    // Warm the lazily allocated workspaces (first call sizes them) outside capture.
-    ctx->shuffle.reserve(ctx->M);
-    ctx->plan.reserve(6 * ctx->M, es.nb);
-    ctx->plan.sort.reserve(6 * ctx->M);
+  set_epoch_params(ctx, tc, lr);
+  const int cur = ctx->cur, nxt = 1 - cur;
+  // The plan of this epoch was normally built by the previous epoch's graph;
+  // otherwise (first epoch, new data, other schedule) build it now.
+  const std::string pk = plan_key(ctx, es, tc, epoch);
+  int64_t eager = 0;
+  if (ctx->slots[cur].key != pk) {
+    set_slot_seed(ctx, cur, epoch_seed(tc.seed, epoch));
     const int64_t before = kernel_launches();
-    cudaGraph_t g;
-    SKG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    try {
-      enqueue_epoch(ctx, es, nullptr);
-    } catch (...) {
-      cudaStreamEndCapture(ctx->stream, &g);
-      if (g) cudaGraphDestroy(g);
-      throw;
-    }
-    SKG_CUDA(cudaStreamEndCapture(ctx->stream, &g));
-    SKG_CUDA(cudaGraphInstantiate(&ctx->graph, g, 0));
-    SKG_CUDA(cudaGraphDestroy(g));
-    ctx->graph_launches = kernel_launches() - before;
-    ctx->graph_key = key;
+    enqueue_plan(ctx, es, cur, ctx->stream);
+    eager = kernel_launches() - before;
+    ctx->slots[cur].key = pk;
+  }
+  // Speculatively build epoch + 1's plan (same data and schedule) alongside.
+  set_slot_seed(ctx, nxt, epoch_seed(tc.seed, epoch + 1));
+  ctx->slots[nxt].key.clear();
+  SKG_CUDA(cudaStreamSynchronize(ctx->stream));  // margin in h_lr[1] is read at capture
+  // Margin is baked into the forward launches, so it is part of the graph key.
+  const std::string gk = graph_key(ctx, es) + "/" + std::to_string(tc.margin);
+  if (!ctx->graphs[cur] || ctx->graph_keys[cur] != gk) {
+    capture_epoch_graph(ctx, es, cur);
+    ctx->graph_keys[cur] = gk;
   }
   SKG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-  SKG_CUDA(cudaGraphLaunch(ctx->graph, ctx->stream));
+  SKG_CUDA(cudaGraphLaunch(ctx->graphs[cur], ctx->stream));
   SKG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-  ctx->last_launches = ctx->graph_launches;
-  finish_epoch(ctx, es, epoch, rep);
+  ctx->last_launches = ctx->graph_launches_k[cur] + eager;
+  ctx->last_slot = cur;
+  ctx->slots[nxt].key = plan_key(ctx, es, tc, epoch + 1);
+  ctx->cur = nxt;
+  try {
+    finish_epoch(ctx, es, epoch, rep);
+  } catch (...) {
+    ctx->slots[nxt].key.clear();  // a failed epoch leaves no reusable prefetch
+    throw;
+  }
   float ms = 0.f;
   SKG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   rep->t_forward_s = 0.0;
@@ -465,6 +538,7 @@ void negative_sample_impl(skg_ctx* ctx, uint64_t seed, bool avoid) {  // trainin
                               ctx->stream))
     throw CudaError("negative_sample: device RNG window exhausted");
   ctx->has_neg = true;
+  ++ctx->data_version;
 }
 
 // ------------------------------------------------------ per-op kernels (small)
@@ -598,11 +672,14 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     SKG_CUDA(cudaEventCreate(&ctx->ev0));
     SKG_CUDA(cudaEventCreate(&ctx->ev1));
+    SKG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     ctx->err_words.ensure(4);
     ctx->counter.ensure(1);
-    ctx->seed_eff.ensure(1);
+    ctx->seed_eff.ensure(2);
     ctx->lr_dev.ensure(2);
-    SKG_CUDA(cudaMallocHost(&ctx->h_seed, sizeof(uint64_t)));
+    SKG_CUDA(cudaMallocHost(&ctx->h_seed, sizeof(uint64_t) * 2));
     SKG_CUDA(cudaMallocHost(&ctx->h_lr, sizeof(float) * 2));
     SKG_CUDA(cudaMallocHost(&ctx->h_err, sizeof(uint32_t) * 4));
     SKG_CUDA(cudaMemset(ctx->err_words.p, 0, sizeof(uint32_t) * 4));
@@ -625,6 +702,11 @@ void skg_destroy(skg_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   dp_destroy(ctx);
   if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+  for (auto g : ctx->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->h_seed) cudaFreeHost(ctx->h_seed);
@@ -740,6 +822,7 @@ skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int6
       if (bad[1] != 0xFFFFFFFFu) throw ShapeError("triple " + std::to_string(bad[1]) + ": relation id out of range");
     }
     ctx->M = m;
+    ++ctx->data_version;
   });
 }
 
@@ -759,6 +842,7 @@ skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const i
       if (bad[0] != 0xFFFFFFFFu) throw ShapeError("triple " + std::to_string(bad[0]) + ": entity id out of range");
     }
     ctx->has_neg = true;
+    ++ctx->data_version;
   });
 }
 
@@ -1056,10 +1140,14 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const sk
   return guard(ctx, [&] {
     EpochShape es{};
     prepare_epoch(ctx, *cfg, *tc, es);
-    set_epoch_params(ctx, *tc, epoch, lr);
+    set_epoch_params(ctx, *tc, lr);
+    set_slot_seed(ctx, ctx->cur, epoch_seed(tc->seed, epoch));
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
     std::vector<cudaEvent_t> ev;
-    enqueue_epoch(ctx, es, &ev);
+    enqueue_epoch(ctx, es, &ev);  // eager, no overlap: every launch is bracketed
+    ctx->last_slot = ctx->cur;
+    ctx->slots[0].key.clear();
+    ctx->slots[1].key.clear();
     finish_epoch(ctx, es, epoch, rep);
     auto el = [&](size_t a, size_t b) {
       float ms = 0.f;
@@ -1094,15 +1182,15 @@ skg_status skg_flush_l2(skg_ctx* ctx) {
 skg_status skg_plan_stats(skg_ctx* ctx, int64_t batch, int64_t* segments, int64_t* entries,
                           int64_t* relation_segments) {
   return guard(ctx, [&] {
-    if (batch < 0 || batch >= ctx->plan.nb || !ctx->plan.seg_base) throw ShapeError("plan_stats: no such batch");
+    if (batch < 0 || batch >= ctx->slots[ctx->last_slot].plan.nb || !ctx->slots[ctx->last_slot].plan.seg_base) throw ShapeError("plan_stats: no such batch");
     uint32_t sb[2];
-    SKG_CUDA(cudaMemcpy(sb, ctx->plan.seg_base + batch, sizeof(sb), cudaMemcpyDeviceToHost));
+    SKG_CUDA(cudaMemcpy(sb, ctx->slots[ctx->last_slot].plan.seg_base + batch, sizeof(sb), cudaMemcpyDeviceToHost));
     uint32_t e0 = 0, e1 = 0;
-    SKG_CUDA(cudaMemcpy(&e0, ctx->plan.seg_start + sb[0], sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    SKG_CUDA(cudaMemcpy(&e1, ctx->plan.seg_start + sb[1], sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    SKG_CUDA(cudaMemcpy(&e0, ctx->slots[ctx->last_slot].plan.seg_start + sb[0], sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    SKG_CUDA(cudaMemcpy(&e1, ctx->slots[ctx->last_slot].plan.seg_start + sb[1], sizeof(uint32_t), cudaMemcpyDeviceToHost));
     std::vector<uint32_t> cols(sb[1] - sb[0]);
     if (!cols.empty())
-      SKG_CUDA(cudaMemcpy(cols.data(), ctx->plan.seg_col + sb[0], sizeof(uint32_t) * cols.size(),
+      SKG_CUDA(cudaMemcpy(cols.data(), ctx->slots[ctx->last_slot].plan.seg_col + sb[0], sizeof(uint32_t) * cols.size(),
                           cudaMemcpyDeviceToHost));
     int64_t nrel = 0;
     for (uint32_t c : cols) nrel += c >= ctx->N;

@@ -44,6 +44,14 @@ struct DevBuf {
 
 struct DpState;  // NCCL replicas (dp.cu)
 
+// One epoch's permutation and transposed-incidence plan. Two slots let the
+// next epoch's plan be built on a side stream while the current one trains.
+struct PlanSlot {
+  DevBuf<int32_t> order, order_g;
+  EpochPlan plan;
+  std::string key;  // which (epoch, seed, data version, shape) the slot holds
+};
+
 }  // namespace skg
 
 struct skg_ctx {
@@ -88,8 +96,17 @@ struct skg_ctx {
   float* h_loss = nullptr;      // pinned, per batch
   int64_t h_loss_cap = 0;
 
-  // ---- captured epoch graph
-  cudaGraphExec_t graph = nullptr;
+  // ---- training-loop plan slots and captured epoch graphs (one per slot)
+  skg::PlanSlot slots[2];
+  int cur = 0;        // slot holding (or to hold) the plan of the next epoch to train
+  int last_slot = 0;  // slot the last trained epoch used (plan_stats)
+  uint64_t data_version = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaGraphExec_t graph = nullptr;  // legacy handle (unused)
+  cudaGraphExec_t graphs[2] = {nullptr, nullptr};
+  std::string graph_keys[2];
+  int64_t graph_launches_k[2] = {0, 0};
   std::string graph_key;
   int64_t graph_launches = 0;
   int64_t last_launches = 0;
