@@ -61,50 +61,49 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons polled through NVML every 2 ms during the timed region."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+            0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device):
         self.device = device
-        self.rows = []
-        self.proc = None
+        self.samples = []
+        self.reasons = 0
+        self.stop_flag = threading.Event()
         self.thread = None
+        self.max_mhz = None
+        self.err = None
+
+    def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_r = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self.stop_flag.is_set():
+                self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                self.reasons |= int(get_r(h))
+                time.sleep(0.002)
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
-            return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+        time.sleep(0.05)
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop_flag.set()
         if self.thread:
             self.thread.join(timeout=5)
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled: " + str(self.err)]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(v for k, v in self.BITS.items() if self.reasons & k),
+                "samples": len(self.samples), "source": "NVML, 2 ms polling"}
 
 
 def dist_setup():
@@ -160,18 +159,28 @@ def algorithmic_bytes(cfg, eng, nb):
 
 
 def cpu_reference(cfg, h, r, t, nh, nt, budget_s, threads):
-    """Reference CPU path (oracle restatement of the reference algorithm) on a
-    bounded sample: whole minibatches of epoch 0 until ~budget_s of CPU work."""
+    """Reference CPU path (oracle restatement of the reference algorithm, see
+    oracle/) on the host cores. Whole epochs (shuffle included) when an epoch
+    fits the budget, else a window of whole minibatches of epoch 0."""
     from oracle.oracle import Oracle
     orc = Oracle("f32")
     orc.set_num_threads(threads)
     st = orc.init_store(cfg["model"], cfg["N"], cfg["R"], cfg["de"], cfg["dr"], SEED)
     tc = orc.train_config(lr=LR, margin=MARGIN, batch_size=cfg["B"], seed=SEED)
-    nb_total = (len(h) + cfg["B"] - 1) // cfg["B"]
-    secs, _ = orc.train_batches(cfg["model"], st, (h, r, t), (nh, nt), tc, 0, LR, 0, 1, norm=cfg["norm"])
-    nb = max(1, min(nb_total - 1, int(budget_s / max(secs, 1e-3))))
+    M = len(h)
+    nb_total = (M + cfg["B"] - 1) // cfg["B"]
+    t1, _ = orc.train_batches(cfg["model"], st, (h, r, t), (nh, nt), tc, 0, LR, 0, 1, norm=cfg["norm"])
+    if t1 * nb_total <= budget_s / 2:
+        done, secs, ep = 0, 0.0, 0
+        while secs < budget_s:
+            rep = orc.train_epoch(cfg["model"], st, (h, r, t), (nh, nt), tc, ep, LR, norm=cfg["norm"])
+            secs += rep.t_forward_s + rep.t_backward_s + rep.t_step_s
+            done += M
+            ep += 1
+        return done / secs, f"{ep} full epochs ({done} pos triples, phase timers of train_epoch)", secs
+    nb = max(1, min(nb_total - 1, int(budget_s / max(t1, 1e-3))))
     secs, _ = orc.train_batches(cfg["model"], st, (h, r, t), (nh, nt), tc, 0, LR, 1, nb, norm=cfg["norm"])
-    done = sum(min(cfg["B"], len(h) - b * cfg["B"]) for b in range(1, 1 + nb))
+    done = sum(min(cfg["B"], M - b * cfg["B"]) for b in range(1, 1 + nb))
     return done / secs, f"{nb} minibatches ({done} pos triples) of epoch 0 after 1 warm-up minibatch", secs
 
 
