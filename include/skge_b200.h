@@ -183,6 +183,10 @@ skg_status skg_flush_l2(skg_ctx* ctx);
 skg_status skg_plan_stats(skg_ctx* ctx, int64_t batch, int64_t* segments, int64_t* entries,
                           int64_t* relation_segments);
 
+/* Tensor-core self test: D = A(m,k) . B(n,k) over 128^3 through the operand
+ * views the TransR kernel uses (0: A,B K-major; 1: B MN-major; 2: both MN). */
+skg_status skg_debug_tc_gemm(skg_ctx* ctx, int32_t mode, const float* A, const float* B, float* D);
+
 /* ---- data-parallel replicas (one process per GPU) ------------------------ */
 /* Joins an NCCL communicator (unique id produced by skg_nccl_unique_id on
  * rank 0 and broadcast by the caller). After this, skg_train_epoch treats the

@@ -1229,3 +1229,16 @@ skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_co
 }
 
 }  // extern "C"
+
+extern "C" skg_status skg_debug_tc_gemm(skg_ctx* ctx, int32_t mode, const float* A, const float* B, float* D) {
+  return guard(ctx, [&] {
+    if (mode < 0 || mode > 2) throw ConfigError("debug_tc_gemm: mode 0..2");
+    DevBuf<float> buf;
+    buf.ensure(3 * 128 * 128);
+    SKG_CUDA(cudaMemcpyAsync(buf.p, A, sizeof(float) * 128 * 128, cudaMemcpyHostToDevice, ctx->stream));
+    SKG_CUDA(cudaMemcpyAsync(buf.p + 128 * 128, B, sizeof(float) * 128 * 128, cudaMemcpyHostToDevice, ctx->stream));
+    transr_tc_selftest(mode, buf.p, buf.p + 128 * 128, buf.p + 2 * 128 * 128, ctx->stream);
+    SKG_CUDA(cudaMemcpyAsync(D, buf.p + 2 * 128 * 128, sizeof(float) * 128 * 128, cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}

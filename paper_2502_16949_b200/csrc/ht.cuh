@@ -37,6 +37,20 @@ void transr_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, i
 void transr_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj, int num_sms,
                            cudaStream_t s, int64_t R);
 
+// TransR on tcgen05 (transr_tc.cu), d_e = d_r = 128
+bool transr_tc_supported(int de, int dr);
+void configure_transr_tc_kernels();
+int64_t transr_tc_slots(int num_sms, int64_t R);
+void launch_transr_tc(bool l2, int mode, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,
+                      const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
+                      const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,
+                      int num_sms, cudaStream_t s);
+void launch_transr_tc_apply(const uint32_t* tile_total, const uint32_t* seg_tiles, const uint32_t* tile_seg,
+                            const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
+                            float* proj, float* rel, const float* lr, bool sgd, const uint32_t* err, int64_t R,
+                            cudaStream_t s);
+void transr_tc_selftest(int mode, const float* A, const float* B, float* D, cudaStream_t s);
+
 // data parallel (dp.cu)
 void dp_destroy(skg_ctx* ctx);
 int dp_rank(const skg_ctx* ctx);

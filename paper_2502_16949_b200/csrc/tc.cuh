@@ -1,0 +1,126 @@
+// tcgen05 (5th-gen tensor core) helpers for sm_100a: TMEM allocation,
+// shared-memory matrix descriptors, kind::tf32 MMA issue/commit, TMEM loads.
+//
+// Operand tiles live in shared memory in the canonical no-swizzle
+// ("interleaved") layout: 16-byte units (4 fp32), grouped in 8x16B core
+// matrices. One physical layout serves both majorness views:
+//   unit(row r, k) = (r % 8) + (r / 8) * R8 + (k / 4) * K4,   element k % 4
+// reads as K-major with SBO = R8, LBO = K4 (rows = M/N, K contiguous in 4s),
+// and the MN-major chunk layout
+//   unit(mn, k)    = (mn / 4) * MN4 + (k % 8) + (k / 8) * K8,  element mn % 4
+// reads as MN-major with SBO = MN4, LBO = K8.
+#pragma once
+
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace skg {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Shared-memory matrix descriptor (no swizzle), tcgen05 "version 1" format:
+// start [0,14) >>4, LBO [16,30) >>4, SBO [32,46) >>4, version bit 46,
+// base offset [49,52) = 0, layout type [61,64) = 0 (SWIZZLE_NONE).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  return d;
+}
+
+// Instruction descriptor for kind::tf32 with an fp32 accumulator.
+__host__ __device__ constexpr uint32_t make_idesc_tf32(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4)                                   // D format F32
+         | (2u << 7)                                 // A format TF32
+         | (2u << 10)                                // B format TF32
+         | (static_cast<uint32_t>(a_mn_major) << 15)  // A major (0 = K)
+         | (static_cast<uint32_t>(b_mn_major) << 16)  // B major
+         | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Whole-warp TMEM allocation; the base address is written to *dst (smem).
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(ncols) : "memory");
+}
+
+// 16 consecutive fp32 columns of this thread's TMEM lane (warp w reads lanes
+// 32*(w%4) .. +31; taddr must carry that lane base in bits [16,32)).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// fp32 -> (hi, lo) with hi exactly representable in tf32 (3xTF32 split).
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  lo = __fsub_rn(x, hi);
+}
+
+// Element offsets (in floats) of the two chunk layouts described above.
+// K-major chunk of `rows` x 32: R8 = 64 units, K4 = 8 units.
+__device__ __forceinline__ int kmaj_off(int r, int k) { return (((r & 7) + (r >> 3) * 64 + (k >> 2) * 8) << 2) + (k & 3); }
+// MN-major chunk of 128 (mn) x 32 (k): MN4 = 8 units, K8 = 256 units.
+__device__ __forceinline__ int mnmaj_off(int mn, int k) {
+  return (((mn >> 2) * 8 + (k & 7) + (k >> 3) * 256) << 2) + (mn & 3);
+}
+constexpr uint32_t kKmajLBO = 8 * 16, kKmajSBO = 64 * 16;        // bytes
+constexpr uint32_t kMnmajLBO = 256 * 16, kMnmajSBO = 8 * 16;     // bytes
+constexpr uint32_t kKmajStepBytes = 2 * kKmajLBO;                // K = 8 per MMA
+constexpr uint32_t kMnmajStepBytes = kMnmajLBO;                  // K = 8 per MMA
+
+}  // namespace tc
+}  // namespace skg

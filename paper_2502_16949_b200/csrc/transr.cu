@@ -18,6 +18,8 @@
 // The three products run as 128x128x128 register-tiled FP32 FMA blocks in this
 // version; the projection has d_r*d_e*2 FLOP per row, so the tile is the unit a
 // tcgen05 (3xTF32) MMA version replaces without changing the data flow.
+#include <algorithm>
+
 #include "common.cuh"
 #include "ht.cuh"
 #include "primitives.cuh"
@@ -389,7 +391,7 @@ Work carve(float* work, int64_t rows, int64_t de, int64_t dr, int64_t R) {
   w.tile_total = w.tile_p0 + mt;
   w.seg_tiles = w.tile_total + 2;
   w.dm_part = work + 3 * mt + 2 * R + 8;
-  w.dr_part = w.dm_part + mt * dr * de;
+  w.dr_part = w.dm_part + std::max<int64_t>(mt, transr_tc_slots(256, R)) * dr * de;
   return w;
 }
 
@@ -449,7 +451,8 @@ void configure_one() {
 
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
-  return 3 * mt + 2 * R + 8 + mt * dr * de + mt * dr + 64;
+  const int64_t parts = std::max<int64_t>(mt, transr_tc_slots(256, R));  // tc path: (CTA, relation) runs
+  return 3 * mt + 2 * R + 8 + parts * dr * de + parts * dr + 64;
 }
 
 void configure_transr_kernels() {
@@ -457,11 +460,37 @@ void configure_transr_kernels() {
   configure_one<true, kRows>();
   configure_one<false, kTrain>();
   configure_one<false, kRows>();
+  configure_transr_tc_kernels();
 }
+
+namespace {
+// tcgen05 path (d_e = d_r = 128): tile list, persistent projection CTAs.
+void run_tc(int kind, int mode, const FwdArgs& fa, const BwdArgs& ba, const Work& w, int num_sms, cudaStream_t s) {
+  transr_tiles_kernel<<<1, 32, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, mode == 0 ? 1 : 0,
+                                       w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  launch_transr_tc(kind == kTransR_L2, mode, fa, ba.ent_val, ba.seg_start, ba.seg_col, w.tile_seg, w.tile_p0,
+                   w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, num_sms, s);
+}
+}  // namespace
 
 void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                         const std::function<void()>* mark, int64_t R) {
   const Work w = carve(work, 2 * static_cast<int64_t>(fa.B), fa.de, fa.dr, R);
+  if (transr_tc_supported(fa.de, fa.dr)) {
+    run_tc(kind, 0, fa, ba, w, num_sms, s);
+    if (mark) (*mark)();
+    BwdArgs eb = ba;
+    eb.entity_only = 1;
+    eb.d = fa.de;
+    launch_segment_backward(kPlainRows, true, eb, num_sms, s);
+    launch_transr_tc_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
+                           const_cast<float*>(fa.proj), const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de),
+                           ba.lr, true, ba.err, R, s);
+    if (mark) (*mark)();
+    return;
+  }
   run_tiles(kind, true, fa, ba, w, true, 2 * static_cast<int64_t>(fa.B), R, s);
   if (mark) (*mark)();
   BwdArgs eb = ba;
@@ -475,14 +504,27 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
 
 void transr_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                   int64_t R) {
-  (void)num_sms;
   const Work w = carve(work, fa.B, fa.de, fa.dr, R);
+  if (transr_tc_supported(fa.de, fa.dr)) {
+    run_tc(kind, 1, fa, ba, w, num_sms, s);
+    return;
+  }
   run_tiles(kind, false, fa, ba, w, false, fa.B, R, s);
 }
 
 void transr_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj, int num_sms,
                            cudaStream_t s, int64_t R) {
   const Work w = carve(work, fa.B, fa.de, fa.dr, R);
+  if (transr_tc_supported(fa.de, fa.dr)) {
+    run_tc(kind, 2, fa, ba, w, num_sms, s);
+    BwdArgs eb = ba;
+    eb.entity_only = 1;
+    eb.d = fa.de;
+    launch_segment_backward(kPlainRows, false, eb, num_sms, s);
+    launch_transr_tc_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
+                           g_proj, ba.Xrel, ba.lr, false, ba.err, R, s);
+    return;
+  }
   run_tiles(kind, false, fa, ba, w, true, fa.B, R, s);
   BwdArgs eb = ba;
   eb.entity_only = 1;

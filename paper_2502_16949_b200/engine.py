@@ -103,6 +103,7 @@ def load_library():
         "skg_init_store": [C.c_uint32, i64, i64, i64, i64, C.c_uint64, vp, vp, vp, vp],
         "skg_flush_l2": [vp],
         "skg_plan_stats": [vp, i64, vp, vp, vp],
+        "skg_debug_tc_gemm": [vp, i32, vp, vp, vp],
     }
     L.skg_host_last_error.restype = C.c_char_p
     for name, args in sig.items():
@@ -284,6 +285,12 @@ class Engine:
     # ------------------------------------------------------------ measurement hooks
     def flush_l2(self):
         self._check(self.L.skg_flush_l2(self.h))
+
+    def debug_tc_gemm(self, mode: int, A, B):
+        A, B = _f32(A), _f32(B)
+        D = np.empty((128, 128), np.float32)
+        self._check(self.L.skg_debug_tc_gemm(self.h, mode, _p(A), _p(B), _p(D)))
+        return D
 
     def plan_stats(self, batch: int):
         s, e, r = C.c_int64(), C.c_int64(), C.c_int64()
