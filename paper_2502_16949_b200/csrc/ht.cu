@@ -27,7 +27,7 @@ namespace skg {
 namespace {
 
 constexpr int kHtThreads = 128;
-constexpr int kRelParts = 16;  // first-level partial blocks per relation segment
+constexpr int kRelParts = 64;  // first-level partial blocks per relation segment
 
 enum Mode : int { kTrain = 0, kScore = 1, kPrep = 2 };
 
@@ -281,7 +281,7 @@ __device__ __forceinline__ bool rel_segment(const RelArgs& a, int k, uint32_t& s
 }
 
 __global__ void __launch_bounds__(128) rel_partial_kernel(const RelArgs a) {
-  __shared__ float part[4][2][256];
+  __shared__ float part[4][2][128];
   if (a.err[0] != 0) return;
   uint32_t s;
   if (!rel_segment(a, blockIdx.x, s)) return;
@@ -292,31 +292,60 @@ __global__ void __launch_bounds__(128) rel_partial_kernel(const RelArgs a) {
   const uint32_t w0 = p0 + static_cast<uint32_t>((static_cast<uint64_t>(p1 - p0) * warp) / 4);
   const uint32_t w1 = p0 + static_cast<uint32_t>((static_cast<uint64_t>(p1 - p0) * (warp + 1)) / 4);
   const int d = a.d;
-  for (int cb = 0; cb < d; cb += 256) {
-    float accA[8], accB[8];
+  for (int cb = 0; cb < d; cb += 128) {
+    float accA[4], accB[4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) accA[q] = accB[q] = 0.f;
-    for (uint32_t e = w0; e < w1; ++e) {
-      const uint32_t row = a.ent_val[e] & 0x7fffffffu;
-      if (a.scal[row] == 0.f) continue;
-      const float* ra = a.srcA + static_cast<size_t>(row) * d;
-      const float* rb = a.srcB + static_cast<size_t>(row) * d;
+    for (int q = 0; q < 4; ++q) accA[q] = accB[q] = 0.f;
+    // entries in order; row ids and activity fetched 32 at a time, rows of
+    // four live entries loaded together (independent loads in flight)
+    for (uint32_t g = w0; g < w1; g += 32) {
+      const uint32_t cnt = min(32u, w1 - g);
+      uint32_t myrow = 0;
+      bool mylive = false;
+      if (lane < cnt) {
+        myrow = a.ent_val[g + lane] & 0x7fffffffu;
+        mylive = a.scal[myrow] != 0.f;
+      }
+      unsigned live = __ballot_sync(kFull, mylive);
+      while (live) {
+        int n = 0;
+        uint32_t rows[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int c = cb + lane + 32 * q;
-        if (c < d) {
-          accA[q] = __fadd_rn(accA[q], ra[c]);
-          accB[q] = __fadd_rn(accB[q], rb[c]);
+        for (int q = 0; q < 4; ++q) {
+          const int k = live ? __ffs(live) - 1 : 0;
+          rows[q] = __shfl_sync(kFull, myrow, k);
+          if (live) {
+            live &= live - 1;
+            ++n;
+          }
         }
+        float va[4][4], vb[4][4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = cb + lane + 32 * q;
+            const bool ok = e < n && c < d;
+            va[e][q] = ok ? __ldg(a.srcA + static_cast<size_t>(rows[e]) * d + c) : 0.f;
+            vb[e][q] = ok ? __ldg(a.srcB + static_cast<size_t>(rows[e]) * d + c) : 0.f;
+          }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e < n)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              accA[q] = __fadd_rn(accA[q], va[e][q]);
+              accB[q] = __fadd_rn(accB[q], vb[e][q]);
+            }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 4; ++q) {
       part[warp][0][lane + 32 * q] = accA[q];
       part[warp][1][lane + 32 * q] = accB[q];
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < 256 && cb + c < d; c += blockDim.x) {
+    for (int c = threadIdx.x; c < 128 && cb + c < d; c += blockDim.x) {
       float x = 0.f, y = 0.f;
       for (int w = 0; w < 4; ++w) {
         x = __fadd_rn(x, part[w][0][c]);

@@ -390,7 +390,7 @@ Work carve(float* work, int64_t rows, int64_t de, int64_t dr, int64_t R) {
   w.tile_p0 = w.tile_seg + mt;
   w.tile_total = w.tile_p0 + mt;
   w.seg_tiles = w.tile_total + 2;
-  w.dm_part = work + 3 * mt + 2 * R + 8;
+  w.dm_part = work + ((3 * mt + 2 * R + 8 + 31) / 32) * 32;  // 128 B aligned (float4 stores)
   w.dr_part = w.dm_part + std::max<int64_t>(mt, transr_tc_slots(256, R)) * dr * de;
   return w;
 }
@@ -452,7 +452,7 @@ void configure_one() {
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
   const int64_t parts = std::max<int64_t>(mt, transr_tc_slots(256, R));  // tc path: (CTA, relation) runs
-  return 3 * mt + 2 * R + 8 + parts * dr * de + parts * dr + 64;
+  return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + parts * dr * de + parts * dr + 64;
 }
 
 void configure_transr_kernels() {

@@ -4,8 +4,9 @@
 // = 128 rows of one relation), but the three products run as 128x128x128
 // MMAs with fp32 accumulators in TMEM:
 //   GEMM1  V  = U M_r^T          A = U (K-major), B = M_r (K-major)
-//   GEMM2  dU = DZ M_r           A = DZ (K-major), B = M_r (MN-major)
-//   GEMM3  dM += DZ^T U          A = DZ (MN-major), B = U (MN-major)
+//   GEMM2  dU = DZ M_r           A = DZ, B = M_r^T (transposed while staging)
+//   GEMM3  dM += DZ^T U          A = DZ^T, B = U^T (transposed while staging)
+// All descriptors are K-major no-swizzle (the MN-major tf32 view is avoided).
 // Precision: 3xTF32 (hi*hi + hi*lo + lo*hi, hi = rna-tf32(x), lo = x - hi),
 // fp32-class results for the 1e-5 parity bar. Operands are kept in fp32 in
 // shared memory (U, DZ) and split into hi/lo 32-wide K chunks staged in the
@@ -33,7 +34,8 @@ namespace {
 constexpr int kD = 128;        // d_e = d_r handled by this kernel
 constexpr int kRows = 128;     // rows per tile
 constexpr int kPairs = 64;
-constexpr int kThreads = 128;  // 4 warps: warp w <-> TMEM lanes 32w..32w+31
+constexpr int kThreads = 256;  // 8 warps: warp w <-> TMEM lanes 32(w%4)..+31
+constexpr int kEpi = 128;      // warps 0-3 run the row-per-thread epilogues
 constexpr int kStride = kD + 4;
 constexpr int kChunk = 32;
 constexpr uint32_t kTmemCols = 512;
@@ -97,16 +99,18 @@ __device__ __forceinline__ void stage_kmajor(float* hi, float* lo, const float* 
   }
 }
 
-// Stage an MN-major chunk (128 mn x 32 k) from a row-major source indexed
-// [k][mn] (row k0 + k, column mn), row stride ld.
-__device__ __forceinline__ void stage_mnmajor(float* hi, float* lo, const float* src, int ld, int k0,
-                                              bool global_src) {
+// Stage a K-major chunk (128 rows x 32 k) from a source indexed [k][row]
+// (row k0 + k, column row), row stride ld: the transposed operand views
+// (M_r as [c][n] for dU, DZ^T and U^T for dM) are built here, so every MMA
+// reads K-major descriptors.
+__device__ __forceinline__ void stage_kmajor_t(float* hi, float* lo, const float* src, int ld, int k0,
+                                               bool global_src) {
   for (int i = threadIdx.x; i < kD * kChunk; i += kThreads) {
-    const int k = i / kD, mn = i % kD;
-    const float x = global_src ? __ldg(src + static_cast<size_t>(k0 + k) * ld + mn) : src[(k0 + k) * ld + mn];
+    const int k = i / kD, r = i % kD;
+    const float x = global_src ? __ldg(src + static_cast<size_t>(k0 + k) * ld + r) : src[(k0 + k) * ld + r];
     float h, l;
     tc::split_tf32(x, h, l);
-    const int o = tc::mnmaj_off(mn, k);
+    const int o = tc::kmaj_off(r, k);
     hi[o] = h;
     lo[o] = l;
   }
@@ -125,8 +129,9 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   __shared__ uint64_t mbar;
   __shared__ uint32_t tmem_base;
-  __shared__ int rrow[kRows];
+  __shared__ int rrow[kRows], rh[kRows], rt[kRows];
   __shared__ float rs[kRows], rsc[kRows];
+  __shared__ float colsum[2][kD];
   __shared__ float tile_loss_sh;
   const FwdArgs& f = a.f;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -141,7 +146,9 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = tmem_base;
-  const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+  const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  const int qrow = (warp & 3) * 32 + lane;  // TMEM lane (row) of this thread
+  const int half = warp >> 2;               // column half for the split epilogues
   uint32_t phase = 0;
 
   const uint32_t T = alive ? a.tile_total[0] : 0u;
@@ -158,15 +165,15 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
   auto flush = [&](int k) {
     // slot index j + k: pieces of the (CTA range) x (relation run) partition
     const uint32_t slot = blockIdx.x + static_cast<uint32_t>(k);
-    float* dst = a.dm_part + static_cast<size_t>(slot) * dr * de + static_cast<size_t>(tid) * de;
+    float* dst = a.dm_part + static_cast<size_t>(slot) * dr * de + static_cast<size_t>(qrow) * de;
     float v[16];
 #pragma unroll 1
-    for (int c = 0; c < de; c += 16) {
+    for (int c = half * 64; c < half * 64 + 64; c += 16) {
       tc::tmem_ld16(tbase + lane_addr + kColDM + c, v);
 #pragma unroll
       for (int q = 0; q < 16; q += 4) *reinterpret_cast<float4*>(dst + c + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
     }
-    a.dr_part[static_cast<size_t>(slot) * dr + tid] = dr_acc;
+    if (tid < kD) a.dr_part[static_cast<size_t>(slot) * dr + tid] = dr_acc;
     dr_acc = 0.f;
   };
 
@@ -194,24 +201,16 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
     cur_k = k;
     const uint32_t units = MODE == kTrain ? len / 2 : len;
     const int np = static_cast<int>(min(static_cast<uint32_t>(MODE == kTrain ? kPairs : kRows), units - p0));
-    // ---- row ids
-    {
-      int row2 = -1;
+    // ---- row ids (thread per row): incidence row, head and tail
+    if (tid < kRows) {
+      int row2 = -1, h = 0, tt = 0;
       if (MODE == kTrain) {
         const int kk = tid & 63;
         if (kk < np) row2 = static_cast<int>(a.ent_val[e0 + (tid < 64 ? 0 : units) + p0 + kk] & 0x7fffffffu);
       } else if (tid < np) {
         row2 = static_cast<int>(a.ent_val[e0 + p0 + tid] & 0x7fffffffu);
       }
-      rrow[tid] = row2;
-    }
-    __syncthreads();
-    // ---- U = h - t (warp per row, float4 lanes)
-    for (int m = warp; m < kRows; m += kThreads / 32) {
-      const int row2 = rrow[m];
-      float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
       if (row2 >= 0) {
-        int h, tt;
         if (MODE == kTrain) {
           const bool neg = row2 >= f.B;
           const int id = f.order[neg ? row2 - f.B : row2];
@@ -221,11 +220,28 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
           h = f.H[row2];
           tt = f.T[row2];
         }
-        const float4 xh = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(h) * de) + lane);
-        const float4 xt = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(tt) * de) + lane);
-        u = make_float4(__fsub_rn(xh.x, xt.x), __fsub_rn(xh.y, xt.y), __fsub_rn(xh.z, xt.z), __fsub_rn(xh.w, xt.w));
       }
-      *reinterpret_cast<float4*>(S.U + m * kStride + 4 * lane) = u;
+      rrow[tid] = row2;
+      rh[tid] = h;
+      rt[tid] = tt;
+    }
+    __syncthreads();
+    // ---- U = h - t: each warp gathers 16 rows, 8 rows (16 x 16 B per lane) in flight
+#pragma unroll 1
+    for (int m0 = warp * 16; m0 < warp * 16 + 16; m0 += 8) {
+      float4 xh[8], xt[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        xh[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rh[m0 + q]) * de) + lane);
+        xt[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rt[m0 + q]) * de) + lane);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 u = rrow[m0 + q] >= 0 ? make_float4(__fsub_rn(xh[q].x, xt[q].x), __fsub_rn(xh[q].y, xt[q].y),
+                                                          __fsub_rn(xh[q].z, xt[q].z), __fsub_rn(xh[q].w, xt[q].w))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(S.U + (m0 + q) * kStride + 4 * lane) = u;
+      }
     }
     __syncthreads();
     const float* Mr = f.proj + r * static_cast<int64_t>(dr) * de;
@@ -242,12 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
       mma_round(&mbar, phase);
       __syncthreads();
     }
-    // ---- epilogue 1: v = V + r, reference-order score, hinge, dz
-    const int m = tid;  // TMEM lane of this thread
+    // ---- epilogue 1 (warps 0-3, thread = row): v = V + r, reference-order score
+    const int m = qrow;
     const float* relr = f.X + f.N * static_cast<int64_t>(de) + r * dr;
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
     bool bad = false;
-    {
+    if (tid < kEpi) {
       float v[16];
       for (int c = 0; c < dr; c += 16) {
         tc::tmem_ld16(tbase + lane_addr + kColV + c, v);
@@ -268,10 +284,12 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
       }
     }
     const float ssum = __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));  // norms.hpp:33 (d >= 8)
-    rs[m] = ssum;
-    if (bad && rrow[m] >= 0) pend |= kPendEntity;
+    if (tid < kEpi) {
+      rs[m] = ssum;
+      if (bad && rrow[m] >= 0) pend |= kPendEntity;
+    }
     __syncthreads();
-    {
+    if (tid < kEpi) {
       const int row2 = rrow[m];
       float up = 0.f;
       if (MODE == kTrain) {
@@ -301,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
     __syncthreads();
     if (MODE == kTrain) lsum = __fadd_rn(lsum, tile_loss_sh);
     if (MODE == kScore) {
-      const int row2 = rrow[m];
+      const int row2 = tid < kEpi ? rrow[m] : -1;
       if (row2 >= 0)
         for (int c = 0; c < de; c += 4)
           *reinterpret_cast<float4*>(f.res_u + static_cast<size_t>(row2) * de + c) =
@@ -309,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
       __syncthreads();
       continue;
     }
-    {  // DZ row (norm_direction) into shared memory
+    if (tid < kEpi) {  // DZ row (norm_direction) into shared memory
       const float sc = rsc[m];
       float v[16];
       for (int c = 0; c < dr; c += 16) {
@@ -323,29 +341,32 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
       }
     }
     __syncthreads();
-    {  // thread n: sum(dz) over the tile's rows, in row order
+    {  // sum(dz) per column: two halves of the rows, combined in fixed order
+      const int n = tid & (kD - 1), hr = tid >> 7;
       float cs = 0.f;
-      for (int mm = 0; mm < kRows; ++mm) cs = __fadd_rn(cs, S.DZ[mm * kStride + tid]);
-      dr_acc = __fadd_rn(dr_acc, cs);
+      for (int mm = hr * 64; mm < hr * 64 + 64; ++mm) cs = __fadd_rn(cs, S.DZ[mm * kStride + n]);
+      colsum[hr][n] = cs;
     }
+    __syncthreads();
+    if (tid < kD) dr_acc = __fadd_rn(dr_acc, __fadd_rn(colsum[0][tid], colsum[1][tid]));
     // ---- GEMM2: dU = DZ M_r (K = dr); B is M_r read MN-major
     for (int kc = 0; kc < dr; kc += kChunk) {
       stage_kmajor(S.Ahi, S.Alo, S.DZ, kStride, kc, kRows, false);
-      stage_mnmajor(S.Bhi, S.Blo, Mr, de, kc, true);
+      stage_kmajor_t(S.Bhi, S.Blo, Mr, de, kc, true);
       tc::fence_async_shared();
       __syncthreads();
       if (tid == 0) {
         tc::fence_after();
-        issue_chunk(S, tbase + kColDU, false, true, kc == 0);
+        issue_chunk(S, tbase + kColDU, false, false, kc == 0);
       }
       mma_round(&mbar, phase);
       __syncthreads();
     }
-    {  // epilogue 2: dU rows of active rows -> entity scatter input
-      const int row2 = rrow[m];
-      const bool act = row2 >= 0 && rsc[m] != 0.f;
+    {  // epilogue 2 (all warps: row qrow, column half): dU rows of active rows
+      const int row2 = rrow[qrow];
+      const bool act = row2 >= 0 && rsc[qrow] != 0.f;
       float v[16];
-      for (int c = 0; c < de; c += 16) {
+      for (int c = half * 64; c < half * 64 + 64; c += 16) {
         tc::tmem_ld16(tbase + lane_addr + kColDU + c, v);
         if (act) {
           float* dst = f.res_u + static_cast<size_t>(row2) * de + c;
@@ -356,13 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
     }
     // ---- GEMM3: dM += DZ^T U (K = rows); both operands read MN-major
     for (int kc = 0; kc < kRows; kc += kChunk) {
-      stage_mnmajor(S.Ahi, S.Alo, S.DZ, kStride, kc, false);
-      stage_mnmajor(S.Bhi, S.Blo, S.U, kStride, kc, false);
+      stage_kmajor_t(S.Ahi, S.Alo, S.DZ, kStride, kc, false);
+      stage_kmajor_t(S.Bhi, S.Blo, S.U, kStride, kc, false);
       tc::fence_async_shared();
       __syncthreads();
       if (tid == 0) {
         tc::fence_after();
-        issue_chunk(S, tbase + kColDM, true, true, dm_first && kc == 0);
+        issue_chunk(S, tbase + kColDM, false, false, dm_first && kc == 0);
       }
       mma_round(&mbar, phase);
       __syncthreads();
@@ -432,7 +453,7 @@ __global__ void transr_tc_apply_kernel(const uint32_t* __restrict__ tile_total, 
     for (int j = 0; j < G; ++j) {
       const uint32_t a0 = static_cast<uint32_t>((static_cast<uint64_t>(T) * j) / G);
       const uint32_t a1 = static_cast<uint32_t>((static_cast<uint64_t>(T) * (j + 1)) / G);
-      if (a1 <= lo || a0 >= hi) continue;
+      if (a0 >= a1 || a1 <= lo || a0 >= hi) continue;  // empty CTA ranges own no slot
       const size_t slot = static_cast<size_t>(j) + k;
       g = __fadd_rn(g, i < kD * kD ? dm_part[slot * kD * kD + i] : dr_part[slot * kD + (i - kD * kD)]);
     }
@@ -461,24 +482,25 @@ __global__ void __launch_bounds__(kThreads, 1) tc_selftest_kernel(int mode, cons
   tc::fence_after();
   uint32_t phase = 0;
   for (int kc = 0; kc < kD; kc += kChunk) {
-    if (mode == 2) stage_mnmajor(S.Ahi, S.Alo, A, kD, kc, true);
+    if (mode == 2) stage_kmajor_t(S.Ahi, S.Alo, A, kD, kc, true);
     else stage_kmajor(S.Ahi, S.Alo, A, kD, kc, kRows, true);
     if (mode == 0) stage_kmajor(S.Bhi, S.Blo, B, kD, kc, kD, true);
-    else stage_mnmajor(S.Bhi, S.Blo, B, kD, kc, true);
+    else stage_kmajor_t(S.Bhi, S.Blo, B, kD, kc, true);
     tc::fence_async_shared();
     __syncthreads();
     if (tid == 0) {
       tc::fence_after();
-      issue_chunk(S, tmem_base, mode == 2, mode != 0, kc == 0);
+      issue_chunk(S, tmem_base, false, false, kc == 0);
     }
     mma_round(&mbar, phase);
     __syncthreads();
   }
   float v[16];
-  for (int c = 0; c < kD; c += 16) {
-    tc::tmem_ld16(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-    for (int q = 0; q < 16; ++q) D[tid * kD + c + q] = v[q];
-  }
+  if (warp < 4)
+    for (int c = 0; c < kD; c += 16) {
+      tc::tmem_ld16(tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+      for (int q = 0; q < 16; ++q) D[tid * kD + c + q] = v[q];
+    }
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem_base, kTmemCols);
