@@ -44,7 +44,8 @@ int64_t transr_tc_slots(int num_sms, int64_t R);
 void launch_transr_tc(bool l2, int mode, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,
                       const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
                       const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,
-                      int num_sms, cudaStream_t s);
+                      float* mr_chunks, int64_t R, int num_sms, cudaStream_t s);
+int64_t transr_tc_mr_floats(int64_t R);
 void launch_transr_tc_apply(const uint32_t* tile_total, const uint32_t* seg_tiles, const uint32_t* tile_seg,
                             const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
                             float* proj, float* rel, const float* lr, bool sgd, const uint32_t* err, int64_t R,

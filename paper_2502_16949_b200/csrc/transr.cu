@@ -378,7 +378,7 @@ size_t tile_smem(int de, int dr) {
 
 struct Work {
   uint32_t *tile_seg, *tile_p0, *tile_total, *seg_tiles;
-  float *dm_part, *dr_part;
+  float *dm_part, *dr_part, *mr_chunks;
 };
 
 int64_t max_tiles(int64_t rows, int64_t R) { return rows / kTilePairs + 2 * R + 2; }
@@ -392,6 +392,7 @@ Work carve(float* work, int64_t rows, int64_t de, int64_t dr, int64_t R) {
   w.seg_tiles = w.tile_total + 2;
   w.dm_part = work + ((3 * mt + 2 * R + 8 + 31) / 32) * 32;  // 128 B aligned (float4 stores)
   w.dr_part = w.dm_part + std::max<int64_t>(mt, transr_tc_slots(256, R)) * dr * de;
+  w.mr_chunks = w.dr_part + ((std::max<int64_t>(mt, transr_tc_slots(256, R)) * dr + 31) / 32) * 32;
   return w;
 }
 
@@ -452,7 +453,8 @@ void configure_one() {
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
   const int64_t parts = std::max<int64_t>(mt, transr_tc_slots(256, R));  // tc path: (CTA, relation) runs
-  return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + parts * dr * de + parts * dr + 64;
+  return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + parts * dr * de + ((parts * dr + 31) / 32) * 32 +
+         transr_tc_mr_floats(R) + 64;
 }
 
 void configure_transr_kernels() {
@@ -465,13 +467,14 @@ void configure_transr_kernels() {
 
 namespace {
 // tcgen05 path (d_e = d_r = 128): tile list, persistent projection CTAs.
-void run_tc(int kind, int mode, const FwdArgs& fa, const BwdArgs& ba, const Work& w, int num_sms, cudaStream_t s) {
+void run_tc(int kind, int mode, const FwdArgs& fa, const BwdArgs& ba, const Work& w, int num_sms, cudaStream_t s,
+            int64_t R) {
   transr_tiles_kernel<<<1, 32, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, mode == 0 ? 1 : 0,
                                        w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err);
   count_launch();
   SKG_LAUNCH_CHECK();
   launch_transr_tc(kind == kTransR_L2, mode, fa, ba.ent_val, ba.seg_start, ba.seg_col, w.tile_seg, w.tile_p0,
-                   w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, num_sms, s);
+                   w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, w.mr_chunks, R, num_sms, s);
 }
 }  // namespace
 
@@ -479,7 +482,7 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
                         const std::function<void()>* mark, int64_t R) {
   const Work w = carve(work, 2 * static_cast<int64_t>(fa.B), fa.de, fa.dr, R);
   if (transr_tc_supported(fa.de, fa.dr)) {
-    run_tc(kind, 0, fa, ba, w, num_sms, s);
+    run_tc(kind, 0, fa, ba, w, num_sms, s, R);
     if (mark) (*mark)();
     BwdArgs eb = ba;
     eb.entity_only = 1;
@@ -506,7 +509,7 @@ void transr_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, i
                   int64_t R) {
   const Work w = carve(work, fa.B, fa.de, fa.dr, R);
   if (transr_tc_supported(fa.de, fa.dr)) {
-    run_tc(kind, 1, fa, ba, w, num_sms, s);
+    run_tc(kind, 1, fa, ba, w, num_sms, s, R);
     return;
   }
   run_tiles(kind, false, fa, ba, w, false, fa.B, R, s);
@@ -516,7 +519,7 @@ void transr_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float
                            cudaStream_t s, int64_t R) {
   const Work w = carve(work, fa.B, fa.de, fa.dr, R);
   if (transr_tc_supported(fa.de, fa.dr)) {
-    run_tc(kind, 2, fa, ba, w, num_sms, s);
+    run_tc(kind, 2, fa, ba, w, num_sms, s, R);
     BwdArgs eb = ba;
     eb.entity_only = 1;
     eb.d = fa.de;

@@ -54,7 +54,31 @@ struct TcArgs {
   const uint32_t* seg_tiles;   // first tile of each relation segment
   float* dm_part;              // [slot][dr*de]
   float* dr_part;              // [slot][dr]
+  const float* mr_chunks;      // per relation: [layout 2][chunk 4][hi,lo][128*32] pre-split M_r
 };
+
+// Per relation r, both K-major views of M_r, split hi/lo and laid out chunk by
+// chunk exactly as the MMA reads them, so the projection CTAs fetch B operands
+// with 16 KB bulk copies instead of re-splitting M_r for every tile.
+//   layout 0 (GEMM1): rows n, k = c;   layout 1 (GEMM2): rows c, k = n.
+constexpr int kChunkFloats = kD * kChunk;
+constexpr int64_t kMrFloatsPerRel = 2 * 4 * 2 * kChunkFloats;
+__global__ void transr_prep_mr_kernel(const float* __restrict__ proj, float* __restrict__ out) {
+  const int r = blockIdx.x, lc = blockIdx.y;  // lc = layout * 4 + chunk
+  const int layout = lc >> 2, kc = (lc & 3) * kChunk;
+  const float* M = proj + static_cast<int64_t>(r) * kD * kD;
+  float* hi = out + r * kMrFloatsPerRel + static_cast<int64_t>(lc) * 2 * kChunkFloats;
+  float* lo = hi + kChunkFloats;
+  for (int i = threadIdx.x; i < kChunkFloats; i += blockDim.x) {
+    const int row = i / kChunk, k = i % kChunk;
+    const float x = layout == 0 ? M[row * kD + kc + k] : M[(kc + k) * kD + row];
+    float h, l;
+    tc::split_tf32(x, h, l);
+    const int o = tc::kmaj_off(row, k);
+    hi[o] = h;
+    lo[o] = l;
+  }
+}
 
 struct Smem {
   float U[kRows * kStride];
@@ -86,10 +110,19 @@ __device__ __forceinline__ void issue_chunk(const Smem& s, uint32_t tmem_d, bool
 }
 
 // Stage a K-major chunk (rows x 32) from a row-major fp32 source (row stride ld).
+// Lane mapping: a warp covers one 8-row x 4-k core matrix (lane>>2 = row,
+// lane&3 = k), so the 32 stores of a warp hit 32 distinct banks.
+__device__ __forceinline__ void lane_rk(int i, int& r, int& k) {
+  const int lane = i & 31, g = i >> 5;
+  r = (g & 15) * 8 + (lane >> 2);
+  k = (g >> 4) * 4 + (lane & 3);
+}
+
 __device__ __forceinline__ void stage_kmajor(float* hi, float* lo, const float* src, int ld, int k0, int rows,
                                              bool global_src) {
   for (int i = threadIdx.x; i < rows * kChunk; i += kThreads) {
-    const int r = i / kChunk, k = i % kChunk;
+    int r, k;
+    lane_rk(i, r, k);
     const float x = global_src ? __ldg(src + static_cast<size_t>(r) * ld + k0 + k) : src[r * ld + k0 + k];
     float h, l;
     tc::split_tf32(x, h, l);
@@ -106,7 +139,8 @@ __device__ __forceinline__ void stage_kmajor(float* hi, float* lo, const float* 
 __device__ __forceinline__ void stage_kmajor_t(float* hi, float* lo, const float* src, int ld, int k0,
                                                bool global_src) {
   for (int i = threadIdx.x; i < kD * kChunk; i += kThreads) {
-    const int k = i / kD, r = i % kD;
+    int r, k;
+    lane_rk(i, r, k);
     const float x = global_src ? __ldg(src + static_cast<size_t>(k0 + k) * ld + r) : src[(k0 + k) * ld + r];
     float h, l;
     tc::split_tf32(x, h, l);
@@ -127,11 +161,12 @@ template <bool L2, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar, bbar;
   __shared__ uint32_t tmem_base;
   __shared__ int rrow[kRows], rh[kRows], rt[kRows];
   __shared__ float rs[kRows], rsc[kRows];
   __shared__ float colsum[2][kD];
+  __shared__ float relsh[kD];
   __shared__ float tile_loss_sh;
   const FwdArgs& f = a.f;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -140,12 +175,28 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
   if (warp == 0) tc::tmem_alloc(&tmem_base, kTmemCols);
   if (tid == 0) {
     tc::mbar_init(&mbar, 1);
+    tc::mbar_init(&bbar, 1);
     tc::fence_barrier_init();
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = tmem_base;
+  uint32_t bphase = 0;
+  // B operand chunk (hi, lo) of M_r by bulk copy; issued before the A staging
+  // so the copy overlaps it, awaited before the MMA.
+  auto load_b = [&](int64_t rr, int layout, int chunk) {
+    if (tid == 0) {
+      const float* src = a.mr_chunks + rr * kMrFloatsPerRel + static_cast<int64_t>(layout * 4 + chunk) * 2 * kChunkFloats;
+      tc::mbar_arrive_expect_tx(&bbar, 2 * kChunkFloats * sizeof(float));
+      tc::bulk_g2s(S.Bhi, src, kChunkFloats * sizeof(float), &bbar);
+      tc::bulk_g2s(S.Blo, src + kChunkFloats, kChunkFloats * sizeof(float), &bbar);
+    }
+  };
+  auto wait_b = [&]() {
+    tc::mbar_wait(&bbar, bphase);
+    bphase ^= 1u;
+  };
   const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
   const int qrow = (warp & 3) * 32 + lane;  // TMEM lane (row) of this thread
   const int half = warp >> 2;               // column half for the split epilogues
@@ -224,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
       rrow[tid] = row2;
       rh[tid] = h;
       rt[tid] = tt;
+      relsh[tid] = __ldg(f.X + f.N * static_cast<int64_t>(de) + r * dr + tid);
     }
     __syncthreads();
     // ---- U = h - t: each warp gathers 16 rows, 8 rows (16 x 16 B per lane) in flight
@@ -247,8 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
     const float* Mr = f.proj + r * static_cast<int64_t>(dr) * de;
     // ---- GEMM1: V = U M_r^T (K = de)
     for (int kc = 0; kc < de; kc += kChunk) {
+      load_b(r, 0, kc / kChunk);
       stage_kmajor(S.Ahi, S.Alo, S.U, kStride, kc, kRows, false);
-      stage_kmajor(S.Bhi, S.Blo, Mr, de, kc, dr, true);
+      wait_b();
       tc::fence_async_shared();
       __syncthreads();
       if (tid == 0) {
@@ -260,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
     }
     // ---- epilogue 1 (warps 0-3, thread = row): v = V + r, reference-order score
     const int m = qrow;
-    const float* relr = f.X + f.N * static_cast<int64_t>(de) + r * dr;
+    const float* relr = relsh;
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
     bool bad = false;
     if (tid < kEpi) {
@@ -269,8 +322,8 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
         tc::tmem_ld16(tbase + lane_addr + kColV + c, v);
 #pragma unroll
         for (int q = 0; q < 16; q += 4) {
-          const float x0 = __fadd_rn(v[q], __ldg(relr + c + q)), x1 = __fadd_rn(v[q + 1], __ldg(relr + c + q + 1));
-          const float x2 = __fadd_rn(v[q + 2], __ldg(relr + c + q + 2)), x3 = __fadd_rn(v[q + 3], __ldg(relr + c + q + 3));
+          const float x0 = __fadd_rn(v[q], relr[c + q]), x1 = __fadd_rn(v[q + 1], relr[c + q + 1]);
+          const float x2 = __fadd_rn(v[q + 2], relr[c + q + 2]), x3 = __fadd_rn(v[q + 3], relr[c + q + 3]);
           bad |= nonfinite(x0) | nonfinite(x1) | nonfinite(x2) | nonfinite(x3);
           s0 = __fadd_rn(s0, norm_term<L2>(x0));
           s1 = __fadd_rn(s1, norm_term<L2>(x1));
@@ -334,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
         tc::tmem_ld16(tbase + lane_addr + kColV + c, v);
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float x = __fadd_rn(v[q], __ldg(relr + c + q));
+          const float x = __fadd_rn(v[q], relr[c + q]);
           S.DZ[m * kStride + c + q] =
               sc == 0.f ? 0.f : (L2 ? __fmul_rn(x, sc) : (x > 0.f ? sc : (x < 0.f ? -sc : 0.f)));
         }
@@ -351,8 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
     if (tid < kD) dr_acc = __fadd_rn(dr_acc, __fadd_rn(colsum[0][tid], colsum[1][tid]));
     // ---- GEMM2: dU = DZ M_r (K = dr); B is M_r read MN-major
     for (int kc = 0; kc < dr; kc += kChunk) {
+      load_b(r, 1, kc / kChunk);
       stage_kmajor(S.Ahi, S.Alo, S.DZ, kStride, kc, kRows, false);
-      stage_kmajor_t(S.Bhi, S.Blo, Mr, de, kc, true);
+      wait_b();
       tc::fence_async_shared();
       __syncthreads();
       if (tid == 0) {
@@ -448,13 +502,23 @@ __global__ void transr_tc_apply_kernel(const uint32_t* __restrict__ tile_total, 
   if (hi <= lo) return;
   const int64_t r = static_cast<int64_t>(seg_col[tile_seg[lo]]) - N;
   const float step = *lr;
-  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < kD * kD + kD; i += gridDim.y * blockDim.x) {
-    float g = 0.f;
-    for (int j = 0; j < G; ++j) {
+  __shared__ int jl[1024];
+  __shared__ int nj;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int j = 0; j < G && c < 1024; ++j) {
       const uint32_t a0 = static_cast<uint32_t>((static_cast<uint64_t>(T) * j) / G);
       const uint32_t a1 = static_cast<uint32_t>((static_cast<uint64_t>(T) * (j + 1)) / G);
       if (a0 >= a1 || a1 <= lo || a0 >= hi) continue;  // empty CTA ranges own no slot
-      const size_t slot = static_cast<size_t>(j) + k;
+      jl[c++] = j;
+    }
+    nj = c;
+  }
+  __syncthreads();
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < kD * kD + kD; i += gridDim.y * blockDim.x) {
+    float g = 0.f;
+    for (int q = 0; q < nj; ++q) {
+      const size_t slot = static_cast<size_t>(jl[q]) + k;
       g = __fadd_rn(g, i < kD * kD ? dm_part[slot * kD * kD + i] : dr_part[slot * kD + (i - kD * kD)]);
     }
     float* p = i < kD * kD ? proj + r * kD * kD + i : rel + r * kD + (i - kD * kD);
@@ -529,11 +593,16 @@ void configure_transr_tc_kernels() {
 
 int64_t transr_tc_slots(int num_sms, int64_t R) { return num_sms + R + 2; }
 
+int64_t transr_tc_mr_floats(int64_t R) { return R * kMrFloatsPerRel; }
+
 void launch_transr_tc(bool l2, int mode, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,
                       const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
                       const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,
-                      int num_sms, cudaStream_t s) {
+                      float* mr_chunks, int64_t R, int num_sms, cudaStream_t s) {
+  transr_prep_mr_kernel<<<dim3(static_cast<unsigned>(R), 8), 256, 0, s>>>(fa.proj, mr_chunks);
+  count_launch();
   TcArgs a{};
+  a.mr_chunks = mr_chunks;
   a.f = fa;
   a.ent_val = ent_val;
   a.seg_start = seg_start;
