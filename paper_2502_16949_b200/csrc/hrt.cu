@@ -33,6 +33,9 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr float kEps = 1e-6f;  // kNormEps for 32-bit reals, common.hpp:34
+#ifndef SKG_BWD_KB
+#define SKG_BWD_KB 4
+#endif
 
 __device__ __forceinline__ float torus_wrap(float x) {  // norms.hpp:96-100
   float d = __fsub_rn(x, rintf(x));
@@ -342,10 +345,13 @@ template <int VEC> struct VecT;
 template <> struct VecT<4> { using T = float4; };
 template <> struct VecT<1> { using T = float; };
 
-// One warp per column segment; two vector chunks per lane per pass.
-template <int KIND, bool SGD, int VEC>
+// One warp per column segment; CH vector chunks per lane per pass (CH = 1
+// covers d <= 128 with float4 lanes). Up to KB residual rows are in flight
+// per round; the adds stay in the segment's entry order.
+template <int KIND, bool SGD, int VEC, int CH>
 __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArgs a) {
   using V = typename VecT<VEC>::T;
+  constexpr int KB = SKG_BWD_KB;
   if (a.err[0] != 0) return;
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -358,13 +364,19 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
     if (a.entity_only && col >= static_cast<uint32_t>(a.N)) continue;
     const uint32_t e0 = a.seg_start[s], e1 = a.seg_start[s + 1];
     V* P = reinterpret_cast<V*>(a.X) + static_cast<size_t>(col) * dv;
-    for (int cb = 0; cb < dv; cb += 64) {
-      const int c0 = cb + lane, c1 = cb + 32 + lane;
-      const bool has0 = c0 < dv, has1 = c1 < dv;
-      V acc0{}, acc1{};
-      if (!SGD) {  // accumulate into an existing sink (score_backward semantics)
-        if (has0) acc0 = P[c0];
-        if (has1) acc1 = P[c1];
+    for (int cb = 0; cb < dv; cb += 32 * CH) {
+      int c[CH];
+      bool has[CH];
+      V acc[CH], p[CH];
+#pragma unroll
+      for (int h = 0; h < CH; ++h) {
+        c[h] = cb + 32 * h + lane;
+        has[h] = c[h] < dv;
+        acc[h] = V{};
+        p[h] = V{};
+        // the owner warp is the only writer of this row: load it up front
+        if (has[h]) p[h] = P[c[h]];
+        if (!SGD) acc[h] = p[h];  // accumulate into an existing sink (score_backward)
       }
       for (uint32_t eb = e0; eb < e1; eb += 32) {
         const int cnt = min(32u, e1 - eb);
@@ -376,46 +388,43 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
         }
         unsigned live = __ballot_sync(kFull, lane < cnt && mysc != 0.f);
         while (live) {
-          int k[4];
+          int k[KB];
           int n = 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < KB; ++q) {
             k[q] = live ? __ffs(live) - 1 : 0;
             if (live) {
               live &= live - 1;
               ++n;
             }
           }
-          uint32_t vq[4];
-          float scq[4];
-          V r0[4], r1[4];
+          uint32_t vq[KB];
+          float scq[KB];
+          V rv[KB][CH];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < KB; ++q) {
             vq[q] = __shfl_sync(kFull, myv, k[q]);
             scq[q] = __shfl_sync(kFull, mysc, k[q]);
             const size_t rowoff = static_cast<size_t>(vq[q] & 0x7fffffffu) * dv;
-            if (q < n) {
-              if (has0) r0[q] = __ldg(RV + rowoff + c0);
-              if (has1) r1[q] = __ldg(RV + rowoff + c1);
-            }
+#pragma unroll
+            for (int h = 0; h < CH; ++h)
+              if (q < n && has[h]) rv[q][h] = __ldg(RV + rowoff + c[h]);
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < KB; ++q)
             if (q < n) {
               const bool neg = (vq[q] >> 31) != 0;
-              if (has0) acc_add<KIND>(acc0, r0[q], scq[q], neg);
-              if (has1) acc_add<KIND>(acc1, r1[q], scq[q], neg);
+#pragma unroll
+              for (int h = 0; h < CH; ++h)
+                if (has[h]) acc_add<KIND>(acc[h], rv[q][h], scq[q], neg);
             }
-          }
         }
       }
-      if (SGD) {
-        const float lr = *a.lr;
-        if (has0) P[c0] = sgd1(P[c0], acc0, lr);
-        if (has1) P[c1] = sgd1(P[c1], acc1, lr);
-      } else {
-        if (has0) P[c0] = acc0;
-        if (has1) P[c1] = acc1;
+#pragma unroll
+      for (int h = 0; h < CH; ++h) {
+        if (!has[h]) continue;
+        if (SGD) P[c[h]] = sgd1(p[h], acc[h], *a.lr);
+        else P[c[h]] = acc[h];
       }
     }
   }
@@ -458,12 +467,23 @@ template <int KIND>
 void launch_bwd_k(bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s) {
   const int grid = num_sms * 8;
   const bool v4 = (a.d % 4) == 0;
+  const bool narrow = v4 ? a.d <= 128 : a.d <= 32;
   if (sgd) {
-    if (v4) segment_backward_kernel<KIND, true, 4><<<grid, kThreads, 0, s>>>(a);
-    else segment_backward_kernel<KIND, true, 1><<<grid, kThreads, 0, s>>>(a);
+    if (v4) {
+      if (narrow) segment_backward_kernel<KIND, true, 4, 1><<<grid, kThreads, 0, s>>>(a);
+      else segment_backward_kernel<KIND, true, 4, 2><<<grid, kThreads, 0, s>>>(a);
+    } else {
+      if (narrow) segment_backward_kernel<KIND, true, 1, 1><<<grid, kThreads, 0, s>>>(a);
+      else segment_backward_kernel<KIND, true, 1, 2><<<grid, kThreads, 0, s>>>(a);
+    }
   } else {
-    if (v4) segment_backward_kernel<KIND, false, 4><<<grid, kThreads, 0, s>>>(a);
-    else segment_backward_kernel<KIND, false, 1><<<grid, kThreads, 0, s>>>(a);
+    if (v4) {
+      if (narrow) segment_backward_kernel<KIND, false, 4, 1><<<grid, kThreads, 0, s>>>(a);
+      else segment_backward_kernel<KIND, false, 4, 2><<<grid, kThreads, 0, s>>>(a);
+    } else {
+      if (narrow) segment_backward_kernel<KIND, false, 1, 1><<<grid, kThreads, 0, s>>>(a);
+      else segment_backward_kernel<KIND, false, 1, 2><<<grid, kThreads, 0, s>>>(a);
+    }
   }
   count_launch();
   SKG_LAUNCH_CHECK();

@@ -21,7 +21,8 @@ KINDS = {1: "ShapeError", 2: "ConfigError", 3: "DegenerateTripleError", 4: "Trai
 
 
 def lib_path() -> str:
-    return os.path.join(HERE, "libskge_b200.so")
+    # SKGE_B200_LIB points at an alternative build of the same engine (A/B experiments)
+    return os.environ.get("SKGE_B200_LIB") or os.path.join(HERE, "libskge_b200.so")
 
 
 class EngineError(RuntimeError):
