@@ -288,6 +288,8 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
       if (Sb > 0) {
         FwdArgs fa = base_fwd(ctx);
         fa.order = ps.order_g.p + b * es.S;
+        fa.pair_ht = ps.plan.pair_ht + b * es.S;
+        fa.pair_r = ps.plan.pair_r + b * es.S;
         fa.H = ctx->H.p;
         fa.Rl = ctx->Rl.p;
         fa.T = ctx->T.p;
@@ -328,6 +330,8 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
     }
     FwdArgs fa = base_fwd(ctx);
     fa.order = ps.order.p + lo;
+    fa.pair_ht = ps.plan.pair_ht + lo;
+    fa.pair_r = ps.plan.pair_r + lo;
     fa.H = ctx->H.p;
     fa.Rl = ctx->Rl.p;
     fa.T = ctx->T.p;

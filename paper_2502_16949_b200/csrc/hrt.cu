@@ -128,8 +128,11 @@ __device__ __forceinline__ float row_scale(float up, float s) {
   return up;                                                                     // L1 sign weight
 }
 
+#ifndef SKG_FWD_MINB
+#define SKG_FWD_MINB 2
+#endif
 template <int KIND, bool TRAIN, int VEC>
-__global__ void __launch_bounds__(kThreads) hrt_forward_kernel(const FwdArgs a) {
+__global__ void __launch_bounds__(kThreads, SKG_FWD_MINB) hrt_forward_kernel(const FwdArgs a) {
   extern __shared__ float4 smem4[];
   __shared__ float warp_loss[kWarps];
   if (a.err[0] != 0) return;  // sticky error: nothing runs after the failing batch
@@ -155,10 +158,17 @@ __global__ void __launch_bounds__(kThreads) hrt_forward_kernel(const FwdArgs a) 
         const bool neg = lane >= 8;
         valid = p < a.B;
         if (valid) {
-          const int id = a.order[p];
-          h = neg ? a.NH[id] : a.H[id];
-          t = neg ? a.NT[id] : a.T[id];
-          r = a.Rl[id];
+          if (a.pair_ht) {  // epoch-plan record of this position: one load, no order -> id chase
+            const int4 q = __ldg(a.pair_ht + p);
+            h = neg ? q.z : q.x;
+            t = neg ? q.w : q.y;
+            r = __ldg(a.pair_r + p);
+          } else {
+            const int id = a.order[p];
+            h = neg ? a.NH[id] : a.H[id];
+            t = neg ? a.NT[id] : a.T[id];
+            r = a.Rl[id];
+          }
           row2 = neg ? a.B + p : p;
         }
       } else {

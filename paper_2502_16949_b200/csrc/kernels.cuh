@@ -38,6 +38,8 @@ struct FwdArgs {
   // rows. TRAIN: pairs p in [0, B) via order[p] -> (H,R,T) / (NH,R,NT);
   //       SCORE: rows i in [0, B) straight from (H,R,T).
   const int32_t* order;
+  const int4* pair_ht;     // TRAIN: per pair {h, t, neg h, neg t} (epoch plan), may be null
+  const int32_t* pair_r;
   const int32_t *H, *Rl, *T, *NH, *NT;
   int B;
   float margin, unit;

@@ -34,7 +34,8 @@ __global__ void gen_train_entries_kernel(const int32_t* __restrict__ order, cons
                                          const int32_t* __restrict__ NH, const int32_t* __restrict__ NT,
                                          int64_t M, int64_t B, int64_t N, int64_t Rn, int cb,
                                          uint32_t invalid, uint32_t* __restrict__ key,
-                                         uint32_t* __restrict__ val) {
+                                         uint32_t* __restrict__ val, int4* __restrict__ pair_ht,
+                                         int32_t* __restrict__ pair_r) {
   for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < 2 * M;
        x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t k = x >> 1;
@@ -45,6 +46,10 @@ __global__ void gen_train_entries_kernel(const int32_t* __restrict__ order, cons
     const int32_t h = p ? NH[id] : H[id];
     const int32_t t = p ? NT[id] : T[id];
     const int64_t base = 6 * b * B + 3 * (p * Bb + i);
+    if (p == 0) {
+      pair_ht[k] = make_int4(h, t, NH[id], NT[id]);
+      pair_r[k] = R[id];
+    }
     emit_row(key, val, base, static_cast<uint32_t>(b) << cb, h, t, R[id],
              static_cast<uint32_t>(p * Bb + i), N, Rn, invalid, true);
   }
@@ -129,6 +134,13 @@ void EpochPlan::reserve(int64_t entries, int64_t batches) {
     scan.reserve(entries);
     cap_entries = entries;
   }
+  if (entries / 6 + 1 > cap_pairs) {
+    if (pair_ht) cudaFree(pair_ht);
+    if (pair_r) cudaFree(pair_r);
+    cap_pairs = entries / 6 + 1;
+    SKG_CUDA(cudaMalloc(&pair_ht, sizeof(int4) * cap_pairs));
+    SKG_CUDA(cudaMalloc(&pair_r, sizeof(int32_t) * cap_pairs));
+  }
   if (batches > cap_batches) {
     if (seg_base) cudaFree(seg_base);
     SKG_CUDA(cudaMalloc(&seg_base, sizeof(uint32_t) * (batches + 1)));
@@ -141,7 +153,11 @@ void EpochPlan::release() {
     if (*b) cudaFree(*b);
     *b = nullptr;
   }
-  cap_entries = cap_batches = 0;
+  if (pair_ht) cudaFree(pair_ht);
+  if (pair_r) cudaFree(pair_r);
+  pair_ht = nullptr;
+  pair_r = nullptr;
+  cap_entries = cap_batches = cap_pairs = 0;
   sort.release();
   scan.release();
 }
@@ -157,7 +173,7 @@ void build_epoch_plan(const int32_t* order, const int32_t* H, const int32_t* R, 
   p.reserve(p.E, p.nb);
   const uint32_t invalid = 1u << (p.kb + p.cb);
   gen_train_entries_kernel<<<grid_for(2 * M), 256, 0, s>>>(order, H, R, T, NH, NT, M, B, N, Rn, p.cb,
-                                                           invalid, p.key, p.val);
+                                                           invalid, p.key, p.val, p.pair_ht, p.pair_r);
   count_launch();
   SKG_LAUNCH_CHECK();
   finish_plan(p, invalid, N, Rn, s);

@@ -31,6 +31,11 @@ struct EpochPlan {
   uint32_t* seg_base = nullptr;   // [nb + 1]
   uint32_t* nseg = nullptr;       // [1]
   const uint32_t* sorted_val = nullptr;
+  // per epoch position k: {h, t, neg h, neg t} and r of triple order[k], so the
+  // forward reads one record per pair instead of chasing order -> ids
+  int4* pair_ht = nullptr;
+  int32_t* pair_r = nullptr;
+  int64_t cap_pairs = 0;
   SortPlan sort;
   ScanPlan scan;
   void reserve(int64_t entries, int64_t batches);
