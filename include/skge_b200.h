@@ -195,6 +195,11 @@ skg_status skg_debug_tc_gemm(skg_ctx* ctx, int32_t mode, const float* A, const f
  * applies the identical update (replicated tables). */
 skg_status skg_nccl_unique_id(char out[128]);
 skg_status skg_dp_init(skg_ctx* ctx, const char unique_id[128], int rank, int world);
+/* Host-only: the shard rank `rank` of `world` trains in every global minibatch
+ * (training.cpp:120-121 batches of batch_size): out = {pairs per full
+ * minibatch, first pair of the last minibatch's shard, its size, pairs over
+ * the epoch, minibatches}. */
+skg_status skg_dp_shard(int64_t m, int64_t batch_size, int32_t world, int32_t rank, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -174,6 +174,24 @@ uint64_t epoch_seed(uint64_t seed, int64_t epoch) {  // training.cpp:109-110
 
 // ----------------------------------------------------------------- epoch body
 
+// Data-parallel shard of rank `rank` in every global minibatch of B pairs
+// (last minibatch Bl = M - (nb-1) B): full minibatches give each rank B/world
+// contiguous pairs, the last one ceil(Bl/world) (the tail ranks may get fewer
+// or none). out = {S, i0_last, s_last, Mg, nb}.
+void dp_shard(int64_t M, int64_t B, int world, int rank, int64_t* out) {
+  const int64_t nb = (M + B - 1) / B;
+  const int64_t S = B / world;
+  const int64_t Bl = M - (nb - 1) * B;
+  const int64_t Sl = (Bl + world - 1) / world;
+  const int64_t i0 = std::min<int64_t>(rank * Sl, Bl);
+  const int64_t sl = std::min<int64_t>(i0 + Sl, Bl) - i0;
+  out[0] = S;
+  out[1] = i0;
+  out[2] = sl;
+  out[3] = (nb - 1) * S + sl;
+  out[4] = nb;
+}
+
 struct EpochShape {
   int64_t B, nb;
   bool shuffle;
@@ -385,12 +403,12 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   if (ctx->dp) {
     if (is_ht(cfg)) throw ConfigError("data-parallel training supports TransE / TorusE in this build");
     if (es.B % es.world != 0) throw ConfigError("data parallel: global batch_size must be a multiple of the world size");
-    es.S = es.B / es.world;
-    const int64_t Bl = ctx->M - (es.nb - 1) * es.B;
-    const int64_t Sl = (Bl + es.world - 1) / es.world;
-    es.i0_last = std::min<int64_t>(es.rank * Sl, Bl);
-    es.s_last = std::min<int64_t>(es.i0_last + Sl, Bl) - es.i0_last;
-    es.Mg = (es.nb - 1) * es.S + es.s_last;
+    int64_t sh[5];
+    dp_shard(ctx->M, es.B, es.world, es.rank, sh);
+    es.S = sh[0];
+    es.i0_last = sh[1];
+    es.s_last = sh[2];
+    es.Mg = sh[3];
     for (auto& sl : ctx->slots) sl.order_g.ensure(es.Mg + 1);
     ctx->dp_grad.ensure((ctx->N + ctx->R) * ctx->de + 2);
   }
@@ -1233,6 +1251,13 @@ skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_co
 }
 
 }  // extern "C"
+
+extern "C" skg_status skg_dp_shard(int64_t m, int64_t batch_size, int32_t world, int32_t rank, int64_t* out) {
+  if (m < 1 || batch_size < 1 || world < 1 || rank < 0 || rank >= world || batch_size % world != 0)
+    return SKG_ERR_CONFIG;
+  dp_shard(m, std::min(batch_size, m), world, rank, out);
+  return SKG_OK;
+}
 
 extern "C" skg_status skg_debug_tc_gemm(skg_ctx* ctx, int32_t mode, const float* A, const float* B, float* D) {
   return guard(ctx, [&] {

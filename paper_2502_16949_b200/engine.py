@@ -105,6 +105,7 @@ def load_library():
         "skg_flush_l2": [vp],
         "skg_plan_stats": [vp, i64, vp, vp, vp],
         "skg_debug_tc_gemm": [vp, i32, vp, vp, vp],
+        "skg_dp_shard": [i64, i64, i32, i32, vp],
     }
     L.skg_host_last_error.restype = C.c_char_p
     for name, args in sig.items():
@@ -297,6 +298,16 @@ class Engine:
         s, e, r = C.c_int64(), C.c_int64(), C.c_int64()
         self._check(self.L.skg_plan_stats(self.h, batch, C.byref(s), C.byref(e), C.byref(r)))
         return s.value, e.value, r.value
+
+
+def dp_shard(m: int, batch_size: int, world: int, rank: int):
+    """Host-only shard geometry of the data-parallel engine (no GPU needed)."""
+    L = load_library()
+    out = np.zeros(5, np.int64)
+    rc = L.skg_dp_shard(m, batch_size, world, rank, _p(out))
+    if rc != 0:
+        raise EngineError(rc, "dp_shard: bad arguments")
+    return dict(S=int(out[0]), i0_last=int(out[1]), s_last=int(out[2]), Mg=int(out[3]), nb=int(out[4]))
 
 
 def _host_check(L, rc):
