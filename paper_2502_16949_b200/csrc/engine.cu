@@ -561,6 +561,7 @@ void negative_sample_impl(skg_ctx* ctx, uint64_t seed, bool avoid) {  // trainin
     throw CudaError("negative_sample: device RNG window exhausted");
   ctx->has_neg = true;
   ++ctx->data_version;
+  ctx->neg_valid_version = ctx->data_version;
 }
 
 // ------------------------------------------------------ per-op kernels (small)
@@ -661,13 +662,18 @@ int grid_for(int64_t n) {
 }
 
 __global__ void narrow_ids_kernel(const int64_t* __restrict__ src, int64_t m, int64_t limit,
-                                  int32_t* __restrict__ dst, uint32_t* __restrict__ first_bad) {
+                                  int32_t* __restrict__ dst, uint32_t* __restrict__ first_bad,
+                                  uint32_t* __restrict__ changed) {
+  bool diff = false;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t v = src[i];
     if (v < 0 || v >= limit) atomicMin(first_bad, static_cast<uint32_t>(i));
-    dst[i] = static_cast<int32_t>(v);
+    const int32_t w = static_cast<int32_t>(v);
+    diff |= dst[i] != w;
+    dst[i] = w;
   }
+  if (diff) *changed = 0;
 }
 
 }  // namespace
@@ -807,17 +813,30 @@ void upload_narrow(skg_ctx* ctx, const int64_t* const* srcs, int32_t* const* dst
   ctx->bad_idx.ensure(3);
   SKG_CUDA(cudaMemsetAsync(ctx->bad_idx.p, 0xFF, sizeof(uint32_t) * 3, ctx->stream));
   for (int k = 0; k < count; ++k) {
-    SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, srcs[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice,
-                             ctx->stream));
-    narrow_ids_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->stage_i64.p + k * m, m, limits[k], dsts[k],
-                                                            ctx->bad_idx.p + slots[k]);
+    // Pinned (page-locked, UVA-mapped) caller arrays are read by the narrowing
+    // kernel straight over PCIe: copy, validation and narrowing in one pass.
+    // Pageable arrays are staged with a plain H2D copy first.
+    const int64_t* src = nullptr;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, srcs[k]) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      src = static_cast<const int64_t*>(pa.devicePointer);
+    else
+      cudaGetLastError();
+    if (!src) {
+      SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, srcs[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice,
+                               ctx->stream));
+      src = ctx->stage_i64.p + k * m;
+    }
+    narrow_ids_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(src, m, limits[k], dsts[k], ctx->bad_idx.p + slots[k],
+                                                            ctx->bad_idx.p + 2);
     count_launch();
   }
   SKG_LAUNCH_CHECK();
-  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->bad_idx.p, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->bad_idx.p, sizeof(uint32_t) * 3, cudaMemcpyDeviceToHost, ctx->stream));
   SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   bad_out[0] = ctx->h_err[0];
   bad_out[1] = ctx->h_err[1];
+  bad_out[2] = ctx->h_err[2];
 }
 
 skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, const int64_t* t,
@@ -825,6 +844,11 @@ skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int6
   return guard(ctx, [&] {
     if (m > 0 && (!h || !r || !t)) throw ShapeError("triple batch: heads/relations/tails length mismatch");
     if (n_ent > INT32_MAX || n_rel > INT32_MAX || m > INT32_MAX) throw ShapeError("id space exceeds 32-bit device ids");
+    // Re-uploading identical triples keeps data_version, so an epoch plan
+    // prefetched inside the previous epoch's graph stays valid.
+    bool same = ctx->triples_valid && m == ctx->M && n_ent == ctx->tN && n_rel == ctx->tR && ctx->H.n >= m + 1 &&
+                ctx->Rl.n >= m + 1 && ctx->T.n >= m + 1;
+    ctx->triples_valid = false;
     ctx->M = 0;
     ctx->has_neg = false;
     ctx->tN = n_ent;
@@ -837,20 +861,26 @@ skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int6
       int32_t* dsts[3] = {ctx->H.p, ctx->Rl.p, ctx->T.p};
       const int64_t lim[3] = {n_ent, n_rel, n_ent};
       const int slots[3] = {0, 1, 0};
-      uint32_t bad[2];
+      uint32_t bad[3];
       upload_narrow(ctx, srcs, dsts, lim, slots, 3, m, bad);
+      same = same && bad[2] == 0xFFFFFFFFu;
+      if (!same) ++ctx->data_version;
       if (bad[0] != 0xFFFFFFFFu && bad[0] <= bad[1])  // incidence.hpp:26-29: entity check first
         throw ShapeError("triple " + std::to_string(bad[0]) + ": entity id out of range");
       if (bad[1] != 0xFFFFFFFFu) throw ShapeError("triple " + std::to_string(bad[1]) + ": relation id out of range");
+    } else if (!same) {
+      ++ctx->data_version;
     }
     ctx->M = m;
-    ++ctx->data_version;
+    ctx->triples_valid = true;
   });
 }
 
 skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
   return guard(ctx, [&] {
     if (m != ctx->M) throw ShapeError("negative set is not aligned with the positive triples");
+    // negatives as they were when the triples were set: no new data_version for an identical re-upload
+    bool same = ctx->neg_valid_version == ctx->data_version && ctx->NH.n >= m + 1 && ctx->NT.n >= m + 1;
     ctx->has_neg = false;
     ctx->NH.ensure(m + 1);
     ctx->NT.ensure(m + 1);
@@ -859,12 +889,19 @@ skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const i
       int32_t* dsts[2] = {ctx->NH.p, ctx->NT.p};
       const int64_t lim[2] = {ctx->tN, ctx->tN};
       const int slots[2] = {0, 0};
-      uint32_t bad[2];
+      uint32_t bad[3];
       upload_narrow(ctx, srcs, dsts, lim, slots, 2, m, bad);
-      if (bad[0] != 0xFFFFFFFFu) throw ShapeError("triple " + std::to_string(bad[0]) + ": entity id out of range");
+      same = same && bad[2] == 0xFFFFFFFFu;
+      if (!same) ++ctx->data_version;
+      if (bad[0] != 0xFFFFFFFFu) {
+        ctx->neg_valid_version = ~0ull;
+        throw ShapeError("triple " + std::to_string(bad[0]) + ": entity id out of range");
+      }
+    } else if (!same) {
+      ++ctx->data_version;
     }
     ctx->has_neg = true;
-    ++ctx->data_version;
+    ctx->neg_valid_version = ctx->data_version;
   });
 }
 

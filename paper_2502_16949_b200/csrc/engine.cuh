@@ -101,6 +101,8 @@ struct skg_ctx {
   int cur = 0;        // slot holding (or to hold) the plan of the next epoch to train
   int last_slot = 0;  // slot the last trained epoch used (plan_stats)
   uint64_t data_version = 0;
+  bool triples_valid = false;              // H/Rl/T hold the last successful set_triples
+  uint64_t neg_valid_version = ~0ull;      // data_version at which NH/NT were last set (or sampled)
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaGraphExec_t graph = nullptr;  // legacy handle (unused)

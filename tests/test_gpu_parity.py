@@ -310,3 +310,60 @@ def test_cpp_shim_drop_in_runs():
                         "-lskge_b200", f"-Wl,-rpath,{lib}"], check=True)
         out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
         assert out.returncode == 0, out.stdout + out.stderr
+
+
+def _pinned(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, np.int64)).pin_memory().numpy()
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_reupload_between_epochs_keeps_parity(eng, orc32, pinned):
+    """The e2e loop re-uploads the same triples/negatives every epoch (identical
+    content keeps the prefetched epoch plan); a changed upload must rebuild it.
+    Pinned caller arrays take the zero-copy narrowing path."""
+    n, r, d, m = 400, 7, 16, 900
+    h, rel, t = orc32.synthetic_train(n, r, m, 9)
+    if pinned:
+        h, rel, t = _pinned(h), _pinned(rel), _pinned(t)
+    st = orc32.init_store("transe", n, r, d, d, 9)
+    cfg = ModelConfig.make("transe", d, d, "l2")
+    tc_e = TrainConfig.make(batch_size=128, seed=5, lr=0.05)
+    tc_o = orc32.train_config(batch_size=128, seed=5, lr=0.05)
+    nh, nt = orc32.negative_sample(h, rel, t, n, r, 3)
+    rng = np.random.default_rng(1)
+    nh2, nt2 = rng.integers(0, n, len(h)), rng.integers(0, n, len(h))
+    if pinned:
+        nh, nt, nh2, nt2 = _pinned(nh), _pinned(nt), _pinned(nh2), _pinned(nt2)
+    eng.store_upload(cfg, st.entity, st.relation)
+    plan = [(nh, nt), (nh, nt), (nh2, nt2), (nh2, nt2), (nh, nt)]
+    for ep, (a, b) in enumerate(plan):
+        eng.set_triples(h, rel, t, n, r)
+        eng.set_negatives(a, b)
+        re = eng.train_epoch(cfg, tc_e, ep, 0.05)
+        ro = orc32.train_epoch("transe", st, (h, rel, t), (a, b), tc_o, ep, 0.05)
+        assert abs(re.loss - ro.loss) <= TOL * max(1.0, abs(ro.loss))
+        ge, gr, _, _ = eng.store_download()
+        assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation), ep
+    # a changed positive set (same size) with the old negatives
+    h3 = (h + 1) % n
+    eng.set_triples(h3, rel, t, n, r)
+    eng.set_negatives(nh, nt)
+    eng.train_epoch(cfg, tc_e, 5, 0.05)
+    orc32.train_epoch("transe", st, (h3, rel, t), (nh, nt), tc_o, 5, 0.05)
+    ge, gr, _, _ = eng.store_download()
+    assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation)
+
+
+def test_pinned_upload_rejects_bad_ids(eng):
+    h = _pinned(np.array([0, 1, 2, 3]))
+    r = _pinned(np.array([0, 0, 1, 0]))
+    t = _pinned(np.array([1, 2, 9, 0]))
+    with pytest.raises(EngineError) as e:
+        eng.set_triples(h, r, t, 5, 2)
+    assert e.value.kind == "ShapeError" and "triple 2: entity id out of range" in e.value.msg
+    r[1] = 7
+    t[2] = 3
+    with pytest.raises(EngineError) as e:
+        eng.set_triples(h, r, t, 5, 2)
+    assert "triple 1: relation id out of range" in e.value.msg

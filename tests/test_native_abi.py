@@ -51,3 +51,15 @@ def test_cpp_shim_compiles():
         subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", out,
                         "-L", os.path.join(ROOT, "paper_2502_16949_b200"), "-lskge_b200",
                         f"-Wl,-rpath,{os.path.join(ROOT, 'paper_2502_16949_b200')}"], check=True)
+
+
+def test_torch_imports_after_engine_library():
+    """libskge_b200.so links the libnccl.so.2 PyTorch ships, so loading the
+    engine first must not break a later `import torch` (shared soname)."""
+    import subprocess
+    import sys
+    from paper_2502_16949_b200.engine import lib_path
+    code = ("import ctypes, sys; ctypes.CDLL(sys.argv[1]); import torch; "
+            "print(torch.cuda.nccl.version() if hasattr(torch.cuda, 'nccl') else 'no-nccl')")
+    out = subprocess.run([sys.executable, "-c", code, lib_path()], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
