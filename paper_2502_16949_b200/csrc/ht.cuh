@@ -51,6 +51,13 @@ void launch_transr_tc_apply(const uint32_t* tile_total, const uint32_t* seg_tile
                             float* proj, float* rel, const float* lr, bool sgd, const uint32_t* err, int64_t R,
                             cudaStream_t s);
 void transr_tc_selftest(int mode, const float* A, const float* B, float* D, cudaStream_t s);
+// Warp-specialized training step (transr_train_tc.cu)
+void configure_transr_train_tc_kernels();
+int64_t transr_train_tc_mr_floats(int64_t R);
+void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,
+                            const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
+                            const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,
+                            float* mr, int64_t R, int num_sms, cudaStream_t s);
 
 // data parallel (dp.cu)
 void dp_destroy(skg_ctx* ctx);

@@ -51,31 +51,78 @@ struct TrArgs {
 };
 
 // One CTA enumerates the batch's relation segments into tiles; seg_tiles[k]
-// is the first tile of the k-th relation segment ([nrel] = total).
-__global__ void transr_tiles_kernel(const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ seg_col,
-                                    const uint32_t* __restrict__ seg_base, int batch, int64_t N, int paired,
-                                    uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_p0,
-                                    uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles,
-                                    const uint32_t* __restrict__ err) {
-  if (threadIdx.x != 0) return;
+// is the first tile of the k-th relation segment ([nrel] = total). Relation
+// segments lead the batch's segment list (relation column keys sort first).
+// Thread per segment, block scan of the tile counts, then every thread
+// writes its own segment's tiles.
+constexpr int kTilesThreads = 1024;
+__global__ void __launch_bounds__(kTilesThreads) transr_tiles_kernel(
+    const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ seg_col, const uint32_t* __restrict__ seg_base,
+    int batch, int64_t N, int paired, uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_p0,
+    uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles, const uint32_t* __restrict__ err) {
+  __shared__ uint32_t wsum[kTilesThreads / 32];
+  __shared__ uint32_t carry_t, nrel;
+  __shared__ int stop;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t s0 = seg_base[batch], s1 = seg_base[batch + 1];
-  uint32_t t = 0, k = 0;
-  if (err[0] == 0) {
-    for (uint32_t s = s0; s < s1 && seg_col[s] >= static_cast<uint32_t>(N); ++s, ++k) {
-      seg_tiles[k] = t;
+  const uint32_t per = paired ? kTilePairs : kTileRows;
+  if (tid == 0) {
+    carry_t = 0;
+    nrel = 0;
+    stop = err[0] != 0;
+  }
+  __syncthreads();
+  for (uint32_t base = s0; base < s1 && !stop; base += kTilesThreads) {
+    const uint32_t s = base + tid;
+    const bool rel = s < s1 && seg_col[s] >= static_cast<uint32_t>(N);
+    uint32_t n = 0, units = 0;
+    if (rel) {
       const uint32_t len = seg_start[s + 1] - seg_start[s];
-      const uint32_t units = paired ? len / 2 : len;
-      const uint32_t per = paired ? kTilePairs : kTileRows;
-      for (uint32_t p = 0; p < units; p += per) {
-        tile_seg[t] = s;
-        tile_p0[t] = p;
-        ++t;
+      units = paired ? len / 2 : len;
+      n = (units + per - 1) / per;
+    }
+    // relation segments are a prefix: count them in this chunk
+    const int nr = __syncthreads_count(rel);
+    uint32_t x = n;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t v = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    const uint32_t first = carry_t + (w > 0 ? wsum[w - 1] : 0u) + x - n;
+    if (rel) {
+      const uint32_t k = nrel + tid;
+      seg_tiles[k] = first;
+      for (uint32_t q = 0; q < n; ++q) {
+        tile_seg[first + q] = s;
+        tile_p0[first + q] = q * per;
       }
     }
+    __syncthreads();
+    if (tid == 0) {
+      carry_t += wsum[kTilesThreads / 32 - 1];
+      nrel += static_cast<uint32_t>(nr);
+      if (nr < kTilesThreads) stop = 1;
+    }
+    __syncthreads();
   }
-  seg_tiles[k] = t;
-  tile_total[0] = t;
-  tile_total[1] = k;
+  if (tid == 0) {
+    seg_tiles[nrel] = carry_t;
+    tile_total[0] = carry_t;
+    tile_total[1] = nrel;
+  }
 }
 
 template <bool L2, int MODE>
@@ -408,7 +455,7 @@ void run_tiles(int kind, bool train, const FwdArgs& fa, const BwdArgs& ba, const
                int64_t rows, int64_t R, cudaStream_t s) {
   if (fa.de > 128 || fa.dr > 128 || tile_smem(fa.de, fa.dr) > 220 * 1024)
     throw CudaError("transr: dimensions above 128 are not supported by the projection tile");
-  transr_tiles_kernel<<<1, 32, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, train ? 1 : 0, w.tile_seg,
+  transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, train ? 1 : 0, w.tile_seg,
                                        w.tile_p0, w.tile_total, w.seg_tiles, ba.err);
   count_launch();
   TrArgs a{};
@@ -454,7 +501,7 @@ int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
   const int64_t parts = std::max<int64_t>(mt, transr_tc_slots(256, R));  // tc path: (CTA, relation) runs
   return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + parts * dr * de + ((parts * dr + 31) / 32) * 32 +
-         transr_tc_mr_floats(R) + 64;
+         std::max(transr_tc_mr_floats(R), transr_train_tc_mr_floats(R)) + 64;
 }
 
 void configure_transr_kernels() {
@@ -463,13 +510,14 @@ void configure_transr_kernels() {
   configure_one<false, kTrain>();
   configure_one<false, kRows>();
   configure_transr_tc_kernels();
+  configure_transr_train_tc_kernels();
 }
 
 namespace {
 // tcgen05 path (d_e = d_r = 128): tile list, persistent projection CTAs.
 void run_tc(int kind, int mode, const FwdArgs& fa, const BwdArgs& ba, const Work& w, int num_sms, cudaStream_t s,
             int64_t R) {
-  transr_tiles_kernel<<<1, 32, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, mode == 0 ? 1 : 0,
+  transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, mode == 0 ? 1 : 0,
                                        w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err);
   count_launch();
   SKG_LAUNCH_CHECK();
@@ -482,7 +530,12 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
                         const std::function<void()>* mark, int64_t R) {
   const Work w = carve(work, 2 * static_cast<int64_t>(fa.B), fa.de, fa.dr, R);
   if (transr_tc_supported(fa.de, fa.dr)) {
-    run_tc(kind, 0, fa, ba, w, num_sms, s, R);
+    transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, 1,
+                                                    w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+    launch_transr_train_tc(kind == kTransR_L2, fa, ba.ent_val, ba.seg_start, ba.seg_col, w.tile_seg, w.tile_p0,
+                           w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, w.mr_chunks, R, num_sms, s);
     if (mark) (*mark)();
     BwdArgs eb = ba;
     eb.entity_only = 1;

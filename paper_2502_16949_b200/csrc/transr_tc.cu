@@ -502,17 +502,27 @@ __global__ void transr_tc_apply_kernel(const uint32_t* __restrict__ tile_total, 
   if (hi <= lo) return;
   const int64_t r = static_cast<int64_t>(seg_col[tile_seg[lo]]) - N;
   const float step = *lr;
+  // CTAs whose tile range [T j / G, T (j+1) / G) meets [lo, hi): a contiguous
+  // j interval (ranges are monotone); empty ranges own no slot.
+  __shared__ unsigned char own[1024];
   __shared__ int jl[1024];
   __shared__ int nj;
-  if (threadIdx.x == 0) {
+  for (int j = threadIdx.x; j < G && j < 1024; j += blockDim.x) {
+    const uint32_t a0 = static_cast<uint32_t>((static_cast<uint64_t>(T) * j) / G);
+    const uint32_t a1 = static_cast<uint32_t>((static_cast<uint64_t>(T) * (j + 1)) / G);
+    own[j] = (a0 < a1 && a1 > lo && a0 < hi) ? 1 : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // ordered compaction, one warp
     int c = 0;
-    for (int j = 0; j < G && c < 1024; ++j) {
-      const uint32_t a0 = static_cast<uint32_t>((static_cast<uint64_t>(T) * j) / G);
-      const uint32_t a1 = static_cast<uint32_t>((static_cast<uint64_t>(T) * (j + 1)) / G);
-      if (a0 >= a1 || a1 <= lo || a0 >= hi) continue;  // empty CTA ranges own no slot
-      jl[c++] = j;
+    for (int j0 = 0; j0 < G && j0 < 1024; j0 += 32) {
+      const int j = j0 + static_cast<int>(threadIdx.x);
+      const bool o = j < G && j < 1024 && own[j];
+      const unsigned m = __ballot_sync(kFull, o);
+      if (o) jl[c + __popc(m & lanemask_lt())] = j;
+      c += __popc(m);
     }
-    nj = c;
+    if (threadIdx.x == 0) nj = c;
   }
   __syncthreads();
   for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < kD * kD + kD; i += gridDim.y * blockDim.x) {

@@ -1,0 +1,649 @@
+// TransR training step on tcgen05, warp-specialized (sm_100a), d_e = d_r = 128.
+//
+// Per tile of 64 (pos, neg) pairs = 128 rows of one relation r
+// (models.cpp:110-156, models.hpp:82-96):
+//   U  = h - t                        gathered by the producer warps
+//   V  = U M_r^T          (GEMM1)     V_row + r -> reference-order score, hinge
+//   DZ = dir(V + r) * up              epilogue warps
+//   dM += DZ^T U          (GEMM3)     accumulated in TMEM over the relation run
+//   dU  = DZ M_r          (GEMM2)     -> res_u rows for the entity segments
+// All three products are 3xTF32 (hi*hi + hi*lo + lo*hi, fp32-class). The
+// tensor core truncates a raw fp32 operand to tf32, so raw U / DZ in shared
+// memory are the "hi" A operands and only the "lo" parts are materialised
+// (in TMEM, as A operands of the third product). M_r arrives pre-split (hi =
+// rna, lo = rest) in 16-wide K chunks through a 3-slot bulk-copy ring; GEMM3
+// contracts over rows, so DZ^T / U^T are staged 8 rows at a time.
+//
+// Roles (320 threads):
+//   warps 0-3  epilogue   thread = row = TMEM lane: score, hinge, DZ, sum(dz),
+//                         dM flush per relation run, dU drain to HBM
+//   warps 4-7  producer   row-id chase, U gather, U lo -> TMEM, G3 staging
+//   warp  8    MMA issue  (whole warp, elect.sync inside the asm)
+//   warp  9    ring loader (bulk copies of M_r chunks)
+// TMEM columns: [0,128) V | [128,256) U lo, then DZ lo | [256,384) dU | [384,512) dM.
+//
+// The CTA-range / relation-run partition (slot = CTA + run ordinal) is the one
+// transr_tc_apply_kernel (transr_tc.cu) reduces in tile order.
+#include "common.cuh"
+#include "ht.cuh"
+#include "primitives.cuh"
+#include "refmath.cuh"
+#include "tc.cuh"
+
+namespace skg {
+
+namespace {
+
+constexpr int kD = 128;
+constexpr int kRows = 128;
+constexpr int kPairs = 64;
+constexpr int kThreads = 320;
+constexpr int kMmaWarp = 8, kLoadWarp = 9;
+
+// sU / sDZ: canonical no-swizzle K-major (m = row, k = feature);
+// 16-byte unit (r, c4) = (r & 7) + (r >> 3) * 256 + c4 * 8.
+__device__ __forceinline__ int tile_unit(int r, int c4) { return (r & 7) + (r >> 3) * 256 + c4 * 8; }
+constexpr uint32_t kTileLBO = 8 * 16, kTileSBO = 256 * 16;
+
+// Ring chunk of M_r: 128 (n) x 16 (k), hi then lo; unit (n, k4) = (n & 7) + (n >> 3) * 32 + k4 * 8.
+constexpr int kChunkK = 16;
+constexpr int kChunkFloats = kD * kChunkK;
+constexpr uint32_t kChunkBytes = 2 * kChunkFloats * sizeof(float);
+constexpr uint32_t kChLBO = 8 * 16, kChSBO = 32 * 16;
+constexpr int kChunksPerGemm = kD / kChunkK;
+constexpr int64_t kMrFloatsPerRel = 2LL * kChunksPerGemm * 2 * kChunkFloats;
+constexpr int kRing = 3;
+
+// GEMM3 staging slot: 8 rows (K) of DZ^T and U^T, hi and lo; arrays [128][8]
+// with unit (i, k4) = (i & 7) + (i >> 3) * 18 + k4 * 9 (padded: the producers'
+// transposing stores hit 32 distinct banks).
+constexpr int kG3Rows = 8;
+constexpr int kG3Units = 16 * 18;
+constexpr int kG3ArrFloats = kG3Units * 4;
+constexpr uint32_t kG3LBO = 9 * 16, kG3SBO = 18 * 16;
+constexpr int kG3Slots = 2;
+constexpr int kG3PerTile = kRows / kG3Rows;
+__device__ __forceinline__ int g3_off(int i, int k) { return (((i & 7) + (i >> 3) * 18 + (k >> 2) * 9) << 2) + (k & 3); }
+
+constexpr uint32_t kColV = 0, kColLo = 128, kColDU = 256, kColDM = 384;
+
+struct Smem {
+  float U[kRows * kD];
+  float DZ[kRows * kD];
+  float ring[kRing][2 * kChunkFloats];
+  float g3[kG3Slots][4][kG3ArrFloats];  // DZ^T hi, DZ^T lo, U^T hi, U^T lo
+  int rrow[2][kRows];                   // incidence row of each tile row (-1: padding)
+  float rel[2][kD];
+  int np[2];
+  int sh_h[kRows], sh_t[kRows];
+  float rs[kRows];
+  float colsum[4][kD];
+  float tl[2];
+  uint64_t u_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty;
+  uint64_t g3_full[kG3Slots], g3_empty[kG3Slots];
+  uint64_t ring_full[kRing], ring_empty[kRing];
+  uint32_t tmem_base;
+  int last;
+};
+
+struct Args {
+  FwdArgs f;
+  const uint32_t* ent_val;
+  const uint32_t* seg_start;
+  const uint32_t* seg_col;
+  const uint32_t* tile_seg;
+  const uint32_t* tile_p0;
+  const uint32_t* tile_total;  // [0] tiles, [1] relation segments
+  const uint32_t* seg_tiles;
+  float* dm_part;
+  float* dr_part;
+  const float* mr;  // per relation: [layout][chunk][hi, lo][128 x 16]
+};
+
+__device__ __forceinline__ uint32_t idesc128() { return tc::make_idesc_tf32(128, 128, 0, 0); }
+
+// Relation-segment ordinal of tile t (tiles of a segment are contiguous).
+__device__ __forceinline__ int run_of(const Args& a, uint32_t t) {
+  uint32_t lo = 0, hi = a.tile_total[1];
+  while (lo + 1 < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a.seg_tiles[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  return static_cast<int>(lo);
+}
+
+// Row ids of tile t for producer thread p (row p): incidence row, head, tail.
+__device__ __forceinline__ void tile_rows(const Args& a, uint32_t t, int p, int& row2, int& h, int& tt, int& np,
+                                          int64_t& r) {
+  const FwdArgs& f = a.f;
+  const uint32_t sseg = __ldg(a.tile_seg + t), p0 = __ldg(a.tile_p0 + t);
+  const uint32_t e0 = __ldg(a.seg_start + sseg), len = __ldg(a.seg_start + sseg + 1) - e0;
+  r = static_cast<int64_t>(__ldg(a.seg_col + sseg)) - f.N;
+  const uint32_t units = len / 2;
+  np = static_cast<int>(min(static_cast<uint32_t>(kPairs), units - p0));
+  const int kk = p & 63;
+  row2 = -1;
+  h = 0;
+  tt = 0;
+  if (kk < np) {
+    const int pos = static_cast<int>(__ldg(a.ent_val + e0 + p0 + kk) & 0x7fffffffu);  // positive row = position
+    const bool neg = p >= 64;
+    row2 = neg ? pos + f.B : pos;
+    if (f.pair_ht) {
+      const int4 q = __ldg(f.pair_ht + pos);
+      h = neg ? q.z : q.x;
+      tt = neg ? q.w : q.y;
+    } else {
+      const int id = __ldg(f.order + pos);
+      h = neg ? __ldg(f.NH + id) : __ldg(f.H + id);
+      tt = neg ? __ldg(f.NT + id) : __ldg(f.T + id);
+    }
+  }
+}
+
+template <bool L2>
+__global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const FwdArgs& f = a.f;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool alive = f.err[0] == 0;
+
+  if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
+  if (tid == 0) {
+    tc::mbar_init(&S.u_full, 128);
+    tc::mbar_init(&S.v_full, 1);
+    tc::mbar_init(&S.dz_full, 128);
+    tc::mbar_init(&S.g2_done, 1);
+    tc::mbar_init(&S.du_empty, 128);
+    tc::mbar_init(&S.dm_full, 1);
+    tc::mbar_init(&S.dm_empty, 128);
+    for (int i = 0; i < kG3Slots; ++i) {
+      tc::mbar_init(&S.g3_full[i], 128);
+      tc::mbar_init(&S.g3_empty[i], 1);
+    }
+    for (int i = 0; i < kRing; ++i) {
+      tc::mbar_init(&S.ring_full[i], 1);
+      tc::mbar_init(&S.ring_empty[i], 1);
+    }
+    tc::fence_barrier_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = S.tmem_base;
+
+  const uint32_t T = alive ? a.tile_total[0] : 0u;
+  const uint32_t G = gridDim.x;
+  const uint32_t t0 = static_cast<uint32_t>((static_cast<uint64_t>(T) * blockIdx.x) / G);
+  const uint32_t t1 = static_cast<uint32_t>((static_cast<uint64_t>(T) * (blockIdx.x + 1)) / G);
+  const uint32_t ntile = t1 - t0;
+
+  float lsum = 0.f;
+  uint32_t pend = 0;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ epilogue
+    const int m = tid;  // row == TMEM lane
+    const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+    float dr_acc = 0.f;
+    int run = -1;
+    uint32_t nrun = 0;
+    for (uint32_t it = 0; it < ntile; ++it) {
+      const uint32_t t = t0 + it;
+      const int k = run_of(a, t);
+      if (run >= 0 && k != run) ++nrun;
+      run = k;
+      const bool last_of_run = (t + 1 == t1) || (a.seg_tiles[k + 1] <= t + 1);
+      const int buf = it & 1;
+      tc::mbar_wait(&S.u_full, it & 1);  // tile metadata (rrow, rel, np)
+      tc::mbar_wait(&S.v_full, it & 1);
+      tc::fence_after();
+      const float* relr = S.rel[buf];
+      const int np = S.np[buf];
+      const int row2 = S.rrow[buf][m];
+      // pass 1: v = V + r, reference-order squared_sum / abs_sum (norms.hpp:19-55)
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      bool bad = false;
+#pragma unroll 1
+      for (int c = 0; c < kD; c += 32) {
+        uint32_t r0[16], r1[16];
+        tc::tmem_ld16_nowait(tbase + lane_addr + kColV + c, r0);
+        tc::tmem_ld16_nowait(tbase + lane_addr + kColV + c + 16, r1);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 32; q += 4) {
+          const uint32_t* rr = q < 16 ? r0 + q : r1 + (q - 16);
+          const float x0 = __fadd_rn(__uint_as_float(rr[0]), relr[c + q]);
+          const float x1 = __fadd_rn(__uint_as_float(rr[1]), relr[c + q + 1]);
+          const float x2 = __fadd_rn(__uint_as_float(rr[2]), relr[c + q + 2]);
+          const float x3 = __fadd_rn(__uint_as_float(rr[3]), relr[c + q + 3]);
+          bad |= nonfinite(x0) | nonfinite(x1) | nonfinite(x2) | nonfinite(x3);
+          s0 = __fadd_rn(s0, norm_term<L2>(x0));
+          s1 = __fadd_rn(s1, norm_term<L2>(x1));
+          s2 = __fadd_rn(s2, norm_term<L2>(x2));
+          s3 = __fadd_rn(s3, norm_term<L2>(x3));
+        }
+      }
+      const float ssum = __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
+      S.rs[m] = L2 ? __fsqrt_rn(ssum) : ssum;
+      if (bad && row2 >= 0) pend |= kPendEntity;
+      tc::named_sync(1, 128);
+      // pair hinge (training.cpp:73-94): term = margin + E_pos - E_neg, active iff > 0
+      const int kk = m & 63;
+      const bool valid = kk < np;
+      float term = 0.f;
+      if (valid) term = __fsub_rn(__fadd_rn(f.margin, S.rs[kk]), S.rs[64 + kk]);
+      const bool active = valid && term > 0.f;
+      const float up = active ? (m < 64 ? f.unit : -f.unit) : 0.f;
+      const float sc = up == 0.f ? 0.f : (L2 ? __fdiv_rn(up, __fsqrt_rn(__fadd_rn(ssum, kNormEpsF))) : up);
+      if (row2 >= 0) f.scal[row2] = active ? 1.f : 0.f;
+      {  // tile loss: positive rows, deterministic tree
+        float v = (m < 64 && active) ? term : 0.f;
+        if (warp < 2) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v = __fadd_rn(v, __shfl_down_sync(kFull, v, o));
+          if (lane == 0) S.tl[warp] = v;
+        }
+      }
+      // pass 2: DZ (norm direction * up) -> sDZ (raw = tf32 hi), lo -> TMEM; column sums of DZ
+#pragma unroll 1
+      for (int c = 0; c < kD; c += 32) {
+        uint32_t r0[16], r1[16];
+        tc::tmem_ld16_nowait(tbase + lane_addr + kColV + c, r0);
+        tc::tmem_ld16_nowait(tbase + lane_addr + kColV + c + 16, r1);
+        tc::tmem_wait_ld();
+        float dz[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const float x = __fadd_rn(__uint_as_float(q < 16 ? r0[q] : r1[q - 16]), relr[c + q]);
+          dz[q] = sc == 0.f ? 0.f : (L2 ? __fmul_rn(x, sc) : (x > 0.f ? sc : (x < 0.f ? -sc : 0.f)));
+        }
+#pragma unroll
+        for (int q = 0; q < 32; q += 4)
+          *reinterpret_cast<float4*>(S.DZ + 4 * tile_unit(m, (c + q) >> 2)) = make_float4(dz[q], dz[q + 1], dz[q + 2], dz[q + 3]);
+        float lo[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) lo[q] = tc::tf32_trunc_lo(dz[q]);
+        tc::tmem_st16(tbase + lane_addr + kColLo + c, lo);
+        tc::tmem_st16(tbase + lane_addr + kColLo + c + 16, lo + 16);
+        // transpose-reduce the 32 x 32 block: lane l ends with the column c + l sum
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) {
+          const bool upper = (lane & w) != 0;
+#pragma unroll
+          for (int q = 0; q < w; ++q) {
+            const float send = upper ? dz[q] : dz[q + w];
+            const float keep = upper ? dz[q + w] : dz[q];
+            dz[q] = __fadd_rn(keep, __shfl_xor_sync(kFull, send, w));
+          }
+        }
+        S.colsum[warp][c + lane] = dz[0];
+      }
+      tc::tmem_wait_st();
+      tc::fence_before();
+      tc::fence_async_shared();
+      tc::mbar_arrive(&S.dz_full);
+      tc::named_sync(1, 128);
+      dr_acc = __fadd_rn(dr_acc, __fadd_rn(__fadd_rn(S.colsum[0][m], S.colsum[1][m]),
+                                           __fadd_rn(S.colsum[2][m], S.colsum[3][m])));
+      if (m == 0) lsum = __fadd_rn(lsum, __fadd_rn(S.tl[0], S.tl[1]));
+      if (last_of_run) {  // flush the run's dM (lane = output row i) and sum(dz)
+        tc::mbar_wait(&S.dm_full, nrun & 1);
+        tc::fence_after();
+        const uint32_t slot = blockIdx.x + static_cast<uint32_t>(k);
+        float* dst = a.dm_part + static_cast<size_t>(slot) * kD * kD + static_cast<size_t>(m) * kD;
+#pragma unroll 1
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t r0[16], r1[16];
+          tc::tmem_ld16_nowait(tbase + lane_addr + kColDM + c, r0);
+          tc::tmem_ld16_nowait(tbase + lane_addr + kColDM + c + 16, r1);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; q += 4) {
+            *reinterpret_cast<float4*>(dst + c + q) = make_float4(__uint_as_float(r0[q]), __uint_as_float(r0[q + 1]),
+                                                                  __uint_as_float(r0[q + 2]), __uint_as_float(r0[q + 3]));
+            *reinterpret_cast<float4*>(dst + c + 16 + q) = make_float4(
+                __uint_as_float(r1[q]), __uint_as_float(r1[q + 1]), __uint_as_float(r1[q + 2]), __uint_as_float(r1[q + 3]));
+          }
+        }
+        a.dr_part[static_cast<size_t>(slot) * kD + m] = dr_acc;
+        dr_acc = 0.f;
+        tc::fence_before();
+        tc::mbar_arrive(&S.dm_empty);
+      }
+      // dU drain: rows of active pairs -> res_u (the entity segments skip the rest)
+      tc::mbar_wait(&S.g2_done, it & 1);
+      tc::fence_after();
+      float* dst = f.res_u + static_cast<size_t>(row2 < 0 ? 0 : row2) * kD;
+#pragma unroll 1
+      for (int c = 0; c < kD; c += 32) {
+        uint32_t r0[16], r1[16];
+        tc::tmem_ld16_nowait(tbase + lane_addr + kColDU + c, r0);
+        tc::tmem_ld16_nowait(tbase + lane_addr + kColDU + c + 16, r1);
+        tc::tmem_wait_ld();
+        if (active) {
+#pragma unroll
+          for (int q = 0; q < 16; q += 4) {
+            *reinterpret_cast<float4*>(dst + c + q) = make_float4(__uint_as_float(r0[q]), __uint_as_float(r0[q + 1]),
+                                                                  __uint_as_float(r0[q + 2]), __uint_as_float(r0[q + 3]));
+            *reinterpret_cast<float4*>(dst + c + 16 + q) = make_float4(
+                __uint_as_float(r1[q]), __uint_as_float(r1[q + 1]), __uint_as_float(r1[q + 2]), __uint_as_float(r1[q + 3]));
+          }
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&S.du_empty);
+    }
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ producers
+    const int p = tid - 128;   // row p == TMEM lane p (warp quadrant = warp % 4)
+    const int pw = warp - 4;
+    const uint32_t lane_addr = static_cast<uint32_t>(pw * 32) << 16;
+    int row2 = -1, hh = 0, tt = 0, np = 0;
+    int64_t r = 0;
+    if (ntile > 0) tile_rows(a, t0, p, row2, hh, tt, np, r);
+    uint32_t g3n = 0;
+    for (uint32_t it = 0; it < ntile; ++it) {
+      const int buf = it & 1;
+      S.sh_h[p] = hh;
+      S.sh_t[p] = tt;
+      S.rrow[buf][p] = row2;
+      S.rel[buf][p] = __ldg(f.X + f.N * static_cast<int64_t>(kD) + r * kD + p);
+      if (p == 0) S.np[buf] = np;
+      tc::named_sync(2, 128);
+      // gather U = h - t (rows 32pw .. +31): lane -> (row + lane % 8, 16-byte chunk + lane / 8)
+#pragma unroll 1
+      for (int rg = 0; rg < 4; rg += 2) {
+        float4 xh[2][8], xt[2][8];
+        int rowm[2];
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          rowm[g] = pw * 32 + (rg + g) * 8 + (lane & 7);
+          const float* ph = f.X + static_cast<size_t>(S.sh_h[rowm[g]]) * kD;
+          const float* pt = f.X + static_cast<size_t>(S.sh_t[rowm[g]]) * kD;
+#pragma unroll
+          for (int cq = 0; cq < 8; ++cq) {
+            const int c4 = cq * 4 + (lane >> 3);
+            xh[g][cq] = __ldg(reinterpret_cast<const float4*>(ph) + c4);
+            xt[g][cq] = __ldg(reinterpret_cast<const float4*>(pt) + c4);
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const bool ok = S.rrow[buf][rowm[g]] >= 0;
+#pragma unroll
+          for (int cq = 0; cq < 8; ++cq) {
+            const int c4 = cq * 4 + (lane >> 3);
+            const float4 u = ok ? make_float4(__fsub_rn(xh[g][cq].x, xt[g][cq].x), __fsub_rn(xh[g][cq].y, xt[g][cq].y),
+                                              __fsub_rn(xh[g][cq].z, xt[g][cq].z), __fsub_rn(xh[g][cq].w, xt[g][cq].w))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(S.U + 4 * tile_unit(rowm[g], c4)) = u;
+          }
+        }
+      }
+      // next tile's row ids: the dependent loads overlap the rest of this tile
+      if (it + 1 < ntile) tile_rows(a, t0 + it + 1, p, row2, hh, tt, np, r);
+      tc::fence_async_shared();
+      tc::named_sync(2, 128);
+      // U lo -> TMEM once GEMM2 of the previous tile has consumed DZ lo
+      if (it > 0) {
+        tc::mbar_wait(&S.g2_done, (it - 1) & 1);
+        tc::fence_after();
+      }
+#pragma unroll 1
+      for (int c = 0; c < kD; c += 16) {
+        float lo[16];
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+          const float4 u = *reinterpret_cast<const float4*>(S.U + 4 * tile_unit(p, (c + q) >> 2));
+          lo[q] = tc::tf32_trunc_lo(u.x);
+          lo[q + 1] = tc::tf32_trunc_lo(u.y);
+          lo[q + 2] = tc::tf32_trunc_lo(u.z);
+          lo[q + 3] = tc::tf32_trunc_lo(u.w);
+        }
+        tc::tmem_st16(tbase + lane_addr + kColLo + c, lo);
+      }
+      tc::tmem_wait_st();
+      tc::fence_before();
+      tc::mbar_arrive(&S.u_full);
+      // GEMM3 staging: DZ^T and U^T, 8 rows per slot, split hi (rna) / lo
+      tc::mbar_wait(&S.dz_full, it & 1);
+      const int kq = p & 7, ig = p >> 3;
+#pragma unroll 1
+      for (int s3 = 0; s3 < kG3PerTile; ++s3, ++g3n) {
+        const int slot = g3n % kG3Slots;
+        if (g3n >= kG3Slots) tc::mbar_wait(&S.g3_empty[slot], ((g3n / kG3Slots) - 1) & 1);
+        const int row = s3 * kG3Rows + kq;
+        float* Ahi = S.g3[slot][0];
+        float* Alo = S.g3[slot][1];
+        float* Bhi = S.g3[slot][2];
+        float* Blo = S.g3[slot][3];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c4 = ig + 16 * h2;
+          const float4 dz = *reinterpret_cast<const float4*>(S.DZ + 4 * tile_unit(row, c4));
+          const float4 u = *reinterpret_cast<const float4*>(S.U + 4 * tile_unit(row, c4));
+          const float dv[4] = {dz.x, dz.y, dz.z, dz.w}, uv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int o = g3_off(4 * c4 + e, kq);
+            float hi, lo;
+            tc::split_tf32(dv[e], hi, lo);
+            Ahi[o] = hi;
+            Alo[o] = lo;
+            tc::split_tf32(uv[e], hi, lo);
+            Bhi[o] = hi;
+            Blo[o] = lo;
+          }
+        }
+        tc::fence_async_shared();
+        tc::mbar_arrive(&S.g3_full[slot]);
+      }
+      tc::named_sync(2, 128);  // sU / sDZ reads done: the next gather may overwrite sU
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issue
+    const uint32_t id = idesc128();
+    const uint32_t sU = tc::smem_u32(S.U), sDZ = tc::smem_u32(S.DZ);
+    uint32_t rn = 0, g3n = 0, nrun = 0;
+    int run = -1;
+    for (uint32_t it = 0; it < ntile; ++it) {
+      const uint32_t t = t0 + it;
+      const int k = run_of(a, t);
+      const bool first_of_run = k != run;
+      if (run >= 0 && first_of_run) ++nrun;
+      run = k;
+      const bool last_of_run = (t + 1 == t1) || (a.seg_tiles[k + 1] <= t + 1);
+      tc::mbar_wait(&S.u_full, it & 1);
+      tc::fence_after();
+      // GEMM1: V = U M_r^T
+      for (int c = 0; c < kChunksPerGemm; ++c, ++rn) {
+        const int s = rn % kRing;
+        tc::mbar_wait(&S.ring_full[s], (rn / kRing) & 1);
+        tc::fence_after();
+        const uint32_t bh = tc::smem_u32(S.ring[s]), bl = bh + kChunkFloats * 4;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int ks = c * 2 + kk;
+          const uint64_t ad = tc::make_desc(sU + ks * 256, kTileLBO, kTileSBO);
+          const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
+          const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
+          tc::mma_ss_elect(tbase + kColV, ad, bhd, id, ks > 0 ? 1u : 0u);
+          tc::mma_ss_elect(tbase + kColV, ad, bld, id, 1u);
+          tc::mma_ts_elect(tbase + kColV, tbase + kColLo + ks * 8, bhd, id, 1u);
+        }
+        tc::commit_elect(&S.ring_empty[s]);
+      }
+      tc::commit_elect(&S.v_full);
+      // GEMM3: dM += DZ^T U over the staged 8-row slots
+      if (first_of_run && nrun > 0) {
+        tc::mbar_wait(&S.dm_empty, (nrun - 1) & 1);
+        tc::fence_after();
+      }
+      for (int s3 = 0; s3 < kG3PerTile; ++s3, ++g3n) {
+        const int slot = g3n % kG3Slots;
+        tc::mbar_wait(&S.g3_full[slot], (g3n / kG3Slots) & 1);
+        tc::fence_after();
+        const uint32_t base = tc::smem_u32(S.g3[slot][0]);
+        const uint64_t ahi = tc::make_desc(base, kG3LBO, kG3SBO);
+        const uint64_t alo = tc::make_desc(base + kG3ArrFloats * 4, kG3LBO, kG3SBO);
+        const uint64_t bhi = tc::make_desc(base + 2 * kG3ArrFloats * 4, kG3LBO, kG3SBO);
+        const uint64_t blo = tc::make_desc(base + 3 * kG3ArrFloats * 4, kG3LBO, kG3SBO);
+        tc::mma_ss_elect(tbase + kColDM, ahi, bhi, id, (first_of_run && s3 == 0) ? 0u : 1u);
+        tc::mma_ss_elect(tbase + kColDM, ahi, blo, id, 1u);
+        tc::mma_ss_elect(tbase + kColDM, alo, bhi, id, 1u);
+        tc::commit_elect(&S.g3_empty[slot]);
+      }
+      if (last_of_run) tc::commit_elect(&S.dm_full);
+      // GEMM2: dU = DZ M_r (sDZ raw = hi, DZ lo from TMEM)
+      tc::mbar_wait(&S.dz_full, it & 1);
+      if (it > 0) tc::mbar_wait(&S.du_empty, (it - 1) & 1);
+      tc::fence_after();
+      for (int c = 0; c < kChunksPerGemm; ++c, ++rn) {
+        const int s = rn % kRing;
+        tc::mbar_wait(&S.ring_full[s], (rn / kRing) & 1);
+        tc::fence_after();
+        const uint32_t bh = tc::smem_u32(S.ring[s]), bl = bh + kChunkFloats * 4;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int ks = c * 2 + kk;
+          const uint64_t ad = tc::make_desc(sDZ + ks * 256, kTileLBO, kTileSBO);
+          const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
+          const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
+          tc::mma_ss_elect(tbase + kColDU, ad, bhd, id, ks > 0 ? 1u : 0u);
+          tc::mma_ss_elect(tbase + kColDU, ad, bld, id, 1u);
+          tc::mma_ts_elect(tbase + kColDU, tbase + kColLo + ks * 8, bhd, id, 1u);
+        }
+        tc::commit_elect(&S.ring_empty[s]);
+      }
+      tc::commit_elect(&S.g2_done);
+    }
+  } else {
+    // ------------------------------------------------------------ ring loader
+    uint32_t rn = 0;
+    for (uint32_t it = 0; it < ntile; ++it) {
+      const uint32_t t = t0 + it;
+      const int64_t r = static_cast<int64_t>(__ldg(a.seg_col + __ldg(a.tile_seg + t))) - f.N;
+      for (int layout = 0; layout < 2; ++layout)
+        for (int c = 0; c < kChunksPerGemm; ++c, ++rn) {
+          const int s = rn % kRing;
+          if (rn >= kRing) tc::mbar_wait(&S.ring_empty[s], ((rn / kRing) - 1) & 1);
+          if (lane == 0) {
+            const float* src = a.mr + r * kMrFloatsPerRel + static_cast<int64_t>(layout * kChunksPerGemm + c) * 2 * kChunkFloats;
+            tc::mbar_arrive_expect_tx(&S.ring_full[s], kChunkBytes);
+            tc::bulk_g2s(S.ring[s], src, kChunkBytes, &S.ring_full[s]);
+          }
+          __syncwarp();
+        }
+    }
+  }
+
+  // ---- teardown, loss: one partial per CTA, the last CTA finalizes (tile order)
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, 512);
+  if (warp < 4) {
+    pend = __reduce_or_sync(kFull, pend);
+    if (lane == 0 && pend) {
+      atomicOr(&f.err[3], pend);
+      __threadfence();
+    }
+  }
+  if (!alive) return;
+  if (tid == 0) {
+    f.block_partial[blockIdx.x] = lsum;
+    __threadfence();
+    S.last = atomicAdd(f.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (S.last && warp == 0) {
+    __threadfence();
+    float acc = 0.f;
+    for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, f.block_partial[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_down_sync(kFull, acc, o));
+    if (lane == 0) {
+      const float loss = __fdiv_rn(acc, f.loss_div > 0.f ? f.loss_div : static_cast<float>(f.B));
+      f.batch_loss[f.batch] = loss;
+      const uint32_t pflags = atomicOr(&f.err[3], 0u);
+      if (nonfinite(loss)) {
+        f.err[1] = f.batch;
+        atomicCAS(&f.err[0], 0u, static_cast<uint32_t>(kErrLossNonFinite));
+      } else if (pflags) {
+        f.err[1] = f.batch;
+        atomicCAS(&f.err[0], 0u, static_cast<uint32_t>(kErrGradEntity));
+      }
+      f.err[3] = 0;
+      *f.counter = 0;
+    }
+  }
+}
+
+// Per relation: both K-major operand views of M_r in 16-wide K chunks, split
+// hi (rna tf32) / lo, laid out exactly as the ring slots are read.
+//   layout 0 (GEMM1 B): n = output row i, k = j;  layout 1 (GEMM2 B): n = j, k = i.
+__global__ void transr_train_prep_kernel(const float* __restrict__ proj, float* __restrict__ out) {
+  const int r = blockIdx.x, lc = blockIdx.y;  // lc = layout * 8 + chunk
+  const int layout = lc >> 3, k0 = (lc & 7) * kChunkK;
+  const float* M = proj + static_cast<int64_t>(r) * kD * kD;
+  float* hi = out + r * kMrFloatsPerRel + static_cast<int64_t>(lc) * 2 * kChunkFloats;
+  float* lo = hi + kChunkFloats;
+  for (int i = threadIdx.x; i < kChunkFloats; i += blockDim.x) {
+    int n, kk;
+    float x;
+    if (layout == 0) {  // M[n][k0 + kk]: 16 consecutive floats per row
+      n = i >> 4;
+      kk = i & 15;
+      x = M[n * kD + k0 + kk];
+    } else {            // M[k0 + kk][n]: coalesced along n
+      kk = i >> 7;
+      n = i & 127;
+      x = M[(k0 + kk) * kD + n];
+    }
+    float h, l;
+    tc::split_tf32(x, h, l);
+    const int o = (((n & 7) + (n >> 3) * 32 + (kk >> 2) * 8) << 2) + (kk & 3);
+    hi[o] = h;
+    lo[o] = l;
+  }
+}
+
+}  // namespace
+
+int64_t transr_train_tc_mr_floats(int64_t R) { return R * kMrFloatsPerRel; }
+
+void configure_transr_train_tc_kernels() {
+  SKG_CUDA(cudaFuncSetAttribute(transr_train_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(Smem))));
+  SKG_CUDA(cudaFuncSetAttribute(transr_train_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(Smem))));
+}
+
+void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,
+                            const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
+                            const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,
+                            float* mr, int64_t R, int num_sms, cudaStream_t s) {
+  transr_train_prep_kernel<<<dim3(static_cast<unsigned>(R), 2 * kChunksPerGemm), 256, 0, s>>>(fa.proj, mr);
+  count_launch();
+  Args a{};
+  a.f = fa;
+  a.ent_val = ent_val;
+  a.seg_start = seg_start;
+  a.seg_col = seg_col;
+  a.tile_seg = tile_seg;
+  a.tile_p0 = tile_p0;
+  a.tile_total = tile_total;
+  a.seg_tiles = seg_tiles;
+  a.dm_part = dm_part;
+  a.dr_part = dr_part;
+  a.mr = mr;
+  const size_t smem = sizeof(Smem);
+  if (l2) transr_train_tc_kernel<true><<<num_sms, kThreads, smem, s>>>(a);
+  else transr_train_tc_kernel<false><<<num_sms, kThreads, smem, s>>>(a);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
+}  // namespace skg
