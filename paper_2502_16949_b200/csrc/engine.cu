@@ -1296,6 +1296,14 @@ extern "C" skg_status skg_dp_shard(int64_t m, int64_t batch_size, int32_t world,
   return SKG_OK;
 }
 
+extern "C" int64_t skg_debug_transr_trace(int32_t enable, unsigned long long* out, int64_t cap) {
+  try {
+    return transr_trace(enable, out, cap);
+  } catch (...) {
+    return -1;
+  }
+}
+
 extern "C" skg_status skg_debug_tc_gemm(skg_ctx* ctx, int32_t mode, const float* A, const float* B, float* D) {
   return guard(ctx, [&] {
     if (mode < 0 || mode > 2) throw ConfigError("debug_tc_gemm: mode 0..2");

@@ -34,6 +34,20 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes
   return d;
 }
 
+// K-major SWIZZLE_128B descriptor: 8-row x 128-byte atoms, 16-byte chunks
+// XOR-permuted by (row % 8); atoms 1024-byte aligned, SBO = stride between
+// 8-row groups, LBO unused (1). K steps inside an atom advance the start
+// address by 32 bytes (tf32 K = 8).
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
 // Instruction descriptor for kind::tf32 with an fp32 accumulator.
 __host__ __device__ constexpr uint32_t make_idesc_tf32(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4)                                   // D format F32

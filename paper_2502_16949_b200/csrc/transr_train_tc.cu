@@ -20,6 +20,7 @@
 //   warps 4-7  producer   row-id chase, U gather, U lo -> TMEM, G3 staging
 //   warp  8    MMA issue  (whole warp, elect.sync inside the asm)
 //   warp  9    ring loader (bulk copies of M_r chunks)
+//   warp 10    row-id chase (tile -> incidence rows -> head / tail), two tiles ahead
 // TMEM columns: [0,128) V | [128,256) U lo, then DZ lo | [256,384) dU | [384,512) dM.
 //
 // The CTA-range / relation-run partition (slot = CTA + run ordinal) is the one
@@ -37,13 +38,17 @@ namespace {
 constexpr int kD = 128;
 constexpr int kRows = 128;
 constexpr int kPairs = 64;
-constexpr int kThreads = 320;
-constexpr int kMmaWarp = 8, kLoadWarp = 9;
+constexpr int kThreads = 352;
+constexpr int kMmaWarp = 8, kLoadWarp = 9, kRowWarp = 10;
 
-// sU / sDZ: canonical no-swizzle K-major (m = row, k = feature);
-// 16-byte unit (r, c4) = (r & 7) + (r >> 3) * 256 + c4 * 8.
-__device__ __forceinline__ int tile_unit(int r, int c4) { return (r & 7) + (r >> 3) * 256 + c4 * 8; }
-constexpr uint32_t kTileLBO = 8 * 16, kTileSBO = 256 * 16;
+// sU / sDZ: K-major SWIZZLE_128B (m = row, k = feature) in four 32-feature
+// column blocks of 128 rows x 128 B; 16-byte unit (r, c4) =
+// block * 1024 + r * 8 + ((c4 & 7) ^ (r & 7)). A row's 32 units land in
+// distinct bank groups per 128 B, so both the coalesced row gather (lane =
+// chunk) and the thread-per-row epilogue stores are conflict-free.
+__device__ __forceinline__ int tile_unit(int r, int c4) { return (c4 >> 3) * 1024 + r * 8 + ((c4 & 7) ^ (r & 7)); }
+__device__ __forceinline__ uint32_t tile_kstep(int ks) { return static_cast<uint32_t>((ks >> 2) * 16384 + (ks & 3) * 32); }
+constexpr uint32_t kTileSBO = 8 * 128;
 
 // Ring chunk of M_r: 128 (n) x 16 (k), hi then lo; unit (n, k4) = (n & 7) + (n >> 3) * 32 + k4 * 8.
 constexpr int kChunkK = 16;
@@ -67,19 +72,29 @@ __device__ __forceinline__ int g3_off(int i, int k) { return (((i & 7) + (i >> 3
 
 constexpr uint32_t kColV = 0, kColLo = 128, kColDU = 256, kColDM = 384;
 
+// Phase timestamps (clock64) for pipeline analysis, off unless enabled through
+// skg_debug_transr_trace: [CTA][tile < 16][event < 16].
+constexpr int kTrCtas = 160, kTrTiles = 16, kTrEvents = 16;
+__device__ unsigned long long g_trace[kTrCtas * kTrTiles * kTrEvents];
+__device__ int g_trace_on;
+__device__ __forceinline__ void trace_ev(bool on, uint32_t it, int ev) {
+  if (on && it < kTrTiles && blockIdx.x < kTrCtas && (threadIdx.x & 31) == 0)
+    g_trace[(blockIdx.x * kTrTiles + it) * kTrEvents + ev] = clock64();
+}
+
 struct Smem {
   float U[kRows * kD];
   float DZ[kRows * kD];
   float ring[kRing][2 * kChunkFloats];
   float g3[kG3Slots][4][kG3ArrFloats];  // DZ^T hi, DZ^T lo, U^T hi, U^T lo
-  int rrow[2][kRows];                   // incidence row of each tile row (-1: padding)
+  int4 rows[2][kRows];                  // {head, tail, incidence row (-1: padding), 0}
   float rel[2][kD];
   int np[2];
-  int sh_h[kRows], sh_t[kRows];
   float rs[kRows];
   float colsum[4][kD];
   float tl[2];
   uint64_t u_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty;
+  uint64_t rows_full[2], rows_empty[2];
   uint64_t g3_full[kG3Slots], g3_empty[kG3Slots];
   uint64_t ring_full[kRing], ring_empty[kRing];
   uint32_t tmem_base;
@@ -113,33 +128,42 @@ __device__ __forceinline__ int run_of(const Args& a, uint32_t t) {
   return static_cast<int>(lo);
 }
 
-// Row ids of tile t for producer thread p (row p): incidence row, head, tail.
-__device__ __forceinline__ void tile_rows(const Args& a, uint32_t t, int p, int& row2, int& h, int& tt, int& np,
-                                          int64_t& r) {
+// Row ids of tile t by one warp: lane l resolves pairs l and l + 32 (positive
+// row = batch position; its negative is row B + position, same relation).
+__device__ __forceinline__ void chase_rows(const Args& a, uint32_t t, int lane, int4* rows, float* rel, int* np_out) {
   const FwdArgs& f = a.f;
   const uint32_t sseg = __ldg(a.tile_seg + t), p0 = __ldg(a.tile_p0 + t);
   const uint32_t e0 = __ldg(a.seg_start + sseg), len = __ldg(a.seg_start + sseg + 1) - e0;
-  r = static_cast<int64_t>(__ldg(a.seg_col + sseg)) - f.N;
-  const uint32_t units = len / 2;
-  np = static_cast<int>(min(static_cast<uint32_t>(kPairs), units - p0));
-  const int kk = p & 63;
-  row2 = -1;
-  h = 0;
-  tt = 0;
-  if (kk < np) {
-    const int pos = static_cast<int>(__ldg(a.ent_val + e0 + p0 + kk) & 0x7fffffffu);  // positive row = position
-    const bool neg = p >= 64;
-    row2 = neg ? pos + f.B : pos;
-    if (f.pair_ht) {
-      const int4 q = __ldg(f.pair_ht + pos);
-      h = neg ? q.z : q.x;
-      tt = neg ? q.w : q.y;
-    } else {
-      const int id = __ldg(f.order + pos);
-      h = neg ? __ldg(f.NH + id) : __ldg(f.H + id);
-      tt = neg ? __ldg(f.NT + id) : __ldg(f.T + id);
-    }
+  const int64_t r = static_cast<int64_t>(__ldg(a.seg_col + sseg)) - f.N;
+  const int np = static_cast<int>(min(static_cast<uint32_t>(kPairs), len / 2 - p0));
+  int pos[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int kk = lane + 32 * q;
+    pos[q] = kk < np ? static_cast<int>(__ldg(a.ent_val + e0 + p0 + kk) & 0x7fffffffu) : -1;
   }
+  const float4 rv = __ldg(reinterpret_cast<const float4*>(f.X + f.N * static_cast<int64_t>(kD) + r * kD) + lane);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int kk = lane + 32 * q;
+    int4 pr = make_int4(0, 0, -1, 0), ng = make_int4(0, 0, -1, 0);
+    if (pos[q] >= 0) {
+      int h, tt, nh, nt;
+      if (f.pair_ht) {
+        const int4 x = __ldg(f.pair_ht + pos[q]);
+        h = x.x, tt = x.y, nh = x.z, nt = x.w;
+      } else {
+        const int id = __ldg(f.order + pos[q]);
+        h = __ldg(f.H + id), tt = __ldg(f.T + id), nh = __ldg(f.NH + id), nt = __ldg(f.NT + id);
+      }
+      pr = make_int4(h, tt, pos[q], 0);
+      ng = make_int4(nh, nt, pos[q] + f.B, 0);
+    }
+    rows[kk] = pr;
+    rows[64 + kk] = ng;
+  }
+  reinterpret_cast<float4*>(rel)[lane] = rv;
+  if (lane == 0) *np_out = np;
 }
 
 template <bool L2>
@@ -149,6 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
   const FwdArgs& f = a.f;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool alive = f.err[0] == 0;
+  const bool tr = g_trace_on == f.batch + 1;  // trace one chosen minibatch
+  auto trace = [&](uint32_t it, int ev) { trace_ev(tr, it, ev); };
 
   if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
   if (tid == 0) {
@@ -163,6 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       tc::mbar_init(&S.g3_full[i], 128);
       tc::mbar_init(&S.g3_empty[i], 1);
     }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&S.rows_full[i], 1);
+      tc::mbar_init(&S.rows_empty[i], 128);
+    }
     for (int i = 0; i < kRing; ++i) {
       tc::mbar_init(&S.ring_full[i], 1);
       tc::mbar_init(&S.ring_empty[i], 1);
@@ -173,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = S.tmem_base;
+  if ((tc::smem_u32(S.U) & 1023u) != 0) __trap();  // SWIZZLE_128B atoms need 1 KB alignment
 
   const uint32_t T = alive ? a.tile_total[0] : 0u;
   const uint32_t G = gridDim.x;
@@ -197,12 +228,14 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       run = k;
       const bool last_of_run = (t + 1 == t1) || (a.seg_tiles[k + 1] <= t + 1);
       const int buf = it & 1;
-      tc::mbar_wait(&S.u_full, it & 1);  // tile metadata (rrow, rel, np)
+      tc::mbar_wait(&S.rows_full[buf], (it >> 1) & 1);  // tile metadata (rows, rel, np)
+      tc::mbar_wait(&S.u_full, it & 1);
       tc::mbar_wait(&S.v_full, it & 1);
       tc::fence_after();
+      if (m == 0) trace(it, 11);
       const float* relr = S.rel[buf];
       const int np = S.np[buf];
-      const int row2 = S.rrow[buf][m];
+      const int row2 = S.rows[buf][m].z;
       // pass 1: v = V + r, reference-order squared_sum / abs_sum (norms.hpp:19-55)
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       bool bad = false;
@@ -285,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       tc::fence_before();
       tc::fence_async_shared();
       tc::mbar_arrive(&S.dz_full);
+      if (m == 0) trace(it, 12);
       tc::named_sync(1, 128);
       dr_acc = __fadd_rn(dr_acc, __fadd_rn(__fadd_rn(S.colsum[0][m], S.colsum[1][m]),
                                            __fadd_rn(S.colsum[2][m], S.colsum[3][m])));
@@ -316,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       // dU drain: rows of active pairs -> res_u (the entity segments skip the rest)
       tc::mbar_wait(&S.g2_done, it & 1);
       tc::fence_after();
+      if (m == 0) trace(it, 13);
       float* dst = f.res_u + static_cast<size_t>(row2 < 0 ? 0 : row2) * kD;
 #pragma unroll 1
       for (int c = 0; c < kD; c += 32) {
@@ -335,58 +370,43 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       }
       tc::fence_before();
       tc::mbar_arrive(&S.du_empty);
+      tc::mbar_arrive(&S.rows_empty[buf]);
+      if (m == 0) trace(it, 14);
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ producers
     const int p = tid - 128;   // row p == TMEM lane p (warp quadrant = warp % 4)
     const int pw = warp - 4;
     const uint32_t lane_addr = static_cast<uint32_t>(pw * 32) << 16;
-    int row2 = -1, hh = 0, tt = 0, np = 0;
-    int64_t r = 0;
-    if (ntile > 0) tile_rows(a, t0, p, row2, hh, tt, np, r);
     uint32_t g3n = 0;
     for (uint32_t it = 0; it < ntile; ++it) {
       const int buf = it & 1;
-      S.sh_h[p] = hh;
-      S.sh_t[p] = tt;
-      S.rrow[buf][p] = row2;
-      S.rel[buf][p] = __ldg(f.X + f.N * static_cast<int64_t>(kD) + r * kD + p);
-      if (p == 0) S.np[buf] = np;
-      tc::named_sync(2, 128);
-      // gather U = h - t (rows 32pw .. +31): lane -> (row + lane % 8, 16-byte chunk + lane / 8)
+      tc::mbar_wait(&S.rows_full[buf], (it >> 1) & 1);
+      if (p == 0) trace(it, 0);
+      const int4* rows = S.rows[buf];
+      // gather U = h - t (rows 32pw .. +31): one 512-byte row per load
+      // instruction (lane = 16-byte chunk), 16 rows (32 loads) in flight
 #pragma unroll 1
-      for (int rg = 0; rg < 4; rg += 2) {
-        float4 xh[2][8], xt[2][8];
-        int rowm[2];
+      for (int r0 = pw * 32; r0 < pw * 32 + 32; r0 += 16) {
+        float4 xh[16], xt[16];
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          rowm[g] = pw * 32 + (rg + g) * 8 + (lane & 7);
-          const float* ph = f.X + static_cast<size_t>(S.sh_h[rowm[g]]) * kD;
-          const float* pt = f.X + static_cast<size_t>(S.sh_t[rowm[g]]) * kD;
-#pragma unroll
-          for (int cq = 0; cq < 8; ++cq) {
-            const int c4 = cq * 4 + (lane >> 3);
-            xh[g][cq] = __ldg(reinterpret_cast<const float4*>(ph) + c4);
-            xt[g][cq] = __ldg(reinterpret_cast<const float4*>(pt) + c4);
-          }
+        for (int q = 0; q < 16; ++q) {
+          const int4 rw = rows[r0 + q];
+          xh[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rw.x) * kD) + lane);
+          xt[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rw.y) * kD) + lane);
         }
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          const bool ok = S.rrow[buf][rowm[g]] >= 0;
-#pragma unroll
-          for (int cq = 0; cq < 8; ++cq) {
-            const int c4 = cq * 4 + (lane >> 3);
-            const float4 u = ok ? make_float4(__fsub_rn(xh[g][cq].x, xt[g][cq].x), __fsub_rn(xh[g][cq].y, xt[g][cq].y),
-                                              __fsub_rn(xh[g][cq].z, xt[g][cq].z), __fsub_rn(xh[g][cq].w, xt[g][cq].w))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-            *reinterpret_cast<float4*>(S.U + 4 * tile_unit(rowm[g], c4)) = u;
-          }
+        for (int q = 0; q < 16; ++q) {
+          const bool ok = rows[r0 + q].z >= 0;
+          const float4 u = ok ? make_float4(__fsub_rn(xh[q].x, xt[q].x), __fsub_rn(xh[q].y, xt[q].y),
+                                            __fsub_rn(xh[q].z, xt[q].z), __fsub_rn(xh[q].w, xt[q].w))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(S.U + 4 * tile_unit(r0 + q, lane)) = u;
         }
       }
-      // next tile's row ids: the dependent loads overlap the rest of this tile
-      if (it + 1 < ntile) tile_rows(a, t0 + it + 1, p, row2, hh, tt, np, r);
       tc::fence_async_shared();
       tc::named_sync(2, 128);
+      if (p == 0) trace(it, 1);
       // U lo -> TMEM once GEMM2 of the previous tile has consumed DZ lo
       if (it > 0) {
         tc::mbar_wait(&S.g2_done, (it - 1) & 1);
@@ -408,8 +428,10 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(&S.u_full);
+      if (p == 0) trace(it, 2);
       // GEMM3 staging: DZ^T and U^T, 8 rows per slot, split hi (rna) / lo
       tc::mbar_wait(&S.dz_full, it & 1);
+      if (p == 0) trace(it, 3);
       const int kq = p & 7, ig = p >> 3;
 #pragma unroll 1
       for (int s3 = 0; s3 < kG3PerTile; ++s3, ++g3n) {
@@ -441,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
         tc::fence_async_shared();
         tc::mbar_arrive(&S.g3_full[slot]);
       }
+      if (p == 0) trace(it, 4);
       tc::named_sync(2, 128);  // sU / sDZ reads done: the next gather may overwrite sU
     }
   } else if (warp == kMmaWarp) {
@@ -458,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       const bool last_of_run = (t + 1 == t1) || (a.seg_tiles[k + 1] <= t + 1);
       tc::mbar_wait(&S.u_full, it & 1);
       tc::fence_after();
+      trace(it, 5);
       // GEMM1: V = U M_r^T
       for (int c = 0; c < kChunksPerGemm; ++c, ++rn) {
         const int s = rn % kRing;
@@ -467,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const int ks = c * 2 + kk;
-          const uint64_t ad = tc::make_desc(sU + ks * 256, kTileLBO, kTileSBO);
+          const uint64_t ad = tc::make_desc_sw128(sU + tile_kstep(ks), kTileSBO);
           const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
           const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
           tc::mma_ss_elect(tbase + kColV, ad, bhd, id, ks > 0 ? 1u : 0u);
@@ -477,15 +501,24 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
         tc::commit_elect(&S.ring_empty[s]);
       }
       tc::commit_elect(&S.v_full);
+      trace(it, 6);
       // GEMM3: dM += DZ^T U over the staged 8-row slots
       if (first_of_run && nrun > 0) {
         tc::mbar_wait(&S.dm_empty, (nrun - 1) & 1);
         tc::fence_after();
       }
+      // GEMM2 (dU = DZ M_r; sDZ raw = hi, DZ lo from TMEM) interleaved with the
+      // GEMM3 slots: one GEMM2 chunk after every second slot keeps the tensor
+      // pipe busy while the producers refill the slot just released.
+      tc::mbar_wait(&S.dz_full, it & 1);
+      if (it > 0) tc::mbar_wait(&S.du_empty, (it - 1) & 1);
+      tc::fence_after();
+      trace(it, 9);
       for (int s3 = 0; s3 < kG3PerTile; ++s3, ++g3n) {
         const int slot = g3n % kG3Slots;
         tc::mbar_wait(&S.g3_full[slot], (g3n / kG3Slots) & 1);
         tc::fence_after();
+        if (s3 == 0) trace(it, 7);
         const uint32_t base = tc::smem_u32(S.g3[slot][0]);
         const uint64_t ahi = tc::make_desc(base, kG3LBO, kG3SBO);
         const uint64_t alo = tc::make_desc(base + kG3ArrFloats * 4, kG3LBO, kG3SBO);
@@ -495,30 +528,39 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
         tc::mma_ss_elect(tbase + kColDM, ahi, blo, id, 1u);
         tc::mma_ss_elect(tbase + kColDM, alo, bhi, id, 1u);
         tc::commit_elect(&S.g3_empty[slot]);
-      }
-      if (last_of_run) tc::commit_elect(&S.dm_full);
-      // GEMM2: dU = DZ M_r (sDZ raw = hi, DZ lo from TMEM)
-      tc::mbar_wait(&S.dz_full, it & 1);
-      if (it > 0) tc::mbar_wait(&S.du_empty, (it - 1) & 1);
-      tc::fence_after();
-      for (int c = 0; c < kChunksPerGemm; ++c, ++rn) {
-        const int s = rn % kRing;
-        tc::mbar_wait(&S.ring_full[s], (rn / kRing) & 1);
-        tc::fence_after();
-        const uint32_t bh = tc::smem_u32(S.ring[s]), bl = bh + kChunkFloats * 4;
+        if (s3 == kG3PerTile - 1 && last_of_run) tc::commit_elect(&S.dm_full);
+        if (s3 & 1) {
+          const int c = s3 >> 1;
+          const int s = rn % kRing;
+          tc::mbar_wait(&S.ring_full[s], (rn / kRing) & 1);
+          tc::fence_after();
+          const uint32_t bh = tc::smem_u32(S.ring[s]), bl = bh + kChunkFloats * 4;
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          const int ks = c * 2 + kk;
-          const uint64_t ad = tc::make_desc(sDZ + ks * 256, kTileLBO, kTileSBO);
-          const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
-          const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
-          tc::mma_ss_elect(tbase + kColDU, ad, bhd, id, ks > 0 ? 1u : 0u);
-          tc::mma_ss_elect(tbase + kColDU, ad, bld, id, 1u);
-          tc::mma_ts_elect(tbase + kColDU, tbase + kColLo + ks * 8, bhd, id, 1u);
+          for (int kk = 0; kk < 2; ++kk) {
+            const int ks = c * 2 + kk;
+            const uint64_t ad = tc::make_desc_sw128(sDZ + tile_kstep(ks), kTileSBO);
+            const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
+            const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
+            tc::mma_ss_elect(tbase + kColDU, ad, bhd, id, ks > 0 ? 1u : 0u);
+            tc::mma_ss_elect(tbase + kColDU, ad, bld, id, 1u);
+            tc::mma_ts_elect(tbase + kColDU, tbase + kColLo + ks * 8, bhd, id, 1u);
+          }
+          tc::commit_elect(&S.ring_empty[s]);
+          ++rn;
         }
-        tc::commit_elect(&S.ring_empty[s]);
       }
+      trace(it, 8);
       tc::commit_elect(&S.g2_done);
+      trace(it, 10);
+    }
+  } else if (warp == kRowWarp) {
+    // ------------------------------------------------------------ row-id chase
+    for (uint32_t it = 0; it < ntile; ++it) {
+      const int buf = it & 1;
+      if (it >= 2) tc::mbar_wait(&S.rows_empty[buf], ((it >> 1) - 1) & 1);
+      chase_rows(a, t0 + it, lane, S.rows[buf], S.rel[buf], &S.np[buf]);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&S.rows_full[buf]);
     }
   } else {
     // ------------------------------------------------------------ ring loader
@@ -613,6 +655,17 @@ __global__ void transr_train_prep_kernel(const float* __restrict__ proj, float* 
 }  // namespace
 
 int64_t transr_train_tc_mr_floats(int64_t R) { return R * kMrFloatsPerRel; }
+
+int64_t transr_trace(int enable, unsigned long long* out, int64_t cap) {
+  SKG_CUDA(cudaMemcpyToSymbol(g_trace_on, &enable, sizeof(int)));
+  const int64_t n = static_cast<int64_t>(kTrCtas) * kTrTiles * kTrEvents;
+  if (enable) {
+    static const unsigned long long zeros[kTrCtas * kTrTiles * kTrEvents] = {};
+    SKG_CUDA(cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros)));
+  }
+  if (out && cap >= n) SKG_CUDA(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * n));
+  return n;
+}
 
 void configure_transr_train_tc_kernels() {
   SKG_CUDA(cudaFuncSetAttribute(transr_train_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
