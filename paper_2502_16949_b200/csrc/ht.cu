@@ -17,6 +17,8 @@
 // (embedding.cpp:181-189).
 //
 // TransR (models.cpp:110-156, models.hpp:82-96) lives in transr.cu.
+#include <algorithm>
+
 #include "common.cuh"
 #include "ht.cuh"
 #include "primitives.cuh"
@@ -473,10 +475,11 @@ void launch_relation_side(const FwdArgs& fa, const BwdArgs& ba, float* partial, 
 // work layout (floats): [nrm rows: rows x d][partials: R x parts x 2 x d]
 int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R) {
   if (kind == kTransR_L2 || kind == kTransR_L1) return transr_work_floats(rows, de, dr, R);
-  return 2 * rows * de + R * kRelParts * 2 * de + 64;
+  return std::max<int64_t>(2 * rows * de + R * kRelParts * 2 * de + 64, transh_tiles_work_floats(rows, R));
 }
 
 void configure_ht_kernels() {
+  configure_transh_tiles_kernels();
   configure_transh_one<true, kTrain, 4>();
   configure_transh_one<true, kTrain, 1>();
   configure_transh_one<true, kScore, 4>();
@@ -496,6 +499,15 @@ void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work,
                     const std::function<void()>* mark, int64_t R) {
   if (kind == kTransR_L2 || kind == kTransR_L1) {
     transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R);
+    return;
+  }
+  if (transh_tiles_supported(fa.de, fa.dr)) {  // relation-tiled path (transh_train.cu)
+    transh_tiles_train_batch(kind == kTransH_L2, fa, ba, work, R, num_sms, s, mark);
+    normals_renorm_kernel<<<static_cast<unsigned>((R * 32 + 127) / 128), 128, 0, s>>>(const_cast<float*>(fa.normals), R,
+                                                                                   fa.de, ba.err);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+    if (mark) (*mark)();
     return;
   }
   float* nrm = work;

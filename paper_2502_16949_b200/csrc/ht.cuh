@@ -27,6 +27,18 @@ void ht_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int n
 void ht_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj, float* g_normals,
                        int num_sms, cudaStream_t s, int64_t R);
 
+// Relation-grouped tiles of 64 (pos, neg) pairs (paired) or 128 rows over a
+// batch's relation segments (transr.cu); shared by TransR and TransH.
+int64_t relation_max_tiles(int64_t rows, int64_t R);
+void launch_relation_tiles(const BwdArgs& ba, int paired, uint32_t* tile_seg, uint32_t* tile_p0, uint32_t* tile_total,
+                           uint32_t* seg_tiles, cudaStream_t s);
+// TransH training on relation tiles (transh_train.cu), d_e = d_r = 128
+bool transh_tiles_supported(int de, int dr);
+void configure_transh_tiles_kernels();
+int64_t transh_tiles_work_floats(int64_t rows, int64_t R);
+void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
+                              cudaStream_t s, const std::function<void()>* mark);
+
 // TransR (transr.cu)
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R);
 void configure_transr_kernels();

@@ -1,0 +1,323 @@
+// TransH training step on relation-grouped tiles (sm_100a), d = 128.
+//
+// The epoch plan's relation segments list a relation's positive rows, then the
+// same pairs' negatives; a CTA owns 64 such (pos, neg) pairs = 128 rows of ONE
+// relation r (models.cpp:158-199, models.hpp:99-113), so the normal w_r and
+// the relation row d_r are loaded once per tile and the relation-side
+// gradients are summed inside the tile:
+//   u = h - t, wu = w.u, v = (u + d_r) - wu w          (hyperplane_forward)
+//   score = ||v|| in the reference's squared_sum / abs_sum order, pair hinge
+//   dz = dir(v) * up, dzw = dz.w
+//   du  = dz - dzw w          -> res_u rows (sorted entity segments, no atomics)
+//   sum dz, sum (dzw u + wu dz) -> one partial per tile (relation gradient and
+//                                  negated normal gradient, models.hpp:112)
+// A second kernel adds each relation's tile partials in tile order and applies
+// SGD; the normals are then renormalized (embedding.cpp:181-189). Compared with
+// the row-wise path (ht.cu) no dz / nrm rows go through HBM and w_r, d_r are
+// not re-gathered per row. Dot products use a fixed warp tree (the reference
+// reduces them with Eigen's redux; TransH parity is tolerance-only).
+#include <algorithm>
+
+#include "common.cuh"
+#include "ht.cuh"
+#include "primitives.cuh"
+#include "refmath.cuh"
+
+namespace skg {
+
+namespace {
+
+constexpr int kD = 128;
+constexpr int kRows = 128;
+constexpr int kPairs = 64;
+constexpr int kThreads = 512;      // 16 warps x 8 rows
+constexpr int kRowsPerWarp = 8;
+constexpr int kStride = kD + 4;    // staged v rows (16-byte aligned, conflict-free row reads)
+
+struct TArgs {
+  FwdArgs f;
+  const uint32_t* ent_val;
+  const uint32_t* seg_start;
+  const uint32_t* seg_col;
+  const uint32_t* tile_seg;
+  const uint32_t* tile_p0;
+  const uint32_t* tile_total;
+  float* partial;  // [tile][2][kD]
+};
+
+__device__ __forceinline__ float4 f4sub(float4 a, float4 b) {
+  return make_float4(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z), __fsub_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 f4scale(float s, float4 a) {
+  return make_float4(__fmul_rn(s, a.x), __fmul_rn(s, a.y), __fmul_rn(s, a.z), __fmul_rn(s, a.w));
+}
+__device__ __forceinline__ float f4dot(float4 a, float4 b) {
+  float acc = __fmul_rn(a.x, b.x);
+  acc = fmaf(a.y, b.y, acc);
+  acc = fmaf(a.z, b.z, acc);
+  return fmaf(a.w, b.w, acc);
+}
+template <bool L2>
+__device__ __forceinline__ float dirf(float v, float sc) {
+  return L2 ? __fmul_rn(v, sc) : (v > 0.f ? sc : (v < 0.f ? -sc : 0.f));
+}
+template <bool L2>
+__device__ __forceinline__ float4 dir4(float4 v, float sc) {
+  return make_float4(dirf<L2>(v.x, sc), dirf<L2>(v.y, sc), dirf<L2>(v.z, sc), dirf<L2>(v.w, sc));
+}
+template <bool L2>
+__global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a) {
+  extern __shared__ float4 smv[];
+  float* Vs = reinterpret_cast<float*>(smv);  // [kRows][kStride]
+  __shared__ int4 rows[kRows];                 // {head, tail, incidence row (-1: padding), 0}
+  __shared__ float score[kRows];
+  __shared__ float wloss[kThreads / 32];
+  __shared__ float4 accs[2][kThreads / 32][32];
+  __shared__ bool last;
+  const FwdArgs& f = a.f;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool alive = f.err[0] == 0;
+  const uint32_t T = alive ? a.tile_total[0] : 0u;
+  float lsum = 0.f;
+  uint32_t pend = 0;
+  for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint32_t sseg = __ldg(a.tile_seg + t), p0 = __ldg(a.tile_p0 + t);
+    const uint32_t e0 = __ldg(a.seg_start + sseg), len = __ldg(a.seg_start + sseg + 1) - e0;
+    const int64_t r = static_cast<int64_t>(__ldg(a.seg_col + sseg)) - f.N;
+    const int np = static_cast<int>(min(static_cast<uint32_t>(kPairs), len / 2 - p0));
+    const float4 w = __ldg(reinterpret_cast<const float4*>(f.normals + r * kD) + lane);
+    const float4 drv = __ldg(reinterpret_cast<const float4*>(f.X + (f.N + r) * kD) + lane);
+    if (tid < kPairs) {  // row ids: positive row = batch position, its negative = B + position
+      const int kk = tid;
+      int4 pr = make_int4(0, 0, -1, 0), ng = make_int4(0, 0, -1, 0);
+      if (kk < np) {
+        const int pos = static_cast<int>(__ldg(a.ent_val + e0 + p0 + kk) & 0x7fffffffu);
+        int h, tt, nh, nt;
+        if (f.pair_ht) {
+          const int4 x = __ldg(f.pair_ht + pos);
+          h = x.x, tt = x.y, nh = x.z, nt = x.w;
+        } else {
+          const int id = __ldg(f.order + pos);
+          h = __ldg(f.H + id), tt = __ldg(f.T + id), nh = __ldg(f.NH + id), nt = __ldg(f.NT + id);
+        }
+        pr = make_int4(h, tt, pos, 0);
+        ng = make_int4(nh, nt, pos + f.B, 0);
+      }
+      rows[kk] = pr;
+      rows[kPairs + kk] = ng;
+    }
+    __syncthreads();
+    // ---- u, wu, v for this warp's 8 rows, all 16 row loads in flight
+    const int m0 = warp * kRowsPerWarp;
+    float4 u[kRowsPerWarp];
+    float wu[kRowsPerWarp];
+    {
+      float4 xh[kRowsPerWarp], xt[kRowsPerWarp];
+#pragma unroll
+      for (int q = 0; q < kRowsPerWarp; ++q) {
+        const int4 rw = rows[m0 + q];
+        xh[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rw.x) * kD) + lane);
+        xt[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rw.y) * kD) + lane);
+      }
+      float part[kRowsPerWarp];
+#pragma unroll
+      for (int q = 0; q < kRowsPerWarp; ++q) {
+        u[q] = rows[m0 + q].z >= 0 ? f4sub(xh[q], xt[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        part[q] = f4dot(w, u[q]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) part[q] = __fadd_rn(part[q], __shfl_xor_sync(kFull, part[q], o));
+#pragma unroll
+      for (int q = 0; q < kRowsPerWarp; ++q) {
+        wu[q] = part[q];
+        const float4 v = f4sub(f4add(u[q], drv), f4scale(wu[q], w));
+        *reinterpret_cast<float4*>(Vs + (m0 + q) * kStride + 4 * lane) = v;
+      }
+    }
+    __syncwarp();
+    // ---- score (lane j < 8 owns row m0 + j): reference-order squared_sum / abs_sum
+    float ssum = 0.f;
+    bool bad = false;
+    const int mj = m0 + (lane & 7);
+    const int row2 = rows[mj].z;
+    if (lane < kRowsPerWarp) {
+      ssum = ref_norm_sum<L2, 4>(Vs + mj * kStride, kD, bad);
+      score[mj] = L2 ? __fsqrt_rn(ssum) : ssum;
+    }
+    __syncthreads();
+    // ---- pair hinge (training.cpp:73-94)
+    const int kk = mj & (kPairs - 1);
+    const bool valid = lane < kRowsPerWarp && kk < np;
+    float term = 0.f;
+    if (valid) term = __fsub_rn(__fadd_rn(f.margin, score[kk]), score[kPairs + kk]);
+    const bool act = valid && term > 0.f;
+    const float up = act ? (mj < kPairs ? f.unit : -f.unit) : 0.f;
+    const float sc = act ? (L2 ? __fdiv_rn(up, __fsqrt_rn(__fadd_rn(ssum, kNormEpsF))) : up) : 0.f;
+    if (valid) f.scal[row2] = act ? 1.f : 0.f;
+    if (valid && bad && (L2 || act)) pend |= kPendEntity;
+    {
+      float tk = (act && mj < kPairs) ? term : 0.f;
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) tk = __fadd_rn(tk, __shfl_down_sync(kFull, tk, o));
+      if (lane == 0) wloss[warp] = tk;
+    }
+    // ---- backward rows (hyperplane_backward, models.hpp:106-113)
+    const unsigned amask = __ballot_sync(kFull, act);
+    float4 acc_dz = make_float4(0.f, 0.f, 0.f, 0.f), acc_n = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (amask) {
+      float4 dz[kRowsPerWarp];
+      float part[kRowsPerWarp];
+#pragma unroll
+      for (int q = 0; q < kRowsPerWarp; ++q) {
+        const float scq = __shfl_sync(kFull, sc, q);
+        dz[q] = dir4<L2>(*reinterpret_cast<const float4*>(Vs + (m0 + q) * kStride + 4 * lane), scq);
+        if (!((amask >> q) & 1u)) dz[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        part[q] = f4dot(dz[q], w);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) part[q] = __fadd_rn(part[q], __shfl_xor_sync(kFull, part[q], o));
+#pragma unroll
+      for (int q = 0; q < kRowsPerWarp; ++q) {
+        if (!((amask >> q) & 1u)) continue;
+        const float dzw = part[q];
+        const int r2 = rows[m0 + q].z;
+        reinterpret_cast<float4*>(f.res_u + static_cast<size_t>(r2) * kD)[lane] = f4sub(dz[q], f4scale(dzw, w));
+        acc_dz = f4add(acc_dz, dz[q]);
+        acc_n = f4add(acc_n, f4add(f4scale(dzw, u[q]), f4scale(wu[q], dz[q])));
+      }
+    }
+    accs[0][warp][lane] = acc_dz;
+    accs[1][warp][lane] = acc_n;
+    __syncthreads();
+    if (tid < 64) {  // tile partial: warps in order
+      const int which = tid >> 5;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < kThreads / 32; ++q) s = f4add(s, accs[which][q][lane]);
+      reinterpret_cast<float4*>(a.partial + (static_cast<size_t>(t) * 2 + which) * kD)[lane] = s;
+    }
+    if (tid == 0)
+      for (int q = 0; q < kPairs / kRowsPerWarp; ++q) lsum = __fadd_rn(lsum, wloss[q]);
+    __syncthreads();  // rows / score / accs reuse by the next tile
+  }
+  pend = __reduce_or_sync(kFull, pend);
+  if (lane == 0 && pend) {
+    atomicOr(&f.err[3], pend);
+    __threadfence();
+  }
+  if (!alive) return;
+  // ---- loss: one partial per tile (tile order), the last CTA finalizes
+  if (tid == 0) {
+    f.block_partial[blockIdx.x] = lsum;
+    __threadfence();
+    last = atomicAdd(f.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && warp == 0) {
+    __threadfence();
+    float acc = 0.f;
+    for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, f.block_partial[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_down_sync(kFull, acc, o));
+    if (lane == 0) {
+      const float loss = __fdiv_rn(acc, f.loss_div > 0.f ? f.loss_div : static_cast<float>(f.B));
+      f.batch_loss[f.batch] = loss;
+      const uint32_t pflags = atomicOr(&f.err[3], 0u);
+      if (nonfinite(loss)) {
+        f.err[1] = f.batch;
+        atomicCAS(&f.err[0], 0u, static_cast<uint32_t>(kErrLossNonFinite));
+      } else if (pflags) {
+        f.err[1] = f.batch;
+        atomicCAS(&f.err[0], 0u, static_cast<uint32_t>(kErrGradEntity));
+      }
+      f.err[3] = 0;
+      *f.counter = 0;
+    }
+  }
+}
+
+// Per relation segment k: tile partials in tile order, then SGD on the relation
+// row and the normal (grads.normals -= nrm, models.hpp:112).
+__global__ void transh_rel_apply_kernel(const uint32_t* __restrict__ tile_total, const uint32_t* __restrict__ seg_tiles,
+                                        const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ seg_col,
+                                        int64_t N, const float* __restrict__ partial, float* __restrict__ rel,
+                                        float* __restrict__ normals, const float* __restrict__ lr,
+                                        const uint32_t* __restrict__ err) {
+  if (err[0] != 0) return;
+  const uint32_t k = blockIdx.x;
+  if (k >= tile_total[1]) return;
+  const uint32_t lo = seg_tiles[k], hi = seg_tiles[k + 1];
+  if (hi <= lo) return;
+  const int64_t r = static_cast<int64_t>(seg_col[tile_seg[lo]]) - N;
+  const int c = threadIdx.x;
+  float gA = 0.f, gB = 0.f;
+  for (uint32_t q = lo; q < hi; ++q) {
+    gA = __fadd_rn(gA, partial[(static_cast<size_t>(q) * 2) * kD + c]);
+    gB = __fadd_rn(gB, partial[(static_cast<size_t>(q) * 2 + 1) * kD + c]);
+  }
+  const float step = *lr;
+  float* pr = rel + r * kD + c;
+  float* pn = normals + r * kD + c;
+  *pr = __fsub_rn(*pr, __fmul_rn(step, gA));
+  *pn = __fsub_rn(*pn, __fmul_rn(step, -gB));
+}
+
+}  // namespace
+
+bool transh_tiles_supported(int de, int dr) { return de == kD && dr == kD; }
+
+int64_t transh_tiles_work_floats(int64_t rows, int64_t R) {
+  const int64_t mt = relation_max_tiles(rows, R);
+  return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + mt * 2 * kD + 64;
+}
+
+void configure_transh_tiles_kernels() {
+  const int smem = static_cast<int>(sizeof(float) * kRows * kStride);
+  SKG_CUDA(cudaFuncSetAttribute(transh_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  SKG_CUDA(cudaFuncSetAttribute(transh_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+}
+
+void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
+                              cudaStream_t s, const std::function<void()>* mark) {
+  const int64_t mt = relation_max_tiles(2 * static_cast<int64_t>(fa.B), R);
+  uint32_t* tile_seg = reinterpret_cast<uint32_t*>(work);
+  uint32_t* tile_p0 = tile_seg + mt;
+  uint32_t* tile_total = tile_p0 + mt;
+  uint32_t* seg_tiles = tile_total + 2;
+  float* partial = work + ((3 * mt + 2 * R + 8 + 31) / 32) * 32;
+  launch_relation_tiles(ba, 1, tile_seg, tile_p0, tile_total, seg_tiles, s);
+  TArgs a{};
+  a.f = fa;
+  a.ent_val = ba.ent_val;
+  a.seg_start = ba.seg_start;
+  a.seg_col = ba.seg_col;
+  a.tile_seg = tile_seg;
+  a.tile_p0 = tile_p0;
+  a.tile_total = tile_total;
+  a.partial = partial;
+  const size_t smem = sizeof(float) * kRows * kStride;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, static_cast<int64_t>(num_sms) * 16));
+  if (l2) transh_tile_kernel<true><<<grid, kThreads, smem, s>>>(a);
+  else transh_tile_kernel<false><<<grid, kThreads, smem, s>>>(a);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  if (mark) (*mark)();
+  BwdArgs eb = ba;
+  eb.entity_only = 1;
+  launch_segment_backward(kPlainRows, true, eb, num_sms, s);
+  float* rel = const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
+  float* normals = const_cast<float*>(fa.normals);
+  transh_rel_apply_kernel<<<static_cast<unsigned>(R), kD, 0, s>>>(tile_total, seg_tiles, tile_seg, ba.seg_col, ba.N,
+                                                                  partial, rel, normals, ba.lr, ba.err);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
+}  // namespace skg

@@ -497,6 +497,16 @@ void configure_one() {
 
 }  // namespace
 
+int64_t relation_max_tiles(int64_t rows, int64_t R) { return max_tiles(rows, R); }
+
+void launch_relation_tiles(const BwdArgs& ba, int paired, uint32_t* tile_seg, uint32_t* tile_p0, uint32_t* tile_total,
+                           uint32_t* seg_tiles, cudaStream_t s) {
+  transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, paired,
+                                                  tile_seg, tile_p0, tile_total, seg_tiles, ba.err);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
   const int64_t parts = std::max<int64_t>(mt, transr_tc_slots(256, R));  // tc path: (CTA, relation) runs
