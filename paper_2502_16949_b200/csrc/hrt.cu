@@ -23,6 +23,7 @@
 // Rows never touched keep p - lr*0 == p, so touching only the segment rows is
 // bitwise the reference's dense step.
 #include "common.cuh"
+#include "plan.cuh"
 #include "kernels.cuh"
 #include "primitives.cuh"
 
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
   const V* RV = reinterpret_cast<const V*>(a.res);
   for (uint32_t s = s0 + gw; s < s1; s += nw) {
     const uint32_t col = a.seg_col[s];
-    if (a.entity_only && col >= static_cast<uint32_t>(a.N)) continue;
+    if (col == kDummyCol || (a.entity_only && col >= static_cast<uint32_t>(a.N))) continue;
     const uint32_t e0 = a.seg_start[s], e1 = a.seg_start[s + 1];
     V* P = reinterpret_cast<V*>(a.X) + static_cast<size_t>(col) * dv;
     for (int cb = 0; cb < dv; cb += 32 * CH) {

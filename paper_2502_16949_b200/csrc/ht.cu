@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "ht.cuh"
+#include "plan.cuh"
 #include "primitives.cuh"
 #include "refmath.cuh"
 
@@ -279,7 +280,7 @@ struct RelArgs {
 __device__ __forceinline__ bool rel_segment(const RelArgs& a, int k, uint32_t& s) {
   const uint32_t s0 = a.seg_base[a.batch], s1 = a.seg_base[a.batch + 1];
   s = s0 + k;
-  return s < s1 && a.seg_col[s] >= static_cast<uint32_t>(a.N);
+  return s < s1 && a.seg_col[s] >= static_cast<uint32_t>(a.N) && a.seg_col[s] != kDummyCol;
 }
 
 __global__ void __launch_bounds__(128) rel_partial_kernel(const RelArgs a) {

@@ -11,21 +11,27 @@ __device__ __forceinline__ uint32_t col_key(int64_t col, int64_t N, int64_t Rn) 
   return static_cast<uint32_t>(col >= N ? col - N : col + Rn);
 }
 
+// Entries that do not exist (the cancelled entity pair of a self-loop row, the
+// relation entry of an ht-layout row) get the per-batch dummy column N + Rn:
+// it sorts after every real column of its batch, forms one segment with
+// seg_col = kDummyCol that every consumer skips, and keeps all batches'
+// entries inside their own block-aligned range (segmented radix sort).
 __device__ __forceinline__ void emit_row(uint32_t* key, uint32_t* val, int64_t base, uint32_t bkey,
                                          int32_t h, int32_t t, int32_t r, uint32_t row2, int64_t N,
-                                         int64_t Rn, uint32_t invalid, bool with_rel) {
+                                         int64_t Rn, bool with_rel) {
+  const uint32_t dummy = bkey | static_cast<uint32_t>(N + Rn);
   if (h != t) {  // +1 and -1 cancel at coo_to_csr time (sparse.hpp:145-155)
     key[base] = bkey | col_key(h, N, Rn);
     val[base] = row2;
     key[base + 1] = bkey | col_key(t, N, Rn);
     val[base + 1] = row2 | 0x80000000u;
   } else {
-    key[base] = invalid;
+    key[base] = dummy;
     val[base] = 0;
-    key[base + 1] = invalid;
+    key[base + 1] = dummy;
     val[base + 1] = 0;
   }
-  key[base + 2] = with_rel ? (bkey | col_key(N + r, N, Rn)) : invalid;
+  key[base + 2] = with_rel ? (bkey | col_key(N + r, N, Rn)) : dummy;
   val[base + 2] = row2;
 }
 
@@ -33,7 +39,7 @@ __global__ void gen_train_entries_kernel(const int32_t* __restrict__ order, cons
                                          const int32_t* __restrict__ R, const int32_t* __restrict__ T,
                                          const int32_t* __restrict__ NH, const int32_t* __restrict__ NT,
                                          int64_t M, int64_t B, int64_t N, int64_t Rn, int cb,
-                                         uint32_t invalid, uint32_t* __restrict__ key,
+                                         uint32_t* __restrict__ key,
                                          uint32_t* __restrict__ val, int4* __restrict__ pair_ht,
                                          int32_t* __restrict__ pair_r) {
   for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < 2 * M;
@@ -51,17 +57,17 @@ __global__ void gen_train_entries_kernel(const int32_t* __restrict__ order, cons
       pair_r[k] = R[id];
     }
     emit_row(key, val, base, static_cast<uint32_t>(b) << cb, h, t, R[id],
-             static_cast<uint32_t>(p * Bb + i), N, Rn, invalid, true);
+             static_cast<uint32_t>(p * Bb + i), N, Rn, true);
   }
 }
 
 __global__ void gen_batch_entries_kernel(const int32_t* __restrict__ H, const int32_t* __restrict__ R,
                                          const int32_t* __restrict__ T, int64_t m, int64_t N,
-                                         int64_t Rn, uint32_t invalid, bool with_rel,
+                                         int64_t Rn, bool with_rel,
                                          uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    emit_row(key, val, 3 * i, 0u, H[i], T[i], R[i], static_cast<uint32_t>(i), N, Rn, invalid, with_rel);
+    emit_row(key, val, 3 * i, 0u, H[i], T[i], R[i], static_cast<uint32_t>(i), N, Rn, with_rel);
 }
 
 __global__ void seg_flag_kernel(const uint32_t* __restrict__ key, int64_t E, uint32_t invalid,
@@ -87,7 +93,7 @@ __global__ void seg_fill_kernel(const uint32_t* __restrict__ key, const uint32_t
       const uint32_t sidx = segid[e];
       seg_start[sidx] = static_cast<uint32_t>(e);
       const int64_t cp = k & cmask;
-      seg_col[sidx] = static_cast<uint32_t>(cp < Rn ? N + cp : cp - Rn);
+      seg_col[sidx] = cp == N + Rn ? kDummyCol : static_cast<uint32_t>(cp < Rn ? N + cp : cp - Rn);
       const uint32_t b = k >> cb;
       if (e == 0 || (key[e - 1] >> cb) != b) seg_base[b] = sidx;
     }
@@ -103,8 +109,13 @@ int grid_for(int64_t n) {
   return static_cast<int>(b < 1 ? 1 : (b > 8192 ? 8192 : b));
 }
 
-void finish_plan(EpochPlan& p, uint32_t invalid, int64_t N, int64_t Rn, cudaStream_t s) {
-  const bool alt = radix_sort_pairs(p.key, p.val, p.key_alt, p.val_alt, p.E, p.kb + p.cb + 1, p.sort, s);
+// seg_items: entries per batch when every batch starts on a sort block
+// boundary (the sort then orders columns inside each batch only), else 0.
+void finish_plan(EpochPlan& p, int64_t seg_items, int64_t N, int64_t Rn, cudaStream_t s) {
+  const uint32_t invalid = 0xFFFFFFFFu;  // never a key (keys use <= 31 bits)
+  const bool seg = seg_items > 0 && p.nb > 1 && radix_segment_ok(seg_items);
+  const bool alt = radix_sort_pairs(p.key, p.val, p.key_alt, p.val_alt, p.E, seg ? p.cb : p.kb + p.cb, p.sort, s,
+                                    seg ? seg_items : 0);
   const uint32_t* k = alt ? p.key_alt : p.key;
   p.sorted_val = alt ? p.val_alt : p.val;
   // the unsorted pair of buffers is free now: flags and segment ids live there
@@ -168,15 +179,14 @@ void build_epoch_plan(const int32_t* order, const int32_t* H, const int32_t* R, 
   p.nb = (M + B - 1) / B;
   p.E = 6 * M;
   p.kb = bits_for(static_cast<uint64_t>(p.nb - 1));
-  p.cb = bits_for(static_cast<uint64_t>(N + Rn - 1));
-  if (p.kb + p.cb + 1 > 32) throw CudaError("epoch plan: batches x columns exceed the 31-bit key space");
+  p.cb = bits_for(static_cast<uint64_t>(N + Rn));  // + the dummy column N + Rn
+  if (p.kb + p.cb > 31) throw CudaError("epoch plan: batches x columns exceed the 31-bit key space");
   p.reserve(p.E, p.nb);
-  const uint32_t invalid = 1u << (p.kb + p.cb);
-  gen_train_entries_kernel<<<grid_for(2 * M), 256, 0, s>>>(order, H, R, T, NH, NT, M, B, N, Rn, p.cb,
-                                                           invalid, p.key, p.val, p.pair_ht, p.pair_r);
+  gen_train_entries_kernel<<<grid_for(2 * M), 256, 0, s>>>(order, H, R, T, NH, NT, M, B, N, Rn, p.cb, p.key,
+                                                           p.val, p.pair_ht, p.pair_r);
   count_launch();
   SKG_LAUNCH_CHECK();
-  finish_plan(p, invalid, N, Rn, s);
+  finish_plan(p, 6 * B, N, Rn, s);
 }
 
 void build_batch_plan(const int32_t* H, const int32_t* R, const int32_t* T, int64_t m, int64_t N,
@@ -184,14 +194,12 @@ void build_batch_plan(const int32_t* H, const int32_t* R, const int32_t* T, int6
   p.nb = 1;
   p.E = 3 * m;
   p.kb = 0;
-  p.cb = bits_for(static_cast<uint64_t>(N + Rn - 1));
+  p.cb = bits_for(static_cast<uint64_t>(N + Rn));
   p.reserve(p.E, 1);
-  const uint32_t invalid = 1u << p.cb;
-  gen_batch_entries_kernel<<<grid_for(m), 256, 0, s>>>(H, R, T, m, N, Rn, invalid, layout == 1, p.key,
-                                                       p.val);
+  gen_batch_entries_kernel<<<grid_for(m), 256, 0, s>>>(H, R, T, m, N, Rn, layout == 1, p.key, p.val);
   count_launch();
   SKG_LAUNCH_CHECK();
-  finish_plan(p, invalid, N, Rn, s);
+  finish_plan(p, 0, N, Rn, s);
 }
 
 }  // namespace skg

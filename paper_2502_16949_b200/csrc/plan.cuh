@@ -18,6 +18,9 @@
 
 namespace skg {
 
+// seg_col of the per-batch dummy segment (entries that do not exist); skipped.
+constexpr uint32_t kDummyCol = 0xFFFFFFFFu;
+
 struct EpochPlan {
   int64_t cap_entries = 0, cap_batches = 0;
   int64_t E = 0, nb = 0;

@@ -1,9 +1,10 @@
 // Exclusive scan and stable LSD radix sort (see primitives.cuh).
 //
-// Radix sort layout: each warp owns a contiguous "subtile" of kSubItems
-// entries and processes it strictly in order, 32 entries at a time, ranking
-// equal digits with __match_any_sync. Per-(digit, subtile) counts are laid out
-// digit-major so one exclusive scan yields every subtile's output base.
+// Radix sort layout: a block owns kSortWarps consecutive "subtiles" of
+// kSubItems entries; each warp ranks its subtile strictly in order, 32 entries
+// at a time, matching equal digits with per-bit ballots. Per-(digit, block) counts are laid out
+// digit-major so one exclusive scan yields every block's output base per digit.
+#include <algorithm>
 #include <atomic>
 
 #include "common.cuh"
@@ -106,62 +107,173 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const uint32_t*
     *total = (offs ? offs[blockIdx.x] : 0u) + btotal;
 }
 
-__global__ void __launch_bounds__(kSortWarps * 32)
-    radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift, int bits,
-                      uint32_t* __restrict__ counts, int64_t nsub) {
-  __shared__ uint32_t hist[kSortWarps][1 << kMaxBits];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t sub = static_cast<int64_t>(blockIdx.x) * kSortWarps + warp;
-  const int nd = 1 << bits;
-  const uint32_t mask = nd - 1;
-  for (int d = lane; d < nd; d += 32) hist[warp][d] = 0;
-  __syncwarp();
-  if (sub < nsub) {
-    const int64_t base = sub * kSubItems;
-#pragma unroll 4
-    for (int c = 0; c < kSubChunks; ++c) {
-      const int64_t e = base + c * 32 + lane;
-      if (e < n) atomicAdd(&hist[warp][(keys[e] >> shift) & mask], 1u);
-    }
-    __syncwarp();
-    for (int d = lane; d < nd; d += 32) counts[static_cast<int64_t>(d) * nsub + sub] = hist[warp][d];
+// Radix pass over blocks of kSortWarps subtiles (8192 entries). The hist
+// kernel counts each block's digits (counts laid out digit-major over blocks,
+// so one exclusive scan gives every block's first output slot per digit). The
+// scatter kernel ranks the block stably (warps own consecutive subtiles,
+// chunks in order, lanes in order), stages keys/values in shared memory in
+// sorted order and writes each digit's run contiguously (coalesced stores).
+constexpr int kBlockItems = kSortWarps * kSubItems;
+
+// Lanes of `active` whose digit equals this lane's d (bits-wide): one ballot
+// per digit bit, cheaper than MATCH.ANY for <= 8-bit digits.
+__device__ __forceinline__ unsigned match_digit(unsigned active, uint32_t d, int bits) {
+  unsigned m = active;
+#pragma unroll
+  for (int b = 0; b < kMaxBits; ++b) {
+    if (b >= bits) break;
+    const bool on = (d >> b) & 1u;
+    const unsigned x = __ballot_sync(kFull, on);
+    m &= on ? x : ~x;
+  }
+  return m;
+}
+
+// Digit-count slot of block blk: segment-major, then digit, then block within
+// the segment (bpb blocks per segment; bpb = all blocks when unsegmented).
+__device__ __forceinline__ int64_t count_slot(int64_t blk, int64_t bpb, int nd, int d) {
+  return ((blk / bpb) * nd + d) * bpb + (blk % bpb);
+}
+
+__device__ __forceinline__ void load_subtile(const uint32_t* __restrict__ src, int64_t base, int64_t n, int lane,
+                                             uint32_t* r) {
+#pragma unroll
+  for (int c = 0; c < kSubChunks; ++c) {
+    const int64_t e = base + c * 32 + lane;
+    r[c] = e < n ? __ldg(src + e) : 0u;
+  }
+}
+
+// Per-warp digit counts of the warp's subtile into h[digit] (zeroed by the caller).
+__device__ __forceinline__ void count_subtile(const uint32_t* k, int64_t base, int64_t n, int lane, int shift,
+                                              int bits, uint32_t* h) {
+  const uint32_t mask = (1u << bits) - 1u;
+#pragma unroll
+  for (int c = 0; c < kSubChunks; ++c) {
+    const bool valid = base + c * 32 + lane < n;
+    const unsigned active = __ballot_sync(kFull, valid);
+    const uint32_t d = (k[c] >> shift) & mask;
+    const unsigned peers = match_digit(active, d, bits);
+    if (valid && lane == __ffs(peers) - 1) atomicAdd(&h[d], static_cast<uint32_t>(__popc(peers)));
   }
 }
 
 __global__ void __launch_bounds__(kSortWarps * 32)
-    radix_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                         uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n,
-                         int shift, int bits, const uint32_t* __restrict__ offsets, int64_t nsub) {
-  __shared__ uint32_t run[kSortWarps][1 << kMaxBits];
+    radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift, int bits,
+                      uint32_t* __restrict__ counts, int64_t bpb) {
+  __shared__ uint32_t hist[kSortWarps][1 << kMaxBits];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t sub = static_cast<int64_t>(blockIdx.x) * kSortWarps + warp;
-  if (sub >= nsub) return;
   const int nd = 1 << bits;
   const uint32_t mask = nd - 1;
-  for (int d = lane; d < nd; d += 32) run[warp][d] = offsets[static_cast<int64_t>(d) * nsub + sub];
-  __syncwarp();
-  const unsigned lt = lanemask_lt();
-  const int64_t base = sub * kSubItems;
-  for (int c = 0; c < kSubChunks; ++c) {
-    const int64_t e = base + c * 32 + lane;
-    const bool valid = e < n;
-    const unsigned active = __ballot_sync(kFull, valid);
-    if (active == 0) break;
-    uint32_t key = 0, val = 0, d = 0, peers = 0;
-    if (valid) {
-      key = kin[e];
-      val = vin[e];
-      d = (key >> shift) & mask;
-      peers = __match_any_sync(active, d);
-      const uint32_t pos = run[warp][d] + __popc(peers & lt);
-      kout[pos] = key;
-      vout[pos] = val;
-    }
-    __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) run[warp][d] += __popc(peers);
-    __syncwarp();
+  for (int d = threadIdx.x; d < kSortWarps * (1 << kMaxBits); d += blockDim.x) (&hist[0][0])[d] = 0;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlockItems + static_cast<int64_t>(warp) * kSubItems;
+  uint32_t k[kSubChunks];
+  load_subtile(keys, base, n, lane, k);
+  count_subtile(k, base, n, lane, shift, bits, hist[warp]);
+  __syncthreads();
+  for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) t += hist[w][d];
+    counts[count_slot(blockIdx.x, bpb, nd, d)] = t;
   }
 }
+
+__global__ void __launch_bounds__(kSortWarps * 32, 2)
+    radix_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                         uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n,
+                         int shift, int bits, const uint32_t* __restrict__ offsets, int64_t bpb) {
+  extern __shared__ uint32_t sm_sort[];
+  uint32_t* sk = sm_sort;           // [kBlockItems]
+  uint32_t* sv = sk + kBlockItems;  // [kBlockItems]
+  uint32_t* run = sv + kBlockItems;  // [kSortWarps][256]
+  uint32_t* lstart = run + kSortWarps * (1 << kMaxBits);
+  uint32_t* gbase = lstart + (1 << kMaxBits);
+  __shared__ uint32_t wtot[kSortWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nd = 1 << bits;
+  const uint32_t mask = nd - 1;
+  const int64_t bbase = static_cast<int64_t>(blockIdx.x) * kBlockItems;
+  const int64_t base = bbase + static_cast<int64_t>(warp) * kSubItems;
+  const int bn = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(kBlockItems), n - bbase)));
+  uint32_t k[kSubChunks], v[kSubChunks];
+  load_subtile(kin, base, n, lane, k);
+  load_subtile(vin, base, n, lane, v);
+  for (int d = threadIdx.x; d < kSortWarps * (1 << kMaxBits); d += blockDim.x) run[d] = 0;
+  __syncthreads();
+  count_subtile(k, base, n, lane, shift, bits, run + warp * (1 << kMaxBits));
+  __syncthreads();
+  {  // thread d: block count of digit d, exclusive scan over digits, per-warp bases
+    const int d = threadIdx.x;  // blockDim == 256 == max digits
+    uint32_t c = 0;
+    if (d < nd)
+#pragma unroll
+      for (int w = 0; w < kSortWarps; ++w) c += run[w * (1 << kMaxBits) + d];
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wtot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t t = lane < kSortWarps ? wtot[lane] : 0u;
+      uint32_t sc = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, sc, o);
+        if (lane >= o) sc += y;
+      }
+      if (lane < kSortWarps) wtot[lane] = sc - t;
+    }
+    __syncthreads();
+    if (d < nd) {
+      const uint32_t ls = wtot[warp] + x - c;
+      lstart[d] = ls;
+      gbase[d] = offsets[count_slot(blockIdx.x, bpb, nd, d)];
+      uint32_t r = ls;
+#pragma unroll
+      for (int w = 0; w < kSortWarps; ++w) {
+        const uint32_t cw = run[w * (1 << kMaxBits) + d];
+        run[w * (1 << kMaxBits) + d] = r;
+        r += cw;
+      }
+    }
+  }
+  __syncthreads();
+  // stable ranking of this warp's subtile into the block's sorted staging
+  uint32_t* wrun = run + warp * (1 << kMaxBits);
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int c = 0; c < kSubChunks; ++c) {
+    const bool valid = base + c * 32 + lane < n;
+    const unsigned active = __ballot_sync(kFull, valid);
+    const uint32_t d = (k[c] >> shift) & mask;
+    const unsigned peers = match_digit(active, d, bits);
+    if (valid) {
+      const uint32_t pos = wrun[d] + __popc(peers & lt);
+      sk[pos] = k[c];
+      sv[pos] = v[c];
+    }
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wrun[d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // coalesced write-out: entry j of the sorted block -> gbase[d] + (j - lstart[d])
+  for (int j = threadIdx.x; j < bn; j += blockDim.x) {
+    const uint32_t key = sk[j];
+    const uint32_t d = (key >> shift) & mask;
+    const uint32_t pos = gbase[d] + (static_cast<uint32_t>(j) - lstart[d]);
+    kout[pos] = key;
+    vout[pos] = sv[j];
+  }
+}
+
+constexpr size_t kScatterSmem =
+    sizeof(uint32_t) * (2 * kBlockItems + kSortWarps * (1 << kMaxBits) + 2 * (1 << kMaxBits));
 
 }  // namespace
 
@@ -222,8 +334,9 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* 
 }
 
 void SortPlan::reserve(int64_t n) {
-  const int64_t nsub = (n + kSubItems - 1) / kSubItems;
-  const int64_t need = nsub * (1 << kMaxBits);
+  // segmented sorts pad the last segment with empty blocks: at most 2x blocks
+  const int64_t nblk = 2 * ((n + kBlockItems - 1) / kBlockItems);
+  const int64_t need = nblk * (1 << kMaxBits);
   if (need > counts_cap) {
     if (counts) cudaFree(counts);
     SKG_CUDA(cudaMalloc(&counts, sizeof(uint32_t) * need));
@@ -239,24 +352,32 @@ void SortPlan::release() {
   scan.release();
 }
 
+bool radix_segment_ok(int64_t seg_items) { return seg_items > 0 && seg_items % kBlockItems == 0; }
+
 bool radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                      int64_t n, int key_bits, SortPlan& plan, cudaStream_t s) {
+                      int64_t n, int key_bits, SortPlan& plan, cudaStream_t s, int64_t seg_items) {
   if (n <= 1 || key_bits <= 0) return false;
-  plan.reserve(n);
+  static bool configured = false;
+  if (!configured) {
+    SKG_CUDA(cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kScatterSmem)));
+    configured = true;
+  }
+  const int64_t nblk = (n + kBlockItems - 1) / kBlockItems;
+  const int64_t bpb = radix_segment_ok(seg_items) ? std::min<int64_t>(seg_items / kBlockItems, nblk) : nblk;
+  const int64_t slots = (nblk + bpb - 1) / bpb * bpb;  // blocks incl. the last segment's empty tail
+  plan.reserve(n);  // no-op once the owner reserved (graph capture forbids allocation)
   const int passes = (key_bits + kMaxBits - 1) / kMaxBits;
-  const int64_t nsub = (n + kSubItems - 1) / kSubItems;
-  const int blocks = ceil_div(nsub, kSortWarps);
   uint32_t *kin = keys, *vin = vals, *kout = keys_alt, *vout = vals_alt;
   int shift = 0;
   for (int p = 0; p < passes; ++p) {
     const int bits = (key_bits - shift + (passes - p) - 1) / (passes - p);
-    radix_hist_kernel<<<blocks, kSortWarps * 32, 0, s>>>(kin, n, shift, bits, plan.counts, nsub);
+    radix_hist_kernel<<<static_cast<unsigned>(slots), kSortWarps * 32, 0, s>>>(kin, n, shift, bits, plan.counts, bpb);
     count_launch();
     SKG_LAUNCH_CHECK();
-    const int64_t nc = nsub << bits;
-    exclusive_scan_u32(plan.counts, plan.counts, nc, nullptr, plan.scan, s);
-    radix_scatter_kernel<<<blocks, kSortWarps * 32, 0, s>>>(kin, vin, kout, vout, n, shift, bits,
-                                                           plan.counts, nsub);
+    exclusive_scan_u32(plan.counts, plan.counts, slots << bits, nullptr, plan.scan, s);
+    radix_scatter_kernel<<<static_cast<unsigned>(nblk), kSortWarps * 32, kScatterSmem, s>>>(
+        kin, vin, kout, vout, n, shift, bits, plan.counts, bpb);
     count_launch();
     SKG_LAUNCH_CHECK();
     shift += bits;

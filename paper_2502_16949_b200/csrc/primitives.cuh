@@ -36,8 +36,12 @@ struct SortPlan {
   void release();
   ~SortPlan() { release(); }
 };
+// seg_items > 0 (a multiple of the sort block, see radix_segment_ok): the
+// input is a sequence of seg_items-long segments that must keep their order;
+// only the low key_bits are sorted, stably, inside each segment.
 bool radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                      int64_t n, int key_bits, SortPlan& plan, cudaStream_t s);
+                      int64_t n, int key_bits, SortPlan& plan, cudaStream_t s, int64_t seg_items = 0);
+bool radix_segment_ok(int64_t seg_items);
 
 // Number of kernel launches the last radix_sort_pairs / exclusive_scan_u32 issued
 // on this thread (for the launch accounting bench.py reports).

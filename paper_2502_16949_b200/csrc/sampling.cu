@@ -1,8 +1,7 @@
 // Device replicas of the reference random streams (see sampling.cuh).
 //
-// MT19937-64: one CTA twists the 312-word state in two dependent halves per
-// block (k < 156 reads only old words; k >= 156 reads new word k-156), double
-// buffered in shared memory, and writes the tempered words in order.
+// MT19937-64: 156 threads keep the 312-word state in registers (two words
+// each) and advance it one full state per block barrier (see mt_kernel).
 //
 // std::shuffle (libstdc++ stl_algo.h): Fisher-Yates i = 1..n-1, swap(a[i],
 // a[j_i]) with j_i uniform in [0, i]; after an optional leading coin call (n
@@ -46,26 +45,51 @@ __device__ void mt_seed(uint64_t seed, uint64_t* x) {
   for (int i = 1; i < kMtN; ++i) x[i] = 6364136223846793005ULL * (x[i - 1] ^ (x[i - 1] >> 62)) + i;
 }
 
-__global__ void __launch_bounds__(320) mt_kernel(const uint64_t* __restrict__ seed_ptr,
-                                                 uint64_t seed_val, uint64_t* __restrict__ out,
-                                                 int64_t n) {
-  __shared__ uint64_t buf[2][kMtN];
-  const uint64_t seed = seed_ptr ? *seed_ptr : seed_val;
-  if (threadIdx.x == 0) mt_seed(seed, buf[0]);
-  __syncthreads();
+// Register-resident twist: thread i (< 156) keeps a_i = x[i] and b_i =
+// x[156 + i] of the current state. The next state is
+//   a'_i = b_i ^ mix(a_i, a_{i+1})            (a_156 := b_0)
+//   b'_i = a'_i ^ mix(b_i, b_{i+1})           (i < 155)
+//   b'_155 = a'_155 ^ mix(b_155, a'_0)
+// so one state needs only the neighbours' previous words: every thread
+// publishes (a_i, b_i) to a double-buffered shared array, one barrier per
+// state, and thread 155 recomputes a'_0 itself. Tempering and the coalesced
+// stores of both halves are off the dependency chain.
+constexpr int kMtThreads = 160;
+
+__global__ void __launch_bounds__(kMtThreads) mt_kernel(const uint64_t* __restrict__ seed_ptr,
+                                                        uint64_t seed_val, uint64_t* __restrict__ out,
+                                                        int64_t n) {
+  __shared__ uint64_t sa[2][kMtM + 1], sb[2][kMtM + 1];
+  __shared__ uint64_t init[kMtN];
   const int i = threadIdx.x;
+  if (i == 0) mt_seed(seed_ptr ? *seed_ptr : seed_val, init);
+  __syncthreads();
+  const bool on = i < kMtM;
+  uint64_t a = on ? init[i] : 0ull, b = on ? init[kMtM + i] : 0ull;
+  const int64_t nstates = (n + kMtN - 1) / kMtN;
   int cur = 0;
-  for (int64_t base = 0; base < n; base += kMtN) {
-    const uint64_t* c = buf[cur];
-    uint64_t* x = buf[cur ^ 1];
-    if (i < kMtN - kMtM) x[i] = c[i + kMtM] ^ mt_mix(c[i], c[i + 1]);
+  for (int64_t s = 0; s < nstates; ++s) {
+    if (on) {
+      sa[cur][i] = a;
+      sb[cur][i] = b;
+    }
     __syncthreads();
-    if (i >= kMtN - kMtM && i < kMtN - 1)
-      x[i] = x[i - (kMtN - kMtM)] ^ mt_mix(c[i], c[i + 1]);
-    else if (i == kMtN - 1)
-      x[i] = x[kMtM - 1] ^ mt_mix(c[i], x[0]);
-    __syncthreads();
-    if (i < kMtN && base + i < n) out[base + i] = mt_temper(x[i]);
+    if (on) {
+      const uint64_t a1 = i + 1 < kMtM ? sa[cur][i + 1] : sb[cur][0];
+      const uint64_t na = b ^ mt_mix(a, a1);
+      uint64_t nb;
+      if (i + 1 < kMtM) {
+        nb = na ^ mt_mix(b, sb[cur][i + 1]);
+      } else {  // b'_155 needs a'_0 = b_0 ^ mix(a_0, a_1)
+        const uint64_t na0 = sb[cur][0] ^ mt_mix(sa[cur][0], sa[cur][1]);
+        nb = na ^ mt_mix(b, na0);
+      }
+      a = na;
+      b = nb;
+      const int64_t base = s * kMtN;
+      if (base + i < n) out[base + i] = mt_temper(a);
+      if (base + kMtM + i < n) out[base + kMtM + i] = mt_temper(b);
+    }
     cur ^= 1;
   }
 }
@@ -394,7 +418,7 @@ int grid_for(int64_t n, int threads = 256) {
 }  // namespace
 
 void mt19937_64_generate(uint64_t seed, uint64_t* out, int64_t n, cudaStream_t s) {
-  mt_kernel<<<1, 320, 0, s>>>(nullptr, seed, out, n);
+  mt_kernel<<<1, kMtThreads, 0, s>>>(nullptr, seed, out, n);
   count_launch();
   SKG_LAUNCH_CHECK();
 }
@@ -442,7 +466,7 @@ void device_shuffle(const uint64_t* d_seed_eff, int64_t n, int32_t* order, Shuff
   const int64_t C = num_calls(n);
   const int64_t nraw = C + kShiftWindow + 64;
   shuffle_reset_kernel<<<1, 1, 0, s>>>(w.ncand, w.nshift);
-  mt_kernel<<<1, 320, 0, s>>>(d_seed_eff, 0, w.raw, nraw);
+  mt_kernel<<<1, kMtThreads, 0, s>>>(d_seed_eff, 0, w.raw, nraw);
   shuffle_candidates_kernel<<<grid_for(C), 256, 0, s>>>(w.raw, nraw, n, w.cand, w.ncand);
   shuffle_resolve_kernel<<<1, 1024, 0, s>>>(w.cand, w.ncand, w.shifts, w.nshift);
   shuffle_map_kernel<<<grid_for(C), 256, 0, s>>>(w.raw, n, w.shifts, w.nshift, w.jpos);
@@ -485,7 +509,7 @@ bool device_negative_sample(const int32_t* h, const int32_t* t, int64_t m, int64
   const int64_t nraw = 2 * m + 4096;
   SKG_CUDA(cudaMemsetAsync(w.first_reject, 0xFF, sizeof(uint32_t), s));
   SKG_CUDA(cudaMemsetAsync(w.first_reject + 1, 0, sizeof(uint32_t), s));
-  mt_kernel<<<1, 320, 0, s>>>(nullptr, seed, w.raw, nraw);
+  mt_kernel<<<1, kMtThreads, 0, s>>>(nullptr, seed, w.raw, nraw);
   neg_map_kernel<<<grid_for(m), 256, 0, s>>>(w.raw, h, t, m, n_ent, avoid ? 1 : 0, out_h, out_t,
                                              w.first_reject);
   neg_fixup_kernel<<<1, 1, 0, s>>>(w.raw, nraw, h, t, m, n_ent, avoid ? 1 : 0, out_h, out_t,

@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "ht.cuh"
+#include "plan.cuh"
 #include "primitives.cuh"
 #include "refmath.cuh"
 
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(kTilesThreads) transr_tiles_kernel(
   __syncthreads();
   for (uint32_t base = s0; base < s1 && !stop; base += kTilesThreads) {
     const uint32_t s = base + tid;
-    const bool rel = s < s1 && seg_col[s] >= static_cast<uint32_t>(N);
+    const bool rel = s < s1 && seg_col[s] >= static_cast<uint32_t>(N) && seg_col[s] != kDummyCol;
     uint32_t n = 0, units = 0;
     if (rel) {
       const uint32_t len = seg_start[s + 1] - seg_start[s];
