@@ -11,8 +11,8 @@
 //   du  = dz - dzw w          -> res_u rows (sorted entity segments, no atomics)
 //   sum dz, sum (dzw u + wu dz) -> one partial per tile (relation gradient and
 //                                  negated normal gradient, models.hpp:112)
-// A second kernel adds each relation's tile partials in tile order and applies
-// SGD; the normals are then renormalized (embedding.cpp:181-189). Compared with
+// The CTA that finishes a relation's last tile adds its tile partials in tile
+// order and applies SGD; the normals are then renormalized (embedding.cpp:181-189). Compared with
 // the row-wise path (ht.cu) no dz / nrm rows go through HBM and w_r, d_r are
 // not re-gathered per row. Dot products use a fixed warp tree (the reference
 // reduces them with Eigen's redux; TransH parity is tolerance-only).
@@ -42,8 +42,23 @@ struct TArgs {
   const uint32_t* tile_seg;
   const uint32_t* tile_p0;
   const uint32_t* tile_total;
-  float* partial;  // [tile][2][kD]
+  const uint32_t* seg_tiles;  // first tile of each relation segment
+  float* partial;             // [tile][2][kD]
+  uint32_t* rel_ticket;       // per relation segment: tiles finished (zeroed by the tile enumerator)
+  float* rel;                 // relation table (SGD)
+  const float* lr;
 };
+
+// Relation-segment ordinal of tile t.
+__device__ __forceinline__ uint32_t seg_of_tile(const TArgs& a, uint32_t t) {
+  uint32_t lo = 0, hi = a.tile_total[1];
+  while (lo + 1 < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a.seg_tiles[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
 
 __device__ __forceinline__ float4 f4sub(float4 a, float4 b) {
   return make_float4(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z), __fsub_rn(a.w, b.w));
@@ -76,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
   __shared__ float score[kRows];
   __shared__ float wloss[kThreads / 32];
   __shared__ float4 accs[2][kThreads / 32][32];
-  __shared__ bool last;
+  __shared__ bool last, rel_last;
   const FwdArgs& f = a.f;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool alive = f.err[0] == 0;
@@ -202,9 +217,31 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
 #pragma unroll
       for (int q = 0; q < kThreads / 32; ++q) s = f4add(s, accs[which][q][lane]);
       reinterpret_cast<float4*>(a.partial + (static_cast<size_t>(t) * 2 + which) * kD)[lane] = s;
+      __threadfence();
     }
     if (tid == 0)
       for (int q = 0; q < kPairs / kRowsPerWarp; ++q) lsum = __fadd_rn(lsum, wloss[q]);
+    __syncthreads();
+    // the CTA finishing a relation's last tile sums its tile partials in tile
+    // order and applies SGD to the relation row and the normal
+    // (grads.normals -= nrm, models.hpp:112; embedding.cpp:165-190)
+    const uint32_t k = seg_of_tile(a, t);
+    const uint32_t lo = a.seg_tiles[k], hi = a.seg_tiles[k + 1];
+    if (tid == 0) rel_last = atomicAdd(a.rel_ticket + k, 1u) == hi - lo - 1;
+    __syncthreads();
+    if (rel_last && tid < kD) {
+      __threadfence();
+      float gA = 0.f, gB = 0.f;
+      for (uint32_t q = lo; q < hi; ++q) {
+        gA = __fadd_rn(gA, __ldcg(a.partial + (static_cast<size_t>(q) * 2) * kD + tid));
+        gB = __fadd_rn(gB, __ldcg(a.partial + (static_cast<size_t>(q) * 2 + 1) * kD + tid));
+      }
+      const float step = *a.lr;
+      float* pr = a.rel + r * kD + tid;
+      float* pn = const_cast<float*>(f.normals) + r * kD + tid;
+      *pr = __fsub_rn(*pr, __fmul_rn(step, gA));
+      *pn = __fsub_rn(*pn, __fmul_rn(step, -gB));
+    }
     __syncthreads();  // rows / score / accs reuse by the next tile
   }
   pend = __reduce_or_sync(kFull, pend);
@@ -243,39 +280,13 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
   }
 }
 
-// Per relation segment k: tile partials in tile order, then SGD on the relation
-// row and the normal (grads.normals -= nrm, models.hpp:112).
-__global__ void transh_rel_apply_kernel(const uint32_t* __restrict__ tile_total, const uint32_t* __restrict__ seg_tiles,
-                                        const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ seg_col,
-                                        int64_t N, const float* __restrict__ partial, float* __restrict__ rel,
-                                        float* __restrict__ normals, const float* __restrict__ lr,
-                                        const uint32_t* __restrict__ err) {
-  if (err[0] != 0) return;
-  const uint32_t k = blockIdx.x;
-  if (k >= tile_total[1]) return;
-  const uint32_t lo = seg_tiles[k], hi = seg_tiles[k + 1];
-  if (hi <= lo) return;
-  const int64_t r = static_cast<int64_t>(seg_col[tile_seg[lo]]) - N;
-  const int c = threadIdx.x;
-  float gA = 0.f, gB = 0.f;
-  for (uint32_t q = lo; q < hi; ++q) {
-    gA = __fadd_rn(gA, partial[(static_cast<size_t>(q) * 2) * kD + c]);
-    gB = __fadd_rn(gB, partial[(static_cast<size_t>(q) * 2 + 1) * kD + c]);
-  }
-  const float step = *lr;
-  float* pr = rel + r * kD + c;
-  float* pn = normals + r * kD + c;
-  *pr = __fsub_rn(*pr, __fmul_rn(step, gA));
-  *pn = __fsub_rn(*pn, __fmul_rn(step, -gB));
-}
-
 }  // namespace
 
 bool transh_tiles_supported(int de, int dr) { return de == kD && dr == kD; }
 
 int64_t transh_tiles_work_floats(int64_t rows, int64_t R) {
   const int64_t mt = relation_max_tiles(rows, R);
-  return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + mt * 2 * kD + 64;
+  return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + mt * 2 * kD + R + 64;
 }
 
 void configure_transh_tiles_kernels() {
@@ -292,7 +303,8 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   uint32_t* tile_total = tile_p0 + mt;
   uint32_t* seg_tiles = tile_total + 2;
   float* partial = work + ((3 * mt + 2 * R + 8 + 31) / 32) * 32;
-  launch_relation_tiles(ba, 1, tile_seg, tile_p0, tile_total, seg_tiles, s);
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(partial + mt * 2 * kD);
+  launch_relation_tiles(ba, 1, tile_seg, tile_p0, tile_total, seg_tiles, s, ticket, static_cast<int>(R + 1));
   TArgs a{};
   a.f = fa;
   a.ent_val = ba.ent_val;
@@ -301,7 +313,11 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   a.tile_seg = tile_seg;
   a.tile_p0 = tile_p0;
   a.tile_total = tile_total;
+  a.seg_tiles = seg_tiles;
   a.partial = partial;
+  a.rel_ticket = ticket;
+  a.rel = const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
+  a.lr = ba.lr;
   const size_t smem = sizeof(float) * kRows * kStride;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, static_cast<int64_t>(num_sms) * 16));
   if (l2) transh_tile_kernel<true><<<grid, kThreads, smem, s>>>(a);
@@ -312,12 +328,6 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   BwdArgs eb = ba;
   eb.entity_only = 1;
   launch_segment_backward(kPlainRows, true, eb, num_sms, s);
-  float* rel = const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
-  float* normals = const_cast<float*>(fa.normals);
-  transh_rel_apply_kernel<<<static_cast<unsigned>(R), kD, 0, s>>>(tile_total, seg_tiles, tile_seg, ba.seg_col, ba.N,
-                                                                  partial, rel, normals, ba.lr, ba.err);
-  count_launch();
-  SKG_LAUNCH_CHECK();
 }
 
 }  // namespace skg

@@ -60,8 +60,10 @@ constexpr int kTilesThreads = 1024;
 __global__ void __launch_bounds__(kTilesThreads) transr_tiles_kernel(
     const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ seg_col, const uint32_t* __restrict__ seg_base,
     int batch, int64_t N, int paired, uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_p0,
-    uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles, const uint32_t* __restrict__ err) {
+    uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles, const uint32_t* __restrict__ err,
+    uint32_t* __restrict__ zero = nullptr, int nzero = 0) {
   __shared__ uint32_t wsum[kTilesThreads / 32];
+  for (int i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0u;  // per-relation tickets of the next kernel
   __shared__ uint32_t carry_t, nrel;
   __shared__ int stop;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -501,9 +503,9 @@ void configure_one() {
 int64_t relation_max_tiles(int64_t rows, int64_t R) { return max_tiles(rows, R); }
 
 void launch_relation_tiles(const BwdArgs& ba, int paired, uint32_t* tile_seg, uint32_t* tile_p0, uint32_t* tile_total,
-                           uint32_t* seg_tiles, cudaStream_t s) {
+                           uint32_t* seg_tiles, cudaStream_t s, uint32_t* zero, int nzero) {
   transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, paired,
-                                                  tile_seg, tile_p0, tile_total, seg_tiles, ba.err);
+                                                  tile_seg, tile_p0, tile_total, seg_tiles, ba.err, zero, nzero);
   count_launch();
   SKG_LAUNCH_CHECK();
 }
