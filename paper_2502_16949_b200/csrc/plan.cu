@@ -113,7 +113,7 @@ int grid_for(int64_t n) {
 // boundary (the sort then orders columns inside each batch only), else 0.
 void finish_plan(EpochPlan& p, int64_t seg_items, int64_t N, int64_t Rn, cudaStream_t s) {
   const uint32_t invalid = 0xFFFFFFFFu;  // never a key (keys use <= 31 bits)
-  const bool seg = seg_items > 0 && p.nb > 1 && radix_segment_ok(seg_items);
+  const bool seg = seg_items > 0 && p.nb > 1 && radix_segment_ok(seg_items, p.E);
   const bool alt = radix_sort_pairs(p.key, p.val, p.key_alt, p.val_alt, p.E, seg ? p.cb : p.kb + p.cb, p.sort, s,
                                     seg ? seg_items : 0);
   const uint32_t* k = alt ? p.key_alt : p.key;

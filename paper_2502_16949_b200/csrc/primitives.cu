@@ -20,8 +20,9 @@ constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 constexpr int kSortWarps = 8;
-constexpr int kSubChunks = 32;                 // 32 chunks of 32 entries
-constexpr int kSubItems = kSubChunks * 32;     // entries per warp subtile
+// Chunks of 32 entries per warp subtile: CH (template) in {1, ..., 32},
+// picked per sort so small sorts still spread over every SM.
+constexpr int kMaxChunks = 32;
 constexpr int kMaxBits = 8;
 
 __device__ __forceinline__ uint32_t block_exclusive_sum(uint32_t v, uint32_t* warp_tot,
@@ -113,7 +114,13 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const uint32_t*
 // scatter kernel ranks the block stably (warps own consecutive subtiles,
 // chunks in order, lanes in order), stages keys/values in shared memory in
 // sorted order and writes each digit's run contiguously (coalesced stores).
-constexpr int kBlockItems = kSortWarps * kSubItems;
+template <int CH>
+struct SortGeom {
+  static constexpr int kSubItems = CH * 32;
+  static constexpr int kBlockItems = kSortWarps * kSubItems;
+  static constexpr size_t kScatterSmem =
+      sizeof(uint32_t) * (2 * kBlockItems + kSortWarps * (1 << kMaxBits) + 2 * (1 << kMaxBits));
+};
 
 // Lanes of `active` whose digit equals this lane's d (bits-wide): one ballot
 // per digit bit, cheaper than MATCH.ANY for <= 8-bit digits.
@@ -135,21 +142,23 @@ __device__ __forceinline__ int64_t count_slot(int64_t blk, int64_t bpb, int nd, 
   return ((blk / bpb) * nd + d) * bpb + (blk % bpb);
 }
 
+template <int CH>
 __device__ __forceinline__ void load_subtile(const uint32_t* __restrict__ src, int64_t base, int64_t n, int lane,
                                              uint32_t* r) {
 #pragma unroll
-  for (int c = 0; c < kSubChunks; ++c) {
+  for (int c = 0; c < CH; ++c) {
     const int64_t e = base + c * 32 + lane;
     r[c] = e < n ? __ldg(src + e) : 0u;
   }
 }
 
 // Per-warp digit counts of the warp's subtile into h[digit] (zeroed by the caller).
+template <int CH>
 __device__ __forceinline__ void count_subtile(const uint32_t* k, int64_t base, int64_t n, int lane, int shift,
                                               int bits, uint32_t* h) {
   const uint32_t mask = (1u << bits) - 1u;
 #pragma unroll
-  for (int c = 0; c < kSubChunks; ++c) {
+  for (int c = 0; c < CH; ++c) {
     const bool valid = base + c * 32 + lane < n;
     const unsigned active = __ballot_sync(kFull, valid);
     const uint32_t d = (k[c] >> shift) & mask;
@@ -158,6 +167,7 @@ __device__ __forceinline__ void count_subtile(const uint32_t* k, int64_t base, i
   }
 }
 
+template <int CH>
 __global__ void __launch_bounds__(kSortWarps * 32)
     radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift, int bits,
                       uint32_t* __restrict__ counts, int64_t bpb) {
@@ -167,10 +177,11 @@ __global__ void __launch_bounds__(kSortWarps * 32)
   const uint32_t mask = nd - 1;
   for (int d = threadIdx.x; d < kSortWarps * (1 << kMaxBits); d += blockDim.x) (&hist[0][0])[d] = 0;
   __syncthreads();
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kBlockItems + static_cast<int64_t>(warp) * kSubItems;
-  uint32_t k[kSubChunks];
-  load_subtile(keys, base, n, lane, k);
-  count_subtile(k, base, n, lane, shift, bits, hist[warp]);
+  using G = SortGeom<CH>;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * G::kBlockItems + static_cast<int64_t>(warp) * G::kSubItems;
+  uint32_t k[CH];
+  load_subtile<CH>(keys, base, n, lane, k);
+  count_subtile<CH>(k, base, n, lane, shift, bits, hist[warp]);
   __syncthreads();
   for (int d = threadIdx.x; d < nd; d += blockDim.x) {
     uint32_t t = 0;
@@ -180,10 +191,13 @@ __global__ void __launch_bounds__(kSortWarps * 32)
   }
 }
 
+template <int CH>
 __global__ void __launch_bounds__(kSortWarps * 32, 2)
     radix_scatter_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                          uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n,
                          int shift, int bits, const uint32_t* __restrict__ offsets, int64_t bpb) {
+  using G = SortGeom<CH>;
+  constexpr int kBlockItems = G::kBlockItems;
   extern __shared__ uint32_t sm_sort[];
   uint32_t* sk = sm_sort;           // [kBlockItems]
   uint32_t* sv = sk + kBlockItems;  // [kBlockItems]
@@ -195,14 +209,14 @@ __global__ void __launch_bounds__(kSortWarps * 32, 2)
   const int nd = 1 << bits;
   const uint32_t mask = nd - 1;
   const int64_t bbase = static_cast<int64_t>(blockIdx.x) * kBlockItems;
-  const int64_t base = bbase + static_cast<int64_t>(warp) * kSubItems;
+  const int64_t base = bbase + static_cast<int64_t>(warp) * G::kSubItems;
   const int bn = static_cast<int>(max(static_cast<int64_t>(0), min(static_cast<int64_t>(kBlockItems), n - bbase)));
-  uint32_t k[kSubChunks], v[kSubChunks];
-  load_subtile(kin, base, n, lane, k);
-  load_subtile(vin, base, n, lane, v);
+  uint32_t k[CH], v[CH];
+  load_subtile<CH>(kin, base, n, lane, k);
+  load_subtile<CH>(vin, base, n, lane, v);
   for (int d = threadIdx.x; d < kSortWarps * (1 << kMaxBits); d += blockDim.x) run[d] = 0;
   __syncthreads();
-  count_subtile(k, base, n, lane, shift, bits, run + warp * (1 << kMaxBits));
+  count_subtile<CH>(k, base, n, lane, shift, bits, run + warp * (1 << kMaxBits));
   __syncthreads();
   {  // thread d: block count of digit d, exclusive scan over digits, per-warp bases
     const int d = threadIdx.x;  // blockDim == 256 == max digits
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(kSortWarps * 32, 2)
   uint32_t* wrun = run + warp * (1 << kMaxBits);
   const unsigned lt = lanemask_lt();
 #pragma unroll
-  for (int c = 0; c < kSubChunks; ++c) {
+  for (int c = 0; c < CH; ++c) {
     const bool valid = base + c * 32 + lane < n;
     const unsigned active = __ballot_sync(kFull, valid);
     const uint32_t d = (k[c] >> shift) & mask;
@@ -272,8 +286,12 @@ __global__ void __launch_bounds__(kSortWarps * 32, 2)
   }
 }
 
-constexpr size_t kScatterSmem =
-    sizeof(uint32_t) * (2 * kBlockItems + kSortWarps * (1 << kMaxBits) + 2 * (1 << kMaxBits));
+// Chunks per warp for an n-entry sort: about two blocks per SM, 1..32.
+int sort_chunks(int64_t n) {
+  int ch = 1;
+  while (ch < kMaxChunks && n / (static_cast<int64_t>(kSortWarps) * 32 * ch) > 2 * 148) ch <<= 1;
+  return ch;
+}
 
 }  // namespace
 
@@ -335,7 +353,8 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* 
 
 void SortPlan::reserve(int64_t n) {
   // segmented sorts pad the last segment with empty blocks: at most 2x blocks
-  const int64_t nblk = 2 * ((n + kBlockItems - 1) / kBlockItems);
+  const int64_t bi = static_cast<int64_t>(kSortWarps) * 32 * sort_chunks(n);
+  const int64_t nblk = 2 * ((n + bi - 1) / bi);
   const int64_t need = nblk * (1 << kMaxBits);
   if (need > counts_cap) {
     if (counts) cudaFree(counts);
@@ -352,31 +371,32 @@ void SortPlan::release() {
   scan.release();
 }
 
-bool radix_segment_ok(int64_t seg_items) { return seg_items > 0 && seg_items % kBlockItems == 0; }
-
-bool radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
-                      int64_t n, int key_bits, SortPlan& plan, cudaStream_t s, int64_t seg_items) {
-  if (n <= 1 || key_bits <= 0) return false;
+namespace {
+template <int CH>
+bool sort_t(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n, int key_bits,
+            SortPlan& plan, cudaStream_t s, int64_t seg_items) {
+  using G = SortGeom<CH>;
   static bool configured = false;
   if (!configured) {
-    SKG_CUDA(cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kScatterSmem)));
+    SKG_CUDA(cudaFuncSetAttribute(radix_scatter_kernel<CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(G::kScatterSmem)));
     configured = true;
   }
-  const int64_t nblk = (n + kBlockItems - 1) / kBlockItems;
-  const int64_t bpb = radix_segment_ok(seg_items) ? std::min<int64_t>(seg_items / kBlockItems, nblk) : nblk;
+  const int64_t nblk = (n + G::kBlockItems - 1) / G::kBlockItems;
+  const bool seg = seg_items > 0 && seg_items % G::kBlockItems == 0;
+  const int64_t bpb = seg ? std::min<int64_t>(seg_items / G::kBlockItems, nblk) : nblk;
   const int64_t slots = (nblk + bpb - 1) / bpb * bpb;  // blocks incl. the last segment's empty tail
-  plan.reserve(n);  // no-op once the owner reserved (graph capture forbids allocation)
   const int passes = (key_bits + kMaxBits - 1) / kMaxBits;
   uint32_t *kin = keys, *vin = vals, *kout = keys_alt, *vout = vals_alt;
   int shift = 0;
   for (int p = 0; p < passes; ++p) {
     const int bits = (key_bits - shift + (passes - p) - 1) / (passes - p);
-    radix_hist_kernel<<<static_cast<unsigned>(slots), kSortWarps * 32, 0, s>>>(kin, n, shift, bits, plan.counts, bpb);
+    radix_hist_kernel<CH><<<static_cast<unsigned>(slots), kSortWarps * 32, 0, s>>>(kin, n, shift, bits, plan.counts,
+                                                                                 bpb);
     count_launch();
     SKG_LAUNCH_CHECK();
     exclusive_scan_u32(plan.counts, plan.counts, slots << bits, nullptr, plan.scan, s);
-    radix_scatter_kernel<<<static_cast<unsigned>(nblk), kSortWarps * 32, kScatterSmem, s>>>(
+    radix_scatter_kernel<CH><<<static_cast<unsigned>(nblk), kSortWarps * 32, G::kScatterSmem, s>>>(
         kin, vin, kout, vout, n, shift, bits, plan.counts, bpb);
     count_launch();
     SKG_LAUNCH_CHECK();
@@ -385,6 +405,25 @@ bool radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32
     std::swap(vin, vout);
   }
   return kin == keys_alt;
+}
+}  // namespace
+
+bool radix_segment_ok(int64_t seg_items, int64_t n) {
+  return seg_items > 0 && seg_items % (static_cast<int64_t>(kSortWarps) * 32 * sort_chunks(n)) == 0;
+}
+
+bool radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
+                      int64_t n, int key_bits, SortPlan& plan, cudaStream_t s, int64_t seg_items) {
+  if (n <= 1 || key_bits <= 0) return false;
+  plan.reserve(n);  // no-op once the owner reserved (graph capture forbids allocation)
+  switch (sort_chunks(n)) {
+    case 1: return sort_t<1>(keys, vals, keys_alt, vals_alt, n, key_bits, plan, s, seg_items);
+    case 2: return sort_t<2>(keys, vals, keys_alt, vals_alt, n, key_bits, plan, s, seg_items);
+    case 4: return sort_t<4>(keys, vals, keys_alt, vals_alt, n, key_bits, plan, s, seg_items);
+    case 8: return sort_t<8>(keys, vals, keys_alt, vals_alt, n, key_bits, plan, s, seg_items);
+    case 16: return sort_t<16>(keys, vals, keys_alt, vals_alt, n, key_bits, plan, s, seg_items);
+    default: return sort_t<32>(keys, vals, keys_alt, vals_alt, n, key_bits, plan, s, seg_items);
+  }
 }
 
 }  // namespace skg

@@ -41,7 +41,7 @@ struct SortPlan {
 // only the low key_bits are sorted, stably, inside each segment.
 bool radix_sort_pairs(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
                       int64_t n, int key_bits, SortPlan& plan, cudaStream_t s, int64_t seg_items = 0);
-bool radix_segment_ok(int64_t seg_items);
+bool radix_segment_ok(int64_t seg_items, int64_t n);
 
 // Number of kernel launches the last radix_sort_pairs / exclusive_scan_u32 issued
 // on this thread (for the launch accounting bench.py reports).
