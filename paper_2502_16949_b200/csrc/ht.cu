@@ -502,7 +502,7 @@ void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work,
     transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R);
     return;
   }
-  if (transh_tiles_supported(fa.de, fa.dr)) {  // relation-tiled path (transh_train.cu)
+  if (transh_tiles_supported(fa.de, fa.dr, R)) {  // relation-tiled path (transh_train.cu)
     transh_tiles_train_batch(kind == kTransH_L2, fa, ba, work, R, num_sms, s, mark);
     normals_renorm_kernel<<<static_cast<unsigned>((R * 32 + 127) / 128), 128, 0, s>>>(const_cast<float*>(fa.normals), R,
                                                                                    fa.de, ba.err);

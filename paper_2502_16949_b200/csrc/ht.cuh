@@ -33,7 +33,7 @@ int64_t relation_max_tiles(int64_t rows, int64_t R);
 void launch_relation_tiles(const BwdArgs& ba, int paired, uint32_t* tile_seg, uint32_t* tile_p0, uint32_t* tile_total,
                            uint32_t* seg_tiles, cudaStream_t s, uint32_t* zero = nullptr, int nzero = 0);
 // TransH training on relation tiles (transh_train.cu), d_e = d_r = 128
-bool transh_tiles_supported(int de, int dr);
+bool transh_tiles_supported(int de, int dr, int64_t R);
 void configure_transh_tiles_kernels();
 int64_t transh_tiles_work_floats(int64_t rows, int64_t R);
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,

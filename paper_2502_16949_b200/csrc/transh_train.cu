@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "ht.cuh"
+#include "plan.cuh"
 #include "primitives.cuh"
 #include "refmath.cuh"
 
@@ -34,31 +35,21 @@ constexpr int kThreads = 512;      // 16 warps x 8 rows
 constexpr int kRowsPerWarp = 8;
 constexpr int kStride = kD + 4;    // staged v rows (16-byte aligned, conflict-free row reads)
 
+constexpr int kMaxRelSeg = 1024;  // relation segments per batch handled in shared memory
+
 struct TArgs {
   FwdArgs f;
   const uint32_t* ent_val;
   const uint32_t* seg_start;
   const uint32_t* seg_col;
-  const uint32_t* tile_seg;
-  const uint32_t* tile_p0;
-  const uint32_t* tile_total;
-  const uint32_t* seg_tiles;  // first tile of each relation segment
+  const uint32_t* seg_base;
+  int batch;
+  int64_t mt;                 // tile capacity of `partial`
   float* partial;             // [tile][2][kD]
   uint32_t* rel_ticket;       // per relation segment: tiles finished (zeroed by the tile enumerator)
   float* rel;                 // relation table (SGD)
   const float* lr;
 };
-
-// Relation-segment ordinal of tile t.
-__device__ __forceinline__ uint32_t seg_of_tile(const TArgs& a, uint32_t t) {
-  uint32_t lo = 0, hi = a.tile_total[1];
-  while (lo + 1 < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a.seg_tiles[mid] <= t) lo = mid;
-    else hi = mid;
-  }
-  return lo;
-}
 
 __device__ __forceinline__ float4 f4sub(float4 a, float4 b) {
   return make_float4(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z), __fsub_rn(a.w, b.w));
@@ -75,6 +66,7 @@ __device__ __forceinline__ float f4dot(float4 a, float4 b) {
   acc = fmaf(a.z, b.z, acc);
   return fmaf(a.w, b.w, acc);
 }
+
 template <bool L2>
 __device__ __forceinline__ float dirf(float v, float sc) {
   return L2 ? __fmul_rn(v, sc) : (v > 0.f ? sc : (v < 0.f ? -sc : 0.f));
@@ -83,6 +75,58 @@ template <bool L2>
 __device__ __forceinline__ float4 dir4(float4 v, float sc) {
   return make_float4(dirf<L2>(v.x, sc), dirf<L2>(v.y, sc), dirf<L2>(v.z, sc), dirf<L2>(v.w, sc));
 }
+
+// Relation tiles of the batch, enumerated by warp 0 of every CTA: the batch's
+// relation segments lead its segment list (relation column keys sort first);
+// first[k] = first tile of relation segment k, first[nrel] = tile count.
+struct RelTiles {
+  uint32_t first[kMaxRelSeg + 1];
+  uint32_t seg[kMaxRelSeg];
+  uint32_t nrel;
+};
+
+__device__ void enumerate_rel_tiles(const TArgs& a, RelTiles& rt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t s0 = a.seg_base[a.batch], s1 = a.seg_base[a.batch + 1];
+  uint32_t carry = 0, k0 = 0;
+  for (uint32_t base = s0; base < s1 && k0 < kMaxRelSeg; base += 32) {
+    const uint32_t s = base + lane;
+    const uint32_t col = s < s1 ? __ldg(a.seg_col + s) : kDummyCol;
+    const bool rel = col >= static_cast<uint32_t>(a.f.N) && col != kDummyCol;
+    uint32_t n = 0;
+    if (rel) n = ((__ldg(a.seg_start + s + 1) - __ldg(a.seg_start + s)) / 2 + kPairs - 1) / kPairs;
+    const unsigned m = __ballot_sync(kFull, rel);
+    const int nr = __popc(~m) == 0 ? 32 : __ffs(~m) - 1;  // relation segments form a prefix
+    uint32_t x = lane < nr ? n : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane < nr && k0 + lane < kMaxRelSeg) {
+      rt.first[k0 + lane] = carry + x - n;
+      rt.seg[k0 + lane] = s;
+    }
+    carry += __shfl_sync(kFull, x, 31);
+    k0 += static_cast<uint32_t>(nr);
+    if (nr < 32) break;
+  }
+  if (lane == 0) {
+    rt.nrel = min(k0, static_cast<uint32_t>(kMaxRelSeg));
+    rt.first[rt.nrel] = carry;
+  }
+}
+
+__device__ __forceinline__ uint32_t rel_of_tile(const RelTiles& rt, uint32_t t) {
+  uint32_t lo = 0, hi = rt.nrel;
+  while (lo + 1 < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (rt.first[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
 template <bool L2>
 __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a) {
   extern __shared__ float4 smv[];
@@ -92,14 +136,18 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
   __shared__ float wloss[kThreads / 32];
   __shared__ float4 accs[2][kThreads / 32][32];
   __shared__ bool last, rel_last;
+  __shared__ RelTiles rt;
   const FwdArgs& f = a.f;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool alive = f.err[0] == 0;
-  const uint32_t T = alive ? a.tile_total[0] : 0u;
+  if (warp == 0 && alive) enumerate_rel_tiles(a, rt);
+  __syncthreads();
+  const uint32_t T = alive ? static_cast<uint32_t>(min(static_cast<int64_t>(rt.first[rt.nrel]), a.mt)) : 0u;
   float lsum = 0.f;
   uint32_t pend = 0;
   for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
-    const uint32_t sseg = __ldg(a.tile_seg + t), p0 = __ldg(a.tile_p0 + t);
+    const uint32_t k = rel_of_tile(rt, t);
+    const uint32_t sseg = rt.seg[k], p0 = (t - rt.first[k]) * kPairs;
     const uint32_t e0 = __ldg(a.seg_start + sseg), len = __ldg(a.seg_start + sseg + 1) - e0;
     const int64_t r = static_cast<int64_t>(__ldg(a.seg_col + sseg)) - f.N;
     const int np = static_cast<int>(min(static_cast<uint32_t>(kPairs), len / 2 - p0));
@@ -225,9 +273,10 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
     // the CTA finishing a relation's last tile sums its tile partials in tile
     // order and applies SGD to the relation row and the normal
     // (grads.normals -= nrm, models.hpp:112; embedding.cpp:165-190)
-    const uint32_t k = seg_of_tile(a, t);
-    const uint32_t lo = a.seg_tiles[k], hi = a.seg_tiles[k + 1];
-    if (tid == 0) rel_last = atomicAdd(a.rel_ticket + k, 1u) == hi - lo - 1;
+    const uint32_t lo = rt.first[k], hi = rt.first[k + 1];
+    if (tid == 0) {
+      rel_last = atomicAdd(a.rel_ticket + k, 1u) == hi - lo - 1;
+    }
     __syncthreads();
     if (rel_last && tid < kD) {
       __threadfence();
@@ -282,11 +331,11 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
 
 }  // namespace
 
-bool transh_tiles_supported(int de, int dr) { return de == kD && dr == kD; }
+bool transh_tiles_supported(int de, int dr, int64_t R) { return de == kD && dr == kD && R <= kMaxRelSeg; }
 
 int64_t transh_tiles_work_floats(int64_t rows, int64_t R) {
   const int64_t mt = relation_max_tiles(rows, R);
-  return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + mt * 2 * kD + R + 64;
+  return mt * 2 * kD + R + 64;
 }
 
 void configure_transh_tiles_kernels() {
@@ -298,22 +347,18 @@ void configure_transh_tiles_kernels() {
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
                               cudaStream_t s, const std::function<void()>* mark) {
   const int64_t mt = relation_max_tiles(2 * static_cast<int64_t>(fa.B), R);
-  uint32_t* tile_seg = reinterpret_cast<uint32_t*>(work);
-  uint32_t* tile_p0 = tile_seg + mt;
-  uint32_t* tile_total = tile_p0 + mt;
-  uint32_t* seg_tiles = tile_total + 2;
-  float* partial = work + ((3 * mt + 2 * R + 8 + 31) / 32) * 32;
+  float* partial = work;
   uint32_t* ticket = reinterpret_cast<uint32_t*>(partial + mt * 2 * kD);
-  launch_relation_tiles(ba, 1, tile_seg, tile_p0, tile_total, seg_tiles, s, ticket, static_cast<int>(R + 1));
+  // per-relation tickets, zeroed for every batch (a memset node in the graph)
+  SKG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(uint32_t) * (R + 1), s));
   TArgs a{};
   a.f = fa;
   a.ent_val = ba.ent_val;
   a.seg_start = ba.seg_start;
   a.seg_col = ba.seg_col;
-  a.tile_seg = tile_seg;
-  a.tile_p0 = tile_p0;
-  a.tile_total = tile_total;
-  a.seg_tiles = seg_tiles;
+  a.seg_base = ba.seg_base;
+  a.batch = ba.batch;
+  a.mt = mt;
   a.partial = partial;
   a.rel_ticket = ticket;
   a.rel = const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
