@@ -51,6 +51,14 @@ METRIC = "train triplets/sec per model at 1/2/4/8 B200; SpMM fwd/bwd HBM GB/s vs
 SEED, LR, MARGIN = 1, 4e-4, 0.5
 
 
+def peak_tflops():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured"
+    except Exception:
+        return 2250.0, "fallback (nominal)"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -161,15 +169,27 @@ def algorithmic_bytes(cfg, eng, nb):
     forward: 3 gathered rows + 1 residual row written per incidence row (8B·d·4),
     plus ids (order + 5 ids per pair) and the per-row scale; backward: one residual
     row + value + scale per nonzero, and a read + write of every touched row."""
-    d = cfg["de"]
+    d, dr = cfg["de"], cfg["dr"]
     fwd = bwd = 0
     M = eng.m
     for b in range(nb):
         Bb = min(cfg["B"], M - b * cfg["B"])
         segs, entries, _ = eng.plan_stats(b)
-        fwd += 2 * Bb * 4 * d * 4 + Bb * 24 + 2 * Bb * 4
+        ids = Bb * 24 + 2 * Bb * 4
+        if cfg["model"] == "transh":    # SURVEY §8d: h, t, d_r, w_r gathers + du write per row
+            fwd += 10 * Bb * d * 4 + ids
+        elif cfg["model"] == "transr":  # (4B d_e + 2B d_r + 2B d_e + R d_r d_e) s
+            fwd += (4 * Bb * d + 2 * Bb * dr + 2 * Bb * d + cfg["R"] * dr * d) * 4 + ids
+        else:                           # TransE / TorusE: 3 gathers + 1 residual row per incidence row
+            fwd += 2 * Bb * 4 * d * 4 + ids
         bwd += entries * (d * 4 + 8) + segs * (2 * d * 4 + 12)
     return fwd, bwd
+
+
+def transr_flops(cfg, M):
+    """Algorithmic fp32 FLOPs of the three TransR products per epoch: V = U M^T, dU = DZ M,
+    dM = DZ^T U over 2 rows per pair, 2 d_r d_e each (196,608 per positive at d=128)."""
+    return 3 * 2 * (2 * M) * cfg["de"] * cfg["dr"]
 
 
 def cpu_reference(cfg, h, r, t, nh, nt, budget_s, threads):
@@ -313,6 +333,14 @@ def main():
     bwd_gbs = bwd_b / nb / (bwd_ms * 1e-3) / 1e9
     dom = "forward" if fwd_ms >= bwd_ms else "backward"
     ach = fwd_gbs if dom == "forward" else bwd_gbs
+    tensor = None
+    if cfg["model"] == "transr" and cfg["de"] == 128 and cfg["dr"] == 128 and dom == "forward":
+        # projection kernel on tcgen05 (3xTF32): fp32-class products at 1/3 of the dense TF32 rate;
+        # TF32 dense = measured bf16 dense / 2 (same tensor pipe, half the K per instruction)
+        bf16, bf16_kind = peak_tflops()
+        tpeak = bf16 / 2 / 3
+        tach = transr_flops(cfg, M) / nb / (fwd_ms * 1e-3) / 1e12
+        tensor = {"achieved": tach, "peak": tpeak, "peak_source": bf16_kind + " bf16 dense / 2 (tf32) / 3 (3xTF32)"}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
@@ -337,11 +365,18 @@ def main():
                            wall_s=round(wall, 4), final_loss=losses[-1]),
             "e2e": {"value": e2e, "unit": "triplets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "skg_set_triples + skg_set_negatives (pinned int64) + skg_train_epoch"},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "forward_gbs": fwd_gbs, "backward_gbs": bwd_gbs, "fwd_ms_per_batch": fwd_ms,
-                         "bwd_ms_per_batch": bwd_ms, "plan_ms_per_epoch": plan_ms,
-                         "note": "algorithmic bytes (no cache credit); C1-C4 tables are L2-resident"},
+            "roofline": ({"bound": "tensor", "kernel": dom, "achieved": tensor["achieved"], "peak": tensor["peak"],
+                          "unit": "TFLOP/s", "frac": tensor["achieved"] / tensor["peak"], "traffic": traffic,
+                          "peak_source": tensor["peak_source"], "hbm_gbs": ach, "hbm_frac": ach / peak,
+                          "forward_gbs": fwd_gbs, "backward_gbs": bwd_gbs, "fwd_ms_per_batch": fwd_ms,
+                          "bwd_ms_per_batch": bwd_ms, "plan_ms_per_epoch": plan_ms,
+                          "note": "algorithmic fp32 FLOPs of the three projections; 3xTF32 issues 3 tf32 MMAs each"}
+                         if tensor else
+                         {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                          "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
+                          "forward_gbs": fwd_gbs, "backward_gbs": bwd_gbs, "fwd_ms_per_batch": fwd_ms,
+                          "bwd_ms_per_batch": bwd_ms, "plan_ms_per_epoch": plan_ms,
+                          "note": "algorithmic bytes (no cache credit); C1-C4 tables are L2-resident"}),
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,
