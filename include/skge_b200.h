@@ -137,6 +137,16 @@ skg_status skg_score_backward(skg_ctx* ctx, const skg_model_config* cfg, int64_t
                               const int64_t* heads, const int64_t* relations,
                               const int64_t* tails, const float* upstream, float* g_entity,
                               float* g_relation, float* g_proj, float* g_normals);
+/* rank_entity (eval.cpp:16-63) of q queries on device, tail side then head side
+ * (the order evaluate() visits them, eval.cpp:80-86): ranks[2i] = tail rank,
+ * ranks[2i + 1] = head rank, rank = 1 + #{c != truth : energy(c) < energy(truth)}.
+ * protocol 1 (filtered) skips candidates whose triple is one of the nf filter
+ * triples (TripleFilter / build_filter, eval.hpp:25-48); 0 = raw. TransE and
+ * TorusE (bit-exact energies); other models return SKG_ERR_CONFIG. */
+skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cfg, int64_t q, const int64_t* heads,
+                             const int64_t* relations, const int64_t* tails, int32_t protocol, int64_t nf,
+                             const int64_t* filter_heads, const int64_t* filter_relations,
+                             const int64_t* filter_tails, int64_t* ranks);
 /* margin_ranking_loss, training.cpp:73-94 */
 skg_status skg_margin_ranking_loss(skg_ctx* ctx, int64_t m, const float* pos_energy,
                                    const float* neg_energy, float margin, float* loss,

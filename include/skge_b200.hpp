@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdint>
 #include <functional>
+#include <map>
 #include <memory>
 #include <optional>
 #include <random>
@@ -312,6 +313,97 @@ inline TrainingRun fit(const ModelConfig& mc, EmbeddingStore& store, const Tripl
     if (on_epoch) on_epoch(e);
   }
   return run;
+}
+
+// ---- link prediction (eval.hpp / eval.cpp) --------------------------------
+enum class Protocol { Raw, Filtered };
+enum class Side { Head, Tail };
+inline const char* protocol_name(Protocol p) { return p == Protocol::Raw ? "raw" : "filtered"; }
+
+// eval.hpp:25-45: the known-true triples; kept as id lists, hashed on device.
+class TripleFilter {
+ public:
+  TripleFilter(Index n_entities = 0, Index n_relations = 0) : n_(n_entities), r_(n_relations) {}
+  void insert(Index h, Index r, Index t) {
+    h_.push_back(h);
+    r_ids_.push_back(r);
+    t_.push_back(t);
+  }
+  void insert(const TripleBatch& b) {
+    for (Index i = 0; i < b.size(); ++i) insert(b.heads[i], b.relations[i], b.tails[i]);
+  }
+  Index size() const { return static_cast<Index>(h_.size()); }
+  const std::vector<Index>& heads() const { return h_; }
+  const std::vector<Index>& relations() const { return r_ids_; }
+  const std::vector<Index>& tails() const { return t_; }
+
+ private:
+  Index n_, r_;
+  std::vector<Index> h_, r_ids_, t_;
+};
+
+struct EvalReport {  // eval.hpp:50-55
+  std::map<Index, double> hits_at;
+  double mrr = 0;
+  Index n_queries = 0;
+  Protocol protocol = Protocol::Raw;
+};
+
+namespace detail {
+inline std::vector<Index> ranks(const ModelConfig& mc, const EmbeddingStore& store, const TripleBatch& q,
+                                const TripleFilter* filter) {
+  detail::upload(mc, store);
+  skg_model_config c = detail::cfg(mc);
+  std::vector<Index> out(2 * static_cast<size_t>(q.size()));
+  static const std::vector<Index> none(1, 0);
+  detail::check(skg_rank_entities(detail::ctx(), &c, q.size(), q.heads.data(), q.relations.data(), q.tails.data(),
+                                  filter ? 1 : 0, filter ? filter->size() : 0,
+                                  filter ? filter->heads().data() : none.data(),
+                                  filter ? filter->relations().data() : none.data(),
+                                  filter ? filter->tails().data() : none.data(), out.data()));
+  return out;
+}
+}  // namespace detail
+
+// eval.cpp:16-63
+inline Index rank_entity(const ModelConfig& mc, const EmbeddingStore& store, Index h, Index r, Index t, Side side,
+                         const TripleFilter* filter) {
+  TripleBatch q;
+  q.heads = {h};
+  q.relations = {r};
+  q.tails = {t};
+  q.num_entities = store.entity.rows();
+  q.num_relations = store.relation.rows();
+  const auto rk = detail::ranks(mc, store, q, filter);
+  return side == Side::Tail ? rk[0] : rk[1];
+}
+
+// eval.cpp:5-12 + 65-96 (filter over every split; MRR / Hits@k accumulated in
+// the reference's order: tail then head per test triple)
+inline EvalReport evaluate(const ModelConfig& mc, const EmbeddingStore& store, const TripleBatch& train,
+                           const TripleBatch& valid, const TripleBatch& test, Protocol protocol,
+                           const std::vector<Index>& ks = {1, 3, 10}) {
+  if (test.size() < 1) throw ConfigError("evaluation needs a nonempty test split");
+  TripleFilter filter(store.entity.rows(), store.relation.rows());
+  if (protocol == Protocol::Filtered) {
+    filter.insert(train);
+    filter.insert(valid);
+    filter.insert(test);
+  }
+  const auto rk = detail::ranks(mc, store, test, protocol == Protocol::Filtered ? &filter : nullptr);
+  EvalReport rep;
+  rep.protocol = protocol;
+  std::vector<Index> hit_counts(ks.size(), 0);
+  double mrr_sum = 0;
+  for (size_t i = 0; i < rk.size(); ++i) {
+    mrr_sum += 1.0 / double(rk[i]);
+    for (size_t k = 0; k < ks.size(); ++k)
+      if (rk[i] <= ks[k]) ++hit_counts[k];
+    ++rep.n_queries;
+  }
+  for (size_t k = 0; k < ks.size(); ++k) rep.hits_at[ks[k]] = double(hit_counts[k]) / double(rep.n_queries);
+  rep.mrr = mrr_sum / double(rep.n_queries);
+  return rep;
 }
 
 // embedding.cpp:165-190

@@ -107,7 +107,7 @@ class Oracle:
                      "orc_epoch_order", "orc_build_incidence", "orc_coo_to_csr", "orc_transpose",
                      "orc_spmm", "orc_spmm_transpose_add", "orc_score_batch", "orc_score_backward",
                      "orc_margin_ranking_loss", "orc_sgd_step", "orc_renormalize_entities",
-                     "orc_train_epoch", "orc_train_batches", "orc_fit"]:
+                     "orc_train_epoch", "orc_train_batches", "orc_fit", "orc_rank_entities"]:
             getattr(L, name).restype = C.c_int
         L.orc_init_store.argtypes = [C.c_uint32, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_uint64] + [C.c_void_p] * 4
@@ -130,6 +130,8 @@ class Oracle:
         L.orc_train_batches.argtypes = [C.c_void_p, C.c_void_p, C.c_int64] + [C.c_void_p] * 6 + [
             C.c_int64, self.real, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
         L.orc_fit.argtypes = [C.c_void_p, C.c_void_p, C.c_int64] + [C.c_void_p] * 4
+        L.orc_rank_entities.argtypes = [C.c_void_p, C.c_void_p, C.c_int64] + [C.c_void_p] * 3 + [
+            C.c_int, C.c_int64] + [C.c_void_p] * 4
 
     # ------------------------------------------------------------ plumbing
     def _check(self, rc):
@@ -260,6 +262,22 @@ class Oracle:
         self._check(self.lib.orc_score_batch(C.byref(cfg), C.byref(st), m, _p(h), _p(r), _p(t),
                                              _p(scores), _p(v), _p(u), _p(dl)))
         return scores, {"v": v, "u": u, "delta": dl}
+
+    def rank_entities(self, model, store: Store, h, r, t, norm="l2", filt=None):
+        """rank_entity (eval.cpp:16-63) of every query, tail then head: int64 (q, 2)."""
+        h, r, t = _i64(h), _i64(r), _i64(t)
+        cfg = self._cfg(model, store.entity.shape[1], store.relation.shape[1], norm)
+        st = self._store(store)
+        ranks = np.empty((len(h), 2), np.int64)
+        if filt is None:
+            fh = fr = ft = np.zeros(1, np.int64)
+            nf, on = 0, 0
+        else:
+            fh, fr, ft = (_i64(x) for x in filt)
+            nf, on = len(fh), 1
+        self._check(self.lib.orc_rank_entities(C.byref(cfg), C.byref(st), len(h), _p(h), _p(r), _p(t), on, nf,
+                                               _p(fh), _p(fr), _p(ft), _p(ranks)))
+        return ranks
 
     def score_backward(self, model, store: Store, h, r, t, up, grads: Store, norm="l2"):
         h, r, t, up = _i64(h), _i64(r), _i64(t), self._f(up)

@@ -6,6 +6,8 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <unordered_set>
+#include <vector>
 
 #include "skge_oracle.hpp"
 
@@ -257,6 +259,50 @@ int orc_score_batch(const orc_model_config* cfg, const orc_store* st, Index m, c
     copy_mat(sb.v, v);
     copy_mat(sb.u, u);
     copy_mat(sb.delta, delta);
+  });
+}
+
+// rank_entity (eval.cpp:16-63) for q queries, Tail then Head side per query
+// (the order evaluate() visits them, eval.cpp:80-86): ranks[2i] = tail rank,
+// ranks[2i+1] = head rank. filtered != 0: competing candidates whose triple is
+// in the nf filter triples (TripleFilter, eval.hpp:25-45) are skipped; the
+// query's own entity never is. Translational models only (no self exclusion).
+int orc_rank_entities(const orc_model_config* cfg, const orc_store* st, Index q, const Index* qh,
+                      const Index* qr, const Index* qt, int filtered, Index nf, const Index* fh,
+                      const Index* fr, const Index* ft, Index* ranks) {
+  return guard([&] {
+    Store s = view_store(st);
+    const ModelConfig mc = mk_cfg(cfg);
+    const Index n = st->num_entities, nr = st->num_relations;
+    auto key = [&](Index h, Index r, Index t) {
+      return (static_cast<std::uint64_t>(h) * static_cast<std::uint64_t>(nr) + static_cast<std::uint64_t>(r)) *
+                 static_cast<std::uint64_t>(n) + static_cast<std::uint64_t>(t);
+    };
+    std::unordered_set<std::uint64_t> known;
+    if (filtered)
+      for (Index i = 0; i < nf; ++i) known.insert(key(fh[i], fr[i], ft[i]));
+    std::vector<Index> ch(n), cr(n), ct(n);
+    for (Index i = 0; i < q; ++i) {
+      const Index h = qh[i], r = qr[i], t = qt[i];
+      if (h < 0 || h >= n || t < 0 || t >= n || r < 0 || r >= nr) throw ShapeError("rank_entity: query ids out of range");
+      for (int side = 0; side < 2; ++side) {  // 0 = Tail, 1 = Head
+        for (Index c = 0; c < n; ++c) {
+          ch[c] = side == 0 ? h : c;
+          cr[c] = r;
+          ct[c] = side == 0 ? c : t;
+        }
+        ScoreBatch sb = score_batch(mc, s, mk_batch(n, ch.data(), cr.data(), ct.data(), n, nr));
+        const Index truth = side == 0 ? t : h;
+        const Real te = sb.scores[truth];  // energy_sign = +1 for the translational models
+        Index better = 0;
+        for (Index c = 0; c < n; ++c) {
+          if (c == truth) continue;
+          if (filtered && known.count(side == 0 ? key(h, r, c) : key(c, r, t))) continue;
+          if (sb.scores[c] < te) ++better;
+        }
+        ranks[2 * i + side] = better + 1;
+      }
+    }
   });
 }
 

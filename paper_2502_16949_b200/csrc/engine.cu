@@ -714,6 +714,7 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaMemset(ctx->counter.p, 0, sizeof(unsigned)));
     configure_hrt_kernels();
     configure_ht_kernels();
+    configure_eval_kernels();
   });
   if (st != SKG_OK) {
     g_create_err = ctx->err;
@@ -1294,6 +1295,52 @@ extern "C" skg_status skg_dp_shard(int64_t m, int64_t batch_size, int32_t world,
     return SKG_ERR_CONFIG;
   dp_shard(m, std::min(batch_size, m), world, rank, out);
   return SKG_OK;
+}
+
+// rank_entity / evaluate (eval.cpp:16-96) on device for the translational
+// hrt models: ranks[2i] = tail-side rank, ranks[2i + 1] = head-side rank.
+extern "C" skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cfg, int64_t q, const int64_t* heads,
+                                        const int64_t* relations, const int64_t* tails, int32_t protocol,
+                                        int64_t nf, const int64_t* fh, const int64_t* fr, const int64_t* ft,
+                                        int64_t* ranks) {
+  return guard(ctx, [&] {
+    check_config(ctx, *cfg, ctx->N, ctx->R);
+    const int kind = kind_of(*cfg);
+    if (!eval_supported(kind)) throw ConfigError("rank_entities: device ranking covers transe / toruse");
+    if (protocol != 0 && protocol != 1) throw ConfigError("rank_entities: protocol must be 0 (raw) or 1 (filtered)");
+    for (int64_t i = 0; i < q; ++i)
+      if (heads[i] < 0 || heads[i] >= ctx->N || tails[i] < 0 || tails[i] >= ctx->N || relations[i] < 0 ||
+          relations[i] >= ctx->R)
+        throw ShapeError("rank_entity: query ids out of range");  // eval.cpp:21
+    if (q == 0) return;
+    std::vector<int32_t> host;
+    validate_ids(q, heads, relations, tails, ctx->N, ctx->R, host);
+    DevBuf<int32_t> qd, fd;
+    qd.ensure(3 * q);
+    SKG_CUDA(cudaMemcpyAsync(qd.p, host.data(), sizeof(int32_t) * 3 * q, cudaMemcpyHostToDevice, ctx->stream));
+    DevBuf<uint64_t> table;
+    uint64_t cap = 0;
+    if (protocol == 1) {
+      std::vector<int32_t> fhost;
+      validate_ids(nf, fh, fr, ft, ctx->N, ctx->R, fhost);
+      cap = eval_filter_capacity(nf);
+      table.ensure(static_cast<int64_t>(cap));
+      fd.ensure(3 * nf + 1);
+      if (nf > 0)
+        SKG_CUDA(cudaMemcpyAsync(fd.p, fhost.data(), sizeof(int32_t) * 3 * nf, cudaMemcpyHostToDevice, ctx->stream));
+      eval_build_filter(fd.p, fd.p + nf, fd.p + 2 * nf, nf, ctx->N, ctx->R, table.p, cap, ctx->stream);
+    }
+    DevBuf<uint32_t> better;
+    DevBuf<float> te;
+    better.ensure(2 * q);
+    te.ensure(2 * q);
+    eval_rank(kind, ctx->tables.p, ctx->N, ctx->R, static_cast<int>(ctx->de), qd.p, qd.p + q, qd.p + 2 * q, q,
+              protocol == 1 ? table.p : nullptr, cap, better.p, te.p, ctx->num_sms, ctx->stream);
+    std::vector<uint32_t> b(2 * q);
+    SKG_CUDA(cudaMemcpyAsync(b.data(), better.p, sizeof(uint32_t) * 2 * q, cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int64_t i = 0; i < 2 * q; ++i) ranks[i] = static_cast<int64_t>(b[i]) + 1;
+  });
 }
 
 extern "C" int64_t skg_debug_transr_trace(int32_t enable, unsigned long long* out, int64_t cap) {

@@ -105,6 +105,7 @@ def load_library():
         "skg_flush_l2": [vp],
         "skg_plan_stats": [vp, i64, vp, vp, vp],
         "skg_debug_tc_gemm": [vp, i32, vp, vp, vp],
+        "skg_rank_entities": [vp, vp, i64, vp, vp, vp, i32, i64, vp, vp, vp, vp],
         "skg_dp_shard": [i64, i64, i32, i32, vp],
     }
     L.skg_host_last_error.restype = C.c_char_p
@@ -287,6 +288,21 @@ class Engine:
     # ------------------------------------------------------------ measurement hooks
     def flush_l2(self):
         self._check(self.L.skg_flush_l2(self.h))
+
+    def rank_entities(self, cfg, h, r, t, filt=None):
+        """rank_entity (eval.cpp:16-63) for every query: int64 (q, 2) = [tail rank, head rank];
+        filt = (heads, relations, tails) of the known-true triples selects the filtered protocol."""
+        h, r, t = _i64(h), _i64(r), _i64(t)
+        ranks = np.empty((len(h), 2), np.int64)
+        if filt is None:
+            z = np.zeros(1, np.int64)
+            self._check(self.L.skg_rank_entities(self.h, C.byref(cfg), len(h), _p(h), _p(r), _p(t), 0, 0,
+                                                 _p(z), _p(z), _p(z), _p(ranks)))
+        else:
+            fh, fr, ft = (_i64(x) for x in filt)
+            self._check(self.L.skg_rank_entities(self.h, C.byref(cfg), len(h), _p(h), _p(r), _p(t), 1, len(fh),
+                                                 _p(fh), _p(fr), _p(ft), _p(ranks)))
+        return ranks
 
     def debug_tc_gemm(self, mode: int, A, B):
         A, B = _f32(A), _f32(B)

@@ -429,3 +429,46 @@ def test_shuffle_is_a_permutation(orc64):  # training.cpp:106-112
         o = orc64.epoch_order(m, 42, 3)
         assert sorted(o.tolist()) == list(range(m))
     assert orc64.epoch_order(10, 1, 0, shuffle=False).tolist() == list(range(10))
+
+
+# ---- link prediction (test_eval.cpp), the oracle's rank_entity restatement
+def _plane_store(orc):  # test_eval.cpp:47-53
+    st = orc.init_store("transe", 5, 1, 2, 2, 0)
+    st.entity[:] = np.array([[0, 0], [0, 1], [1, 0], [2, 0], [0.5, 0]])
+    st.relation[:] = np.array([[1, 0]])
+    return st
+
+
+def test_rank_entity_goldens(orc64):  # test_eval.cpp:55-79
+    st = _plane_store(orc64)
+    assert orc64.rank_entities("transe", st, [0], [0], [3])[0, 0] == 3
+    filt = ([0, 0, 0], [0, 0, 0], [2, 4, 3])  # the query itself stays eligible
+    assert orc64.rank_entities("transe", st, [0], [0], [3], filt=filt)[0, 0] == 1
+    tie = orc64.init_store("transe", 6, 1, 3, 3, 0)
+    tie.entity[:] = 0.25
+    tie.relation[:] = 0.0
+    assert (orc64.rank_entities("transe", tie, [0], [0], [4]) == 1).all()
+
+
+def test_evaluate_mrr_0625(orc64):  # test_eval.cpp:87-101: ranks 1 (tail) and 4 (head)
+    st = orc64.init_store("transe", 5, 1, 2, 2, 0)
+    st.entity[:] = np.array([[0, 0], [-0.4, 0], [-0.6, 0], [-0.5, 0.1], [0.5, 0]])
+    st.relation[:] = np.array([[1, 0]])
+    rk = orc64.rank_entities("transe", st, [0], [0], [4])
+    assert rk.tolist() == [[1, 4]]
+    assert abs(np.mean(1.0 / rk) - 0.625) < 1e-12
+
+
+def test_evaluate_exact_translations(orc64):  # test_eval.cpp:103-115
+    st = orc64.init_store("transe", 4, 1, 2, 2, 0)
+    st.entity[:] = np.array([[0, 0], [1, 0], [0, 1], [1, 1]])
+    st.relation[:] = np.array([[1, 0]])
+    assert (orc64.rank_entities("transe", st, [0, 2], [0, 0], [1, 3]) == 1).all()
+
+
+def test_rank_entity_rejects_bad_ids(orc64):  # test_eval.cpp:81-85
+    st = _plane_store(orc64)
+    with pytest.raises(Exception):
+        orc64.rank_entities("transe", st, [0], [0], [9])
+    with pytest.raises(Exception):
+        orc64.rank_entities("transe", st, [0], [3], [1])
