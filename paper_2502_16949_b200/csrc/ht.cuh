@@ -67,6 +67,10 @@ void transr_tc_selftest(int mode, const float* A, const float* B, float* D, cuda
 void configure_transr_train_tc_kernels();
 int64_t transr_train_tc_mr_floats(int64_t R);
 int64_t transr_trace(int enable, unsigned long long* out, int64_t cap);  // debug: phase timestamps
+void launch_transr_train_apply(const uint32_t* tile_total, const uint32_t* seg_tiles, const uint32_t* tile_seg,
+                               const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
+                               float* proj, float* rel, const float* lr, const uint32_t* err, float* mr, int64_t R,
+                               cudaStream_t s);
 void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,
                             const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
                             const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,

@@ -436,13 +436,17 @@ int64_t max_tiles(int64_t rows, int64_t R) { return rows / kTilePairs + 2 * R + 
 Work carve(float* work, int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
   Work w;
-  w.tile_seg = reinterpret_cast<uint32_t*>(work);
+  // the split M_r chunks come first: their offset must not depend on the batch
+  // size (the training apply of batch b refreshes them for batch b + 1, and the
+  // last batch of an epoch is shorter)
+  w.mr_chunks = work;
+  float* rest = work + ((std::max(transr_tc_mr_floats(R), transr_train_tc_mr_floats(R)) + 31) / 32) * 32;
+  w.tile_seg = reinterpret_cast<uint32_t*>(rest);
   w.tile_p0 = w.tile_seg + mt;
   w.tile_total = w.tile_p0 + mt;
   w.seg_tiles = w.tile_total + 2;
-  w.dm_part = work + ((3 * mt + 2 * R + 8 + 31) / 32) * 32;  // 128 B aligned (float4 stores)
+  w.dm_part = rest + ((3 * mt + 2 * R + 8 + 31) / 32) * 32;  // 128 B aligned (float4 stores)
   w.dr_part = w.dm_part + std::max<int64_t>(mt, transr_tc_slots(256, R)) * dr * de;
-  w.mr_chunks = w.dr_part + ((std::max<int64_t>(mt, transr_tc_slots(256, R)) * dr + 31) / 32) * 32;
   return w;
 }
 
@@ -513,8 +517,8 @@ void launch_relation_tiles(const BwdArgs& ba, int paired, uint32_t* tile_seg, ui
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
   const int64_t parts = std::max<int64_t>(mt, transr_tc_slots(256, R));  // tc path: (CTA, relation) runs
-  return ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + parts * dr * de + ((parts * dr + 31) / 32) * 32 +
-         std::max(transr_tc_mr_floats(R), transr_train_tc_mr_floats(R)) + 64;
+  return ((std::max(transr_tc_mr_floats(R), transr_train_tc_mr_floats(R)) + 31) / 32) * 32 +
+         ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + parts * dr * de + ((parts * dr + 31) / 32) * 32 + 64;
 }
 
 void configure_transr_kernels() {
@@ -554,9 +558,9 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
     eb.entity_only = 1;
     eb.d = fa.de;
     launch_segment_backward(kPlainRows, true, eb, num_sms, s);
-    launch_transr_tc_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
-                           const_cast<float*>(fa.proj), const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de),
-                           ba.lr, true, ba.err, R, s);
+    launch_transr_train_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
+                              const_cast<float*>(fa.proj), const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de),
+                              ba.lr, ba.err, w.mr_chunks, R, s);
     if (mark) (*mark)();
     return;
   }

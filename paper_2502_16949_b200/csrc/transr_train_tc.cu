@@ -652,6 +652,83 @@ __global__ void transr_train_prep_kernel(const float* __restrict__ proj, float* 
   }
 }
 
+// Per relation segment k of the batch: sum the (CTA, relation run) partials
+// j + k in CTA order (the partition transr_train_tc_kernel used), SGD on M_r
+// and the relation row, and refresh M_r's pre-split ring chunks so the next
+// minibatch needs no separate split pass.
+__global__ void transr_train_apply_kernel(const uint32_t* __restrict__ tile_total,
+                                          const uint32_t* __restrict__ seg_tiles,
+                                          const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ seg_col,
+                                          int64_t N, int G, const float* __restrict__ dm_part,
+                                          const float* __restrict__ dr_part, float* __restrict__ proj,
+                                          float* __restrict__ rel, const float* __restrict__ lr,
+                                          const uint32_t* __restrict__ err, float* __restrict__ mr) {
+  if (err[0] != 0) return;
+  const uint32_t k = blockIdx.x;
+  if (k >= tile_total[1]) return;
+  const uint32_t T = tile_total[0];
+  const uint32_t lo = seg_tiles[k], hi = seg_tiles[k + 1];
+  if (hi <= lo) return;
+  const int64_t r = static_cast<int64_t>(seg_col[tile_seg[lo]]) - N;
+  const float step = *lr;
+  __shared__ int jl[1024];
+  __shared__ int nj;
+  if (threadIdx.x < 32) {  // CTAs j whose tile range [T j / G, T (j+1) / G) meets [lo, hi), in order
+    int c = 0;
+    for (int j0 = 0; j0 < G && j0 < 1024; j0 += 32) {
+      const int j = j0 + static_cast<int>(threadIdx.x);
+      bool o = false;
+      if (j < G && j < 1024) {
+        const uint32_t a0 = static_cast<uint32_t>((static_cast<uint64_t>(T) * j) / G);
+        const uint32_t a1 = static_cast<uint32_t>((static_cast<uint64_t>(T) * (j + 1)) / G);
+        o = a0 < a1 && a1 > lo && a0 < hi;
+      }
+      const unsigned m = __ballot_sync(kFull, o);
+      if (o) jl[c + __popc(m & lanemask_lt())] = j;
+      c += __popc(m);
+    }
+    if (threadIdx.x == 0) nj = c;
+  }
+  __syncthreads();
+  float* mrr = mr + r * kMrFloatsPerRel;
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < kD * kD + kD; i += gridDim.y * blockDim.x) {
+    const bool pm = i < kD * kD;
+    float g = 0.f;
+    int q = 0;
+    for (; q + 4 <= nj; q += 4) {  // four independent loads in flight, added in order
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const size_t slot = static_cast<size_t>(jl[q + e]) + k;
+        v[e] = pm ? __ldcg(dm_part + slot * kD * kD + i) : __ldcg(dr_part + slot * kD + (i - kD * kD));
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) g = __fadd_rn(g, v[e]);
+    }
+    for (; q < nj; ++q) {
+      const size_t slot = static_cast<size_t>(jl[q]) + k;
+      g = __fadd_rn(g, pm ? __ldcg(dm_part + slot * kD * kD + i) : __ldcg(dr_part + slot * kD + (i - kD * kD)));
+    }
+    float* p = pm ? proj + r * kD * kD + i : rel + r * kD + (i - kD * kD);
+    const float nv = __fsub_rn(*p, __fmul_rn(step, g));
+    *p = nv;
+    if (pm) {  // element (row a = output dim, col b = entity dim) of M_r into both ring layouts
+      const int a = i / kD, b = i - a * kD;
+      float h, l;
+      tc::split_tf32(nv, h, l);
+      float* c0 = mrr + static_cast<int64_t>(b / kChunkK) * 2 * kChunkFloats;                   // layout 0: n = a, k = b
+      float* c1 = mrr + static_cast<int64_t>(kChunksPerGemm + a / kChunkK) * 2 * kChunkFloats;  // layout 1: n = b, k = a
+      const int kb = b % kChunkK, ka = a % kChunkK;
+      const int o0 = (((a & 7) + (a >> 3) * 32 + (kb >> 2) * 8) << 2) + (kb & 3);
+      const int o1 = (((b & 7) + (b >> 3) * 32 + (ka >> 2) * 8) << 2) + (ka & 3);
+      c0[o0] = h;
+      c0[kChunkFloats + o0] = l;
+      c1[o1] = h;
+      c1[kChunkFloats + o1] = l;
+    }
+  }
+}
+
 }  // namespace
 
 int64_t transr_train_tc_mr_floats(int64_t R) { return R * kMrFloatsPerRel; }
@@ -678,8 +755,12 @@ void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val,
                             const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
                             const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,
                             float* mr, int64_t R, int num_sms, cudaStream_t s) {
-  transr_train_prep_kernel<<<dim3(static_cast<unsigned>(R), 2 * kChunksPerGemm), 256, 0, s>>>(fa.proj, mr);
-  count_launch();
+  // the split M_r chunks are refreshed by every batch's apply; the first batch
+  // of an epoch re-splits from proj (the store may have been replaced)
+  if (fa.batch == 0) {
+    transr_train_prep_kernel<<<dim3(static_cast<unsigned>(R), 2 * kChunksPerGemm), 256, 0, s>>>(fa.proj, mr);
+    count_launch();
+  }
   Args a{};
   a.f = fa;
   a.ent_val = ent_val;
@@ -695,6 +776,17 @@ void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val,
   const size_t smem = sizeof(Smem);
   if (l2) transr_train_tc_kernel<true><<<num_sms, kThreads, smem, s>>>(a);
   else transr_train_tc_kernel<false><<<num_sms, kThreads, smem, s>>>(a);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
+void launch_transr_train_apply(const uint32_t* tile_total, const uint32_t* seg_tiles, const uint32_t* tile_seg,
+                               const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
+                               float* proj, float* rel, const float* lr, const uint32_t* err, float* mr, int64_t R,
+                               cudaStream_t s) {
+  transr_train_apply_kernel<<<dim3(static_cast<unsigned>(R), 16), 256, 0, s>>>(tile_total, seg_tiles, tile_seg, seg_col,
+                                                                              N, G, dm_part, dr_part, proj, rel, lr,
+                                                                              err, mr);
   count_launch();
   SKG_LAUNCH_CHECK();
 }

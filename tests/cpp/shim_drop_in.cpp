@@ -39,5 +39,23 @@ int main() {
     return 2;
   } catch (const ConfigError&) {
   }
+  // link prediction through the shim (test_eval.cpp:47-79)
+  {
+    ModelConfig pc;
+    pc.model = ModelKind::TransE;
+    pc.dim_entity = pc.dim_relation = 2;
+    auto plane = init_store(ModelKind::TransE, 5, 1, 2, 2, 0);
+    const Real xy[5][2] = {{0, 0}, {0, 1}, {1, 0}, {2, 0}, {0.5f, 0}};
+    for (int i = 0; i < 5; ++i) plane.entity(i, 0) = xy[i][0], plane.entity(i, 1) = xy[i][1];
+    plane.relation(0, 0) = 1, plane.relation(0, 1) = 0;
+    TripleFilter filter(5, 1);
+    filter.insert(0, 0, 2);
+    filter.insert(0, 0, 4);
+    filter.insert(0, 0, 3);
+    const Index raw = rank_entity(pc, plane, 0, 0, 3, Side::Tail, nullptr);
+    const Index fil = rank_entity(pc, plane, 0, 0, 3, Side::Tail, &filter);
+    std::printf("shim rank_entity: raw %lld filtered %lld\n", static_cast<long long>(raw), static_cast<long long>(fil));
+    if (raw != 3 || fil != 1) return 3;
+  }
   return last < 0.5f * first ? 0 : 1;
 }
