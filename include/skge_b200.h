@@ -97,6 +97,23 @@ skg_status skg_store_download(skg_ctx* ctx, float* entity, float* relation, floa
  * Grads are host tables shaped like the store; non-finite -> SKG_ERR_TRAINING. */
 skg_status skg_sgd_step(skg_ctx* ctx, const float* g_entity, const float* g_relation,
                         const float* g_proj, const float* g_normals, float lr);
+/* ---- checkpoints (embedding.cpp:35-125, 200-251: SKGECKPT v1) ------------
+ * Host-side file I/O on host tables (download / upload the device store
+ * around them). f64 on disk, fp32 in memory, exactly like the reference's
+ * 32-bit build. Real-valued model tags only (0 TransE .. 3 TorusE); errors:
+ * SKG_ERR_PARSE / SKG_ERR_CONFIG with skg_checkpoint_last_error(). */
+typedef struct skg_checkpoint_header { /* CheckpointHeader, embedding.hpp:134-140 */
+  uint32_t model;
+  int64_t num_entities, num_relations, dim_entity, dim_relation;
+} skg_checkpoint_header;
+skg_status skg_peek_checkpoint(const char* path, skg_checkpoint_header* out);
+skg_status skg_save_checkpoint(const char* path, uint32_t model, int64_t num_entities, int64_t num_relations,
+                               int64_t dim_entity, int64_t dim_relation, const float* entity, const float* relation,
+                               const float* proj, const float* normals);
+skg_status skg_load_checkpoint(const char* path, uint32_t expected_model, float* entity, float* relation,
+                               float* proj, float* normals);
+const char* skg_checkpoint_last_error(void);
+
 /* renormalize_entities, embedding.cpp:192-198 */
 skg_status skg_renormalize_entities(skg_ctx* ctx);
 

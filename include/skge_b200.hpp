@@ -315,6 +315,50 @@ inline TrainingRun fit(const ModelConfig& mc, EmbeddingStore& store, const Tripl
   return run;
 }
 
+// ---- checkpoints (embedding.hpp:134-152, embedding.cpp:200-251) -----------
+struct CheckpointHeader {
+  ModelKind model = ModelKind::TransE;
+  Index num_entities = 0, num_relations = 0, dim_entity = 0, dim_relation = 0;
+};
+
+namespace detail {
+[[noreturn]] inline void rethrow_ckpt(skg_status st) {
+  const std::string msg = skg_checkpoint_last_error();
+  if (st == SKG_ERR_CONFIG) throw ConfigError(msg);
+  throw ParseError(msg);
+}
+}  // namespace detail
+
+inline CheckpointHeader peek_checkpoint(const std::string& path) {
+  skg_checkpoint_header h{};
+  const skg_status st = skg_peek_checkpoint(path.c_str(), &h);
+  if (st != SKG_OK) detail::rethrow_ckpt(st);
+  return CheckpointHeader{static_cast<ModelKind>(h.model), h.num_entities, h.num_relations, h.dim_entity,
+                          h.dim_relation};
+}
+
+inline void save_checkpoint(const std::string& path, ModelKind model, const EmbeddingStore& s) {
+  const skg_status st = skg_save_checkpoint(path.c_str(), static_cast<std::uint32_t>(model), s.entity.rows(),
+                                            s.relation.rows(), s.entity.cols(), s.relation.cols(), s.entity.data(),
+                                            s.relation.data(), s.proj.size() ? s.proj.data() : nullptr,
+                                            s.normals.size() ? s.normals.data() : nullptr);
+  if (st != SKG_OK) detail::rethrow_ckpt(st);
+}
+
+inline EmbeddingStore load_checkpoint(const std::string& path, ModelKind expected) {
+  const CheckpointHeader h = peek_checkpoint(path);
+  EmbeddingStore s;
+  s.entity = Matrix(h.num_entities, h.dim_entity);
+  s.relation = Matrix(h.num_relations, h.dim_relation);
+  if (h.model == ModelKind::TransR) s.proj = Matrix(h.num_relations, h.dim_relation * h.dim_entity);
+  if (h.model == ModelKind::TransH) s.normals = Matrix(h.num_relations, h.dim_entity);
+  const skg_status st = skg_load_checkpoint(path.c_str(), static_cast<std::uint32_t>(expected), s.entity.data(),
+                                            s.relation.data(), s.proj.size() ? s.proj.data() : nullptr,
+                                            s.normals.size() ? s.normals.data() : nullptr);
+  if (st != SKG_OK) detail::rethrow_ckpt(st);
+  return s;
+}
+
 // ---- link prediction (eval.hpp / eval.cpp) --------------------------------
 enum class Protocol { Raw, Filtered };
 enum class Side { Head, Tail };

@@ -1104,8 +1104,6 @@ skg_status skg_margin_ranking_loss(skg_ctx* ctx, int64_t m, const float* pos, co
     DevBuf<float> buf;
     buf.ensure(5 * m + 1);
     float *p = buf.p, *n = buf.p + m, *dp = buf.p + 2 * m, *dn = buf.p + 3 * m, *term = buf.p + 4 * m;
-    float* out = buf.p + 5 * m;
-    buf.ensure(5 * m + 1);
     DevBuf<float> o;
     o.ensure(1);
     SKG_CUDA(cudaMemcpyAsync(p, pos, sizeof(float) * m, cudaMemcpyHostToDevice, ctx->stream));
@@ -1114,7 +1112,6 @@ skg_status skg_margin_ranking_loss(skg_ctx* ctx, int64_t m, const float* pos, co
     seq_sum_kernel<<<1, 1, 0, ctx->stream>>>(term, m, o.p);
     count_launch(2);
     SKG_LAUNCH_CHECK();
-    (void)out;
     SKG_CUDA(cudaMemcpyAsync(d_pos, dp, sizeof(float) * m, cudaMemcpyDeviceToHost, ctx->stream));
     SKG_CUDA(cudaMemcpyAsync(d_neg, dn, sizeof(float) * m, cudaMemcpyDeviceToHost, ctx->stream));
     SKG_CUDA(cudaMemcpyAsync(loss, o.p, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));

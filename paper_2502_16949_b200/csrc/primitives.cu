@@ -174,7 +174,6 @@ __global__ void __launch_bounds__(kSortWarps * 32)
   __shared__ uint32_t hist[kSortWarps][1 << kMaxBits];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nd = 1 << bits;
-  const uint32_t mask = nd - 1;
   for (int d = threadIdx.x; d < kSortWarps * (1 << kMaxBits); d += blockDim.x) (&hist[0][0])[d] = 0;
   __syncthreads();
   using G = SortGeom<CH>;

@@ -296,7 +296,6 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
       }
     }
     __syncthreads();
-    const float* Mr = f.proj + r * static_cast<int64_t>(dr) * de;
     // ---- GEMM1: V = U M_r^T (K = de)
     for (int kc = 0; kc < de; kc += kChunk) {
       load_b(r, 0, kc / kChunk);

@@ -39,7 +39,7 @@ constexpr int kD = 128;
 constexpr int kRows = 128;
 constexpr int kPairs = 64;
 constexpr int kThreads = 352;
-constexpr int kMmaWarp = 8, kLoadWarp = 9, kRowWarp = 10;
+constexpr int kMmaWarp = 8, kRowWarp = 10;  // warp 9: ring loader
 
 // sU / sDZ: K-major SWIZZLE_128B (m = row, k = feature) in four 32-feature
 // column blocks of 128 rows x 128 B; 16-byte unit (r, c4) =

@@ -107,8 +107,12 @@ def load_library():
         "skg_debug_tc_gemm": [vp, i32, vp, vp, vp],
         "skg_rank_entities": [vp, vp, i64, vp, vp, vp, i32, i64, vp, vp, vp, vp],
         "skg_dp_shard": [i64, i64, i32, i32, vp],
+        "skg_peek_checkpoint": [C.c_char_p, vp],
+        "skg_save_checkpoint": [C.c_char_p, C.c_uint32, i64, i64, i64, i64, vp, vp, vp, vp],
+        "skg_load_checkpoint": [C.c_char_p, C.c_uint32, vp, vp, vp, vp],
     }
     L.skg_host_last_error.restype = C.c_char_p
+    L.skg_checkpoint_last_error.restype = C.c_char_p
     for name, args in sig.items():
         fn = getattr(L, name)
         fn.argtypes = args
@@ -356,4 +360,44 @@ def init_store(model: str, n_entities: int, n_relations: int, de: int, dr: int, 
     p = np.empty((n_relations, dr * de), np.float32) if model == "transr" else None
     n = np.empty((n_relations, de), np.float32) if model == "transh" else None
     _host_check(L, L.skg_init_store(MODELS[model], n_entities, n_relations, de, dr, seed, _p(e), _p(r), _p(p), _p(n)))
+    return e, r, p, n
+
+
+# ---- checkpoints (embedding.cpp:200-251, SKGECKPT v1) ----------------------
+class CheckpointHeader(C.Structure):  # embedding.hpp:134-140
+    _fields_ = [("model", C.c_uint32), ("num_entities", C.c_int64), ("num_relations", C.c_int64),
+                ("dim_entity", C.c_int64), ("dim_relation", C.c_int64)]
+
+
+def _ckpt_check(L, rc):
+    if rc != 0:
+        raise EngineError(rc, L.skg_checkpoint_last_error().decode())
+
+
+def peek_checkpoint(path: str) -> CheckpointHeader:
+    L = load_library()
+    h = CheckpointHeader()
+    _ckpt_check(L, L.skg_peek_checkpoint(path.encode(), C.byref(h)))
+    return h
+
+
+def save_checkpoint(path: str, model: str, entity, relation, proj=None, normals=None):
+    """save_checkpoint(path, model, store): fp32 host tables written as f64 (the reference's 32-bit build)."""
+    L = load_library()
+    e, r = _f32(entity), _f32(relation)
+    p = None if proj is None else _f32(proj)
+    n = None if normals is None else _f32(normals)
+    _ckpt_check(L, L.skg_save_checkpoint(path.encode(), MODELS[model], e.shape[0], r.shape[0], e.shape[1], r.shape[1],
+                                         _p(e), _p(r), _p(p), _p(n)))
+
+
+def load_checkpoint(path: str, expected: str):
+    """load_checkpoint<Real>(path, expected) -> (entity, relation, proj, normals) fp32 tables."""
+    L = load_library()
+    h = peek_checkpoint(path)
+    e = np.empty((h.num_entities, h.dim_entity), np.float32)
+    r = np.empty((h.num_relations, h.dim_relation), np.float32)
+    p = np.empty((h.num_relations, h.dim_relation * h.dim_entity), np.float32) if h.model == 1 else None
+    n = np.empty((h.num_relations, h.dim_entity), np.float32) if h.model == 2 else None
+    _ckpt_check(L, L.skg_load_checkpoint(path.encode(), MODELS[expected], _p(e), _p(r), _p(p), _p(n)))
     return e, r, p, n
