@@ -145,34 +145,50 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
   const uint32_t T = alive ? static_cast<uint32_t>(min(static_cast<int64_t>(rt.first[rt.nrel]), a.mt)) : 0u;
   float lsum = 0.f;
   uint32_t pend = 0;
+  // Row ids of tile tt for pair kk = tid < 64: stage 1 reads the relation
+  // segment entry (positive row = batch position), stage 2 its pair record.
+  // The next tile's chase is issued while the current tile computes.
+  auto stage1 = [&](uint32_t tt, int kk) -> int {
+    const uint32_t kq = rel_of_tile(rt, tt);
+    const uint32_t sq = rt.seg[kq], pq = (tt - rt.first[kq]) * kPairs;
+    const uint32_t e0q = __ldg(a.seg_start + sq), lenq = __ldg(a.seg_start + sq + 1) - e0q;
+    const int npq = static_cast<int>(min(static_cast<uint32_t>(kPairs), lenq / 2 - pq));
+    return kk < npq ? static_cast<int>(__ldg(a.ent_val + e0q + pq + kk) & 0x7fffffffu) : -1;
+  };
+  auto stage2 = [&](int pos, int4& pr, int4& ng) {
+    pr = make_int4(0, 0, -1, 0);
+    ng = make_int4(0, 0, -1, 0);
+    if (pos < 0) return;
+    int h, tt, nh, nt;
+    if (f.pair_ht) {
+      const int4 x = __ldg(f.pair_ht + pos);
+      h = x.x, tt = x.y, nh = x.z, nt = x.w;
+    } else {
+      const int id = __ldg(f.order + pos);
+      h = __ldg(f.H + id), tt = __ldg(f.T + id), nh = __ldg(f.NH + id), nt = __ldg(f.NT + id);
+    }
+    pr = make_int4(h, tt, pos, 0);
+    ng = make_int4(nh, nt, pos + f.B, 0);
+  };
+  int4 pr_next = make_int4(0, 0, -1, 0), ng_next = make_int4(0, 0, -1, 0);
+  int pos_next = -1;
+  if (tid < kPairs && blockIdx.x < T) stage2(stage1(blockIdx.x, tid), pr_next, ng_next);
   for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
     const uint32_t k = rel_of_tile(rt, t);
     const uint32_t sseg = rt.seg[k], p0 = (t - rt.first[k]) * kPairs;
     const uint32_t e0 = __ldg(a.seg_start + sseg), len = __ldg(a.seg_start + sseg + 1) - e0;
     const int64_t r = static_cast<int64_t>(__ldg(a.seg_col + sseg)) - f.N;
     const int np = static_cast<int>(min(static_cast<uint32_t>(kPairs), len / 2 - p0));
+    (void)e0;
     const float4 w = __ldg(reinterpret_cast<const float4*>(f.normals + r * kD) + lane);
     const float4 drv = __ldg(reinterpret_cast<const float4*>(f.X + (f.N + r) * kD) + lane);
-    if (tid < kPairs) {  // row ids: positive row = batch position, its negative = B + position
-      const int kk = tid;
-      int4 pr = make_int4(0, 0, -1, 0), ng = make_int4(0, 0, -1, 0);
-      if (kk < np) {
-        const int pos = static_cast<int>(__ldg(a.ent_val + e0 + p0 + kk) & 0x7fffffffu);
-        int h, tt, nh, nt;
-        if (f.pair_ht) {
-          const int4 x = __ldg(f.pair_ht + pos);
-          h = x.x, tt = x.y, nh = x.z, nt = x.w;
-        } else {
-          const int id = __ldg(f.order + pos);
-          h = __ldg(f.H + id), tt = __ldg(f.T + id), nh = __ldg(f.NH + id), nt = __ldg(f.NT + id);
-        }
-        pr = make_int4(h, tt, pos, 0);
-        ng = make_int4(nh, nt, pos + f.B, 0);
-      }
-      rows[kk] = pr;
-      rows[kPairs + kk] = ng;
+    if (tid < kPairs) {
+      rows[tid] = pr_next;
+      rows[kPairs + tid] = ng_next;
     }
     __syncthreads();
+    const uint32_t tn = t + gridDim.x;
+    if (tid < kPairs && tn < T) pos_next = stage1(tn, tid);  // in flight during this tile
     // ---- u, wu, v for this warp's 8 rows, all 16 row loads in flight
     const int m0 = warp * kRowsPerWarp;
     float4 u[kRowsPerWarp];
@@ -213,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
       score[mj] = L2 ? __fsqrt_rn(ssum) : ssum;
     }
     __syncthreads();
+    if (tid < kPairs && tn < T) stage2(pos_next, pr_next, ng_next);
     // ---- pair hinge (training.cpp:73-94)
     const int kk = mj & (kPairs - 1);
     const bool valid = lane < kRowsPerWarp && kk < np;
@@ -364,7 +381,7 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   a.rel = const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
   a.lr = ba.lr;
   const size_t smem = sizeof(float) * kRows * kStride;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, static_cast<int64_t>(num_sms) * 16));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, static_cast<int64_t>(num_sms)));  // persistent
   if (l2) transh_tile_kernel<true><<<grid, kThreads, smem, s>>>(a);
   else transh_tile_kernel<false><<<grid, kThreads, smem, s>>>(a);
   count_launch();
