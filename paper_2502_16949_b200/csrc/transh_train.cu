@@ -298,7 +298,21 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
     if (rel_last && tid < kD) {
       __threadfence();
       float gA = 0.f, gB = 0.f;
-      for (uint32_t q = lo; q < hi; ++q) {
+      uint32_t q = lo;
+      for (; q + 8 <= hi; q += 8) {  // eight tiles' loads in flight, added in tile order
+        float va[8], vb[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          va[e] = __ldcg(a.partial + (static_cast<size_t>(q + e) * 2) * kD + tid);
+          vb[e] = __ldcg(a.partial + (static_cast<size_t>(q + e) * 2 + 1) * kD + tid);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          gA = __fadd_rn(gA, va[e]);
+          gB = __fadd_rn(gB, vb[e]);
+        }
+      }
+      for (; q < hi; ++q) {
         gA = __fadd_rn(gA, __ldcg(a.partial + (static_cast<size_t>(q) * 2) * kD + tid));
         gB = __fadd_rn(gB, __ldcg(a.partial + (static_cast<size_t>(q) * 2 + 1) * kD + tid));
       }
