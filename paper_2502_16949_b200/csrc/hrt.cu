@@ -129,6 +129,42 @@ __device__ __forceinline__ float row_scale(float up, float s) {
   return up;                                                                     // L1 sign weight
 }
 
+// TRAIN-mode gather of a tile's 8 (pos, neg) pairs: lanes k and k + 8 hold
+// the ids of pair k's positive and negative row (same relation).
+template <int KIND, int P>
+__device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int d4, int64_t N, int h, int t, int r,
+                                             float* rows, int S, int lane) {
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += P) {
+    int hp[P], tp[P], hn[P], tn[P], rr[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      hp[q] = __shfl_sync(kFull, h, k0 + q);
+      tp[q] = __shfl_sync(kFull, t, k0 + q);
+      hn[q] = __shfl_sync(kFull, h, k0 + q + 8);
+      tn[q] = __shfl_sync(kFull, t, k0 + q + 8);
+      rr[q] = __shfl_sync(kFull, r, k0 + q);
+    }
+    for (int c = lane; c < d4; c += 32) {
+      float4 xa[P], xb[P], xe[P], xf[P], xr[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        xa[q] = __ldg(X4 + static_cast<size_t>(hp[q]) * d4 + c);
+        xb[q] = __ldg(X4 + static_cast<size_t>(tp[q]) * d4 + c);
+        xe[q] = __ldg(X4 + static_cast<size_t>(hn[q]) * d4 + c);
+        xf[q] = __ldg(X4 + static_cast<size_t>(tn[q]) * d4 + c);
+        xr[q] = __ldg(X4 + static_cast<size_t>(N + rr[q]) * d4 + c);
+      }
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        *reinterpret_cast<float4*>(rows + (k0 + q) * S + 4 * c) = hrt_combine<KIND>(xa[q], xb[q], xr[q], hp[q] == tp[q]);
+        *reinterpret_cast<float4*>(rows + (k0 + q + 8) * S + 4 * c) =
+            hrt_combine<KIND>(xe[q], xf[q], xr[q], hn[q] == tn[q]);
+      }
+    }
+  }
+}
+
 #ifndef SKG_FWD_MINB
 #define SKG_FWD_MINB 2
 #endif
@@ -186,7 +222,14 @@ __global__ void __launch_bounds__(kThreads, SKG_FWD_MINB) hrt_forward_kernel(con
     const unsigned vmask = __ballot_sync(kFull, valid);
 
     // ---- gather 16 residual rows into shared memory
-    if (VEC == 4) {
+    if (TRAIN && VEC == 4) {
+      // pair-grouped: a pair's positive (row k) and negative (row k + 8) share
+      // the relation row, so P pairs need 5P row loads, all in flight at once
+      const int d4 = d >> 2;
+      if (d4 <= 32) gather_pairs<KIND, 4>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
+      else if (d4 <= 64) gather_pairs<KIND, 2>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
+      else gather_pairs<KIND, 1>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
+    } else if (VEC == 4) {
       const float4* X4 = reinterpret_cast<const float4*>(a.X);
       const int d4 = d >> 2;
 #pragma unroll
