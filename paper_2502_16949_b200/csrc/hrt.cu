@@ -185,21 +185,37 @@ __global__ void __launch_bounds__(kThreads, SKG_FWD_MINB) hrt_forward_kernel(con
   uint32_t pend = 0;
 
   const int nwarps = blockDim.x >> 5;
+  // epoch-plan pair records of the warp's next tile, loaded while the current
+  // tile is processed (one load per pair, no order -> id chase)
+  int4 pq_next = make_int4(0, 0, 0, 0);
+  int pr_next = 0;
+  auto prefetch = [&](int tl) {
+    if (TRAIN && a.pair_ht && lane < 16) {
+      const int p = tl * 8 + (lane & 7);
+      if (tl < ntiles && p < a.B) {
+        pq_next = __ldg(a.pair_ht + p);
+        pr_next = __ldg(a.pair_r + p);
+      }
+    }
+  };
+  prefetch(blockIdx.x * nwarps + warp);
   for (int tile = blockIdx.x * nwarps + warp; tile < ntiles; tile += gridDim.x * nwarps) {
     // ---- row ids: lane j < 16 describes row j of the tile
     int h = 0, t = 0, r = 0, row2 = 0;
     bool valid = false;
+    const int4 pq = pq_next;
+    const int prr = pr_next;
+    prefetch(tile + gridDim.x * nwarps);
     if (lane < 16) {
       if (TRAIN) {
         const int p = tile * 8 + (lane & 7);
         const bool neg = lane >= 8;
         valid = p < a.B;
         if (valid) {
-          if (a.pair_ht) {  // epoch-plan record of this position: one load, no order -> id chase
-            const int4 q = __ldg(a.pair_ht + p);
-            h = neg ? q.z : q.x;
-            t = neg ? q.w : q.y;
-            r = __ldg(a.pair_r + p);
+          if (a.pair_ht) {
+            h = neg ? pq.z : pq.x;
+            t = neg ? pq.w : pq.y;
+            r = prr;
           } else {
             const int id = a.order[p];
             h = neg ? a.NH[id] : a.H[id];
