@@ -159,7 +159,9 @@ skg_status skg_score_backward(skg_ctx* ctx, const skg_model_config* cfg, int64_t
  * ranks[2i + 1] = head rank, rank = 1 + #{c != truth : energy(c) < energy(truth)}.
  * protocol 1 (filtered) skips candidates whose triple is one of the nf filter
  * triples (TripleFilter / build_filter, eval.hpp:25-48); 0 = raw. TransE and
- * TorusE (bit-exact energies); other models return SKG_ERR_CONFIG. */
+ * TorusE energies are bit-exact; TransH / TransR rank against per-relation
+ * projected entity tables (P_r a - P_r b + r, equal to the reference's
+ * P_r (a - b) + r up to rounding: these models are tolerance-only). */
 skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cfg, int64_t q, const int64_t* heads,
                              const int64_t* relations, const int64_t* tails, int32_t protocol, int64_t nf,
                              const int64_t* filter_heads, const int64_t* filter_relations,

@@ -1303,7 +1303,7 @@ extern "C" skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cf
   return guard(ctx, [&] {
     check_config(ctx, *cfg, ctx->N, ctx->R);
     const int kind = kind_of(*cfg);
-    if (!eval_supported(kind)) throw ConfigError("rank_entities: device ranking covers transe / toruse");
+    if (!eval_supported(kind)) throw ConfigError("rank_entities: model not supported");
     if (protocol != 0 && protocol != 1) throw ConfigError("rank_entities: protocol must be 0 (raw) or 1 (filtered)");
     for (int64_t i = 0; i < q; ++i)
       if (heads[i] < 0 || heads[i] >= ctx->N || tails[i] < 0 || tails[i] >= ctx->N || relations[i] < 0 ||
@@ -1314,7 +1314,6 @@ extern "C" skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cf
     validate_ids(q, heads, relations, tails, ctx->N, ctx->R, host);
     DevBuf<int32_t> qd, fd;
     qd.ensure(3 * q);
-    SKG_CUDA(cudaMemcpyAsync(qd.p, host.data(), sizeof(int32_t) * 3 * q, cudaMemcpyHostToDevice, ctx->stream));
     DevBuf<uint64_t> table;
     uint64_t cap = 0;
     if (protocol == 1) {
@@ -1331,10 +1330,45 @@ extern "C" skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cf
     DevBuf<float> te;
     better.ensure(2 * q);
     te.ensure(2 * q);
-    eval_rank(kind, ctx->tables.p, ctx->N, ctx->R, static_cast<int>(ctx->de), qd.p, qd.p + q, qd.p + 2 * q, q,
-              protocol == 1 ? table.p : nullptr, cap, better.p, te.p, ctx->num_sms, ctx->stream);
+    const uint64_t* tp = protocol == 1 ? table.p : nullptr;
     std::vector<uint32_t> b(2 * q);
-    SKG_CUDA(cudaMemcpyAsync(b.data(), better.p, sizeof(uint32_t) * 2 * q, cudaMemcpyDeviceToHost, ctx->stream));
+    if (eval_exact(kind)) {  // TransE / TorusE: the stacked tables as they are
+      SKG_CUDA(cudaMemcpyAsync(qd.p, host.data(), sizeof(int32_t) * 3 * q, cudaMemcpyHostToDevice, ctx->stream));
+      eval_rank(kind, ctx->tables.p, ctx->tables.p + ctx->N * ctx->de, ctx->N, ctx->R, static_cast<int>(ctx->de),
+                qd.p, qd.p + q, qd.p + 2 * q, q, tp, cap, better.p, te.p, ctx->num_sms, ctx->stream);
+      SKG_CUDA(cudaMemcpyAsync(b.data(), better.p, sizeof(uint32_t) * 2 * q, cudaMemcpyDeviceToHost, ctx->stream));
+    } else {  // TransH / TransR: per relation, rank against the projected entity table
+      const int dr = static_cast<int>(ctx->dr);
+      DevBuf<float> pe;
+      pe.ensure(ctx->N * dr);
+      std::vector<std::vector<int64_t>> by_rel(static_cast<size_t>(ctx->R));
+      for (int64_t i = 0; i < q; ++i) by_rel[static_cast<size_t>(relations[i])].push_back(i);
+      std::vector<int32_t> sub;
+      std::vector<uint32_t> bs;
+      for (int64_t r = 0; r < ctx->R; ++r) {
+        const auto& ids = by_rel[static_cast<size_t>(r)];
+        if (ids.empty()) continue;
+        const int64_t m = static_cast<int64_t>(ids.size());
+        sub.resize(3 * m);
+        for (int64_t k = 0; k < m; ++k) {
+          sub[k] = host[ids[k]];
+          sub[m + k] = host[q + ids[k]];
+          sub[2 * m + k] = host[2 * q + ids[k]];
+        }
+        SKG_CUDA(cudaMemcpyAsync(qd.p, sub.data(), sizeof(int32_t) * 3 * m, cudaMemcpyHostToDevice, ctx->stream));
+        eval_project(kind, ctx->tables.p, ctx->proj.p, ctx->normals.p, r, ctx->N, static_cast<int>(ctx->de), dr, pe.p,
+                     ctx->stream);
+        eval_rank(kind, pe.p, ctx->tables.p + ctx->N * ctx->de, ctx->N, ctx->R, dr, qd.p, qd.p + m, qd.p + 2 * m, m,
+                  tp, cap, better.p, te.p, ctx->num_sms, ctx->stream);
+        bs.resize(2 * m);
+        SKG_CUDA(cudaMemcpyAsync(bs.data(), better.p, sizeof(uint32_t) * 2 * m, cudaMemcpyDeviceToHost, ctx->stream));
+        SKG_CUDA(cudaStreamSynchronize(ctx->stream));  // qd / better are reused by the next relation
+        for (int64_t k = 0; k < m; ++k) {
+          b[2 * ids[k]] = bs[2 * k];
+          b[2 * ids[k] + 1] = bs[2 * k + 1];
+        }
+      }
+    }
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int64_t i = 0; i < 2 * q; ++i) ranks[i] = static_cast<int64_t>(b[i]) + 1;
   });

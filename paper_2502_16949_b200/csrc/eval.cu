@@ -112,7 +112,8 @@ __device__ float row_energy(const float* __restrict__ a, const float* __restrict
 }
 
 struct EvalArgs {
-  const float* X;  // stacked [entity; relation]
+  const float* X;   // entity-side rows (the entity table, or a per-relation projected copy)
+  const float* Rt;  // relation rows (R x d)
   int64_t N, R;
   int d;
   const int32_t *qh, *qr, *qt;
@@ -131,7 +132,7 @@ __global__ void true_energy_kernel(EvalArgs a, float* __restrict__ te) {
   const int64_t qi = i >> 1;
   const int side = static_cast<int>(i & 1);
   const int64_t h = a.qh[qi], r = a.qr[qi], t = a.qt[qi];
-  const float* rel = a.X + (a.N + r) * a.d;
+  const float* rel = a.Rt + r * a.d;
   // the truth row is the query itself on both sides: (h, r, t)
   te[i] = row_energy<KIND>(a.X + h * a.d, a.X + t * a.d, rel, a.d, h == t);
   (void)side;
@@ -144,7 +145,7 @@ __global__ void rank_simple_kernel(EvalArgs a) {
   const int64_t h = a.qh[qi], r = a.qr[qi], t = a.qt[qi];
   const int64_t fixed = a.side == 0 ? h : t, truth = a.side == 0 ? t : h;
   const float te = a.te[2 * qi + a.side];
-  const float* rel = a.X + (a.N + r) * a.d;
+  const float* rel = a.Rt + r * a.d;
   uint32_t cnt = 0;
   for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < a.N;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kEvalThreads) rank_tiled_kernel(EvalArgs a, in
     const int qq = i / d4, c = i - qq * d4;
     reinterpret_cast<float4*>(F + qq * S)[c] = __ldg(reinterpret_cast<const float4*>(a.X + qfix[qq] * d) + c);
     reinterpret_cast<float4*>(Rr + qq * S)[c] =
-        __ldg(reinterpret_cast<const float4*>(a.X + (a.N + qr[qq]) * d) + c);
+        __ldg(reinterpret_cast<const float4*>(a.Rt + qr[qq] * d) + c);
   }
   const int qi = tid >> 4, cg = tid & 15;
   const float* fq = F + qi * S;
@@ -299,7 +300,73 @@ void configure_tiled() {
 
 }  // namespace
 
-bool eval_supported(int kind) { return kind == kTransE_L2 || kind == kTransE_L1 || kind == kTorusE_L2 || kind == kTorusE_L1; }
+bool eval_supported(int kind) { return kind >= kTransE_L2 && kind <= kTransR_L1; }
+bool eval_exact(int kind) { return kind <= kTorusE_L1; }
+
+// TransH / TransR rank through per-relation projected entity tables: the ht
+// row (a, r, b) scores ||P_r a - P_r b + r_vec|| with the linear map
+// P_r x = x - (w_r.x) w_r (TransH, models.hpp:99-103) or M_r x (TransR,
+// models.hpp:82-86) applied to both entities, which is the reference's
+// v = P_r (a - b) + r_vec up to rounding (these models are tolerance-only).
+__global__ void project_transh_kernel(const float* __restrict__ E, const float* __restrict__ w, int64_t N, int d,
+                                      float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; row < N;
+       row += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const float* x = E + row * d;
+    float s = 0.f;
+    for (int j = lane; j < d; j += 32) s = fmaf(__ldg(w + j), __ldg(x + j), s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    for (int j = lane; j < d; j += 32) out[row * d + j] = __fsub_rn(__ldg(x + j), __fmul_rn(s, __ldg(w + j)));
+  }
+}
+
+// out (N x dr) = E (N x de) M^T with M (dr x de) row-major: 64 x 64 output
+// tiles, 16-wide K slabs through shared memory, 4 x 4 outputs per thread.
+__global__ void __launch_bounds__(256) project_transr_kernel(const float* __restrict__ E, const float* __restrict__ M,
+                                                              int64_t N, int de, int dr, float* __restrict__ out) {
+  __shared__ float As[16][65], Bs[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int c0 = blockIdx.y * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < de; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int rr = i / 16, kk = i % 16;
+      As[kk][rr] = (r0 + rr < N && k0 + kk < de) ? __ldg(E + (r0 + rr) * de + k0 + kk) : 0.f;
+      Bs[kk][rr] = (c0 + rr < dr && k0 + kk < de) ? __ldg(M + static_cast<int64_t>(c0 + rr) * de + k0 + kk) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(As[kk][ty * 4 + i], Bs[kk][tx * 4 + j], acc[i][j]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t rr = r0 + ty * 4 + i;
+      const int cc = c0 + tx * 4 + j;
+      if (rr < N && cc < dr) out[rr * dr + cc] = acc[i][j];
+    }
+}
+
+void eval_project(int kind, const float* E, const float* proj, const float* normals, int64_t r, int64_t N, int de,
+                  int dr, float* out, cudaStream_t s) {
+  if (kind == kTransH_L2 || kind == kTransH_L1) {
+    project_transh_kernel<<<ceil_div(N * 32, 256), 256, 0, s>>>(E, normals + r * de, N, de, out);
+  } else {
+    dim3 grid(static_cast<unsigned>((N + 63) / 64), static_cast<unsigned>((dr + 63) / 64));
+    project_transr_kernel<<<grid, 256, 0, s>>>(E, proj + r * static_cast<int64_t>(dr) * de, N, de, dr, out);
+  }
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
 
 void configure_eval_kernels() {
   configure_tiled<kTransE_L2, 0>();
@@ -328,13 +395,14 @@ void eval_build_filter(const int32_t* h, const int32_t* r, const int32_t* t, int
   }
 }
 
-void eval_rank(int kind, const float* X, int64_t N, int64_t R, int d, const int32_t* qh, const int32_t* qr,
-               const int32_t* qt, int64_t q, const uint64_t* table, uint64_t cap, uint32_t* better, float* te,
-               int num_sms, cudaStream_t s) {
+void eval_rank(int kind, const float* X, const float* Rt, int64_t N, int64_t R, int d, const int32_t* qh,
+               const int32_t* qr, const int32_t* qt, int64_t q, const uint64_t* table, uint64_t cap, uint32_t* better,
+               float* te, int num_sms, cudaStream_t s) {
   SKG_CUDA(cudaMemsetAsync(better, 0, sizeof(uint32_t) * 2 * q, s));
   if (q == 0) return;
   EvalArgs a{};
   a.X = X;
+  a.Rt = Rt;
   a.N = N;
   a.R = R;
   a.d = d;
@@ -345,6 +413,8 @@ void eval_rank(int kind, const float* X, int64_t N, int64_t R, int d, const int3
   a.table = table;
   a.mask = cap ? cap - 1 : 0;
   a.better = better;
+  if (kind == kTransH_L2 || kind == kTransR_L2) kind = kTransE_L2;  // projected tables: ||P a - P b + r||
+  if (kind == kTransH_L1 || kind == kTransR_L1) kind = kTransE_L1;
   switch (kind) {
     case kTransE_L2: launch_kind<kTransE_L2>(a, te, num_sms, s); break;
     case kTransE_L1: launch_kind<kTransE_L1>(a, te, num_sms, s); break;

@@ -78,13 +78,16 @@ void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val,
 
 // link-prediction ranking (eval.cu)
 bool eval_supported(int kind);
+bool eval_exact(int kind);
+void eval_project(int kind, const float* E, const float* proj, const float* normals, int64_t r, int64_t N, int de,
+                  int dr, float* out, cudaStream_t s);
 void configure_eval_kernels();
 uint64_t eval_filter_capacity(int64_t nf);
 void eval_build_filter(const int32_t* h, const int32_t* r, const int32_t* t, int64_t nf, int64_t N, int64_t R,
                        uint64_t* table, uint64_t cap, cudaStream_t s);
-void eval_rank(int kind, const float* X, int64_t N, int64_t R, int d, const int32_t* qh, const int32_t* qr,
-               const int32_t* qt, int64_t q, const uint64_t* table, uint64_t cap, uint32_t* better, float* te,
-               int num_sms, cudaStream_t s);
+void eval_rank(int kind, const float* X, const float* Rt, int64_t N, int64_t R, int d, const int32_t* qh,
+               const int32_t* qr, const int32_t* qt, int64_t q, const uint64_t* table, uint64_t cap, uint32_t* better,
+               float* te, int num_sms, cudaStream_t s);
 
 // data parallel (dp.cu)
 void dp_destroy(skg_ctx* ctx);

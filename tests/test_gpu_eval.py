@@ -113,3 +113,37 @@ def test_trained_c1_shape_slice(eng, orc32):
         got = eng.rank_entities(cfg, qh, qr, qt, filt=filt)
         ref = orc32.rank_entities("transe", st, qh, qr, qt, norm="l2", filt=filt)
         assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("model,norm,de,dr", [("transh", "l2", 16, 16), ("transh", "l1", 128, 128),
+                                              ("transr", "l2", 16, 12), ("transr", "l1", 32, 32),
+                                              ("transr", "l2", 128, 128)])
+@pytest.mark.parametrize("filtered", [False, True])
+def test_ht_ranks_within_tolerance(eng, orc32, model, norm, de, dr, filtered):
+    """TransH / TransR scores are tolerance-only (Eigen reductions in the reference):
+    a device rank may differ from the oracle's only by candidates whose energy lies
+    within 1e-5 (relative) of the truth's."""
+    n, r, q = 400, 5, 12
+    rng = np.random.default_rng(de * 5 + dr + filtered)
+    st = orc32.init_store(model, n, r, de, dr, 3)
+    if model == "transr":
+        st.proj += rng.uniform(-0.2, 0.2, st.proj.shape).astype(np.float32)
+    h, rel, t = rng.integers(0, n, q), rng.integers(0, r, q), rng.integers(0, n, q)
+    h[0] = t[0]
+    filt = None
+    if filtered:
+        fh, fr, ft = rng.integers(0, n, 2000), rng.integers(0, r, 2000), rng.integers(0, n, 2000)
+        filt = (np.concatenate([fh, h]), np.concatenate([fr, rel]), np.concatenate([ft, t]))
+    cfg = ModelConfig.make(model, de, dr, norm)
+    eng.store_upload(cfg, st.entity, st.relation, st.proj, st.normals)
+    got = eng.rank_entities(cfg, h, rel, t, filt=filt)
+    ref = orc32.rank_entities(model, st, h, rel, t, norm=norm, filt=filt)
+    c = np.arange(n)
+    for i in range(q):
+        for side in (0, 1):
+            ch = np.full(n, h[i]) if side == 0 else c
+            ct = c if side == 0 else np.full(n, t[i])
+            e, _ = orc32.score_batch(model, st, ch, np.full(n, rel[i]), ct, norm=norm)
+            truth = t[i] if side == 0 else h[i]
+            near = np.abs(e - e[truth]) <= 1e-5 * np.maximum(1.0, np.abs(e[truth]))
+            assert abs(int(got[i, side]) - int(ref[i, side])) <= int(near.sum()) - 1, (i, side, got[i], ref[i])
