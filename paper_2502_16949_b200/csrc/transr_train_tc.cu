@@ -10,7 +10,7 @@
 // All three products are 3xTF32 (hi*hi + hi*lo + lo*hi, fp32-class). The
 // tensor core truncates a raw fp32 operand to tf32, so raw U / DZ in shared
 // memory are the "hi" A operands and only the "lo" parts are materialised
-// (in TMEM, as A operands of the third product). M_r arrives pre-split (hi =
+// (U and DZ hi / lo also sit in TMEM as the A operands of GEMM1 / GEMM2). M_r arrives pre-split (hi =
 // rna, lo = rest) in 16-wide K chunks through a 3-slot bulk-copy ring; GEMM3
 // contracts over rows, so DZ^T / U^T are staged 8 rows at a time.
 //
@@ -47,8 +47,7 @@ constexpr int kMmaWarp = 8, kRowWarp = 10;  // warp 9: ring loader
 // distinct bank groups per 128 B, so both the coalesced row gather (lane =
 // chunk) and the thread-per-row epilogue stores are conflict-free.
 __device__ __forceinline__ int tile_unit(int r, int c4) { return (c4 >> 3) * 1024 + r * 8 + ((c4 & 7) ^ (r & 7)); }
-__device__ __forceinline__ uint32_t tile_kstep(int ks) { return static_cast<uint32_t>((ks >> 2) * 16384 + (ks & 3) * 32); }
-constexpr uint32_t kTileSBO = 8 * 128;
+
 
 // Ring chunk of M_r: 128 (n) x 16 (k), hi then lo; unit (n, k4) = (n & 7) + (n >> 3) * 32 + k4 * 8.
 constexpr int kChunkK = 16;
@@ -70,7 +69,11 @@ constexpr int kG3Slots = 2;
 constexpr int kG3PerTile = kRows / kG3Rows;
 __device__ __forceinline__ int g3_off(int i, int k) { return (((i & 7) + (i >> 3) * 18 + (k >> 2) * 9) << 2) + (k & 3); }
 
-constexpr uint32_t kColV = 0, kColLo = 128, kColDU = 256, kColDM = 384;
+// TMEM columns: [0,128) U hi -> DZ hi and [128,256) U lo -> DZ lo (A operands
+// of GEMM1 / GEMM2 read straight from TMEM), [256,384) V, then dU (GEMM2
+// writes dU over the consumed V; GEMM1 of the next tile waits for the drain),
+// [384,512) dM.
+constexpr uint32_t kColHi = 0, kColLo = 128, kColV = 256, kColDU = 256, kColDM = 384;
 
 // Phase timestamps (clock64) for pipeline analysis, off unless enabled through
 // skg_debug_transr_trace: [CTA][tile < 16][event < 16].
@@ -299,6 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
         float lo[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) lo[q] = tc::tf32_trunc_lo(dz[q]);
+        tc::tmem_st16(tbase + lane_addr + kColHi + c, dz);
+        tc::tmem_st16(tbase + lane_addr + kColHi + c + 16, dz + 16);
         tc::tmem_st16(tbase + lane_addr + kColLo + c, lo);
         tc::tmem_st16(tbase + lane_addr + kColLo + c + 16, lo + 16);
         // transpose-reduce the 32 x 32 block: lane l ends with the column c + l sum
@@ -414,15 +419,17 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       }
 #pragma unroll 1
       for (int c = 0; c < kD; c += 16) {
-        float lo[16];
+        float hi[16], lo[16];
 #pragma unroll
         for (int q = 0; q < 16; q += 4) {
           const float4 u = *reinterpret_cast<const float4*>(S.U + 4 * tile_unit(p, (c + q) >> 2));
+          hi[q] = u.x, hi[q + 1] = u.y, hi[q + 2] = u.z, hi[q + 3] = u.w;
           lo[q] = tc::tf32_trunc_lo(u.x);
           lo[q + 1] = tc::tf32_trunc_lo(u.y);
           lo[q + 2] = tc::tf32_trunc_lo(u.z);
           lo[q + 3] = tc::tf32_trunc_lo(u.w);
         }
+        tc::tmem_st16(tbase + lane_addr + kColHi + c, hi);
         tc::tmem_st16(tbase + lane_addr + kColLo + c, lo);
       }
       tc::tmem_wait_st();
@@ -469,7 +476,6 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issue
     const uint32_t id = idesc128();
-    const uint32_t sU = tc::smem_u32(S.U), sDZ = tc::smem_u32(S.DZ);
     uint32_t rn = 0, g3n = 0, nrun = 0;
     int run = -1;
     for (uint32_t it = 0; it < ntile; ++it) {
@@ -480,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       run = k;
       const bool last_of_run = (t + 1 == t1) || (a.seg_tiles[k + 1] <= t + 1);
       tc::mbar_wait(&S.u_full, it & 1);
+      if (it > 0) tc::mbar_wait(&S.du_empty, (it - 1) & 1);  // V shares columns with the drained dU
       tc::fence_after();
       trace(it, 5);
       // GEMM1: V = U M_r^T
@@ -491,11 +498,10 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const int ks = c * 2 + kk;
-          const uint64_t ad = tc::make_desc_sw128(sU + tile_kstep(ks), kTileSBO);
           const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
           const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
-          tc::mma_ss_elect(tbase + kColV, ad, bhd, id, ks > 0 ? 1u : 0u);
-          tc::mma_ss_elect(tbase + kColV, ad, bld, id, 1u);
+          tc::mma_ts_elect(tbase + kColV, tbase + kColHi + ks * 8, bhd, id, ks > 0 ? 1u : 0u);
+          tc::mma_ts_elect(tbase + kColV, tbase + kColHi + ks * 8, bld, id, 1u);
           tc::mma_ts_elect(tbase + kColV, tbase + kColLo + ks * 8, bhd, id, 1u);
         }
         tc::commit_elect(&S.ring_empty[s]);
@@ -507,11 +513,10 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
         tc::mbar_wait(&S.dm_empty, (nrun - 1) & 1);
         tc::fence_after();
       }
-      // GEMM2 (dU = DZ M_r; sDZ raw = hi, DZ lo from TMEM) interleaved with the
+      // GEMM2 (dU = DZ M_r; DZ hi / lo from TMEM) interleaved with the
       // GEMM3 slots: one GEMM2 chunk after every second slot keeps the tensor
       // pipe busy while the producers refill the slot just released.
       tc::mbar_wait(&S.dz_full, it & 1);
-      if (it > 0) tc::mbar_wait(&S.du_empty, (it - 1) & 1);
       tc::fence_after();
       trace(it, 9);
       for (int s3 = 0; s3 < kG3PerTile; ++s3, ++g3n) {
@@ -538,11 +543,10 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk) {
             const int ks = c * 2 + kk;
-            const uint64_t ad = tc::make_desc_sw128(sDZ + tile_kstep(ks), kTileSBO);
             const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
             const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
-            tc::mma_ss_elect(tbase + kColDU, ad, bhd, id, ks > 0 ? 1u : 0u);
-            tc::mma_ss_elect(tbase + kColDU, ad, bld, id, 1u);
+            tc::mma_ts_elect(tbase + kColDU, tbase + kColHi + ks * 8, bhd, id, ks > 0 ? 1u : 0u);
+            tc::mma_ts_elect(tbase + kColDU, tbase + kColHi + ks * 8, bld, id, 1u);
             tc::mma_ts_elect(tbase + kColDU, tbase + kColLo + ks * 8, bhd, id, 1u);
           }
           tc::commit_elect(&S.ring_empty[s]);
