@@ -8,11 +8,12 @@
 //   dM += DZ^T U          (GEMM3)     accumulated in TMEM over the relation run
 //   dU  = DZ M_r          (GEMM2)     -> res_u rows for the entity segments
 // All three products are 3xTF32 (hi*hi + hi*lo + lo*hi, fp32-class). The
-// tensor core truncates a raw fp32 operand to tf32, so raw U / DZ in shared
-// memory are the "hi" A operands and only the "lo" parts are materialised
-// (U and DZ hi / lo also sit in TMEM as the A operands of GEMM1 / GEMM2). M_r arrives pre-split (hi =
+// tensor core truncates a raw fp32 operand to tf32, so raw U / DZ serve as the
+// "hi" A operands and only lo = x - trunc(x) is materialised; GEMM1 / GEMM2
+// read both from TMEM (tcgen05.mma [a_tmem]). M_r arrives pre-split (hi =
 // rna, lo = rest) in 16-wide K chunks through a 3-slot bulk-copy ring; GEMM3
-// contracts over rows, so DZ^T / U^T are staged 8 rows at a time.
+// contracts over rows, so DZ^T / U^T are staged 8 rows at a time from the
+// shared-memory copies of U and DZ.
 //
 // Roles (320 threads):
 //   warps 0-3  epilogue   thread = row = TMEM lane: score, hinge, DZ, sum(dz),
@@ -21,7 +22,7 @@
 //   warp  8    MMA issue  (whole warp, elect.sync inside the asm)
 //   warp  9    ring loader (bulk copies of M_r chunks)
 //   warp 10    row-id chase (tile -> incidence rows -> head / tail), two tiles ahead
-// TMEM columns: [0,128) V | [128,256) U lo, then DZ lo | [256,384) dU | [384,512) dM.
+// TMEM columns: see kColHi .. kColDM below.
 //
 // The CTA-range / relation-run partition (slot = CTA + run ordinal) is the one
 // transr_tc_apply_kernel (transr_tc.cu) reduces in tile order.
