@@ -661,17 +661,63 @@ int grid_for(int64_t n) {
   return static_cast<int>(b < 1 ? 1 : (b > 4096 ? 4096 : b));
 }
 
-__global__ void narrow_ids_kernel(const int64_t* __restrict__ src, int64_t m, int64_t limit,
-                                  int32_t* __restrict__ dst, uint32_t* __restrict__ first_bad,
-                                  uint32_t* __restrict__ changed) {
+// One id array to narrow: int64 source (HBM or UVA-mapped pinned host), int32
+// destination, exclusive upper bound and the slot of its first-bad index.
+struct NarrowJob {
+  const int64_t* src;
+  int32_t* dst;
+  int64_t limit;
+  uint32_t* bad;
+};
+struct NarrowJobs {
+  NarrowJob j[3];
+};
+
+// Every array of one set_* call in one launch (blockIdx.y = array): 16-byte
+// loads, four in flight per thread, so the pinned-host reads keep enough PCIe
+// requests outstanding to run at DMA speed; validation (TripleBatch::validate,
+// incidence.hpp:18-31), narrowing and the changed-data check in the same pass.
+__global__ void __launch_bounds__(256) narrow_ids_kernel(NarrowJobs jobs, int64_t m, uint32_t* __restrict__ changed) {
+  const NarrowJob J = jobs.j[blockIdx.y];
   bool diff = false;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t v = src[i];
-    if (v < 0 || v >= limit) atomicMin(first_bad, static_cast<uint32_t>(i));
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(J.src) | reinterpret_cast<uintptr_t>(J.dst) * 2) & 15) == 0;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t n2 = m / 2;
+    const longlong2* s2 = reinterpret_cast<const longlong2*>(J.src);
+    int2* d2 = reinterpret_cast<int2*>(J.dst);
+    constexpr int U = 4;
+    for (int64_t base = tid; base < n2; base += U * stride) {
+      longlong2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = base + u * stride;
+        if (k < n2) v[u] = s2[k];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = base + u * stride;
+        if (k >= n2) break;
+        int2 w;
+        if (v[u].x < 0 || v[u].x >= J.limit) atomicMin(J.bad, static_cast<uint32_t>(2 * k));
+        if (v[u].y < 0 || v[u].y >= J.limit) atomicMin(J.bad, static_cast<uint32_t>(2 * k + 1));
+        w.x = static_cast<int32_t>(v[u].x);
+        w.y = static_cast<int32_t>(v[u].y);
+        const int2 old = d2[k];
+        diff |= old.x != w.x || old.y != w.y;
+        d2[k] = w;
+      }
+    }
+    done = 2 * n2;
+  }
+  for (int64_t i = done + tid; i < m; i += stride) {
+    const int64_t v = J.src[i];
+    if (v < 0 || v >= J.limit) atomicMin(J.bad, static_cast<uint32_t>(i));
     const int32_t w = static_cast<int32_t>(v);
-    diff |= dst[i] != w;
-    dst[i] = w;
+    diff |= J.dst[i] != w;
+    J.dst[i] = w;
   }
   if (diff) *changed = 0;
 }
@@ -813,6 +859,7 @@ void upload_narrow(skg_ctx* ctx, const int64_t* const* srcs, int32_t* const* dst
   ctx->stage_i64.ensure(3 * m + 1);
   ctx->bad_idx.ensure(3);
   SKG_CUDA(cudaMemsetAsync(ctx->bad_idx.p, 0xFF, sizeof(uint32_t) * 3, ctx->stream));
+  NarrowJobs jobs{};
   for (int k = 0; k < count; ++k) {
     // Pinned (page-locked, UVA-mapped) caller arrays are read by the narrowing
     // kernel straight over PCIe: copy, validation and narrowing in one pass.
@@ -828,10 +875,12 @@ void upload_narrow(skg_ctx* ctx, const int64_t* const* srcs, int32_t* const* dst
                                ctx->stream));
       src = ctx->stage_i64.p + k * m;
     }
-    narrow_ids_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(src, m, limits[k], dsts[k], ctx->bad_idx.p + slots[k],
-                                                            ctx->bad_idx.p + 2);
-    count_launch();
+    jobs.j[k] = NarrowJob{src, dsts[k], limits[k], ctx->bad_idx.p + slots[k]};
   }
+  const int64_t per = (m / 2 + 255) / 256;  // blocks for one 16-byte load per thread
+  const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(per, 4L * ctx->num_sms)));
+  narrow_ids_kernel<<<dim3(gx, count), 256, 0, ctx->stream>>>(jobs, m, ctx->bad_idx.p + 2);
+  count_launch();
   SKG_LAUNCH_CHECK();
   SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->bad_idx.p, sizeof(uint32_t) * 3, cudaMemcpyDeviceToHost, ctx->stream));
   SKG_CUDA(cudaStreamSynchronize(ctx->stream));
