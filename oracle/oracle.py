@@ -16,7 +16,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 BUILD = os.path.join(HERE, "_build")
 
-MODELS = {"transe": 0, "transr": 1, "transh": 2, "toruse": 3}
+MODELS = {"transe": 0, "transr": 1, "transh": 2, "toruse": 3, "distmult": 4, "complex": 5, "rotate": 6}
+COMPLEX = ("complex", "rotate")  # tables of interleaved (re, im) pairs: 2 * dim columns
 NORMS = {"l1": 0, "l2": 1}
 STATUS_NAMES = {1: "ShapeError", 2: "ConfigError", 3: "DegenerateTripleError",
                 4: "TrainingError", 5: "ParseError", 7: "Error"}
@@ -159,6 +160,10 @@ class Oracle:
     def _cfg(model, de, dr, norm="l2"):
         return _ModelConfig(MODELS[model], NORMS[norm], de, dr)
 
+    def _cfg_for(self, model, store, norm="l2"):
+        w = 2 if model in COMPLEX else 1
+        return self._cfg(model, store.entity.shape[1] // w, store.relation.shape[1] // w, norm)
+
     def train_config(self, lr=4e-4, margin=0.5, epochs=200, batch_size=1024, seed=0,
                      scheduler=None, shuffle=True, resample_negatives=False, renorm_entities=False):
         every, factor = scheduler if scheduler else (50, 0.5)
@@ -188,8 +193,9 @@ class Oracle:
         return h[s:].copy(), r[s:].copy(), t[s:].copy()
 
     def init_store(self, model, n_ent, n_rel, de, dr, seed) -> Store:
-        e = np.empty((n_ent, de), self.dtype)
-        r = np.empty((n_rel, dr), self.dtype)
+        w = 2 if model in COMPLEX else 1
+        e = np.empty((n_ent, w * de), self.dtype)
+        r = np.empty((n_rel, w * dr), self.dtype)
         p = np.empty((n_rel, dr * de), self.dtype) if model == "transr" else None
         n = np.empty((n_rel, de), self.dtype) if model == "transh" else None
         self._check(self.lib.orc_init_store(MODELS[model], n_ent, n_rel, de, dr, seed,
@@ -215,7 +221,7 @@ class Oracle:
         col = np.empty(3 * m, np.int64)
         val = np.empty(3 * m, self.dtype)
         nnz = C.c_int64()
-        self._check(self.lib.orc_build_incidence({"ht": 0, "hrt": 1}[kind], m, _p(h), _p(r), _p(t),
+        self._check(self.lib.orc_build_incidence({"ht": 0, "hrt": 1, "mult": 2, "mult_conj": 3}[kind], m, _p(h), _p(r), _p(t),
                                                  n_ent, n_rel, _p(rp), _p(col), _p(val), C.byref(nnz)))
         return rp, col[:nnz.value].copy(), val[:nnz.value].copy()
 
@@ -253,9 +259,9 @@ class Oracle:
         h, r, t = _i64(h), _i64(r), _i64(t)
         de, dr = store.entity.shape[1], store.relation.shape[1]
         m = len(h)
-        cfg = self._cfg(model, de, dr, norm)
+        cfg = self._cfg_for(model, store, norm)
         scores = np.empty(m, self.dtype)
-        v = np.empty((m, dr), self.dtype) if model in ("transe", "transr", "transh") else None
+        v = np.empty((m, dr), self.dtype) if model in ("transe", "transr", "transh", "rotate") else None
         u = np.empty((m, de), self.dtype) if model in ("transr", "transh") else None
         dl = np.empty((m, de), self.dtype) if model == "toruse" else None
         st = self._store(store)
@@ -266,7 +272,7 @@ class Oracle:
     def rank_entities(self, model, store: Store, h, r, t, norm="l2", filt=None):
         """rank_entity (eval.cpp:16-63) of every query, tail then head: int64 (q, 2)."""
         h, r, t = _i64(h), _i64(r), _i64(t)
-        cfg = self._cfg(model, store.entity.shape[1], store.relation.shape[1], norm)
+        cfg = self._cfg_for(model, store, norm)
         st = self._store(store)
         ranks = np.empty((len(h), 2), np.int64)
         if filt is None:
@@ -281,7 +287,7 @@ class Oracle:
 
     def score_backward(self, model, store: Store, h, r, t, up, grads: Store, norm="l2"):
         h, r, t, up = _i64(h), _i64(r), _i64(t), self._f(up)
-        cfg = self._cfg(model, store.entity.shape[1], store.relation.shape[1], norm)
+        cfg = self._cfg_for(model, store, norm)
         st, gs = self._store(store), self._store(grads)
         self._check(self.lib.orc_score_backward(C.byref(cfg), C.byref(st), len(h), _p(h), _p(r), _p(t),
                                                 _p(up), C.byref(gs)))
@@ -305,7 +311,7 @@ class Oracle:
 
     def train_epoch(self, model, store: Store, pos, neg, tc, epoch, lr, norm="l2"):
         (ph, pr, pt), (nh, nt) = [_i64(a) for a in pos], [_i64(a) for a in neg]
-        cfg = self._cfg(model, store.entity.shape[1], store.relation.shape[1], norm)
+        cfg = self._cfg_for(model, store, norm)
         st = self._store(store)
         rep = _EpochReport()
         self._check(self.lib.orc_train_epoch(C.byref(cfg), C.byref(st), len(ph), _p(ph), _p(pr), _p(pt),
@@ -314,7 +320,7 @@ class Oracle:
 
     def train_batches(self, model, store: Store, pos, neg, tc, epoch, lr, b0, nb, norm="l2"):
         (ph, pr, pt), (nh, nt) = [_i64(a) for a in pos], [_i64(a) for a in neg]
-        cfg = self._cfg(model, store.entity.shape[1], store.relation.shape[1], norm)
+        cfg = self._cfg_for(model, store, norm)
         st = self._store(store)
         secs, ls = C.c_double(), C.c_double()
         self._check(self.lib.orc_train_batches(C.byref(cfg), C.byref(st), len(ph), _p(ph), _p(pr), _p(pt),
@@ -324,7 +330,7 @@ class Oracle:
 
     def fit(self, model, store: Store, h, r, t, tc, norm="l2"):
         h, r, t = _i64(h), _i64(r), _i64(t)
-        cfg = self._cfg(model, store.entity.shape[1], store.relation.shape[1], norm)
+        cfg = self._cfg_for(model, store, norm)
         st = self._store(store)
         reps = (_EpochReport * max(1, tc.epochs))()
         self._check(self.lib.orc_fit(C.byref(cfg), C.byref(st), len(h), _p(h), _p(r), _p(t), C.byref(tc), reps))

@@ -3,7 +3,9 @@
 // liboracle_f32.so and double in liboracle_f64.so. Errors come back as status
 // codes mirroring skg_status (include/skge_b200.h) plus orc_last_error().
 #include <chrono>
+#include <algorithm>
 #include <cstring>
+#include <limits>
 #include <random>
 #include <string>
 #include <unordered_set>
@@ -177,12 +179,13 @@ int orc_epoch_order(Index m, std::uint64_t seed, int shuffle, Index epoch, Index
   });
 }
 
-// kind 0 = ht (incidence.hpp:38), 1 = hrt (:62). row_ptr has m+1 slots, col/val 3m.
+// kind 0 = ht (incidence.hpp:38), 1 = hrt (:62), 2 = multiplicative, 3 = multiplicative
+// with the conjugate tail marker (:93). row_ptr has m+1 slots, col/val 3m.
 int orc_build_incidence(int kind, Index m, const Index* h, const Index* r, const Index* t,
                         Index n_ent, Index n_rel, Index* row_ptr, Index* col, Real* val, Index* nnz) {
   return guard([&] {
     TripleBatch b = mk_batch(m, h, r, t, n_ent, n_rel);
-    CsrMatrix c = coo_to_csr(kind == 0 ? build_ht(b) : build_hrt(b));
+    CsrMatrix c = coo_to_csr(kind == 0 ? build_ht(b) : kind == 1 ? build_hrt(b) : build_multiplicative(b, kind == 3));
     std::memcpy(row_ptr, c.row_ptr.data(), sizeof(Index) * c.row_ptr.size());
     std::memcpy(col, c.col_idx.data(), sizeof(Index) * c.col_idx.size());
     std::memcpy(val, c.vals.data(), sizeof(Real) * c.vals.size());
@@ -266,7 +269,8 @@ int orc_score_batch(const orc_model_config* cfg, const orc_store* st, Index m, c
 // (the order evaluate() visits them, eval.cpp:80-86): ranks[2i] = tail rank,
 // ranks[2i+1] = head rank. filtered != 0: competing candidates whose triple is
 // in the nf filter triples (TripleFilter, eval.hpp:25-45) are skipped; the
-// query's own entity never is. Translational models only (no self exclusion).
+// query's own entity never is. Multiplicative models exclude the self-loop
+// candidate (energy +inf, eval.cpp:36-37); energies carry energy_sign.
 int orc_rank_entities(const orc_model_config* cfg, const orc_store* st, Index q, const Index* qh,
                       const Index* qr, const Index* qt, int filtered, Index nf, const Index* fh,
                       const Index* fr, const Index* ft, Index* ranks) {
@@ -281,24 +285,33 @@ int orc_rank_entities(const orc_model_config* cfg, const orc_store* st, Index q,
     std::unordered_set<std::uint64_t> known;
     if (filtered)
       for (Index i = 0; i < nf; ++i) known.insert(key(fh[i], fr[i], ft[i]));
-    std::vector<Index> ch(n), cr(n), ct(n);
+    const bool no_self = is_multiplicative_model(mc.model);  // eval.cpp:24, 36-37
+    const Real sign = energy_sign(mc.model);
+    std::vector<Index> ch, cr, ct, cand;
+    std::vector<Real> energy(static_cast<size_t>(n));
     for (Index i = 0; i < q; ++i) {
       const Index h = qh[i], r = qr[i], t = qt[i];
       if (h < 0 || h >= n || t < 0 || t >= n || r < 0 || r >= nr) throw ShapeError("rank_entity: query ids out of range");
       for (int side = 0; side < 2; ++side) {  // 0 = Tail, 1 = Head
+        const Index fixed = side == 0 ? h : t;
+        ch.clear(), cr.clear(), ct.clear(), cand.clear();
         for (Index c = 0; c < n; ++c) {
-          ch[c] = side == 0 ? h : c;
-          cr[c] = r;
-          ct[c] = side == 0 ? c : t;
+          if (no_self && c == fixed) continue;  // unrepresentable candidate, ranks worst
+          cand.push_back(c);
+          ch.push_back(side == 0 ? h : c);
+          cr.push_back(r);
+          ct.push_back(side == 0 ? c : t);
         }
-        ScoreBatch sb = score_batch(mc, s, mk_batch(n, ch.data(), cr.data(), ct.data(), n, nr));
+        ScoreBatch sb = score_batch(mc, s, mk_batch(static_cast<Index>(cand.size()), ch.data(), cr.data(), ct.data(), n, nr));
+        std::fill(energy.begin(), energy.end(), std::numeric_limits<Real>::infinity());
+        for (size_t k = 0; k < cand.size(); ++k) energy[cand[k]] = sign * sb.scores[k];
         const Index truth = side == 0 ? t : h;
-        const Real te = sb.scores[truth];  // energy_sign = +1 for the translational models
+        const Real te = energy[truth];
         Index better = 0;
         for (Index c = 0; c < n; ++c) {
           if (c == truth) continue;
           if (filtered && known.count(side == 0 ? key(h, r, c) : key(c, r, t))) continue;
-          if (sb.scores[c] < te) ++better;
+          if (energy[c] < te) ++better;
         }
         ranks[2 * i + side] = better + 1;
       }
@@ -389,11 +402,17 @@ int orc_train_batches(const orc_model_config* cfg, orc_store* st, Index m, const
         nb2.heads.push_back(neg.heads[i]), nb2.relations.push_back(neg.relations[i]), nb2.tails.push_back(neg.tails[i]);
       }
       ScoreBatch ps = score_batch(mc, s, pb), ns = score_batch(mc, s, nb2);
-      LossGrad lg = margin_ranking_loss(ps.scores, ns.scores, t.margin);
+      const Real sign = energy_sign(mc.model);
+      auto sg = [sign](const std::vector<Real>& v) {
+        std::vector<Real> o(v.size());
+        for (size_t k = 0; k < v.size(); ++k) o[k] = sign * v[k];
+        return o;
+      };
+      LossGrad lg = margin_ranking_loss(sg(ps.scores), sg(ns.scores), t.margin);
       ls += lg.loss * Real(hi - lo);
       grads.entity.set_zero(), grads.relation.set_zero(), grads.proj.set_zero(), grads.normals.set_zero();
-      score_backward(mc, s, ps, lg.d_pos, grads);
-      score_backward(mc, s, ns, lg.d_neg, grads);
+      score_backward(mc, s, ps, sg(lg.d_pos), grads);
+      score_backward(mc, s, ns, sg(lg.d_neg), grads);
       sgd_step(s, grads, lr);
     }
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -7,6 +7,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <numeric>
 #include <random>
 #include <unordered_set>
@@ -25,6 +26,9 @@ const char* model_name(ModelKind m) {
     case ModelKind::TransR: return "transr";
     case ModelKind::TransH: return "transh";
     case ModelKind::TorusE: return "toruse";
+    case ModelKind::DistMult: return "distmult";
+    case ModelKind::ComplEx: return "complex";
+    case ModelKind::RotatE: return "rotate";
   }
   return "unknown";
 }
@@ -273,6 +277,27 @@ CooMatrix build_hrt(const TripleBatch& b) {  // incidence.hpp:62-85
   return out;
 }
 
+// incidence.hpp:93-121: +1 at head and relation, the tail +1 or the -1
+// conjugate marker; head == tail is not representable.
+CooMatrix build_multiplicative(const TripleBatch& b, bool conjugate_tail) {
+  b.validate();
+  CooMatrix out;
+  out.num_rows = b.size();
+  out.num_cols = b.num_entities + b.num_relations;
+  const Real tail_marker = conjugate_tail ? Real(-1) : Real(1);
+  for (Index i = 0; i < b.size(); ++i) {
+    if (b.heads[i] == b.tails[i])
+      throw DegenerateTripleError("triple " + std::to_string(i) +
+                                  ": head == tail is not representable in the "
+                                  "multiplicative incidence layout");
+    out.rows.push_back(i), out.cols.push_back(b.heads[i]), out.vals.push_back(Real(1));
+    out.rows.push_back(i), out.cols.push_back(b.tails[i]), out.vals.push_back(tail_marker);
+    out.rows.push_back(i), out.cols.push_back(b.num_entities + b.relations[i]),
+        out.vals.push_back(Real(1));
+  }
+  return out;
+}
+
 // ------------------------------------------------------------------ norms.hpp
 
 Real squared_sum(const Real* v, Index n) {  // norms.hpp:19-36
@@ -384,7 +409,7 @@ namespace {
 
 void check_config(const ModelConfig& cfg, const Store& store, const TripleBatch& b) {  // models.hpp:65-76
   cfg.validate();
-  if (store.dim_entity() != cfg.dim_entity || store.dim_relation() != cfg.dim_relation)
+  if (store.dim_entity() != cfg.width_entity() || store.dim_relation() != cfg.width_relation())
     throw ConfigError("store dimensions do not match the model config");
   if (store.num_entities() != b.num_entities || store.num_relations() != b.num_relations)
     throw ConfigError("store table sizes do not match the batch id space");
@@ -553,6 +578,195 @@ void transh_backward(const ModelConfig& cfg, const Store& store, const ScoreBatc
 
 }  // namespace
 
+// ---- multiplicative family (models.cpp:201-263) ----
+//
+// Complex arithmetic is restated on interleaved (re, im) Real pairs with the
+// operation order of std::complex / Eigen's packet product (no FMA):
+// (a * b).re = a.re*b.re - a.im*b.im, (a * b).im = a.re*b.im + a.im*b.re.
+// semiring_detail::selects (sparse.hpp:72-77): a marker with positive real
+// part selects the operand, a negative one its conjugate.
+
+namespace {
+
+inline bool selects(Real marker) { return marker > Real(0); }
+
+// acc *= x (or conj(x)) elementwise over d coordinates (TimesTimes, sparse.hpp:94-106)
+void times_row(Real* acc, const Real* x, Index d, bool cplx, bool conj) {
+  if (!cplx) {
+    for (Index j = 0; j < d; ++j) acc[j] = acc[j] * x[j];
+    return;
+  }
+  for (Index j = 0; j < d; ++j) {
+    const Real ar = acc[2 * j], ai = acc[2 * j + 1];
+    const Real br = x[2 * j], bi = conj ? -x[2 * j + 1] : x[2 * j + 1];
+    const Real t0 = ar * br, t1 = ai * bi, t2 = ar * bi, t3 = ai * br;
+    acc[2 * j] = t0 - t1;
+    acc[2 * j + 1] = t2 + t3;
+  }
+}
+
+void set_identity(Real* acc, Index d, bool cplx) {
+  for (Index j = 0; j < d; ++j) {
+    if (cplx) {
+      acc[2 * j] = Real(1);
+      acc[2 * j + 1] = Real(0);
+    } else {
+      acc[j] = Real(1);
+    }
+  }
+}
+
+// spmm<TimesTimes> row (sparse.hpp:254-262): identity, then every entry in stored order.
+void times_spmm_row(const CsrMatrix& a, const Stacked& x, Index i, Index d, bool cplx, Real* out) {
+  set_identity(out, d, cplx);
+  for (Index p = a.row_ptr[i]; p < a.row_ptr[i + 1]; ++p)
+    times_row(out, x.row(a.col_idx[p]), d, cplx, !selects(a.vals[p]));
+}
+
+Real sum_row(const Real* v, Index n) {  // norms.hpp:76-80
+  Real s = 0;
+  for (Index j = 0; j < n; ++j) s += v[j];
+  return s;
+}
+Real sum_real(const Real* v, Index n) {  // norms.hpp:82-86 (v interleaved)
+  Real s = 0;
+  for (Index j = 0; j < n; ++j) s += v[2 * j];
+  return s;
+}
+Real cabs(Real re, Real im) { return std::abs(std::complex<Real>(re, im)); }
+Real sum_abs(const Real* v, Index n) {  // norms.hpp:88-92
+  Real s = 0;
+  for (Index j = 0; j < n; ++j) s += cabs(v[2 * j], v[2 * j + 1]);
+  return s;
+}
+
+ScoreBatch product_forward(const ModelConfig& cfg, const Store& store, const TripleBatch& b) {  // models.cpp:203-231
+  const bool cplx = cfg.model == ModelKind::ComplEx;
+  ScoreBatch sb;
+  sb.batch = b;
+  sb.a = coo_to_csr(build_multiplicative(b, cplx));
+  const Index m = b.size(), d = cfg.dim_entity;
+  const Stacked x{&store.entity, &store.relation};
+  sb.scores.assign(static_cast<size_t>(m), Real(0));
+  parallel_for(m, [&](Index lo, Index hi) {
+    std::vector<Real> prow(static_cast<size_t>(cfg.width_entity()));
+    for (Index i = lo; i < hi; ++i) {
+      times_spmm_row(sb.a, x, i, d, cplx, prow.data());
+      sb.scores[i] = cplx ? sum_real(prow.data(), d) : sum_row(prow.data(), d);
+    }
+  });
+  return sb;
+}
+
+ScoreBatch rotate_forward(const ModelConfig& cfg, const Store& store, const TripleBatch& b) {  // models.cpp:233-248
+  ScoreBatch sb;
+  sb.batch = b;
+  sb.a = coo_to_csr(build_multiplicative(b, true));
+  const Index m = b.size(), d = cfg.dim_entity;
+  const Stacked x{&store.entity, &store.relation};
+  sb.v = Mat(m, 2 * d);
+  sb.scores.assign(static_cast<size_t>(m), Real(0));
+  parallel_for(m, [&](Index lo, Index hi) {
+    std::vector<Real> prod(static_cast<size_t>(2 * d)), sub(static_cast<size_t>(2 * d));
+    for (Index i = lo; i < hi; ++i) {  // spmm_mulsub, sparse.hpp:345-365
+      set_identity(prod.data(), d, true);
+      for (Index j = 0; j < 2 * d; ++j) sub[j] = Real(0);
+      for (Index p = sb.a.row_ptr[i]; p < sb.a.row_ptr[i + 1]; ++p) {
+        const Real* xr = x.row(sb.a.col_idx[p]);
+        if (selects(sb.a.vals[p])) {
+          times_row(prod.data(), xr, d, true, false);
+        } else {
+          for (Index j = 0; j < 2 * d; ++j) sub[j] = sub[j] + xr[j];
+        }
+      }
+      Real* q = sb.v.row(i);
+      for (Index j = 0; j < 2 * d; ++j) q[j] = prod[j] - sub[j];
+      sb.scores[i] = sum_abs(q, d);
+    }
+  });
+  return sb;
+}
+
+// spmm_product_grad_add (sparse.hpp:315-339): entry p of row i receives
+// upstream_i * (product of the row's other operands), conjugated when p selects.
+// Sequential over rows and entries (output rows collide across triples).
+void product_backward(const ModelConfig& cfg, const Store& store, const ScoreBatch& sb,
+                      const std::vector<Real>& up, Gradients& g) {
+  const bool cplx = cfg.model == ModelKind::ComplEx;
+  const Index d = cfg.dim_entity, w = cfg.width_entity();
+  const Stacked x{&store.entity, &store.relation};
+  StackedMut sink{&g.entity, &g.relation};
+  const CsrMatrix& a = sb.a;
+  std::vector<Real> others(static_cast<size_t>(w));
+  for (Index i = 0; i < a.num_rows; ++i) {
+    const Index lo = a.row_ptr[i], hi = a.row_ptr[i + 1];
+    for (Index p = lo; p < hi; ++p) {
+      set_identity(others.data(), d, cplx);
+      for (Index q = lo; q < hi; ++q) {
+        if (q == p) continue;
+        times_row(others.data(), x.row(a.col_idx[q]), d, cplx, !selects(a.vals[q]));
+      }
+      Real* out = sink.row(a.col_idx[p]);
+      const bool conj = cplx && selects(a.vals[p]);
+      for (Index j = 0; j < w; ++j) {
+        const Real o = (conj && (j & 1)) ? -others[j] : others[j];
+        const Real t = up[i] * o;
+        out[j] = out[j] + t;
+      }
+    }
+  }
+}
+
+// modulus_direction (norms.hpp:129-135) + spmm_mulsub_grad_add (sparse.hpp:367-391)
+void rotate_backward(const ModelConfig& cfg, const Store& store, const ScoreBatch& sb,
+                     const std::vector<Real>& up, Gradients& g) {
+  const Index d = cfg.dim_entity, m = sb.batch.size();
+  Mat dq(m, 2 * d);
+  parallel_for(m, [&](Index lo, Index hi) {
+    for (Index i = lo; i < hi; ++i) {
+      const Real* q = sb.v.row(i);
+      Real* o = dq.row(i);
+      for (Index j = 0; j < d; ++j) {
+        const Real re = q[2 * j], im = q[2 * j + 1];
+        const Real m2 = re * re + im * im;
+        const Real inv = up[i] / std::sqrt(m2 + kNormEps);
+        o[2 * j] = re * inv;
+        o[2 * j + 1] = im * inv;
+      }
+    }
+  });
+  const Stacked x{&store.entity, &store.relation};
+  StackedMut sink{&g.entity, &g.relation};
+  const CsrMatrix& a = sb.a;
+  std::vector<Real> others(static_cast<size_t>(2 * d));
+  for (Index i = 0; i < a.num_rows; ++i) {
+    const Index lo = a.row_ptr[i], hi = a.row_ptr[i + 1];
+    const Real* dqi = dq.row(i);
+    for (Index p = lo; p < hi; ++p) {
+      Real* out = sink.row(a.col_idx[p]);
+      if (!selects(a.vals[p])) {
+        for (Index j = 0; j < 2 * d; ++j) out[j] = out[j] - dqi[j];
+        continue;
+      }
+      set_identity(others.data(), d, true);
+      for (Index q = lo; q < hi; ++q) {
+        if (q == p || !selects(a.vals[q])) continue;
+        times_row(others.data(), x.row(a.col_idx[q]), d, true, false);
+      }
+      for (Index j = 0; j < d; ++j) {  // out += dq * conj(others)
+        const Real ar = dqi[2 * j], ai = dqi[2 * j + 1];
+        const Real br = others[2 * j], bi = -others[2 * j + 1];
+        const Real t0 = ar * br, t1 = ai * bi, t2 = ar * bi, t3 = ai * br;
+        const Real re = t0 - t1, im = t2 + t3;
+        out[2 * j] = out[2 * j] + re;
+        out[2 * j + 1] = out[2 * j + 1] + im;
+      }
+    }
+  }
+}
+
+}  // namespace
+
 ScoreBatch score_batch(const ModelConfig& cfg, const Store& store, const TripleBatch& b) {  // models.cpp:267-289
   check_config(cfg, store, b);
   switch (cfg.model) {
@@ -560,6 +774,9 @@ ScoreBatch score_batch(const ModelConfig& cfg, const Store& store, const TripleB
     case ModelKind::TransR: return transr_forward(cfg, store, b);
     case ModelKind::TransH: return transh_forward(cfg, store, b);
     case ModelKind::TorusE: return toruse_forward(cfg, store, b);
+    case ModelKind::DistMult:
+    case ModelKind::ComplEx: return product_forward(cfg, store, b);
+    case ModelKind::RotatE: return rotate_forward(cfg, store, b);
   }
   throw ConfigError("unknown model");
 }
@@ -574,6 +791,9 @@ void score_backward(const ModelConfig& cfg, const Store& store, const ScoreBatch
     case ModelKind::TransR: transr_backward(cfg, store, sb, up, g); return;
     case ModelKind::TransH: transh_backward(cfg, store, sb, up, g); return;
     case ModelKind::TorusE: toruse_backward(cfg, sb, up, g); return;
+    case ModelKind::DistMult:
+    case ModelKind::ComplEx: product_backward(cfg, store, sb, up, g); return;
+    case ModelKind::RotatE: rotate_backward(cfg, store, sb, up, g); return;
   }
 }
 
@@ -597,9 +817,11 @@ Store init_store(ModelKind model, Index n_ent, Index n_rel, Index de, Index dr, 
   if (n_ent < 1 || n_rel < 1) throw ConfigError("store needs at least one entity and one relation");
   std::mt19937_64 rng(seed);
   Store s;
-  s.entity = Mat(n_ent, de);
+  // complex coefficients: re then im per coordinate (embedding.cpp:21-25)
+  const Index wc = is_complex_model(model) ? 2 : 1;
+  s.entity = Mat(n_ent, wc * de);
   fill_uniform(s.entity, 6.0 / std::sqrt(static_cast<double>(de)), rng);
-  s.relation = Mat(n_rel, dr);
+  s.relation = Mat(n_rel, wc * dr);
   fill_uniform(s.relation, 6.0 / std::sqrt(static_cast<double>(dr)), rng);
   if (model == ModelKind::TransR) {
     s.proj = Mat(n_rel, dr * de);
@@ -680,6 +902,12 @@ Index draw_excluding(std::mt19937_64& rng, Index n, Index ex0, Index ex1) {
   return v;
 }
 
+std::vector<Real> signed_scores(Real sign, const std::vector<Real>& v) {  // sign * RealVector
+  std::vector<Real> out(v.size());
+  for (size_t i = 0; i < v.size(); ++i) out[i] = sign * v[i];
+  return out;
+}
+
 TripleBatch take(const TripleBatch& b, const IndexVector& order, Index lo, Index hi) {  // training.cpp:33-47
   TripleBatch out;
   out.num_entities = b.num_entities;
@@ -758,6 +986,7 @@ EpochReport train_epoch(const ModelConfig& mc, Store& store, const TripleBatch& 
   if (m < 1) throw ConfigError("training requires at least one triple");
   if (neg.size() != m) throw ShapeError("negative set is not aligned with the positive triples");
   const IndexVector order = epoch_order(m, tc, epoch);
+  const Real sign = energy_sign(mc.model);  // models.hpp:35-38
   EpochReport rep;
   rep.epoch = epoch;
   Gradients grads = make_gradients(store);
@@ -772,8 +1001,7 @@ EpochReport train_epoch(const ModelConfig& mc, Store& store, const TripleBatch& 
       const TripleBatch nb = take(neg, order, lo, hi);
       ps = score_batch(mc, store, pb);
       ns = score_batch(mc, store, nb);
-      // energy_sign(+1) for every translational model (models.hpp:35-38)
-      lg = margin_ranking_loss(ps.scores, ns.scores, tc.margin);
+      lg = margin_ranking_loss(signed_scores(sign, ps.scores), signed_scores(sign, ns.scores), tc.margin);
     }
     if (!std::isfinite(lg.loss))
       throw TrainingError("non-finite loss at epoch " + std::to_string(epoch) + ", batch " +
@@ -785,8 +1013,8 @@ EpochReport train_epoch(const ModelConfig& mc, Store& store, const TripleBatch& 
       grads.relation.set_zero();
       grads.proj.set_zero();
       grads.normals.set_zero();
-      score_backward(mc, store, ps, lg.d_pos, grads);
-      score_backward(mc, store, ns, lg.d_neg, grads);
+      score_backward(mc, store, ps, signed_scores(sign, lg.d_pos), grads);
+      score_backward(mc, store, ns, signed_scores(sign, lg.d_neg), grads);
       ps = ScoreBatch{};
       ns = ScoreBatch{};
     }
@@ -805,10 +1033,11 @@ std::vector<EpochReport> fit(const ModelConfig& mc, Store& store, const TripleBa
   tc.validate();
   std::vector<EpochReport> run;
   if (tc.epochs == 0) return run;
-  TripleBatch neg = negative_sample(train, tc.seed, false);  // no multiplicative models here
+  const bool no_self_loops = is_multiplicative_model(mc.model);
+  TripleBatch neg = negative_sample(train, tc.seed, no_self_loops);
   for (Index e = 0; e < tc.epochs; ++e) {
     if (tc.resample_negatives && e > 0)
-      neg = negative_sample(train, tc.seed + static_cast<std::uint64_t>(e) * 0x9E3779B9ULL, false);
+      neg = negative_sample(train, tc.seed + static_cast<std::uint64_t>(e) * 0x9E3779B9ULL, no_self_loops);
     Real lr = tc.lr;
     if (tc.has_scheduler)
       lr = tc.lr * static_cast<Real>(std::pow(tc.decay_factor, double(e / tc.decay_every)));

@@ -54,9 +54,18 @@ struct TrainingError : std::runtime_error { using std::runtime_error::runtime_er
 struct ParseError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 // common.hpp:62-72 (stable checkpoint tags)
-enum class ModelKind : std::uint32_t { TransE = 0, TransR = 1, TransH = 2, TorusE = 3 };
+enum class ModelKind : std::uint32_t {
+  TransE = 0, TransR = 1, TransH = 2, TorusE = 3, DistMult = 4, ComplEx = 5, RotatE = 6
+};
 enum class NormKind : std::uint32_t { L1 = 0, L2 = 1 };
 const char* model_name(ModelKind m);
+// common.hpp:74-82, models.hpp:32-38
+inline bool is_complex_model(ModelKind m) { return m == ModelKind::ComplEx || m == ModelKind::RotatE; }
+inline bool is_multiplicative_model(ModelKind m) {
+  return m == ModelKind::DistMult || m == ModelKind::ComplEx || m == ModelKind::RotatE;
+}
+inline bool higher_is_better(ModelKind m) { return m == ModelKind::DistMult || m == ModelKind::ComplEx; }
+inline Real energy_sign(ModelKind m) { return higher_is_better(m) ? Real(-1) : Real(1); }
 
 // common.hpp:112-147 — thread-per-call contiguous chunking.
 void set_num_threads(int n);
@@ -143,6 +152,10 @@ CsrMatrix coo_to_csr(const CooMatrix& m);            // sparse.hpp:110-161
 CsrMatrix transpose(const CsrMatrix& a);              // sparse.hpp:164-183
 CooMatrix build_ht(const TripleBatch& b);             // incidence.hpp:38-57
 CooMatrix build_hrt(const TripleBatch& b);            // incidence.hpp:62-85
+// incidence.hpp:93-121. Complex stores are tables of interleaved (re, im)
+// pairs (std::complex<Real> row-major, embedding.hpp:15-31), so one complex
+// coordinate is two Real columns; the CSR itself is real (+1 / -1 markers).
+CooMatrix build_multiplicative(const TripleBatch& b, bool conjugate_tail);
 Mat spmm(const CsrMatrix& a, const Mat& x);           // sparse.hpp:242-266
 void spmm_transpose_add(const CsrMatrix& a, const Mat& g, Mat& out);  // sparse.hpp:273-306
 
@@ -161,10 +174,13 @@ struct ModelConfig {
   Index dim_entity = 0, dim_relation = 0;
   NormKind norm = NormKind::L2;
   void validate() const;
+  Index width_entity() const { return is_complex_model(model) ? 2 * dim_entity : dim_entity; }
+  Index width_relation() const { return is_complex_model(model) ? 2 * dim_relation : dim_relation; }
 };
 
 // embedding.hpp:15-59. Tables are [entity; relation] stacked in one buffer
 // when the caller provides them that way; the oracle only needs row access.
+// Complex models (ComplEx, RotatE) store 2 * dim Real columns per row.
 struct Store {
   Mat entity, relation, proj, normals;
   Index num_entities() const { return entity.rows; }

@@ -472,3 +472,108 @@ def test_rank_entity_rejects_bad_ids(orc64):  # test_eval.cpp:81-85
         orc64.rank_entities("transe", st, [0], [0], [9])
     with pytest.raises(Exception):
         orc64.rank_entities("transe", st, [0], [3], [1])
+
+
+# ---------------------------- multiplicative family (test_models.cpp:174-230)
+def cstore(ent, rel):
+    """Complex store from complex arrays: interleaved (re, im) float64 tables."""
+    f = lambda a: np.ascontiguousarray(np.asarray(a, np.complex128)).view(np.float64).reshape(len(a), -1).copy()
+    return Store(f(ent), f(rel))
+
+
+def test_build_multiplicative_layout(orc64):  # incidence.hpp:93-121
+    rp, col, val = orc64.build_incidence("mult", *one(5, 2, 3), 20, 4)
+    assert col.tolist() == [3, 5, 22] and val.tolist() == [1.0, 1.0, 1.0]
+    rp, col, val = orc64.build_incidence("mult_conj", *one(5, 2, 3), 20, 4)
+    assert col.tolist() == [3, 5, 22] and val.tolist() == [-1.0, 1.0, 1.0]
+    with pytest.raises(OracleError) as e:
+        orc64.build_incidence("mult", *one(4, 0, 4), 20, 4)
+    assert e.value.kind == "DegenerateTripleError" and "triple 0: head == tail" in e.value.msg
+
+
+def test_distmult_golden_and_symmetry(orc64):  # test_models.cpp:174-189
+    st = Store(np.array([[2.0], [5.0]]), np.array([[3.0]]))
+    assert orc64.score_batch("distmult", st, *one(0, 0, 1))[0][0] == 30.0
+    st = orc64.init_store("distmult", 10, 3, 6, 6, 19)
+    rng = np.random.default_rng(19)
+    h, r, t = rng.integers(0, 10, 15), rng.integers(0, 3, 15), rng.integers(0, 10, 15)
+    t = np.where(t == h, (t + 1) % 10, t)
+    a = orc64.score_batch("distmult", st, h, r, t)[0]
+    b = orc64.score_batch("distmult", st, t, r, h)[0]
+    assert np.array_equal(a, b)
+
+
+def test_complex_tail_conjugated(orc64):  # :191-198
+    st = cstore([[1j], [1j]], [[1.0]])
+    assert orc64.score_batch("complex", st, *one(0, 0, 1))[0][0] == 1.0
+
+
+def test_rotate_goldens(orc64):  # :200-211
+    st = cstore([[1.0], [1j]], [[1j]])
+    assert orc64.score_batch("rotate", st, *one(0, 0, 1))[0][0] == 0.0
+    st.entity[1] = 0.0
+    assert orc64.score_batch("rotate", st, *one(0, 0, 1))[0][0] == 1.0
+
+
+@pytest.mark.parametrize("model", ["distmult", "complex", "rotate"])
+def test_multiplicative_rejects_self_loops(orc64, model):  # :213-221
+    st = orc64.init_store(model, 5, 2, 3, 3, 1)
+    with pytest.raises(OracleError) as e:
+        orc64.score_batch(model, st, *one(2, 0, 2))
+    assert e.value.kind == "DegenerateTripleError"
+
+
+@pytest.mark.parametrize("model", ["distmult", "complex", "rotate"])
+def test_finite_differences_product_family(orc64, model):  # test_models.cpp:414-433
+    n, nr, m = 5, 2, 4
+    for seed in range(5000, 5500):
+        st = orc64.init_store(model, n, nr, 3, 3, seed)
+        rng = np.random.default_rng(seed * 13 + 1)
+        h, r, t = rng.integers(0, n, m), rng.integers(0, nr, m), rng.integers(0, n, m)
+        t = np.where(t == h, (t + 1) % n, t)
+        sc, aux = orc64.score_batch(model, st, h, r, t)
+        if model == "rotate":  # modulus gradient needs |q| clear of the origin
+            q = aux["v"].view(np.complex128)
+            if (np.abs(q) < 1e-2).any():
+                continue
+        break
+    up = rng.uniform(0.25, 1, m) * np.where(np.arange(m) % 2, 1, -1)
+    g = orc64.score_backward(model, st, h, r, t, up, st.zeros_like())
+    f = lambda: float(up @ orc64.score_batch(model, st, h, r, t)[0])
+    for name in ("entity", "relation"):
+        assert _max_rel_err(getattr(g, name), _numeric_grad(f, getattr(st, name))) < 1e-5, name
+
+
+def test_polarity_and_fit_product_family(orc64):  # test_models.cpp:223-231, test_training.cpp:290-320
+    rng = np.random.default_rng(12)
+    h, r, t = rng.integers(0, 10, 40), rng.integers(0, 3, 40), rng.integers(0, 10, 40)
+    t = np.where(t == h, (t + 1) % 10, t)
+    tc = orc64.train_config(lr=0.01, epochs=2, batch_size=16, seed=12)
+    for model in ("distmult", "complex", "rotate"):
+        st = orc64.init_store(model, 10, 3, 6, 6, 3)
+        reps = orc64.fit(model, st, h, r, t, tc)
+        assert len(reps) == 2 and math.isfinite(reps[-1].loss)
+    # DistMult scores plausibility: the hinge sees -score (energy_sign = -1)
+    st = Store(np.array([[1.0], [1.0], [3.0]]), np.array([[1.0]]))
+    tc1 = orc64.train_config(lr=0.0, epochs=1, batch_size=4, seed=1, shuffle=False)
+    rep = orc64.train_epoch("distmult", st, one(0, 0, 1), (np.array([0]), np.array([2])), tc1, 0, 0.0)
+    # pos score 1, neg score 3: energies -1 and -3 -> term = 0.5 + (-1) - (-3) = 2.5
+    assert rep.loss == 2.5
+
+
+def test_complex_init_bound(orc64):  # test_embedding.cpp:44-53
+    d = 8
+    st = orc64.init_store("complex", 30, 4, d, d, 11)
+    assert st.entity.shape == (30, 2 * d)
+    assert (np.abs(st.entity) <= 6 / math.sqrt(d)).all()
+    # draws: re then im per coordinate, entity then relation (embedding.cpp:17-30)
+    real = orc64.init_store("distmult", 30, 4, 2 * d, 2 * d, 11)
+    assert not np.array_equal(real.entity, st.entity)  # bound differs (6/sqrt(2d))
+    assert np.allclose(real.entity * math.sqrt(2 * d), st.entity * math.sqrt(d))
+
+
+def test_degenerate_multiplicative_queries_rank_last(orc64):  # test_eval.cpp:185-197
+    st = orc64.init_store("distmult", 5, 1, 3, 3, 4)
+    assert orc64.rank_entities("distmult", st, [2], [0], [2]).tolist() == [[5, 5]]
+    r = orc64.rank_entities("distmult", st, [2], [0], [1])[0, 0]
+    assert 1 <= r <= 4
