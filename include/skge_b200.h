@@ -40,12 +40,18 @@ typedef enum skg_status {
   SKG_ERR_CUDA = 6        /* device/runtime failure (no reference analogue) */
 } skg_status;
 
-/* ModelKind tags (common.hpp:62-70); only the translational family is built. */
-enum { SKG_TRANSE = 0, SKG_TRANSR = 1, SKG_TRANSH = 2, SKG_TORUSE = 3 };
+/* ModelKind tags (common.hpp:62-70). ComplEx and RotatE use complex stores:
+ * every table row holds dim interleaved (re, im) float pairs, the reference's
+ * std::complex<float> row-major layout (embedding.hpp:15-31), so a complex
+ * table of dim d is passed as 2*d floats per row. Norm is ignored by the
+ * multiplicative family, as in the reference. */
+enum { SKG_TRANSE = 0, SKG_TRANSR = 1, SKG_TRANSH = 2, SKG_TORUSE = 3,
+       SKG_DISTMULT = 4, SKG_COMPLEX = 5, SKG_ROTATE = 6 };
 /* NormKind (common.hpp:72) */
 enum { SKG_L1 = 0, SKG_L2 = 1 };
-/* Incidence layouts: build_ht (incidence.hpp:38), build_hrt (:62) */
-enum { SKG_LAYOUT_HT = 0, SKG_LAYOUT_HRT = 1 };
+/* Incidence layouts: build_ht (incidence.hpp:38), build_hrt (:62),
+ * build_multiplicative (:93) without / with the conjugate tail marker */
+enum { SKG_LAYOUT_HT = 0, SKG_LAYOUT_HRT = 1, SKG_LAYOUT_MULT = 2, SKG_LAYOUT_MULT_CONJ = 3 };
 
 typedef struct skg_model_config { /* ModelConfig, models.hpp:17-30 */
   uint32_t model;

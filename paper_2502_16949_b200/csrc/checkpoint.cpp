@@ -3,8 +3,11 @@
 // four u64 dims, then little-endian f64 row-major blocks in the order entity,
 // relation, projections (TransR), normals (TransH). The engine's fp32 tables
 // are written as doubles exactly like the reference's 32-bit build
-// (write_block) and read back with static_cast<float> (read_block). Host code:
-// the caller downloads / uploads the device store around these calls.
+// (write_block) and read back with static_cast<float> (read_block). Complex
+// models (ComplEx, RotatE) carry dim interleaved (re, im) pairs per row in
+// both the fp32 tables and the f64 payload (std::complex layout), so the
+// header dims count complex coordinates. Host code: the caller downloads /
+// uploads the device store around these calls.
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -20,6 +23,7 @@ constexpr uint32_t kVersion = 1;
 constexpr uint32_t kMaxTag = 6;  // RotatE (common.hpp:62-70)
 const char* kNames[] = {"transe", "transr", "transh", "toruse", "distmult", "complex", "rotate"};
 
+bool is_complex(uint32_t tag) { return tag == 5 || tag == 6; }  // common.hpp:74-76
 struct Fail {
   skg_status st;
   std::string msg;
@@ -91,7 +95,6 @@ skg_status skg_save_checkpoint(const char* path, uint32_t model, int64_t num_ent
                                const float* proj, const float* normals) {
   return guard([&] {
     if (model > kMaxTag) throw Fail{SKG_ERR_CONFIG, "unknown model tag " + std::to_string(model)};
-    if (model >= 4) throw Fail{SKG_ERR_CONFIG, "checkpoint scalar kind does not match the model tag"};
     if ((model == 1) != (proj != nullptr))
       throw Fail{SKG_ERR_CONFIG, "projection table presence does not match the model tag"};
     if ((model == 2) != (normals != nullptr))
@@ -104,8 +107,9 @@ skg_status skg_save_checkpoint(const char* path, uint32_t model, int64_t num_ent
     const uint64_t d[4] = {static_cast<uint64_t>(num_entities), static_cast<uint64_t>(num_relations),
                            static_cast<uint64_t>(dim_entity), static_cast<uint64_t>(dim_relation)};
     out.write(reinterpret_cast<const char*>(d), sizeof(d));
-    write_block(out, entity, num_entities * dim_entity);
-    write_block(out, relation, num_relations * dim_relation);
+    const int64_t w = is_complex(model) ? 2 : 1;
+    write_block(out, entity, num_entities * dim_entity * w);
+    write_block(out, relation, num_relations * dim_relation * w);
     if (proj) write_block(out, proj, num_relations * dim_relation * dim_entity);
     if (normals) write_block(out, normals, num_relations * dim_entity);
     if (!out) throw Fail{SKG_ERR_PARSE, std::string("short write while saving checkpoint: ") + path};
@@ -121,9 +125,9 @@ skg_status skg_load_checkpoint(const char* path, uint32_t expected_model, float*
     if (h.model != expected_model)
       throw Fail{SKG_ERR_CONFIG, std::string("checkpoint holds a ") + kNames[h.model] + " model, expected " +
                                      (expected_model <= kMaxTag ? kNames[expected_model] : "unknown")};
-    if (h.model >= 4) throw Fail{SKG_ERR_CONFIG, "checkpoint scalar kind does not match the requested store type"};
-    read_block(in, entity, h.num_entities * h.dim_entity);
-    read_block(in, relation, h.num_relations * h.dim_relation);
+    const int64_t w = is_complex(h.model) ? 2 : 1;
+    read_block(in, entity, h.num_entities * h.dim_entity * w);
+    read_block(in, relation, h.num_relations * h.dim_relation * w);
     if (h.model == 1) read_block(in, proj, h.num_relations * h.dim_relation * h.dim_entity);
     if (h.model == 2) read_block(in, normals, h.num_relations * h.dim_entity);
     in.peek();

@@ -24,6 +24,9 @@ const char* model_name(uint32_t m) {  // common.hpp:82-93
     case SKG_TRANSR: return "transr";
     case SKG_TRANSH: return "transh";
     case SKG_TORUSE: return "toruse";
+    case SKG_DISTMULT: return "distmult";
+    case SKG_COMPLEX: return "complex";
+    case SKG_ROTATE: return "rotate";
   }
   return "unknown";
 }
@@ -43,6 +46,9 @@ skg_status guard(skg_ctx* ctx, F&& f) {
   } catch (const TrainingError& e) {
     if (ctx) ctx->err = e.what();
     return SKG_ERR_TRAINING;
+  } catch (const DegenerateTripleError& e) {
+    if (ctx) ctx->err = e.what();
+    return SKG_ERR_DEGENERATE;
   } catch (const std::exception& e) {
     if (ctx) ctx->err = e.what();
     return SKG_ERR_CUDA;
@@ -56,14 +62,20 @@ int kind_of(const skg_model_config& c) {
     case SKG_TORUSE: return l2 ? kTorusE_L2 : kTorusE_L1;
     case SKG_TRANSH: return l2 ? kTransH_L2 : kTransH_L1;
     case SKG_TRANSR: return l2 ? kTransR_L2 : kTransR_L1;
+    case SKG_DISTMULT: return kDistMult;
+    case SKG_COMPLEX: return kComplEx;
+    case SKG_ROTATE: return kRotatE;
   }
   throw ConfigError("unknown model tag " + std::to_string(c.model));
 }
 
 bool is_ht(const skg_model_config& c) { return c.model == SKG_TRANSH || c.model == SKG_TRANSR; }
+bool is_mult(const skg_model_config& c) { return c.model >= SKG_DISTMULT && c.model <= SKG_ROTATE; }  // common.hpp:80-82
+bool is_complex(uint32_t m) { return m == SKG_COMPLEX || m == SKG_ROTATE; }                        // common.hpp:74-76
+int64_t width(uint32_t m, int64_t dim) { return is_complex(m) ? 2 * dim : dim; }  // floats per table row
 
 void validate_model(const skg_model_config& c) {  // models.hpp:23-29
-  if (c.model > SKG_TORUSE) throw ConfigError("unknown model tag " + std::to_string(c.model));
+  if (c.model > SKG_ROTATE) throw ConfigError("unknown model tag " + std::to_string(c.model));
   if (c.norm > SKG_L2) throw ConfigError("unknown norm tag " + std::to_string(c.norm));
   if (c.dim_entity < 1 || c.dim_relation < 1) throw ConfigError("embedding dimensions must be at least 1");
   if (c.model != SKG_TRANSR && c.dim_relation != c.dim_entity)
@@ -73,7 +85,12 @@ void validate_model(const skg_model_config& c) {  // models.hpp:23-29
 void check_config(skg_ctx* ctx, const skg_model_config& c, int64_t n_ent, int64_t n_rel) {  // models.hpp:65-76
   validate_model(c);
   if (!ctx->has_store) throw ConfigError("no parameter store uploaded");
-  if (ctx->de != c.dim_entity || ctx->dr != c.dim_relation)
+  // score_batch<Real> / <Complex> dispatch (models.cpp:267-289): the store's scalar type must match
+  if (is_complex(c.model) && !is_complex(ctx->cfg.model))
+    throw ConfigError(std::string(model_name(c.model)) + " needs a complex-valued store");
+  if (!is_complex(c.model) && is_complex(ctx->cfg.model))
+    throw ConfigError(std::string(model_name(c.model)) + " uses a real-valued store");
+  if (ctx->de != width(c.model, c.dim_entity) || ctx->dr != width(c.model, c.dim_relation))
     throw ConfigError("store dimensions do not match the model config");
   if (ctx->N != n_ent || ctx->R != n_rel)
     throw ConfigError("store table sizes do not match the batch id space");
@@ -118,9 +135,18 @@ void upload_ids(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, con
                              cudaMemcpyHostToDevice, ctx->stream));
 }
 
-void ensure_workspace(skg_ctx* ctx, int64_t rows) {
+// build_multiplicative (incidence.hpp:104-108): the first head == tail triple.
+void reject_self_loops(int64_t m, const int64_t* h, const int64_t* t) {
+  for (int64_t i = 0; i < m; ++i)
+    if (h[i] == t[i])
+      throw DegenerateTripleError("triple " + std::to_string(i) +
+                                  ": head == tail is not representable in the "
+                                  "multiplicative incidence layout");
+}
+
+void ensure_workspace(skg_ctx* ctx, int64_t rows, int kind) {
   const int64_t d = std::max(ctx->de, ctx->dr);
-  ctx->res.ensure(rows * d);
+  ctx->res.ensure(rows * d * (is_mult_kind(kind) ? 3 : 1));  // multiplicative: 3 gradient planes
   ctx->res_u.ensure(rows * ctx->de);
   ctx->scal.ensure(rows);
   ctx->scores.ensure(rows);
@@ -143,6 +169,7 @@ FwdArgs base_fwd(skg_ctx* ctx) {
   a.counter = ctx->counter.p;
   a.batch_loss = ctx->batch_loss.p;
   a.err = ctx->err_words.p;
+  a.sign = 1.f;
   return a;
 }
 
@@ -202,7 +229,21 @@ struct EpochShape {
   int64_t i0_last = 0;  // shard start inside the last minibatch
   int64_t s_last = 0;   // shard size of the last minibatch (may be 0)
   int64_t Mg = 0;       // rows of this rank's shards over the epoch
+  int64_t nb_run = -1;  // run only the first nb_run minibatches (-1: all)
 };
+
+// Multiplicative models: positions (in epoch order) of the first positive and
+// first negative self-loop triple, which build_multiplicative rejects.
+__global__ void first_loop_kernel(const int32_t* __restrict__ order, const int32_t* __restrict__ H,
+                                  const int32_t* __restrict__ T, const int32_t* __restrict__ NH,
+                                  const int32_t* __restrict__ NT, int64_t M, uint32_t* __restrict__ first) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < M;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t id = order ? order[k] : static_cast<int32_t>(k);
+    if (H[id] == T[id]) atomicMin(first, static_cast<uint32_t>(k));
+    if (NH[id] == NT[id]) atomicMin(first + 1, static_cast<uint32_t>(k));
+  }
+}
 
 __global__ void shard_order_kernel(const int32_t* __restrict__ order, int64_t B, int64_t S, int rank,
                                    int64_t nb, int64_t i0_last, int64_t Mg, int32_t* __restrict__ order_g) {
@@ -292,9 +333,11 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
   const bool dp = es.world > 1 || ctx->dp != nullptr;
   reset_err(ctx, s);
   if (dp) SKG_CUDA(cudaMemsetAsync(ctx->batch_loss.p, 0, sizeof(float) * es.nb, s));
-  const bool ht = es.kind >= kTransH_L2;
+  const bool ht = is_ht_kind(es.kind);
+  const bool mult = is_mult_kind(es.kind);
   const int64_t n_params = (ctx->N + ctx->R) * ctx->de;
-  for (int64_t b = 0; b < es.nb; ++b) {
+  const int64_t nb_run = es.nb_run >= 0 ? es.nb_run : es.nb;
+  for (int64_t b = 0; b < nb_run; ++b) {
     const int64_t lo = b * es.B;
     const int Bb = static_cast<int>(std::min(es.B, ctx->M - lo));
     if (dp) {
@@ -373,7 +416,18 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
     ba.batch = static_cast<int>(b);
     ba.lr = ctx->lr_dev.p;
     ba.err = ctx->err_words.p;
-    if (!ht) {
+    if (mult) {
+      fa.de = static_cast<int>(ctx->cfg.dim_entity);
+      fa.plane_rows = 2 * es.B;
+      fa.sign = (es.kind == kRotatE) ? 1.f : -1.f;  // energy_sign (models.hpp:32-38)
+      fa.res_u = nullptr;
+      ba.res = ctx->res.p;
+      ba.plane_rows = 2 * es.B;
+      launch_mult_forward(es.kind, true, fa, ctx->num_sms, s);
+      mark();
+      launch_segment_backward(kMultRows, true, ba, ctx->num_sms, s);
+      mark();
+    } else if (!ht) {
       launch_hrt_forward(es.kind, true, fa, ctx->num_sms, s);
       mark();
       launch_segment_backward(es.kind, true, ba, ctx->num_sms, s);
@@ -401,7 +455,8 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   es.world = dp_world(ctx);
   es.rank = dp_rank(ctx);
   if (ctx->dp) {
-    if (is_ht(cfg)) throw ConfigError("data-parallel training supports TransE / TorusE in this build");
+    if (is_ht(cfg) || is_mult(cfg))
+      throw ConfigError("data-parallel training supports TransE / TorusE in this build");
     if (es.B % es.world != 0) throw ConfigError("data parallel: global batch_size must be a multiple of the world size");
     int64_t sh[5];
     dp_shard(ctx->M, es.B, es.world, es.rank, sh);
@@ -417,7 +472,7 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
     sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
   }
   ctx->shuffle.reserve(ctx->M);
-  ensure_workspace(ctx, 2 * es.B);
+  ensure_workspace(ctx, 2 * es.B, es.kind);
   if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, 2 * es.B, ctx->de, ctx->dr, ctx->R));
   ctx->batch_loss.ensure(es.nb);
   if (ctx->h_loss_cap < es.nb) {
@@ -503,6 +558,50 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
   ctx->graph_launches_k[cur] = kernel_launches() - before;
 }
 
+// Does any positive or negative triple have head == tail? (cached per data version)
+bool has_self_loops(skg_ctx* ctx) {
+  if (ctx->loops_version == ctx->data_version) return ctx->has_loops;
+  ctx->bad_idx.ensure(3);
+  SKG_CUDA(cudaMemsetAsync(ctx->bad_idx.p, 0xFF, sizeof(uint32_t) * 2, ctx->stream));
+  first_loop_kernel<<<grid_for(ctx->M), 256, 0, ctx->stream>>>(nullptr, ctx->H.p, ctx->T.p, ctx->NH.p, ctx->NT.p,
+                                                               ctx->M, ctx->bad_idx.p);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->bad_idx.p, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->has_loops = ctx->h_err[0] != 0xFFFFFFFFu || ctx->h_err[1] != 0xFFFFFFFFu;
+  ctx->loops_version = ctx->data_version;
+  return ctx->has_loops;
+}
+
+// training.cpp:117-125 with a self-loop triple in the epoch: the batches before
+// the first one containing it train normally, then score_batch throws (the
+// positive sub-batch is scored before the negative one).
+[[noreturn]] void train_until_degenerate(skg_ctx* ctx, EpochShape es, int64_t epoch, int cur) {
+  SKG_CUDA(cudaMemsetAsync(ctx->bad_idx.p, 0xFF, sizeof(uint32_t) * 2, ctx->stream));
+  first_loop_kernel<<<grid_for(ctx->M), 256, 0, ctx->stream>>>(ctx->slots[cur].order.p, ctx->H.p, ctx->T.p,
+                                                               ctx->NH.p, ctx->NT.p, ctx->M, ctx->bad_idx.p);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->bad_idx.p, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int64_t kp = ctx->h_err[0], kn = ctx->h_err[1];
+  const int64_t kmin = std::min(kp, kn);
+  const int64_t bf = kmin / es.B;
+  const int64_t i = (kp / es.B == bf ? kp : kn) - bf * es.B;
+  ctx->slots[1 - cur].key.clear();
+  es.nb_run = bf;
+  if (bf > 0) {
+    enqueue_batches(ctx, es, cur, ctx->stream, nullptr);
+    SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err_words.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    raise_device_error(ctx->h_err, epoch);
+  }
+  throw DegenerateTripleError("triple " + std::to_string(i) +
+                              ": head == tail is not representable in the multiplicative incidence layout");
+}
+
 void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
                       int64_t epoch, float lr, skg_epoch_report* rep) {
   EpochShape es{};
@@ -519,6 +618,9 @@ void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train
     enqueue_plan(ctx, es, cur, ctx->stream);
     eager = kernel_launches() - before;
     ctx->slots[cur].key = pk;
+  }
+  if (is_mult(cfg) && has_self_loops(ctx)) {
+    train_until_degenerate(ctx, es, epoch, cur);  // always throws
   }
   // Speculatively build epoch + 1's plan (same data and schedule) alongside.
   set_slot_seed(ctx, nxt, epoch_seed(tc.seed, epoch + 1));
@@ -571,7 +673,7 @@ __global__ void incidence_count_kernel(const int32_t* __restrict__ ids, int64_t 
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const bool self = ids[i] == ids[2 * m + i];
-    cnt[i] = (self ? 0u : 2u) + (layout == SKG_LAYOUT_HRT ? 1u : 0u);
+    cnt[i] = layout >= SKG_LAYOUT_MULT ? 3u : (self ? 0u : 2u) + (layout == SKG_LAYOUT_HRT ? 1u : 0u);
   }
 }
 
@@ -585,6 +687,18 @@ __global__ void incidence_fill_kernel(const int32_t* __restrict__ ids, int64_t m
     const int64_t h = ids[i], r = ids[m + i], t = ids[2 * m + i];
     int64_t p = off[i];
     row_ptr[i] = p;
+    if (layout >= SKG_LAYOUT_MULT) {  // build_multiplicative (incidence.hpp:93-121), h != t checked on the host
+      const float tail_marker = layout == SKG_LAYOUT_MULT_CONJ ? -1.f : 1.f;
+      const bool hf = h < t;
+      col[p] = hf ? h : t;
+      val[p++] = hf ? 1.f : tail_marker;
+      col[p] = hf ? t : h;
+      val[p++] = hf ? tail_marker : 1.f;
+      col[p] = N + r;
+      val[p++] = 1.f;
+      if (i == m - 1) row_ptr[m] = p;
+      continue;
+    }
     if (h != t) {
       const bool hf = h < t;
       col[p] = hf ? h : t;
@@ -761,6 +875,7 @@ skg_status skg_create(int device, skg_ctx** out) {
     configure_hrt_kernels();
     configure_ht_kernels();
     configure_eval_kernels();
+    configure_mult_kernels();
   });
   if (st != SKG_OK) {
     g_create_err = ctx->err;
@@ -811,8 +926,8 @@ skg_status skg_store_upload(skg_ctx* ctx, const skg_model_config* cfg, int64_t n
     ctx->cfg = *cfg;
     ctx->N = n_ent;
     ctx->R = n_rel;
-    ctx->de = cfg->dim_entity;
-    ctx->dr = cfg->dim_relation;
+    ctx->de = width(cfg->model, cfg->dim_entity);  // complex: interleaved (re, im) pairs
+    ctx->dr = width(cfg->model, cfg->dim_relation);
     ctx->tables.ensure(n_ent * ctx->de + n_rel * ctx->dr);
     SKG_CUDA(cudaMemcpyAsync(ctx->tables.p, entity, sizeof(float) * n_ent * ctx->de, cudaMemcpyHostToDevice,
                              ctx->stream));
@@ -995,8 +1110,9 @@ skg_status skg_build_incidence(skg_ctx* ctx, int32_t layout, int64_t m, const in
                                const int64_t* t, int64_t n_ent, int64_t n_rel, int64_t* row_ptr,
                                int64_t* col_idx, float* vals, int64_t* nnz) {
   return guard(ctx, [&] {
-    if (layout != SKG_LAYOUT_HT && layout != SKG_LAYOUT_HRT) throw ConfigError("unknown incidence layout");
+    if (layout < SKG_LAYOUT_HT || layout > SKG_LAYOUT_MULT_CONJ) throw ConfigError("unknown incidence layout");
     upload_ids(ctx, m, h, r, t, n_ent, n_rel);
+    if (layout >= SKG_LAYOUT_MULT) reject_self_loops(m, h, t);
     DevBuf<uint32_t> cnt, off;
     DevBuf<int64_t> drp, dcol;
     DevBuf<float> dval;
@@ -1035,16 +1151,22 @@ skg_status skg_score_batch(skg_ctx* ctx, const skg_model_config* cfg, int64_t m,
   return guard(ctx, [&] {
     check_config(ctx, *cfg, ctx->N, ctx->R);
     upload_ids(ctx, m, h, r, t, ctx->N, ctx->R);
+    if (is_mult(*cfg)) reject_self_loops(m, h, t);
     if (m == 0) return;
-    ensure_workspace(ctx, m);
-    reset_err(ctx);
     const int kind = kind_of(*cfg);
+    ensure_workspace(ctx, m, kind);
+    reset_err(ctx);
     FwdArgs a = base_fwd(ctx);
     a.H = ctx->tmp_i32.p;
     a.Rl = ctx->tmp_i32.p + m;
     a.T = ctx->tmp_i32.p + 2 * m;
     a.B = static_cast<int>(m);
-    if (is_ht(*cfg)) {
+    if (is_mult(*cfg)) {
+      a.de = static_cast<int>(cfg->dim_entity);
+      a.plane_rows = m;
+      a.res_u = (residual && kind == kRotatE) ? ctx->res_u.p : nullptr;  // RotatE keeps q (ScoreBatch::v)
+      launch_mult_forward(kind, false, a, ctx->num_sms, ctx->stream);
+    } else if (is_ht(*cfg)) {
       ctx->ht_work.ensure(ht_work_floats(kind, m, ctx->de, ctx->dr, ctx->R));
       build_batch_plan(a.H, a.Rl, a.T, m, ctx->N, ctx->R, SKG_LAYOUT_HRT, ctx->plan, ctx->stream);
       BwdArgs ba{};
@@ -1062,7 +1184,10 @@ skg_status skg_score_batch(skg_ctx* ctx, const skg_model_config* cfg, int64_t m,
       launch_hrt_forward(kind, false, a, ctx->num_sms, ctx->stream);
     }
     SKG_CUDA(cudaMemcpyAsync(scores, ctx->scores.p, sizeof(float) * m, cudaMemcpyDeviceToHost, ctx->stream));
-    if (residual) {
+    if (residual && kind == kRotatE) {
+      SKG_CUDA(cudaMemcpyAsync(residual, ctx->res_u.p, sizeof(float) * m * ctx->de, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    } else if (residual && !is_mult(*cfg)) {
       const int64_t d = cfg->model == SKG_TORUSE || cfg->model == SKG_TRANSE ? ctx->de : ctx->dr;
       SKG_CUDA(cudaMemcpyAsync(residual, ctx->res.p, sizeof(float) * m * d, cudaMemcpyDeviceToHost, ctx->stream));
     }
@@ -1076,10 +1201,11 @@ skg_status skg_score_backward(skg_ctx* ctx, const skg_model_config* cfg, int64_t
   return guard(ctx, [&] {
     check_config(ctx, *cfg, ctx->N, ctx->R);
     upload_ids(ctx, m, h, r, t, ctx->N, ctx->R);
+    if (is_mult(*cfg)) reject_self_loops(m, h, t);
     if (m == 0) return;
-    ensure_workspace(ctx, m);
-    reset_err(ctx);
     const int kind = kind_of(*cfg);
+    ensure_workspace(ctx, m, kind);
+    reset_err(ctx);
     const int64_t ne = ctx->N * ctx->de, nr = ctx->R * ctx->dr;
     const int64_t np = ctx->proj.n, nn = ctx->normals.n;
     ctx->grad_sink.ensure(ne + nr + np + nn + 1);
@@ -1112,7 +1238,20 @@ skg_status skg_score_backward(skg_ctx* ctx, const skg_model_config* cfg, int64_t
     ba.batch = 0;
     ba.lr = ctx->lr_dev.p;
     ba.err = ctx->err_words.p;
-    if (is_ht(*cfg)) {
+    if (is_mult(*cfg)) {
+      a.de = static_cast<int>(cfg->dim_entity);
+      a.plane_rows = m;
+      a.res_u = nullptr;
+      launch_mult_forward(kind, false, a, ctx->num_sms, ctx->stream);
+      build_batch_plan(a.H, a.Rl, a.T, m, ctx->N, ctx->R, SKG_LAYOUT_HRT, ctx->plan, ctx->stream);
+      ba.res = ctx->res.p;
+      ba.plane_rows = m;
+      ba.ent_val = ctx->plan.sorted_val;
+      ba.seg_start = ctx->plan.seg_start;
+      ba.seg_col = ctx->plan.seg_col;
+      ba.seg_base = ctx->plan.seg_base;
+      launch_segment_backward(kMultRows, false, ba, ctx->num_sms, ctx->stream);
+    } else if (is_ht(*cfg)) {
       ctx->ht_work.ensure(ht_work_floats(kind, m, ctx->de, ctx->dr, ctx->R));
       build_batch_plan(a.H, a.Rl, a.T, m, ctx->N, ctx->R, SKG_LAYOUT_HRT, ctx->plan, ctx->stream);
       ba.res = ctx->res_u.p;
@@ -1312,10 +1451,11 @@ skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_co
     validate_model(*cfg);
     validate_train(*tc);
     if (tc->epochs == 0) return;
-    negative_sample_impl(ctx, tc->seed, false);  // no multiplicative models in this engine
+    const bool no_self_loops = is_mult(*cfg);  // training.cpp:176
+    negative_sample_impl(ctx, tc->seed, no_self_loops);
     for (int64_t e = 0; e < tc->epochs; ++e) {
       if (tc->resample_negatives && e > 0)
-        negative_sample_impl(ctx, tc->seed + static_cast<uint64_t>(e) * 0x9E3779B9ULL, false);
+        negative_sample_impl(ctx, tc->seed + static_cast<uint64_t>(e) * 0x9E3779B9ULL, no_self_loops);
       float lr = tc->lr;
       if (tc->has_scheduler)
         lr = tc->lr * static_cast<float>(std::pow(tc->decay_factor, double(e / tc->decay_every)));

@@ -20,6 +20,7 @@ namespace skg {
 struct ShapeError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct ConfigError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 struct TrainingError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DegenerateTripleError : std::invalid_argument { using std::invalid_argument::invalid_argument; };
 
 template <class T>
 struct DevBuf {
@@ -63,7 +64,7 @@ struct skg_ctx {
   // ---- store (embedding.hpp:15-31)
   bool has_store = false;
   skg_model_config cfg{};
-  int64_t N = 0, R = 0, de = 0, dr = 0;
+  int64_t N = 0, R = 0, de = 0, dr = 0;  // de / dr: floats per row (2 x dim for complex stores)
   skg::DevBuf<float> tables;  // [entity N x de ; relation R x dr]
   skg::DevBuf<float> proj, normals;
 
@@ -103,6 +104,8 @@ struct skg_ctx {
   uint64_t data_version = 0;
   bool triples_valid = false;              // H/Rl/T hold the last successful set_triples
   uint64_t neg_valid_version = ~0ull;      // data_version at which NH/NT were last set (or sampled)
+  uint64_t loops_version = ~0ull;          // data_version the self-loop scan below refers to
+  bool has_loops = false;                  // some positive or negative triple has head == tail
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaGraphExec_t graph = nullptr;  // legacy handle (unused)

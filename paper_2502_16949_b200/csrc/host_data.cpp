@@ -83,8 +83,11 @@ skg_status skg_init_store(uint32_t model, int64_t n_ent, int64_t n_rel, int64_t 
     return SKG_ERR_CONFIG;
   }
   std::mt19937_64 rng(seed);
-  fill_uniform(entity, n_ent, de, 6.0 / std::sqrt(static_cast<double>(de)), rng);
-  fill_uniform(relation, n_rel, dr, 6.0 / std::sqrt(static_cast<double>(dr)), rng);
+  // complex stores draw re then im per coordinate (embedding.cpp:21-25): the
+  // same stream order as a real table of twice the width, bound 6 / sqrt(dim)
+  const int64_t w = (model == SKG_COMPLEX || model == SKG_ROTATE) ? 2 : 1;
+  fill_uniform(entity, n_ent, w * de, 6.0 / std::sqrt(static_cast<double>(de)), rng);
+  fill_uniform(relation, n_rel, w * dr, 6.0 / std::sqrt(static_cast<double>(dr)), rng);
   if (model == SKG_TRANSR && proj) {
     std::memset(proj, 0, sizeof(float) * n_rel * dr * de);
     for (int64_t r = 0; r < n_rel; ++r)

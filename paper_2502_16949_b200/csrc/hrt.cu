@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, SKG_FWD_MINB) hrt_forward_kernel(con
 // L2: v * (up / ||v||_eps); torus-L2: (up * 2) * delta; L1 / torus-L1: sign weight.
 template <int KIND>
 __device__ __forceinline__ float dir1(float r, float sc) {
-  if (KIND == kPlainRows) return r;
+  if (KIND == kPlainRows || KIND == kMultRows) return r;
   if (KIND == kTransE_L2 || KIND == kTorusE_L2) return __fmul_rn(r, sc);
   return r > 0.f ? sc : (r < 0.f ? -sc : 0.f);
 }
@@ -475,7 +475,11 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
           for (int q = 0; q < KB; ++q) {
             vq[q] = __shfl_sync(kFull, myv, k[q]);
             scq[q] = __shfl_sync(kFull, mysc, k[q]);
-            const size_t rowoff = static_cast<size_t>(vq[q] & 0x7fffffffu) * dv;
+            size_t rowoff = static_cast<size_t>(vq[q] & 0x7fffffffu) * dv;
+            if (KIND == kMultRows) {  // the entry's own gradient plane: head, tail or relation
+              const uint32_t slot = col >= static_cast<uint32_t>(a.N) ? 2u : (vq[q] >> 31);
+              rowoff += static_cast<size_t>(slot) * a.plane_rows * dv;
+            }
 #pragma unroll
             for (int h = 0; h < CH; ++h)
               if (q < n && has[h]) rv[q][h] = __ldg(RV + rowoff + c[h]);
@@ -483,7 +487,7 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
 #pragma unroll
           for (int q = 0; q < KB; ++q)
             if (q < n) {
-              const bool neg = (vq[q] >> 31) != 0;
+              const bool neg = KIND != kMultRows && (vq[q] >> 31) != 0;
 #pragma unroll
               for (int h = 0; h < CH; ++h)
                 if (has[h]) acc_add<KIND>(acc[h], rv[q][h], scq[q], neg);
@@ -600,6 +604,7 @@ void launch_segment_backward(int kind, bool sgd, const BwdArgs& a, int num_sms, 
     case kTorusE_L2: launch_bwd_k<kTorusE_L2>(sgd, a, num_sms, s); break;
     case kTorusE_L1: launch_bwd_k<kTorusE_L1>(sgd, a, num_sms, s); break;
     case kPlainRows: launch_bwd_k<kPlainRows>(sgd, a, num_sms, s); break;
+    case kMultRows: launch_bwd_k<kMultRows>(sgd, a, num_sms, s); break;
     default: throw CudaError("launch_segment_backward: unsupported kind");
   }
 }

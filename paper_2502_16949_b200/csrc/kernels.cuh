@@ -5,6 +5,10 @@
 //                 71-92; norms.hpp; training.cpp:73-94)
 //   ht_forward    TransH hyperplane / TransR projection forward on the ht
 //                 layout (models.cpp:110-134, 158-181)
+//   mult_forward  DistMult / ComplEx / RotatE forward on the multiplicative
+//                 layout: times-times (or mulsub) row, exact-order score sum,
+//                 hinge, loss and the three per-entry gradient rows
+//                 (models.cpp:201-263, sparse.hpp:91-106, 315-391)
 //   segment_backward  transposed-SpMM scatter A^T D as a sorted-segment,
 //                 warp-per-column reduction fused with the SGD update
 //                 (sparse.hpp:273-306, embedding.cpp:165-190)
@@ -26,7 +30,13 @@ enum Kind : int {
   kTransR_L2 = 6,
   kTransR_L1 = 7,
   kPlainRows = 8,  // backward rows already hold a*D (ht models' du rows)
+  kDistMult = 9,   // multiplicative family (norm ignored, as in the reference)
+  kComplEx = 10,
+  kRotatE = 11,
+  kMultRows = 12,  // backward rows: per-entry gradient planes [head | tail | relation]
 };
+inline bool is_mult_kind(int k) { return k >= kDistMult && k <= kRotatE; }
+inline bool is_ht_kind(int k) { return k >= kTransH_L2 && k <= kTransR_L1; }
 
 struct FwdArgs {
   // parameters
@@ -50,6 +60,8 @@ struct FwdArgs {
   float* res_u;   // ht models: u = h - t rows (de wide)
   float* scal;    // per-row gradient scale (0 = inactive)
   float* scores;  // SCORE mode
+  int64_t plane_rows;  // multiplicative: rows per gradient plane (res holds 3 planes)
+  float sign;          // multiplicative: energy_sign (models.hpp:35-38)
   // loss reduction
   float* block_partial;
   unsigned* counter;
@@ -73,11 +85,14 @@ struct BwdArgs {
   const float* lr;  // device scalar (lets one captured graph serve every epoch)
   uint32_t* err;
   int entity_only;  // skip relation-column segments (ht models reduce them separately)
+  int64_t plane_rows;  // kMultRows: rows per plane; slot = relation column ? 2 : tail entry ? 1 : 0
 };
 
 void configure_hrt_kernels();
 void configure_ht_kernels();
 void launch_hrt_forward(int kind, bool train, const FwdArgs& a, int num_sms, cudaStream_t s);
 void launch_segment_backward(int kind, bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s);
+void configure_mult_kernels();
+void launch_mult_forward(int kind, bool train, const FwdArgs& a, int num_sms, cudaStream_t s);
 
 }  // namespace skg

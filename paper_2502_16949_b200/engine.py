@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-MODELS = {"transe": 0, "transr": 1, "transh": 2, "toruse": 3}
+MODELS = {"transe": 0, "transr": 1, "transh": 2, "toruse": 3, "distmult": 4, "complex": 5, "rotate": 6}
+COMPLEX_TAGS = (5, 6)  # ComplEx / RotatE tables: dim interleaved (re, im) float pairs per row
 NORMS = {"l1": 0, "l2": 1}
 KINDS = {1: "ShapeError", 2: "ConfigError", 3: "DegenerateTripleError", 4: "TrainingError",
          5: "ParseError", 6: "CudaError"}
@@ -166,7 +167,8 @@ class Engine:
     # ------------------------------------------------------------ store
     def store_upload(self, cfg: ModelConfig, entity, relation, proj=None, normals=None):
         entity, relation, proj, normals = _f32(entity), _f32(relation), _f32(proj), _f32(normals)
-        self.dims = (entity.shape[0], relation.shape[0], cfg.dim_entity, cfg.dim_relation,
+        w = 2 if cfg.model in COMPLEX_TAGS else 1
+        self.dims = (entity.shape[0], relation.shape[0], w * cfg.dim_entity, w * cfg.dim_relation,
                      proj is not None, normals is not None)
         self._check(self.L.skg_store_upload(self.h, C.byref(cfg), entity.shape[0], relation.shape[0], _p(entity),
                                             _p(relation), _p(proj), _p(normals)))
@@ -217,7 +219,7 @@ class Engine:
         col = np.empty(3 * m + 1, np.int64)
         val = np.empty(3 * m + 1, np.float32)
         nnz = C.c_int64()
-        self._check(self.L.skg_build_incidence(self.h, {"ht": 0, "hrt": 1}[layout], m, _p(h), _p(r), _p(t),
+        self._check(self.L.skg_build_incidence(self.h, {"ht": 0, "hrt": 1, "mult": 2, "mult_conj": 3}[layout], m, _p(h), _p(r), _p(t),
                                                num_entities, num_relations, _p(rp), _p(col), _p(val),
                                                C.byref(nnz)))
         return rp, col[:nnz.value].copy(), val[:nnz.value].copy()
@@ -226,8 +228,8 @@ class Engine:
         h, r, t = _i64(h), _i64(r), _i64(t)
         m = len(h)
         scores = np.empty(max(m, 1), np.float32)
-        d = cfg.dim_entity if cfg.model in (0, 3) else cfg.dim_relation
-        res = np.empty((max(m, 1), d), np.float32) if residual else None
+        d = cfg.dim_entity if cfg.model in (0, 3) else 2 * cfg.dim_entity if cfg.model == 6 else cfg.dim_relation
+        res = np.empty((max(m, 1), d), np.float32) if residual else None  # RotatE: q rows (re, im)
         self._check(self.L.skg_score_batch(self.h, C.byref(cfg), m, _p(h), _p(r), _p(t), _p(scores), _p(res)))
         return (scores[:m], res[:m]) if residual else scores[:m]
 
@@ -355,8 +357,9 @@ def generate_synthetic(n_entities: int, n_relations: int, n_triples: int, seed: 
 def init_store(model: str, n_entities: int, n_relations: int, de: int, dr: int, seed: int):
     """init_store (embedding.cpp:129-163) on the host; returns fp32 tables."""
     L = load_library()
-    e = np.empty((n_entities, de), np.float32)
-    r = np.empty((n_relations, dr), np.float32)
+    w = 2 if MODELS[model] in COMPLEX_TAGS else 1
+    e = np.empty((n_entities, w * de), np.float32)
+    r = np.empty((n_relations, w * dr), np.float32)
     p = np.empty((n_relations, dr * de), np.float32) if model == "transr" else None
     n = np.empty((n_relations, de), np.float32) if model == "transh" else None
     _host_check(L, L.skg_init_store(MODELS[model], n_entities, n_relations, de, dr, seed, _p(e), _p(r), _p(p), _p(n)))
@@ -387,16 +390,18 @@ def save_checkpoint(path: str, model: str, entity, relation, proj=None, normals=
     e, r = _f32(entity), _f32(relation)
     p = None if proj is None else _f32(proj)
     n = None if normals is None else _f32(normals)
-    _ckpt_check(L, L.skg_save_checkpoint(path.encode(), MODELS[model], e.shape[0], r.shape[0], e.shape[1], r.shape[1],
-                                         _p(e), _p(r), _p(p), _p(n)))
+    w = 2 if MODELS[model] in COMPLEX_TAGS else 1
+    _ckpt_check(L, L.skg_save_checkpoint(path.encode(), MODELS[model], e.shape[0], r.shape[0], e.shape[1] // w,
+                                         r.shape[1] // w, _p(e), _p(r), _p(p), _p(n)))
 
 
 def load_checkpoint(path: str, expected: str):
     """load_checkpoint<Real>(path, expected) -> (entity, relation, proj, normals) fp32 tables."""
     L = load_library()
     h = peek_checkpoint(path)
-    e = np.empty((h.num_entities, h.dim_entity), np.float32)
-    r = np.empty((h.num_relations, h.dim_relation), np.float32)
+    w = 2 if h.model in COMPLEX_TAGS else 1
+    e = np.empty((h.num_entities, w * h.dim_entity), np.float32)
+    r = np.empty((h.num_relations, w * h.dim_relation), np.float32)
     p = np.empty((h.num_relations, h.dim_relation * h.dim_entity), np.float32) if h.model == 1 else None
     n = np.empty((h.num_relations, h.dim_entity), np.float32) if h.model == 2 else None
     _ckpt_check(L, L.skg_load_checkpoint(path.encode(), MODELS[expected], _p(e), _p(r), _p(p), _p(n)))
