@@ -1523,7 +1523,8 @@ extern "C" skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cf
     std::vector<uint32_t> b(2 * q);
     if (eval_exact(kind)) {  // TransE / TorusE: the stacked tables as they are
       SKG_CUDA(cudaMemcpyAsync(qd.p, host.data(), sizeof(int32_t) * 3 * q, cudaMemcpyHostToDevice, ctx->stream));
-      eval_rank(kind, ctx->tables.p, ctx->tables.p + ctx->N * ctx->de, ctx->N, ctx->R, static_cast<int>(ctx->de),
+      eval_rank(kind, ctx->tables.p, ctx->tables.p + ctx->N * ctx->de, ctx->N, ctx->R,
+                static_cast<int>(is_mult(*cfg) ? cfg->dim_entity : ctx->de),
                 qd.p, qd.p + q, qd.p + 2 * q, q, tp, cap, better.p, te.p, ctx->num_sms, ctx->stream);
       SKG_CUDA(cudaMemcpyAsync(b.data(), better.p, sizeof(uint32_t) * 2 * q, cudaMemcpyDeviceToHost, ctx->stream));
     } else {  // TransH / TransR: per relation, rank against the projected entity table

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "ht.cuh"
 #include "kernels.cuh"
+#include "multmath.cuh"
 #include "primitives.cuh"
 #include "refmath.cuh"
 
@@ -264,6 +265,68 @@ __global__ void __launch_bounds__(kEvalThreads) rank_tiled_kernel(EvalArgs a, in
   if (cg == 0 && qi < nq && cnt) atomicAdd(a.better + 2 * (q0 + qi) + SIDE, cnt);
 }
 
+// Multiplicative family: energy_sign * score of the row (hc, r, tc), +inf for
+// the unrepresentable self-loop candidate (eval.cpp:24, 36-37, 44-47).
+template <int KIND>
+__device__ float mult_energy(const float* __restrict__ X, const float* __restrict__ Rt, int64_t hc, int64_t r,
+                             int64_t tc, int d) {
+  if (hc == tc) return __int_as_float(0x7f800000);
+  using U = Unit<KIND>;
+  const int W = KIND == kDistMult ? d : 2 * d;
+  const bool tail_lo = tc < hc;
+  float s = 0.f;
+  for (int j = 0; j < d; ++j)
+    s = __fadd_rn(s, U::term(U::load(X, hc, W, j), U::load(X, tc, W, j), U::load(Rt, r, W, j), tail_lo));
+  return KIND == kRotatE ? s : -s;  // DistMult / ComplEx score plausibility (models.hpp:32-38)
+}
+
+template <int KIND>
+__global__ void mult_true_energy_kernel(EvalArgs a, float* __restrict__ te) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= 2 * a.q) return;
+  const int64_t qi = i >> 1;
+  te[i] = mult_energy<KIND>(a.X, a.Rt, a.qh[qi], a.qr[qi], a.qt[qi], a.d);
+}
+
+// Thread per (query, candidate); the fixed and relation rows are shared by
+// the whole block (L1 broadcast), candidate rows stream from L2.
+template <int KIND>
+__global__ void mult_rank_kernel(EvalArgs a) {
+  const int64_t qi = blockIdx.y;
+  const int64_t h = a.qh[qi], r = a.qr[qi], t = a.qt[qi];
+  const int64_t truth = a.side == 0 ? t : h;
+  const float te = a.te[2 * qi + a.side];
+  uint32_t cnt = 0;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < a.N;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (c == truth) continue;
+    const float e = a.side == 0 ? mult_energy<KIND>(a.X, a.Rt, h, r, c, a.d) : mult_energy<KIND>(a.X, a.Rt, c, r, t, a.d);
+    if (!(e < te)) continue;
+    if (a.table && filter_contains(a.table, a.mask, a.side == 0 ? triple_key(h, r, c, a.N, a.R)
+                                                                 : triple_key(c, r, t, a.N, a.R)))
+      continue;
+    ++cnt;
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(kFull, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(a.better + 2 * qi + a.side, cnt);
+}
+
+template <int KIND>
+void launch_mult(EvalArgs a, float* te, int num_sms, cudaStream_t s) {
+  mult_true_energy_kernel<KIND><<<ceil_div(2 * a.q, 256), 256, 0, s>>>(a, te);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  a.te = te;
+  const int64_t per_q = std::max<int64_t>(1, std::min<int64_t>((a.N + 255) / 256, (4 * num_sms + a.q - 1) / a.q));
+  for (int side = 0; side < 2; ++side) {
+    a.side = side;
+    dim3 grid(static_cast<unsigned>(per_q), static_cast<unsigned>(a.q));
+    mult_rank_kernel<KIND><<<grid, 256, 0, s>>>(a);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+  }
+}
+
 template <int KIND>
 void launch_kind(EvalArgs a, float* te, int num_sms, cudaStream_t s) {
   true_energy_kernel<KIND><<<ceil_div(2 * a.q, 256), 256, 0, s>>>(a, te);
@@ -300,8 +363,8 @@ void configure_tiled() {
 
 }  // namespace
 
-bool eval_supported(int kind) { return kind >= kTransE_L2 && kind <= kTransR_L1; }
-bool eval_exact(int kind) { return kind <= kTorusE_L1; }
+bool eval_supported(int kind) { return (kind >= kTransE_L2 && kind <= kTransR_L1) || is_mult_kind(kind); }
+bool eval_exact(int kind) { return kind <= kTorusE_L1 || is_mult_kind(kind); }
 
 // TransH / TransR rank through per-relation projected entity tables: the ht
 // row (a, r, b) scores ||P_r a - P_r b + r_vec|| with the linear map
@@ -420,6 +483,9 @@ void eval_rank(int kind, const float* X, const float* Rt, int64_t N, int64_t R, 
     case kTransE_L1: launch_kind<kTransE_L1>(a, te, num_sms, s); break;
     case kTorusE_L2: launch_kind<kTorusE_L2>(a, te, num_sms, s); break;
     case kTorusE_L1: launch_kind<kTorusE_L1>(a, te, num_sms, s); break;
+    case kDistMult: launch_mult<kDistMult>(a, te, num_sms, s); break;
+    case kComplEx: launch_mult<kComplEx>(a, te, num_sms, s); break;
+    case kRotatE: launch_mult<kRotatE>(a, te, num_sms, s); break;
     default: throw CudaError("eval: model kind not supported on device");
   }
 }

@@ -12,7 +12,6 @@ import numpy as np
 import pytest
 
 from paper_2502_16949_b200 import Engine, EngineError, ModelConfig, TrainConfig
-from oracle.oracle import Store
 
 pytestmark = pytest.mark.gpu
 
@@ -196,3 +195,34 @@ def test_nonfinite_gradient_raises(eng, orc32, model):
     with pytest.raises(EngineError) as e:
         eng.train_epoch(cfg, TrainConfig.make(batch_size=16, seed=2, lr=0.1), 0, 0.1)
     assert e.value.kind == "TrainingError"
+
+
+def test_degenerate_queries_rank_last(eng, orc32):  # test_eval.cpp:185-197
+    st = orc32.init_store("distmult", 5, 1, 3, 3, 4)
+    cfg = upload(eng, "distmult", st)
+    assert eng.rank_entities(cfg, [2], [0], [2]).tolist() == [[5, 5]]
+    got = eng.rank_entities(cfg, [2], [0], [1])
+    assert 1 <= got[0, 0] <= 4
+    assert np.array_equal(got, orc32.rank_entities("distmult", st, [2], [0], [1]))
+
+
+@pytest.mark.parametrize("model", MODELS)
+@pytest.mark.parametrize("d", [1, 6, 32])
+@pytest.mark.parametrize("filtered", [False, True])
+def test_ranks_bitexact(eng, orc32, model, d, filtered):  # eval.cpp:16-63
+    n, r, q = 300, 5, 20
+    rng = np.random.default_rng(d * 11 + filtered)
+    st = orc32.init_store(model, n, r, d, d, 7)
+    if d == 1:  # coarse values: exact ties
+        st.entity[:] = rng.integers(-3, 4, st.entity.shape) / 4.0
+        st.relation[:] = rng.integers(-3, 4, st.relation.shape) / 4.0
+    h, rel, t = rng.integers(0, n, q), rng.integers(0, r, q), rng.integers(0, n, q)
+    h[:2] = t[:2]  # self-loop queries rank dead last
+    filt = None
+    if filtered:
+        fh, fr, ft = rng.integers(0, n, 3000), rng.integers(0, r, 3000), rng.integers(0, n, 3000)
+        filt = (np.concatenate([fh, h]), np.concatenate([fr, rel]), np.concatenate([ft, t]))
+    cfg = upload(eng, model, st)
+    got = eng.rank_entities(cfg, h, rel, t, filt=filt)
+    ref = orc32.rank_entities(model, st, h, rel, t, filt=filt)
+    assert np.array_equal(got, ref), np.argwhere(got != ref)[:5]
