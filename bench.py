@@ -47,6 +47,17 @@ CONFIGS = {
                desc="TransE d=256 on synthetic ogbl-wikikg2-shaped graph (2.5M ent, 535 rel, 16.1M triples), "
                     "batch 131072"),
 }
+# Not BASELINE configs: the multiplicative family on the C1
+# graph at the C1 batch, for its own throughput / roofline lines. Complex
+# models use dim 64 (128 floats per row, the same bytes as C1's d=128).
+EXTRA = {
+    "M1": dict(CONFIGS["C1"], model="distmult", desc="DistMult d=128 on the C1 (FB15k-shaped) graph, batch 32768"),
+    "M2": dict(CONFIGS["C1"], model="complex", de=64, dr=64,
+               desc="ComplEx d=64 complex (128 floats) on the C1 (FB15k-shaped) graph, batch 32768"),
+    "M3": dict(CONFIGS["C1"], model="rotate", de=64, dr=64,
+               desc="RotatE d=64 complex (128 floats) on the C1 (FB15k-shaped) graph, batch 32768"),
+}
+MULT = ("distmult", "complex", "rotate")
 METRIC = "train triplets/sec per model at 1/2/4/8 B200; SpMM fwd/bwd HBM GB/s vs peak"
 SEED, LR, MARGIN = 1, 4e-4, 0.5
 
@@ -170,6 +181,8 @@ def algorithmic_bytes(cfg, eng, nb):
     plus ids (order + 5 ids per pair) and the per-row scale; backward: one residual
     row + value + scale per nonzero, and a read + write of every touched row."""
     d, dr = cfg["de"], cfg["dr"]
+    if cfg["model"] in ("complex", "rotate"):
+        d = dr = 2 * cfg["de"]  # floats per row
     fwd = bwd = 0
     M = eng.m
     for b in range(nb):
@@ -180,6 +193,8 @@ def algorithmic_bytes(cfg, eng, nb):
             fwd += 10 * Bb * d * 4 + ids
         elif cfg["model"] == "transr":  # (4B d_e + 2B d_r + 2B d_e + R d_r d_e) s
             fwd += (4 * Bb * d + 2 * Bb * dr + 2 * Bb * d + cfg["R"] * dr * d) * 4 + ids
+        elif cfg["model"] in MULT:      # 3 gathers + 3 per-entry gradient rows per incidence row
+            fwd += 2 * Bb * 6 * d * 4 + ids
         else:                           # TransE / TorusE: 3 gathers + 1 residual row per incidence row
             fwd += 2 * Bb * 4 * d * 4 + ids
         bwd += entries * (d * 4 + 8) + segs * (2 * d * 4 + 12)
@@ -223,12 +238,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS) + sorted(EXTRA))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for the CPU legs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = CONFIGS.get(args.config) or EXTRA[args.config]
+    avoid = cfg["model"] in MULT  # fit: negative_sample(..., is_multiplicative_model) (training.cpp:176)
     rank, world, local = dist_setup()
     threads = os.cpu_count() or 1
     config_obj = {"workload": args.config + ": " + cfg["desc"], "model": cfg["model"], "norm": cfg["norm"],
@@ -246,7 +262,7 @@ def main():
             return
         from oracle.oracle import Oracle
         orc = Oracle("f32")
-        nh, nt = orc.negative_sample(h, r, t, cfg["N"], cfg["R"], SEED)
+        nh, nt = orc.negative_sample(h, r, t, cfg["N"], cfg["R"], SEED, avoid)
         vals = []
         sample = ""
         for _ in range(max(1, args.steps)):
@@ -272,7 +288,7 @@ def main():
     ent, rel, proj, nrm = init_store(cfg["model"], cfg["N"], cfg["R"], cfg["de"], cfg["dr"], SEED)
     eng.store_upload(mcfg, ent, rel, proj, nrm)
     eng.set_triples(h, r, t, cfg["N"], cfg["R"])
-    nh, nt = eng.negative_sample(SEED)
+    nh, nt = eng.negative_sample(SEED, avoid)
     if world > 1:
         uid = broadcast_bytes(Engine.nccl_unique_id() if rank == 0 else None, world)
         eng.dp_init(uid, rank, world)

@@ -41,8 +41,17 @@ struct TrainingError : std::runtime_error { using std::runtime_error::runtime_er
 struct ParseError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
 
-enum class ModelKind : std::uint32_t { TransE = 0, TransR = 1, TransH = 2, TorusE = 3 };
+enum class ModelKind : std::uint32_t {
+  TransE = 0, TransR = 1, TransH = 2, TorusE = 3, DistMult = 4, ComplEx = 5, RotatE = 6
+};
 enum class NormKind : std::uint32_t { L1 = 0, L2 = 1 };
+// common.hpp:74-82, models.hpp:32-38
+inline bool is_complex_model(ModelKind m) { return m == ModelKind::ComplEx || m == ModelKind::RotatE; }
+inline bool is_multiplicative_model(ModelKind m) {
+  return m == ModelKind::DistMult || m == ModelKind::ComplEx || m == ModelKind::RotatE;
+}
+inline bool higher_is_better(ModelKind m) { return m == ModelKind::DistMult || m == ModelKind::ComplEx; }
+inline Real energy_sign(ModelKind m) { return higher_is_better(m) ? Real(-1) : Real(1); }
 enum class Engine { Sparse, Dense };
 
 struct Matrix {  // row-major, one embedding per row
@@ -75,7 +84,10 @@ struct ModelConfig {  // models.hpp:17-30
   NormKind norm = NormKind::L2;
 };
 
-struct EmbeddingStore {  // embedding.hpp:15-31
+// embedding.hpp:15-31. ComplEx / RotatE stores (EmbeddingStoreT<Complex> in the
+// reference) hold dim interleaved (re, im) pairs per row: 2 * dim columns here,
+// the same bytes as a row-major std::complex<float> matrix.
+struct EmbeddingStore {
   Matrix entity, relation, proj, normals;
   Index num_entities() const { return entity.rows(); }
   Index num_relations() const { return relation.rows(); }
@@ -175,8 +187,9 @@ inline skg_train_config tcfg(const TrainConfig& t) {
 }
 inline void upload(const ModelConfig& mc, const EmbeddingStore& s) {
   skg_model_config c = cfg(mc);
-  c.dim_entity = s.dim_entity();
-  c.dim_relation = s.dim_relation();
+  const Index w = is_complex_model(mc.model) ? 2 : 1;
+  c.dim_entity = s.dim_entity() / w;
+  c.dim_relation = s.dim_relation() / w;
   check(skg_store_upload(ctx(), &c, s.num_entities(), s.num_relations(), s.entity.data(), s.relation.data(),
                          s.has_proj() ? s.proj.data() : nullptr, s.has_normals() ? s.normals.data() : nullptr));
 }
@@ -200,9 +213,10 @@ inline EmbeddingStore init_store(ModelKind model, Index n_ent, Index n_rel, Inde
   if (n_ent < 1 || n_rel < 1) throw ConfigError("store needs at least one entity and one relation");
   std::mt19937_64 rng(seed);
   EmbeddingStore s;
-  s.entity = Matrix(n_ent, de);
+  const Index w = is_complex_model(model) ? 2 : 1;  // re then im per coordinate (embedding.cpp:21-25)
+  s.entity = Matrix(n_ent, w * de);
   detail::fill_uniform(s.entity, 6.0 / std::sqrt(static_cast<double>(de)), rng);
-  s.relation = Matrix(n_rel, dr);
+  s.relation = Matrix(n_rel, w * dr);
   detail::fill_uniform(s.relation, 6.0 / std::sqrt(static_cast<double>(dr)), rng);
   if (model == ModelKind::TransR) {
     s.proj = Matrix(n_rel, dr * de);
@@ -253,10 +267,13 @@ inline ScoreBatch score_batch(const ModelConfig& cfg, const EmbeddingStore& stor
   skg_model_config c = detail::cfg(cfg);
   ScoreBatch sb;
   sb.scores.resize(static_cast<size_t>(b.size()));
-  const Index d = (cfg.model == ModelKind::TransE || cfg.model == ModelKind::TorusE) ? cfg.dim_entity : cfg.dim_relation;
-  sb.v = Matrix(b.size(), d);
+  const Index d = (cfg.model == ModelKind::TransE || cfg.model == ModelKind::TorusE) ? cfg.dim_entity
+                  : cfg.model == ModelKind::RotatE                                    ? 2 * cfg.dim_entity
+                  : is_multiplicative_model(cfg.model)                                ? 0
+                                                                                      : cfg.dim_relation;
+  sb.v = Matrix(b.size(), d);  // DistMult / ComplEx keep no residual (models.cpp:203-231)
   detail::check(skg_score_batch(detail::ctx(), &c, b.size(), b.heads.data(), b.relations.data(), b.tails.data(),
-                                sb.scores.data(), sb.v.data()));
+                                sb.scores.data(), d ? sb.v.data() : nullptr));
   return sb;
 }
 
@@ -338,8 +355,9 @@ inline CheckpointHeader peek_checkpoint(const std::string& path) {
 }
 
 inline void save_checkpoint(const std::string& path, ModelKind model, const EmbeddingStore& s) {
+  const Index w = is_complex_model(model) ? 2 : 1;
   const skg_status st = skg_save_checkpoint(path.c_str(), static_cast<std::uint32_t>(model), s.entity.rows(),
-                                            s.relation.rows(), s.entity.cols(), s.relation.cols(), s.entity.data(),
+                                            s.relation.rows(), s.entity.cols() / w, s.relation.cols() / w, s.entity.data(),
                                             s.relation.data(), s.proj.size() ? s.proj.data() : nullptr,
                                             s.normals.size() ? s.normals.data() : nullptr);
   if (st != SKG_OK) detail::rethrow_ckpt(st);
@@ -348,8 +366,9 @@ inline void save_checkpoint(const std::string& path, ModelKind model, const Embe
 inline EmbeddingStore load_checkpoint(const std::string& path, ModelKind expected) {
   const CheckpointHeader h = peek_checkpoint(path);
   EmbeddingStore s;
-  s.entity = Matrix(h.num_entities, h.dim_entity);
-  s.relation = Matrix(h.num_relations, h.dim_relation);
+  const Index w = is_complex_model(h.model) ? 2 : 1;
+  s.entity = Matrix(h.num_entities, w * h.dim_entity);
+  s.relation = Matrix(h.num_relations, w * h.dim_relation);
   if (h.model == ModelKind::TransR) s.proj = Matrix(h.num_relations, h.dim_relation * h.dim_entity);
   if (h.model == ModelKind::TransH) s.normals = Matrix(h.num_relations, h.dim_entity);
   const skg_status st = skg_load_checkpoint(path.c_str(), static_cast<std::uint32_t>(expected), s.entity.data(),

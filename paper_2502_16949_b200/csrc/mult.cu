@@ -84,10 +84,35 @@ __device__ __forceinline__ void contributions(typename Unit<KIND>::T h, typename
 __device__ __forceinline__ bool fin(float a) { return finite_f(a); }
 __device__ __forceinline__ bool fin(float2 a) { return finite2(a); }
 
+// 16-byte chunks of a table row: 4 real coordinates or 2 complex ones.
+template <int KIND>
+struct Chunk {
+  static constexpr int NU = KIND == kDistMult ? 4 : 2;  // coordinates per float4
+  using T = typename Unit<KIND>::T;
+  static __device__ __forceinline__ T get(const float4& v, int k) {
+    if constexpr (KIND == kDistMult) {
+      return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+    } else {
+      return k == 0 ? make_float2(v.x, v.y) : make_float2(v.z, v.w);
+    }
+  }
+  static __device__ __forceinline__ void put(float4& v, int k, T x) {
+    if constexpr (KIND == kDistMult) {
+      if (k == 0) v.x = x;
+      else if (k == 1) v.y = x;
+      else if (k == 2) v.z = x;
+      else v.w = x;
+    } else {
+      if (k == 0) v.x = x.x, v.y = x.y;
+      else v.z = x.x, v.w = x.y;
+    }
+  }
+};
+
 // A warp owns a tile of 8 (pos, neg) pairs (TRAIN) or 16 rows (SCORE); lanes
 // run over the row's coordinates. Per-coordinate score terms are staged in
 // shared memory so that lane j then sums row j in the reference's order.
-template <int KIND, bool TRAIN>
+template <int KIND, bool TRAIN, int VEC>
 __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a) {
   using U = Unit<KIND>;
   using T = typename U::T;
@@ -147,21 +172,48 @@ __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a)
         rj[q] = __shfl_sync(kFull, r, j0 + q);
       }
       bool nf[4] = {false, false, false, false};
-      for (int c = lane; c < d; c += 32) {
-        T xh[4], xt[4], xr[4];
+      if constexpr (VEC == 4) {
+        using CK = Chunk<KIND>;
+        const float4* X4 = reinterpret_cast<const float4*>(a.X);
+        const int W4 = W >> 2;
+        for (int c = lane; c < W4; c += 32) {
+          float4 xh[4], xt[4], xr[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (!((vmask >> (j0 + q)) & 1u)) continue;
-          xh[q] = U::load(a.X, hj[q], W, c);
-          xt[q] = U::load(a.X, tj[q], W, c);
-          xr[q] = U::load(a.X, N + rj[q], W, c);
+          for (int q = 0; q < 4; ++q) {
+            if (!((vmask >> (j0 + q)) & 1u)) continue;
+            xh[q] = __ldg(X4 + static_cast<size_t>(hj[q]) * W4 + c);
+            xt[q] = __ldg(X4 + static_cast<size_t>(tj[q]) * W4 + c);
+            xr[q] = __ldg(X4 + static_cast<size_t>(N + rj[q]) * W4 + c);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (!((vmask >> (j0 + q)) & 1u)) continue;
+#pragma unroll
+            for (int k = 0; k < CK::NU; ++k) {
+              const T h1 = CK::get(xh[q], k), t1 = CK::get(xt[q], k), r1 = CK::get(xr[q], k);
+              const float v = U::term(h1, t1, r1, tj[q] < hj[q]);
+              nf[q] |= !finite_f(v) || !fin(h1) || !fin(t1) || !fin(r1);
+              rows[(j0 + q) * S + c * CK::NU + k] = v;
+            }
+          }
         }
+      } else {
+        for (int c = lane; c < d; c += 32) {
+          T xh[4], xt[4], xr[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (!((vmask >> (j0 + q)) & 1u)) continue;
-          const float v = U::term(xh[q], xt[q], xr[q], tj[q] < hj[q]);
-          nf[q] |= !finite_f(v) || !fin(xh[q]) || !fin(xt[q]) || !fin(xr[q]);
-          rows[(j0 + q) * S + c] = v;
+          for (int q = 0; q < 4; ++q) {
+            if (!((vmask >> (j0 + q)) & 1u)) continue;
+            xh[q] = U::load(a.X, hj[q], W, c);
+            xt[q] = U::load(a.X, tj[q], W, c);
+            xr[q] = U::load(a.X, N + rj[q], W, c);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (!((vmask >> (j0 + q)) & 1u)) continue;
+            const float v = U::term(xh[q], xt[q], xr[q], tj[q] < hj[q]);
+            nf[q] |= !finite_f(v) || !fin(xh[q]) || !fin(xt[q]) || !fin(xr[q]);
+            rows[(j0 + q) * S + c] = v;
+          }
         }
       }
 #pragma unroll
@@ -220,19 +272,55 @@ __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a)
       const int r2 = __shfl_sync(kFull, row2, j);
       const float uj = __shfl_sync(kFull, u, j);
       bool bad_e = false, bad_r = false;
-      for (int c = lane; c < d; c += 32) {
-        const T xh = U::load(a.X, hj, W, c), xt = U::load(a.X, tj, W, c), xr = U::load(a.X, N + rj, W, c);
-        if constexpr (KIND == kRotatE) {
-          if (want_q) reinterpret_cast<float2*>(a.res_u)[static_cast<size_t>(r2) * d + c] = Unit<kRotatE>::q(xh, xt, xr);
+      if constexpr (VEC == 4) {
+        using CK = Chunk<KIND>;
+        const float4* X4 = reinterpret_cast<const float4*>(a.X);
+        float4* P4 = reinterpret_cast<float4*>(a.res);
+        const int W4 = W >> 2;
+        for (int c = lane; c < W4; c += 32) {
+          const float4 xh = __ldg(X4 + static_cast<size_t>(hj) * W4 + c);
+          const float4 xt = __ldg(X4 + static_cast<size_t>(tj) * W4 + c);
+          const float4 xr = __ldg(X4 + static_cast<size_t>(N + rj) * W4 + c);
+          if constexpr (KIND == kRotatE) {
+            if (want_q) {
+              float4 qv;
+#pragma unroll
+              for (int k = 0; k < CK::NU; ++k)
+                CK::put(qv, k, Unit<kRotatE>::q(CK::get(xh, k), CK::get(xt, k), CK::get(xr, k)));
+              reinterpret_cast<float4*>(a.res_u)[static_cast<size_t>(r2) * W4 + c] = qv;
+            }
+          }
+          if (uj == 0.f) continue;
+          float4 vh, vt, vr;
+#pragma unroll
+          for (int k = 0; k < CK::NU; ++k) {
+            T ch, ct, cr;
+            contributions<KIND>(CK::get(xh, k), CK::get(xt, k), CK::get(xr, k), tj < hj, uj, ch, ct, cr);
+            bad_e |= !fin(ch) || !fin(ct);
+            bad_r |= !fin(cr);
+            CK::put(vh, k, ch);
+            CK::put(vt, k, ct);
+            CK::put(vr, k, cr);
+          }
+          P4[(static_cast<size_t>(0) * a.plane_rows + r2) * W4 + c] = vh;
+          P4[(static_cast<size_t>(1) * a.plane_rows + r2) * W4 + c] = vt;
+          P4[(static_cast<size_t>(2) * a.plane_rows + r2) * W4 + c] = vr;
         }
-        if (uj == 0.f) continue;
-        T ch, ct, cr;
-        contributions<KIND>(xh, xt, xr, tj < hj, uj, ch, ct, cr);
-        bad_e |= !fin(ch) || !fin(ct);
-        bad_r |= !fin(cr);
-        P0[(static_cast<size_t>(0) * a.plane_rows + r2) * d + c] = ch;
-        P0[(static_cast<size_t>(1) * a.plane_rows + r2) * d + c] = ct;
-        P0[(static_cast<size_t>(2) * a.plane_rows + r2) * d + c] = cr;
+      } else {
+        for (int c = lane; c < d; c += 32) {
+          const T xh = U::load(a.X, hj, W, c), xt = U::load(a.X, tj, W, c), xr = U::load(a.X, N + rj, W, c);
+          if constexpr (KIND == kRotatE) {
+            if (want_q) reinterpret_cast<float2*>(a.res_u)[static_cast<size_t>(r2) * d + c] = Unit<kRotatE>::q(xh, xt, xr);
+          }
+          if (uj == 0.f) continue;
+          T ch, ct, cr;
+          contributions<KIND>(xh, xt, xr, tj < hj, uj, ch, ct, cr);
+          bad_e |= !fin(ch) || !fin(ct);
+          bad_r |= !fin(cr);
+          P0[(static_cast<size_t>(0) * a.plane_rows + r2) * d + c] = ch;
+          P0[(static_cast<size_t>(1) * a.plane_rows + r2) * d + c] = ct;
+          P0[(static_cast<size_t>(2) * a.plane_rows + r2) * d + c] = cr;
+        }
       }
       if (TRAIN || a.upstream) {
         if (__any_sync(kFull, bad_e)) pend |= kPendEntity;
@@ -285,7 +373,7 @@ __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a)
 
 constexpr size_t kSmemCap = 200 * 1024;
 
-template <int KIND, bool TRAIN>
+template <int KIND, bool TRAIN, int VEC>
 void launch_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
   const int S = (a.de & 1) ? a.de : a.de + 1;
   const size_t per_warp = static_cast<size_t>(16) * S * sizeof(float);
@@ -300,23 +388,36 @@ void launch_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
   int grid = (ntiles + wpb - 1) / wpb;
   if (grid > num_sms * per_sm) grid = num_sms * per_sm;
   if (grid < 1) grid = 1;
-  mult_forward_kernel<KIND, TRAIN><<<grid, wpb * 32, smem, s>>>(a);
+  mult_forward_kernel<KIND, TRAIN, VEC><<<grid, wpb * 32, smem, s>>>(a);
   count_launch();
   SKG_LAUNCH_CHECK();
 }
 
 template <int KIND>
 void launch_k(bool train, const FwdArgs& a, int num_sms, cudaStream_t s) {
-  if (train) launch_t<KIND, true>(a, num_sms, s);
-  else launch_t<KIND, false>(a, num_sms, s);
+  // 16-byte chunks when a row is a whole number of them (and the tables are aligned)
+  const int W = KIND == kDistMult ? a.de : 2 * a.de;
+  const bool v4 = W % 4 == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  if (train) {
+    if (v4) launch_t<KIND, true, 4>(a, num_sms, s);
+    else launch_t<KIND, true, 1>(a, num_sms, s);
+  } else {
+    if (v4) launch_t<KIND, false, 4>(a, num_sms, s);
+    else launch_t<KIND, false, 1>(a, num_sms, s);
+  }
 }
 
+template <int KIND, bool TRAIN, int VEC>
+void configure_one() {
+  SKG_CUDA(cudaFuncSetAttribute(mult_forward_kernel<KIND, TRAIN, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmemCap)));
+}
 template <int KIND>
 void configure_k() {
-  SKG_CUDA(cudaFuncSetAttribute(mult_forward_kernel<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kSmemCap)));
-  SKG_CUDA(cudaFuncSetAttribute(mult_forward_kernel<KIND, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kSmemCap)));
+  configure_one<KIND, true, 4>();
+  configure_one<KIND, true, 1>();
+  configure_one<KIND, false, 4>();
+  configure_one<KIND, false, 1>();
 }
 
 }  // namespace

@@ -14,14 +14,16 @@ from paper_2502_16949_b200.engine import (EngineError, init_store, load_checkpoi
                                           save_checkpoint)
 
 
-@pytest.mark.parametrize("model,de,dr", [("transe", 5, 5), ("transr", 5, 3), ("transh", 4, 4), ("toruse", 6, 6)])
+@pytest.mark.parametrize("model,de,dr", [("transe", 5, 5), ("transr", 5, 3), ("transh", 4, 4), ("toruse", 6, 6),
+                                         ("distmult", 4, 4), ("complex", 3, 3), ("rotate", 5, 5)])
 def test_round_trip_exact(tmp_path, model, de, dr):  # test_embedding.cpp:220-245
     e, r, p, n = init_store(model, 7, 3, de, dr, 42)
     path = str(tmp_path / f"ckpt_{model}.bin")
     save_checkpoint(path, model, e, r, p, n)
     h = peek_checkpoint(path)
     assert (h.model, h.num_entities, h.num_relations, h.dim_entity, h.dim_relation) == (
-        {"transe": 0, "transr": 1, "transh": 2, "toruse": 3}[model], 7, 3, de, dr)
+        {"transe": 0, "transr": 1, "transh": 2, "toruse": 3, "distmult": 4, "complex": 5, "rotate": 6}[model],
+        7, 3, de, dr)
     e2, r2, p2, n2 = load_checkpoint(path, model)
     assert np.array_equal(e, e2) and np.array_equal(r, r2)
     assert (p is None and p2 is None) or np.array_equal(p, p2)
@@ -70,3 +72,17 @@ def test_save_validates_tables(tmp_path):  # test_embedding.cpp:322-329
         save_checkpoint(path, "transr", e, r)
     assert ei.value.kind == "ConfigError"
     assert not os.path.exists(path) or os.path.getsize(path) == 0
+
+
+def test_complex_payload_layout(tmp_path):  # test_embedding.cpp:246-256: interleaved (re, im) doubles
+    e, r, _, _ = init_store("rotate", 6, 2, 5, 5, 77)
+    assert e.shape == (6, 10) and r.shape == (2, 10)
+    path = str(tmp_path / "ckpt_rotate.bin")
+    save_checkpoint(path, "rotate", e, r)
+    b = open(path, "rb").read()
+    assert len(b) == 8 + 4 + 4 + 4 * 8 + 8 * (6 * 10 + 2 * 10)
+    v = np.frombuffer(b[48:48 + 8 * 60], np.float64).reshape(6, 10)
+    assert np.array_equal(v.astype(np.float32), e)
+    with pytest.raises(EngineError) as ei:
+        load_checkpoint(path, "complex")
+    assert ei.value.kind == "ConfigError"
