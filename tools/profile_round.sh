@@ -2,8 +2,8 @@
 # ncu --set full capture per hot kernel (summarised into profiles/ afterwards).
 set -x
 mkdir -p gpurun_out/prof
-for c in C1 C2 C3 C4 C5; do
-  extra=""; [ $c != C1 ] && extra="--no-cpu-baseline"
+for c in C1 C2 C3 C4 C5 M1 M2 M3; do
+  extra=""; [ $c != C1 ] && [ $c != M1 ] && extra="--no-cpu-baseline"
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 $extra > gpurun_out/prof/bench_$c.json 2> gpurun_out/prof/bench_$c.err
 done
 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/prof/launches_C1.csv \
@@ -20,4 +20,6 @@ cap C4_tc C4 transr_train_tc 10
 cap C5_fwd C5 hrt_forward 20
 cap C5_bwd C5 segment_backward 20
 cap C5_scatter C5 radix_scatter 8
+cap M1_fwd M1 mult_forward 20
+cap M1_bwd M1 segment_backward 20
 echo done
