@@ -15,11 +15,15 @@ cap() {  # name config kernel-regex skip
 cap C1_fwd C1 hrt_forward 20
 cap C1_bwd C1 segment_backward 20
 cap C2_tile C2 transh_tile 10
+cap C2_bwd C2 segment_backward 10
 cap C3_fwd C3 hrt_forward 12
+cap C3_bwd C3 segment_backward 12
 cap C4_tc C4 transr_train_tc 10
+cap C4_apply C4 transr_train_apply 10
 cap C5_fwd C5 hrt_forward 20
 cap C5_bwd C5 segment_backward 20
 cap C5_scatter C5 radix_scatter 8
 cap M1_fwd M1 mult_forward 20
 cap M1_bwd M1 segment_backward 20
+python tools/make_profiles.py --src gpurun_out/prof > gpurun_out/prof/make_profiles.log 2>&1
 echo done
