@@ -361,10 +361,19 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
         fa.loss_div = static_cast<float>(Bb);
         fa.margin = ctx->h_lr[1];
         fa.batch = static_cast<int>(b);
-        launch_hrt_forward(es.kind, true, fa, ctx->num_sms, s);
+        if (mult) {
+          fa.de = static_cast<int>(ctx->cfg.dim_entity);
+          fa.plane_rows = 2 * es.S;
+          fa.sign = (es.kind == kRotatE) ? 1.f : -1.f;
+          fa.res_u = nullptr;
+          launch_mult_forward(es.kind, true, fa, ctx->num_sms, s);
+        } else {
+          launch_hrt_forward(es.kind, true, fa, ctx->num_sms, s);
+        }
         mark();
         BwdArgs ba{};
         ba.X = G;
+        ba.plane_rows = 2 * es.S;
         ba.res = ctx->res.p;
         ba.scal = ctx->scal.p;
         ba.N = ctx->N;
@@ -376,7 +385,7 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
         ba.batch = static_cast<int>(b);
         ba.lr = ctx->lr_dev.p;
         ba.err = ctx->err_words.p;
-        launch_segment_backward(es.kind, false, ba, ctx->num_sms, s);
+        launch_segment_backward(mult ? static_cast<int>(kMultRows) : es.kind, false, ba, ctx->num_sms, s);
       } else {
         mark();
       }
@@ -455,8 +464,8 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   es.world = dp_world(ctx);
   es.rank = dp_rank(ctx);
   if (ctx->dp) {
-    if (is_ht(cfg) || is_mult(cfg))
-      throw ConfigError("data-parallel training supports TransE / TorusE in this build");
+    if (is_ht(cfg))
+      throw ConfigError("data-parallel training supports TransE / TorusE / DistMult / ComplEx / RotatE in this build");
     if (es.B % es.world != 0) throw ConfigError("data parallel: global batch_size must be a multiple of the world size");
     int64_t sh[5];
     dp_shard(ctx->M, es.B, es.world, es.rank, sh);

@@ -13,11 +13,12 @@ from paper_2502_16949_b200 import Engine, EngineError, ModelConfig, TrainConfig
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("model,norm", [("transe", "l2"), ("toruse", "l1")])
+@pytest.mark.parametrize("model,norm", [("transe", "l2"), ("toruse", "l1"), ("distmult", "l2"), ("complex", "l2"),
+                                        ("rotate", "l2")])
 def test_dp_world1_matches_oracle_bitwise(orc32, model, norm):
     n, r, d = 1500, 30, 32
     h, rel, t = orc32.synthetic_train(n, r, 12000, 2)
-    st = orc32.init_store(model, n, r, d, d, 2)
+    st = orc32.init_store(model, n, r, d, d, 2)  # complex models: 2 * d floats per row
     eng = Engine(0)
     eng.dp_init(Engine.nccl_unique_id(), 0, 1)
     cfg = ModelConfig.make(model, d, d, norm)
