@@ -335,7 +335,10 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
   if (dp) SKG_CUDA(cudaMemsetAsync(ctx->batch_loss.p, 0, sizeof(float) * es.nb, s));
   const bool ht = is_ht_kind(es.kind);
   const bool mult = is_mult_kind(es.kind);
-  const int64_t n_params = (ctx->N + ctx->R) * ctx->de;
+  // data-parallel gradient sink: [entity | relation | proj | normals] + 2 flag slots
+  const int64_t n_params = ctx->N * ctx->de + ctx->R * ctx->dr;
+  const int64_t n_proj = ctx->proj.n, n_norm = ctx->normals.n;
+  const int64_t n_sink = n_params + (ht ? n_proj + n_norm : 0);
   const int64_t nb_run = es.nb_run >= 0 ? es.nb_run : es.nb;
   for (int64_t b = 0; b < nb_run; ++b) {
     const int64_t lo = b * es.B;
@@ -345,7 +348,7 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
       // into the dense sink, NCCL sum over NVLink, identical step on all ranks
       const int64_t Sb = b < es.nb - 1 ? es.S : es.s_last;
       float* G = ctx->dp_grad.p;
-      SKG_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * (n_params + 2), s));
+      SKG_CUDA(cudaMemsetAsync(G, 0, sizeof(float) * (n_sink + 2), s));
       if (Sb > 0) {
         FwdArgs fa = base_fwd(ctx);
         fa.order = ps.order_g.p + b * es.S;
@@ -361,7 +364,25 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
         fa.loss_div = static_cast<float>(Bb);
         fa.margin = ctx->h_lr[1];
         fa.batch = static_cast<int>(b);
-        if (mult) {
+        if (ht) {  // TransH / TransR: this rank's gradients into the sink, no in-place step
+          BwdArgs hb{};
+          hb.X = G;
+          hb.Xrel = G + ctx->N * ctx->de;
+          hb.res = ctx->res_u.p;
+          hb.scal = ctx->scal.p;
+          hb.N = ctx->N;
+          hb.d = static_cast<int>(ctx->de);
+          hb.ent_val = ps.plan.sorted_val;
+          hb.seg_start = ps.plan.seg_start;
+          hb.seg_col = ps.plan.seg_col;
+          hb.seg_base = ps.plan.seg_base;
+          hb.batch = static_cast<int>(b);
+          hb.lr = ctx->lr_dev.p;
+          hb.err = ctx->err_words.p;
+          HtSinks sk{G + ctx->N * ctx->de, n_proj ? G + n_params : nullptr,
+                     n_norm ? G + n_params + n_proj : nullptr};
+          ht_train_batch(es.kind, fa, hb, ctx->ht_work.p, ctx->num_sms, s, nullptr, ctx->R, &sk);
+        } else if (mult) {
           fa.de = static_cast<int>(ctx->cfg.dim_entity);
           fa.plane_rows = 2 * es.S;
           fa.sign = (es.kind == kRotatE) ? 1.f : -1.f;
@@ -385,15 +406,27 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
         ba.batch = static_cast<int>(b);
         ba.lr = ctx->lr_dev.p;
         ba.err = ctx->err_words.p;
-        launch_segment_backward(mult ? static_cast<int>(kMultRows) : es.kind, false, ba, ctx->num_sms, s);
+        if (!ht) launch_segment_backward(mult ? static_cast<int>(kMultRows) : es.kind, false, ba, ctx->num_sms, s);
       } else {
         mark();
       }
-      dp_flags_kernel<<<1, 1, 0, s>>>(ctx->err_words.p, G + n_params);
-      dp_allreduce_sum(ctx, G, n_params + 2, s);
-      dp_sgd_kernel<<<grid_for(n_params), 256, 0, s>>>(ctx->tables.p, G, n_params, ctx->lr_dev.p, G + n_params,
+      float* flags = G + n_sink;
+      dp_flags_kernel<<<1, 1, 0, s>>>(ctx->err_words.p, flags);
+      dp_allreduce_sum(ctx, G, n_sink + 2, s);
+      dp_sgd_kernel<<<grid_for(n_params), 256, 0, s>>>(ctx->tables.p, G, n_params, ctx->lr_dev.p, flags,
                                                         ctx->err_words.p, static_cast<int>(b));
       count_launch(2);
+      if (ht && n_proj) {
+        dp_sgd_kernel<<<grid_for(n_proj), 256, 0, s>>>(ctx->proj.p, G + n_params, n_proj, ctx->lr_dev.p, flags,
+                                                        ctx->err_words.p, static_cast<int>(b));
+        count_launch();
+      }
+      if (ht && n_norm) {
+        dp_sgd_kernel<<<grid_for(n_norm), 256, 0, s>>>(ctx->normals.p, G + n_params + n_proj, n_norm, ctx->lr_dev.p,
+                                                        flags, ctx->err_words.p, static_cast<int>(b));
+        count_launch();
+        launch_normals_renorm(ctx->normals.p, ctx->R, static_cast<int>(ctx->de), ctx->err_words.p, s);
+      }
       SKG_LAUNCH_CHECK();
       mark();
       continue;
@@ -464,8 +497,6 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   es.world = dp_world(ctx);
   es.rank = dp_rank(ctx);
   if (ctx->dp) {
-    if (is_ht(cfg))
-      throw ConfigError("data-parallel training supports TransE / TorusE / DistMult / ComplEx / RotatE in this build");
     if (es.B % es.world != 0) throw ConfigError("data parallel: global batch_size must be a multiple of the world size");
     int64_t sh[5];
     dp_shard(ctx->M, es.B, es.world, es.rank, sh);
@@ -474,7 +505,7 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
     es.s_last = sh[2];
     es.Mg = sh[3];
     for (auto& sl : ctx->slots) sl.order_g.ensure(es.Mg + 1);
-    ctx->dp_grad.ensure((ctx->N + ctx->R) * ctx->de + 2);
+    ctx->dp_grad.ensure(ctx->N * ctx->de + ctx->R * ctx->dr + ctx->proj.n + ctx->normals.n + 2);
   }
   for (auto& sl : ctx->slots) {
     sl.order.ensure(ctx->M + 1);

@@ -473,6 +473,12 @@ void launch_relation_side(const FwdArgs& fa, const BwdArgs& ba, float* partial, 
 
 }  // namespace
 
+void launch_normals_renorm(float* normals, int64_t R, int d, uint32_t* err, cudaStream_t s) {
+  normals_renorm_kernel<<<static_cast<unsigned>((R * 32 + 127) / 128), 128, 0, s>>>(normals, R, d, err);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
 // work layout (floats): [nrm rows: rows x d][partials: R x parts x 2 x d]
 int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R) {
   if (kind == kTransR_L2 || kind == kTransR_L1) return transr_work_floats(rows, de, dr, R);
@@ -497,17 +503,19 @@ void configure_ht_kernels() {
 }
 
 void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                    const std::function<void()>* mark, int64_t R) {
+                    const std::function<void()>* mark, int64_t R, const HtSinks* sinks) {
   if (kind == kTransR_L2 || kind == kTransR_L1) {
-    transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R);
+    transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R, sinks);
     return;
   }
+  float* normals = const_cast<float*>(fa.normals);
   if (transh_tiles_supported(fa.de, fa.dr, R)) {  // relation-tiled path (transh_train.cu)
-    transh_tiles_train_batch(kind == kTransH_L2, fa, ba, work, R, num_sms, s, mark);
-    normals_renorm_kernel<<<static_cast<unsigned>((R * 32 + 127) / 128), 128, 0, s>>>(const_cast<float*>(fa.normals), R,
-                                                                                   fa.de, ba.err);
-    count_launch();
-    SKG_LAUNCH_CHECK();
+    transh_tiles_train_batch(kind == kTransH_L2, fa, ba, work, R, num_sms, s, mark, sinks);
+    if (!sinks) {  // data parallel renormalizes after the dense step
+      normals_renorm_kernel<<<static_cast<unsigned>((R * 32 + 127) / 128), 128, 0, s>>>(normals, R, fa.de, ba.err);
+      count_launch();
+      SKG_LAUNCH_CHECK();
+    }
     if (mark) (*mark)();
     return;
   }
@@ -517,13 +525,14 @@ void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work,
   if (mark) (*mark)();
   BwdArgs eb = ba;
   eb.entity_only = 1;
-  launch_segment_backward(kPlainRows, true, eb, num_sms, s);
-  float* rel = const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
-  float* normals = const_cast<float*>(fa.normals);
-  launch_relation_side(fa, ba, partial, rel, normals, true, R, nrm, s);
-  normals_renorm_kernel<<<static_cast<unsigned>((R * 32 + 127) / 128), 128, 0, s>>>(normals, R, fa.de, ba.err);
-  count_launch();
-  SKG_LAUNCH_CHECK();
+  launch_segment_backward(kPlainRows, sinks == nullptr, eb, num_sms, s);
+  float* rel = sinks ? sinks->rel : const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
+  launch_relation_side(fa, ba, partial, rel, sinks ? sinks->normals : normals, sinks == nullptr, R, nrm, s);
+  if (!sinks) {
+    normals_renorm_kernel<<<static_cast<unsigned>((R * 32 + 127) / 128), 128, 0, s>>>(normals, R, fa.de, ba.err);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+  }
   if (mark) (*mark)();
 }
 

@@ -11,6 +11,17 @@ struct skg_ctx;
 
 namespace skg {
 
+// Data-parallel training of the ht models: the step writes this rank's
+// gradients into zeroed sinks instead of applying SGD (the engine sums them
+// over NVLink and applies one dense step); the entity sink is BwdArgs::X.
+struct HtSinks {
+  float* rel;      // R x d_r
+  float* proj;     // TransR: R x (d_r d_e)
+  float* normals;  // TransH: R x d_e
+};
+
+// embedding.cpp:181-189 on the TransH normals (after a data-parallel dense step)
+void launch_normals_renorm(float* normals, int64_t R, int d, uint32_t* err, cudaStream_t s);
 // Floats of per-batch scratch the ht kernels need for `rows` rows.
 int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R);
 
@@ -19,7 +30,7 @@ int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R
 // renormalization). `mark` (nullable) is called after the forward and after
 // the backward for per-phase profiling.
 void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                    const std::function<void()>* mark, int64_t R);
+                    const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr);
 // score_batch for ht models (res = v, res_u = u, scores). `ba` carries the
 // batch's plan (TransR groups rows by relation through it).
 void ht_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s, int64_t R);
@@ -37,13 +48,13 @@ bool transh_tiles_supported(int de, int dr, int64_t R);
 void configure_transh_tiles_kernels();
 int64_t transh_tiles_work_floats(int64_t rows, int64_t R);
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
-                              cudaStream_t s, const std::function<void()>* mark);
+                              cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks = nullptr);
 
 // TransR (transr.cu)
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R);
 void configure_transr_kernels();
 void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                        const std::function<void()>* mark, int64_t R);
+                        const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr);
 void transr_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                   int64_t R);
 void transr_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj, int num_sms,
@@ -67,14 +78,17 @@ void transr_tc_selftest(int mode, const float* A, const float* B, float* D, cuda
 void configure_transr_train_tc_kernels();
 int64_t transr_train_tc_mr_floats(int64_t R);
 int64_t transr_trace(int enable, unsigned long long* out, int64_t cap);  // debug: phase timestamps
+// sink != 0: write the summed gradient to proj / rel (zeroed sinks) and leave mr alone
 void launch_transr_train_apply(const uint32_t* tile_total, const uint32_t* seg_tiles, const uint32_t* tile_seg,
                                const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
                                float* proj, float* rel, const float* lr, const uint32_t* err, float* mr, int64_t R,
-                               cudaStream_t s);
+                               cudaStream_t s, int sink = 0);
+// always_prep: re-split M_r into the tf32 ring chunks before this batch (data parallel:
+// the dense step outside the kernel moved proj), otherwise only at batch 0
 void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,
                             const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
                             const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,
-                            float* mr, int64_t R, int num_sms, cudaStream_t s);
+                            float* mr, int64_t R, int num_sms, cudaStream_t s, bool always_prep = false);
 
 // link-prediction ranking (eval.cu)
 bool eval_supported(int kind);

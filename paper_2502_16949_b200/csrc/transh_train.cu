@@ -47,8 +47,9 @@ struct TArgs {
   int64_t mt;                 // tile capacity of `partial`
   float* partial;             // [tile][2][kD]
   uint32_t* rel_ticket;       // per relation segment: tiles finished (zeroed by the tile enumerator)
-  float* rel;                 // relation table (SGD)
+  float* rel;                 // relation table (SGD), or the relation gradient sink
   const float* lr;
+  float* nrm_sink;            // data parallel: normals gradient sink (null: SGD in place)
 };
 
 __device__ __forceinline__ float4 f4sub(float4 a, float4 b) {
@@ -316,11 +317,16 @@ __global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a)
         gA = __fadd_rn(gA, __ldcg(a.partial + (static_cast<size_t>(q) * 2) * kD + tid));
         gB = __fadd_rn(gB, __ldcg(a.partial + (static_cast<size_t>(q) * 2 + 1) * kD + tid));
       }
-      const float step = *a.lr;
       float* pr = a.rel + r * kD + tid;
-      float* pn = const_cast<float*>(f.normals) + r * kD + tid;
-      *pr = __fsub_rn(*pr, __fmul_rn(step, gA));
-      *pn = __fsub_rn(*pn, __fmul_rn(step, -gB));
+      if (a.nrm_sink) {  // data parallel: this rank's gradient rows (summed over ranks, then one dense step)
+        *pr = gA;
+        a.nrm_sink[r * kD + tid] = -gB;
+      } else {
+        const float step = *a.lr;
+        float* pn = const_cast<float*>(f.normals) + r * kD + tid;
+        *pr = __fsub_rn(*pr, __fmul_rn(step, gA));
+        *pn = __fsub_rn(*pn, __fmul_rn(step, -gB));
+      }
     }
     __syncthreads();  // rows / score / accs reuse by the next tile
   }
@@ -376,7 +382,7 @@ void configure_transh_tiles_kernels() {
 }
 
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
-                              cudaStream_t s, const std::function<void()>* mark) {
+                              cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks) {
   const int64_t mt = relation_max_tiles(2 * static_cast<int64_t>(fa.B), R);
   float* partial = work;
   uint32_t* ticket = reinterpret_cast<uint32_t*>(partial + mt * 2 * kD);
@@ -392,8 +398,9 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   a.mt = mt;
   a.partial = partial;
   a.rel_ticket = ticket;
-  a.rel = const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
+  a.rel = sinks ? sinks->rel : const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
   a.lr = ba.lr;
+  a.nrm_sink = sinks ? sinks->normals : nullptr;
   const size_t smem = sizeof(float) * kRows * kStride;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, static_cast<int64_t>(num_sms)));  // persistent
   if (l2) transh_tile_kernel<true><<<grid, kThreads, smem, s>>>(a);
@@ -403,7 +410,7 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   if (mark) (*mark)();
   BwdArgs eb = ba;
   eb.entity_only = 1;
-  launch_segment_backward(kPlainRows, true, eb, num_sms, s);
+  launch_segment_backward(kPlainRows, sinks == nullptr, eb, num_sms, s);  // sink: ba.X is the entity gradient
 }
 
 }  // namespace skg

@@ -544,23 +544,27 @@ void run_tc(int kind, int mode, const FwdArgs& fa, const BwdArgs& ba, const Work
 }  // namespace
 
 void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                        const std::function<void()>* mark, int64_t R) {
+                        const std::function<void()>* mark, int64_t R, const HtSinks* sinks) {
   const Work w = carve(work, 2 * static_cast<int64_t>(fa.B), fa.de, fa.dr, R);
+  // data parallel (sinks): entity rows accumulate into ba.X, proj / relation
+  // gradients land in the sinks, and the engine applies one dense step
+  float* proj_dst = sinks ? sinks->proj : const_cast<float*>(fa.proj);
+  float* rel_dst = sinks ? sinks->rel : const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
   if (transr_tc_supported(fa.de, fa.dr)) {
     transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, 1,
                                                     w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err);
     count_launch();
     SKG_LAUNCH_CHECK();
     launch_transr_train_tc(kind == kTransR_L2, fa, ba.ent_val, ba.seg_start, ba.seg_col, w.tile_seg, w.tile_p0,
-                           w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, w.mr_chunks, R, num_sms, s);
+                           w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, w.mr_chunks, R, num_sms, s,
+                           sinks != nullptr);
     if (mark) (*mark)();
     BwdArgs eb = ba;
     eb.entity_only = 1;
     eb.d = fa.de;
-    launch_segment_backward(kPlainRows, true, eb, num_sms, s);
+    launch_segment_backward(kPlainRows, sinks == nullptr, eb, num_sms, s);
     launch_transr_train_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
-                              const_cast<float*>(fa.proj), const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de),
-                              ba.lr, ba.err, w.mr_chunks, R, s);
+                              proj_dst, rel_dst, ba.lr, ba.err, w.mr_chunks, R, s, sinks != nullptr);
     if (mark) (*mark)();
     return;
   }
@@ -569,9 +573,8 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
   BwdArgs eb = ba;
   eb.entity_only = 1;
   eb.d = fa.de;
-  launch_segment_backward(kPlainRows, true, eb, num_sms, s);
-  apply(fa, ba, w, const_cast<float*>(fa.proj), const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de), true,
-        R, s);
+  launch_segment_backward(kPlainRows, sinks == nullptr, eb, num_sms, s);
+  apply(fa, ba, w, proj_dst, rel_dst, sinks == nullptr, R, s);
   if (mark) (*mark)();
 }
 

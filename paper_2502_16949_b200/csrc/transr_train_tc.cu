@@ -667,7 +667,7 @@ __global__ void transr_train_apply_kernel(const uint32_t* __restrict__ tile_tota
                                           int64_t N, int G, const float* __restrict__ dm_part,
                                           const float* __restrict__ dr_part, float* __restrict__ proj,
                                           float* __restrict__ rel, const float* __restrict__ lr,
-                                          const uint32_t* __restrict__ err, float* __restrict__ mr) {
+                                          const uint32_t* __restrict__ err, float* __restrict__ mr, int sink) {
   if (err[0] != 0) return;
   const uint32_t k = blockIdx.x;
   if (k >= tile_total[1]) return;
@@ -715,6 +715,10 @@ __global__ void transr_train_apply_kernel(const uint32_t* __restrict__ tile_tota
       g = __fadd_rn(g, pm ? __ldcg(dm_part + slot * kD * kD + i) : __ldcg(dr_part + slot * kD + (i - kD * kD)));
     }
     float* p = pm ? proj + r * kD * kD + i : rel + r * kD + (i - kD * kD);
+    if (sink) {  // data parallel: this rank's gradient, one dense step after the all-reduce
+      *p = g;
+      continue;
+    }
     const float nv = __fsub_rn(*p, __fmul_rn(step, g));
     *p = nv;
     if (pm) {  // element (row a = output dim, col b = entity dim) of M_r into both ring layouts
@@ -759,10 +763,10 @@ void configure_transr_train_tc_kernels() {
 void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,
                             const uint32_t* seg_col, const uint32_t* tile_seg, const uint32_t* tile_p0,
                             const uint32_t* tile_total, const uint32_t* seg_tiles, float* dm_part, float* dr_part,
-                            float* mr, int64_t R, int num_sms, cudaStream_t s) {
+                            float* mr, int64_t R, int num_sms, cudaStream_t s, bool always_prep) {
   // the split M_r chunks are refreshed by every batch's apply; the first batch
   // of an epoch re-splits from proj (the store may have been replaced)
-  if (fa.batch == 0) {
+  if (fa.batch == 0 || always_prep) {
     transr_train_prep_kernel<<<dim3(static_cast<unsigned>(R), 2 * kChunksPerGemm), 256, 0, s>>>(fa.proj, mr);
     count_launch();
   }
@@ -788,10 +792,10 @@ void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val,
 void launch_transr_train_apply(const uint32_t* tile_total, const uint32_t* seg_tiles, const uint32_t* tile_seg,
                                const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
                                float* proj, float* rel, const float* lr, const uint32_t* err, float* mr, int64_t R,
-                               cudaStream_t s) {
+                               cudaStream_t s, int sink) {
   transr_train_apply_kernel<<<dim3(static_cast<unsigned>(R), 16), 256, 0, s>>>(tile_total, seg_tiles, tile_seg, seg_col,
                                                                               N, G, dm_part, dr_part, proj, rel, lr,
-                                                                              err, mr);
+                                                                              err, mr, sink);
   count_launch();
   SKG_LAUNCH_CHECK();
 }

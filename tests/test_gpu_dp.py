@@ -34,15 +34,34 @@ def test_dp_world1_matches_oracle_bitwise(orc32, model, norm):
     eng.close()
 
 
-def test_dp_rejects_ht_models(orc32):
+@pytest.mark.parametrize("model,norm,d,dr", [("transh", "l2", 128, 128), ("transh", "l1", 16, 16),
+                                             ("transr", "l2", 128, 128), ("transr", "l1", 16, 12)])
+def test_dp_world1_ht_models(orc32, model, norm, d, dr):
+    """TransH / TransR under data parallel (replicated tables for C1-C4): each rank's
+    gradients go to the dense sink (relation, projection and normal sinks included), NCCL sums
+    them, one dense step (+ normal renormalization). Tolerance-only models: 1e-5."""
+    n, r = 1500, 12
+    h, rel, t = orc32.synthetic_train(n, r, 4000, 3)
+    st = orc32.init_store(model, n, r, d, dr, 3)
+    if model == "transr":
+        st.proj += np.random.default_rng(3).uniform(-0.1, 0.1, st.proj.shape).astype(np.float32)
     eng = Engine(0)
     eng.dp_init(Engine.nccl_unique_id(), 0, 1)
-    st = orc32.init_store("transh", 50, 3, 8, 8, 1)
-    cfg = ModelConfig.make("transh", 8, 8)
-    eng.store_upload(cfg, st.entity, st.relation, None, st.normals)
-    eng.set_triples([0, 1], [0, 1], [1, 2], 50, 3)
-    eng.negative_sample(1)
-    with pytest.raises(EngineError) as e:
-        eng.train_epoch(cfg, TrainConfig.make(batch_size=2), 0, 0.1)
-    assert e.value.kind == "ConfigError"
+    cfg = ModelConfig.make(model, d, dr, norm)
+    eng.store_upload(cfg, st.entity, st.relation, st.proj, st.normals)
+    eng.set_triples(h, rel, t, n, r)
+    kw = dict(lr=0.05, batch_size=512, seed=4)
+    rg = eng.fit(cfg, TrainConfig.make(epochs=2, **kw))
+    ro = orc32.fit(model, st, h, rel, t, orc32.train_config(epochs=2, **kw), norm=norm)
+    for a, b in zip(rg, ro):
+        assert abs(a.loss - b.loss) <= 1e-5 * max(1.0, abs(b.loss)), (a.loss, b.loss)
+    ge, gr, gp, gn = eng.store_download()
+
+    def rel_err(a, b):
+        return float(np.max(np.abs(a.astype(np.float64) - b) / np.maximum(1.0, np.abs(b))))
+    assert rel_err(ge, st.entity) <= 1e-5 and rel_err(gr, st.relation) <= 1e-5
+    if gp is not None:
+        assert rel_err(gp, st.proj) <= 1e-5
+    if gn is not None:
+        assert rel_err(gn, st.normals) <= 1e-5
     eng.close()
