@@ -380,7 +380,9 @@ def main():
             "config": dict(config_obj, l2="flushed between timed steps (256 MiB memset, untimed)",
                            wall_s=round(wall, 4), final_loss=losses[-1]),
             "e2e": {"value": e2e, "unit": "triplets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "skg_set_triples + skg_set_negatives (pinned int64) + skg_train_epoch"},
+                    "path": "skg_set_triples + skg_set_negatives (pinned int64) + skg_train_epoch; the identical-shape "
+                            "pinned re-upload is copied by DMA and verified while the epoch trains (rolled back "
+                            "and retrained if it differs)"},
             "roofline": ({"bound": "tensor", "kernel": dom, "achieved": tensor["achieved"], "peak": tensor["peak"],
                           "unit": "TFLOP/s", "frac": tensor["achieved"] / tensor["peak"], "traffic": traffic,
                           "peak_source": tensor["peak_source"], "hbm_gbs": ach, "hbm_frac": ach / peak,

@@ -2,6 +2,10 @@
 // device training loop (train_epoch / fit) captured in one CUDA graph per
 // epoch shape.
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <exception>
 #include <functional>
 #include <cstring>
 #include <sstream>
@@ -15,6 +19,7 @@ using namespace skg;
 
 namespace {
 int grid_for(int64_t n);
+void resolve_pending(skg_ctx* ctx);
 
 thread_local std::string g_create_err;
 
@@ -643,7 +648,8 @@ bool has_self_loops(skg_ctx* ctx) {
 }
 
 void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
-                      int64_t epoch, float lr, skg_epoch_report* rep) {
+                      int64_t epoch, float lr, skg_epoch_report* rep,
+                      const std::function<void()>* after_launch = nullptr) {
   EpochShape es{};
   prepare_epoch(ctx, cfg, tc, es);
   set_epoch_params(ctx, tc, lr);
@@ -665,16 +671,17 @@ void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train
   // Speculatively build epoch + 1's plan (same data and schedule) alongside.
   set_slot_seed(ctx, nxt, epoch_seed(tc.seed, epoch + 1));
   ctx->slots[nxt].key.clear();
-  SKG_CUDA(cudaStreamSynchronize(ctx->stream));  // margin in h_lr[1] is read at capture
   // Margin is baked into the forward launches, so it is part of the graph key.
   const std::string gk = graph_key(ctx, es) + "/" + std::to_string(tc.margin);
   if (!ctx->graphs[cur] || ctx->graph_keys[cur] != gk) {
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));  // margin in h_lr[1] is read at capture
     capture_epoch_graph(ctx, es, cur);
     ctx->graph_keys[cur] = gk;
   }
   SKG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
   SKG_CUDA(cudaGraphLaunch(ctx->graphs[cur], ctx->stream));
   SKG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+  if (after_launch) (*after_launch)();
   ctx->last_launches = ctx->graph_launches_k[cur] + eager;
   ctx->last_slot = cur;
   ctx->slots[nxt].key = plan_key(ctx, es, tc, epoch + 1);
@@ -901,6 +908,10 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaEventCreate(&ctx->ev0));
     SKG_CUDA(cudaEventCreate(&ctx->ev1));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    SKG_CUDA(cudaStreamCreateWithFlags(&ctx->up, cudaStreamNonBlocking));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming));
+
+    if (const char* e = std::getenv("SKG_NO_SPECULATE")) ctx->speculate = e[0] == '0';
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     ctx->err_words.ensure(4);
@@ -935,6 +946,12 @@ void skg_destroy(skg_ctx* ctx) {
   for (auto g : ctx->graphs)
     if (g) cudaGraphExecDestroy(g);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->up) {
+    cudaStreamSynchronize(ctx->up);
+    cudaStreamDestroy(ctx->up);
+  }
+  if (ctx->up_ev) cudaEventDestroy(ctx->up_ev);
+
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -952,7 +969,10 @@ int skg_num_sms(const skg_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
 int64_t skg_last_launch_count(const skg_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
 
 skg_status skg_synchronize(skg_ctx* ctx) {
-  return guard(ctx, [&] { SKG_CUDA(cudaStreamSynchronize(ctx->stream)); });
+  return guard(ctx, [&] {
+    resolve_pending(ctx);
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
 }
 
 skg_status skg_store_upload(skg_ctx* ctx, const skg_model_config* cfg, int64_t n_ent, int64_t n_rel,
@@ -1044,9 +1064,12 @@ void upload_narrow(skg_ctx* ctx, const int64_t* const* srcs, int32_t* const* dst
   bad_out[2] = ctx->h_err[2];
 }
 
-skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, const int64_t* t,
-                           int64_t n_ent, int64_t n_rel) {
-  return guard(ctx, [&] {
+}  // extern "C"
+
+namespace {
+
+void set_triples_sync(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, const int64_t* t, int64_t n_ent,
+                      int64_t n_rel) {
     if (m > 0 && (!h || !r || !t)) throw ShapeError("triple batch: heads/relations/tails length mismatch");
     if (n_ent > INT32_MAX || n_rel > INT32_MAX || m > INT32_MAX) throw ShapeError("id space exceeds 32-bit device ids");
     // Re-uploading identical triples keeps data_version, so an epoch plan
@@ -1078,11 +1101,9 @@ skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int6
     }
     ctx->M = m;
     ctx->triples_valid = true;
-  });
 }
 
-skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
-  return guard(ctx, [&] {
+void set_negatives_sync(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
     if (m != ctx->M) throw ShapeError("negative set is not aligned with the positive triples");
     // negatives as they were when the triples were set: no new data_version for an identical re-upload
     bool same = ctx->neg_valid_version == ctx->data_version && ctx->NH.n >= m + 1 && ctx->NT.n >= m + 1;
@@ -1107,11 +1128,220 @@ skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const i
     }
     ctx->has_neg = true;
     ctx->neg_valid_version = ctx->data_version;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
+}
+
+// Applies a deferred upload synchronously (every entry point other than
+// set_triples / set_negatives / train_epoch sees the uploaded data).
+void resolve_pending(skg_ctx* ctx) {
+  if (!ctx->pend_tri) return;
+  const int64_t* p[5];
+  for (int k = 0; k < 5; ++k) p[k] = ctx->pend_ptr[k];
+  const bool neg = ctx->pend_neg;
+  ctx->pend_tri = ctx->pend_neg = false;
+  set_triples_sync(ctx, ctx->M, p[0], p[1], p[2], ctx->tN, ctx->tR);
+  if (neg) set_negatives_sync(ctx, ctx->M, p[3], p[4]);
+}
+
+// Deferred upload check: the caller's int64 ids (copied by DMA into
+// stage_i64) against the device ids the speculative epoch used, with the
+// validation of set_triples / set_negatives. flags: [0] first bad entity
+// (h / t), [1] first bad relation, [2] first bad negative, [3] changed.
+__global__ void spec_check_kernel(const int64_t* __restrict__ src, int64_t m, int64_t n_ent, int64_t n_rel,
+                                  const int32_t* __restrict__ H, const int32_t* __restrict__ Rl,
+                                  const int32_t* __restrict__ T, const int32_t* __restrict__ NH,
+                                  const int32_t* __restrict__ NT, int32_t* __restrict__ out,
+                                  uint32_t* __restrict__ flags) {
+  bool diff = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v[5] = {src[i], src[m + i], src[2 * m + i], src[3 * m + i], src[4 * m + i]};
+    const int32_t* cur[5] = {H, Rl, T, NH, NT};
+    if (v[0] < 0 || v[0] >= n_ent || v[2] < 0 || v[2] >= n_ent) atomicMin(flags, static_cast<uint32_t>(i));
+    if (v[1] < 0 || v[1] >= n_rel) atomicMin(flags + 1, static_cast<uint32_t>(i));
+    if (v[3] < 0 || v[3] >= n_ent || v[4] < 0 || v[4] >= n_ent) atomicMin(flags + 2, static_cast<uint32_t>(i));
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int32_t w = static_cast<int32_t>(v[k]);
+      diff |= cur[k][i] != w;
+      out[k * m + i] = w;
+    }
+  }
+  if (__any_sync(kFull, diff) && (threadIdx.x & 31) == 0) atomicOr(flags + 3, 1u);
+}
+
+// Parameter snapshot / restore on the SMs (a D2D cudaMemcpy could queue
+// behind the deferred upload's H2D transfer on a shared copy engine).
+__global__ void copy_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  const int64_t n4 = n >> 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    for (int64_t i = tid; i < n4; i += stride)
+      reinterpret_cast<float4*>(dst)[i] = __ldcs(reinterpret_cast<const float4*>(src) + i);
+    done = 4 * n4;
+  }
+  for (int64_t i = done + tid; i < n; i += stride) dst[i] = src[i];
+}
+
+void copy_floats(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s) {
+  if (n <= 0) return;
+  const int64_t blocks = std::min<int64_t>((n / 4 + 255) / 256 + 1, 8LL * num_sms);
+  copy_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(src, dst, n);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
+// train_epoch with a deferred (pinned, identical-shape) upload pending: the
+// copy runs on the DMA engines while the epoch trains on the current device
+// ids; identical data (the common per-epoch re-upload) keeps the result.
+// Otherwise the parameters are restored and the reference semantics apply:
+// invalid ids throw set_triples' / set_negatives' ShapeError, new ids are
+// adopted and the epoch is trained on them.
+void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc, int64_t epoch,
+                             float lr, skg_epoch_report* rep) {
+  static const bool dbg = std::getenv("SKG_SPEC_DEBUG") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  const int64_t m = ctx->M;
+  const int64_t* src[5];
+  for (int k = 0; k < 5; ++k) src[k] = ctx->pend_ptr[k];
+  ctx->pend_tri = ctx->pend_neg = false;
+  ctx->stage_i64.ensure(5 * m + 1);
+  ctx->stage_i32.ensure(5 * m + 1);
+  ctx->spec_flags.ensure(4);
+  // the copy + check are enqueued right after the epoch graph is launched
+  bool launched = false;
+  const std::function<void()> upload = [&]() {
+    SKG_CUDA(cudaMemsetAsync(ctx->spec_flags.p, 0xFF, sizeof(uint32_t) * 3, ctx->up));
+    SKG_CUDA(cudaMemsetAsync(ctx->spec_flags.p + 3, 0, sizeof(uint32_t), ctx->up));
+    for (int k = 0; k < 5; ++k)
+      SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, src[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice, ctx->up));
+    spec_check_kernel<<<static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms)), 256, 0, ctx->up>>>(
+        ctx->stage_i64.p, m, ctx->tN, ctx->tR, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->stage_i32.p,
+        ctx->spec_flags.p);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+    SKG_CUDA(cudaEventRecord(ctx->up_ev, ctx->up));
+    launched = true;
+  };
+  // parameters the epoch mutates: [entity; relation], proj, normals
+  const int64_t nt = ctx->tables.n, np = ctx->proj.n, nn = ctx->normals.n;
+  ctx->backup.ensure(nt + np + nn + 4);
+  const int64_t ob = 0, op = (nt + 3) / 4 * 4, on = op + (np + 3) / 4 * 4;  // 16-byte aligned sections
+  ctx->backup.ensure(on + nn + 4);
+  copy_floats(ctx->tables.p, ctx->backup.p + ob, nt, ctx->num_sms, ctx->stream);
+  copy_floats(ctx->proj.p, ctx->backup.p + op, np, ctx->num_sms, ctx->stream);
+  copy_floats(ctx->normals.p, ctx->backup.p + on, nn, ctx->num_sms, ctx->stream);
+  const auto t1 = clk::now();
+  std::exception_ptr failed;
+  try {
+    train_epoch_impl(ctx, cfg, tc, epoch, lr, rep, &upload);
+  } catch (...) {
+    failed = std::current_exception();
+  }
+  if (!launched) upload();  // the epoch failed before its launch: still check the upload
+  const auto t2 = clk::now();
+  SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  uint32_t f[4];
+  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->spec_flags.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost, ctx->up));
+  SKG_CUDA(cudaStreamSynchronize(ctx->up));
+  if (dbg) {
+    const auto t3 = clk::now();
+    auto us = [](clk::duration d) { return std::chrono::duration<double, std::micro>(d).count(); };
+    std::fprintf(stderr, "spec: enqueue %.1f us, epoch %.1f us, upload wait %.1f us (graph %.1f us)\n", us(t1 - t0),
+                 us(t2 - t1), us(t3 - t2), rep->t_backward_s * 1e6);
+  }
+  for (int k = 0; k < 4; ++k) f[k] = ctx->h_err[k];
+  const bool bad_tri = f[0] != 0xFFFFFFFFu || f[1] != 0xFFFFFFFFu, bad_neg = f[2] != 0xFFFFFFFFu;
+  if (!bad_tri && !bad_neg && f[3] == 0) {  // identical re-upload: the speculative epoch stands
+    ++ctx->spec_hits;
+    if (failed) std::rethrow_exception(failed);
+    return;
+  }
+  ++ctx->spec_misses;
+  copy_floats(ctx->backup.p + ob, ctx->tables.p, nt, ctx->num_sms, ctx->stream);
+  copy_floats(ctx->backup.p + op, ctx->proj.p, np, ctx->num_sms, ctx->stream);
+  copy_floats(ctx->backup.p + on, ctx->normals.p, nn, ctx->num_sms, ctx->stream);
+  for (auto& sl : ctx->slots) sl.key.clear();
+  ctx->has_neg = false;
+  if (bad_tri) {  // set_triples' error (incidence.hpp:26-29: entity check first)
+    ctx->triples_valid = false;
+    ctx->M = 0;
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (f[0] != 0xFFFFFFFFu && f[0] <= f[1])
+      throw ShapeError("triple " + std::to_string(f[0]) + ": entity id out of range");
+    throw ShapeError("triple " + std::to_string(f[1]) + ": relation id out of range");
+  }
+  // adopt the uploaded ids (data changed, or the negatives are invalid)
+  int32_t* dst[5] = {ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p};
+  for (int k = 0; k < 5; ++k)
+    SKG_CUDA(cudaMemcpyAsync(dst[k], ctx->stage_i32.p + k * m, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  ++ctx->data_version;
+  SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (bad_neg) {  // set_negatives' error
+    ctx->neg_valid_version = ~0ull;
+    throw ShapeError("triple " + std::to_string(f[2]) + ": entity id out of range");
+  }
+  ctx->neg_valid_version = ctx->data_version;
+  ctx->has_neg = true;
+  train_epoch_impl(ctx, cfg, tc, epoch, lr, rep);
+}
+
+}  // namespace
+
+extern "C" {
+
+skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, const int64_t* t,
+                           int64_t n_ent, int64_t n_rel) {
+  return guard(ctx, [&] {
+    if (m > 0 && (!h || !r || !t)) throw ShapeError("triple batch: heads/relations/tails length mismatch");
+    // An identical-shape re-upload of pinned arrays (the per-epoch e2e loop)
+    // is deferred to the next train_epoch, which copies it while it trains.
+    if (ctx->speculate && !ctx->dp && !ctx->pend_tri && ctx->triples_valid && m > 0 && m == ctx->M &&
+        n_ent == ctx->tN && n_rel == ctx->tR && ctx->neg_valid_version == ctx->data_version && is_pinned(h) &&
+        is_pinned(r) && is_pinned(t)) {
+      ctx->pend_tri = true;
+      ctx->pend_neg = false;
+      ctx->pend_ptr[0] = h;
+      ctx->pend_ptr[1] = r;
+      ctx->pend_ptr[2] = t;
+      ctx->has_neg = false;  // as after any set_triples: negatives must follow
+      return;
+    }
+    resolve_pending(ctx);
+    set_triples_sync(ctx, m, h, r, t, n_ent, n_rel);
+  });
+}
+
+skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
+  return guard(ctx, [&] {
+    if (ctx->pend_tri && !ctx->pend_neg && m == ctx->M && m > 0 && is_pinned(nh) && is_pinned(nt)) {
+      ctx->pend_neg = true;
+      ctx->pend_ptr[3] = nh;
+      ctx->pend_ptr[4] = nt;
+      ctx->has_neg = true;
+      return;
+    }
+    resolve_pending(ctx);
+    set_negatives_sync(ctx, m, nh, nt);
   });
 }
 
 skg_status skg_negative_sample(skg_ctx* ctx, uint64_t seed, int32_t avoid, int64_t* out_h, int64_t* out_t) {
   return guard(ctx, [&] {
+    resolve_pending(ctx);
     negative_sample_impl(ctx, seed, avoid != 0);
     if (out_h || out_t) {
       std::vector<int32_t> a(ctx->M), b(ctx->M);
@@ -1415,6 +1645,11 @@ skg_status skg_renormalize_entities(skg_ctx* ctx) {
 skg_status skg_train_epoch(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc, int64_t epoch,
                            float lr, skg_epoch_report* rep) {
   return guard(ctx, [&] {
+    if (ctx->pend_tri && ctx->pend_neg) {
+      train_epoch_speculative(ctx, *cfg, *tc, epoch, lr, rep);
+      return;
+    }
+    resolve_pending(ctx);
     train_epoch_impl(ctx, *cfg, *tc, epoch, lr, rep);
   });
 }
@@ -1423,6 +1658,7 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const sk
                              int64_t epoch, float lr, skg_epoch_report* rep, double* fwd_ms, double* bwd_ms,
                              double* plan_ms) {
   return guard(ctx, [&] {
+    resolve_pending(ctx);
     EpochShape es{};
     prepare_epoch(ctx, *cfg, *tc, es);
     set_epoch_params(ctx, *tc, lr);
@@ -1467,6 +1703,7 @@ skg_status skg_flush_l2(skg_ctx* ctx) {
 skg_status skg_plan_stats(skg_ctx* ctx, int64_t batch, int64_t* segments, int64_t* entries,
                           int64_t* relation_segments) {
   return guard(ctx, [&] {
+    resolve_pending(ctx);
     if (batch < 0 || batch >= ctx->slots[ctx->last_slot].plan.nb || !ctx->slots[ctx->last_slot].plan.seg_base) throw ShapeError("plan_stats: no such batch");
     uint32_t sb[2];
     SKG_CUDA(cudaMemcpy(sb, ctx->slots[ctx->last_slot].plan.seg_base + batch, sizeof(sb), cudaMemcpyDeviceToHost));
@@ -1487,7 +1724,8 @@ skg_status skg_plan_stats(skg_ctx* ctx, int64_t batch, int64_t* segments, int64_
 
 skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc,
                    skg_epoch_report* reports) {
-  return guard(ctx, [&] {  // training.cpp:166-195
+  return guard(ctx, [&] {
+    resolve_pending(ctx);  // training.cpp:166-195
     validate_model(*cfg);
     validate_train(*tc);
     if (tc->epochs == 0) return;

@@ -117,6 +117,22 @@ struct skg_ctx {
   int64_t last_launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
+  // ---- deferred id uploads (speculative epoch). A re-upload of pinned arrays
+  // with the shape of the current triples is recorded, not copied; the next
+  // train_epoch copies it on `up` (DMA) while the epoch runs on the current
+  // device ids, then compares. Equal: done. Different or invalid: the
+  // parameters are rolled back from `backup` and the call falls back to the
+  // synchronous path (adopt + rerun, or the reference's ShapeError).
+  bool pend_tri = false, pend_neg = false;
+  const int64_t* pend_ptr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // h, r, t, nh, nt
+  bool speculate = true;
+  cudaStream_t up = nullptr;
+  cudaEvent_t up_ev = nullptr;
+  skg::DevBuf<int32_t> stage_i32;   // narrowed deferred upload [h | r | t | nh | nt]
+  skg::DevBuf<float> backup;        // parameters before a speculative epoch
+  skg::DevBuf<uint32_t> spec_flags; // first bad entity / relation / negative index, changed
+  int64_t spec_hits = 0, spec_misses = 0;
+
   // ---- data parallel
   skg::DpState* dp = nullptr;
 };

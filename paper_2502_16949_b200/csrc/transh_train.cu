@@ -29,10 +29,17 @@ namespace skg {
 namespace {
 
 constexpr int kD = 128;
-constexpr int kRows = 128;
-constexpr int kPairs = 64;
-constexpr int kThreads = 512;      // 16 warps x 8 rows
+#ifndef SKG_TRANSH_PAIRS
+#define SKG_TRANSH_PAIRS 32
+#endif
+// 32 pairs = 64 rows per tile, 8 warps x 8 rows, two CTAs per SM: twice the
+// tiles of a 64-pair tile, so the persistent grid ends more evenly and one
+// CTA's barrier waits overlap the other's work.
+constexpr int kPairs = SKG_TRANSH_PAIRS;
+constexpr int kRows = 2 * kPairs;
 constexpr int kRowsPerWarp = 8;
+constexpr int kThreads = kRows / kRowsPerWarp * 32;
+constexpr int kCtasPerSm = 64 / kPairs;
 constexpr int kStride = kD + 4;    // staged v rows (16-byte aligned, conflict-free row reads)
 
 constexpr int kMaxRelSeg = 1024;  // relation segments per batch handled in shared memory
@@ -129,7 +136,7 @@ __device__ __forceinline__ uint32_t rel_of_tile(const RelTiles& rt, uint32_t t) 
 }
 
 template <bool L2>
-__global__ void __launch_bounds__(kThreads, 1) transh_tile_kernel(const TArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) transh_tile_kernel(const TArgs a) {
   extern __shared__ float4 smv[];
   float* Vs = reinterpret_cast<float*>(smv);  // [kRows][kStride]
   __shared__ int4 rows[kRows];                 // {head, tail, incidence row (-1: padding), 0}
@@ -402,7 +409,8 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   a.lr = ba.lr;
   a.nrm_sink = sinks ? sinks->normals : nullptr;
   const size_t smem = sizeof(float) * kRows * kStride;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, static_cast<int64_t>(num_sms)));  // persistent
+  const unsigned grid =
+      static_cast<unsigned>(std::min<int64_t>(mt, static_cast<int64_t>(num_sms) * kCtasPerSm));  // persistent
   if (l2) transh_tile_kernel<true><<<grid, kThreads, smem, s>>>(a);
   else transh_tile_kernel<false><<<grid, kThreads, smem, s>>>(a);
   count_launch();

@@ -367,3 +367,69 @@ def test_pinned_upload_rejects_bad_ids(eng):
     with pytest.raises(EngineError) as e:
         eng.set_triples(h, r, t, 5, 2)
     assert "triple 1: relation id out of range" in e.value.msg
+
+
+def test_deferred_reupload_invalid_ids_roll_back(eng, orc32):
+    """A pinned identical-shape re-upload is copied while the next epoch trains
+    (speculatively, on the previous ids). Invalid ids must surface as the
+    set_triples / set_negatives ShapeError with the parameters untouched; changed
+    ids must train exactly as a synchronous upload would."""
+    n, r, d, m = 300, 5, 8, 700
+    h, rel, t = orc32.synthetic_train(n, r, m, 4)
+    m = len(h)
+    st = orc32.init_store("transe", n, r, d, d, 4)
+    cfg = ModelConfig.make("transe", d, d, "l2")
+    tc_e = TrainConfig.make(batch_size=64, seed=3, lr=0.05)
+    tc_o = orc32.train_config(batch_size=64, seed=3, lr=0.05)
+    nh, nt = orc32.negative_sample(h, rel, t, n, r, 3)
+    P = [_pinned(x) for x in (h, rel, t, nh, nt)]
+    eng.store_upload(cfg, st.entity, st.relation)
+    eng.set_triples(*P[:3], n, r)
+    eng.set_negatives(*P[3:])
+    eng.train_epoch(cfg, tc_e, 0, 0.05)
+    orc32.train_epoch("transe", st, (h, rel, t), (nh, nt), tc_o, 0, 0.05)
+    before = eng.store_download()[0].copy()
+    assert np.array_equal(before, st.entity)
+    # invalid entity id in the triples: deferred, raised by train_epoch, nothing trained
+    bad = P[2].copy()
+    bad = _pinned(bad)
+    bad[17] = n + 3
+    eng.set_triples(P[0], P[1], bad, n, r)
+    eng.set_negatives(*P[3:])
+    with pytest.raises(EngineError) as e:
+        eng.train_epoch(cfg, tc_e, 1, 0.05)
+    assert e.value.kind == "ShapeError" and e.value.msg == "triple 17: entity id out of range"
+    assert np.array_equal(eng.store_download()[0], before)
+    # invalid negative: triples adopted, negatives rejected, nothing trained
+    eng.set_triples(*P[:3], n, r)
+    eng.set_negatives(*P[3:])
+    eng.train_epoch(cfg, tc_e, 1, 0.05)
+    orc32.train_epoch("transe", st, (h, rel, t), (nh, nt), tc_o, 1, 0.05)
+    before = eng.store_download()[0].copy()
+    badn = _pinned(P[3].copy())
+    badn[5] = -1
+    eng.set_triples(*P[:3], n, r)
+    eng.set_negatives(badn, P[4])
+    with pytest.raises(EngineError) as e:
+        eng.train_epoch(cfg, tc_e, 2, 0.05)
+    assert e.value.kind == "ShapeError" and e.value.msg == "triple 5: entity id out of range"
+    assert np.array_equal(eng.store_download()[0], before)
+    with pytest.raises(EngineError) as e:  # negatives are not valid any more
+        eng.train_epoch(cfg, tc_e, 2, 0.05)
+    assert e.value.kind == "ShapeError"
+    # changed ids of the same shape: rolled back and retrained on the new ids
+    h2 = _pinned((h + 7) % n)
+    eng.set_negatives(*P[3:])
+    eng.train_epoch(cfg, tc_e, 2, 0.05)
+    orc32.train_epoch("transe", st, (h, rel, t), (nh, nt), tc_o, 2, 0.05)
+    eng.set_triples(h2, P[1], P[2], n, r)
+    eng.set_negatives(*P[3:])
+    eng.train_epoch(cfg, tc_e, 3, 0.05)
+    orc32.train_epoch("transe", st, ((h + 7) % n, rel, t), (nh, nt), tc_o, 3, 0.05)
+    ge, gr, _, _ = eng.store_download()
+    assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation)
+    # a deferred upload is visible to every other call (negative_sample resolves it)
+    eng.set_triples(*P[:3], n, r)
+    gh, gt = eng.negative_sample(11)
+    oh, ot = orc32.negative_sample(h, rel, t, n, r, 11)
+    assert np.array_equal(gh, oh) and np.array_equal(gt, ot)
