@@ -125,7 +125,15 @@ skg_status skg_renormalize_entities(skg_ctx* ctx);
 
 /* ---- triples and negatives ------------------------------------------------ */
 /* Training triples (TripleBatch, incidence.hpp:14-33) with their id space;
- * validated like TripleBatch::validate (ShapeError on a bad id). */
+ * validated like TripleBatch::validate (ShapeError on a bad id).
+ * Deferred re-upload: when the context already holds triples + negatives of
+ * the same shape and the new arrays are page-locked (cudaHostAlloc /
+ * torch pin_memory), skg_set_triples + skg_set_negatives only record the
+ * pointers; the next skg_train_epoch copies and validates them while it
+ * trains (an invalid id then fails that call with the same ShapeError, the
+ * parameters untouched). Such pinned arrays must stay valid and unchanged
+ * until the next engine call on the context, as with cudaMemcpyAsync.
+ * Pageable arrays are always copied and validated inside the call. */
 skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* heads, const int64_t* relations,
                            const int64_t* tails, int64_t num_entities, int64_t num_relations);
 /* Corrupted tails/heads aligned with the training triples (NegativeSet,
