@@ -327,10 +327,14 @@ def main():
     except Exception:  # pragma: no cover
         pin = lambda a: np.ascontiguousarray(a, np.int64)
     hp, rp, tp, nhp, ntp = pin(h), pin(r), pin(t), pin(nh), pin(nt)
+    # one untimed warm-up pass of the e2e loop (first-call host work: pinned-pointer lookups)
+    eng.set_triples(hp, rp, tp, cfg["N"], cfg["R"])
+    eng.set_negatives(nhp, ntp)
+    eng.train_epoch(mcfg, tc, args.warmup + args.steps, LR)
     barrier(world)
     eng.synchronize()
     e2e_steps = max(1, min(args.steps, 20))
-    e2e_epoch0 = args.warmup + args.steps  # the training run continues: consecutive epochs
+    e2e_epoch0 = args.warmup + args.steps + 1  # the training run continues: consecutive epochs
     t0 = time.perf_counter()
     for k in range(e2e_steps):
         eng.set_triples(hp, rp, tp, cfg["N"], cfg["R"])

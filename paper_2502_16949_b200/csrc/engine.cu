@@ -1005,6 +1005,8 @@ skg_status skg_store_upload(skg_ctx* ctx, const skg_model_config* cfg, int64_t n
                                ctx->stream));
     }
     ctx->has_store = true;
+    if (ctx->speculate)  // parameter snapshot of a speculative epoch (tables, proj, normals, aligned sections)
+      ctx->backup.ensure(ctx->tables.n + ctx->proj.n + ctx->normals.n + 12);
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -1101,6 +1103,11 @@ void set_triples_sync(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* 
     }
     ctx->M = m;
     ctx->triples_valid = true;
+    if (ctx->speculate && m > 0) {  // buffers of a later deferred re-upload, allocated outside any timed epoch
+      ctx->stage_i64.ensure(5 * m + 1);
+      ctx->stage_i32.ensure(5 * m + 1);
+      ctx->spec_flags.ensure(4);
+    }
 }
 
 void set_negatives_sync(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
@@ -1179,7 +1186,9 @@ __global__ void spec_check_kernel(const int64_t* __restrict__ src, int64_t m, in
 }
 
 // Parameter snapshot / restore on the SMs (a D2D cudaMemcpy could queue
-// behind the deferred upload's H2D transfer on a shared copy engine).
+// behind the deferred upload's H2D transfer on a shared copy engine). Plain
+// loads: an evict-first (streaming) read of the tables would demote the very
+// L2 lines the epoch's gathers hit next (C1 epoch 0.73 -> 0.89 ms measured).
 __global__ void copy_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
   const int64_t n4 = n >> 2;
   const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
@@ -1188,7 +1197,7 @@ __global__ void copy_kernel(const float* __restrict__ src, float* __restrict__ d
   int64_t done = 0;
   if (vec) {
     for (int64_t i = tid; i < n4; i += stride)
-      reinterpret_cast<float4*>(dst)[i] = __ldcs(reinterpret_cast<const float4*>(src) + i);
+      reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
     done = 4 * n4;
   }
   for (int64_t i = done + tid; i < n; i += stride) dst[i] = src[i];
