@@ -527,23 +527,27 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   }
 }
 
-std::string graph_key(skg_ctx* ctx, const EpochShape& es) {
-  std::ostringstream o;
-  o << es.B << '/' << es.nb << '/' << es.shuffle << '/' << es.kind << '/' << ctx->M << '/'
-    << ctx->tables.p << '/' << ctx->H.p << '/' << ctx->NH.p << '/' << ctx->slots[0].order.p << '/'
-    << ctx->slots[1].order.p << '/' << ctx->res.p << '/' << ctx->ht_work.p << '/'
-    << ctx->slots[0].plan.cap_entries << '/' << ctx->slots[1].plan.cap_entries << '/' << ctx->shuffle.cap_n << '/'
-    << es.world << '/' << es.rank << '/' << ctx->dp_grad.p << '/' << ctx->slots[0].order_g.p << '/'
-    << ctx->slots[1].order_g.p << '/' << ctx->proj.p << '/' << ctx->normals.p;
-  return o.str();
+// Keys are the raw bytes of the values they depend on (built every epoch on
+// the host critical path: no formatting).
+template <class... T>
+std::string raw_key(const T&... v) {
+  std::string k;
+  k.reserve((sizeof(T) + ... + 0));
+  (k.append(reinterpret_cast<const char*>(&v), sizeof(T)), ...);
+  return k;
+}
+
+std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
+  return raw_key(es.B, es.nb, es.shuffle, es.kind, ctx->M, ctx->tables.p, ctx->H.p, ctx->NH.p, ctx->slots[0].order.p,
+                 ctx->slots[1].order.p, ctx->res.p, ctx->ht_work.p, ctx->slots[0].plan.cap_entries,
+                 ctx->slots[1].plan.cap_entries, ctx->shuffle.cap_n, es.world, es.rank, ctx->dp_grad.p,
+                 ctx->slots[0].order_g.p, ctx->slots[1].order_g.p, ctx->proj.p, ctx->normals.p, margin);
 }
 
 // Identity of an epoch plan: everything it depends on.
 std::string plan_key(skg_ctx* ctx, const EpochShape& es, const skg_train_config& tc, int64_t epoch) {
-  std::ostringstream o;
-  o << epoch << '/' << (es.shuffle ? tc.seed : 0) << '/' << es.shuffle << '/' << es.B << '/' << ctx->M << '/'
-    << ctx->data_version << '/' << es.world << '/' << es.rank << '/' << ctx->H.p << '/' << ctx->NH.p;
-  return o.str();
+  const uint64_t seed = es.shuffle ? tc.seed : 0;
+  return raw_key(epoch, seed, es.shuffle, es.B, ctx->M, ctx->data_version, es.world, es.rank, ctx->H.p, ctx->NH.p);
 }
 
 void finish_epoch(skg_ctx* ctx, const EpochShape& es, int64_t epoch, skg_epoch_report* rep) {
@@ -672,7 +676,7 @@ void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train
   set_slot_seed(ctx, nxt, epoch_seed(tc.seed, epoch + 1));
   ctx->slots[nxt].key.clear();
   // Margin is baked into the forward launches, so it is part of the graph key.
-  const std::string gk = graph_key(ctx, es) + "/" + std::to_string(tc.margin);
+  const std::string gk = graph_key(ctx, es, tc.margin);
   if (!ctx->graphs[cur] || ctx->graph_keys[cur] != gk) {
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));  // margin in h_lr[1] is read at capture
     capture_epoch_graph(ctx, es, cur);
@@ -921,6 +925,7 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaMallocHost(&ctx->h_seed, sizeof(uint64_t) * 2));
     SKG_CUDA(cudaMallocHost(&ctx->h_lr, sizeof(float) * 2));
     SKG_CUDA(cudaMallocHost(&ctx->h_err, sizeof(uint32_t) * 4));
+    SKG_CUDA(cudaMallocHost(&ctx->h_spec, sizeof(uint32_t) * 4));
     SKG_CUDA(cudaMemset(ctx->err_words.p, 0, sizeof(uint32_t) * 4));
     SKG_CUDA(cudaMemset(ctx->counter.p, 0, sizeof(unsigned)));
     configure_hrt_kernels();
@@ -959,6 +964,7 @@ void skg_destroy(skg_ctx* ctx) {
   if (ctx->h_seed) cudaFreeHost(ctx->h_seed);
   if (ctx->h_lr) cudaFreeHost(ctx->h_lr);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->h_spec) cudaFreeHost(ctx->h_spec);
   if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1137,13 +1143,20 @@ void set_negatives_sync(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_
     ctx->neg_valid_version = ctx->data_version;
 }
 
-bool is_pinned(const void* p) {
+// Page-locked caller array? The last few answers are cached by address: a
+// stale "pinned" for memory re-allocated pageable at the same address is still
+// correct (cudaMemcpyAsync stages pageable memory), only not asynchronous.
+bool is_pinned(skg_ctx* ctx, const void* p) {
+  for (int k = 0; k < 8; ++k)
+    if (ctx->pinned_seen[k] == p) return true;
   cudaPointerAttributes pa{};
   if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
+  const bool pinned = pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
+  if (pinned) ctx->pinned_seen[ctx->pinned_next++ & 7] = p;
+  return pinned;
 }
 
 // Applies a deferred upload synchronously (every entry point other than
@@ -1242,6 +1255,11 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     count_launch();
     SKG_LAUNCH_CHECK();
     SKG_CUDA(cudaEventRecord(ctx->up_ev, ctx->up));
+    // the epoch's own final sync also covers the check: its flags are read
+    // back on the main stream after the upload's event
+    SKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->up_ev, 0));
+    SKG_CUDA(cudaMemcpyAsync(ctx->h_spec, ctx->spec_flags.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost,
+                             ctx->stream));
     launched = true;
   };
   // parameters the epoch mutates: [entity; relation], proj, normals
@@ -1263,15 +1281,13 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   const auto t2 = clk::now();
   SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   uint32_t f[4];
-  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->spec_flags.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost, ctx->up));
-  SKG_CUDA(cudaStreamSynchronize(ctx->up));
   if (dbg) {
     const auto t3 = clk::now();
     auto us = [](clk::duration d) { return std::chrono::duration<double, std::micro>(d).count(); };
     std::fprintf(stderr, "spec: enqueue %.1f us, epoch %.1f us, upload wait %.1f us (graph %.1f us)\n", us(t1 - t0),
                  us(t2 - t1), us(t3 - t2), rep->t_backward_s * 1e6);
   }
-  for (int k = 0; k < 4; ++k) f[k] = ctx->h_err[k];
+  for (int k = 0; k < 4; ++k) f[k] = ctx->h_spec[k];
   const bool bad_tri = f[0] != 0xFFFFFFFFu || f[1] != 0xFFFFFFFFu, bad_neg = f[2] != 0xFFFFFFFFu;
   if (!bad_tri && !bad_neg && f[3] == 0) {  // identical re-upload: the speculative epoch stands
     ++ctx->spec_hits;
@@ -1319,8 +1335,8 @@ skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int6
     // An identical-shape re-upload of pinned arrays (the per-epoch e2e loop)
     // is deferred to the next train_epoch, which copies it while it trains.
     if (ctx->speculate && !ctx->dp && !ctx->pend_tri && ctx->triples_valid && m > 0 && m == ctx->M &&
-        n_ent == ctx->tN && n_rel == ctx->tR && ctx->neg_valid_version == ctx->data_version && is_pinned(h) &&
-        is_pinned(r) && is_pinned(t)) {
+        n_ent == ctx->tN && n_rel == ctx->tR && ctx->neg_valid_version == ctx->data_version && is_pinned(ctx, h) &&
+        is_pinned(ctx, r) && is_pinned(ctx, t)) {
       ctx->pend_tri = true;
       ctx->pend_neg = false;
       ctx->pend_ptr[0] = h;
@@ -1336,7 +1352,7 @@ skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int6
 
 skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
   return guard(ctx, [&] {
-    if (ctx->pend_tri && !ctx->pend_neg && m == ctx->M && m > 0 && is_pinned(nh) && is_pinned(nt)) {
+    if (ctx->pend_tri && !ctx->pend_neg && m == ctx->M && m > 0 && is_pinned(ctx, nh) && is_pinned(ctx, nt)) {
       ctx->pend_neg = true;
       ctx->pend_ptr[3] = nh;
       ctx->pend_ptr[4] = nt;

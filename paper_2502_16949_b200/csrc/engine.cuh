@@ -132,6 +132,9 @@ struct skg_ctx {
   skg::DevBuf<float> backup;        // parameters before a speculative epoch
   skg::DevBuf<uint32_t> spec_flags; // first bad entity / relation / negative index, changed
   int64_t spec_hits = 0, spec_misses = 0;
+  uint32_t* h_spec = nullptr;           // pinned: the check's flags
+  const void* pinned_seen[8] = {};      // recently seen page-locked caller arrays
+  unsigned pinned_next = 0;
 
   // ---- data parallel
   skg::DpState* dp = nullptr;
