@@ -40,6 +40,7 @@ constexpr int kRows = 2 * kPairs;
 constexpr int kRowsPerWarp = 8;
 constexpr int kThreads = kRows / kRowsPerWarp * 32;
 constexpr int kCtasPerSm = 64 / kPairs;
+static_assert(kThreads >= 2 * 128, "the relation reduction uses one thread per (column, vector)");
 constexpr int kStride = kD + 4;    // staged v rows (16-byte aligned, conflict-free row reads)
 
 constexpr int kMaxRelSeg = 1024;  // relation segments per batch handled in shared memory
@@ -303,36 +304,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transh_tile_kernel(const
       rel_last = atomicAdd(a.rel_ticket + k, 1u) == hi - lo - 1;
     }
     __syncthreads();
-    if (rel_last && tid < kD) {
+    if (rel_last && tid < 2 * kD) {
+      // thread (c, v): column c of the relation gradient (v = 0) or of the
+      // normal's (v = 1); 16 tiles' loads in flight, added in tile order
       __threadfence();
-      float gA = 0.f, gB = 0.f;
+      const int c = tid & (kD - 1), v = tid / kD;
+      const float* src = a.partial + static_cast<size_t>(v) * kD + c;
+      float g = 0.f;
       uint32_t q = lo;
-      for (; q + 8 <= hi; q += 8) {  // eight tiles' loads in flight, added in tile order
-        float va[8], vb[8];
+      for (; q + 16 <= hi; q += 16) {
+        float x[16];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          va[e] = __ldcg(a.partial + (static_cast<size_t>(q + e) * 2) * kD + tid);
-          vb[e] = __ldcg(a.partial + (static_cast<size_t>(q + e) * 2 + 1) * kD + tid);
-        }
+        for (int e = 0; e < 16; ++e) x[e] = __ldcg(src + static_cast<size_t>(q + e) * 2 * kD);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          gA = __fadd_rn(gA, va[e]);
-          gB = __fadd_rn(gB, vb[e]);
-        }
+        for (int e = 0; e < 16; ++e) g = __fadd_rn(g, x[e]);
       }
-      for (; q < hi; ++q) {
-        gA = __fadd_rn(gA, __ldcg(a.partial + (static_cast<size_t>(q) * 2) * kD + tid));
-        gB = __fadd_rn(gB, __ldcg(a.partial + (static_cast<size_t>(q) * 2 + 1) * kD + tid));
-      }
-      float* pr = a.rel + r * kD + tid;
+      for (; q < hi; ++q) g = __fadd_rn(g, __ldcg(src + static_cast<size_t>(q) * 2 * kD));
       if (a.nrm_sink) {  // data parallel: this rank's gradient rows (summed over ranks, then one dense step)
-        *pr = gA;
-        a.nrm_sink[r * kD + tid] = -gB;
+        if (v == 0) a.rel[r * kD + c] = g;
+        else a.nrm_sink[r * kD + c] = -g;
       } else {
         const float step = *a.lr;
-        float* pn = const_cast<float*>(f.normals) + r * kD + tid;
-        *pr = __fsub_rn(*pr, __fmul_rn(step, gA));
-        *pn = __fsub_rn(*pn, __fmul_rn(step, -gB));
+        float* p = v == 0 ? a.rel + r * kD + c : const_cast<float*>(f.normals) + r * kD + c;
+        *p = __fsub_rn(*p, __fmul_rn(step, v == 0 ? g : -g));
       }
     }
     __syncthreads();  // rows / score / accs reuse by the next tile
