@@ -171,8 +171,11 @@ __device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int 
 #ifndef SKG_FWD_P128
 #define SKG_FWD_P128 4  // pairs gathered together when d <= 128 (5 row loads each)
 #endif
-template <int KIND, bool TRAIN, int VEC>
-__global__ void __launch_bounds__(kThreads, SKG_FWD_MINB) hrt_forward_kernel(const FwdArgs a) {
+#ifndef SKG_FWD_P256
+#define SKG_FWD_P256 2  // ... when d <= 256
+#endif
+template <int KIND, bool TRAIN, int VEC, int MINB = SKG_FWD_MINB>
+__global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdArgs a) {
   extern __shared__ float4 smem4[];
   __shared__ float warp_loss[kWarps];
   if (a.err[0] != 0) return;  // sticky error: nothing runs after the failing batch
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, SKG_FWD_MINB) hrt_forward_kernel(con
       // the relation row, so P pairs need 5P row loads, all in flight at once
       const int d4 = d >> 2;
       if (d4 <= 32) gather_pairs<KIND, SKG_FWD_P128>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
-      else if (d4 <= 64) gather_pairs<KIND, 2>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
+      else if (d4 <= 64) gather_pairs<KIND, SKG_FWD_P256>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
       else gather_pairs<KIND, 1>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
     } else if (VEC == 4) {
       const float4* X4 = reinterpret_cast<const float4*>(a.X);
@@ -522,7 +525,10 @@ void launch_fwd_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
   int grid = (ntiles + wpb - 1) / wpb;
   if (grid > num_sms * per_sm) grid = num_sms * per_sm;
   if (grid < 1) grid = 1;
-  hrt_forward_kernel<KIND, TRAIN, VEC><<<grid, wpb * 32, smem, s>>>(a);
+  // d > 128: three blocks' worth of registers per SM (more rows in flight for
+  // the DRAM-resident wide tables; C5 +3 %), d <= 128: two (C1 -1.5 % with three)
+  if (a.de > 128) hrt_forward_kernel<KIND, TRAIN, VEC, 3><<<grid, wpb * 32, smem, s>>>(a);
+  else hrt_forward_kernel<KIND, TRAIN, VEC><<<grid, wpb * 32, smem, s>>>(a);
   count_launch();
   SKG_LAUNCH_CHECK();
 }
@@ -570,6 +576,8 @@ void launch_bwd_k(bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s) {
 template <int KIND, bool TRAIN, int VEC>
 void configure_one() {
   SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC, 3>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 }
 template <int KIND>
