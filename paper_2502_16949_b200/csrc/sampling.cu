@@ -94,6 +94,85 @@ __global__ void __launch_bounds__(kMtThreads) mt_kernel(const uint64_t* __restri
   }
 }
 
+// Chunked stream: block j generates words [j L, min((j + 1) L, n)) of the
+// same stream, starting from the seeded state advanced j L words. The jump
+// evaluates sum_i p_i A^i s0 for p = x^(jL) mod f (mt_jump.cpp) by Horner's
+// rule 64 coefficients at a time: acc = A^64(acc) ^ sum_k p_(64w+k) A^k s0,
+// where A^64 is 64 independent word steps (each new word reads only words of
+// the old window) and A^k s0 is s0's own word sequence from word k. L is a
+// multiple of 312, so every chunk starts on a whole state and continues with
+// the register twist of mt_kernel.
+constexpr int kJumpThreads = 320;
+constexpr int kJumpWords = 312;  // coefficient words per jump polynomial (19937 bits)
+
+__global__ void __launch_bounds__(kJumpThreads) mt_chunk_kernel(const uint64_t* __restrict__ seed_ptr,
+                                                                uint64_t seed_val,
+                                                                const uint64_t* __restrict__ polys, int64_t L,
+                                                                uint64_t* __restrict__ out, int64_t n) {
+  __shared__ uint64_t s0[kMtN + 64];  // seeded state and the next 64 words of its sequence
+  __shared__ uint64_t acc[kMtN];
+  __shared__ uint64_t sa[2][kMtM + 1], sb[2][kMtM + 1];
+  const int tid = threadIdx.x;
+  const int64_t j = blockIdx.x;
+  if (tid == 0) mt_seed(seed_ptr ? *seed_ptr : seed_val, s0);
+  __syncthreads();
+  if (tid < 64) s0[kMtN + tid] = s0[kMtM + tid] ^ mt_mix(s0[tid], s0[tid + 1]);
+  for (int i = tid; i < kMtN; i += blockDim.x) acc[i] = j == 0 ? s0[i] : 0ull;
+  __syncthreads();
+  int h = 0;
+  if (j > 0) {
+    const uint64_t* p = polys + (j - 1) * kJumpWords;
+    for (int wi = kJumpWords - 1; wi >= 0; --wi) {
+      const uint64_t bits = __ldg(p + wi);
+      uint64_t nw = 0;
+      if (tid < 64) {
+        const int k = h + tid;
+        nw = acc[(k + kMtM) % kMtN] ^ mt_mix(acc[k % kMtN], acc[(k + 1) % kMtN]);
+      }
+      __syncthreads();
+      if (tid < 64) acc[(h + tid) % kMtN] = nw;
+      h = (h + 64) % kMtN;
+      __syncthreads();
+      if (bits && tid < kMtN) {
+        uint64_t x = 0;
+        for (uint64_t m = bits; m; m &= m - 1) x ^= s0[__ffsll(static_cast<long long>(m)) - 1 + tid];
+        acc[(h + tid) % kMtN] ^= x;
+      }
+      __syncthreads();
+    }
+  }
+  // generate the chunk from the jumped window (thread i < 156 keeps words i and 156 + i)
+  const bool on = tid < kMtM;
+  uint64_t a = on ? acc[(h + tid) % kMtN] : 0ull, b = on ? acc[(h + kMtM + tid) % kMtN] : 0ull;
+  const int64_t w0 = j * L, w1 = min(n, w0 + L);
+  const int64_t nstates = (w1 - w0 + kMtN - 1) / kMtN;
+  int cur = 0;
+  for (int64_t st = 0; st < nstates; ++st) {
+    if (on) {
+      sa[cur][tid] = a;
+      sb[cur][tid] = b;
+    }
+    __syncthreads();
+    if (on) {
+      const uint64_t a1 = tid + 1 < kMtM ? sa[cur][tid + 1] : sb[cur][0];
+      const uint64_t na = b ^ mt_mix(a, a1);
+      uint64_t nb;
+      if (tid + 1 < kMtM) {
+        nb = na ^ mt_mix(b, sb[cur][tid + 1]);
+      } else {
+        const uint64_t na0 = sb[cur][0] ^ mt_mix(sa[cur][0], sa[cur][1]);
+        nb = na ^ mt_mix(b, na0);
+      }
+      a = na;
+      b = nb;
+      const int64_t base = w0 + st * kMtN;
+      if (base + tid < w1) out[base + tid] = mt_temper(a);
+      if (base + kMtM + tid < w1) out[base + kMtM + tid] = mt_temper(b);
+    }
+    cur ^= 1;
+  }
+}
+
 // Sequential single-thread MT19937-64 (fallback paths only).
 struct SeqMt {
   uint64_t x[kMtN];
@@ -417,6 +496,48 @@ int grid_for(int64_t n, int threads = 256) {
 
 }  // namespace
 
+// Chunk plan of a raw stream of n words: P chunks of L words (L a multiple of
+// 312) with their jump polynomials on device; P = 1 below ~320 K words, where
+// the single-block generator is faster than a jump.
+void MtJump::prepare(int64_t n) {
+  if (n == n_prepared) return;
+  int64_t P = n / (static_cast<int64_t>(kMtN) * 1024);
+  P = P < 2 ? 1 : (P > 32 ? 32 : P);
+  int64_t L = (n + P - 1) / P;
+  L = (L + kMtN - 1) / kMtN * kMtN;
+  P = (n + L - 1) / L;
+  chunks = static_cast<int>(P);
+  chunk_words = L;
+  if (P > 1) {
+    const std::vector<uint64_t>& h = mt_jump_polys(L, static_cast<int>(P));
+    if (static_cast<int64_t>(h.size()) > cap) {
+      if (polys) cudaFree(polys);
+      SKG_CUDA(cudaMalloc(&polys, sizeof(uint64_t) * h.size()));
+      cap = static_cast<int64_t>(h.size());
+    }
+    SKG_CUDA(cudaMemcpy(polys, h.data(), sizeof(uint64_t) * h.size(), cudaMemcpyHostToDevice));
+  }
+  n_prepared = n;
+}
+
+void MtJump::release() {
+  if (polys) cudaFree(polys);
+  polys = nullptr;
+  cap = 0;
+  n_prepared = -1;
+}
+
+void MtJump::generate(const uint64_t* seed_ptr, uint64_t seed_val, uint64_t* out, int64_t n, cudaStream_t s) const {
+  if (n != n_prepared) throw CudaError("mt stream: jump plan not prepared for this length");
+  if (chunks <= 1) {
+    mt_kernel<<<1, kMtThreads, 0, s>>>(seed_ptr, seed_val, out, n);
+  } else {
+    mt_chunk_kernel<<<chunks, kJumpThreads, 0, s>>>(seed_ptr, seed_val, polys, chunk_words, out, n);
+  }
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
 void mt19937_64_generate(uint64_t seed, uint64_t* out, int64_t n, cudaStream_t s) {
   mt_kernel<<<1, kMtThreads, 0, s>>>(nullptr, seed, out, n);
   count_launch();
@@ -424,10 +545,15 @@ void mt19937_64_generate(uint64_t seed, uint64_t* out, int64_t n, cudaStream_t s
 }
 
 void ShuffleWork::reserve(int64_t n) {
-  if (n <= cap_n) return;
+  // the jump plan follows the current length (prepare_epoch runs this outside any capture)
+  if (n <= cap_n) {
+    jump.prepare(num_calls(n) + kShiftWindow + 64);
+    return;
+  }
   release();
   const int64_t nraw = num_calls(n) + kShiftWindow + 64;
   SKG_CUDA(cudaMalloc(&raw, sizeof(uint64_t) * nraw));
+  jump.prepare(nraw);  // uploads the jump polynomials
   SKG_CUDA(cudaMalloc(&cand, sizeof(uint64_t) * kCandCap));
   SKG_CUDA(cudaMalloc(&ncand, sizeof(uint32_t) * 2));
   SKG_CUDA(cudaMalloc(&shifts, sizeof(uint64_t) * kCandCap));
@@ -447,6 +573,7 @@ void ShuffleWork::release() {
   ncand = nshift = jkey = jval = jkey_alt = jval_alt = jpos = gstart = nextsame = nullptr;
   cap_n = 0;
   sort.release();
+  jump.release();
 }
 
 void device_iota(int32_t* order, int64_t n, cudaStream_t s) {
@@ -466,13 +593,15 @@ void device_shuffle(const uint64_t* d_seed_eff, int64_t n, int32_t* order, Shuff
   const int64_t C = num_calls(n);
   const int64_t nraw = C + kShiftWindow + 64;
   shuffle_reset_kernel<<<1, 1, 0, s>>>(w.ncand, w.nshift);
-  mt_kernel<<<1, kMtThreads, 0, s>>>(d_seed_eff, 0, w.raw, nraw);
+  count_launch();
+  w.jump.prepare(nraw);  // no-op after reserve (a smaller n than reserved re-plans, never inside a capture)
+  w.jump.generate(d_seed_eff, 0, w.raw, nraw, s);
   shuffle_candidates_kernel<<<grid_for(C), 256, 0, s>>>(w.raw, nraw, n, w.cand, w.ncand);
   shuffle_resolve_kernel<<<1, 1024, 0, s>>>(w.cand, w.ncand, w.shifts, w.nshift);
   shuffle_map_kernel<<<grid_for(C), 256, 0, s>>>(w.raw, n, w.shifts, w.nshift, w.jpos);
   shuffle_fallback_kernel<<<1, 1, 0, s>>>(d_seed_eff, n, order, w.ncand);
   shuffle_keys_kernel<<<grid_for(n), 256, 0, s>>>(w.jpos, n, w.jkey, w.jval);
-  count_launch(7);
+  count_launch(5);
   SKG_LAUNCH_CHECK();
   const int kb = bits_for(static_cast<uint64_t>(n - 1));
   const bool alt = radix_sort_pairs(w.jkey, w.jval, w.jkey_alt, w.jval_alt, n - 1, kb, w.sort, s);
@@ -499,6 +628,7 @@ void NegWork::release() {
   raw = nullptr;
   first_reject = nullptr;
   cap = 0;
+  jump.release();
 }
 
 bool device_negative_sample(const int32_t* h, const int32_t* t, int64_t m, int64_t n_ent,
@@ -509,12 +639,13 @@ bool device_negative_sample(const int32_t* h, const int32_t* t, int64_t m, int64
   const int64_t nraw = 2 * m + 4096;
   SKG_CUDA(cudaMemsetAsync(w.first_reject, 0xFF, sizeof(uint32_t), s));
   SKG_CUDA(cudaMemsetAsync(w.first_reject + 1, 0, sizeof(uint32_t), s));
-  mt_kernel<<<1, kMtThreads, 0, s>>>(nullptr, seed, w.raw, nraw);
+  w.jump.prepare(nraw);  // eager path (never captured)
+  w.jump.generate(nullptr, seed, w.raw, nraw, s);
   neg_map_kernel<<<grid_for(m), 256, 0, s>>>(w.raw, h, t, m, n_ent, avoid ? 1 : 0, out_h, out_t,
                                              w.first_reject);
   neg_fixup_kernel<<<1, 1, 0, s>>>(w.raw, nraw, h, t, m, n_ent, avoid ? 1 : 0, out_h, out_t,
                                    w.first_reject);
-  count_launch(3);
+  count_launch(2);
   SKG_LAUNCH_CHECK();
   uint32_t flags[2];
   SKG_CUDA(cudaMemcpyAsync(flags, w.first_reject, sizeof(flags), cudaMemcpyDeviceToHost, s));
