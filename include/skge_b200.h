@@ -229,6 +229,10 @@ skg_status skg_plan_stats(skg_ctx* ctx, int64_t batch, int64_t* segments, int64_
 /* Tensor-core self test: D = A(m,k) . B(n,k) over 128^3 through the operand
  * views the TransR kernel uses (0: A,B K-major; 1: B MN-major; 2: both MN). */
 skg_status skg_debug_tc_gemm(skg_ctx* ctx, int32_t mode, const float* A, const float* B, float* D);
+/* Host-only check of the MT19937-64 jump-ahead (sampling streams): the state
+ * J words ahead of std::mt19937_64(seed), from the jump polynomial, continues
+ * the reference stream exactly. Returns 1 on success. */
+int32_t skg_debug_mt_jump_selftest(uint64_t seed, int64_t jump);
 
 /* ---- data-parallel replicas (one process per GPU) ------------------------ */
 /* Joins an NCCL communicator (unique id produced by skg_nccl_unique_id on

@@ -1867,6 +1867,14 @@ extern "C" skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cf
   });
 }
 
+extern "C" int32_t skg_debug_mt_jump_selftest(uint64_t seed, int64_t jump) {
+  try {
+    return skg::mt_jump_selftest(seed, jump) ? 1 : 0;
+  } catch (...) {
+    return 0;
+  }
+}
+
 extern "C" int64_t skg_debug_transr_trace(int32_t enable, unsigned long long* out, int64_t cap) {
   try {
     return transr_trace(enable, out, cap);

@@ -63,3 +63,15 @@ def test_torch_imports_after_engine_library():
             "print(torch.cuda.nccl.version() if hasattr(torch.cuda, 'nccl') else 'no-nccl')")
     out = subprocess.run([sys.executable, "-c", code, lib_path()], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
+
+
+def test_mt_jump_ahead_continues_the_reference_stream():
+    """Host part of the chunked MT19937-64 generator (mt_jump.cpp): states advanced by
+    x^J mod f (Berlekamp-Massey characteristic polynomial) continue std::mt19937_64."""
+    import ctypes as C
+    from paper_2502_16949_b200.engine import load_library
+    L = load_library()
+    L.skg_debug_mt_jump_selftest.restype = C.c_int32
+    L.skg_debug_mt_jump_selftest.argtypes = [C.c_uint64, C.c_int64]
+    for seed, jump in [(5489, 1), (1, 312), (7, 312 * 1000 + 5), (0x9E3779B97F4A7C15, 8_000_000)]:
+        assert L.skg_debug_mt_jump_selftest(seed, jump) == 1, (seed, jump)
