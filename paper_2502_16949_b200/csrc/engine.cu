@@ -1111,7 +1111,6 @@ void set_triples_sync(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* 
     ctx->triples_valid = true;
     if (ctx->speculate && m > 0) {  // buffers of a later deferred re-upload, allocated outside any timed epoch
       ctx->stage_i64.ensure(5 * m + 1);
-      ctx->stage_i32.ensure(5 * m + 1);
       ctx->spec_flags.ensure(4);
     }
 }
@@ -1178,24 +1177,33 @@ void resolve_pending(skg_ctx* ctx) {
 __global__ void spec_check_kernel(const int64_t* __restrict__ src, int64_t m, int64_t n_ent, int64_t n_rel,
                                   const int32_t* __restrict__ H, const int32_t* __restrict__ Rl,
                                   const int32_t* __restrict__ T, const int32_t* __restrict__ NH,
-                                  const int32_t* __restrict__ NT, int32_t* __restrict__ out,
-                                  uint32_t* __restrict__ flags) {
+                                  const int32_t* __restrict__ NT, uint32_t* __restrict__ flags) {
+  // Read-only and evict-first on the staged copy: the epoch running alongside
+  // keeps its L2-resident tables (the staged ids are dead after this pass;
+  // they are re-narrowed from HBM only when they differ).
   bool diff = false;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t v[5] = {src[i], src[m + i], src[2 * m + i], src[3 * m + i], src[4 * m + i]};
+    const int64_t v[5] = {__ldcs(src + i), __ldcs(src + m + i), __ldcs(src + 2 * m + i), __ldcs(src + 3 * m + i),
+                          __ldcs(src + 4 * m + i)};
     const int32_t* cur[5] = {H, Rl, T, NH, NT};
     if (v[0] < 0 || v[0] >= n_ent || v[2] < 0 || v[2] >= n_ent) atomicMin(flags, static_cast<uint32_t>(i));
     if (v[1] < 0 || v[1] >= n_rel) atomicMin(flags + 1, static_cast<uint32_t>(i));
     if (v[3] < 0 || v[3] >= n_ent || v[4] < 0 || v[4] >= n_ent) atomicMin(flags + 2, static_cast<uint32_t>(i));
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const int32_t w = static_cast<int32_t>(v[k]);
-      diff |= cur[k][i] != w;
-      out[k * m + i] = w;
-    }
+    for (int k = 0; k < 5; ++k) diff |= __ldg(cur[k] + i) != static_cast<int32_t>(v[k]);
   }
   if (__any_sync(kFull, diff) && (threadIdx.x & 31) == 0) atomicOr(flags + 3, 1u);
+}
+
+__global__ void narrow_staged_kernel(const int64_t* __restrict__ src, int64_t m, int32_t* __restrict__ H,
+                                     int32_t* __restrict__ Rl, int32_t* __restrict__ T, int32_t* __restrict__ NH,
+                                     int32_t* __restrict__ NT) {
+  int32_t* dst[5] = {H, Rl, T, NH, NT};
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) dst[k][i] = static_cast<int32_t>(src[k * m + i]);
 }
 
 // Parameter snapshot / restore on the SMs (a D2D cudaMemcpy could queue
@@ -1240,7 +1248,6 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   for (int k = 0; k < 5; ++k) src[k] = ctx->pend_ptr[k];
   ctx->pend_tri = ctx->pend_neg = false;
   ctx->stage_i64.ensure(5 * m + 1);
-  ctx->stage_i32.ensure(5 * m + 1);
   ctx->spec_flags.ensure(4);
   // the copy + check are enqueued right after the epoch graph is launched
   bool launched = false;
@@ -1250,8 +1257,7 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     for (int k = 0; k < 5; ++k)
       SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, src[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice, ctx->up));
     spec_check_kernel<<<static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms)), 256, 0, ctx->up>>>(
-        ctx->stage_i64.p, m, ctx->tN, ctx->tR, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->stage_i32.p,
-        ctx->spec_flags.p);
+        ctx->stage_i64.p, m, ctx->tN, ctx->tR, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->spec_flags.p);
     count_launch();
     SKG_LAUNCH_CHECK();
     SKG_CUDA(cudaEventRecord(ctx->up_ev, ctx->up));
@@ -1309,10 +1315,10 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     throw ShapeError("triple " + std::to_string(f[1]) + ": relation id out of range");
   }
   // adopt the uploaded ids (data changed, or the negatives are invalid)
-  int32_t* dst[5] = {ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p};
-  for (int k = 0; k < 5; ++k)
-    SKG_CUDA(cudaMemcpyAsync(dst[k], ctx->stage_i32.p + k * m, sizeof(int32_t) * m, cudaMemcpyDeviceToDevice,
-                             ctx->stream));
+  narrow_staged_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->stage_i64.p, m, ctx->H.p, ctx->Rl.p, ctx->T.p,
+                                                            ctx->NH.p, ctx->NT.p);
+  count_launch();
+  SKG_LAUNCH_CHECK();
   ++ctx->data_version;
   SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   if (bad_neg) {  // set_negatives' error

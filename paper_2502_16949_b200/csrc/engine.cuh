@@ -128,7 +128,6 @@ struct skg_ctx {
   bool speculate = true;
   cudaStream_t up = nullptr;
   cudaEvent_t up_ev = nullptr;
-  skg::DevBuf<int32_t> stage_i32;   // narrowed deferred upload [h | r | t | nh | nt]
   skg::DevBuf<float> backup;        // parameters before a speculative epoch
   skg::DevBuf<uint32_t> spec_flags; // first bad entity / relation / negative index, changed
   int64_t spec_hits = 0, spec_misses = 0;
