@@ -10,6 +10,10 @@
 #include "common.cuh"
 #include "primitives.cuh"
 
+#ifndef SKG_PLAN_STREAMING
+#define SKG_PLAN_STREAMING 1  // sort passes stream through L2 (evict-first): the concurrent minibatch chain keeps its tables and residual rows
+#endif
+
 namespace skg {
 
 namespace {
@@ -148,7 +152,11 @@ __device__ __forceinline__ void load_subtile(const uint32_t* __restrict__ src, i
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     const int64_t e = base + c * 32 + lane;
+#if SKG_PLAN_STREAMING
+    r[c] = e < n ? __ldcs(src + e) : 0u;
+#else
     r[c] = e < n ? __ldg(src + e) : 0u;
+#endif
   }
 }
 
@@ -280,8 +288,13 @@ __global__ void __launch_bounds__(kSortWarps * 32, 2)
     const uint32_t key = sk[j];
     const uint32_t d = (key >> shift) & mask;
     const uint32_t pos = gbase[d] + (static_cast<uint32_t>(j) - lstart[d]);
+#if SKG_PLAN_STREAMING
+    __stcs(kout + pos, key);
+    __stcs(vout + pos, sv[j]);
+#else
     kout[pos] = key;
     vout[pos] = sv[j];
+#endif
   }
 }
 
