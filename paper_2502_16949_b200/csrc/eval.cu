@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kEvalThreads) rank_tiled_kernel(EvalArgs a, in
   float* Rr = F + kQB * S;                       // [kQB][S] relation rows
   float* Cc = Rr + kQB * S;                      // [kCB][S] candidate rows
   __shared__ int64_t qfix[kQB], qtruth[kQB], qh[kQB], qr[kQB], qt[kQB];
-  __shared__ float qte[kQB];
+  __shared__ float qte[kQB], qself[kQB];
   const int tid = threadIdx.x;
   const int64_t q0 = static_cast<int64_t>(blockIdx.x) * kQB;
   const int nq = static_cast<int>(min(static_cast<int64_t>(kQB), a.q - q0));
@@ -187,6 +187,9 @@ __global__ void __launch_bounds__(kEvalThreads) rank_tiled_kernel(EvalArgs a, in
     qfix[tid] = SIDE == 0 ? qh[tid] : qt[tid];
     qtruth[tid] = SIDE == 0 ? qt[tid] : qh[tid];
     qte[tid] = a.te[2 * qi + SIDE];
+    // the candidate equal to the fixed entity is the cancelled self-loop row
+    // (energy of r alone); every other candidate skips that select in the loop
+    qself[tid] = row_energy<KIND>(a.X + qfix[tid] * d, a.X + qfix[tid] * d, a.Rt + qr[tid] * d, d, true);
   }
   __syncthreads();
   const int d4 = d >> 2;
@@ -209,9 +212,7 @@ __global__ void __launch_bounds__(kEvalThreads) rank_tiled_kernel(EvalArgs a, in
     }
     __syncthreads();
     if (qi >= nq) continue;
-    bool sl[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) sl[k] = cb + cg + 16 * k == qfix[qi];
+    constexpr bool sl[4] = {false, false, false, false};
     float e[4];
     if (is_torus(KIND)) {
       float s[4] = {0.f, 0.f, 0.f, 0.f};
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(kEvalThreads) rank_tiled_kernel(EvalArgs a, in
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t c = cb + cg + 16 * k;
+      if (c == qfix[qi]) e[k] = qself[qi];
       if (cg + 16 * k >= nc || c == qtruth[qi] || !(e[k] < qte[qi])) continue;
       if (a.table && filter_contains(a.table, a.mask, SIDE == 0 ? triple_key(qh[qi], qr[qi], c, a.N, a.R)
                                                                 : triple_key(c, qr[qi], qt[qi], a.N, a.R)))
