@@ -121,6 +121,31 @@ __device__ float ref_reduce(const float* v, int n, bool& bad) {
   return s;
 }
 
+// TransE rows (d >= 8, d % 4 == 0) reduced by the whole warp: lane 2 r + h
+// runs accumulators 2h and 2h + 1 of row r over float2 steps, then
+// (s0 + s1) + (s2 + s3) — ref_reduce's association with every lane busy
+// (lanes 0-15 / 16-31 read 16 distinct bank pairs per half-warp request).
+// Row j's sum lands on lane j < 16.
+template <int KIND>
+__device__ __forceinline__ float warp_reduce16(const float* rows, int S, int d, int lane, bool& bad) {
+  const int r = lane >> 1, hb = lane & 1;
+  const float* v = rows + r * S + 2 * hb;
+  float sa = 0.f, sb = 0.f;
+  bool nf = false;
+#pragma unroll 8
+  for (int j = 0; j < d; j += 4) {
+    const float2 x = *reinterpret_cast<const float2*>(v + j);
+    nf |= !(fabsf(x.x) <= 3.402823466e38f) | !(fabsf(x.y) <= 3.402823466e38f);
+    sa = __fadd_rn(sa, term_of(KIND, x.x));
+    sb = __fadd_rn(sb, term_of(KIND, x.y));
+  }
+  const float pair = __fadd_rn(sa, sb);                // s0 + s1 (h = 0) or s2 + s3 (h = 1)
+  const float tot = __fadd_rn(pair, __shfl_down_sync(kFull, pair, 1));  // on h == 0 lanes
+  const unsigned nfm = __ballot_sync(kFull, nf);
+  bad = ((nfm >> (2 * (lane & 15))) & 3u) != 0u;
+  return __shfl_sync(kFull, tot, 2 * (lane & 15));
+}
+
 // Per-row gradient scale: D_row = dir(residual, scale) in the backward.
 template <int KIND>
 __device__ __forceinline__ float row_scale(float up, float s) {
@@ -293,7 +318,15 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
     // ---- exact-order reduction: lane j reduces row j
     float s = 0.f, score = 0.f;
     bool bad = false;
-    if (lane < 16 && valid) {
+    if ((KIND == kTransE_L2 || KIND == kTransE_L1) && VEC == 4 && d >= 8) {
+      bool b = false;
+      const float sw = warp_reduce16<KIND>(rows, S, d, lane, b);
+      if (lane < 16 && valid) {
+        s = sw;
+        bad = b;
+        score = (KIND == kTransE_L2) ? __fsqrt_rn(s) : s;  // norms.hpp:57-62
+      }
+    } else if (lane < 16 && valid) {
       s = ref_reduce<KIND, VEC>(rows + lane * S, d, bad);
       score = (KIND == kTransE_L2) ? __fsqrt_rn(s) : s;  // norms.hpp:57-62, 107-115
     }

@@ -56,6 +56,33 @@ __device__ float ref_norm_sum(const float* v, int n, bool& bad) {
   return s;
 }
 
+// squared_sum / abs_sum of 8 rows of n (>= 8, multiple of 4) floats with the
+// whole warp: lane 4q + k runs accumulator k of row q (elements k, k + 4, ...
+// in order), then (s0 + s1) + (s2 + s3) — the reference association
+// (norms.hpp:19-55) with every lane busy. Returns row q's sum on lane q < 8;
+// `bad` = a non-finite element in row q (lanes q < 8). Rows are `stride`
+// floats apart; stride = 4 (mod 32) keeps the 32 reads of a step on 32 banks.
+template <bool SQUARE>
+__device__ __forceinline__ float warp_norm8(const float* rows, int stride, int n, int lane, bool& bad) {
+  const int q = lane >> 2, k = lane & 3;
+  const float* v = rows + q * stride + k;
+  float s = 0.f;
+  bool nf = false;
+#pragma unroll 8
+  for (int j = 0; j < n; j += 4) {
+    const float x = v[j];
+    nf |= nonfinite(x);
+    s = __fadd_rn(s, norm_term<SQUARE>(x));
+  }
+  const unsigned full = 0xffffffffu;
+  const float s1 = __shfl_down_sync(full, s, 1), s2 = __shfl_down_sync(full, s, 2), s3 = __shfl_down_sync(full, s, 3);
+  const float tot = __fadd_rn(__fadd_rn(s, s1), __fadd_rn(s2, s3));  // valid on lanes k == 0
+  const unsigned nfm = __ballot_sync(full, nf);
+  const float out = __shfl_sync(full, tot, (lane & 7) * 4);
+  bad = ((nfm >> ((lane & 7) * 4)) & 0xFu) != 0u;
+  return out;
+}
+
 // Deterministic warp sum: tree down to lane 0, then broadcast (every lane gets
 // the identical value, unlike an xor butterfly).
 __device__ __forceinline__ float warp_sum_bcast(float v) {

@@ -233,9 +233,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transh_tile_kernel(const
     bool bad = false;
     const int mj = m0 + (lane & 7);
     const int row2 = rows[mj].z;
-    if (lane < kRowsPerWarp) {
-      ssum = ref_norm_sum<L2, 4>(Vs + mj * kStride, kD, bad);
-      score[mj] = L2 ? __fsqrt_rn(ssum) : ssum;
+    {  // whole warp, reference association (warp_norm8); row j lands on lane j
+      bool b = false;
+      const float sj = warp_norm8<L2>(Vs + m0 * kStride, kStride, kD, lane, b);
+      if (lane < kRowsPerWarp) {
+        ssum = sj;
+        bad = b;
+        score[mj] = L2 ? __fsqrt_rn(ssum) : ssum;
+      }
     }
     __syncthreads();
     if (tid < kPairs && tn < T) stage2(pos_next, pr_next, ng_next);
