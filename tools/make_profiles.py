@@ -31,8 +31,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--src", default=os.path.join(ROOT, "gpurun_out", "prof"))
     ap.add_argument("--round", default="r01")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles"))
     a = ap.parse_args()
-    out = os.path.join(ROOT, "profiles")
+    out = a.out
+    os.makedirs(out, exist_ok=True)
+    if out != os.path.join(ROOT, "profiles"):  # previous traffic figures for directions not captured
+        for f in glob.glob(os.path.join(ROOT, "profiles", "traffic_*.json")):
+            dst = os.path.join(out, os.path.basename(f))
+            if not os.path.exists(dst):
+                shutil.copy(f, dst)
     for f in sorted(glob.glob(os.path.join(a.src, "bench_*.json"))):
         cfg = os.path.basename(f)[6:-5]
         lines = [x for x in open(f).read().splitlines() if x.strip().startswith("{")]

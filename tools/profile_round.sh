@@ -25,5 +25,7 @@ cap C5_bwd C5 segment_backward 20
 cap C5_scatter C5 radix_scatter 8
 cap M1_fwd M1 mult_forward 20
 cap M1_bwd M1 segment_backward 20
-python tools/make_profiles.py --src gpurun_out/prof > gpurun_out/prof/make_profiles.log 2>&1
+# summaries on the box (the .ncu-rep files stay there: gpurun_out merges are capped at 64 MiB)
+python tools/make_profiles.py --src gpurun_out/prof --out gpurun_out/profiles_new > gpurun_out/make_profiles.log 2>&1
+rm -f gpurun_out/prof/*.ncu-rep
 echo done
