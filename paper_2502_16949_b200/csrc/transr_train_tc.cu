@@ -58,6 +58,9 @@ constexpr uint32_t kChLBO = 8 * 16, kChSBO = 32 * 16;
 constexpr int kChunksPerGemm = kD / kChunkK;
 constexpr int64_t kMrFloatsPerRel = 2LL * kChunksPerGemm * 2 * kChunkFloats;
 constexpr int kRing = 3;
+#ifndef SKG_APPLY_Y
+#define SKG_APPLY_Y 32  // relation-parallel blocks x 32 slices of the 16 K-element proj block
+#endif
 
 // GEMM3 staging slot: 8 rows (K) of DZ^T and U^T, hi and lo; arrays [128][8]
 // with unit (i, k4) = (i & 7) + (i >> 3) * 18 + k4 * 9 (padded: the producers'
@@ -793,7 +796,7 @@ void launch_transr_train_apply(const uint32_t* tile_total, const uint32_t* seg_t
                                const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
                                float* proj, float* rel, const float* lr, const uint32_t* err, float* mr, int64_t R,
                                cudaStream_t s, int sink) {
-  transr_train_apply_kernel<<<dim3(static_cast<unsigned>(R), 16), 256, 0, s>>>(tile_total, seg_tiles, tile_seg, seg_col,
+  transr_train_apply_kernel<<<dim3(static_cast<unsigned>(R), SKG_APPLY_Y), 256, 0, s>>>(tile_total, seg_tiles, tile_seg, seg_col,
                                                                               N, G, dm_part, dr_part, proj, rel, lr,
                                                                               err, mr, sink);
   count_launch();
