@@ -22,6 +22,8 @@
 // (no atomics) and applies p -= lr * g to the touched row in the same kernel.
 // Rows never touched keep p - lr*0 == p, so touching only the segment rows is
 // bitwise the reference's dense step.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "plan.cuh"
 #include "kernels.cuh"
@@ -146,6 +148,29 @@ __device__ __forceinline__ float warp_reduce16(const float* rows, int S, int d, 
   return __shfl_sync(kFull, tot, 2 * (lane & 15));
 }
 
+// Eight TransE rows per warp (4-pair tiles, d > 128): lane 4 r + k runs
+// accumulator k of row r, then (s0 + s1) + (s2 + s3); row j lands on lane j.
+// S = 4 (mod 32) keeps each step's 32 scalar reads on 32 banks.
+template <int KIND>
+__device__ __forceinline__ float warp_reduce8(const float* rows, int S, int d, int lane, bool& bad) {
+  const int r = lane >> 2, k = lane & 3;
+  const float* v = rows + r * S + k;
+  float sacc = 0.f;
+  bool nf = false;
+#pragma unroll 8
+  for (int j = 0; j < d; j += 4) {
+    const float x = v[j];
+    nf |= !(fabsf(x) <= 3.402823466e38f);
+    sacc = __fadd_rn(sacc, term_of(KIND, x));
+  }
+  const float s1 = __shfl_down_sync(kFull, sacc, 1), s2 = __shfl_down_sync(kFull, sacc, 2),
+              s3 = __shfl_down_sync(kFull, sacc, 3);
+  const float tot = __fadd_rn(__fadd_rn(sacc, s1), __fadd_rn(s2, s3));  // on k == 0 lanes
+  const unsigned nfm = __ballot_sync(kFull, nf);
+  bad = ((nfm >> (4 * (lane & 7))) & 0xFu) != 0u;
+  return __shfl_sync(kFull, tot, 4 * (lane & 7));
+}
+
 // Per-row gradient scale: D_row = dir(residual, scale) in the backward.
 template <int KIND>
 __device__ __forceinline__ float row_scale(float up, float s) {
@@ -156,18 +181,18 @@ __device__ __forceinline__ float row_scale(float up, float s) {
 
 // TRAIN-mode gather of a tile's 8 (pos, neg) pairs: lanes k and k + 8 hold
 // the ids of pair k's positive and negative row (same relation).
-template <int KIND, int P>
+template <int KIND, int P, int TP = 8>
 __device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int d4, int64_t N, int h, int t, int r,
                                              float* rows, int S, int lane) {
 #pragma unroll
-  for (int k0 = 0; k0 < 8; k0 += P) {
+  for (int k0 = 0; k0 < TP; k0 += P) {
     int hp[P], tp[P], hn[P], tn[P], rr[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) {
       hp[q] = __shfl_sync(kFull, h, k0 + q);
       tp[q] = __shfl_sync(kFull, t, k0 + q);
-      hn[q] = __shfl_sync(kFull, h, k0 + q + 8);
-      tn[q] = __shfl_sync(kFull, t, k0 + q + 8);
+      hn[q] = __shfl_sync(kFull, h, k0 + q + TP);
+      tn[q] = __shfl_sync(kFull, t, k0 + q + TP);
       rr[q] = __shfl_sync(kFull, r, k0 + q);
     }
     for (int c = lane; c < d4; c += 32) {
@@ -183,7 +208,7 @@ __device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int 
 #pragma unroll
       for (int q = 0; q < P; ++q) {
         *reinterpret_cast<float4*>(rows + (k0 + q) * S + 4 * c) = hrt_combine<KIND>(xa[q], xb[q], xr[q], hp[q] == tp[q]);
-        *reinterpret_cast<float4*>(rows + (k0 + q + 8) * S + 4 * c) =
+        *reinterpret_cast<float4*>(rows + (k0 + q + TP) * S + 4 * c) =
             hrt_combine<KIND>(xe[q], xf[q], xr[q], hn[q] == tn[q]);
       }
     }
@@ -199,7 +224,7 @@ __device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int 
 #ifndef SKG_FWD_P256
 #define SKG_FWD_P256 2  // ... when d <= 256
 #endif
-template <int KIND, bool TRAIN, int VEC, int MINB = SKG_FWD_MINB>
+template <int KIND, bool TRAIN, int VEC, int MINB = SKG_FWD_MINB, int TP = 8>
 __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdArgs a) {
   extern __shared__ float4 smem4[];
   __shared__ float warp_loss[kWarps];
@@ -208,8 +233,9 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = a.de;
   const int S = VEC == 4 ? d + 4 : d + 1;
-  float* rows = smem + warp * 16 * S;
-  constexpr int kUnits = TRAIN ? 8 : 16;
+  constexpr int RW = TRAIN ? 2 * TP : 16;  // rows per warp tile
+  float* rows = smem + warp * RW * S;
+  constexpr int kUnits = TRAIN ? TP : 16;
   const int ntiles = (a.B + kUnits - 1) / kUnits;
   const int64_t N = a.N;
   float lsum = 0.f;
@@ -221,8 +247,8 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
   int4 pq_next = make_int4(0, 0, 0, 0);
   int pr_next = 0;
   auto prefetch = [&](int tl) {
-    if (TRAIN && a.pair_ht && lane < 16) {
-      const int p = tl * 8 + (lane & 7);
+    if (TRAIN && a.pair_ht && lane < RW) {
+      const int p = tl * TP + (lane & (TP - 1));
       if (tl < ntiles && p < a.B) {
         pq_next = __ldg(a.pair_ht + p);
         pr_next = __ldg(a.pair_r + p);
@@ -237,10 +263,10 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
     const int4 pq = pq_next;
     const int prr = pr_next;
     prefetch(tile + gridDim.x * nwarps);
-    if (lane < 16) {
+    if (lane < RW) {
       if (TRAIN) {
-        const int p = tile * 8 + (lane & 7);
-        const bool neg = lane >= 8;
+        const int p = tile * TP + (lane & (TP - 1));
+        const bool neg = lane >= TP;
         valid = p < a.B;
         if (valid) {
           if (a.pair_ht) {
@@ -273,9 +299,10 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
       // pair-grouped: a pair's positive (row k) and negative (row k + 8) share
       // the relation row, so P pairs need 5P row loads, all in flight at once
       const int d4 = d >> 2;
-      if (d4 <= 32) gather_pairs<KIND, SKG_FWD_P128>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
-      else if (d4 <= 64) gather_pairs<KIND, SKG_FWD_P256>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
-      else gather_pairs<KIND, 1>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
+      constexpr int P128 = SKG_FWD_P128 < TP ? SKG_FWD_P128 : TP, P256 = SKG_FWD_P256 < TP ? SKG_FWD_P256 : TP;
+      if (d4 <= 32) gather_pairs<KIND, P128, TP>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
+      else if (d4 <= 64) gather_pairs<KIND, P256, TP>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
+      else gather_pairs<KIND, 1, TP>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
     } else if (VEC == 4) {
       const float4* X4 = reinterpret_cast<const float4*>(a.X);
       const int d4 = d >> 2;
@@ -320,13 +347,13 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
     bool bad = false;
     if ((KIND == kTransE_L2 || KIND == kTransE_L1) && VEC == 4 && d >= 8) {
       bool b = false;
-      const float sw = warp_reduce16<KIND>(rows, S, d, lane, b);
-      if (lane < 16 && valid) {
+      const float sw = RW == 8 ? warp_reduce8<KIND>(rows, S, d, lane, b) : warp_reduce16<KIND>(rows, S, d, lane, b);
+      if (lane < RW && valid) {
         s = sw;
         bad = b;
         score = (KIND == kTransE_L2) ? __fsqrt_rn(s) : s;  // norms.hpp:57-62
       }
-    } else if (lane < 16 && valid) {
+    } else if (lane < RW && valid) {
       s = ref_reduce<KIND, VEC>(rows + lane * S, d, bad);
       score = (KIND == kTransE_L2) ? __fsqrt_rn(s) : s;  // norms.hpp:57-62, 107-115
     }
@@ -335,19 +362,19 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
     bool act = false;
     if (TRAIN) {
       // ---- margin hinge on (pos = lane k, neg = lane k + 8), training.cpp:86-96
-      const float ns = __shfl_down_sync(kFull, score, 8);
+      const float ns = __shfl_down_sync(kFull, score, TP);
       float term = 0.f;
-      if (lane < 8 && valid) {
+      if (lane < TP && valid) {
         term = __fsub_rn(__fadd_rn(a.margin, score), ns);
         act = term > 0.f;  // strict
       }
       const float tk = act ? term : 0.f;
       float tsum = 0.f;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) tsum = __fadd_rn(tsum, __shfl_sync(kFull, tk, k));
+      for (int k = 0; k < TP; ++k) tsum = __fadd_rn(tsum, __shfl_sync(kFull, tk, k));
       lsum = __fadd_rn(lsum, tsum);
-      act = __shfl_sync(kFull, act, lane & 7) && lane < 16 && valid;
-      up = act ? (lane < 8 ? a.unit : -a.unit) : 0.f;
+      act = __shfl_sync(kFull, act, lane & (TP - 1)) && lane < RW && valid;
+      up = act ? (lane < TP ? a.unit : -a.unit) : 0.f;
     } else {
       act = lane < 16 && valid;
       up = (act && a.upstream) ? a.upstream[row2] : 0.f;
@@ -358,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
     if ((KIND == kTransE_L2 || KIND == kTorusE_L2) && bad && (TRAIN || a.upstream))
       pend |= (h != t) ? kPendEntity : kPendRelation;
 
-    if (lane < 16 && valid) {
+    if (lane < RW && valid) {
       a.scal[row2] = sc;
       if (!TRAIN) a.scores[row2] = score;
     }
@@ -545,13 +572,18 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
 template <int KIND, bool TRAIN, int VEC>
 void launch_fwd_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
   constexpr size_t kSmemCap = 200 * 1024;
+  // d > 128 (DRAM-resident wide tables, C5): 4-pair tiles, half the shared
+  // memory per warp, so twice the warps (and row loads) in flight per SM
+  // (TransE only: the torus sums are lane-serial, so their 16-row tiles stay)
+  const bool small_tile = TRAIN && VEC == 4 && (KIND == kTransE_L2 || KIND == kTransE_L1) && a.de > 128 &&
+                          std::getenv("SKG_FWD_TILE8") == nullptr;
   const int S = VEC == 4 ? a.de + 4 : a.de + 1;
-  const size_t per_warp = static_cast<size_t>(16) * S * sizeof(float);
+  const size_t per_warp = static_cast<size_t>(small_tile ? 8 : 16) * S * sizeof(float);
   if (per_warp > kSmemCap) throw CudaError("hrt_forward: embedding dimension too large for the staged tile");
   int wpb = static_cast<int>(kSmemCap / 3 / per_warp);  // aim for >= 3 resident blocks per SM
   wpb = wpb < 1 ? 1 : (wpb > kWarps ? kWarps : wpb);
   const size_t smem = wpb * per_warp;
-  const int units = TRAIN ? 8 : 16;
+  const int units = TRAIN ? (small_tile ? 4 : 8) : 16;
   const int ntiles = (a.B + units - 1) / units;
   int per_sm = static_cast<int>(kSmemCap / (smem + 1024));
   per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
@@ -560,7 +592,8 @@ void launch_fwd_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
   if (grid < 1) grid = 1;
   // d > 128: three blocks' worth of registers per SM (more rows in flight for
   // the DRAM-resident wide tables; C5 +3 %), d <= 128: two (C1 -1.5 % with three)
-  if (a.de > 128) hrt_forward_kernel<KIND, TRAIN, VEC, 3><<<grid, wpb * 32, smem, s>>>(a);
+  if (small_tile) hrt_forward_kernel<KIND, TRAIN, VEC, 3, 4><<<grid, wpb * 32, smem, s>>>(a);
+  else if (a.de > 128) hrt_forward_kernel<KIND, TRAIN, VEC, 3><<<grid, wpb * 32, smem, s>>>(a);
   else hrt_forward_kernel<KIND, TRAIN, VEC><<<grid, wpb * 32, smem, s>>>(a);
   count_launch();
   SKG_LAUNCH_CHECK();
@@ -611,6 +644,8 @@ void configure_one() {
   SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC, 3>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC, 3, 4>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 }
 template <int KIND>
