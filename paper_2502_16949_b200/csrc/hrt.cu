@@ -221,6 +221,9 @@ __device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int 
 #ifndef SKG_FWD_P128
 #define SKG_FWD_P128 4  // pairs gathered together when d <= 128 (5 row loads each)
 #endif
+#ifndef SKG_FWD_MINB_SMALL
+#define SKG_FWD_MINB_SMALL 3
+#endif
 #ifndef SKG_FWD_P256
 #define SKG_FWD_P256 2  // ... when d <= 256
 #endif
@@ -592,7 +595,7 @@ void launch_fwd_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
   if (grid < 1) grid = 1;
   // d > 128: three blocks' worth of registers per SM (more rows in flight for
   // the DRAM-resident wide tables; C5 +3 %), d <= 128: two (C1 -1.5 % with three)
-  if (small_tile) hrt_forward_kernel<KIND, TRAIN, VEC, 3, 4><<<grid, wpb * 32, smem, s>>>(a);
+  if (small_tile) hrt_forward_kernel<KIND, TRAIN, VEC, SKG_FWD_MINB_SMALL, 4><<<grid, wpb * 32, smem, s>>>(a);
   else if (a.de > 128) hrt_forward_kernel<KIND, TRAIN, VEC, 3><<<grid, wpb * 32, smem, s>>>(a);
   else hrt_forward_kernel<KIND, TRAIN, VEC><<<grid, wpb * 32, smem, s>>>(a);
   count_launch();
@@ -645,7 +648,7 @@ void configure_one() {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC, 3>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC, 3, 4>,
+  SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, TRAIN, VEC, SKG_FWD_MINB_SMALL, 4>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 }
 template <int KIND>
