@@ -65,3 +65,38 @@ def test_dp_world1_ht_models(orc32, model, norm, d, dr):
     if gn is not None:
         assert rel_err(gn, st.normals) <= 1e-5
     eng.close()
+
+
+def test_dp_world1_bench_paths(orc32):
+    """Every engine call bench.py makes under torchrun (N > 1 uses the same code with a
+    larger communicator): graph-captured epochs, the evented profiling epoch and the e2e
+    re-upload loop, on an NCCL communicator of size 1; tables stay equal to the oracle."""
+    n, r, d = 1500, 30, 32
+    h, rel, t = orc32.synthetic_train(n, r, 12000, 5)
+    st = orc32.init_store("transe", n, r, d, d, 5)
+    eng = Engine(0)
+    cfg = ModelConfig.make("transe", d, d, "l2")
+    eng.store_upload(cfg, st.entity, st.relation)
+    eng.set_triples(h, rel, t, n, r)
+    nh, nt = eng.negative_sample(5)
+    eng.dp_init(Engine.nccl_unique_id(), 0, 1)
+    tc_e = TrainConfig.make(lr=0.05, batch_size=1000, seed=9)
+    tc_o = orc32.train_config(lr=0.05, batch_size=1000, seed=9)
+    ep = 0
+    for _ in range(2):  # captured epoch graphs
+        eng.train_epoch(cfg, tc_e, ep, 0.05)
+        orc32.train_epoch("transe", st, (h, rel, t), (nh, nt), tc_o, ep, 0.05)
+        ep += 1
+    rep, fwd_ms, bwd_ms, plan_ms = eng.profile_epoch(cfg, tc_e, ep, 0.05)  # evented, eager
+    orc32.train_epoch("transe", st, (h, rel, t), (nh, nt), tc_o, ep, 0.05)
+    ep += 1
+    assert fwd_ms > 0 and bwd_ms > 0
+    for _ in range(2):  # e2e loop: host ids re-uploaded every epoch (synchronous under data parallel)
+        eng.set_triples(h, rel, t, n, r)
+        eng.set_negatives(nh, nt)
+        eng.train_epoch(cfg, tc_e, ep, 0.05)
+        orc32.train_epoch("transe", st, (h, rel, t), (nh, nt), tc_o, ep, 0.05)
+        ep += 1
+    ge, gr, _, _ = eng.store_download()
+    assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation)
+    eng.close()
