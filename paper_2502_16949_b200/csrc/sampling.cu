@@ -123,27 +123,46 @@ __global__ void __launch_bounds__(kJumpThreads) mt_chunk_kernel(const uint64_t* 
   if (j > 0) {
     const uint64_t* p = polys + (j - 1) * kJumpWords;
     for (int wi = kJumpWords - 1; wi >= 0; --wi) {
-      const uint64_t bits = __ldg(p + wi);
+      const uint64_t bits = __ldg(p + wi);  // block-uniform
+      // acc = A^64(acc): 64 independent word steps (reads of the old window first)
       uint64_t nw = 0;
+      int slot = 0;
       if (tid < 64) {
-        const int k = h + tid;
-        nw = acc[(k + kMtM) % kMtN] ^ mt_mix(acc[k % kMtN], acc[(k + 1) % kMtN]);
+        int k0 = h + tid;
+        k0 -= k0 >= kMtN ? kMtN : 0;
+        int k1 = k0 + 1;
+        k1 -= k1 >= kMtN ? kMtN : 0;
+        int km = k0 + kMtM;
+        km -= km >= kMtN ? kMtN : 0;
+        nw = acc[km] ^ mt_mix(acc[k0], acc[k1]);
+        slot = k0;
       }
       __syncthreads();
-      if (tid < 64) acc[(h + tid) % kMtN] = nw;
-      h = (h + 64) % kMtN;
+      if (tid < 64) acc[slot] = nw;
+      h += 64;
+      h -= h >= kMtN ? kMtN : 0;
       __syncthreads();
+      // acc ^= sum_k p_(64 wi + k) A^k s0: a uniform branch per coefficient,
+      // consecutive threads read consecutive words of s0's sequence
       if (bits && tid < kMtN) {
         uint64_t x = 0;
-        for (uint64_t m = bits; m; m &= m - 1) x ^= s0[__ffsll(static_cast<long long>(m)) - 1 + tid];
-        acc[(h + tid) % kMtN] ^= x;
+#pragma unroll 16
+        for (int k = 0; k < 64; ++k)
+          if ((bits >> k) & 1u) x ^= s0[k + tid];
+        int w = h + tid;
+        w -= w >= kMtN ? kMtN : 0;
+        acc[w] ^= x;
       }
       __syncthreads();
     }
   }
   // generate the chunk from the jumped window (thread i < 156 keeps words i and 156 + i)
   const bool on = tid < kMtM;
-  uint64_t a = on ? acc[(h + tid) % kMtN] : 0ull, b = on ? acc[(h + kMtM + tid) % kMtN] : 0ull;
+  int ia = h + tid, ib = h + kMtM + tid;
+  ia -= ia >= kMtN ? kMtN : 0;
+  ib -= ib >= kMtN ? kMtN : 0;
+  ib -= ib >= kMtN ? kMtN : 0;
+  uint64_t a = on ? acc[ia] : 0ull, b = on ? acc[ib] : 0ull;
   const int64_t w0 = j * L, w1 = min(n, w0 + L);
   const int64_t nstates = (w1 - w0 + kMtN - 1) / kMtN;
   int cur = 0;
