@@ -320,11 +320,9 @@ void enqueue_plan(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s) 
                                                         ps.order_g.p);
     count_launch();
     SKG_LAUNCH_CHECK();
-    build_epoch_plan(ps.order_g.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, es.Mg, es.S, ctx->N,
-                     ctx->R, ps.plan, s);
+    build_epoch_plan(ps.order_g.p, ctx->quad.p, ctx->Rl.p, es.Mg, es.S, ctx->N, ctx->R, ps.plan, s);
   } else {
-    build_epoch_plan(ps.order.p, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->M, es.B, ctx->N,
-                     ctx->R, ps.plan, s);
+    build_epoch_plan(ps.order.p, ctx->quad.p, ctx->Rl.p, ctx->M, es.B, ctx->N, ctx->R, ps.plan, s);
   }
 }
 
@@ -517,6 +515,11 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
     sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
   }
   ctx->shuffle.reserve(ctx->M);
+  if (ctx->quad_version != ctx->data_version || ctx->quad.n < ctx->M + 1) {  // packed ids for the plan
+    ctx->quad.ensure(ctx->M + 1);
+    pack_triple_quads(ctx->H.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->M, ctx->quad.p, ctx->stream);
+    ctx->quad_version = ctx->data_version;
+  }
   ensure_workspace(ctx, 2 * es.B, es.kind);
   if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, 2 * es.B, ctx->de, ctx->dr, ctx->R));
   ctx->batch_loss.ensure(es.nb);
@@ -538,7 +541,8 @@ std::string raw_key(const T&... v) {
 }
 
 std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
-  return raw_key(es.B, es.nb, es.shuffle, es.kind, ctx->M, ctx->tables.p, ctx->H.p, ctx->NH.p, ctx->slots[0].order.p,
+  return raw_key(es.B, es.nb, es.shuffle, es.kind, ctx->M, ctx->tables.p, ctx->H.p, ctx->NH.p, ctx->quad.p,
+                 ctx->slots[0].order.p,
                  ctx->slots[1].order.p, ctx->res.p, ctx->ht_work.p, ctx->slots[0].plan.cap_entries,
                  ctx->slots[1].plan.cap_entries, ctx->shuffle.cap_n, es.world, es.rank, ctx->dp_grad.p,
                  ctx->slots[0].order_g.p, ctx->slots[1].order_g.p, ctx->proj.p, ctx->normals.p, margin);

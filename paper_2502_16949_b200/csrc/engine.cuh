@@ -71,6 +71,8 @@ struct skg_ctx {
   // ---- triples
   int64_t M = 0, tN = 0, tR = 0;
   skg::DevBuf<int32_t> H, Rl, T, NH, NT;
+  skg::DevBuf<int4> quad;            // {H, T, NH, NT} per triple, packed for the plan's gathers
+  uint64_t quad_version = ~0ull;     // data_version quad was packed at
   bool has_neg = false;
 
   // ---- epoch machinery

@@ -35,30 +35,35 @@ __device__ __forceinline__ void emit_row(uint32_t* key, uint32_t* val, int64_t b
   val[base + 2] = row2;
 }
 
-__global__ void gen_train_entries_kernel(const int32_t* __restrict__ order, const int32_t* __restrict__ H,
-                                         const int32_t* __restrict__ R, const int32_t* __restrict__ T,
-                                         const int32_t* __restrict__ NH, const int32_t* __restrict__ NT,
-                                         int64_t M, int64_t B, int64_t N, int64_t Rn, int cb,
-                                         uint32_t* __restrict__ key,
+// One thread per epoch position k: the triple's packed ids {h, t, nh, nt}
+// (one 16-byte read instead of four scattered 4-byte ones) and its relation
+// give the pair record and the positive and negative rows' entries.
+__global__ void gen_train_entries_kernel(const int32_t* __restrict__ order, const int4* __restrict__ quad,
+                                         const int32_t* __restrict__ R, int64_t M, int64_t B, int64_t N,
+                                         int64_t Rn, int cb, uint32_t* __restrict__ key,
                                          uint32_t* __restrict__ val, int4* __restrict__ pair_ht,
                                          int32_t* __restrict__ pair_r) {
-  for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < 2 * M;
-       x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t k = x >> 1;
-    const int p = static_cast<int>(x & 1);
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < M;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t b = k / B, i = k - b * B;
     const int64_t Bb = min(B, M - b * B);
-    const int32_t id = order[k];
-    const int32_t h = p ? NH[id] : H[id];
-    const int32_t t = p ? NT[id] : T[id];
-    const int64_t base = 6 * b * B + 3 * (p * Bb + i);
-    if (p == 0) {
-      pair_ht[k] = make_int4(h, t, NH[id], NT[id]);
-      pair_r[k] = R[id];
-    }
-    emit_row(key, val, base, static_cast<uint32_t>(b) << cb, h, t, R[id],
-             static_cast<uint32_t>(p * Bb + i), N, Rn, true);
+    const int32_t id = __ldg(order + k);
+    const int4 q = __ldg(quad + id);
+    const int32_t r = __ldg(R + id);
+    pair_ht[k] = q;
+    pair_r[k] = r;
+    const uint32_t bkey = static_cast<uint32_t>(b) << cb;
+    emit_row(key, val, 6 * b * B + 3 * i, bkey, q.x, q.y, r, static_cast<uint32_t>(i), N, Rn, true);
+    emit_row(key, val, 6 * b * B + 3 * (Bb + i), bkey, q.z, q.w, r, static_cast<uint32_t>(Bb + i), N, Rn, true);
   }
+}
+
+__global__ void pack_quad_kernel(const int32_t* __restrict__ H, const int32_t* __restrict__ T,
+                                 const int32_t* __restrict__ NH, const int32_t* __restrict__ NT, int64_t M,
+                                 int4* __restrict__ quad) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < M;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    quad[i] = make_int4(H[i], T[i], NH[i], NT[i]);
 }
 
 __global__ void gen_batch_entries_kernel(const int32_t* __restrict__ H, const int32_t* __restrict__ R,
@@ -173,8 +178,15 @@ void EpochPlan::release() {
   scan.release();
 }
 
-void build_epoch_plan(const int32_t* order, const int32_t* H, const int32_t* R, const int32_t* T,
-                      const int32_t* NH, const int32_t* NT, int64_t M, int64_t B, int64_t N,
+void pack_triple_quads(const int32_t* H, const int32_t* T, const int32_t* NH, const int32_t* NT, int64_t M,
+                       int4* quad, cudaStream_t s) {
+  if (M <= 0) return;
+  pack_quad_kernel<<<grid_for(M), 256, 0, s>>>(H, T, NH, NT, M, quad);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
+void build_epoch_plan(const int32_t* order, const int4* quad, const int32_t* R, int64_t M, int64_t B, int64_t N,
                       int64_t Rn, EpochPlan& p, cudaStream_t s) {
   p.nb = (M + B - 1) / B;
   p.E = 6 * M;
@@ -182,8 +194,8 @@ void build_epoch_plan(const int32_t* order, const int32_t* H, const int32_t* R, 
   p.cb = bits_for(static_cast<uint64_t>(N + Rn));  // + the dummy column N + Rn
   if (p.kb + p.cb > 31) throw CudaError("epoch plan: batches x columns exceed the 31-bit key space");
   p.reserve(p.E, p.nb);
-  gen_train_entries_kernel<<<grid_for(2 * M), 256, 0, s>>>(order, H, R, T, NH, NT, M, B, N, Rn, p.cb, p.key,
-                                                           p.val, p.pair_ht, p.pair_r);
+  gen_train_entries_kernel<<<grid_for(M), 256, 0, s>>>(order, quad, R, M, B, N, Rn, p.cb, p.key, p.val, p.pair_ht,
+                                                       p.pair_r);
   count_launch();
   SKG_LAUNCH_CHECK();
   finish_plan(p, 6 * B, N, Rn, s);

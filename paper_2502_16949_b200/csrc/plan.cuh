@@ -46,10 +46,12 @@ struct EpochPlan {
   ~EpochPlan() { release(); }
 };
 
-// Training epoch: pos/neg rows through `order`, batch size B.
-void build_epoch_plan(const int32_t* order, const int32_t* H, const int32_t* R, const int32_t* T,
-                      const int32_t* NH, const int32_t* NT, int64_t M, int64_t B, int64_t N,
+// Training epoch: pos/neg rows through `order`, batch size B. quad[id] =
+// {H, T, NH, NT}[id] (pack_triple_quads, once per data version).
+void build_epoch_plan(const int32_t* order, const int4* quad, const int32_t* R, int64_t M, int64_t B, int64_t N,
                       int64_t Rn, EpochPlan& p, cudaStream_t s);
+void pack_triple_quads(const int32_t* H, const int32_t* T, const int32_t* NH, const int32_t* NT, int64_t M,
+                       int4* quad, cudaStream_t s);
 // One explicit batch (score_backward parity path): rows i with (H,R,T)[i].
 // layout 0 = ht (no relation entries), 1 = hrt.
 void build_batch_plan(const int32_t* H, const int32_t* R, const int32_t* T, int64_t m, int64_t N,
