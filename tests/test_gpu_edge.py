@@ -94,3 +94,24 @@ def test_tiny_and_ragged_batches(eng, orc32, model, m, bs):
     ge, gr, _, _ = eng.store_download()
     assert ge.shape[1] == w * d
     assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation)
+
+
+@pytest.mark.parametrize("model", ["transe", "complex"])
+def test_fit_with_entity_renormalization(eng, orc32, model):  # training.cpp:187, embedding.cpp:192-198
+    """fit(renorm_entities): every entity row back to unit norm after each epoch (row.norm()
+    is an Eigen reduction: tolerance). Complex rows normalise over their (re, im) pairs."""
+    n, r, d = 1500, 12, 8
+    h, rel, t = orc32.synthetic_train(n, r, 4000, 4)
+    st = orc32.init_store(model, n, r, d, d, 4)
+    cfg = ModelConfig.make(model, d, d)
+    eng.store_upload(cfg, st.entity, st.relation)
+    eng.set_triples(h, rel, t, n, r)
+    kw = dict(lr=0.05, batch_size=128, seed=6, renorm_entities=True)
+    rg = eng.fit(cfg, TrainConfig.make(epochs=3, **kw))
+    ro = orc32.fit(model, st, h, rel, t, orc32.train_config(epochs=3, **kw))
+    for a, b in zip(rg, ro):
+        assert abs(a.loss - b.loss) <= 1e-5 * max(1.0, abs(b.loss))
+    ge, gr, _, _ = eng.store_download()
+    err = np.max(np.abs(ge.astype(np.float64) - st.entity) / np.maximum(1.0, np.abs(st.entity)))
+    assert err <= 1e-5, err
+    assert np.allclose(np.linalg.norm(ge.astype(np.float64), axis=1), 1.0, atol=1e-5)
