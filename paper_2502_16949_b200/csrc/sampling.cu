@@ -145,10 +145,17 @@ __global__ void __launch_bounds__(kJumpThreads) mt_chunk_kernel(const uint64_t* 
       // acc ^= sum_k p_(64 wi + k) A^k s0: a uniform branch per coefficient,
       // consecutive threads read consecutive words of s0's sequence
       if (bits && tid < kMtN) {
-        uint64_t x = 0;
-#pragma unroll 16
-        for (int k = 0; k < 64; ++k)
-          if ((bits >> k) & 1u) x ^= s0[k + tid];
+        // four independent XOR chains so the shared-memory loads overlap
+        uint64_t x0 = 0, x1 = 0, x2 = 0, x3 = 0;
+        const uint64_t* src = s0 + tid;
+#pragma unroll
+        for (int k = 0; k < 64; k += 4) {
+          if ((bits >> k) & 1u) x0 ^= src[k];
+          if ((bits >> (k + 1)) & 1u) x1 ^= src[k + 1];
+          if ((bits >> (k + 2)) & 1u) x2 ^= src[k + 2];
+          if ((bits >> (k + 3)) & 1u) x3 ^= src[k + 3];
+        }
+        const uint64_t x = (x0 ^ x1) ^ (x2 ^ x3);
         int w = h + tid;
         w -= w >= kMtN ? kMtN : 0;
         acc[w] ^= x;
