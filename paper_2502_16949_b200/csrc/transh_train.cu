@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transh_tile_kernel(const
     const uint32_t lo = rt.first[k], hi = rt.first[k + 1];
     if (tid == 0) {
       rel_last = atomicAdd(a.rel_ticket + k, 1u) == hi - lo - 1;
+      if (rel_last) a.rel_ticket[k] = 0;  // every tile of k has arrived: ready for the next batch
     }
     __syncthreads();
     if (rel_last && tid < 2 * kD) {
@@ -390,10 +391,13 @@ void configure_transh_tiles_kernels() {
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
                               cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks) {
   const int64_t mt = relation_max_tiles(2 * static_cast<int64_t>(fa.B), R);
-  float* partial = work;
-  uint32_t* ticket = reinterpret_cast<uint32_t*>(partial + mt * 2 * kD);
-  // per-relation tickets, zeroed for every batch (a memset node in the graph)
-  SKG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(uint32_t) * (R + 1), s));
+  // tickets lead the workspace (a fixed address for every batch size), the
+  // float4 tile partials follow
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(work);
+  float* partial = work + ((R + 1 + 3) & ~static_cast<int64_t>(3));
+  // per-relation tickets: zeroed at the epoch's first batch, then reset by the
+  // CTA that retires each relation (no memset node between the batch kernels)
+  if (ba.batch == 0) SKG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(uint32_t) * (R + 1), s));
   TArgs a{};
   a.f = fa;
   a.ent_val = ba.ent_val;
