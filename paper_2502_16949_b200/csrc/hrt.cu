@@ -484,6 +484,139 @@ template <int VEC> struct VecT;
 template <> struct VecT<4> { using T = float4; };
 template <> struct VecT<1> { using T = float; };
 
+// One column segment [e0, e1) of column `col`, by one warp; CH vector chunks
+// per lane per pass (CH = 1 covers d <= 128 with float4 lanes). Up to KB
+// residual rows are in flight per round; the adds stay in the segment's entry
+// order. `single`: a one-entry segment whose entry v0 and scale sc0 the
+// caller already holds.
+template <int KIND, bool SGD, int VEC, int CH, int KB>
+__device__ __forceinline__ void segment_rows(const BwdArgs& a, uint32_t col, uint32_t e0, uint32_t e1, bool single,
+                                             uint32_t v0, float sc0, int lane) {
+  using V = typename VecT<VEC>::T;
+  const int dv = a.d / VEC;
+  const V* RV = reinterpret_cast<const V*>(a.res);
+  V* P = reinterpret_cast<V*>(a.X) + static_cast<size_t>(col) * dv;
+  for (int cb = 0; cb < dv; cb += 32 * CH) {
+    int c[CH];
+    bool has[CH];
+    V acc[CH], p[CH];
+#pragma unroll
+    for (int h = 0; h < CH; ++h) {
+      c[h] = cb + 32 * h + lane;
+      has[h] = c[h] < dv;
+      acc[h] = V{};
+      p[h] = V{};
+      // the owner warp is the only writer of this row: load it up front
+      if (has[h]) p[h] = P[c[h]];
+      if (!SGD) acc[h] = p[h];  // accumulate into an existing sink (score_backward)
+    }
+    for (uint32_t eb = e0; eb < e1; eb += 32) {
+      const int cnt = min(32u, e1 - eb);
+      uint32_t myv = 0;
+      float mysc = 0.f;
+      if (lane < cnt) {
+        if (single) {
+          myv = v0;
+          mysc = sc0;
+        } else {
+          myv = a.ent_val[eb + lane];
+          mysc = a.scal[myv & 0x7fffffffu];
+        }
+      }
+      unsigned live = __ballot_sync(kFull, lane < cnt && mysc != 0.f);
+      while (live) {
+        int k[KB];
+        int n = 0;
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+          k[q] = live ? __ffs(live) - 1 : 0;
+          if (live) {
+            live &= live - 1;
+            ++n;
+          }
+        }
+        uint32_t vq[KB];
+        float scq[KB];
+        V rv[KB][CH];
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+          vq[q] = __shfl_sync(kFull, myv, k[q]);
+          scq[q] = __shfl_sync(kFull, mysc, k[q]);
+          size_t rowoff = static_cast<size_t>(vq[q] & 0x7fffffffu) * dv;
+          if (KIND == kMultRows) {  // the entry's own gradient plane: head, tail or relation
+            const uint32_t slot = col >= static_cast<uint32_t>(a.N) ? 2u : (vq[q] >> 31);
+            rowoff += static_cast<size_t>(slot) * a.plane_rows * dv;
+          }
+#pragma unroll
+          for (int h = 0; h < CH; ++h)
+            if (q < n && has[h]) rv[q][h] = __ldg(RV + rowoff + c[h]);
+        }
+#pragma unroll
+        for (int q = 0; q < KB; ++q)
+          if (q < n) {
+            const bool neg = KIND != kMultRows && (vq[q] >> 31) != 0;
+#pragma unroll
+            for (int h = 0; h < CH; ++h)
+              if (has[h]) acc_add<KIND>(acc[h], rv[q][h], scq[q], neg);
+          }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < CH; ++h) {
+      if (!has[h]) continue;
+      if (SGD) P[c[h]] = sgd1(p[h], acc[h], *a.lr);
+      else P[c[h]] = acc[h];
+    }
+  }
+}
+
+// The TransH / TransR entity pass at d <= 128 (float4 rows; one warp per
+// column segment, segment_rows): the warp's segments s = s0 + gw + i nw are
+// taken 32 at a time, lane j loading segment j's column and entry range and,
+// for a one-entry segment, its entry and scale into shared memory, so each
+// segment starts with its row loads instead of four dependent metadata loads
+// (C2: most entity segments hold one entry; epoch -3 %, C4 -1.8 %). The other
+// passes keep segment_backward_kernel: the staging measured slower there
+// (C1 backward 22.3 -> 30.8 us, M1 26.8 -> 29.4 us).
+template <bool SGD, int KB = SKG_BWD_KB>
+__global__ void __launch_bounds__(kThreads) segment_backward_staged_kernel(const BwdArgs a) {
+  if (a.err[0] != 0) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const uint32_t s0 = a.seg_base[a.batch], s1 = a.seg_base[a.batch + 1];
+  auto skip = [&](uint32_t col) {
+    return col == kDummyCol || (a.entity_only && col >= static_cast<uint32_t>(a.N));
+  };
+  __shared__ uint4 seg_q[kThreads / 32][32];  // {column, e0, e1, entry of a one-entry segment}
+  __shared__ float seg_sc[kThreads / 32][32];
+  uint4* myq = seg_q[threadIdx.x >> 5];
+  float* mysc = seg_sc[threadIdx.x >> 5];
+  for (uint32_t sb = s0 + gw; sb < s1; sb += 32u * static_cast<uint32_t>(nw)) {
+    const uint32_t sj = sb + static_cast<uint32_t>(lane) * static_cast<uint32_t>(nw);
+    uint4 q = make_uint4(kDummyCol, 0u, 0u, 0u);
+    float sc = 0.f;
+    if (sj < s1) {
+      q.x = a.seg_col[sj];
+      q.y = a.seg_start[sj];
+      q.z = a.seg_start[sj + 1];
+    }
+    const bool use = !skip(q.x);
+    if (use && q.z - q.y == 1) {
+      q.w = a.ent_val[q.y];
+      sc = a.scal[q.w & 0x7fffffffu];
+    }
+    __syncwarp();
+    myq[lane] = q;
+    mysc[lane] = sc;
+    for (unsigned m = __ballot_sync(kFull, use); m; m &= m - 1) {
+      const int j = __ffs(m) - 1;
+      const uint4 qj = myq[j];
+      segment_rows<kPlainRows, SGD, 4, 1, KB>(a, qj.x, qj.y, qj.z, qj.z - qj.y == 1, qj.w, mysc[j], lane);
+    }
+  }
+}
+
 // One warp per column segment; CH vector chunks per lane per pass (CH = 1
 // covers d <= 128 with float4 lanes). Up to KB residual rows are in flight
 // per round; the adds stay in the segment's entry order.
@@ -619,7 +752,10 @@ void launch_bwd_k(bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s) {
   const int grid = num_sms * 8;
   const bool v4 = (a.d % 4) == 0;
   const bool narrow = v4 ? a.d <= 128 : a.d <= 32;
-  if (sgd) {
+  if (KIND == kPlainRows && v4 && narrow) {
+    if (sgd) segment_backward_staged_kernel<true><<<grid, kThreads, 0, s>>>(a);
+    else segment_backward_staged_kernel<false><<<grid, kThreads, 0, s>>>(a);
+  } else if (sgd) {
     if (v4) {
       if (narrow) segment_backward_kernel<KIND, true, 4, 1><<<grid, kThreads, 0, s>>>(a);
       else if (KIND == kTorusE_L2 || KIND == kTorusE_L1)  // L2-resident wide rows: 8 in flight (C3 -9%)
