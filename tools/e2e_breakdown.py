@@ -38,6 +38,7 @@ def main():
         eng.set_negatives(nhp, ntp)
         eng.train_epoch(cfg, tc, w, bench.LR)
     acc = np.zeros(4)
+    per_step = []
     eng.synchronize()
     t_all = time.perf_counter()
     for k in range(args.steps):
@@ -49,11 +50,13 @@ def main():
         rep = eng.train_epoch(cfg, tc, 3 + k, bench.LR)
         t3 = time.perf_counter()
         acc += [t1 - t0, t2 - t1, t3 - t2, rep.t_backward_s]
+        per_step.append((round((t3 - t0) * 1e3, 2), round(rep.t_backward_s * 1e3, 2)))
     tot = time.perf_counter() - t_all
     acc /= args.steps
     print(f"{args.config}: M={M} step {tot / args.steps * 1e3:.3f} ms  e2e {M * args.steps / tot / 1e6:.1f} M/s")
     print(f"  set_triples {acc[0] * 1e3:.3f} ms  set_negatives {acc[1] * 1e3:.3f} ms  "
           f"train_epoch {acc[2] * 1e3:.3f} ms (graph {acc[3] * 1e3:.3f} ms)")
+    print("  per step (host ms, graph ms):", per_step)
     mb = 5 * M * 8 / 1e6
     print(f"  H2D {mb:.1f} MB -> {mb / 1e3 / (acc[0] + acc[1]):.1f} GB/s effective over the two set_* calls")
     # plain DMA of the same bytes for comparison
