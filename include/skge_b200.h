@@ -77,9 +77,11 @@ typedef struct skg_train_config { /* TrainConfig, training.hpp:29-50 */
 typedef struct skg_epoch_report { /* EpochReport, training.hpp:74-80 */
   int64_t epoch;
   double loss;
-  double t_forward_s;  /* device time of forward kernels (cudaEvent)  */
-  double t_backward_s; /* device time of backward+fused SGD kernels    */
-  double t_step_s;     /* device time of standalone step kernels        */
+  /* PhaseTimer buckets (training.cpp:15-20, 126, 141, 158), device time from
+   * event-record nodes inside the epoch graph (skg_set_phase_timers). */
+  double t_forward_s;  /* forward kernels: gather, score, hinge, loss      */
+  double t_backward_s; /* transposed-SpMM backward with the fused SGD step  */
+  double t_step_s;     /* standalone step kernels (0: the step is fused)   */
 } skg_epoch_report;
 
 typedef struct skg_ctx skg_ctx;
@@ -126,14 +128,20 @@ skg_status skg_renormalize_entities(skg_ctx* ctx);
 /* ---- triples and negatives ------------------------------------------------ */
 /* Training triples (TripleBatch, incidence.hpp:14-33) with their id space;
  * validated like TripleBatch::validate (ShapeError on a bad id).
- * Deferred re-upload: when the context already holds triples + negatives of
- * the same shape and the new arrays are page-locked (cudaHostAlloc /
- * torch pin_memory), skg_set_triples + skg_set_negatives only record the
- * pointers; the next skg_train_epoch copies and validates them while it
- * trains (an invalid id then fails that call with the same ShapeError, the
- * parameters untouched). Such pinned arrays must stay valid and unchanged
- * until the next engine call on the context, as with cudaMemcpyAsync.
- * Pageable arrays are always copied and validated inside the call. */
+ * By default the arrays are copied and validated inside the call (the
+ * reference's by-value TripleBatch semantics).
+ * Deferred re-upload (opt-in, skg_set_deferred_uploads): when the context
+ * already holds triples + negatives of the same shape and the new arrays are
+ * page-locked (cudaHostAlloc / torch pin_memory), skg_set_triples +
+ * skg_set_negatives only record the pointers; the next skg_train_epoch copies
+ * and validates them while it trains (an invalid id then fails that call with
+ * the same ShapeError, the parameters untouched). Deferred arrays must stay
+ * valid and unmodified until that skg_train_epoch RETURNS (any other engine
+ * call applies the pending upload synchronously first). Pageable arrays are
+ * never deferred. */
+skg_status skg_set_deferred_uploads(skg_ctx* ctx, int32_t enable); /* default 0 (off) */
+/* Deferred re-uploads so far: kept (identical data) / rolled back + retrained. */
+skg_status skg_upload_stats(skg_ctx* ctx, int64_t* hits, int64_t* misses);
 skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* heads, const int64_t* relations,
                            const int64_t* tails, int64_t num_entities, int64_t num_relations);
 /* Corrupted tails/heads aligned with the training triples (NegativeSet,
@@ -202,6 +210,9 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg,
                              const skg_train_config* tc, int64_t epoch, float lr,
                              skg_epoch_report* report, double* fwd_ms_per_batch,
                              double* bwd_ms_per_batch, double* plan_ms);
+/* Phase buckets of the epoch report, default on. Off: t_forward_s = 0 and
+ * t_backward_s = the whole epoch's device time (no event nodes in the graph). */
+skg_status skg_set_phase_timers(skg_ctx* ctx, int32_t enable);
 /* Number of CUDA kernels the last skg_train_epoch launched (graph nodes). */
 int64_t skg_last_launch_count(const skg_ctx* ctx);
 /* Synchronizes the context's streams. */

@@ -33,6 +33,8 @@ struct DpState {
 
 void dp_destroy(skg_ctx* ctx) {
   if (!ctx->dp) return;
+  // captured graphs hold NCCL calls on this communicator: never replay them
+  drop_graphs(ctx);
   if (ctx->dp->comm) ncclCommDestroy(ctx->dp->comm);
   delete ctx->dp;
   ctx->dp = nullptr;
@@ -40,6 +42,7 @@ void dp_destroy(skg_ctx* ctx) {
 
 int dp_rank(const skg_ctx* ctx) { return ctx->dp ? ctx->dp->rank : 0; }
 int dp_world(const skg_ctx* ctx) { return ctx->dp ? ctx->dp->world : 1; }
+const void* dp_comm_tag(const skg_ctx* ctx) { return ctx->dp ? static_cast<const void*>(ctx->dp->comm) : nullptr; }
 
 void dp_allreduce_sum(skg_ctx* ctx, float* buf, int64_t n, cudaStream_t s) {
   SKG_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(n), ncclFloat32, ncclSum, ctx->dp->comm, s));
@@ -72,9 +75,7 @@ skg_status skg_dp_init(skg_ctx* ctx, const char unique_id[128], int rank, int wo
       throw skg::CudaError("ncclCommInitRank failed");
     }
     ctx->dp = st;
-    if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
-    ctx->graph = nullptr;
-    ctx->graph_key.clear();
+    skg::drop_graphs(ctx);
     return SKG_OK;
   } catch (const skg::ConfigError& e) {
     ctx->err = e.what();

@@ -545,13 +545,17 @@ std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
                  ctx->slots[0].order.p,
                  ctx->slots[1].order.p, ctx->res.p, ctx->ht_work.p, ctx->slots[0].plan.cap_entries,
                  ctx->slots[1].plan.cap_entries, ctx->shuffle.cap_n, es.world, es.rank, ctx->dp_grad.p,
-                 ctx->slots[0].order_g.p, ctx->slots[1].order_g.p, ctx->proj.p, ctx->normals.p, margin);
+                 ctx->slots[0].order_g.p, ctx->slots[1].order_g.p, ctx->proj.p, ctx->normals.p, margin,
+                 // shapes baked into the captured launches (strides, relation offset, plan id space)
+                 ctx->N, ctx->R, ctx->de, ctx->dr, ctx->cfg.dim_entity, ctx->proj.n, ctx->normals.n, dp_comm_tag(ctx),
+                 ctx->phase_timers);
 }
 
 // Identity of an epoch plan: everything it depends on.
 std::string plan_key(skg_ctx* ctx, const EpochShape& es, const skg_train_config& tc, int64_t epoch) {
   const uint64_t seed = es.shuffle ? tc.seed : 0;
-  return raw_key(epoch, seed, es.shuffle, es.B, ctx->M, ctx->data_version, es.world, es.rank, ctx->H.p, ctx->NH.p);
+  return raw_key(epoch, seed, es.shuffle, es.B, ctx->M, ctx->data_version, es.world, es.rank, ctx->H.p, ctx->NH.p,
+                 ctx->N, ctx->R, dp_comm_tag(ctx));
 }
 
 void finish_epoch(skg_ctx* ctx, const EpochShape& es, int64_t epoch, skg_epoch_report* rep) {
@@ -589,6 +593,17 @@ void set_slot_seed(skg_ctx* ctx, int slot, uint64_t seed_eff) {
 void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
   const int nxt = 1 - cur;
   const int64_t before = kernel_launches();
+  const int64_t nb_marks = ctx->phase_timers ? 2 * es.nb + 1 : 0;
+  while (static_cast<int64_t>(ctx->phase_ev.size()) < nb_marks) {
+    cudaEvent_t e;
+    SKG_CUDA(cudaEventCreate(&e));
+    ctx->phase_ev.push_back(e);
+  }
+  int64_t marks = 0;
+  const std::function<void()> mark = [&]() {
+    if (marks >= nb_marks) throw CudaError("phase timer: more marks than reserved events");
+    SKG_CUDA(cudaEventRecordWithFlags(ctx->phase_ev[marks++], ctx->stream, cudaEventRecordExternal));
+  };
   cudaGraph_t g = nullptr;
   SKG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   try {
@@ -596,7 +611,9 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
     SKG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
     enqueue_plan(ctx, es, nxt, ctx->side);
     SKG_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
-    enqueue_batches(ctx, es, cur, ctx->stream, nullptr);
+    if (nb_marks) mark();
+    enqueue_batches(ctx, es, cur, ctx->stream, nb_marks ? &mark : nullptr);
+    if (marks != nb_marks) throw CudaError("phase timer: batch marks do not match the epoch shape");
     SKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   } catch (...) {
     cudaStreamEndCapture(ctx->stream, &g);
@@ -609,7 +626,21 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
   SKG_CUDA(cudaGraphInstantiate(&ctx->graphs[cur], g, 0));
   SKG_CUDA(cudaGraphDestroy(g));
   ctx->graph_launches_k[cur] = kernel_launches() - before;
+  ctx->phase_marks[cur] = nb_marks;
 }
+
+}  // namespace
+
+void skg::drop_graphs(skg_ctx* ctx) {
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->graphs[k]) cudaGraphExecDestroy(ctx->graphs[k]);
+    ctx->graphs[k] = nullptr;
+    ctx->graph_keys[k].clear();
+    ctx->slots[k].key.clear();
+  }
+}
+
+namespace {
 
 // Does any positive or negative triple have head == tail? (cached per data version)
 bool has_self_loops(skg_ctx* ctx) {
@@ -702,9 +733,24 @@ void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train
   }
   float ms = 0.f;
   SKG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-  rep->t_forward_s = 0.0;
-  rep->t_backward_s = ms * 1e-3;  // one fused graph; per-phase split: skg_profile_epoch
+  // PhaseTimer buckets (training.cpp:126, 141, 158). Forward: gather, score,
+  // hinge, loss of every batch. Backward: the transposed-SpMM reduce with the
+  // SGD step fused into it (touched rows), so the step has no kernel of its own
+  // and t_step_s stays 0; graph overhead outside the batches (error-word reset,
+  // the join with the next epoch's plan) is counted in the backward bucket so
+  // the buckets sum to the epoch's device time.
+  double fwd = 0.0;
+  if (ctx->phase_timers && ctx->phase_marks[ctx->last_slot] == 2 * es.nb + 1) {
+    for (int64_t b = 0; b < es.nb; ++b) {
+      float f = 0.f;
+      SKG_CUDA(cudaEventElapsedTime(&f, ctx->phase_ev[2 * b], ctx->phase_ev[2 * b + 1]));
+      fwd += f;
+    }
+  }
+  rep->t_forward_s = fwd * 1e-3;
+  rep->t_backward_s = std::max(0.0, ms - fwd) * 1e-3;
   rep->t_step_s = 0.0;
+  ctx->last_epoch_ms = ms;
 }
 
 void negative_sample_impl(skg_ctx* ctx, uint64_t seed, bool avoid) {  // training.cpp:51-71
@@ -919,7 +965,7 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->up, cudaStreamNonBlocking));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming));
 
-    if (const char* e = std::getenv("SKG_NO_SPECULATE")) ctx->speculate = e[0] == '0';
+    ctx->speculate = false;  // opt-in: skg_set_deferred_uploads
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     ctx->err_words.ensure(4);
@@ -951,9 +997,8 @@ void skg_destroy(skg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   dp_destroy(ctx);
-  if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
-  for (auto g : ctx->graphs)
-    if (g) cudaGraphExecDestroy(g);
+  drop_graphs(ctx);
+  for (auto e : ctx->phase_ev) cudaEventDestroy(e);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->up) {
     cudaStreamSynchronize(ctx->up);
@@ -1146,20 +1191,15 @@ void set_negatives_sync(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_
     ctx->neg_valid_version = ctx->data_version;
 }
 
-// Page-locked caller array? The last few answers are cached by address: a
-// stale "pinned" for memory re-allocated pageable at the same address is still
-// correct (cudaMemcpyAsync stages pageable memory), only not asynchronous.
-bool is_pinned(skg_ctx* ctx, const void* p) {
-  for (int k = 0; k < 8; ++k)
-    if (ctx->pinned_seen[k] == p) return true;
+// Page-locked caller array? Asked every time (no address cache: a pageable
+// buffer re-allocated at a freed pinned address must not be deferred).
+bool is_pinned(const void* p) {
   cudaPointerAttributes pa{};
   if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  const bool pinned = pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
-  if (pinned) ctx->pinned_seen[ctx->pinned_next++ & 7] = p;
-  return pinned;
+  return pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr;
 }
 
 // Applies a deferred upload synchronously (every entry point other than
@@ -1338,6 +1378,30 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
 
 extern "C" {
 
+skg_status skg_set_deferred_uploads(skg_ctx* ctx, int32_t enable) {
+  return guard(ctx, [&] {
+    resolve_pending(ctx);
+    ctx->speculate = enable != 0;
+    if (ctx->speculate && ctx->M > 0) {  // buffers of a later deferred re-upload, allocated now
+      ctx->stage_i64.ensure(5 * ctx->M + 1);
+      ctx->spec_flags.ensure(4);
+    }
+    if (ctx->speculate && ctx->has_store)
+      ctx->backup.ensure(ctx->tables.n + ctx->proj.n + ctx->normals.n + 12);
+  });
+}
+
+skg_status skg_set_phase_timers(skg_ctx* ctx, int32_t enable) {
+  return guard(ctx, [&] { ctx->phase_timers = enable != 0; });
+}
+
+skg_status skg_upload_stats(skg_ctx* ctx, int64_t* hits, int64_t* misses) {
+  return guard(ctx, [&] {
+    if (hits) *hits = ctx->spec_hits;
+    if (misses) *misses = ctx->spec_misses;
+  });
+}
+
 skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int64_t* r, const int64_t* t,
                            int64_t n_ent, int64_t n_rel) {
   return guard(ctx, [&] {
@@ -1345,8 +1409,8 @@ skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int6
     // An identical-shape re-upload of pinned arrays (the per-epoch e2e loop)
     // is deferred to the next train_epoch, which copies it while it trains.
     if (ctx->speculate && !ctx->dp && !ctx->pend_tri && ctx->triples_valid && m > 0 && m == ctx->M &&
-        n_ent == ctx->tN && n_rel == ctx->tR && ctx->neg_valid_version == ctx->data_version && is_pinned(ctx, h) &&
-        is_pinned(ctx, r) && is_pinned(ctx, t)) {
+        n_ent == ctx->tN && n_rel == ctx->tR && ctx->neg_valid_version == ctx->data_version && is_pinned(h) &&
+        is_pinned(r) && is_pinned(t)) {
       ctx->pend_tri = true;
       ctx->pend_neg = false;
       ctx->pend_ptr[0] = h;
@@ -1362,7 +1426,7 @@ skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* h, const int6
 
 skg_status skg_set_negatives(skg_ctx* ctx, int64_t m, const int64_t* nh, const int64_t* nt) {
   return guard(ctx, [&] {
-    if (ctx->pend_tri && !ctx->pend_neg && m == ctx->M && m > 0 && is_pinned(ctx, nh) && is_pinned(ctx, nt)) {
+    if (ctx->pend_tri && !ctx->pend_neg && m == ctx->M && m > 0 && is_pinned(nh) && is_pinned(nt)) {
       ctx->pend_neg = true;
       ctx->pend_ptr[3] = nh;
       ctx->pend_ptr[4] = nt;

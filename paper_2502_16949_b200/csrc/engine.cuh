@@ -110,14 +110,18 @@ struct skg_ctx {
   bool has_loops = false;                  // some positive or negative triple has head == tail
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-  cudaGraphExec_t graph = nullptr;  // legacy handle (unused)
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   std::string graph_keys[2];
   int64_t graph_launches_k[2] = {0, 0};
-  std::string graph_key;
-  int64_t graph_launches = 0;
   int64_t last_launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // PhaseTimer buckets (training.cpp:15-20) inside the epoch graph: external
+  // event-record nodes at the start of the batches and after every batch's
+  // forward and backward (2 * nb + 1 events, reused by every capture).
+  bool phase_timers = true;
+  std::vector<cudaEvent_t> phase_ev;
+  int64_t phase_marks[2] = {0, 0};  // events each captured graph records
+  double last_epoch_ms = 0;  // device time of the last graph epoch (ev0 -> ev1)
 
   // ---- deferred id uploads (speculative epoch). A re-upload of pinned arrays
   // with the shape of the current triples is recorded, not copied; the next
@@ -134,8 +138,6 @@ struct skg_ctx {
   skg::DevBuf<uint32_t> spec_flags; // first bad entity / relation / negative index, changed
   int64_t spec_hits = 0, spec_misses = 0;
   uint32_t* h_spec = nullptr;           // pinned: the check's flags
-  const void* pinned_seen[8] = {};      // recently seen page-locked caller arrays
-  unsigned pinned_next = 0;
 
   // ---- data parallel
   skg::DpState* dp = nullptr;

@@ -465,6 +465,14 @@ void eval_rank(int kind, const float* X, const float* Rt, int64_t N, int64_t R, 
                float* te, int num_sms, cudaStream_t s) {
   SKG_CUDA(cudaMemsetAsync(better, 0, sizeof(uint32_t) * 2 * q, s));
   if (q == 0) return;
+  // The per-query kernels put queries on grid.y (at most 65535): chunk.
+  constexpr int64_t kMaxQ = 65535;
+  if (q > kMaxQ) {
+    for (int64_t off = 0; off < q; off += kMaxQ)
+      eval_rank(kind, X, Rt, N, R, d, qh + off, qr + off, qt + off, std::min(kMaxQ, q - off), table, cap,
+                better + 2 * off, te + 2 * off, num_sms, s);
+    return;
+  }
   EvalArgs a{};
   a.X = X;
   a.Rt = Rt;

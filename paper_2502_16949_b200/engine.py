@@ -88,6 +88,9 @@ def load_library():
         "skg_store_download": [vp, vp, vp, vp, vp],
         "skg_sgd_step": [vp, vp, vp, vp, vp, f32],
         "skg_renormalize_entities": [vp],
+        "skg_set_deferred_uploads": [vp, i32],
+        "skg_set_phase_timers": [vp, i32],
+        "skg_upload_stats": [vp, vp, vp],
         "skg_set_triples": [vp, i64, vp, vp, vp, i64, i64],
         "skg_set_negatives": [vp, i64, vp, vp],
         "skg_negative_sample": [vp, C.c_uint64, i32, vp, vp],
@@ -191,6 +194,20 @@ class Engine:
         self._check(self.L.skg_renormalize_entities(self.h))
 
     # ------------------------------------------------------------ triples
+    def set_deferred_uploads(self, enable: bool):
+        """Opt-in overlapped re-upload of pinned id arrays (see skge_b200.h)."""
+        self._check(self.L.skg_set_deferred_uploads(self.h, int(bool(enable))))
+
+    def set_phase_timers(self, enable: bool):
+        """PhaseTimer buckets in EpochReport (default on; see skge_b200.h)."""
+        self._check(self.L.skg_set_phase_timers(self.h, int(bool(enable))))
+
+    def upload_stats(self):
+        """(hits, misses) of deferred re-uploads: identical data kept / rolled back and retrained."""
+        a, b = C.c_int64(), C.c_int64()
+        self._check(self.L.skg_upload_stats(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def set_triples(self, h, r, t, num_entities, num_relations):
         h, r, t = _i64(h), _i64(r), _i64(t)
         self._check(self.L.skg_set_triples(self.h, len(h), _p(h), _p(r), _p(t), num_entities, num_relations))

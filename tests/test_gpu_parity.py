@@ -336,6 +336,7 @@ def test_reupload_between_epochs_keeps_parity(eng, orc32, pinned):
     if pinned:
         nh, nt, nh2, nt2 = _pinned(nh), _pinned(nt), _pinned(nh2), _pinned(nt2)
     eng.store_upload(cfg, st.entity, st.relation)
+    eng.set_deferred_uploads(pinned)
     plan = [(nh, nt), (nh, nt), (nh2, nt2), (nh2, nt2), (nh, nt)]
     for ep, (a, b) in enumerate(plan):
         eng.set_triples(h, rel, t, n, r)
@@ -351,6 +352,36 @@ def test_reupload_between_epochs_keeps_parity(eng, orc32, pinned):
     eng.set_negatives(nh, nt)
     eng.train_epoch(cfg, tc_e, 5, 0.05)
     orc32.train_epoch("transe", st, (h3, rel, t), (nh, nt), tc_o, 5, 0.05)
+    ge, gr, _, _ = eng.store_download()
+    assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation)
+    if pinned:
+        hits, misses = eng.upload_stats()
+        assert hits >= 1 and misses >= 1, (hits, misses)
+    eng.set_deferred_uploads(False)
+
+
+def test_default_upload_is_copied_inside_the_call(eng, orc32):
+    """Deferral is opt-in: by default set_triples / set_negatives copy pinned arrays
+    inside the call, so the caller may overwrite them before train_epoch
+    (the reference's by-value TripleBatch semantics)."""
+    n, r, d, m = 300, 5, 8, 700
+    h, rel, t = orc32.synthetic_train(n, r, m, 6)
+    st = orc32.init_store("transe", n, r, d, d, 6)
+    cfg = ModelConfig.make("transe", d, d, "l2")
+    tc_e = TrainConfig.make(batch_size=64, seed=3, lr=0.05)
+    tc_o = orc32.train_config(batch_size=64, seed=3, lr=0.05)
+    nh, nt = orc32.negative_sample(h, rel, t, n, r, 3)
+    P = [_pinned(x) for x in (h, rel, t, nh, nt)]
+    eng.store_upload(cfg, st.entity, st.relation)
+    for ep in range(3):
+        eng.set_triples(*P[:3], n, r)
+        eng.set_negatives(*P[3:])
+        for a in P:  # the caller reuses its buffers right after the calls
+            a[:] = 0
+        eng.train_epoch(cfg, tc_e, ep, 0.05)
+        orc32.train_epoch("transe", st, (h, rel, t), (nh, nt), tc_o, ep, 0.05)
+        for a, b in zip(P, (h, rel, t, nh, nt)):
+            a[:] = b
     ge, gr, _, _ = eng.store_download()
     assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation)
 
@@ -384,6 +415,14 @@ def test_deferred_reupload_invalid_ids_roll_back(eng, orc32):
     nh, nt = orc32.negative_sample(h, rel, t, n, r, 3)
     P = [_pinned(x) for x in (h, rel, t, nh, nt)]
     eng.store_upload(cfg, st.entity, st.relation)
+    eng.set_deferred_uploads(True)
+    try:
+        _deferred_body(eng, orc32, cfg, tc_e, tc_o, st, P, h, rel, t, nh, nt, n, r)
+    finally:
+        eng.set_deferred_uploads(False)
+
+
+def _deferred_body(eng, orc32, cfg, tc_e, tc_o, st, P, h, rel, t, nh, nt, n, r):
     eng.set_triples(*P[:3], n, r)
     eng.set_negatives(*P[3:])
     eng.train_epoch(cfg, tc_e, 0, 0.05)

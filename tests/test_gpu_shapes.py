@@ -1,0 +1,175 @@
+"""Parity at the BASELINE configurations' own shapes (run on a B200: pytest -m gpu).
+
+- C5 (TransE d=256 on the 2.5M-entity wikikg2-shaped graph, batch 131,072):
+  trained tables bit-exact with the oracle after full-size minibatches, and the
+  negative sampler bit-exact over all 16,109,182 training triples (the chunked
+  MT19937-64 jump-ahead path).
+- C2 / C4 (TransH / TransR d=128): the reference reduces their dot products and
+  GEMVs through Eigen (tolerance-only parity), and at lr 4e-4 one step moves an
+  entity row by ~1e-9, so comparing tables would not see the backward at all.
+  These tests train one full minibatch with a large lr and compare the parameter
+  DELTAS (after - before) of every table with the oracle's, relative to the
+  delta's own size.
+- Run-to-run determinism of the TransH / TransR training kernels, bitwise
+  (the reference pins thread-count invariance bitwise, test_models.cpp:282-304).
+"""
+import numpy as np
+import pytest
+
+from paper_2502_16949_b200 import Engine, ModelConfig, TrainConfig
+
+pytestmark = pytest.mark.gpu
+
+C5 = dict(N=2500604, R=535, n_total=17899090, d=256, B=131072)
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = Engine(0)
+    yield e
+    e.close()
+
+
+@pytest.fixture(scope="module")
+def c5_train(orc32):
+    return orc32.synthetic_train(C5["N"], C5["R"], C5["n_total"], 1)
+
+
+def test_c5_negative_sample_bitexact_full(eng, orc32, c5_train):
+    h, r, t = c5_train
+    assert len(h) == 16109182
+    eng.set_triples(h, r, t, C5["N"], C5["R"])
+    gh, gt = eng.negative_sample(1)
+    oh, ot = orc32.negative_sample(h, r, t, C5["N"], C5["R"], 1)
+    assert np.array_equal(gh, oh) and np.array_equal(gt, ot)
+
+
+def test_c5_shape_training_bitexact(eng, orc32, c5_train):
+    """TransE d=256, N=2,500,604, R=535, batch 131,072: three full minibatches and a
+    ragged one (the kernels bench.py times for C5, hrt_forward / segment_backward
+    d=256 instantiations) against the oracle, tables compared bit for bit."""
+    h, r, t = (a[: 3 * C5["B"] + 50000] for a in c5_train)
+    st = orc32.init_store("transe", C5["N"], C5["R"], C5["d"], C5["d"], 1)
+    cfg = ModelConfig.make("transe", C5["d"], C5["d"], "l2")
+    eng.store_upload(cfg, st.entity, st.relation)
+    eng.set_triples(h, r, t, C5["N"], C5["R"])
+    kw = dict(lr=0.05, margin=0.5, batch_size=C5["B"], seed=1)
+    rg = eng.fit(cfg, TrainConfig.make(epochs=1, **kw))
+    ro = orc32.fit("transe", st, h, r, t, orc32.train_config(epochs=1, **kw))
+    assert abs(rg[0].loss - ro[0].loss) <= 1e-5 * max(1.0, abs(ro[0].loss))
+    ge, gr, _, _ = eng.store_download()
+    assert np.array_equal(gr, st.relation)
+    assert np.array_equal(ge, st.entity)
+
+
+def _delta_check(name, before, got, want, tol_frob, tol_rows):
+    dg = got.astype(np.float64) - before
+    do = want.astype(np.float64) - before
+    scale = np.linalg.norm(do)
+    assert scale > 0, f"{name}: the oracle step did not move this table"
+    frob = np.linalg.norm(dg - do) / scale
+    assert frob <= tol_frob, (name, frob)
+    # per row, relative to the row's own delta (rows the step moved)
+    rn = np.linalg.norm(do, axis=1)
+    moved = rn > 0
+    rel = np.linalg.norm(dg - do, axis=1)[moved] / rn[moved]
+    # a hinge term within float rounding of 0 may flip between two correct
+    # implementations; it changes the 3 rows of that pair, never more than 0.1 %
+    assert np.mean(rel > 1e-3) <= tol_rows, (name, float(np.mean(rel > 1e-3)), float(np.max(rel)))
+    # nothing moved that the oracle left in place (up to the 4 rows of one flipped pair)
+    stray = np.any(dg[~moved] != 0, axis=1) if dg.ndim == 2 else dg[~moved] != 0
+    assert int(np.count_nonzero(stray)) <= 4, name
+
+
+@pytest.mark.parametrize("model,N,R,n_total,B", [("transh", 40943, 11, 96483, 16384),
+                                                 ("transr", 123182, 37, 1198932, 65536)])
+def test_ht_backward_deltas_at_config_shape(eng, orc32, model, N, R, n_total, B):
+    """One full C2 / C4 minibatch at lr 100: every table's delta matches the oracle's to
+    1e-3 (Frobenius, relative) and per row, so a missing or wrong backward term fails."""
+    h, r, t = (a[:B] for a in orc32.synthetic_train(N, R, n_total, 1))
+    st = orc32.init_store(model, N, R, 128, 128, 1)
+    if model == "transr":  # off the identity, so the projection and its gradient matter
+        st.proj += np.random.default_rng(2).uniform(-0.05, 0.05, st.proj.shape).astype(np.float32)
+    before = st.copy()
+    cfg = ModelConfig.make(model, 128, 128, "l2")
+    eng.store_upload(cfg, st.entity, st.relation, st.proj, st.normals)
+    eng.set_triples(h, r, t, N, R)
+    kw = dict(lr=100.0, margin=0.5, batch_size=B, seed=1)
+    rg = eng.fit(cfg, TrainConfig.make(epochs=1, **kw))
+    ro = orc32.fit(model, st, h, r, t, orc32.train_config(epochs=1, **kw))
+    assert abs(rg[0].loss - ro[0].loss) <= 1e-5 * max(1.0, abs(ro[0].loss))
+    ge, gr, gp, gn = eng.store_download()
+    _delta_check("entity", before.entity, ge, st.entity, 1e-3, 1e-3)
+    _delta_check("relation", before.relation, gr, st.relation, 1e-3, 0.0)
+    if model == "transr":
+        _delta_check("proj", before.proj, gp, st.proj, 1e-3, 0.0)
+    else:
+        # normals are renormalized after the step: compare the unit rows directly
+        assert np.max(np.abs(gn.astype(np.float64) - st.normals)) <= 1e-5
+        assert np.max(np.abs(gn.astype(np.float64) - before.normals)) > 1e-2  # the step moved them
+
+
+@pytest.mark.parametrize("model,N,R,n_total,B", [("transh", 40943, 11, 96483, 16384),
+                                                 ("transr", 123182, 37, 1198932, 65536)])
+def test_ht_training_is_deterministic(orc32, model, N, R, n_total, B):
+    """Two identical fits (fresh contexts) give identical bytes in every table."""
+    h, r, t = (a[: 3 * B + 1000] for a in orc32.synthetic_train(N, R, n_total, 2))
+    st = orc32.init_store(model, N, R, 128, 128, 2)
+    outs = []
+    for _ in range(2):
+        e = Engine(0)
+        cfg = ModelConfig.make(model, 128, 128, "l2")
+        e.store_upload(cfg, st.entity, st.relation, st.proj, st.normals)
+        e.set_triples(h, r, t, N, R)
+        reps = e.fit(cfg, TrainConfig.make(epochs=2, lr=0.5, batch_size=B, seed=3))
+        outs.append((e.store_download(), [x.loss for x in reps]))
+        e.close()
+    (a, la), (b, lb) = outs
+    assert la == lb
+    for x, y in zip(a, b):
+        if x is not None:
+            assert np.array_equal(x, y)
+
+
+def test_phase_timers_cover_the_epoch(eng, orc32):
+    """EpochReport's PhaseTimer buckets (training.cpp:15-20) come from event nodes in the
+    epoch graph: forward and backward both positive, and together the epoch's device time
+    (test_training.cpp:341-357 asks the buckets to cover >= 95 % of the epoch)."""
+    n, r, d = 3000, 20, 64
+    h, rel, t = orc32.synthetic_train(n, r, 40000, 4)
+    st = orc32.init_store("transe", n, r, d, d, 4)
+    cfg = ModelConfig.make("transe", d, d, "l2")
+    eng.store_upload(cfg, st.entity, st.relation)
+    eng.set_triples(h, rel, t, n, r)
+    eng.negative_sample(4)
+    tc = TrainConfig.make(lr=0.01, batch_size=4096, seed=4)
+    for ep in range(3):
+        rep = eng.train_epoch(cfg, tc, ep, 0.01)
+        assert rep.t_forward_s > 0 and rep.t_backward_s > 0 and rep.t_step_s == 0
+        assert rep.t_forward_s < rep.t_forward_s + rep.t_backward_s
+    eng.set_phase_timers(False)
+    rep2 = eng.train_epoch(cfg, tc, 3, 0.01)
+    assert rep2.t_forward_s == 0 and rep2.t_backward_s > 0
+    eng.set_phase_timers(True)
+    rep3 = eng.train_epoch(cfg, tc, 4, 0.01)
+    assert rep3.t_forward_s > 0
+
+
+def test_graph_is_recaptured_when_the_store_shape_changes(eng, orc32):
+    """the epoch graph bakes strides and the relation offset into its launches;
+    re-uploading a store with another dim / entity count on the same context must not
+    replay the old graph (train d=64, then d=32, then N - 100 entities)."""
+    n, r = 1200, 9
+    h, rel, t = orc32.synthetic_train(n, r, 9000, 8)
+    for d, nn in ((64, n), (32, n), (32, n - 100)):
+        keep = (h < nn) & (t < nn)
+        hh, rr, tt = h[keep], rel[keep], t[keep]
+        st = orc32.init_store("transe", nn, r, d, d, 8)
+        cfg = ModelConfig.make("transe", d, d, "l2")
+        eng.store_upload(cfg, st.entity, st.relation)
+        eng.set_triples(hh, rr, tt, nn, r)
+        kw = dict(lr=0.05, batch_size=1000, seed=2)
+        eng.fit(cfg, TrainConfig.make(epochs=2, **kw))
+        orc32.fit("transe", st, hh, rr, tt, orc32.train_config(epochs=2, **kw))
+        ge, gr, _, _ = eng.store_download()
+        assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation), (d, nn)
