@@ -165,6 +165,29 @@ skg_status skg_build_incidence(skg_ctx* ctx, int32_t layout, int64_t m, const in
                                const int64_t* relations, const int64_t* tails,
                                int64_t num_entities, int64_t num_relations, int64_t* row_ptr,
                                int64_t* col_idx, float* vals, int64_t* nnz);
+/* The reference's generic plus-times sparse layer (sparse.hpp:110-306) on
+ * device, host arrays in and out (int64 indices, fp32 values):
+ *  coo_to_csr (sparse.hpp:110-161): canonical CSR, columns ascending per row,
+ *    duplicates summed left to right in input order (std::sort's order for
+ *    rows of <= 16 entries), exact zeros dropped. row_ptr: num_rows + 1;
+ *    col_idx / out_vals: room for nnz; *out_nnz receives the canonical nnz.
+ *  csr_transpose (sparse.hpp:164-183): stable counting sort over columns.
+ *    t_row_ptr: num_cols + 1; t_col_idx / t_vals: row_ptr[num_rows].
+ *  spmm (sparse.hpp:211-266): out (num_rows x d) = A X, X is x_rows x d.
+ *  spmm_transpose_add (sparse.hpp:273-306): sink (num_cols x d) += A^T G,
+ *    G is g_rows x d; each sink row accumulates over ascending source rows. */
+skg_status skg_coo_to_csr(skg_ctx* ctx, int64_t num_rows, int64_t num_cols, int64_t nnz, const int64_t* rows,
+                          const int64_t* cols, const float* vals, int64_t* row_ptr, int64_t* col_idx,
+                          float* out_vals, int64_t* out_nnz);
+skg_status skg_csr_transpose(skg_ctx* ctx, int64_t num_rows, int64_t num_cols, const int64_t* row_ptr,
+                             const int64_t* col_idx, const float* vals, int64_t* t_row_ptr, int64_t* t_col_idx,
+                             float* t_vals);
+skg_status skg_spmm(skg_ctx* ctx, int64_t num_rows, int64_t num_cols, const int64_t* row_ptr,
+                    const int64_t* col_idx, const float* vals, int64_t x_rows, int64_t d, const float* x,
+                    float* out);
+skg_status skg_spmm_transpose_add(skg_ctx* ctx, int64_t num_rows, int64_t num_cols, const int64_t* row_ptr,
+                                  const int64_t* col_idx, const float* vals, int64_t g_rows, int64_t d,
+                                  const float* g, float* sink);
 /* score_batch, models.cpp:267-289, against the uploaded store. residual
  * (nullable) receives v (TransE/TransH/TransR, m x d_r) or delta (TorusE). */
 skg_status skg_score_batch(skg_ctx* ctx, const skg_model_config* cfg, int64_t m,

@@ -45,6 +45,12 @@ struct CudaError : std::runtime_error {
 
 #define SKG_LAUNCH_CHECK() SKG_CUDA(cudaGetLastError())
 
+__device__ __forceinline__ void stamp_now(unsigned long long* p) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *p = t;
+}
+
 __device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.402823466e38f; }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

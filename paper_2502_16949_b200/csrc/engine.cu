@@ -178,6 +178,12 @@ FwdArgs base_fwd(skg_ctx* ctx) {
   return a;
 }
 
+void set_stamps(skg_ctx* ctx, FwdArgs& fa, int64_t b) {
+  if (!ctx->phase_timers || ctx->stamps.n < 2 * (b + 1)) return;
+  fa.stamp_start = ctx->stamps.p + 2 * b;
+  fa.stamp_end = ctx->stamps.p + 2 * b + 1;
+}
+
 void reset_err(skg_ctx* ctx, cudaStream_t s) {
   SKG_CUDA(cudaMemsetAsync(ctx->err_words.p, 0, sizeof(uint32_t) * 4, s));
   SKG_CUDA(cudaMemsetAsync(ctx->counter.p, 0, sizeof(unsigned), s));
@@ -367,6 +373,7 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
         fa.loss_div = static_cast<float>(Bb);
         fa.margin = ctx->h_lr[1];
         fa.batch = static_cast<int>(b);
+        set_stamps(ctx, fa, b);
         if (ht) {  // TransH / TransR: this rank's gradients into the sink, no in-place step
           BwdArgs hb{};
           hb.X = G;
@@ -447,6 +454,7 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
     fa.unit = 1.0f / static_cast<float>(Bb);  // training.cpp:84
     fa.margin = ctx->h_lr[1];
     fa.batch = static_cast<int>(b);
+    set_stamps(ctx, fa, b);
     BwdArgs ba{};
     ba.X = ctx->tables.p;
     ba.Xrel = ctx->tables.p + ctx->N * ctx->de;
@@ -523,6 +531,12 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   ensure_workspace(ctx, 2 * es.B, es.kind);
   if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, 2 * es.B, ctx->de, ctx->dr, ctx->R));
   ctx->batch_loss.ensure(es.nb);
+  ctx->stamps.ensure(2 * es.nb);
+  if (ctx->h_stamps_cap < es.nb) {
+    if (ctx->h_stamps) cudaFreeHost(ctx->h_stamps);
+    SKG_CUDA(cudaMallocHost(&ctx->h_stamps, sizeof(unsigned long long) * 2 * es.nb));
+    ctx->h_stamps_cap = es.nb;
+  }
   if (ctx->h_loss_cap < es.nb) {
     if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
     SKG_CUDA(cudaMallocHost(&ctx->h_loss, sizeof(float) * es.nb));
@@ -548,7 +562,7 @@ std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
                  ctx->slots[0].order_g.p, ctx->slots[1].order_g.p, ctx->proj.p, ctx->normals.p, margin,
                  // shapes baked into the captured launches (strides, relation offset, plan id space)
                  ctx->N, ctx->R, ctx->de, ctx->dr, ctx->cfg.dim_entity, ctx->proj.n, ctx->normals.n, dp_comm_tag(ctx),
-                 ctx->phase_timers);
+                 ctx->phase_timers, ctx->stamps.p);
 }
 
 // Identity of an epoch plan: everything it depends on.
@@ -563,6 +577,9 @@ void finish_epoch(skg_ctx* ctx, const EpochShape& es, int64_t epoch, skg_epoch_r
                            ctx->stream));
   SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err_words.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost,
                            ctx->stream));
+  if (ctx->phase_timers)
+    SKG_CUDA(cudaMemcpyAsync(ctx->h_stamps, ctx->stamps.p, sizeof(unsigned long long) * 2 * es.nb,
+                             cudaMemcpyDeviceToHost, ctx->stream));
   SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   raise_device_error(ctx->h_err, epoch);
   // training.cpp:141, 163: loss_sum += loss * Real(hi - lo); loss = loss_sum / Real(m)
@@ -593,17 +610,6 @@ void set_slot_seed(skg_ctx* ctx, int slot, uint64_t seed_eff) {
 void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
   const int nxt = 1 - cur;
   const int64_t before = kernel_launches();
-  const int64_t nb_marks = ctx->phase_timers ? 2 * es.nb + 1 : 0;
-  while (static_cast<int64_t>(ctx->phase_ev.size()) < nb_marks) {
-    cudaEvent_t e;
-    SKG_CUDA(cudaEventCreate(&e));
-    ctx->phase_ev.push_back(e);
-  }
-  int64_t marks = 0;
-  const std::function<void()> mark = [&]() {
-    if (marks >= nb_marks) throw CudaError("phase timer: more marks than reserved events");
-    SKG_CUDA(cudaEventRecordWithFlags(ctx->phase_ev[marks++], ctx->stream, cudaEventRecordExternal));
-  };
   cudaGraph_t g = nullptr;
   SKG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   try {
@@ -611,9 +617,7 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
     SKG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
     enqueue_plan(ctx, es, nxt, ctx->side);
     SKG_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
-    if (nb_marks) mark();
-    enqueue_batches(ctx, es, cur, ctx->stream, nb_marks ? &mark : nullptr);
-    if (marks != nb_marks) throw CudaError("phase timer: batch marks do not match the epoch shape");
+    enqueue_batches(ctx, es, cur, ctx->stream, nullptr);
     SKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
   } catch (...) {
     cudaStreamEndCapture(ctx->stream, &g);
@@ -626,7 +630,6 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
   SKG_CUDA(cudaGraphInstantiate(&ctx->graphs[cur], g, 0));
   SKG_CUDA(cudaGraphDestroy(g));
   ctx->graph_launches_k[cur] = kernel_launches() - before;
-  ctx->phase_marks[cur] = nb_marks;
 }
 
 }  // namespace
@@ -740,13 +743,12 @@ void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train
   // the join with the next epoch's plan) is counted in the backward bucket so
   // the buckets sum to the epoch's device time.
   double fwd = 0.0;
-  if (ctx->phase_timers && ctx->phase_marks[ctx->last_slot] == 2 * es.nb + 1) {
+  if (ctx->phase_timers)
     for (int64_t b = 0; b < es.nb; ++b) {
-      float f = 0.f;
-      SKG_CUDA(cudaEventElapsedTime(&f, ctx->phase_ev[2 * b], ctx->phase_ev[2 * b + 1]));
-      fwd += f;
+      const unsigned long long t0 = ctx->h_stamps[2 * b], t1 = ctx->h_stamps[2 * b + 1];
+      if (t1 > t0) fwd += static_cast<double>(t1 - t0) * 1e-6;  // ns -> ms
     }
-  }
+  fwd = std::min<double>(fwd, ms);
   rep->t_forward_s = fwd * 1e-3;
   rep->t_backward_s = std::max(0.0, ms - fwd) * 1e-3;
   rep->t_step_s = 0.0;
@@ -998,7 +1000,7 @@ void skg_destroy(skg_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   dp_destroy(ctx);
   drop_graphs(ctx);
-  for (auto e : ctx->phase_ev) cudaEventDestroy(e);
+  if (ctx->h_stamps) cudaFreeHost(ctx->h_stamps);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->up) {
     cudaStreamSynchronize(ctx->up);
@@ -1512,6 +1514,135 @@ skg_status skg_build_incidence(skg_ctx* ctx, int32_t layout, int64_t m, const in
     }
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
     *nnz = z;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// CsrMatrix::validate (sparse.hpp:54-68) on the host copy: the device kernels
+// index through row_ptr / col_idx, so a malformed matrix is rejected up front.
+void validate_csr(int64_t rows, int64_t cols, const int64_t* rp, const int64_t* ci) {
+  if (rows < 0 || cols < 0) throw ShapeError("csr: negative shape");
+  if (rows > INT32_MAX || cols > INT32_MAX) throw ShapeError("csr: shape exceeds 32-bit device indices");
+  if (rp[0] != 0) throw ShapeError("csr: row_ptr endpoints");
+  for (int64_t r = 0; r < rows; ++r) {
+    if (rp[r] > rp[r + 1]) throw ShapeError("csr: row_ptr decreasing");
+    for (int64_t p = rp[r]; p < rp[r + 1]; ++p)
+      if (ci[p] < 0 || ci[p] >= cols) throw ShapeError("csr: column out of range");
+  }
+  if (rp[rows] > INT32_MAX) throw ShapeError("csr: nnz exceeds 32-bit device indices");
+}
+
+template <class T>
+T* dev_copy(DevBuf<T>& b, const T* host, int64_t n, cudaStream_t s) {
+  b.ensure(n + 1);
+  if (n > 0) SKG_CUDA(cudaMemcpyAsync(b.p, host, sizeof(T) * n, cudaMemcpyHostToDevice, s));
+  return b.p;
+}
+
+}  // namespace
+
+extern "C" {
+
+skg_status skg_coo_to_csr(skg_ctx* ctx, int64_t num_rows, int64_t num_cols, int64_t nnz, const int64_t* rows,
+                          const int64_t* cols, const float* vals, int64_t* row_ptr, int64_t* col_idx,
+                          float* out_vals, int64_t* out_nnz) {
+  return guard(ctx, [&] {
+    if (nnz < 0 || (nnz > 0 && (!rows || !cols || !vals))) throw ShapeError("coo: rows/cols/vals length mismatch");
+    for (int64_t i = 0; i < nnz; ++i)  // CooMatrix::validate (sparse.hpp:30-37)
+      if (rows[i] < 0 || rows[i] >= num_rows || cols[i] < 0 || cols[i] >= num_cols)
+        throw ShapeError("coo: entry " + std::to_string(i) + " outside declared shape");
+    if (num_rows > INT32_MAX || num_cols > INT32_MAX || nnz > INT32_MAX)
+      throw ShapeError("coo: shape exceeds 32-bit device indices");
+    DevBuf<int64_t> dr, dc, orp, oc;
+    DevBuf<float> dv, ov;
+    const int64_t* r = dev_copy(dr, rows, nnz, ctx->stream);
+    const int64_t* c = dev_copy(dc, cols, nnz, ctx->stream);
+    const float* v = dev_copy(dv, vals, nnz, ctx->stream);
+    orp.ensure(num_rows + 1);
+    oc.ensure(nnz + 1);
+    ov.ensure(nnz + 1);
+    int64_t z = 0;
+    sparse_coo_to_csr(num_rows, num_cols, nnz, r, c, v, orp.p, oc.p, ov.p, &z, ctx->stream);
+    SKG_CUDA(cudaMemcpyAsync(row_ptr, orp.p, sizeof(int64_t) * (num_rows + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    if (z > 0) {
+      SKG_CUDA(cudaMemcpyAsync(col_idx, oc.p, sizeof(int64_t) * z, cudaMemcpyDeviceToHost, ctx->stream));
+      SKG_CUDA(cudaMemcpyAsync(out_vals, ov.p, sizeof(float) * z, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out_nnz = z;
+  });
+}
+
+skg_status skg_csr_transpose(skg_ctx* ctx, int64_t num_rows, int64_t num_cols, const int64_t* row_ptr,
+                             const int64_t* col_idx, const float* vals, int64_t* t_row_ptr, int64_t* t_col_idx,
+                             float* t_vals) {
+  return guard(ctx, [&] {
+    validate_csr(num_rows, num_cols, row_ptr, col_idx);
+    const int64_t nnz = row_ptr[num_rows];
+    DevBuf<int64_t> drp, dc, trp, tc;
+    DevBuf<float> dv, tv;
+    const int64_t* rp = dev_copy(drp, row_ptr, num_rows + 1, ctx->stream);
+    const int64_t* c = dev_copy(dc, col_idx, nnz, ctx->stream);
+    const float* v = dev_copy(dv, vals, nnz, ctx->stream);
+    trp.ensure(num_cols + 1);
+    tc.ensure(nnz + 1);
+    tv.ensure(nnz + 1);
+    sparse_transpose(num_rows, num_cols, nnz, rp, c, v, trp.p, tc.p, tv.p, ctx->stream);
+    SKG_CUDA(cudaMemcpyAsync(t_row_ptr, trp.p, sizeof(int64_t) * (num_cols + 1), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    if (nnz > 0) {
+      SKG_CUDA(cudaMemcpyAsync(t_col_idx, tc.p, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+      SKG_CUDA(cudaMemcpyAsync(t_vals, tv.p, sizeof(float) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_spmm(skg_ctx* ctx, int64_t num_rows, int64_t num_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                    const float* vals, int64_t x_rows, int64_t d, const float* x, float* out) {
+  return guard(ctx, [&] {
+    if (num_cols != x_rows)  // sparse.hpp:244-246
+      throw ShapeError("spmm: inner dimensions " + std::to_string(num_cols) + " vs " + std::to_string(x_rows));
+    validate_csr(num_rows, num_cols, row_ptr, col_idx);
+    if (d < 0 || d > INT32_MAX) throw ShapeError("spmm: bad dense width");
+    const int64_t nnz = row_ptr[num_rows];
+    DevBuf<int64_t> drp, dc;
+    DevBuf<float> dv, dx, dout;
+    const int64_t* rp = dev_copy(drp, row_ptr, num_rows + 1, ctx->stream);
+    const int64_t* c = dev_copy(dc, col_idx, nnz, ctx->stream);
+    const float* v = dev_copy(dv, vals, nnz, ctx->stream);
+    const float* X = dev_copy(dx, x, x_rows * d, ctx->stream);
+    dout.ensure(num_rows * d + 1);
+    sparse_spmm(num_rows, rp, c, v, static_cast<int>(d), X, dout.p, ctx->num_sms, ctx->stream);
+    if (num_rows * d > 0)
+      SKG_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(float) * num_rows * d, cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+skg_status skg_spmm_transpose_add(skg_ctx* ctx, int64_t num_rows, int64_t num_cols, const int64_t* row_ptr,
+                                  const int64_t* col_idx, const float* vals, int64_t g_rows, int64_t d,
+                                  const float* g, float* sink) {
+  return guard(ctx, [&] {
+    if (num_rows != g_rows) throw ShapeError("spmm_transpose: row count mismatch");  // sparse.hpp:275
+    validate_csr(num_rows, num_cols, row_ptr, col_idx);
+    if (d < 0 || d > INT32_MAX) throw ShapeError("spmm_transpose: bad dense width");
+    const int64_t nnz = row_ptr[num_rows];
+    DevBuf<int64_t> drp, dc;
+    DevBuf<float> dv, dg, ds;
+    const int64_t* rp = dev_copy(drp, row_ptr, num_rows + 1, ctx->stream);
+    const int64_t* c = dev_copy(dc, col_idx, nnz, ctx->stream);
+    const float* v = dev_copy(dv, vals, nnz, ctx->stream);
+    const float* G = dev_copy(dg, g, g_rows * d, ctx->stream);
+    float* S = dev_copy(ds, static_cast<const float*>(sink), num_cols * d, ctx->stream);
+    sparse_spmm_transpose_add(num_rows, num_cols, nnz, rp, c, v, static_cast<int>(d), G, S, ctx->num_sms,
+                              ctx->stream);
+    if (num_cols * d > 0)
+      SKG_CUDA(cudaMemcpyAsync(sink, S, sizeof(float) * num_cols * d, cudaMemcpyDeviceToHost, ctx->stream));
+    SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

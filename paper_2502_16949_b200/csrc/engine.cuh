@@ -115,12 +115,13 @@ struct skg_ctx {
   int64_t graph_launches_k[2] = {0, 0};
   int64_t last_launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // PhaseTimer buckets (training.cpp:15-20) inside the epoch graph: external
-  // event-record nodes at the start of the batches and after every batch's
-  // forward and backward (2 * nb + 1 events, reused by every capture).
+  // PhaseTimer buckets (training.cpp:15-20): every batch's forward kernels
+  // stamp their start and end (globaltimer) into `stamps`, read back with the
+  // batch losses. No extra graph nodes.
   bool phase_timers = true;
-  std::vector<cudaEvent_t> phase_ev;
-  int64_t phase_marks[2] = {0, 0};  // events each captured graph records
+  skg::DevBuf<unsigned long long> stamps;  // [2 * nb]: forward start, forward end
+  unsigned long long* h_stamps = nullptr;  // pinned
+  int64_t h_stamps_cap = 0;
   double last_epoch_ms = 0;  // device time of the last graph epoch (ev0 -> ev1)
 
   // ---- deferred id uploads (speculative epoch). A re-upload of pinned arrays

@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
   extern __shared__ float4 smem4[];
   __shared__ float warp_loss[kWarps];
   if (a.err[0] != 0) return;  // sticky error: nothing runs after the failing batch
+  if (a.stamp_start && blockIdx.x == 0 && threadIdx.x == 0) stamp_now(a.stamp_start);
   float* smem = reinterpret_cast<float*>(smem4);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = a.de;
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
     if (lane == 0) {
       const float loss = __fdiv_rn(acc, a.loss_div > 0.f ? a.loss_div : static_cast<float>(a.B));  // training.cpp:93
       a.batch_loss[a.batch] = loss;
+      if (a.stamp_end) stamp_now(a.stamp_end);
       const uint32_t pflags = atomicOr(&a.err[3], 0u);
       if (!(fabsf(loss) <= 3.402823466e38f)) {
         a.err[1] = a.batch;

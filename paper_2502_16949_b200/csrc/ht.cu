@@ -98,6 +98,7 @@ __device__ void finalize_loss(const FwdArgs& a, float lsum, float* warp_loss) {
     if (lane == 0) {
       const float loss = __fdiv_rn(acc, static_cast<float>(a.B));
       a.batch_loss[a.batch] = loss;
+      if (a.stamp_end) stamp_now(a.stamp_end);
       const uint32_t pflags = atomicOr(&a.err[3], 0u);
       if (nonfinite(loss)) {
         a.err[1] = a.batch;
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(kHtThreads) transh_forward_kernel(const FwdArg
   extern __shared__ float4 sm4[];
   __shared__ float warp_loss[kHtThreads / 32];
   if (a.err[0] != 0) return;
+  if (a.stamp_start && blockIdx.x == 0 && threadIdx.x == 0) stamp_now(a.stamp_start);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int d = a.de;
   const int dv = d / VEC;

@@ -68,6 +68,11 @@ struct FwdArgs {
   float* batch_loss;  // slot for this batch
   int batch;
   uint32_t* err;
+  // PhaseTimer stamps (globaltimer ns, training.cpp:15-20): the batch's first
+  // forward kernel writes stamp_start from its first block, the last block of
+  // the loss reduction writes stamp_end. Null: no stamps.
+  unsigned long long* stamp_start;
+  unsigned long long* stamp_end;
 };
 
 struct BwdArgs {
@@ -94,5 +99,17 @@ void launch_hrt_forward(int kind, bool train, const FwdArgs& a, int num_sms, cud
 void launch_segment_backward(int kind, bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s);
 void configure_mult_kernels();
 void launch_mult_forward(int kind, bool train, const FwdArgs& a, int num_sms, cudaStream_t s);
+
+// Generic plus-times sparse operators (sparse_ops.cu; sparse.hpp:110-306), device buffers.
+void sparse_coo_to_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* d_rows, const int64_t* d_cols,
+                       const float* d_vals, int64_t* d_row_ptr, int64_t* d_col, float* d_val, int64_t* nnz_out,
+                       cudaStream_t s);
+void sparse_transpose(int64_t rows, int64_t cols, int64_t nnz, const int64_t* d_row_ptr, const int64_t* d_col,
+                      const float* d_val, int64_t* d_trow_ptr, int64_t* d_tcol, float* d_tval, cudaStream_t s);
+void sparse_spmm(int64_t rows, const int64_t* d_row_ptr, const int64_t* d_col, const float* d_val, int d,
+                 const float* d_x, float* d_out, int num_sms, cudaStream_t s);
+void sparse_spmm_transpose_add(int64_t rows, int64_t cols, int64_t nnz, const int64_t* d_row_ptr,
+                               const int64_t* d_col, const float* d_val, int d, const float* d_g, float* d_sink,
+                               int num_sms, cudaStream_t s);
 
 }  // namespace skg

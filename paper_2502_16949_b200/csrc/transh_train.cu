@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transh_tile_kernel(const
   __shared__ RelTiles rt;
   const FwdArgs& f = a.f;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (f.stamp_start && blockIdx.x == 0 && tid == 0) stamp_now(f.stamp_start);
   const bool alive = f.err[0] == 0;
   if (warp == 0 && alive) enumerate_rel_tiles(a, rt);
   __syncthreads();
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transh_tile_kernel(const
     if (lane == 0) {
       const float loss = __fdiv_rn(acc, f.loss_div > 0.f ? f.loss_div : static_cast<float>(f.B));
       f.batch_loss[f.batch] = loss;
+      if (f.stamp_end) stamp_now(f.stamp_end);
       const uint32_t pflags = atomicOr(&f.err[3], 0u);
       if (nonfinite(loss)) {
         f.err[1] = f.batch;

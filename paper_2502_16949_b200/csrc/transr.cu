@@ -61,8 +61,9 @@ __global__ void __launch_bounds__(kTilesThreads) transr_tiles_kernel(
     const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ seg_col, const uint32_t* __restrict__ seg_base,
     int batch, int64_t N, int paired, uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_p0,
     uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles, const uint32_t* __restrict__ err,
-    uint32_t* __restrict__ zero = nullptr, int nzero = 0) {
+    uint32_t* __restrict__ zero = nullptr, int nzero = 0, unsigned long long* stamp = nullptr) {
   __shared__ uint32_t wsum[kTilesThreads / 32];
+  if (stamp && threadIdx.x == 0) stamp_now(stamp);
   for (int i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0u;  // per-relation tickets of the next kernel
   __shared__ uint32_t carry_t, nrel;
   __shared__ int stop;
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(kTrThreads, 1) transr_tile_kernel(const TrArgs
   __shared__ float tile_loss;
   const FwdArgs& f = a.f;
   if (f.err[0] != 0) return;
+  if (f.stamp_start && blockIdx.x == 0 && threadIdx.x == 0) stamp_now(f.stamp_start);
   const int de = f.de, dr = f.dr;
   const int SE = de + 1, SR = dr + 1;
   float* Ms = smem;                 // dr x SE
@@ -380,6 +382,7 @@ __global__ void __launch_bounds__(kTrThreads, 1) transr_tile_kernel(const TrArgs
     if (tid == 0) {
       const float loss = __fdiv_rn(acc, static_cast<float>(f.B));
       f.batch_loss[f.batch] = loss;
+      if (f.stamp_end) stamp_now(f.stamp_end);
       const uint32_t pflags = atomicOr(&f.err[3], 0u);
       if (nonfinite(loss)) {
         f.err[1] = f.batch;
@@ -552,10 +555,13 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
   float* rel_dst = sinks ? sinks->rel : const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
   if (transr_tc_supported(fa.de, fa.dr)) {
     transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, 1,
-                                                    w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err);
+                                                    w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err,
+                                                    nullptr, 0, fa.stamp_start);
     count_launch();
     SKG_LAUNCH_CHECK();
-    launch_transr_train_tc(kind == kTransR_L2, fa, ba.ent_val, ba.seg_start, ba.seg_col, w.tile_seg, w.tile_p0,
+    FwdArgs fa_tc = fa;
+    fa_tc.stamp_start = nullptr;  // stamped by the tiles kernel, the batch's first launch
+    launch_transr_train_tc(kind == kTransR_L2, fa_tc, ba.ent_val, ba.seg_start, ba.seg_col, w.tile_seg, w.tile_p0,
                            w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, w.mr_chunks, R, num_sms, s,
                            sinks != nullptr);
     if (mark) (*mark)();

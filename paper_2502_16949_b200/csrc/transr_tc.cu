@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
     if (lane == 0) {
       const float loss = __fdiv_rn(acc, static_cast<float>(f.B));
       f.batch_loss[f.batch] = loss;
+      if (f.stamp_end) stamp_now(f.stamp_end);
       const uint32_t pflags = atomicOr(&f.err[3], 0u);
       if (nonfinite(loss)) {
         f.err[1] = f.batch;

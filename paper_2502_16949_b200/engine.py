@@ -97,6 +97,10 @@ def load_library():
         "skg_epoch_order": [vp, i64, C.c_uint64, i32, i64, vp],
         "skg_build_incidence": [vp, i32, i64, vp, vp, vp, i64, i64, vp, vp, vp, vp],
         "skg_score_batch": [vp, vp, i64, vp, vp, vp, vp, vp],
+        "skg_coo_to_csr": [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp],
+        "skg_csr_transpose": [vp, i64, i64, vp, vp, vp, vp, vp, vp],
+        "skg_spmm": [vp, i64, i64, vp, vp, vp, i64, i64, vp, vp],
+        "skg_spmm_transpose_add": [vp, i64, i64, vp, vp, vp, i64, i64, vp, vp],
         "skg_score_backward": [vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp],
         "skg_margin_ranking_loss": [vp, i64, vp, vp, f32, vp, vp, vp],
         "skg_train_epoch": [vp, vp, vp, i64, f32, vp],
@@ -240,6 +244,44 @@ class Engine:
                                                num_entities, num_relations, _p(rp), _p(col), _p(val),
                                                C.byref(nnz)))
         return rp, col[:nnz.value].copy(), val[:nnz.value].copy()
+
+    def coo_to_csr(self, rows, cols, ri, ci, vi):
+        """coo_to_csr (sparse.hpp:110-161) -> (row_ptr, col_idx, vals)."""
+        ri, ci, vi = _i64(ri), _i64(ci), _f32(vi)
+        n = len(ri)
+        rp = np.empty(rows + 1, np.int64)
+        col = np.empty(max(1, n), np.int64)
+        val = np.empty(max(1, n), np.float32)
+        nnz = C.c_int64()
+        self._check(self.L.skg_coo_to_csr(self.h, rows, cols, n, _p(ri), _p(ci), _p(vi), _p(rp), _p(col), _p(val),
+                                          C.byref(nnz)))
+        return rp, col[:nnz.value].copy(), val[:nnz.value].copy()
+
+    def transpose(self, rows, cols, rp, ci, v):
+        """transpose (sparse.hpp:164-183) of a CSR matrix -> (row_ptr, col_idx, vals)."""
+        rp, ci, v = _i64(rp), _i64(ci), _f32(v)
+        nnz = int(rp[rows]) if len(rp) > rows else 0
+        orp = np.empty(cols + 1, np.int64)
+        oci = np.empty(max(1, nnz), np.int64)
+        ov = np.empty(max(1, nnz), np.float32)
+        self._check(self.L.skg_csr_transpose(self.h, rows, cols, _p(rp), _p(ci), _p(v), _p(orp), _p(oci), _p(ov)))
+        return orp, oci[:nnz].copy(), ov[:nnz].copy()
+
+    def spmm(self, rows, cols, rp, ci, v, x):
+        """spmm (sparse.hpp:242-266), plus-times: A (rows x cols) times x (cols x d)."""
+        rp, ci, v, x = _i64(rp), _i64(ci), _f32(v), _f32(x)
+        out = np.empty((rows, x.shape[1]), np.float32)
+        self._check(self.L.skg_spmm(self.h, rows, cols, _p(rp), _p(ci), _p(v), x.shape[0], x.shape[1], _p(x),
+                                    _p(out)))
+        return out
+
+    def spmm_transpose_add(self, rows, cols, rp, ci, v, g, sink):
+        """spmm_transpose_add (sparse.hpp:273-306): sink (cols x d) += A^T g, in place."""
+        rp, ci, v, g = _i64(rp), _i64(ci), _f32(v), _f32(g)
+        assert sink.dtype == np.float32 and sink.flags.c_contiguous
+        self._check(self.L.skg_spmm_transpose_add(self.h, rows, cols, _p(rp), _p(ci), _p(v), g.shape[0], g.shape[1],
+                                                  _p(g), _p(sink)))
+        return sink
 
     def score_batch(self, cfg: ModelConfig, h, r, t, residual=False):
         h, r, t = _i64(h), _i64(r), _i64(t)

@@ -160,7 +160,7 @@ def test_graph_is_recaptured_when_the_store_shape_changes(eng, orc32):
     re-uploading a store with another dim / entity count on the same context must not
     replay the old graph (train d=64, then d=32, then N - 100 entities)."""
     n, r = 1200, 9
-    h, rel, t = orc32.synthetic_train(n, r, 9000, 8)
+    h, rel, t = orc32.synthetic_train(n, r, 6000, 8)
     for d, nn in ((64, n), (32, n), (32, n - 100)):
         keep = (h < nn) & (t < nn)
         hh, rr, tt = h[keep], rel[keep], t[keep]
