@@ -296,8 +296,11 @@ def test_lr0_freezes(eng, orc32):
     assert rep.loss > 0 and np.array_equal(eng.store_download()[0], st.entity)
 
 
-def test_cpp_shim_drop_in_runs():
-    """A reference-style C++ caller runs unchanged over the shim + C ABI."""
+@pytest.mark.parametrize("name", ["shim_drop_in", "ref_cases"])
+def test_cpp_shim_drop_in_runs(name):
+    """A reference-style C++ caller, and the reference's own unit-test case bodies
+    (test_models / test_training / test_embedding / test_sparse / test_incidence,
+    adapted to fp32, tests/cpp/ref_cases.cpp), run over the shim + C ABI."""
     import os
     import subprocess
     import tempfile
@@ -306,7 +309,7 @@ def test_cpp_shim_drop_in_runs():
     with tempfile.TemporaryDirectory() as d:
         exe = os.path.join(d, "shim")
         subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"),
-                        os.path.join(root, "tests", "cpp", "shim_drop_in.cpp"), "-o", exe, "-L", lib,
+                        os.path.join(root, "tests", "cpp", name + ".cpp"), "-o", exe, "-L", lib,
                         "-lskge_b200", f"-Wl,-rpath,{lib}"], check=True)
         out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
         assert out.returncode == 0, out.stdout + out.stderr

@@ -41,11 +41,13 @@ def test_create_without_gpu_fails_loudly():
     assert e.value.kind == "CudaError"
 
 
-def test_cpp_shim_compiles():
-    """The reference-signature C++ shim (include/skge_b200.hpp) compiles against the ABI."""
+@pytest.mark.parametrize("name", ["shim_drop_in", "ref_cases"])
+def test_cpp_shim_compiles(name):
+    """The reference-signature C++ shim (include/skge_b200.hpp) compiles against the ABI, with
+    a reference-style caller and with the adapted reference unit-test case bodies."""
     import subprocess
     import tempfile
-    src = os.path.join(ROOT, "tests", "cpp", "shim_drop_in.cpp")
+    src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "shim")
         subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", out,
