@@ -374,6 +374,20 @@ inline void upload(const ModelConfig& mc, const EmbeddingStore& s) {
   check(skg_store_upload(ctx(), &c, s.num_entities(), s.num_relations(), s.entity.data(), s.relation.data(),
                          s.has_proj() ? s.proj.data() : nullptr, s.has_normals() ? s.normals.data() : nullptr));
 }
+// models.hpp:65-76 (the C ABI checks the same against the uploaded store; the
+// batch's own id space is only visible here)
+inline void check_config(const ModelConfig& cfg, const EmbeddingStore& store, const TripleBatch& b) {
+  cfg.validate();
+  const Index w = is_complex_model(cfg.model) ? 2 : 1;
+  if (store.dim_entity() != w * cfg.dim_entity || store.dim_relation() != w * cfg.dim_relation)
+    throw ConfigError("store dimensions do not match the model config");
+  if (store.num_entities() != b.num_entities || store.num_relations() != b.num_relations)
+    throw ConfigError("store table sizes do not match the batch id space");
+  if (cfg.model == ModelKind::TransR && !store.has_proj())
+    throw ConfigError("transr store is missing the projection table");
+  if (cfg.model == ModelKind::TransH && !store.has_normals())
+    throw ConfigError("transh store is missing the hyperplane normals");
+}
 // sgd_step / renormalize_entities take no ModelConfig (embedding.hpp:127-132):
 // the table set decides the tag the device store is uploaded under.
 inline void upload_tables(const EmbeddingStore& s) {
@@ -548,6 +562,7 @@ inline LossGrad margin_ranking_loss(const RealVector& pos, const RealVector& neg
 // models.cpp:267-289: scores, the incidence operand and the residual rows the
 // backward pass reads (v / delta from the device forward; u = h - t, exact).
 inline ScoreBatch score_batch(const ModelConfig& cfg, const EmbeddingStore& store, const TripleBatch& b) {
+  detail::check_config(cfg, store, b);
   detail::upload(cfg, store);
   skg_model_config c = detail::cfg(cfg);
   ScoreBatch sb;
@@ -595,6 +610,7 @@ inline ScoreBatch score_batch(const ModelConfig& cfg, const EmbeddingStore& stor
 inline void score_backward(const ModelConfig& cfg, const EmbeddingStore& store, const ScoreBatch& sb,
                            const RealVector& upstream, Gradients& grads) {
   const TripleBatch& b = sb.batch;
+  detail::check_config(cfg, store, b);
   if (upstream.size() != b.size()) throw ShapeError("score_backward: upstream length does not match the batch");
   detail::upload(cfg, store);
   skg_model_config c = detail::cfg(cfg);
