@@ -282,6 +282,35 @@ skg_status skg_dp_init(skg_ctx* ctx, const char unique_id[128], int rank, int wo
  * the epoch, minibatches}. */
 skg_status skg_dp_shard(int64_t m, int64_t batch_size, int32_t world, int32_t rank, int64_t* out);
 
+/* ---- row-sharded data parallel (wikikg2-scale tables) ---------
+ * TransE / TorusE. The entity table is split by owner (entity e on rank e % G,
+ * G in {1, 2, 4, 8}) and the relation table replicated; each global minibatch
+ * (training.cpp:120-161 at batch_size = global batch) is split into G pair
+ * shards. Per batch every rank runs the forward of its shard, gathering entity
+ * rows from their owners over NVLink; after a barrier every rank reduces the
+ * columns it owns over the WHOLE global batch in the reference's order
+ * (pulling residual rows from the ranks that computed them) and applies SGD;
+ * relation owners write the new row into every replica; a second barrier.
+ * Results equal the single-device run at batch_size = global batch bit for
+ * bit (tables; the loss within 1e-5: shard losses are summed per rank).
+ * Set up after store upload, triples and negatives; batch_size is the GLOBAL
+ * batch and must be a multiple of G. skg_store_download gathers the full
+ * tables from all ranks; skg_store_upload re-scatters.
+ *
+ * One process driving all ranks (contexts on distinct GPUs, or on one GPU):
+ *   skg_shard_group_init + skg_shard_group_train_epoch (ctxs[k] = rank k).
+ * One process per GPU: skg_shard_export (this rank's IPC handle) on every
+ * rank, an all-gather of the handles by the caller, skg_shard_import (all G
+ * handles, rank order); then skg_train_epoch / skg_fit run sharded. */
+#define SKG_SHARD_HANDLE_BYTES 128
+skg_status skg_shard_group_init(skg_ctx* const* ctxs, int world, int64_t batch_size);
+skg_status skg_shard_group_train_epoch(skg_ctx* const* ctxs, int world, const skg_model_config* cfg,
+                                       const skg_train_config* tc, int64_t epoch, float lr,
+                                       skg_epoch_report* reports);
+skg_status skg_shard_export(skg_ctx* ctx, int rank, int world, int64_t batch_size, void* handle);
+skg_status skg_shard_import(skg_ctx* ctx, const void* handles);
+skg_status skg_shard_release(skg_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

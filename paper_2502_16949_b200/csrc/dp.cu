@@ -40,8 +40,8 @@ void dp_destroy(skg_ctx* ctx) {
   ctx->dp = nullptr;
 }
 
-int dp_rank(const skg_ctx* ctx) { return ctx->dp ? ctx->dp->rank : 0; }
-int dp_world(const skg_ctx* ctx) { return ctx->dp ? ctx->dp->world : 1; }
+int dp_rank(const skg_ctx* ctx) { return ctx->dp ? ctx->dp->rank : ctx->shard ? shard_rank(ctx) : 0; }
+int dp_world(const skg_ctx* ctx) { return ctx->dp ? ctx->dp->world : ctx->shard ? shard_world(ctx) : 1; }
 const void* dp_comm_tag(const skg_ctx* ctx) { return ctx->dp ? static_cast<const void*>(ctx->dp->comm) : nullptr; }
 
 void dp_allreduce_sum(skg_ctx* ctx, float* buf, int64_t n, cudaStream_t s) {

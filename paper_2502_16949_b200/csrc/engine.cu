@@ -14,6 +14,7 @@
 #include "engine.cuh"
 #include "ht.cuh"
 #include "primitives.cuh"
+#include "shard.cuh"
 
 using namespace skg;
 
@@ -202,6 +203,7 @@ void raise_device_error(const uint32_t* w, int64_t epoch) {
     case kErrGradNormals: throw TrainingError("non-finite gradient in hyperplane normals");
     case kErrNormalCollapsed:
       throw TrainingError("hyperplane normal " + std::to_string(w[2]) + " collapsed to zero");
+    case 8u: throw CudaError("sharded data parallel: a peer rank did not reach the barrier within 20 s");
     default: throw CudaError("device error word " + std::to_string(w[0]));
   }
 }
@@ -295,6 +297,49 @@ __global__ void dp_sgd_kernel(float* __restrict__ X, const float* __restrict__ G
 void enqueue_plan(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s);
 void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s,
                      const std::function<void()>* markp);
+void enqueue_shard_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s,
+                           const std::function<void()>* markp);
+
+// Row-sharded epoch (shard.cu): per global batch, the forward of this rank's
+// pair shard (entity rows gathered from their owners over NVLink), a barrier,
+// the owner-side reduce + SGD of the columns this rank owns (residual rows
+// pulled from the ranks that computed them), a barrier.
+void enqueue_shard_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s,
+                           const std::function<void()>* markp) {
+  auto mark = [&]() {
+    if (markp) (*markp)();
+  };
+  ShardState* st = ctx->shard;
+  const ShardPlanBufs& sp = st->plan[slot];
+  reset_err(ctx, s);
+  SKG_CUDA(cudaMemsetAsync(st->peers.loss[st->rank], 0, sizeof(float) * es.nb, s));
+  const int64_t nb_run = es.nb_run >= 0 ? es.nb_run : es.nb;
+  for (int64_t b = 0; b < nb_run; ++b) {
+    const int64_t lo = b * es.B;
+    const int64_t Bb = std::min(es.B, ctx->M - lo);
+    const int64_t Sb = b < es.nb - 1 ? es.S : es.s_last;
+    if (Sb > 0) {
+      FwdArgs fa = base_fwd(ctx);
+      shard_fill_fwd(ctx, fa);
+      fa.pair_ht = sp.pair_ht + b * es.S;
+      fa.pair_r = sp.pair_r + b * es.S;
+      fa.B = static_cast<int>(Sb);
+      fa.unit = 1.0f / static_cast<float>(Bb);  // training.cpp:84 with the global batch
+      fa.loss_div = static_cast<float>(Bb);
+      fa.margin = ctx->h_lr[1];
+      fa.batch = static_cast<int>(b);
+      set_stamps(ctx, fa, b);
+      launch_hrt_forward(es.kind, true, fa, ctx->num_sms, s);
+    }
+    mark();
+    shard_barrier(ctx, s);
+    shard_backward(ctx, es.kind, slot, b, s);
+    shard_barrier(ctx, s);
+    mark();
+  }
+  shard_finish_losses(ctx, es.nb, s);
+  shard_barrier(ctx, s);  // every rank has read the shard losses before any rank clears them
+}
 
 void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>* ev) {
   cudaStream_t s = ctx->stream;
@@ -321,6 +366,14 @@ void enqueue_plan(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s) 
     device_shuffle(seed, ctx->M, ps.order.p, ctx->shuffle, s);
   else
     device_iota(ps.order.p, ctx->M, s);
+  if (ctx->shard) {  // this rank's forward pairs + the owned-column plan of the global batches
+    shard_order_kernel<<<grid_for(es.Mg), 256, 0, s>>>(ps.order.p, es.B, es.S, es.rank, es.nb, es.i0_last, es.Mg,
+                                                        ps.order_g.p);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+    shard_build_plan(ctx, ps.order.p, ps.order_g.p, es.Mg, slot, s);
+    return;
+  }
   if (es.world > 1 || ctx->dp != nullptr) {
     shard_order_kernel<<<grid_for(es.Mg), 256, 0, s>>>(ps.order.p, es.B, es.S, es.rank, es.nb, es.i0_last, es.Mg,
                                                         ps.order_g.p);
@@ -338,6 +391,10 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
   auto mark = [&]() {
     if (markp) (*markp)();
   };
+  if (ctx->shard) {
+    enqueue_shard_batches(ctx, es, slot, s, markp);
+    return;
+  }
   PlanSlot& ps = ctx->slots[slot];
   const bool dp = es.world > 1 || ctx->dp != nullptr;
   reset_err(ctx, s);
@@ -498,16 +555,25 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   check_config(ctx, cfg, ctx->tN, ctx->tR);
   if (ctx->M < 1) throw ConfigError("training requires at least one triple");
   if (!ctx->has_neg) throw ShapeError("negative set is not aligned with the positive triples");
-  es.B = std::min<int64_t>(tc.batch_size, ctx->M);
   es.nb = (ctx->M + tc.batch_size - 1) / tc.batch_size;
-  es.B = tc.batch_size < ctx->M ? tc.batch_size : ctx->M;
+  // data parallel keeps the configured global batch (a single short batch is
+  // the ragged last one of the shard geometry)
+  es.B = (ctx->dp || ctx->shard) ? tc.batch_size : std::min<int64_t>(tc.batch_size, ctx->M);
   if (es.B > (1 << 30)) throw ConfigError("batch_size too large for 32-bit row ids");
   es.shuffle = tc.shuffle != 0;
   es.kind = kind_of(cfg);
   ctx->order.ensure(ctx->M);
   es.world = dp_world(ctx);
   es.rank = dp_rank(ctx);
-  if (ctx->dp) {
+  if (ctx->shard) {
+    if (es.kind != kTransE_L2 && es.kind != kTransE_L1 && es.kind != kTorusE_L2 && es.kind != kTorusE_L1)
+      throw ConfigError("sharded data parallel covers the hrt models (transe, toruse)");
+    if (tc.batch_size != ctx->shard->B)
+      throw ConfigError("sharded context was initialised for batch_size " + std::to_string(ctx->shard->B));
+    if (es.nb > ctx->shard->nb_cap) throw ConfigError("sharded context: triples changed size since init");
+    if (!ctx->shard->linked) throw ConfigError("sharded context: peers not linked");
+  }
+  if (ctx->dp || ctx->shard) {
     if (es.B % es.world != 0) throw ConfigError("data parallel: global batch_size must be a multiple of the world size");
     int64_t sh[5];
     dp_shard(ctx->M, es.B, es.world, es.rank, sh);
@@ -516,17 +582,21 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
     es.s_last = sh[2];
     es.Mg = sh[3];
     for (auto& sl : ctx->slots) sl.order_g.ensure(es.Mg + 1);
-    ctx->dp_grad.ensure(ctx->N * ctx->de + ctx->R * ctx->dr + ctx->proj.n + ctx->normals.n + 2);
+    if (ctx->dp) ctx->dp_grad.ensure(ctx->N * ctx->de + ctx->R * ctx->dr + ctx->proj.n + ctx->normals.n + 2);
   }
   for (auto& sl : ctx->slots) {
     sl.order.ensure(ctx->M + 1);
-    sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
+    if (!ctx->shard) sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
   }
   ctx->shuffle.reserve(ctx->M);
   if (ctx->quad_version != ctx->data_version || ctx->quad.n < ctx->M + 1) {  // packed ids for the plan
     ctx->quad.ensure(ctx->M + 1);
     pack_triple_quads(ctx->H.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->M, ctx->quad.p, ctx->stream);
     ctx->quad_version = ctx->data_version;
+  }
+  if (ctx->shard) {  // plan buffers of both slots sized before any capture (owned entries per epoch are fixed)
+    const int64_t E = shard_entry_count(ctx);
+    for (auto& p : ctx->shard->plan) p.reserve(es.Mg, 2 * ctx->M, E, es.nb);
   }
   ensure_workspace(ctx, 2 * es.B, es.kind);
   if (is_ht(cfg)) ctx->ht_work.ensure(ht_work_floats(es.kind, 2 * es.B, ctx->de, ctx->dr, ctx->R));
@@ -562,7 +632,7 @@ std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
                  ctx->slots[0].order_g.p, ctx->slots[1].order_g.p, ctx->proj.p, ctx->normals.p, margin,
                  // shapes baked into the captured launches (strides, relation offset, plan id space)
                  ctx->N, ctx->R, ctx->de, ctx->dr, ctx->cfg.dim_entity, ctx->proj.n, ctx->normals.n, dp_comm_tag(ctx),
-                 ctx->phase_timers, ctx->stamps.p);
+                 ctx->phase_timers, ctx->stamps.p, ctx->shard, shard_tag(ctx));
 }
 
 // Identity of an epoch plan: everything it depends on.
@@ -689,22 +759,35 @@ bool has_self_loops(skg_ctx* ctx) {
                               ": head == tail is not representable in the multiplicative incidence layout");
 }
 
-void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
-                      int64_t epoch, float lr, skg_epoch_report* rep,
-                      const std::function<void()>* after_launch = nullptr) {
-  EpochShape es{};
+// One epoch in three steps, so a driver of several sharded contexts can stage
+// every rank (allocations, plan, graph capture: host work that may block)
+// before firing any graph whose barriers wait for the others.
+struct StagedEpoch {
+  EpochShape es;
+  int cur = 0, nxt = 1;
+  int64_t eager = 0;
+  int64_t epoch = 0;
+  std::string next_key;
+};
+
+StagedEpoch stage_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc, int64_t epoch,
+                        float lr) {
+  StagedEpoch sg;
+  EpochShape& es = sg.es;
+  sg.epoch = epoch;
   prepare_epoch(ctx, cfg, tc, es);
   set_epoch_params(ctx, tc, lr);
   const int cur = ctx->cur, nxt = 1 - cur;
+  sg.cur = cur;
+  sg.nxt = nxt;
   // The plan of this epoch was normally built by the previous epoch's graph;
   // otherwise (first epoch, new data, other schedule) build it now.
   const std::string pk = plan_key(ctx, es, tc, epoch);
-  int64_t eager = 0;
   if (ctx->slots[cur].key != pk) {
     set_slot_seed(ctx, cur, epoch_seed(tc.seed, epoch));
     const int64_t before = kernel_launches();
     enqueue_plan(ctx, es, cur, ctx->stream);
-    eager = kernel_launches() - before;
+    sg.eager = kernel_launches() - before;
     ctx->slots[cur].key = pk;
   }
   if (is_mult(cfg) && has_self_loops(ctx)) {
@@ -720,18 +803,26 @@ void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train
     capture_epoch_graph(ctx, es, cur);
     ctx->graph_keys[cur] = gk;
   }
+  sg.next_key = plan_key(ctx, es, tc, epoch + 1);
+  return sg;
+}
+
+void fire_epoch(skg_ctx* ctx, const StagedEpoch& sg) {
   SKG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-  SKG_CUDA(cudaGraphLaunch(ctx->graphs[cur], ctx->stream));
+  SKG_CUDA(cudaGraphLaunch(ctx->graphs[sg.cur], ctx->stream));
   SKG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-  if (after_launch) (*after_launch)();
-  ctx->last_launches = ctx->graph_launches_k[cur] + eager;
-  ctx->last_slot = cur;
-  ctx->slots[nxt].key = plan_key(ctx, es, tc, epoch + 1);
-  ctx->cur = nxt;
+  ctx->last_launches = ctx->graph_launches_k[sg.cur] + sg.eager;
+  ctx->last_slot = sg.cur;
+  ctx->slots[sg.nxt].key = sg.next_key;
+  ctx->cur = sg.nxt;
+}
+
+void complete_epoch(skg_ctx* ctx, const StagedEpoch& sg, skg_epoch_report* rep) {
+  const EpochShape& es = sg.es;
   try {
-    finish_epoch(ctx, es, epoch, rep);
+    finish_epoch(ctx, es, sg.epoch, rep);
   } catch (...) {
-    ctx->slots[nxt].key.clear();  // a failed epoch leaves no reusable prefetch
+    ctx->slots[sg.nxt].key.clear();  // a failed epoch leaves no reusable prefetch
     throw;
   }
   float ms = 0.f;
@@ -753,6 +844,16 @@ void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train
   rep->t_backward_s = std::max(0.0, ms - fwd) * 1e-3;
   rep->t_step_s = 0.0;
   ctx->last_epoch_ms = ms;
+}
+
+
+void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
+                      int64_t epoch, float lr, skg_epoch_report* rep,
+                      const std::function<void()>* after_launch = nullptr) {
+  const StagedEpoch sg = stage_epoch(ctx, cfg, tc, epoch, lr);
+  fire_epoch(ctx, sg);
+  if (after_launch) (*after_launch)();
+  complete_epoch(ctx, sg, rep);
 }
 
 void negative_sample_impl(skg_ctx* ctx, uint64_t seed, bool avoid) {  // training.cpp:51-71
@@ -871,6 +972,18 @@ __global__ void row_normalize_kernel(float* __restrict__ x, int64_t rows, int d,
     }
     for (int j = lane; j < d; j += 32) row[j] = __fdiv_rn(row[j], n);
   }
+}
+
+// embedding.cpp:192-198 on the rows this context holds (all of them, or the
+// owned shard of a sharded context: the renorm is per row).
+void renormalize_entities_impl(skg_ctx* ctx) {
+  float* rows = ctx->shard ? ctx->shard->peers.ent[ctx->shard->rank] : ctx->tables.p;
+  const int64_t n = ctx->shard ? ctx->shard->NEo : ctx->N;
+  if (n == 0) return;
+  row_normalize_kernel<<<grid_for(n * 32), 256, 0, ctx->stream>>>(rows, n, static_cast<int>(ctx->de), 0,
+                                                                 ctx->err_words.p);
+  count_launch();
+  SKG_LAUNCH_CHECK();
 }
 
 int grid_for(int64_t n) {
@@ -1062,6 +1175,12 @@ skg_status skg_store_upload(skg_ctx* ctx, const skg_model_config* cfg, int64_t n
                                ctx->stream));
     }
     ctx->has_store = true;
+    if (ctx->shard) {  // sharded: this rank keeps its owned rows and the relation replica
+      if (n_ent != ctx->N || ctx->de != ctx->shard->d || n_rel * ctx->dr != static_cast<int64_t>(ctx->R) * ctx->shard->d)
+        throw ConfigError("sharded context: store shape changed since init (release the shard first)");
+      SKG_CUDA(cudaStreamSynchronize(ctx->stream));
+      shard_scatter_store(ctx);
+    }
     if (ctx->speculate)  // parameter snapshot of a speculative epoch (tables, proj, normals, aligned sections)
       ctx->backup.ensure(ctx->tables.n + ctx->proj.n + ctx->normals.n + 12);
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1071,6 +1190,7 @@ skg_status skg_store_upload(skg_ctx* ctx, const skg_model_config* cfg, int64_t n
 skg_status skg_store_download(skg_ctx* ctx, float* entity, float* relation, float* proj, float* normals) {
   return guard(ctx, [&] {
     if (!ctx->has_store) throw ConfigError("no parameter store uploaded");
+    if (ctx->shard) shard_gather_store(ctx);  // every rank's owned rows (peer reads) into the full table
     if (entity)
       SKG_CUDA(cudaMemcpyAsync(entity, ctx->tables.p, sizeof(float) * ctx->N * ctx->de, cudaMemcpyDeviceToHost,
                                ctx->stream));
@@ -1649,6 +1769,7 @@ skg_status skg_spmm_transpose_add(skg_ctx* ctx, int64_t num_rows, int64_t num_co
 skg_status skg_score_batch(skg_ctx* ctx, const skg_model_config* cfg, int64_t m, const int64_t* h,
                            const int64_t* r, const int64_t* t, float* scores, float* residual) {
   return guard(ctx, [&] {
+    if (ctx->shard) shard_gather_store(ctx);  // per-op calls read the full tables
     check_config(ctx, *cfg, ctx->N, ctx->R);
     upload_ids(ctx, m, h, r, t, ctx->N, ctx->R);
     if (is_mult(*cfg)) reject_self_loops(m, h, t);
@@ -1699,6 +1820,7 @@ skg_status skg_score_backward(skg_ctx* ctx, const skg_model_config* cfg, int64_t
                               const int64_t* r, const int64_t* t, const float* up, float* g_entity,
                               float* g_relation, float* g_proj, float* g_normals) {
   return guard(ctx, [&] {
+    if (ctx->shard) shard_gather_store(ctx);
     check_config(ctx, *cfg, ctx->N, ctx->R);
     upload_ids(ctx, m, h, r, t, ctx->N, ctx->R);
     if (is_mult(*cfg)) reject_self_loops(m, h, t);
@@ -1811,6 +1933,7 @@ skg_status skg_sgd_step(skg_ctx* ctx, const float* g_entity, const float* g_rela
                         const float* g_normals, float lr) {
   return guard(ctx, [&] {
     if (!ctx->has_store) throw ConfigError("no parameter store uploaded");
+    if (ctx->shard) throw ConfigError("sgd_step on a sharded context: download, step and re-upload the store");
     const int64_t ne = ctx->N * ctx->de, nr = ctx->R * ctx->dr, np = ctx->proj.n, nn = ctx->normals.n;
     ctx->grad_sink.ensure(ne + nr + np + nn + 1);
     float* G = ctx->grad_sink.p;
@@ -1863,11 +1986,7 @@ skg_status skg_sgd_step(skg_ctx* ctx, const float* g_entity, const float* g_rela
 skg_status skg_renormalize_entities(skg_ctx* ctx) {
   return guard(ctx, [&] {
     if (!ctx->has_store) throw ConfigError("no parameter store uploaded");
-    row_normalize_kernel<<<grid_for(ctx->N * 32), 256, 0, ctx->stream>>>(ctx->tables.p, ctx->N,
-                                                                        static_cast<int>(ctx->de), 0,
-                                                                        ctx->err_words.p);
-    count_launch();
-    SKG_LAUNCH_CHECK();
+    renormalize_entities_impl(ctx);
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -1969,13 +2088,7 @@ skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_co
         lr = tc->lr * static_cast<float>(std::pow(tc->decay_factor, double(e / tc->decay_every)));
       skg_epoch_report rep{};
       train_epoch_impl(ctx, *cfg, *tc, e, lr, &rep);
-      if (tc->renorm_entities) {
-        row_normalize_kernel<<<grid_for(ctx->N * 32), 256, 0, ctx->stream>>>(ctx->tables.p, ctx->N,
-                                                                            static_cast<int>(ctx->de), 0,
-                                                                            ctx->err_words.p);
-        count_launch();
-        SKG_LAUNCH_CHECK();
-      }
+      if (tc->renorm_entities) renormalize_entities_impl(ctx);
       reports[e] = rep;
     }
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1998,6 +2111,7 @@ extern "C" skg_status skg_rank_entities(skg_ctx* ctx, const skg_model_config* cf
                                         int64_t nf, const int64_t* fh, const int64_t* fr, const int64_t* ft,
                                         int64_t* ranks) {
   return guard(ctx, [&] {
+    if (ctx->shard) shard_gather_store(ctx);
     check_config(ctx, *cfg, ctx->N, ctx->R);
     const int kind = kind_of(*cfg);
     if (!eval_supported(kind)) throw ConfigError("rank_entities: model not supported");
@@ -2100,3 +2214,148 @@ extern "C" skg_status skg_debug_tc_gemm(skg_ctx* ctx, int32_t mode, const float*
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
+
+// =================================================================== row-sharded data parallel
+
+namespace {
+struct ShardHandle {  // what one rank publishes to the others (skg_shard_export)
+  cudaIpcMemHandle_t mem;
+  int32_t device, rank, world, pad;
+  uint64_t arena_bytes;
+};
+static_assert(sizeof(ShardHandle) <= SKG_SHARD_HANDLE_BYTES, "shard handle size");
+
+template <class F>
+skg_status guard_group(skg_ctx* const* ctxs, int world, F&& f) {
+  if (!ctxs || world < 1) return SKG_ERR_CONFIG;
+  for (int k = 0; k < world; ++k)
+    if (!ctxs[k]) return SKG_ERR_CONFIG;
+  int failed = 0;
+  const skg_status st = guard(ctxs[0], [&] { f(failed); });
+  if (st != SKG_OK && failed != 0) ctxs[failed]->err = ctxs[0]->err;
+  return st;
+}
+}  // namespace
+
+extern "C" {
+
+skg_status skg_shard_group_init(skg_ctx* const* ctxs, int world, int64_t batch_size) {
+  return guard_group(ctxs, world, [&](int& failed) {
+    for (int k = 0; k < world; ++k) {
+      skg_ctx* c = ctxs[k];
+      if (c->shard) throw ConfigError("sharded tables already initialised on this context");
+      if (c->dp) throw ConfigError("context already joined a replicated (NCCL) data-parallel group");
+      if (k > 0 && (c->N != ctxs[0]->N || c->R != ctxs[0]->R || c->de != ctxs[0]->de || c->M != ctxs[0]->M))
+        throw ConfigError("sharded group: contexts hold different stores or triples");
+    }
+    std::vector<void*> bases(static_cast<size_t>(world));
+    try {
+      for (int k = 0; k < world; ++k) {
+        failed = k;
+        SKG_CUDA(cudaSetDevice(ctxs[k]->device));
+        resolve_pending(ctxs[k]);
+        shard_alloc(ctxs[k], k, world, batch_size);
+        bases[k] = ctxs[k]->shard->arena;
+      }
+      for (int k = 0; k < world; ++k)  // peer access between distinct devices (same device: plain pointers)
+        for (int j = 0; j < world; ++j) {
+          if (ctxs[k]->device == ctxs[j]->device) continue;
+          SKG_CUDA(cudaSetDevice(ctxs[k]->device));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[j]->device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) SKG_CUDA(e);
+          cudaGetLastError();
+        }
+      for (int k = 0; k < world; ++k) {
+        failed = k;
+        SKG_CUDA(cudaSetDevice(ctxs[k]->device));
+        shard_link(ctxs[k], bases.data());
+      }
+    } catch (...) {
+      for (int k = 0; k < world; ++k) shard_destroy(ctxs[k]);
+      SKG_CUDA(cudaSetDevice(ctxs[0]->device));
+      throw;
+    }
+    SKG_CUDA(cudaSetDevice(ctxs[0]->device));
+  });
+}
+
+skg_status skg_shard_group_train_epoch(skg_ctx* const* ctxs, int world, const skg_model_config* cfg,
+                                       const skg_train_config* tc, int64_t epoch, float lr,
+                                       skg_epoch_report* reports) {
+  return guard_group(ctxs, world, [&](int& failed) {
+    std::vector<StagedEpoch> sg(static_cast<size_t>(world));
+    for (int k = 0; k < world; ++k) {  // host-side work of every rank first (no barrier is running yet)
+      failed = k;
+      if (!ctxs[k]->shard || ctxs[k]->shard->world != world || ctxs[k]->shard->rank != k)
+        throw ConfigError("sharded group: contexts are not ranks 0..world-1 of one group");
+      SKG_CUDA(cudaSetDevice(ctxs[k]->device));
+      resolve_pending(ctxs[k]);
+      sg[k] = stage_epoch(ctxs[k], *cfg, *tc, epoch, lr);
+    }
+    for (int k = 0; k < world; ++k) {
+      SKG_CUDA(cudaSetDevice(ctxs[k]->device));
+      fire_epoch(ctxs[k], sg[k]);
+    }
+    std::exception_ptr first;
+    for (int k = 0; k < world; ++k) {  // every rank completes (and syncs) even if one failed
+      try {
+        SKG_CUDA(cudaSetDevice(ctxs[k]->device));
+        complete_epoch(ctxs[k], sg[k], reports + k);
+      } catch (...) {
+        if (!first) {
+          first = std::current_exception();
+          failed = k;
+        }
+      }
+    }
+    SKG_CUDA(cudaSetDevice(ctxs[0]->device));
+    if (first) std::rethrow_exception(first);
+  });
+}
+
+skg_status skg_shard_export(skg_ctx* ctx, int rank, int world, int64_t batch_size, void* handle) {
+  return guard(ctx, [&] {
+    if (!handle) throw ConfigError("shard_export: null handle buffer");
+    if (ctx->dp) throw ConfigError("context already joined a replicated (NCCL) data-parallel group");
+    resolve_pending(ctx);
+    shard_alloc(ctx, rank, world, batch_size);
+    ShardHandle h{};
+    SKG_CUDA(cudaIpcGetMemHandle(&h.mem, ctx->shard->arena));
+    h.device = ctx->device;
+    h.rank = rank;
+    h.world = world;
+    h.arena_bytes = ctx->shard->arena_bytes;
+    std::memset(handle, 0, SKG_SHARD_HANDLE_BYTES);
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+skg_status skg_shard_import(skg_ctx* ctx, const void* handles) {
+  return guard(ctx, [&] {
+    ShardState* st = ctx->shard;
+    if (!st) throw ConfigError("shard_import: call skg_shard_export first");
+    if (st->linked) throw ConfigError("shard_import: peers already linked");
+    std::vector<void*> bases(static_cast<size_t>(st->world));
+    for (int k = 0; k < st->world; ++k) {
+      ShardHandle h;
+      std::memcpy(&h, static_cast<const char*>(handles) + static_cast<size_t>(k) * SKG_SHARD_HANDLE_BYTES, sizeof(h));
+      if (h.rank != k || h.world != st->world || h.arena_bytes != st->arena_bytes)
+        throw ConfigError("shard_import: handle " + std::to_string(k) + " does not belong to this group");
+      if (k == st->rank) {
+        bases[k] = st->arena;
+        continue;
+      }
+      void* p = nullptr;
+      SKG_CUDA(cudaIpcOpenMemHandle(&p, h.mem, cudaIpcMemLazyEnablePeerAccess));
+      st->opened[k] = p;
+      bases[k] = p;
+    }
+    shard_link(ctx, bases.data());
+  });
+}
+
+skg_status skg_shard_release(skg_ctx* ctx) {
+  return guard(ctx, [&] { shard_destroy(ctx); });
+}
+
+}  // extern "C"

@@ -43,7 +43,8 @@ struct DevBuf {
   ~DevBuf() { release(); }
 };
 
-struct DpState;  // NCCL replicas (dp.cu)
+struct DpState;     // NCCL replicas (dp.cu)
+struct ShardState;  // row-sharded tables (shard.cu)
 
 // One epoch's permutation and transposed-incidence plan. Two slots let the
 // next epoch's plan be built on a side stream while the current one trains.
@@ -141,5 +142,6 @@ struct skg_ctx {
   uint32_t* h_spec = nullptr;           // pinned: the check's flags
 
   // ---- data parallel
-  skg::DpState* dp = nullptr;
+  skg::DpState* dp = nullptr;        // replicated tables, NCCL all-reduce
+  skg::ShardState* shard = nullptr;  // row-sharded tables, peer memory
 };

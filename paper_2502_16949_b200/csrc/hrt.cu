@@ -181,8 +181,28 @@ __device__ __forceinline__ float row_scale(float up, float s) {
 
 // TRAIN-mode gather of a tile's 8 (pos, neg) pairs: lanes k and k + 8 hold
 // the ids of pair k's positive and negative row (same relation).
-template <int KIND, int P, int TP = 8>
-__device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int d4, int64_t N, int h, int t, int r,
+// Row addressing: the stacked [entity; relation] table, or (SH) entity rows
+// on their owner rank's shard (peer memory) and relation rows in the local
+// replica (shard.cu).
+template <bool SH>
+struct RowSrc {
+  const float4* X4;
+  const float* const* peer;  // SH: per-rank entity shards
+  const float4* rel4;        // SH: relation replica
+  int glog;
+  int64_t N;
+  __device__ __forceinline__ const float4* ent(int e, int d4) const {
+    if (SH)
+      return reinterpret_cast<const float4*>(peer[e & ((1 << glog) - 1)]) + static_cast<size_t>(e >> glog) * d4;
+    return X4 + static_cast<size_t>(e) * d4;
+  }
+  __device__ __forceinline__ const float4* rel(int r, int d4) const {
+    return SH ? rel4 + static_cast<size_t>(r) * d4 : X4 + static_cast<size_t>(N + r) * d4;
+  }
+};
+
+template <int KIND, int P, int TP = 8, bool SH = false>
+__device__ __forceinline__ void gather_pairs(const RowSrc<SH>& src, int d4, int h, int t, int r,
                                              float* rows, int S, int lane) {
 #pragma unroll
   for (int k0 = 0; k0 < TP; k0 += P) {
@@ -199,11 +219,11 @@ __device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int 
       float4 xa[P], xb[P], xe[P], xf[P], xr[P];
 #pragma unroll
       for (int q = 0; q < P; ++q) {
-        xa[q] = __ldg(X4 + static_cast<size_t>(hp[q]) * d4 + c);
-        xb[q] = __ldg(X4 + static_cast<size_t>(tp[q]) * d4 + c);
-        xe[q] = __ldg(X4 + static_cast<size_t>(hn[q]) * d4 + c);
-        xf[q] = __ldg(X4 + static_cast<size_t>(tn[q]) * d4 + c);
-        xr[q] = __ldg(X4 + static_cast<size_t>(N + rr[q]) * d4 + c);
+        xa[q] = __ldg(src.ent(hp[q], d4) + c);
+        xb[q] = __ldg(src.ent(tp[q], d4) + c);
+        xe[q] = __ldg(src.ent(hn[q], d4) + c);
+        xf[q] = __ldg(src.ent(tn[q], d4) + c);
+        xr[q] = __ldg(src.rel(rr[q], d4) + c);
       }
 #pragma unroll
       for (int q = 0; q < P; ++q) {
@@ -227,11 +247,16 @@ __device__ __forceinline__ void gather_pairs(const float4* __restrict__ X4, int 
 #ifndef SKG_FWD_P256
 #define SKG_FWD_P256 2  // ... when d <= 256
 #endif
-template <int KIND, bool TRAIN, int VEC, int MINB = SKG_FWD_MINB, int TP = 8>
+template <int KIND, bool TRAIN, int VEC, int MINB = SKG_FWD_MINB, int TP = 8, bool SH = false>
 __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdArgs a) {
   extern __shared__ float4 smem4[];
   __shared__ float warp_loss[kWarps];
+  __shared__ const float* s_peer[8];
   if (a.err[0] != 0) return;  // sticky error: nothing runs after the failing batch
+  if (SH) {
+    if (threadIdx.x < 8) s_peer[threadIdx.x] = a.ent_peer[threadIdx.x];
+    __syncthreads();
+  }
   if (a.stamp_start && blockIdx.x == 0 && threadIdx.x == 0) stamp_now(a.stamp_start);
   float* smem = reinterpret_cast<float*>(smem4);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -304,9 +329,11 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
       // the relation row, so P pairs need 5P row loads, all in flight at once
       const int d4 = d >> 2;
       constexpr int P128 = SKG_FWD_P128 < TP ? SKG_FWD_P128 : TP, P256 = SKG_FWD_P256 < TP ? SKG_FWD_P256 : TP;
-      if (d4 <= 32) gather_pairs<KIND, P128, TP>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
-      else if (d4 <= 64) gather_pairs<KIND, P256, TP>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
-      else gather_pairs<KIND, 1, TP>(reinterpret_cast<const float4*>(a.X), d4, N, h, t, r, rows, S, lane);
+      const RowSrc<SH> src{reinterpret_cast<const float4*>(a.X), s_peer, reinterpret_cast<const float4*>(a.rel_rows),
+                           a.glog, N};
+      if (d4 <= 32) gather_pairs<KIND, P128, TP, SH>(src, d4, h, t, r, rows, S, lane);
+      else if (d4 <= 64) gather_pairs<KIND, P256, TP, SH>(src, d4, h, t, r, rows, S, lane);
+      else gather_pairs<KIND, 1, TP, SH>(src, d4, h, t, r, rows, S, lane);
     } else if (VEC == 4) {
       const float4* X4 = reinterpret_cast<const float4*>(a.X);
       const int d4 = d >> 2;
@@ -730,7 +757,13 @@ void launch_fwd_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
   if (grid < 1) grid = 1;
   // d > 128: three blocks' worth of registers per SM (more rows in flight for
   // the DRAM-resident wide tables; C5 +3 %), d <= 128: two (C1 -1.5 % with three)
-  if (small_tile) hrt_forward_kernel<KIND, TRAIN, VEC, SKG_FWD_MINB_SMALL, 4><<<grid, wpb * 32, smem, s>>>(a);
+  const bool sharded = a.ent_peer[0] != nullptr;
+  if (sharded && !(TRAIN && VEC == 4)) throw CudaError("hrt_forward: sharded tables need training mode and d % 4 == 0");
+  if (sharded && TRAIN && VEC == 4) {
+    if (small_tile) hrt_forward_kernel<KIND, true, 4, SKG_FWD_MINB_SMALL, 4, true><<<grid, wpb * 32, smem, s>>>(a);
+    else if (a.de > 128) hrt_forward_kernel<KIND, true, 4, 3, 8, true><<<grid, wpb * 32, smem, s>>>(a);
+    else hrt_forward_kernel<KIND, true, 4, SKG_FWD_MINB, 8, true><<<grid, wpb * 32, smem, s>>>(a);
+  } else if (small_tile) hrt_forward_kernel<KIND, TRAIN, VEC, SKG_FWD_MINB_SMALL, 4><<<grid, wpb * 32, smem, s>>>(a);
   else if (a.de > 128) hrt_forward_kernel<KIND, TRAIN, VEC, 3><<<grid, wpb * 32, smem, s>>>(a);
   else hrt_forward_kernel<KIND, TRAIN, VEC><<<grid, wpb * 32, smem, s>>>(a);
   count_launch();
@@ -791,6 +824,12 @@ void configure_one() {
 }
 template <int KIND>
 void configure_kind() {
+  SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, true, 4, SKG_FWD_MINB, 8, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, true, 4, 3, 8, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SKG_CUDA(cudaFuncSetAttribute(hrt_forward_kernel<KIND, true, 4, SKG_FWD_MINB_SMALL, 4, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   configure_one<KIND, true, 4>();
   configure_one<KIND, true, 1>();
   configure_one<KIND, false, 4>();

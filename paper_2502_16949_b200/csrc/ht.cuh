@@ -107,7 +107,10 @@ void eval_rank(int kind, const float* X, const float* Rt, int64_t N, int64_t R, 
 void dp_destroy(skg_ctx* ctx);
 int dp_rank(const skg_ctx* ctx);
 int dp_world(const skg_ctx* ctx);
-const void* dp_comm_tag(const skg_ctx* ctx);  // identity of the communicator (graph keys)
+const void* dp_comm_tag(const skg_ctx* ctx);
+int shard_rank(const skg_ctx* ctx);
+uint64_t shard_tag(const skg_ctx* ctx);
+int shard_world(const skg_ctx* ctx);  // identity of the communicator (graph keys)
 void drop_graphs(skg_ctx* ctx);               // destroys captured epoch graphs and plan-slot keys
 void dp_allreduce_sum(skg_ctx* ctx, float* buf, int64_t n, cudaStream_t s);
 

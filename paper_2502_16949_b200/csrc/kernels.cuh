@@ -73,6 +73,13 @@ struct FwdArgs {
   // the loss reduction writes stamp_end. Null: no stamps.
   unsigned long long* stamp_start;
   unsigned long long* stamp_end;
+  // Row-sharded tables (shard.cu): entity e lives on rank e % G at
+  // local row e / G of ent_peer[e % G] (peer memory, G = 1 << glog); relation
+  // rows come from the local replica rel_rows. ent_peer[0] == null: the
+  // stacked table X as usual.
+  const float* ent_peer[8];
+  int glog;
+  const float* rel_rows;
 };
 
 struct BwdArgs {

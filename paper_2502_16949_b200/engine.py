@@ -115,6 +115,11 @@ def load_library():
         "skg_debug_tc_gemm": [vp, i32, vp, vp, vp],
         "skg_rank_entities": [vp, vp, i64, vp, vp, vp, i32, i64, vp, vp, vp, vp],
         "skg_dp_shard": [i64, i64, i32, i32, vp],
+        "skg_shard_group_init": [vp, C.c_int, i64],
+        "skg_shard_group_train_epoch": [vp, C.c_int, vp, vp, i64, f32, vp],
+        "skg_shard_export": [vp, C.c_int, C.c_int, i64, vp],
+        "skg_shard_import": [vp, vp],
+        "skg_shard_release": [vp],
         "skg_peek_checkpoint": [C.c_char_p, vp],
         "skg_save_checkpoint": [C.c_char_p, C.c_uint32, i64, i64, i64, i64, vp, vp, vp, vp],
         "skg_load_checkpoint": [C.c_char_p, C.c_uint32, vp, vp, vp, vp],
@@ -349,6 +354,47 @@ class Engine:
     def dp_init(self, unique_id: bytes, rank: int, world: int):
         buf = C.create_string_buffer(unique_id, 128)
         self._check(self.L.skg_dp_init(self.h, buf, rank, world))
+
+    # ------------------------------------------------------------ row-sharded data parallel
+    SHARD_HANDLE_BYTES = 128
+
+    @staticmethod
+    def _handles(engines):
+        arr = (C.c_void_p * len(engines))(*[e.h.value for e in engines])
+        return arr
+
+    @staticmethod
+    def shard_group_init(engines, batch_size: int):
+        """One process drives every rank: engines[k] is rank k (skg_shard_group_init)."""
+        L = load_library()
+        rc = L.skg_shard_group_init(Engine._handles(engines), len(engines), batch_size)
+        if rc != 0:
+            raise EngineError(rc, L.skg_last_error(engines[0].h).decode())
+
+    @staticmethod
+    def shard_group_train_epoch(engines, cfg: ModelConfig, tc: TrainConfig, epoch: int, lr: float):
+        L = load_library()
+        reps = (EpochReport * len(engines))()
+        rc = L.skg_shard_group_train_epoch(Engine._handles(engines), len(engines), C.byref(cfg), C.byref(tc),
+                                           epoch, lr, reps)
+        if rc != 0:
+            msgs = [L.skg_last_error(e.h).decode() for e in engines]
+            raise EngineError(rc, next((m for m in msgs if m), ""))
+        return [reps[i] for i in range(len(engines))]
+
+    def shard_export(self, rank: int, world: int, batch_size: int) -> bytes:
+        """This rank's IPC handle (one process per GPU); all-gather it, then shard_import."""
+        buf = C.create_string_buffer(self.SHARD_HANDLE_BYTES)
+        self._check(self.L.skg_shard_export(self.h, rank, world, batch_size, buf))
+        return buf.raw
+
+    def shard_import(self, handles):
+        blob = b"".join(handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        self._check(self.L.skg_shard_import(self.h, buf))
+
+    def shard_release(self):
+        self._check(self.L.skg_shard_release(self.h))
 
     # ------------------------------------------------------------ measurement hooks
     def flush_l2(self):
