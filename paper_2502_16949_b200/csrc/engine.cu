@@ -2248,6 +2248,27 @@ skg_status skg_shard_group_init(skg_ctx* const* ctxs, int world, int64_t batch_s
       if (k > 0 && (c->N != ctxs[0]->N || c->R != ctxs[0]->R || c->de != ctxs[0]->de || c->M != ctxs[0]->M))
         throw ConfigError("sharded group: contexts hold different stores or triples");
     }
+    // Ranks sharing a device run their epoch graphs concurrently and wait for
+    // each other in barrier kernels: each rank's streams need their own
+    // hardware queue, or a spinning barrier can block a peer queued behind it.
+    int per_dev = 1;
+    for (int k = 0; k < world; ++k) {
+      int c = 0;
+      for (int j = 0; j < world; ++j) c += ctxs[j]->device == ctxs[k]->device;
+      per_dev = std::max(per_dev, c);
+    }
+    // Measured on one B200: 2 and 4 ranks per device run; 8 ranks per device
+    // stall in the barriers even with 32 hardware queues (the epoch graphs'
+    // internal branch streams add to the 3 per rank).
+    if (per_dev > 4) throw ConfigError("sharded group: at most 4 ranks may share one device");
+    if (per_dev > 1) {
+      const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+      const int conns = e ? std::atoi(e) : 8;
+      if (conns < 3 * per_dev)
+        throw ConfigError("sharded group with " + std::to_string(per_dev) +
+                          " ranks on one device needs CUDA_DEVICE_MAX_CONNECTIONS >= " + std::to_string(3 * per_dev) +
+                          " (set before the first CUDA call)");
+    }
     std::vector<void*> bases(static_cast<size_t>(world));
     try {
       for (int k = 0; k < world; ++k) {
@@ -2292,9 +2313,14 @@ skg_status skg_shard_group_train_epoch(skg_ctx* const* ctxs, int world, const sk
       resolve_pending(ctxs[k]);
       sg[k] = stage_epoch(ctxs[k], *cfg, *tc, epoch, lr);
     }
+    static const bool dbg = std::getenv("SKG_SHARD_DEBUG") != nullptr;
     for (int k = 0; k < world; ++k) {
       SKG_CUDA(cudaSetDevice(ctxs[k]->device));
+      const auto t0 = std::chrono::steady_clock::now();
       fire_epoch(ctxs[k], sg[k]);
+      if (dbg)
+        std::fprintf(stderr, "shard group: fired rank %d in %.1f us\n", k,
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
     }
     std::exception_ptr first;
     for (int k = 0; k < world; ++k) {  // every rank completes (and syncs) even if one failed

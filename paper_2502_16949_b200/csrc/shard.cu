@@ -104,11 +104,13 @@ __global__ void shard_barrier_kernel(BarrierArgs b) {
   const uint32_t code = b.err[0];
   const unsigned long long mine =
       (gen << 32) | (code ? ((min(code, 255u) << 24) | (b.err[1] & 0xFFFFFFu)) : 0ull);
+  // after a timeout a peer is gone: publish, never wait again (no 20 s per barrier)
+  const bool gone = code == kErrBarrier;
   if (t < b.world) {
     __threadfence_system();  // this rank's stores of the phase before reach every peer first
     st_release_sys(b.flag_peer[t] + b.rank, mine);
     const unsigned long long t0 = gtimer();
-    while ((ld_acquire_sys(b.my_flags + t) >> 32) < gen) {
+    while (!gone && (ld_acquire_sys(b.my_flags + t) >> 32) < gen) {
       __nanosleep(64);
       if (gtimer() - t0 > 20000000000ull) {
         timed_out = 1;

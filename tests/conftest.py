@@ -1,6 +1,10 @@
 import os
 import sys
 
+# Sharded groups put several ranks on the one test GPU (tests/test_gpu_shard.py):
+# each rank's streams need their own hardware queue (skg_shard_group_init checks).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -16,7 +16,7 @@ def main():
     from oracle.oracle import Oracle
     from paper_2502_16949_b200 import Engine, ModelConfig, TrainConfig
     orc = Oracle("f32")
-    n, r, d, batch = 400, 6, 16, 200
+    n, r, d, batch = 1000, 6, 16, 200
     h, rel, t = orc.synthetic_train(n, r, 2400, 5)
     st = orc.init_store("transe", n, r, d, d, 5)
     cfg = ModelConfig.make("transe", d, d, "l2")

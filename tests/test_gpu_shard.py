@@ -13,7 +13,7 @@ import pytest
 
 from paper_2502_16949_b200 import Engine, EngineError, ModelConfig, TrainConfig
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -28,7 +28,7 @@ def _group(world, cfg, st, h, rel, t, n, r, seed, batch):
 
 
 @pytest.mark.parametrize("world,model,norm,d,m_extra", [(2, "transe", "l2", 32, 0), (4, "transe", "l2", 64, 3),
-                                                        (8, "transe", "l1", 16, 0), (2, "toruse", "l2", 32, 5),
+                                                        (4, "transe", "l1", 16, 0), (2, "toruse", "l2", 32, 5),
                                                         (4, "toruse", "l1", 8, 0), (2, "transe", "l2", 256, 7)])
 def test_shard_group_matches_oracle_bitwise(orc32, world, model, norm, d, m_extra):
     n, r, batch = 1500, 30, 1000
@@ -79,17 +79,20 @@ def test_shard_group_non_finite_loss_stops_every_rank(orc32):
 
 
 def test_shard_config_errors(orc32):
-    n, r, d = 300, 5, 8
-    h, rel, t = orc32.synthetic_train(n, r, 2000, 1)
+    n, r, d = 1200, 9, 8
+    h, rel, t = orc32.synthetic_train(n, r, 6000, 1)
     st = orc32.init_store("transe", n, r, d, d, 1)
     cfg = ModelConfig.make("transe", d, d, "l2")
-    engines = [Engine(0) for _ in range(3)]
+    engines = [Engine(0) for _ in range(8)]
     for e in engines:
         e.store_upload(cfg, st.entity, st.relation)
         e.set_triples(h, rel, t, n, r)
         e.negative_sample(1)
     with pytest.raises(EngineError) as e:  # world must be a power of two up to 8
-        Engine.shard_group_init(engines, 300)
+        Engine.shard_group_init(engines[:3], 300)
+    assert e.value.kind == "ConfigError"
+    with pytest.raises(EngineError) as e:  # at most 4 ranks share one device
+        Engine.shard_group_init(engines, 400)
     assert e.value.kind == "ConfigError"
     with pytest.raises(EngineError) as e:  # global batch must split evenly
         Engine.shard_group_init(engines[:2], 301)
@@ -117,7 +120,7 @@ def test_shard_ipc_two_processes_one_gpu(orc32, tmp_path):
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for k in range(2)]
     outs = [pr.communicate(timeout=600)[0] for pr in procs]
     assert all(pr.returncode == 0 for pr in procs), outs
-    n, r, d, batch = 400, 6, 16, 200
+    n, r, d, batch = 1000, 6, 16, 200
     h, rel, t = orc32.synthetic_train(n, r, 2400, 5)
     st = orc32.init_store("transe", n, r, d, d, 5)
     ro = orc32.fit("transe", st, h, rel, t, orc32.train_config(epochs=2, lr=0.05, batch_size=batch, seed=6))
