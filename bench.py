@@ -9,9 +9,11 @@ forward (gather + distance + hinge + loss) and fused transposed-SpMM backward
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1..C5] [--impl ours|reference]
 
 N > 1 runs under torchrun: one process per GPU, data parallel over the global
-minibatch (per-GPU batch fixed -> weak scaling per step), gradients summed
-over NVLink by NCCL inside the engine; torch.distributed (gloo) is only the
-rendezvous / timing plumbing. --impl reference times the reference CPU path
+minibatch (per-GPU batch fixed -> weak scaling per step). TransE / TorusE use
+row-sharded tables (each rank owns 1/N of the entities; rows and residuals
+move over NVLink peer memory inside the epoch graph); the other models keep
+replicated tables with an NCCL all-reduce. torch.distributed (gloo) is only
+the rendezvous (IPC-handle exchange) / timing plumbing. --impl reference times the reference CPU path
 (oracle restatement, reference unbuildable here) on the host cores.
 """
 from __future__ import annotations
@@ -286,15 +288,29 @@ def main():
     from paper_2502_16949_b200.engine import generate_synthetic, init_store
     h, r, t = generate_synthetic(cfg["N"], cfg["R"], cfg["n_total"], SEED)
     M = len(h)
-    eng = Engine(local)
+    # SKG_BENCH_ONE_DEVICE=1 puts every rank on device 0: exercises the multi-process plumbing on a
+    # one-GPU box (ranks then time-slice one GPU; such a run is a plumbing check, not a measurement)
+    eng = Engine(0 if os.environ.get("SKG_BENCH_ONE_DEVICE") == "1" else local)
     mcfg = ModelConfig.make(cfg["model"], cfg["de"], cfg["dr"], cfg["norm"])
     ent, rel, proj, nrm = init_store(cfg["model"], cfg["N"], cfg["R"], cfg["de"], cfg["dr"], SEED)
     eng.store_upload(mcfg, ent, rel, proj, nrm)
     eng.set_triples(h, r, t, cfg["N"], cfg["R"])
     nh, nt = eng.negative_sample(SEED, avoid)
-    if world > 1:
+    sharded = world > 1 and cfg["model"] in ("transe", "toruse")
+    if sharded:
+        # row-sharded tables: each rank keeps the entities it owns; IPC handles of the
+        # sharded buffers are all-gathered over the gloo rendezvous, then the epoch graphs talk over
+        # NVLink peer memory (no NCCL on the data path)
+        import torch.distributed as dist
+        mine = eng.shard_export(rank, world, cfg["B"] * world)
+        handles = [None] * world
+        dist.all_gather_object(handles, mine)
+        eng.shard_import(handles)
+    elif world > 1:  # replicated tables, dense NCCL all-reduce (C2 / C4 / multiplicative models)
         uid = broadcast_bytes(Engine.nccl_unique_id() if rank == 0 else None, world)
         eng.dp_init(uid, rank, world)
+    layout = ("row-sharded entity table, replicated relations, peer-memory exchange" if sharded else
+              "replicated tables, NCCL all-reduce" if world > 1 else "single device")
     tc = TrainConfig.make(lr=LR, margin=MARGIN, batch_size=cfg["B"] * world, seed=SEED)
     nb = (M + cfg["B"] * world - 1) // (cfg["B"] * world)
 
@@ -405,7 +421,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference lattice generator, data_io.cpp:128-211), init_store(seed=1)",
             "config": config_obj,
-            "wall_s": round(wall, 4), "final_loss": losses[-1],
+            "wall_s": round(wall, 4), "final_loss": losses[-1], "parallel_layout": layout,
             "e2e": {"value": e2e, "unit": "triplets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "skg_set_triples + skg_set_negatives (pinned int64) + skg_train_epoch; the identical-shape "
                             "pinned re-upload is copied by DMA and verified while the epoch trains (rolled back "
