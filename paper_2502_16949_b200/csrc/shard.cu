@@ -500,8 +500,11 @@ void shard_alloc(skg_ctx* ctx, int rank, int world, int64_t batch_size) {
   st->nb_cap = (std::max<int64_t>(ctx->M, 1) + batch_size - 1) / batch_size + 1;
   auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
   size_t o = 0;
+  // every rank uses the same layout (peers' buffers are addressed with this
+  // rank's offsets): the entity region holds ceil(N / G) rows on all ranks
+  const int64_t ne_cap = (ctx->N + world - 1) / world;
   st->off_ent = o;
-  o += al(sizeof(float) * st->NEo * st->d + 16);
+  o += al(sizeof(float) * ne_cap * st->d + 16);
   st->off_rel = o;
   o += al(sizeof(float) * ctx->R * st->d);
   st->off_res = o;

@@ -31,7 +31,7 @@ def _group(world, cfg, st, h, rel, t, n, r, seed, batch):
                                                         (4, "transe", "l1", 16, 0), (2, "toruse", "l2", 32, 5),
                                                         (4, "toruse", "l1", 8, 0), (2, "transe", "l2", 256, 7)])
 def test_shard_group_matches_oracle_bitwise(orc32, world, model, norm, d, m_extra):
-    n, r, batch = 1500, 30, 1000
+    n, r, batch = 1501, 31, 1000  # ranks own different entity / relation counts
     h, rel, t = orc32.synthetic_train(n, r, 12000, 2)
     if m_extra:  # a ragged last batch whose shards are uneven
         h, rel, t = (np.concatenate([a, a[:m_extra]]) for a in (h, rel, t))
