@@ -177,7 +177,7 @@ def broadcast_bytes(b, world):
     return obj[0]
 
 
-def algorithmic_bytes(cfg, eng, nb):
+def algorithmic_bytes(cfg, eng, nb, world=1):
     """Per-epoch algorithmic bytes of the forward and backward kernels:
     forward: 3 gathered rows + 1 residual row written per incidence row (8B·d·4),
     plus ids (order + 5 ids per pair) and the per-row scale; backward: one residual
@@ -188,7 +188,8 @@ def algorithmic_bytes(cfg, eng, nb):
     fwd = bwd = 0
     M = eng.m
     for b in range(nb):
-        Bb = min(cfg["B"], M - b * cfg["B"])
+        Bb = min(cfg["B"] * world, M - b * cfg["B"] * world)
+        Bb = (Bb + world - 1) // world  # this rank's shard of the global batch (its forward rows)
         segs, entries, _ = eng.plan_stats(b)
         ids = Bb * 24 + 2 * Bb * 4
         if cfg["model"] == "transh":    # h, t, d_r, w_r gathers + du write per row
@@ -386,7 +387,7 @@ def main():
 
     # ---- roofline of the dominant kernel (profiled epoch, per-launch events)
     rep, fwd_ms, bwd_ms, plan_ms = eng.profile_epoch(mcfg, tc, 200, LR)
-    fwd_b, bwd_b = algorithmic_bytes(cfg, eng, nb)
+    fwd_b, bwd_b = algorithmic_bytes(cfg, eng, nb, world)
     peak, peak_kind = peaks()
     fwd_gbs = fwd_b / nb / (fwd_ms * 1e-3) / 1e9
     bwd_gbs = bwd_b / nb / (bwd_ms * 1e-3) / 1e9

@@ -2053,6 +2053,26 @@ skg_status skg_plan_stats(skg_ctx* ctx, int64_t batch, int64_t* segments, int64_
                           int64_t* relation_segments) {
   return guard(ctx, [&] {
     resolve_pending(ctx);
+    if (ctx->shard) {  // this rank's owned-column plan (shard.cu)
+      const ShardPlanBufs& p = ctx->shard->plan[ctx->last_slot];
+      if (batch < 0 || batch >= p.nb || !p.seg_base) throw ShapeError("plan_stats: no such batch");
+      uint32_t sb[2];
+      SKG_CUDA(cudaMemcpy(sb, p.seg_base + batch, sizeof(sb), cudaMemcpyDeviceToHost));
+      uint32_t e0 = 0, e1 = 0;
+      if (sb[1] > sb[0]) {
+        SKG_CUDA(cudaMemcpy(&e0, p.seg_start + sb[0], sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        SKG_CUDA(cudaMemcpy(&e1, p.seg_start + sb[1], sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      }
+      std::vector<uint32_t> cols(sb[1] - sb[0]);
+      if (!cols.empty())
+        SKG_CUDA(cudaMemcpy(cols.data(), p.seg_col + sb[0], sizeof(uint32_t) * cols.size(), cudaMemcpyDeviceToHost));
+      int64_t nrel = 0;
+      for (uint32_t c : cols) nrel += (c & 0x80000000u) != 0;
+      *segments = sb[1] - sb[0];
+      *entries = static_cast<int64_t>(e1) - e0;
+      *relation_segments = nrel;
+      return;
+    }
     if (batch < 0 || batch >= ctx->slots[ctx->last_slot].plan.nb || !ctx->slots[ctx->last_slot].plan.seg_base) throw ShapeError("plan_stats: no such batch");
     uint32_t sb[2];
     SKG_CUDA(cudaMemcpy(sb, ctx->slots[ctx->last_slot].plan.seg_base + batch, sizeof(sb), cudaMemcpyDeviceToHost));
