@@ -1362,43 +1362,6 @@ __global__ void spec_check_kernel(const int64_t* __restrict__ src, int64_t m, in
   if (__any_sync(kFull, diff) && (threadIdx.x & 31) == 0) atomicOr(flags + 3, 1u);
 }
 
-// Zero-copy variant: the caller's page-locked int64 arrays are read straight
-// over PCIe (UVA host pointers, streaming loads that do not linger in L2) and
-// compared with the resident ids the epoch is using; nothing is written to HBM
-// unless they differ (then the caller's arrays are copied in afterwards). The
-// DMA path wrote the 5 x 8 x M staged bytes through L2 while the epoch ran
-// (C1: the graph slowed from 0.70 to 0.81 ms). A small grid leaves the SMs to
-// the epoch; PCIe latency is covered by 4 x 16-byte loads per thread.
-struct HostIds {
-  const int64_t* p[5];  // h, r, t, nh, nt (device-visible aliases of pinned host memory)
-};
-__global__ void __launch_bounds__(256) spec_check_zc_kernel(HostIds src, int64_t m, int64_t n_ent, int64_t n_rel,
-                                                            const int32_t* __restrict__ H, const int32_t* __restrict__ Rl,
-                                                            const int32_t* __restrict__ T, const int32_t* __restrict__ NH,
-                                                            const int32_t* __restrict__ NT, uint32_t* __restrict__ flags) {
-  bool diff = false;
-  const int64_t n2 = m / 2;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  auto check = [&](int64_t i, int64_t h, int64_t r, int64_t t, int64_t nh, int64_t nt) {
-    if (h < 0 || h >= n_ent || t < 0 || t >= n_ent) atomicMin(flags, static_cast<uint32_t>(i));
-    if (r < 0 || r >= n_rel) atomicMin(flags + 1, static_cast<uint32_t>(i));
-    if (nh < 0 || nh >= n_ent || nt < 0 || nt >= n_ent) atomicMin(flags + 2, static_cast<uint32_t>(i));
-    diff |= __ldg(H + i) != static_cast<int32_t>(h) || __ldg(T + i) != static_cast<int32_t>(t) ||
-            __ldg(NH + i) != static_cast<int32_t>(nh) || __ldg(NT + i) != static_cast<int32_t>(nt) ||
-            __ldg(Rl + i) != static_cast<int32_t>(r);
-  };
-  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n2; j += stride) {
-    longlong2 v[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) v[k] = __ldcs(reinterpret_cast<const longlong2*>(src.p[k]) + j);
-    check(2 * j, v[0].x, v[1].x, v[2].x, v[3].x, v[4].x);
-    check(2 * j + 1, v[0].y, v[1].y, v[2].y, v[3].y, v[4].y);
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (m & 1))
-    check(m - 1, src.p[0][m - 1], src.p[1][m - 1], src.p[2][m - 1], src.p[3][m - 1], src.p[4][m - 1]);
-  if (__any_sync(kFull, diff) && (threadIdx.x & 31) == 0) atomicOr(flags + 3, 1u);
-}
-
 __global__ void narrow_staged_kernel(const int64_t* __restrict__ src, int64_t m, int32_t* __restrict__ H,
                                      int32_t* __restrict__ Rl, int32_t* __restrict__ T, int32_t* __restrict__ NH,
                                      int32_t* __restrict__ NT) {
@@ -1454,31 +1417,13 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   ctx->spec_flags.ensure(4);
   // the copy + check are enqueued right after the epoch graph is launched
   bool launched = false;
-  // zero-copy verification when every array is 16-byte aligned and device-visible (SKG_SPEC_DMA=1: DMA path)
-  static const bool force_dma = std::getenv("SKG_SPEC_DMA") != nullptr;
-  HostIds hz{};
-  bool zc = !force_dma;
-  for (int k = 0; k < 5 && zc; ++k) {
-    cudaPointerAttributes pa{};
-    zc = cudaPointerGetAttributes(&pa, src[k]) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
-         (reinterpret_cast<uintptr_t>(pa.devicePointer) & 15) == 0;
-    hz.p[k] = zc ? static_cast<const int64_t*>(pa.devicePointer) : nullptr;
-  }
-  cudaGetLastError();
   const std::function<void()> upload = [&]() {
     SKG_CUDA(cudaMemsetAsync(ctx->spec_flags.p, 0xFF, sizeof(uint32_t) * 3, ctx->up));
     SKG_CUDA(cudaMemsetAsync(ctx->spec_flags.p + 3, 0, sizeof(uint32_t), ctx->up));
-    if (zc) {
-      spec_check_zc_kernel<<<static_cast<unsigned>(std::max(1, ctx->num_sms / 8)), 256, 0, ctx->up>>>(
-          hz, m, ctx->tN, ctx->tR, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->spec_flags.p);
-    } else {
-      for (int k = 0; k < 5; ++k)
-        SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, src[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice,
-                                 ctx->up));
-      spec_check_kernel<<<static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms)), 256, 0,
-                          ctx->up>>>(ctx->stage_i64.p, m, ctx->tN, ctx->tR, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p,
-                                     ctx->NT.p, ctx->spec_flags.p);
-    }
+    for (int k = 0; k < 5; ++k)
+      SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, src[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice, ctx->up));
+    spec_check_kernel<<<static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms)), 256, 0, ctx->up>>>(
+        ctx->stage_i64.p, m, ctx->tN, ctx->tR, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->spec_flags.p);
     count_launch();
     SKG_LAUNCH_CHECK();
     SKG_CUDA(cudaEventRecord(ctx->up_ev, ctx->up));
@@ -1536,10 +1481,6 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     throw ShapeError("triple " + std::to_string(f[1]) + ": relation id out of range");
   }
   // adopt the uploaded ids (data changed, or the negatives are invalid)
-  if (zc)  // the zero-copy check staged nothing: copy the caller's arrays in now
-    for (int k = 0; k < 5; ++k)
-      SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, src[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice,
-                               ctx->stream));
   narrow_staged_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->stage_i64.p, m, ctx->H.p, ctx->Rl.p, ctx->T.p,
                                                             ctx->NH.p, ctx->NT.p);
   count_launch();
