@@ -253,6 +253,10 @@ skg_status skg_init_store(uint32_t model, int64_t num_entities, int64_t num_rela
 const char* skg_host_last_error(void);
 
 /* ---- measurement hooks ----------------------------------------------------- */
+/* Random-row gather bandwidth (GB/s) over a table of table_bytes with rows of
+ * row_floats floats (128-bit loads, full occupancy): the roofline denominator
+ * for the gather kernels when the table is L2-resident (C1-C4). */
+skg_status skg_measure_gather(skg_ctx* ctx, int64_t table_bytes, int32_t row_floats, double* gbs);
 /* Overwrites a 256 MiB scratch buffer on the context stream (evicts L2). */
 skg_status skg_flush_l2(skg_ctx* ctx);
 /* Plan statistics of minibatch `batch` of the last epoch: touched columns

@@ -2041,6 +2041,71 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const sk
   });
 }
 
+}  // extern "C"
+
+namespace {
+// Random-row gather probe (the roofline denominator for L2-resident tables):
+// every warp gathers rows of `rf` floats at pseudo-random indices with 128-bit
+// loads, 4 rows in flight per warp, full occupancy. Returns nothing useful; the
+// XOR of the loaded words defeats dead-code elimination.
+__global__ void __launch_bounds__(256) gather_probe_kernel(const float4* __restrict__ X, int64_t nrows, int rf4,
+                                                           int64_t total_rows, uint32_t* __restrict__ sink) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint32_t acc = 0;
+  for (int64_t i = gw * 4; i < total_rows; i += nw * 4) {
+    float4 v[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t h = (static_cast<uint64_t>(i + q) * 0x9E3779B97F4A7C15ull) >> 17;
+      const int64_t row = static_cast<int64_t>(h % static_cast<uint64_t>(nrows));
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col = lane + 32 * c;
+        v[q][c] = col < rf4 ? __ldg(X + row * rf4 + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        acc ^= __float_as_uint(v[q][c].x) ^ __float_as_uint(v[q][c].y) ^ __float_as_uint(v[q][c].z) ^
+               __float_as_uint(v[q][c].w);
+  }
+  if (acc == 0x12345678u) sink[0] = acc;
+}
+}  // namespace
+
+extern "C" skg_status skg_measure_gather(skg_ctx* ctx, int64_t table_bytes, int32_t row_floats, double* gbs) {
+  return guard(ctx, [&] {
+    if (row_floats < 4 || row_floats % 4 || row_floats > 256) throw ConfigError("measure_gather: row_floats 4..256, multiple of 4");
+    const int64_t nrows = std::max<int64_t>(1, table_bytes / (4LL * row_floats));
+    DevBuf<float> tab;
+    tab.ensure(nrows * row_floats);
+    SKG_CUDA(cudaMemsetAsync(tab.p, 0, sizeof(float) * nrows * row_floats, ctx->stream));
+    DevBuf<uint32_t> sink;
+    sink.ensure(1);
+    const int64_t total = std::max<int64_t>(4LL << 20, nrows);  // rows gathered per launch
+    const int grid = ctx->num_sms * 8;
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {  // first launch warms the table into L2 (or not, if it is larger)
+      SKG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+      gather_probe_kernel<<<grid, 256, 0, ctx->stream>>>(reinterpret_cast<const float4*>(tab.p), nrows,
+                                                         row_floats / 4, total, sink.p);
+      SKG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+      SKG_LAUNCH_CHECK();
+      SKG_CUDA(cudaEventSynchronize(ctx->ev1));
+      float ms = 0.f;
+      SKG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+      if (rep > 0) best = std::min(best, ms);
+    }
+    *gbs = static_cast<double>(total) * row_floats * 4.0 / (best * 1e-3) / 1e9;
+  });
+}
+
+extern "C" {
+
 skg_status skg_flush_l2(skg_ctx* ctx) {
   return guard(ctx, [&] {
     ctx->flush_buf.ensure(256ll << 20);

@@ -111,6 +111,7 @@ def load_library():
         "skg_generate_synthetic": [i64, i64, i64, C.c_uint64, vp, vp, vp],
         "skg_init_store": [C.c_uint32, i64, i64, i64, i64, C.c_uint64, vp, vp, vp, vp],
         "skg_flush_l2": [vp],
+        "skg_measure_gather": [vp, i64, i32, vp],
         "skg_plan_stats": [vp, i64, vp, vp, vp],
         "skg_debug_tc_gemm": [vp, i32, vp, vp, vp],
         "skg_rank_entities": [vp, vp, i64, vp, vp, vp, i32, i64, vp, vp, vp, vp],
@@ -397,6 +398,12 @@ class Engine:
         self._check(self.L.skg_shard_release(self.h))
 
     # ------------------------------------------------------------ measurement hooks
+    def measure_gather(self, table_bytes: int, row_floats: int) -> float:
+        """Random-row gather GB/s over a table of table_bytes (L2-resident when it fits)."""
+        g = C.c_double()
+        self._check(self.L.skg_measure_gather(self.h, table_bytes, row_floats, C.byref(g)))
+        return g.value
+
     def flush_l2(self):
         self._check(self.L.skg_flush_l2(self.h))
 
