@@ -389,6 +389,11 @@ def main():
     rep, fwd_ms, bwd_ms, plan_ms = eng.profile_epoch(mcfg, tc, 200, LR)
     fwd_b, bwd_b = algorithmic_bytes(cfg, eng, nb, world)
     peak, peak_kind = peaks()
+    # Random-row gather peak over a table of this config's size (L2-resident for C1-C4): the
+    # ceiling the gather kernels actually face; reported beside the HBM copy peak.
+    row_floats = 128 if cfg["de"] * (2 if cfg["model"] in ("complex", "rotate") else 1) <= 128 else 256
+    table_bytes = (cfg["N"] + cfg["R"]) * cfg["de"] * 4 * (2 if cfg["model"] in ("complex", "rotate") else 1)
+    gather_peak = eng.measure_gather(table_bytes, row_floats)
     fwd_gbs = fwd_b / nb / (fwd_ms * 1e-3) / 1e9
     bwd_gbs = bwd_b / nb / (bwd_ms * 1e-3) / 1e9
     dom = "forward" if fwd_ms >= bwd_ms else "backward"
@@ -439,7 +444,12 @@ def main():
                           "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
                           "forward_gbs": fwd_gbs, "backward_gbs": bwd_gbs, "fwd_ms_per_batch": fwd_ms,
                           "bwd_ms_per_batch": bwd_ms, "plan_ms_per_epoch": plan_ms,
-                          "note": "algorithmic bytes (no cache credit); C1-C4 tables are L2-resident"}),
+                          "gather_peak_gbs": gather_peak, "gather_frac": ach / gather_peak,
+                          "gather_peak_source": f"skg_measure_gather: random {row_floats * 4}-byte rows of a "
+                                                f"{table_bytes / 2**20:.1f} MiB table (L2-resident below ~100 MiB)",
+                          "note": "algorithmic bytes (no cache credit); C1-C4 tables are L2-resident, so "
+                                  "gather_frac (against the measured gather peak of a table this size) is the "
+                                  "binding roofline there, frac (against the HBM copy peak) for C5"}),
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,

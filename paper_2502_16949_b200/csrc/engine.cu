@@ -2050,28 +2050,29 @@ namespace {
 // XOR of the loaded words defeats dead-code elimination.
 __global__ void __launch_bounds__(256) gather_probe_kernel(const float4* __restrict__ X, int64_t nrows, int rf4,
                                                            int64_t total_rows, uint32_t* __restrict__ sink) {
+  // unit = one 512-byte chunk of a row (32 lanes x 16 B); 8 units in flight per warp
+  constexpr int kU = 8;
   const int lane = threadIdx.x & 31;
+  const int per_row = rf4 / 32;
+  const int lg = per_row == 1 ? 0 : per_row == 2 ? 1 : per_row == 4 ? 2 : 3;
+  const int64_t total_units = total_rows * per_row;
   const int64_t gw = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   uint32_t acc = 0;
-  for (int64_t i = gw * 4; i < total_rows; i += nw * 4) {
-    float4 v[4][2];
+  for (int64_t i = gw * kU; i < total_units; i += nw * kU) {
+    float4 v[kU];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t h = (static_cast<uint64_t>(i + q) * 0x9E3779B97F4A7C15ull) >> 17;
-      const int64_t row = static_cast<int64_t>(h % static_cast<uint64_t>(nrows));
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int col = lane + 32 * c;
-        v[q][c] = col < rf4 ? __ldg(X + row * rf4 + col) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+    for (int q = 0; q < kU; ++q) {  // cheap index math: the probe must be bound by the loads
+      const uint32_t u = static_cast<uint32_t>(i + q);
+      const uint32_t r = u >> lg;
+      const uint32_t h = r * 0x9E3779B9u;
+      const uint32_t row = __umulhi(h, static_cast<uint32_t>(nrows));
+      v[q] = (i + q) < total_units ? __ldg(X + static_cast<size_t>(row) * rf4 + ((u & ((1u << lg) - 1)) << 5) + lane)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        acc ^= __float_as_uint(v[q][c].x) ^ __float_as_uint(v[q][c].y) ^ __float_as_uint(v[q][c].z) ^
-               __float_as_uint(v[q][c].w);
+    for (int q = 0; q < kU; ++q)
+      acc ^= __float_as_uint(v[q].x) ^ __float_as_uint(v[q].y) ^ __float_as_uint(v[q].z) ^ __float_as_uint(v[q].w);
   }
   if (acc == 0x12345678u) sink[0] = acc;
 }
@@ -2079,7 +2080,8 @@ __global__ void __launch_bounds__(256) gather_probe_kernel(const float4* __restr
 
 extern "C" skg_status skg_measure_gather(skg_ctx* ctx, int64_t table_bytes, int32_t row_floats, double* gbs) {
   return guard(ctx, [&] {
-    if (row_floats < 4 || row_floats % 4 || row_floats > 256) throw ConfigError("measure_gather: row_floats 4..256, multiple of 4");
+    if (row_floats != 128 && row_floats != 256 && row_floats != 512 && row_floats != 1024)
+      throw ConfigError("measure_gather: row_floats 128, 256, 512 or 1024");
     const int64_t nrows = std::max<int64_t>(1, table_bytes / (4LL * row_floats));
     DevBuf<float> tab;
     tab.ensure(nrows * row_floats);
