@@ -286,6 +286,30 @@ skg_status skg_dp_init(skg_ctx* ctx, const char unique_id[128], int rank, int wo
  * the epoch, minibatches}. */
 skg_status skg_dp_shard(int64_t m, int64_t batch_size, int32_t world, int32_t rank, int64_t* out);
 
+/* ---- run artifacts of `kge train` (tools/kge.cpp:181-247) -----------------
+ * Host-side writers: train_log.jsonl (one compact JSON record per epoch,
+ * flushed per line), loss.log ("<epoch> <loss %.17g>") and summary.json, in
+ * the reference's formats (nlohmann::json output: sorted keys, shortest
+ * round-trip doubles). Open appends to the files under out_dir (created if
+ * needed); errors: SKG_ERR_PARSE with skg_run_log_last_error(). */
+typedef struct skg_run_log skg_run_log;
+typedef struct skg_run_summary { /* the parts of summary.json the engine cannot know */
+  const char* engine;          /* "sparse" | "dense" (the CLI's --engine) */
+  const char* dataset_source;  /* "synthetic" or the dataset directory */
+  int64_t entities, relations, train, valid, test, dropped_valid, dropped_test;
+  int32_t threads;
+  int64_t epochs_run;          /* TrainingRun::epochs.size() */
+  double final_loss;           /* TrainingRun::final_loss() */
+  double t_forward_s, t_backward_s, t_step_s; /* TrainingRun totals */
+  const char* checkpoint_path; /* NULL: <out_dir>/checkpoint.bin */
+} skg_run_summary;
+skg_status skg_run_log_open(const char* out_dir, skg_run_log** out);
+skg_status skg_run_log_epoch(skg_run_log* log, const skg_epoch_report* report);
+skg_status skg_run_log_summary(skg_run_log* log, const skg_model_config* cfg, const skg_train_config* tc,
+                               const skg_run_summary* info);
+void skg_run_log_close(skg_run_log* log);
+const char* skg_run_log_last_error(void);
+
 /* ---- row-sharded data parallel (wikikg2-scale tables) ---------
  * TransE / TorusE. The entity table is split by owner (entity e on rank e % G,
  * G in {1, 2, 4, 8}) and the relation table replicated; each global minibatch

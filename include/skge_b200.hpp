@@ -847,4 +847,37 @@ inline void renormalize_entities(EmbeddingStore& store) {
   detail::download(store);
 }
 
+// kge.cpp:181-247: the `kge train` artifacts (train_log.jsonl, loss.log,
+// summary.json) written through the C ABI; pass log.callback() as fit's on_epoch.
+class RunLog {
+ public:
+  explicit RunLog(const std::string& out_dir) {
+    if (skg_run_log_open(out_dir.c_str(), &h_) != SKG_OK) throw ParseError(skg_run_log_last_error());
+  }
+  ~RunLog() { skg_run_log_close(h_); }
+  RunLog(const RunLog&) = delete;
+  RunLog& operator=(const RunLog&) = delete;
+  void epoch(const EpochReport& r) {
+    const skg_epoch_report c{r.epoch, static_cast<double>(r.loss), r.t_forward_s, r.t_backward_s, r.t_step_s};
+    if (skg_run_log_epoch(h_, &c) != SKG_OK) throw ParseError(skg_run_log_last_error());
+  }
+  std::function<void(const EpochReport&)> callback() {
+    return [this](const EpochReport& r) { epoch(r); };
+  }
+  void summary(const ModelConfig& mc, const TrainConfig& tc, const TrainingRun& run, const skg_run_summary& info) {
+    skg_model_config c = detail::cfg(mc);
+    skg_train_config t = detail::tcfg(tc);
+    skg_run_summary s = info;
+    s.epochs_run = static_cast<int64_t>(run.epochs.size());
+    s.final_loss = run.final_loss();
+    s.t_forward_s = run.t_forward_s;
+    s.t_backward_s = run.t_backward_s;
+    s.t_step_s = run.t_step_s;
+    if (skg_run_log_summary(h_, &c, &t, &s) != SKG_OK) throw ParseError(skg_run_log_last_error());
+  }
+
+ private:
+  skg_run_log* h_ = nullptr;
+};
+
 }  // namespace skge

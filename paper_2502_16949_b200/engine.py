@@ -484,6 +484,46 @@ class CheckpointHeader(C.Structure):  # embedding.hpp:134-140
                 ("dim_entity", C.c_int64), ("dim_relation", C.c_int64)]
 
 
+class RunSummary(C.Structure):
+    _fields_ = [("engine", C.c_char_p), ("dataset_source", C.c_char_p), ("entities", C.c_int64),
+                ("relations", C.c_int64), ("train", C.c_int64), ("valid", C.c_int64), ("test", C.c_int64),
+                ("dropped_valid", C.c_int64), ("dropped_test", C.c_int64), ("threads", C.c_int32),
+                ("epochs_run", C.c_int64), ("final_loss", C.c_double), ("t_forward_s", C.c_double),
+                ("t_backward_s", C.c_double), ("t_step_s", C.c_double), ("checkpoint_path", C.c_char_p)]
+
+
+class RunLog:
+    """train_log.jsonl / loss.log / summary.json writers of `kge train` (kge.cpp:181-247)."""
+
+    def __init__(self, out_dir: str):
+        self.L = load_library()
+        for name, args in {"skg_run_log_open": [C.c_char_p, C.c_void_p],
+                           "skg_run_log_epoch": [C.c_void_p, C.c_void_p],
+                           "skg_run_log_summary": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]}.items():
+            getattr(self.L, name).argtypes = args
+            getattr(self.L, name).restype = C.c_int
+        self.L.skg_run_log_close.argtypes = [C.c_void_p]
+        self.L.skg_run_log_close.restype = None
+        self.L.skg_run_log_last_error.restype = C.c_char_p
+        self.h = C.c_void_p()
+        self._check(self.L.skg_run_log_open(out_dir.encode(), C.byref(self.h)))
+
+    def _check(self, rc):
+        if rc != 0:
+            raise EngineError(rc, self.L.skg_run_log_last_error().decode())
+
+    def epoch(self, rep: EpochReport):
+        self._check(self.L.skg_run_log_epoch(self.h, C.byref(rep)))
+
+    def summary(self, cfg: ModelConfig, tc: TrainConfig, info: RunSummary):
+        self._check(self.L.skg_run_log_summary(self.h, C.byref(cfg), C.byref(tc), C.byref(info)))
+
+    def close(self):
+        if self.h:
+            self.L.skg_run_log_close(self.h)
+            self.h = None
+
+
 def _ckpt_check(L, rc):
     if rc != 0:
         raise EngineError(rc, L.skg_checkpoint_last_error().decode())
