@@ -153,7 +153,9 @@ void reject_self_loops(int64_t m, const int64_t* h, const int64_t* t) {
 void ensure_workspace(skg_ctx* ctx, int64_t rows, int kind) {
   const int64_t d = std::max(ctx->de, ctx->dr);
   ctx->res.ensure(rows * d * (is_mult_kind(kind) ? 3 : 1));  // multiplicative: 3 gradient planes
-  ctx->res_u.ensure(rows * ctx->de);
+  // TransR tcgen05 training writes dU in tile-blocked slots (kTileSlotRows): up to R + 1 partial tiles more
+  const bool tile_rows = (kind == kTransR_L2 || kind == kTransR_L1) && ctx->de == 128;
+  ctx->res_u.ensure(tile_rows ? std::max(rows * ctx->de, tile_rows_floats(rows, ctx->R)) : rows * ctx->de);
   ctx->scal.ensure(rows);
   ctx->scores.ensure(rows);
   ctx->block_partial.ensure(static_cast<int64_t>(ctx->num_sms) * 16 + 64);
@@ -675,6 +677,45 @@ void set_slot_seed(skg_ctx* ctx, int slot, uint64_t seed_eff) {
                            ctx->stream));
 }
 
+// L2 residency of the parameter tables. The per-batch streams (residual / dU
+// rows, plan entries) together with a mid-size table exceed the 126 MB L2 (C4:
+// 63 MB table + 67 MB dU rows), so without a hint every minibatch re-reads the
+// table from HBM at gather latency. When the stacked table fits the
+// persisting carve-out, every kernel node of the epoch graph gets an access
+// policy window over it (hits persist, misses stream). SKG_L2_PERSIST=0 turns
+// it off.
+void apply_l2_policy(skg_ctx* ctx, cudaGraph_t g) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("SKG_L2_PERSIST");
+    return !(e && e[0] == '0');
+  }();
+  const size_t bytes = sizeof(float) * static_cast<size_t>(ctx->tables.n);
+  if (!enabled || bytes < (size_t(16) << 20)) return;  // small tables stay L2-resident on their own
+  int max_persist = 0, max_win = 0;
+  SKG_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+  SKG_CUDA(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
+  if (bytes > static_cast<size_t>(max_persist) || bytes > static_cast<size_t>(max_win)) return;
+  size_t cur = 0;
+  SKG_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  if (cur < bytes) SKG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+  cudaLaunchAttributeValue v{};
+  v.accessPolicyWindow.base_ptr = ctx->tables.p;
+  v.accessPolicyWindow.num_bytes = bytes;
+  v.accessPolicyWindow.hitRatio = 1.0f;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  size_t n = 0;
+  SKG_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  SKG_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    SKG_CUDA(cudaGraphNodeGetType(nd, &t));
+    if (t == cudaGraphNodeTypeKernel)
+      SKG_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributeAccessPolicyWindow, &v));
+  }
+}
+
 // One captured graph per plan slot: the main branch trains every minibatch on
 // slot `cur`; a side branch builds the next epoch's plan into the other slot.
 void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
@@ -695,6 +736,12 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
     throw;
   }
   SKG_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+  try {
+    apply_l2_policy(ctx, g);
+  } catch (...) {
+    cudaGraphDestroy(g);
+    throw;
+  }
   if (ctx->graphs[cur]) cudaGraphExecDestroy(ctx->graphs[cur]);
   ctx->graphs[cur] = nullptr;
   SKG_CUDA(cudaGraphInstantiate(&ctx->graphs[cur], g, 0));

@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
 // L2: v * (up / ||v||_eps); torus-L2: (up * 2) * delta; L1 / torus-L1: sign weight.
 template <int KIND>
 __device__ __forceinline__ float dir1(float r, float sc) {
-  if (KIND == kPlainRows || KIND == kMultRows) return r;
+  if (KIND == kPlainRows || KIND == kMultRows || KIND == kTileSlotRows) return r;
   if (KIND == kTransE_L2 || KIND == kTorusE_L2) return __fmul_rn(r, sc);
   return r > 0.f ? sc : (r < 0.f ? -sc : 0.f);
 }
@@ -552,7 +552,8 @@ __device__ __forceinline__ void segment_rows(const BwdArgs& a, uint32_t col, uin
           mysc = a.scal[myv & 0x7fffffffu];
         }
       }
-      unsigned live = __ballot_sync(kFull, lane < cnt && mysc != 0.f);
+      const bool on = KIND == kTileSlotRows ? __float_as_uint(mysc) != 0u : mysc != 0.f;
+      unsigned live = __ballot_sync(kFull, lane < cnt && on);
       while (live) {
         int k[KB];
         int n = 0;
@@ -572,13 +573,21 @@ __device__ __forceinline__ void segment_rows(const BwdArgs& a, uint32_t col, uin
           vq[q] = __shfl_sync(kFull, myv, k[q]);
           scq[q] = __shfl_sync(kFull, mysc, k[q]);
           size_t rowoff = static_cast<size_t>(vq[q] & 0x7fffffffu) * dv;
+          if (KIND == kTileSlotRows) {  // d = 128, float4 lanes: chunk c of slot s
+            const uint32_t sl = __float_as_uint(scq[q]) - 1u;
+            rowoff = (static_cast<size_t>(sl >> 7) * 128 * 128 + (sl & 127u) * kDuGroup) / 4;
+            scq[q] = 1.f;
+          }
           if (KIND == kMultRows) {  // the entry's own gradient plane: head, tail or relation
             const uint32_t slot = col >= static_cast<uint32_t>(a.N) ? 2u : (vq[q] >> 31);
             rowoff += static_cast<size_t>(slot) * a.plane_rows * dv;
           }
 #pragma unroll
           for (int h = 0; h < CH; ++h)
-            if (q < n && has[h]) rv[q][h] = __ldg(RV + rowoff + c[h]);
+            if (q < n && has[h])
+              rv[q][h] = __ldg(RV + rowoff +
+                               (KIND == kTileSlotRows ? (c[h] / (kDuGroup / 4)) * (32 * kDuGroup) + c[h] % (kDuGroup / 4)
+                                                      : c[h]));
         }
 #pragma unroll
         for (int q = 0; q < KB; ++q)
@@ -607,7 +616,7 @@ __device__ __forceinline__ void segment_rows(const BwdArgs& a, uint32_t col, uin
 // (C2: most entity segments hold one entry; epoch -3 %, C4 -1.8 %). The other
 // passes keep segment_backward_kernel: the staging measured slower there
 // (C1 backward 22.3 -> 30.8 us, M1 26.8 -> 29.4 us).
-template <bool SGD, int KB = SKG_BWD_KB>
+template <bool SGD, int KIND = kPlainRows, int KB = SKG_BWD_KB>
 __global__ void __launch_bounds__(kThreads) segment_backward_staged_kernel(const BwdArgs a) {
   if (a.err[0] != 0) return;
   const int lane = threadIdx.x & 31;
@@ -641,7 +650,7 @@ __global__ void __launch_bounds__(kThreads) segment_backward_staged_kernel(const
     for (unsigned m = __ballot_sync(kFull, use); m; m &= m - 1) {
       const int j = __ffs(m) - 1;
       const uint4 qj = myq[j];
-      segment_rows<kPlainRows, SGD, 4, 1, KB>(a, qj.x, qj.y, qj.z, qj.z - qj.y == 1, qj.w, mysc[j], lane);
+      segment_rows<KIND, SGD, 4, 1, KB>(a, qj.x, qj.y, qj.z, qj.z - qj.y == 1, qj.w, mysc[j], lane);
     }
   }
 }
@@ -787,7 +796,11 @@ void launch_bwd_k(bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s) {
   const int grid = num_sms * 8;
   const bool v4 = (a.d % 4) == 0;
   const bool narrow = v4 ? a.d <= 128 : a.d <= 32;
-  if (KIND == kPlainRows && v4 && narrow) {
+  if constexpr (KIND == kTileSlotRows) {
+    if (a.d != 128) throw CudaError("tile-blocked dU rows need d = 128");
+    if (sgd) segment_backward_staged_kernel<true, kTileSlotRows><<<grid, kThreads, 0, s>>>(a);
+    else segment_backward_staged_kernel<false, kTileSlotRows><<<grid, kThreads, 0, s>>>(a);
+  } else if (KIND == kPlainRows && v4 && narrow) {
     if (sgd) segment_backward_staged_kernel<true><<<grid, kThreads, 0, s>>>(a);
     else segment_backward_staged_kernel<false><<<grid, kThreads, 0, s>>>(a);
   } else if (sgd) {
@@ -865,6 +878,7 @@ void launch_segment_backward(int kind, bool sgd, const BwdArgs& a, int num_sms, 
     case kTorusE_L1: launch_bwd_k<kTorusE_L1>(sgd, a, num_sms, s); break;
     case kPlainRows: launch_bwd_k<kPlainRows>(sgd, a, num_sms, s); break;
     case kMultRows: launch_bwd_k<kMultRows>(sgd, a, num_sms, s); break;
+    case kTileSlotRows: launch_bwd_k<kTileSlotRows>(sgd, a, num_sms, s); break;
     default: throw CudaError("launch_segment_backward: unsupported kind");
   }
 }

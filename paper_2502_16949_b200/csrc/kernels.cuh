@@ -34,7 +34,18 @@ enum Kind : int {
   kComplEx = 10,
   kRotatE = 11,
   kMultRows = 12,  // backward rows: per-entry gradient planes [head | tail | relation]
+  kTileSlotRows = 13,  // TransR tcgen05 training: dU rows in tile-blocked order, scal = slot + 1 (0: inactive)
 };
+// kTileSlotRows layout of a d = 128 dU row (tile slot s = 128 * tile + lane):
+// kDuGroup-float groups g of the row at s / 128 * 128 * 128 + g * 128 * kDuGroup
+// + (s % 128) * kDuGroup: the producing warp (thread = row) stores whole groups
+// with 32-byte stores into one contiguous run per group, a reader fetches whole
+// kDuGroup * 4-byte pieces.
+#ifndef SKG_TR_DU_GROUP
+#define SKG_TR_DU_GROUP 16
+#endif
+constexpr int kDuGroup = SKG_TR_DU_GROUP;
+__host__ __device__ inline int64_t tile_rows_floats(int64_t rows, int64_t R) { return (rows + 128 * (R + 1)) * 128; }
 inline bool is_mult_kind(int k) { return k >= kDistMult && k <= kRotatE; }
 inline bool is_ht_kind(int k) { return k >= kTransH_L2 && k <= kTransR_L1; }
 

@@ -128,6 +128,16 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
                : "memory");
 }
 
+// 16-byte cp.async (LDGSTS, L1 bypass) and the mbarrier arrival that fires
+// once all of this thread's earlier cp.async copies have landed (.noinc: the
+// barrier's expected count already includes this arrival).
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* mbar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+
 // ---- warp-uniform issue: the whole warp executes these; elect.sync picks
 // one lane inside the asm, so descriptors stay in uniform registers and the
 // compiler emits no per-lane waterfall around UTCHMMA (measured: 64 cycles per

@@ -568,7 +568,7 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
     BwdArgs eb = ba;
     eb.entity_only = 1;
     eb.d = fa.de;
-    launch_segment_backward(kPlainRows, sinks == nullptr, eb, num_sms, s);
+    launch_segment_backward(kTileSlotRows, sinks == nullptr, eb, num_sms, s);
     launch_transr_train_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
                               proj_dst, rel_dst, ba.lr, ba.err, w.mr_chunks, R, s, sinks != nullptr);
     if (mark) (*mark)();

@@ -39,8 +39,8 @@ namespace {
 constexpr int kD = 128;
 constexpr int kRows = 128;
 constexpr int kPairs = 64;
-constexpr int kThreads = 352;
-constexpr int kMmaWarp = 8, kRowWarp = 10;  // warp 9: ring loader
+constexpr int kThreads = 384;
+constexpr int kMmaWarp = 8, kRowWarp = 10, kGatherWarp = 11;  // warp 9: ring loader
 
 // sU / sDZ: K-major SWIZZLE_128B (m = row, k = feature) in four 32-feature
 // column blocks of 128 rows x 128 B; 16-byte unit (r, c4) =
@@ -100,9 +100,10 @@ struct Smem {
   float rs[kRows];
   float colsum[4][kD];
   float tl[2];
-  uint64_t u_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty;
+  uint64_t g_full, u_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty;
   uint64_t rows_full[2], rows_empty[2];
   uint64_t g3_full[kG3Slots], g3_empty[kG3Slots];
+  uint64_t stg[kRows / 8];  // row group s staged: its sU / sDZ rows may be refilled
   uint64_t ring_full[kRing], ring_empty[kRing];
   uint32_t tmem_base;
   int last;
@@ -121,6 +122,12 @@ struct Args {
   float* dr_part;
   const float* mr;  // per relation: [layout][chunk][hi, lo][128 x 16]
 };
+
+__device__ __forceinline__ void st_global_v8(float* p, const uint32_t* v) {  // one 32-byte store
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
 
 __device__ __forceinline__ uint32_t idesc128() { return tc::make_idesc_tf32(128, 128, 0, 0); }
 
@@ -174,7 +181,8 @@ __device__ __forceinline__ void chase_rows(const Args& a, uint32_t t, int lane, 
 }
 
 template <bool L2>
-__global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args a) {
+__global__ void __launch_bounds__(kThreads, 1)
+    transr_train_tc_kernel(const Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const FwdArgs& f = a.f;
@@ -185,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
 
   if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
   if (tid == 0) {
+    tc::mbar_init(&S.g_full, 32);
     tc::mbar_init(&S.u_full, 128);
     tc::mbar_init(&S.v_full, 1);
     tc::mbar_init(&S.dz_full, 128);
@@ -200,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       tc::mbar_init(&S.rows_full[i], 1);
       tc::mbar_init(&S.rows_empty[i], 128);
     }
+    for (int i = 0; i < kRows / 8; ++i) tc::mbar_init(&S.stg[i], 128);
     for (int i = 0; i < kRing; ++i) {
       tc::mbar_init(&S.ring_full[i], 1);
       tc::mbar_init(&S.ring_empty[i], 1);
@@ -278,7 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       const bool active = valid && term > 0.f;
       const float up = active ? (m < 64 ? f.unit : -f.unit) : 0.f;
       const float sc = up == 0.f ? 0.f : (L2 ? __fdiv_rn(up, __fsqrt_rn(__fadd_rn(ssum, kNormEpsF))) : up);
-      if (row2 >= 0) f.scal[row2] = active ? 1.f : 0.f;
+      // entity pass (kTileSlotRows): scal carries the dU row's tile slot + 1, 0 when inactive
+      if (row2 >= 0) reinterpret_cast<uint32_t*>(f.scal)[row2] = active ? (t * kRows + static_cast<uint32_t>(m) + 1u) : 0u;
       {  // tile loss: positive rows, deterministic tree
         float v = (m < 64 && active) ? term : 0.f;
         if (warp < 2) {
@@ -356,25 +367,26 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
         tc::fence_before();
         tc::mbar_arrive(&S.dm_empty);
       }
-      // dU drain: rows of active pairs -> res_u (the entity segments skip the rest)
+      // dU drain in tile-blocked order (kTileSlotRows): kDuGroup-float groups,
+      // thread = row, 32-byte stores
       tc::mbar_wait(&S.g2_done, it & 1);
       tc::fence_after();
       if (m == 0) trace(it, 13);
-      float* dst = f.res_u + static_cast<size_t>(row2 < 0 ? 0 : row2) * kD;
+      float* dst = f.res_u + static_cast<size_t>(t) * kRows * kD + static_cast<size_t>(m) * kDuGroup;
 #pragma unroll 1
       for (int c = 0; c < kD; c += 32) {
-        uint32_t r0[16], r1[16];
-        tc::tmem_ld16_nowait(tbase + lane_addr + kColDU + c, r0);
-        tc::tmem_ld16_nowait(tbase + lane_addr + kColDU + c + 16, r1);
+        uint32_t r[32];
+        tc::tmem_ld16_nowait(tbase + lane_addr + kColDU + c, r);
+        tc::tmem_ld16_nowait(tbase + lane_addr + kColDU + c + 16, r + 16);
         tc::tmem_wait_ld();
+#ifdef SKG_TR_NO_DRAIN
+        if (false) {
+#else
         if (active) {
+#endif
 #pragma unroll
-          for (int q = 0; q < 16; q += 4) {
-            *reinterpret_cast<float4*>(dst + c + q) = make_float4(__uint_as_float(r0[q]), __uint_as_float(r0[q + 1]),
-                                                                  __uint_as_float(r0[q + 2]), __uint_as_float(r0[q + 3]));
-            *reinterpret_cast<float4*>(dst + c + 16 + q) = make_float4(
-                __uint_as_float(r1[q]), __uint_as_float(r1[q + 1]), __uint_as_float(r1[q + 2]), __uint_as_float(r1[q + 3]));
-          }
+          for (int q = 0; q < 32; q += 8)
+            st_global_v8(dst + ((c + q) / kDuGroup) * (kRows * kDuGroup) + (c + q) % kDuGroup, r + q);
         }
       }
       tc::fence_before();
@@ -393,40 +405,27 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       tc::mbar_wait(&S.rows_full[buf], (it >> 1) & 1);
       if (p == 0) trace(it, 0);
       const int4* rows = S.rows[buf];
-      // gather U = h - t (rows 32pw .. +31): one 512-byte row per load
-      // instruction (lane = 16-byte chunk), 16 rows (32 loads) in flight
-#pragma unroll 1
-      for (int r0 = pw * 32; r0 < pw * 32 + 32; r0 += 16) {
-        float4 xh[16], xt[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int4 rw = rows[r0 + q];
-          xh[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rw.x) * kD) + lane);
-          xt[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rw.y) * kD) + lane);
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const bool ok = rows[r0 + q].z >= 0;
-          const float4 u = ok ? make_float4(__fsub_rn(xh[q].x, xt[q].x), __fsub_rn(xh[q].y, xt[q].y),
-                                            __fsub_rn(xh[q].z, xt[q].z), __fsub_rn(xh[q].w, xt[q].w))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-          *reinterpret_cast<float4*>(S.U + 4 * tile_unit(r0 + q, lane)) = u;
-        }
-      }
-      tc::fence_async_shared();
-      tc::named_sync(2, 128);
+      tc::mbar_wait(&S.g_full, it & 1);  // head rows in sU, tail rows in sDZ
       if (p == 0) trace(it, 1);
-      // U lo -> TMEM once GEMM2 of the previous tile has consumed DZ lo
+      // U = h - t in place (row p), hi / lo -> TMEM once GEMM2 of the previous
+      // tile has consumed DZ hi / lo
       if (it > 0) {
         tc::mbar_wait(&S.g2_done, (it - 1) & 1);
         tc::fence_after();
       }
+      const bool ok = rows[p].z >= 0;
 #pragma unroll 1
       for (int c = 0; c < kD; c += 16) {
         float hi[16], lo[16];
 #pragma unroll
         for (int q = 0; q < 16; q += 4) {
-          const float4 u = *reinterpret_cast<const float4*>(S.U + 4 * tile_unit(p, (c + q) >> 2));
+          float4* up = reinterpret_cast<float4*>(S.U + 4 * tile_unit(p, (c + q) >> 2));
+          const float4 xh = *up;
+          const float4 xt = *reinterpret_cast<const float4*>(S.DZ + 4 * tile_unit(p, (c + q) >> 2));
+          const float4 u = ok ? make_float4(__fsub_rn(xh.x, xt.x), __fsub_rn(xh.y, xt.y), __fsub_rn(xh.z, xt.z),
+                                            __fsub_rn(xh.w, xt.w))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          *up = u;
           hi[q] = u.x, hi[q + 1] = u.y, hi[q + 2] = u.z, hi[q + 3] = u.w;
           lo[q] = tc::tf32_trunc_lo(u.x);
           lo[q + 1] = tc::tf32_trunc_lo(u.y);
@@ -440,7 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       tc::fence_before();
       tc::mbar_arrive(&S.u_full);
       if (p == 0) trace(it, 2);
-      // GEMM3 staging: DZ^T and U^T, 8 rows per slot, split hi (rna) / lo
+      // GEMM3 staging: DZ^T and U^T, 8 rows per slot, split hi (rna) / lo;
+      // each staged row group's sU / sDZ rows are refilled with the next
+      // tile's head / tail rows by the gather warp
       tc::mbar_wait(&S.dz_full, it & 1);
       if (p == 0) trace(it, 3);
       const int kq = p & 7, ig = p >> 3;
@@ -464,18 +465,22 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
             const int o = g3_off(4 * c4 + e, kq);
             float hi, lo;
             tc::split_tf32(dv[e], hi, lo);
+#ifndef SKG_TR_NO_HI_STAGE
             Ahi[o] = hi;
+#endif
             Alo[o] = lo;
             tc::split_tf32(uv[e], hi, lo);
+#ifndef SKG_TR_NO_HI_STAGE
             Bhi[o] = hi;
+#endif
             Blo[o] = lo;
           }
         }
         tc::fence_async_shared();
         tc::mbar_arrive(&S.g3_full[slot]);
+        tc::mbar_arrive(&S.stg[s3]);
       }
       if (p == 0) trace(it, 4);
-      tc::named_sync(2, 128);  // sU / sDZ reads done: the next gather may overwrite sU
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issue
@@ -569,6 +574,47 @@ __global__ void __launch_bounds__(kThreads, 1) transr_train_tc_kernel(const Args
       chase_rows(a, t0 + it, lane, S.rows[buf], S.rel[buf], &S.np[buf]);
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.rows_full[buf]);
+#ifndef SKG_TR_NO_PREFETCH
+      // pull the tile's head / tail rows into L2 now, a tile or more before
+      // the gather warp copies them (they miss L2 about half the time at C4:
+      // the table and the per-batch dU rows together exceed it)
+#pragma unroll 4
+      for (int k = lane; k < 4 * kRows; k += 32) {
+        const int4 rw = S.rows[buf][k >> 2];
+        const float* row = f.X + static_cast<size_t>((k & 1) ? rw.y : rw.x) * kD + ((k >> 1) & 1) * 64;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 32));
+      }
+#endif
+    }
+  } else if (warp == kGatherWarp) {
+    // ------------------------------------------------------------ row gather
+    // 16-byte cp.async per lane (lane = chunk of a 512-byte row): head rows
+    // into sU, tail rows into sDZ at tile_unit; one warp keeps a tile's 256
+    // rows in flight without registers. (TMA tile::gather4 of 128-byte boxes
+    // measured ~16 cycles per box row per SM here, too slow to hide.)
+    auto gather8 = [&](const int4* rows, int r0) {  // rows r0 .. r0 + 7, head and tail
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int4 rw = rows[r0 + q];
+        tc::cp_async16(S.U + 4 * tile_unit(r0 + q, lane), f.X + static_cast<size_t>(rw.x) * kD + 4 * lane);
+        tc::cp_async16(S.DZ + 4 * tile_unit(r0 + q, lane), f.X + static_cast<size_t>(rw.y) * kD + 4 * lane);
+      }
+    };
+    for (uint32_t it = 0; it < ntile; ++it) {
+      const int buf = it & 1;
+      tc::mbar_wait(&S.rows_full[buf], (it >> 1) & 1);
+      const int4* rows = S.rows[buf];
+#ifdef SKG_TR_GATHER_BULK
+      if (it > 0) tc::mbar_wait(&S.stg[kG3PerTile - 1], (it - 1) & 1);
+#endif
+#pragma unroll 1
+      for (int s3 = 0; s3 < kG3PerTile; ++s3) {
+        // tile it's rows go into the row groups tile it - 1 has finished staging
+        if (it > 0) tc::mbar_wait(&S.stg[s3], (it - 1) & 1);
+        gather8(rows, s3 * 8);
+      }
+      tc::cp_async_mbar_arrive(&S.g_full);
     }
   } else {
     // ------------------------------------------------------------ ring loader
