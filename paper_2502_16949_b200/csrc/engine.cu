@@ -450,7 +450,8 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
           hb.err = ctx->err_words.p;
           HtSinks sk{G + ctx->N * ctx->de, n_proj ? G + n_params : nullptr,
                      n_norm ? G + n_params + n_proj : nullptr};
-          ht_train_batch(es.kind, fa, hb, ctx->ht_work.p, ctx->num_sms, s, nullptr, ctx->R, &sk);
+          const Branch br{ctx->aux, ctx->aux_fork, ctx->aux_join};
+          ht_train_batch(es.kind, fa, hb, ctx->ht_work.p, ctx->num_sms, s, nullptr, ctx->R, &sk, &br);
         } else if (mult) {
           fa.de = static_cast<int>(ctx->cfg.dim_entity);
           fa.plane_rows = 2 * es.S;
@@ -545,7 +546,8 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
       launch_segment_backward(es.kind, true, ba, ctx->num_sms, s);
       mark();
     } else {
-      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, markp, ctx->R);
+      const Branch br{ctx->aux, ctx->aux_fork, ctx->aux_join};
+      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, markp, ctx->R, nullptr, &br);
     }
   }
   if (dp) dp_allreduce_sum(ctx, ctx->batch_loss.p, es.nb, s);  // shard losses -> global batch losses
@@ -1124,6 +1126,9 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaEventCreate(&ctx->ev0));
     SKG_CUDA(cudaEventCreate(&ctx->ev1));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    SKG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->up, cudaStreamNonBlocking));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->up_ev, cudaEventDisableTiming));
 
@@ -1162,6 +1167,9 @@ void skg_destroy(skg_ctx* ctx) {
   drop_graphs(ctx);
   if (ctx->h_stamps) cudaFreeHost(ctx->h_stamps);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->aux_fork) cudaEventDestroy(ctx->aux_fork);
+  if (ctx->aux_join) cudaEventDestroy(ctx->aux_join);
   if (ctx->up) {
     cudaStreamSynchronize(ctx->up);
     cudaStreamDestroy(ctx->up);
@@ -2331,6 +2339,14 @@ extern "C" int32_t skg_debug_mt_jump_selftest(uint64_t seed, int64_t jump) {
 extern "C" int64_t skg_debug_transr_trace(int32_t enable, unsigned long long* out, int64_t cap) {
   try {
     return transr_trace(enable, out, cap);
+  } catch (...) {
+    return -1;
+  }
+}
+
+extern "C" int64_t skg_debug_transh_trace(int32_t enable, unsigned long long* out, int64_t cap) {
+  try {
+    return transh_trace(enable, out, cap);
   } catch (...) {
     return -1;
   }

@@ -111,6 +111,8 @@ struct skg_ctx {
   bool has_loops = false;                  // some positive or negative triple has head == tail
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t aux = nullptr;  // per-batch side branch (TransH relation step beside the entity pass)
+  cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   std::string graph_keys[2];
   int64_t graph_launches_k[2] = {0, 0};

@@ -505,19 +505,15 @@ void configure_ht_kernels() {
 }
 
 void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                    const std::function<void()>* mark, int64_t R, const HtSinks* sinks) {
+                    const std::function<void()>* mark, int64_t R, const HtSinks* sinks, const Branch* br) {
   if (kind == kTransR_L2 || kind == kTransR_L1) {
     transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R, sinks);
     return;
   }
   float* normals = const_cast<float*>(fa.normals);
   if (transh_tiles_supported(fa.de, fa.dr, R)) {  // relation-tiled path (transh_train.cu)
-    transh_tiles_train_batch(kind == kTransH_L2, fa, ba, work, R, num_sms, s, mark, sinks);
-    if (!sinks) {  // data parallel renormalizes after the dense step
-      normals_renorm_kernel<<<static_cast<unsigned>((R * 32 + 127) / 128), 128, 0, s>>>(normals, R, fa.de, ba.err);
-      count_launch();
-      SKG_LAUNCH_CHECK();
-    }
+    // the tile kernel renormalizes the normals itself (data parallel: after the dense step)
+    transh_tiles_train_batch(kind == kTransH_L2, fa, ba, work, R, num_sms, s, mark, sinks, br);
     if (mark) (*mark)();
     return;
   }

@@ -20,6 +20,13 @@ struct HtSinks {
   float* normals;  // TransH: R x d_e
 };
 
+// A second stream and a fork / join event pair: work that may run beside the
+// main stream's next launch (captured as a parallel graph branch).
+struct Branch {
+  cudaStream_t aux;
+  cudaEvent_t fork, join;
+};
+
 // embedding.cpp:181-189 on the TransH normals (after a data-parallel dense step)
 void launch_normals_renorm(float* normals, int64_t R, int d, uint32_t* err, cudaStream_t s);
 // Floats of per-batch scratch the ht kernels need for `rows` rows.
@@ -30,7 +37,8 @@ int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R
 // renormalization). `mark` (nullable) is called after the forward and after
 // the backward for per-phase profiling.
 void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                    const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr);
+                    const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr,
+                    const Branch* br = nullptr);
 // score_batch for ht models (res = v, res_u = u, scores). `ba` carries the
 // batch's plan (TransR groups rows by relation through it).
 void ht_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s, int64_t R);
@@ -47,8 +55,10 @@ void launch_relation_tiles(const BwdArgs& ba, int paired, uint32_t* tile_seg, ui
 bool transh_tiles_supported(int de, int dr, int64_t R);
 void configure_transh_tiles_kernels();
 int64_t transh_tiles_work_floats(int64_t rows, int64_t R);
+int64_t transh_trace(int enable, unsigned long long* out, int64_t cap);  // debug: phase timestamps
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
-                              cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks = nullptr);
+                              cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks = nullptr,
+                              const Branch* br = nullptr);
 
 // TransR (transr.cu)
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R);

@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "tc.cuh"
 #include "ht.cuh"
 #include "plan.cuh"
 #include "primitives.cuh"
@@ -32,16 +33,18 @@ constexpr int kD = 128;
 #ifndef SKG_TRANSH_PAIRS
 #define SKG_TRANSH_PAIRS 32
 #endif
-// 32 pairs = 64 rows per tile, 8 warps x 8 rows, two CTAs per SM: twice the
-// tiles of a 64-pair tile, so the persistent grid ends more evenly and one
-// CTA's barrier waits overlap the other's work.
 constexpr int kPairs = SKG_TRANSH_PAIRS;
 constexpr int kRows = 2 * kPairs;
-constexpr int kRowsPerWarp = 8;
-constexpr int kThreads = kRows / kRowsPerWarp * 32;
-constexpr int kCtasPerSm = 64 / kPairs;
-static_assert(kThreads >= 2 * 128, "the relation reduction uses one thread per (column, vector)");
-constexpr int kStride = kD + 4;    // staged v rows (16-byte aligned, conflict-free row reads)
+#ifndef SKG_TRANSH_RPW
+#define SKG_TRANSH_RPW 4
+#endif
+constexpr int kRowsPerWarp = SKG_TRANSH_RPW;  // rows 0 .. RPW/2-1: positives of the warp's pairs, then their negatives
+constexpr int kHalf = kRowsPerWarp / 2;       // pairs per compute warp
+constexpr int kLanesPerRow = 32 / kRowsPerWarp;
+constexpr int kLaneRowShift = kRowsPerWarp == 8 ? 2 : 3;
+static_assert(kRowsPerWarp == 4 || kRowsPerWarp == 8, "4 or 8 rows per compute warp");
+static_assert(kPairs == 32, "a tile is 32 pairs");
+constexpr int kStride = kD;        // staged rows (float4 row reads are conflict-free)
 
 constexpr int kMaxRelSeg = 1024;  // relation segments per batch handled in shared memory
 
@@ -54,10 +57,11 @@ struct TArgs {
   int batch;
   int64_t mt;                 // tile capacity of `partial`
   float* partial;             // [tile][2][kD]
-  uint32_t* rel_ticket;       // per relation segment: tiles finished (zeroed by the tile enumerator)
+  uint32_t* info;             // [0] relation runs, [1] tiles, then per run {r, first tile, end tile}
   float* rel;                 // relation table (SGD), or the relation gradient sink
   const float* lr;
   float* nrm_sink;            // data parallel: normals gradient sink (null: SGD in place)
+  int64_t R;
 };
 
 __device__ __forceinline__ float4 f4sub(float4 a, float4 b) {
@@ -136,222 +140,399 @@ __device__ __forceinline__ uint32_t rel_of_tile(const RelTiles& rt, uint32_t t) 
   return lo;
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined relation tiles. One persistent CTA per SM walks a contiguous range
+// of the batch's tiles [T b / G, T (b + 1) / G): a loader warp chases each
+// tile's row ids and streams the head / tail rows into a kStages-deep shared
+// ring with 16-byte cp.async (no registers held across the copy latency); 8
+// compute warps own 4 (pos, neg) pairs each, so a pair's hinge never leaves
+// its warp. Relation-side sums are accumulated per warp over the CTA's run of
+// one relation and flushed once per (CTA, relation run) to slot b + k (unique:
+// CTA ranges are ordered); the run that completes a relation sums the slots in
+// CTA order, applies SGD to d_r / w_r and renormalizes w_r.
+constexpr int kCompute = kPairs / kHalf;       // compute warps
+#ifndef SKG_TRANSH_LOADERS
+#define SKG_TRANSH_LOADERS 4
+#endif
+constexpr int kLoaders = SKG_TRANSH_LOADERS;   // copy warps (one warp's cp.async stream cannot fill an SM's L2 bandwidth)
+constexpr int kPipeThreads = (kCompute + kLoaders) * 32;
+constexpr int kLoaderWarp = kCompute;          // first loader: enumerates the tiles, writes the stage metadata
+#ifndef SKG_TH_STAGES
+#define SKG_TH_STAGES 3
+#endif
+constexpr int kStages = SKG_TH_STAGES;
+static_assert(kPairs % kLoaders == 0, "loaders split a tile's pairs evenly");
+
+struct PipeMeta {
+  int4 rows[kRows];  // warp-major: rows 8w..8w+3 = pos of pairs 4w..4w+3, 8w+4.. = their negatives
+  float wr[kD], dr[kD];  // w_r and d_r rows (copied with the stage)
+  int k, r, np;
+  uint32_t first, end;  // relation k's tile range [first, end)
+};
+struct PipeSmem {
+  float H[kStages][kRows * kStride];  // head rows (v overwrites them)
+  float Tl[kStages][kRows * kStride]; // tail rows
+  PipeMeta meta[kStages];
+  float4 wpart[kCompute][2][32];
+  RelTiles rt;
+  float wl[kCompute];
+  uint64_t full[kStages], empty[kStages];
+  uint32_t ntile, t0, T;
+  int last_cta;
+};
+
+// CTA b's tiles start at range_start(b): T b / G when every CTA gets a tile,
+// else one tile each for b < T, so the CTAs meeting a relation are always a
+// contiguous run of non-empty ranges.
+__device__ __forceinline__ uint32_t range_start(uint32_t b, uint32_t T, uint32_t G) {
+  return T >= G ? static_cast<uint32_t>((static_cast<uint64_t>(T) * b) / G) : min(b, T);
+}
+// Transpose-reduce of kRowsPerWarp per-lane partials (one per row) over the
+// warp in a fixed tree: each level hands half of the rows to the partner lane,
+// then the remaining lanes of a row are summed; afterwards p[0] on lane L holds
+// row (L >> kLaneRowShift)'s total, bitwise equal on that row's lanes.
+// 9 (8 rows) / 6 (4 rows) shuffles instead of rows x 5.
+__device__ __forceinline__ void warp_reduce_rows(float (&p)[kRowsPerWarp]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int n = kRowsPerWarp / 2, m = 16; n >= 1; n >>= 1, m >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int q = 0; q < n; ++q) {
+      const float send = up ? p[q] : p[q + n];
+      const float keep = up ? p[q + n] : p[q];
+      p[q] = __fadd_rn(keep, __shfl_xor_sync(kFull, send, m));
+    }
+  }
+#pragma unroll
+  for (int m = kLanesPerRow / 2; m >= 1; m >>= 1) p[0] = __fadd_rn(p[0], __shfl_xor_sync(kFull, p[0], m));
+}
+
+// embedding.cpp:181-189 on one normal, by a warp (normals_renorm_kernel's order:
+// lane-strided squares, then the warp tree)
+__device__ __forceinline__ void renorm_normal(float* normals, int64_t r, int lane, uint32_t* err) {
+  float* row = normals + r * kD;
+  float x[kD / 32];
+  float ss = 0.f;
+#pragma unroll
+  for (int q = 0; q < kD / 32; ++q) {
+    x[q] = row[lane + 32 * q];
+    ss = __fadd_rn(ss, __fmul_rn(x[q], x[q]));
+  }
+  const float nn = __fsqrt_rn(warp_sum_bcast(ss));
+  if (!(nn > 0.f)) {
+    if (lane == 0 && atomicCAS(&err[0], 0u, static_cast<uint32_t>(kErrNormalCollapsed)) == 0u)
+      err[2] = static_cast<uint32_t>(r);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < kD / 32; ++q) row[lane + 32 * q] = __fdiv_rn(x[q], nn);
+}
+
+__device__ __forceinline__ uint32_t cta_of_tile(uint32_t t, uint32_t T, uint32_t G) {  // max j: range_start(j) <= t
+  return T >= G ? static_cast<uint32_t>(((static_cast<uint64_t>(t) + 1) * G - 1) / T) : t;
+}
+
+// Debug phase stamps (globaltimer ns) of one chosen minibatch, off unless
+// enabled through skg_debug_transh_trace: [CTA < 160][event < 32].
+constexpr int kThTrCtas = 160, kThTrEvents = 32;
+__device__ unsigned long long g_thtrace[kThTrCtas * kThTrEvents];
+__device__ int g_thtrace_on;
+__device__ __forceinline__ void th_stamp(bool on, int ev) {
+  if (on && blockIdx.x < kThTrCtas && ev < kThTrEvents) stamp_now(&g_thtrace[blockIdx.x * kThTrEvents + ev]);
+}
+
 template <bool L2>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) transh_tile_kernel(const TArgs a) {
-  extern __shared__ float4 smv[];
-  float* Vs = reinterpret_cast<float*>(smv);  // [kRows][kStride]
-  __shared__ int4 rows[kRows];                 // {head, tail, incidence row (-1: padding), 0}
-  __shared__ float score[kRows];
-  __shared__ float wloss[kThreads / 32];
-  __shared__ float4 accs[2][kThreads / 32][32];
-  __shared__ bool last, rel_last;
-  __shared__ RelTiles rt;
+__global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
   const FwdArgs& f = a.f;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (f.stamp_start && blockIdx.x == 0 && tid == 0) stamp_now(f.stamp_start);
   const bool alive = f.err[0] == 0;
-  if (warp == 0 && alive) enumerate_rel_tiles(a, rt);
-  __syncthreads();
-  const uint32_t T = alive ? static_cast<uint32_t>(min(static_cast<int64_t>(rt.first[rt.nrel]), a.mt)) : 0u;
-  float lsum = 0.f;
-  uint32_t pend = 0;
-  // Row ids of tile tt for pair kk = tid < 64: stage 1 reads the relation
-  // segment entry (positive row = batch position), stage 2 its pair record.
-  // The next tile's chase is issued while the current tile computes.
-  auto stage1 = [&](uint32_t tt, int kk) -> int {
-    const uint32_t kq = rel_of_tile(rt, tt);
-    const uint32_t sq = rt.seg[kq], pq = (tt - rt.first[kq]) * kPairs;
-    const uint32_t e0q = __ldg(a.seg_start + sq), lenq = __ldg(a.seg_start + sq + 1) - e0q;
-    const int npq = static_cast<int>(min(static_cast<uint32_t>(kPairs), lenq / 2 - pq));
-    return kk < npq ? static_cast<int>(__ldg(a.ent_val + e0q + pq + kk) & 0x7fffffffu) : -1;
-  };
-  auto stage2 = [&](int pos, int4& pr, int4& ng) {
-    pr = make_int4(0, 0, -1, 0);
-    ng = make_int4(0, 0, -1, 0);
-    if (pos < 0) return;
-    int h, tt, nh, nt;
-    if (f.pair_ht) {
-      const int4 x = __ldg(f.pair_ht + pos);
-      h = x.x, tt = x.y, nh = x.z, nt = x.w;
-    } else {
-      const int id = __ldg(f.order + pos);
-      h = __ldg(f.H + id), tt = __ldg(f.T + id), nh = __ldg(f.NH + id), nt = __ldg(f.NT + id);
-    }
-    pr = make_int4(h, tt, pos, 0);
-    ng = make_int4(nh, nt, pos + f.B, 0);
-  };
-  int4 pr_next = make_int4(0, 0, -1, 0), ng_next = make_int4(0, 0, -1, 0);
-  int pos_next = -1;
-  if (tid < kPairs && blockIdx.x < T) stage2(stage1(blockIdx.x, tid), pr_next, ng_next);
-  for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
-    const uint32_t k = rel_of_tile(rt, t);
-    const uint32_t sseg = rt.seg[k], p0 = (t - rt.first[k]) * kPairs;
-    const uint32_t e0 = __ldg(a.seg_start + sseg), len = __ldg(a.seg_start + sseg + 1) - e0;
-    const int64_t r = static_cast<int64_t>(__ldg(a.seg_col + sseg)) - f.N;
-    const int np = static_cast<int>(min(static_cast<uint32_t>(kPairs), len / 2 - p0));
-    (void)e0;
-    const float4 w = __ldg(reinterpret_cast<const float4*>(f.normals + r * kD) + lane);
-    const float4 drv = __ldg(reinterpret_cast<const float4*>(f.X + (f.N + r) * kD) + lane);
-    if (tid < kPairs) {
-      rows[tid] = pr_next;
-      rows[kPairs + tid] = ng_next;
-    }
-    __syncthreads();
-    const uint32_t tn = t + gridDim.x;
-    if (tid < kPairs && tn < T) pos_next = stage1(tn, tid);  // in flight during this tile
-    // ---- u, wu, v for this warp's 8 rows, all 16 row loads in flight
-    const int m0 = warp * kRowsPerWarp;
-    float4 u[kRowsPerWarp];
-    float wu[kRowsPerWarp];
-    {
-      float4 xh[kRowsPerWarp], xt[kRowsPerWarp];
-#pragma unroll
-      for (int q = 0; q < kRowsPerWarp; ++q) {
-        const int4 rw = rows[m0 + q];
-        xh[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rw.x) * kD) + lane);
-        xt[q] = __ldg(reinterpret_cast<const float4*>(f.X + static_cast<size_t>(rw.y) * kD) + lane);
-      }
-      float part[kRowsPerWarp];
-#pragma unroll
-      for (int q = 0; q < kRowsPerWarp; ++q) {
-        u[q] = rows[m0 + q].z >= 0 ? f4sub(xh[q], xt[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        part[q] = f4dot(w, u[q]);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int q = 0; q < kRowsPerWarp; ++q) part[q] = __fadd_rn(part[q], __shfl_xor_sync(kFull, part[q], o));
-#pragma unroll
-      for (int q = 0; q < kRowsPerWarp; ++q) {
-        wu[q] = part[q];
-        const float4 v = f4sub(f4add(u[q], drv), f4scale(wu[q], w));
-        *reinterpret_cast<float4*>(Vs + (m0 + q) * kStride + 4 * lane) = v;
-      }
-    }
+  const uint32_t G = gridDim.x;
+  const bool tr = g_thtrace_on == f.batch + 1;
+  if (tid == 0) th_stamp(tr, 0);
+  if (warp == kLoaderWarp) {
+    if (alive) enumerate_rel_tiles(a, S.rt);
     __syncwarp();
-    // ---- score (lane j < 8 owns row m0 + j): reference-order squared_sum / abs_sum
-    float ssum = 0.f;
-    bool bad = false;
-    const int mj = m0 + (lane & 7);
-    const int row2 = rows[mj].z;
-    {  // whole warp, reference association (warp_norm8); row j lands on lane j
-      bool b = false;
-      const float sj = warp_norm8<L2>(Vs + m0 * kStride, kStride, kD, lane, b);
-      if (lane < kRowsPerWarp) {
-        ssum = sj;
-        bad = b;
-        score[mj] = L2 ? __fsqrt_rn(ssum) : ssum;
+    if (blockIdx.x == 0 && alive)
+      for (uint32_t q = lane; q < S.rt.nrel; q += 32) {
+        a.info[4 + 3 * q] = static_cast<uint32_t>(__ldg(a.seg_col + S.rt.seg[q]) - static_cast<uint32_t>(a.f.N));
+        a.info[5 + 3 * q] = S.rt.first[q];
+        a.info[6 + 3 * q] = S.rt.first[q + 1];
       }
-    }
-    __syncthreads();
-    if (tid < kPairs && tn < T) stage2(pos_next, pr_next, ng_next);
-    // ---- pair hinge (training.cpp:73-94)
-    const int kk = mj & (kPairs - 1);
-    const bool valid = lane < kRowsPerWarp && kk < np;
-    float term = 0.f;
-    if (valid) term = __fsub_rn(__fadd_rn(f.margin, score[kk]), score[kPairs + kk]);
-    const bool act = valid && term > 0.f;
-    const float up = act ? (mj < kPairs ? f.unit : -f.unit) : 0.f;
-    const float sc = act ? (L2 ? __fdiv_rn(up, __fsqrt_rn(__fadd_rn(ssum, kNormEpsF))) : up) : 0.f;
-    if (valid) f.scal[row2] = act ? 1.f : 0.f;
-    if (valid && bad && (L2 || act)) pend |= kPendEntity;
-    {
-      float tk = (act && mj < kPairs) ? term : 0.f;
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) tk = __fadd_rn(tk, __shfl_down_sync(kFull, tk, o));
-      if (lane == 0) wloss[warp] = tk;
-    }
-    // ---- backward rows (hyperplane_backward, models.hpp:106-113)
-    const unsigned amask = __ballot_sync(kFull, act);
-    float4 acc_dz = make_float4(0.f, 0.f, 0.f, 0.f), acc_n = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (amask) {
-      float4 dz[kRowsPerWarp];
-      float part[kRowsPerWarp];
-#pragma unroll
-      for (int q = 0; q < kRowsPerWarp; ++q) {
-        const float scq = __shfl_sync(kFull, sc, q);
-        dz[q] = dir4<L2>(*reinterpret_cast<const float4*>(Vs + (m0 + q) * kStride + 4 * lane), scq);
-        if (!((amask >> q) & 1u)) dz[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        part[q] = f4dot(dz[q], w);
+    if (lane == 0) {
+      const uint32_t T = alive ? static_cast<uint32_t>(min(static_cast<int64_t>(S.rt.first[S.rt.nrel]), a.mt)) : 0u;
+      const uint32_t t0 = range_start(blockIdx.x, T, G), t1 = range_start(blockIdx.x + 1, T, G);
+      S.T = T;
+      S.t0 = t0;
+      S.ntile = t1 - t0;
+      if (blockIdx.x == 0 && alive) {  // the batch's relation runs, for transh_rel_finalize_kernel
+        a.info[0] = S.rt.nrel;
+        a.info[1] = T;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int q = 0; q < kRowsPerWarp; ++q) part[q] = __fadd_rn(part[q], __shfl_xor_sync(kFull, part[q], o));
-#pragma unroll
-      for (int q = 0; q < kRowsPerWarp; ++q) {
-        if (!((amask >> q) & 1u)) continue;
-        const float dzw = part[q];
-        const int r2 = rows[m0 + q].z;
-        reinterpret_cast<float4*>(f.res_u + static_cast<size_t>(r2) * kD)[lane] = f4sub(dz[q], f4scale(dzw, w));
-        acc_dz = f4add(acc_dz, dz[q]);
-        acc_n = f4add(acc_n, f4add(f4scale(dzw, u[q]), f4scale(wu[q], dz[q])));
+      for (int i = 0; i < kStages; ++i) {
+        tc::mbar_init(&S.full[i], 32 * kLoaders + 1);  // cp.async arrivals of every loader lane + the metadata arrive
+        tc::mbar_init(&S.empty[i], kCompute);
       }
+      tc::fence_barrier_init();
     }
-    accs[0][warp][lane] = acc_dz;
-    accs[1][warp][lane] = acc_n;
-    __syncthreads();
-    if (tid < 64) {  // tile partial: warps in order
-      const int which = tid >> 5;
-      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int q = 0; q < kThreads / 32; ++q) s = f4add(s, accs[which][q][lane]);
-      reinterpret_cast<float4*>(a.partial + (static_cast<size_t>(t) * 2 + which) * kD)[lane] = s;
-      __threadfence();
-    }
-    if (tid == 0)
-      for (int q = 0; q < kPairs / kRowsPerWarp; ++q) lsum = __fadd_rn(lsum, wloss[q]);
-    __syncthreads();
-    // the CTA finishing a relation's last tile sums its tile partials in tile
-    // order and applies SGD to the relation row and the normal
-    // (grads.normals -= nrm, models.hpp:112; embedding.cpp:165-190)
-    const uint32_t lo = rt.first[k], hi = rt.first[k + 1];
-    if (tid == 0) {
-      rel_last = atomicAdd(a.rel_ticket + k, 1u) == hi - lo - 1;
-      if (rel_last) a.rel_ticket[k] = 0;  // every tile of k has arrived: ready for the next batch
-    }
-    __syncthreads();
-    if (rel_last && tid < 2 * kD) {
-      // thread (c, v): column c of the relation gradient (v = 0) or of the
-      // normal's (v = 1); 16 tiles' loads in flight, added in tile order
-      __threadfence();
-      const int c = tid & (kD - 1), v = tid / kD;
-      const float* src = a.partial + static_cast<size_t>(v) * kD + c;
-      float g = 0.f;
-      uint32_t q = lo;
-      for (; q + 16 <= hi; q += 16) {
-        float x[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) x[e] = __ldcg(src + static_cast<size_t>(q + e) * 2 * kD);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) g = __fadd_rn(g, x[e]);
-      }
-      for (; q < hi; ++q) g = __fadd_rn(g, __ldcg(src + static_cast<size_t>(q) * 2 * kD));
-      if (a.nrm_sink) {  // data parallel: this rank's gradient rows (summed over ranks, then one dense step)
-        if (v == 0) a.rel[r * kD + c] = g;
-        else a.nrm_sink[r * kD + c] = -g;
-      } else {
-        const float step = *a.lr;
-        float* p = v == 0 ? a.rel + r * kD + c : const_cast<float*>(f.normals) + r * kD + c;
-        *p = __fsub_rn(*p, __fmul_rn(step, v == 0 ? g : -g));
-      }
-    }
-    __syncthreads();  // rows / score / accs reuse by the next tile
   }
+  __syncthreads();
+  if (tid == 0) th_stamp(tr, 1);
+  const uint32_t ntile = S.ntile, t0 = S.t0, T = S.T;
+  uint32_t pend = 0;
+
+  if (warp >= kLoaderWarp) {
+    // ------------------------------------------------------------ loaders
+    // Row ids of kChase tiles are chased together (lane = pair; their
+    // dependent ent_val -> pair record loads overlap), then each tile's rows
+    // are copied into its stage as the stage frees up. Every loader warp
+    // chases the same ids (L1 hits) and copies kPairs / kLoaders pairs.
+    const int lw = warp - kLoaderWarp;
+    const bool lead = lw == 0;
+    constexpr int kChase = 4;
+    for (uint32_t g = 0; g < ntile; g += kChase) {
+      int pos[kChase], np[kChase];
+      uint32_t kq[kChase];
+#pragma unroll
+      for (int c = 0; c < kChase; ++c) {
+        pos[c] = -1;
+        np[c] = 0;
+        kq[c] = 0;
+        if (g + c < ntile) {
+          const uint32_t t = t0 + g + c;
+          kq[c] = rel_of_tile(S.rt, t);
+          const uint32_t sq = S.rt.seg[kq[c]], pq = (t - S.rt.first[kq[c]]) * kPairs;
+          const uint32_t e0 = __ldg(a.seg_start + sq), len = __ldg(a.seg_start + sq + 1) - e0;
+          np[c] = static_cast<int>(min(static_cast<uint32_t>(kPairs), len / 2 - pq));
+          if (lane < np[c]) pos[c] = static_cast<int>(__ldg(a.ent_val + e0 + pq + lane) & 0x7fffffffu);
+        }
+      }
+      if (lead && lane == 0 && g == 0) th_stamp(tr, 2);
+      int4 pr[kChase], ng[kChase];
+#pragma unroll
+      for (int c = 0; c < kChase; ++c) {
+        pr[c] = make_int4(0, 0, -1, 0);
+        ng[c] = make_int4(0, 0, -1, 0);
+        if (pos[c] >= 0) {
+          int h, tt, nh, nt;
+          if (f.pair_ht) {
+            const int4 x = __ldg(f.pair_ht + pos[c]);
+            h = x.x, tt = x.y, nh = x.z, nt = x.w;
+          } else {
+            const int id = __ldg(f.order + pos[c]);
+            h = __ldg(f.H + id), tt = __ldg(f.T + id), nh = __ldg(f.NH + id), nt = __ldg(f.NT + id);
+          }
+          pr[c] = make_int4(h, tt, pos[c], 0);
+          ng[c] = make_int4(nh, nt, pos[c] + f.B, 0);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kChase; ++c) {
+        const uint32_t i = g + c;
+        if (i >= ntile) break;
+        const int s = static_cast<int>(i % kStages);
+        if (i >= kStages) tc::mbar_wait(&S.empty[s], ((i / kStages) - 1) & 1);
+        PipeMeta& M = S.meta[s];
+        if (lead) {
+          const int mp = kRowsPerWarp * (lane / kHalf) + lane % kHalf;  // warp-major slot of pair `lane`
+          M.rows[mp] = pr[c];
+          M.rows[mp + kHalf] = ng[c];
+          const int64_t r = static_cast<int64_t>(__ldg(a.seg_col + S.rt.seg[kq[c]])) - f.N;
+          if (lane == 0) {
+            M.k = static_cast<int>(kq[c]);
+            M.r = static_cast<int>(r);
+            M.np = np[c];
+            M.first = S.rt.first[kq[c]];
+            M.end = S.rt.first[kq[c] + 1];
+          }
+          tc::cp_async16(M.wr + 4 * lane, f.normals + r * kD + 4 * lane);
+          tc::cp_async16(M.dr + 4 * lane, f.X + (f.N + r) * kD + 4 * lane);
+        }
+        // rows: lane = 16-byte chunk of a 512-byte row
+        float* Hs = S.H[s];
+        float* Ts = S.Tl[s];
+#pragma unroll 4
+        for (int p = lw * (kPairs / kLoaders); p < (lw + 1) * (kPairs / kLoaders); ++p) {
+          const int hp = __shfl_sync(kFull, pr[c].x, p), tp = __shfl_sync(kFull, pr[c].y, p);
+          const int hn = __shfl_sync(kFull, ng[c].x, p), tn = __shfl_sync(kFull, ng[c].y, p);
+          const int m = kRowsPerWarp * (p / kHalf) + p % kHalf;
+          tc::cp_async16(Hs + m * kStride + 4 * lane, f.X + static_cast<size_t>(hp) * kD + 4 * lane);
+          tc::cp_async16(Ts + m * kStride + 4 * lane, f.X + static_cast<size_t>(tp) * kD + 4 * lane);
+          tc::cp_async16(Hs + (m + kHalf) * kStride + 4 * lane, f.X + static_cast<size_t>(hn) * kD + 4 * lane);
+          tc::cp_async16(Ts + (m + kHalf) * kStride + 4 * lane, f.X + static_cast<size_t>(tn) * kD + 4 * lane);
+        }
+        tc::cp_async_mbar_arrive(&S.full[s]);
+        __syncwarp();
+        if (lead && lane == 0) {
+          tc::mbar_arrive(&S.full[s]);
+          if (i < 4) th_stamp(tr, 3 + static_cast<int>(i));
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ compute
+    const int m0 = warp * kRowsPerWarp;
+    float lw = 0.f;  // this warp's loss terms, tile order
+    float4 acc_dz = make_float4(0.f, 0.f, 0.f, 0.f), acc_n = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 w = make_float4(0.f, 0.f, 0.f, 0.f), drv = w;
+    int run = -1, run_r = 0;
+    // (CTA, run) flush: warps in order -> slot b + k; the run completing relation
+    // k sums the slots in CTA order and applies SGD (+ renormalization of w_r)
+    auto flush = [&]() {
+      S.wpart[warp][0][lane] = acc_dz;
+      S.wpart[warp][1][lane] = acc_n;
+      tc::named_sync(1, kCompute * 32);
+      if (tid < 64) {
+        const int which = tid >> 5;
+        float4 sum = S.wpart[0][which][lane];
+#pragma unroll
+        for (int q = 1; q < kCompute; ++q) sum = f4add(sum, S.wpart[q][which][lane]);
+        reinterpret_cast<float4*>(a.partial + (static_cast<size_t>(blockIdx.x + run) * 2 + which) * kD)[lane] = sum;
+      }
+      tc::named_sync(1, kCompute * 32);  // wpart free for the next run
+      acc_dz = make_float4(0.f, 0.f, 0.f, 0.f);
+      acc_n = acc_dz;
+    };
+    for (uint32_t i = 0; i < ntile; ++i) {
+      const int s = static_cast<int>(i % kStages);
+      tc::mbar_wait(&S.full[s], (i / kStages) & 1);
+      if (tid == 0 && i < 4) th_stamp(tr, 7 + static_cast<int>(i));
+      const PipeMeta& M = S.meta[s];
+      if (M.k != run) {
+        if (run >= 0) flush();
+        run = M.k;
+        run_r = M.r;
+        w = reinterpret_cast<const float4*>(M.wr)[lane];
+        drv = reinterpret_cast<const float4*>(M.dr)[lane];
+      }
+      const int np = M.np;
+      float* Hs = S.H[s] + m0 * kStride;
+      const float* Ts = S.Tl[s] + m0 * kStride;
+      // ---- u, wu, v for the warp's 8 rows, all in registers (lane = 4 columns)
+      float4 u[kRowsPerWarp], v[kRowsPerWarp];
+      float wu[kRowsPerWarp];
+      int rz[kRowsPerWarp];  // incidence row of each row (-1: padding)
+      {
+        float part[kRowsPerWarp];
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+          const float4 xh = *reinterpret_cast<const float4*>(Hs + q * kStride + 4 * lane);
+          const float4 xt = *reinterpret_cast<const float4*>(Ts + q * kStride + 4 * lane);
+          rz[q] = M.rows[m0 + q].z;
+          u[q] = f4sub(xh, xt);
+        }
+        // everything this warp needs from the stage is in registers: release it
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.empty[s]);
+        if (tid == 0 && i < 2) th_stamp(tr, 19 + 4 * static_cast<int>(i));
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+          if (rz[q] < 0) u[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          part[q] = f4dot(w, u[q]);
+        }
+        warp_reduce_rows(part);
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+          wu[q] = __shfl_sync(kFull, part[0], kLanesPerRow * q);
+          v[q] = f4sub(f4add(u[q], drv), f4scale(wu[q], w));
+        }
+      }
+      if (tid == 0 && i < 2) th_stamp(tr, 20 + 4 * static_cast<int>(i));
+      // ---- score: squared / absolute sums reduced in a fixed tree (lane 4q.. holds row q)
+      float ssum;
+      unsigned nfbits = 0;
+      {
+        float part[kRowsPerWarp];
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+          const float4 x = v[q];
+          if (nonfinite(x.x) | nonfinite(x.y) | nonfinite(x.z) | nonfinite(x.w)) nfbits |= 1u << q;
+          part[q] = __fadd_rn(__fadd_rn(norm_term<L2>(x.x), norm_term<L2>(x.y)),
+                              __fadd_rn(norm_term<L2>(x.z), norm_term<L2>(x.w)));
+        }
+        warp_reduce_rows(part);
+        ssum = part[0];
+      }
+      nfbits = __reduce_or_sync(kFull, nfbits);
+      const int qrow = lane >> kLaneRowShift;     // this lane's row (its lanes hold identical sums)
+      const float score = L2 ? __fsqrt_rn(ssum) : ssum;
+      // ---- pair hinge (training.cpp:73-94): rows 0-3 pos of pairs 4w..4w+3, rows 4-7 their negatives
+      const int jq = qrow % kHalf;
+      const int pidx = kHalf * warp + jq;
+      const float sother = __shfl_xor_sync(kFull, score, 16);
+      const bool is_pos = qrow < kHalf;
+      const bool valid = pidx < np;
+      const float term = valid ? (is_pos ? __fsub_rn(__fadd_rn(f.margin, score), sother)
+                                         : __fsub_rn(__fadd_rn(f.margin, sother), score))
+                               : 0.f;
+      const bool act = valid && term > 0.f;
+      const float up = act ? (is_pos ? f.unit : -f.unit) : 0.f;
+      const float sc = act ? (L2 ? __fdiv_rn(up, __fsqrt_rn(__fadd_rn(ssum, kNormEpsF))) : up) : 0.f;
+      if (lane % kLanesPerRow == 0) {
+        int row2 = rz[0];
+#pragma unroll
+        for (int q = 1; q < kRowsPerWarp; ++q) row2 = qrow == q ? rz[q] : row2;
+        if (valid) f.scal[row2] = act ? 1.f : 0.f;
+        if (valid && ((nfbits >> qrow) & 1u) && (L2 || act)) pend |= kPendEntity;
+      }
+      {
+        float tk = (act && is_pos && lane % kLanesPerRow == 0) ? term : 0.f;  // first lane of each pos row
+#pragma unroll
+        for (int o = 8; o >= kLanesPerRow; o >>= 1) tk = __fadd_rn(tk, __shfl_down_sync(kFull, tk, o));
+        lw = __fadd_rn(lw, __shfl_sync(kFull, tk, 0));
+      }
+      if (tid == 0 && i < 2) th_stamp(tr, 21 + 4 * static_cast<int>(i));
+      // ---- backward rows (hyperplane_backward, models.hpp:106-113)
+      const unsigned amask = __ballot_sync(kFull, act);  // row q active <=> bit kLanesPerRow * q
+      if (amask) {
+        float4 dz[kRowsPerWarp];
+        float part[kRowsPerWarp];
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+          const float scq = __shfl_sync(kFull, sc, kLanesPerRow * q);
+          dz[q] = ((amask >> (kLanesPerRow * q)) & 1u) ? dir4<L2>(v[q], scq) : make_float4(0.f, 0.f, 0.f, 0.f);
+          part[q] = f4dot(dz[q], w);
+        }
+        warp_reduce_rows(part);
+        if (tid == 0 && i < 2) th_stamp(tr, 22 + 4 * static_cast<int>(i));
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+          const float dzw = __shfl_sync(kFull, part[0], kLanesPerRow * q);
+          if (!((amask >> (kLanesPerRow * q)) & 1u)) continue;
+          const int r2 = rz[q];
+          reinterpret_cast<float4*>(f.res_u + static_cast<size_t>(r2) * kD)[lane] = f4sub(dz[q], f4scale(dzw, w));
+          acc_dz = f4add(acc_dz, dz[q]);
+          acc_n = f4add(acc_n, f4add(f4scale(dzw, u[q]), f4scale(wu[q], dz[q])));
+        }
+      }
+      if (tid == 0 && i < 4) th_stamp(tr, 11 + static_cast<int>(i));
+    }
+    if (tid == 0) th_stamp(tr, 15);
+    if (run >= 0) flush();
+    if (tid == 0) th_stamp(tr, 16);
+    if (lane == 0) S.wl[warp] = lw;
+  }
+  // ---- loss: warps in order -> one partial per CTA, the last CTA finalizes
   pend = __reduce_or_sync(kFull, pend);
   if (lane == 0 && pend) {
     atomicOr(&f.err[3], pend);
     __threadfence();
   }
+  __syncthreads();
+  if (tid == 0) th_stamp(tr, 17);
   if (!alive) return;
-  // ---- loss: one partial per tile (tile order), the last CTA finalizes
   if (tid == 0) {
+    float lsum = 0.f;
+    for (int q = 0; q < kCompute; ++q) lsum = __fadd_rn(lsum, S.wl[q]);
     f.block_partial[blockIdx.x] = lsum;
     __threadfence();
-    last = atomicAdd(f.counter, 1u) == gridDim.x - 1;
+    S.last_cta = atomicAdd(f.counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && warp == 0) {
+  if (S.last_cta && warp == 0) {
     __threadfence();
     float acc = 0.f;
     for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, f.block_partial[b]);
@@ -373,33 +554,90 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) transh_tile_kernel(const
       *f.counter = 0;
     }
   }
+  if (tid == 0) th_stamp(tr, 18);
+}
+
+// Relation side of the batch (runs beside the entity segment pass; both read
+// only the forward's outputs): block k < runs sums relation run k's (CTA, run)
+// slots in CTA order (cta_of_tile's partition), applies SGD to d_r and w_r and
+// renormalizes w_r; block b also renormalizes normal b when relation b is
+// absent from the batch (embedding.cpp:165-190 steps every row, then
+// renormalizes every normal). Data parallel (nrm_sink): the slot sums go to
+// the sinks and the dense step + renormalization follow the all-reduce.
+__global__ void __launch_bounds__(2 * kD) transh_rel_finalize_kernel(const TArgs a, uint32_t G) {
+  const FwdArgs& f = a.f;
+  if (f.err[0] != 0) return;  // nothing is applied for a failing batch
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t b = blockIdx.x, nrel = a.info[0], T = a.info[1];
+  if (b < nrel) {
+    const int64_t r = a.info[4 + 3 * b];
+    const uint32_t j0 = cta_of_tile(a.info[5 + 3 * b], T, G), j1 = cta_of_tile(a.info[6 + 3 * b] - 1, T, G);
+    const int c = tid & (kD - 1), v = tid / kD;  // (column, vector)
+    const float* src = a.partial + static_cast<size_t>(v) * kD + c;
+    float g = 0.f;
+    uint32_t j = j0;
+    for (; j + 8 <= j1 + 1; j += 8) {
+      float x[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = __ldcg(src + static_cast<size_t>(j + e + b) * 2 * kD);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) g = __fadd_rn(g, x[e]);
+    }
+    for (; j <= j1; ++j) g = __fadd_rn(g, __ldcg(src + static_cast<size_t>(j + b) * 2 * kD));
+    if (a.nrm_sink) {  // data parallel: this rank's gradient rows (summed over ranks, then one dense step)
+      if (v == 0) a.rel[r * kD + c] = g;
+      else a.nrm_sink[r * kD + c] = -g;
+      return;
+    }
+    const float step = *a.lr;
+    float* p = v == 0 ? a.rel + r * kD + c : const_cast<float*>(f.normals) + r * kD + c;
+    *p = __fsub_rn(*p, __fmul_rn(step, v == 0 ? g : -g));  // grads.normals -= nrm (models.hpp:112)
+    __syncthreads();
+    if (warp == 0) renorm_normal(const_cast<float*>(f.normals), r, lane, f.err);
+  }
+  if (a.nrm_sink || static_cast<int64_t>(b) >= a.R || warp != 0) return;
+  bool present = false;
+  for (uint32_t q0 = 0; q0 < nrel && !present; q0 += 32) {
+    const uint32_t q = q0 + lane;
+    present = __any_sync(kFull, q < nrel && a.info[4 + 3 * q] == b);
+  }
+  if (!present) renorm_normal(const_cast<float*>(f.normals), b, lane, f.err);
 }
 
 }  // namespace
 
 bool transh_tiles_supported(int de, int dr, int64_t R) { return de == kD && dr == kD && R <= kMaxRelSeg; }
 
+int64_t transh_trace(int enable, unsigned long long* out, int64_t cap) {
+  SKG_CUDA(cudaMemcpyToSymbol(g_thtrace_on, &enable, sizeof(int)));
+  const int64_t n = static_cast<int64_t>(kThTrCtas) * kThTrEvents;
+  if (enable) {
+    static const unsigned long long zeros[kThTrCtas * kThTrEvents] = {};
+    SKG_CUDA(cudaMemcpyToSymbol(g_thtrace, zeros, sizeof(zeros)));
+  }
+  if (out && cap >= n) SKG_CUDA(cudaMemcpyFromSymbol(out, g_thtrace, sizeof(unsigned long long) * n));
+  return n;
+}
+
 int64_t transh_tiles_work_floats(int64_t rows, int64_t R) {
   const int64_t mt = relation_max_tiles(rows, R);
-  return mt * 2 * kD + R + 64;
+  return (mt + R + 1) * 2 * kD + 3 * R + 64;  // run info, then (CTA, relation run) slots b + k, b < grid <= mt
 }
 
 void configure_transh_tiles_kernels() {
-  const int smem = static_cast<int>(sizeof(float) * kRows * kStride);
-  SKG_CUDA(cudaFuncSetAttribute(transh_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  SKG_CUDA(cudaFuncSetAttribute(transh_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int smem = static_cast<int>(sizeof(PipeSmem));
+  SKG_CUDA(cudaFuncSetAttribute(transh_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  SKG_CUDA(cudaFuncSetAttribute(transh_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 }
 
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
-                              cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks) {
+                              cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks,
+                              const Branch* br) {
   const int64_t mt = relation_max_tiles(2 * static_cast<int64_t>(fa.B), R);
-  // tickets lead the workspace (a fixed address for every batch size), the
-  // float4 tile partials follow
-  uint32_t* ticket = reinterpret_cast<uint32_t*>(work);
-  float* partial = work + ((R + 1 + 3) & ~static_cast<int64_t>(3));
-  // per-relation tickets: zeroed at the epoch's first batch, then reset by the
-  // CTA that retires each relation (no memset node between the batch kernels)
-  if (ba.batch == 0) SKG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(uint32_t) * (R + 1), s));
+  // run info leads the workspace (a fixed address for every batch size), the
+  // float4 run partials follow
+  uint32_t* info = reinterpret_cast<uint32_t*>(work);
+  float* partial = work + ((4 + 3 * R + 3) & ~static_cast<int64_t>(3));
   TArgs a{};
   a.f = fa;
   a.ent_val = ba.ent_val;
@@ -409,21 +647,36 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   a.batch = ba.batch;
   a.mt = mt;
   a.partial = partial;
-  a.rel_ticket = ticket;
+  a.info = info;
   a.rel = sinks ? sinks->rel : const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
   a.lr = ba.lr;
   a.nrm_sink = sinks ? sinks->normals : nullptr;
-  const size_t smem = sizeof(float) * kRows * kStride;
-  const unsigned grid =
-      static_cast<unsigned>(std::min<int64_t>(mt, static_cast<int64_t>(num_sms) * kCtasPerSm));  // persistent
-  if (l2) transh_tile_kernel<true><<<grid, kThreads, smem, s>>>(a);
-  else transh_tile_kernel<false><<<grid, kThreads, smem, s>>>(a);
+  a.R = R;
+  const size_t smem = sizeof(PipeSmem);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, num_sms));  // persistent, one CTA per SM
+  if (l2) transh_pipe_kernel<true><<<grid, kPipeThreads, smem, s>>>(a);
+  else transh_pipe_kernel<false><<<grid, kPipeThreads, smem, s>>>(a);
   count_launch();
   SKG_LAUNCH_CHECK();
   if (mark) (*mark)();
+  // relation side on a forked branch, beside the entity segment pass
+  cudaStream_t rs = s;
+#ifdef SKG_TH_NOBRANCH
+  br = nullptr;
+#endif
+  if (br) {
+    SKG_CUDA(cudaEventRecord(br->fork, s));
+    SKG_CUDA(cudaStreamWaitEvent(br->aux, br->fork, 0));
+    rs = br->aux;
+  }
+  transh_rel_finalize_kernel<<<static_cast<unsigned>(std::max<int64_t>(R, 1)), 2 * kD, 0, rs>>>(a, grid);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+  if (br) SKG_CUDA(cudaEventRecord(br->join, br->aux));
   BwdArgs eb = ba;
   eb.entity_only = 1;
   launch_segment_backward(kPlainRows, sinks == nullptr, eb, num_sms, s);  // sink: ba.X is the entity gradient
+  if (br) SKG_CUDA(cudaStreamWaitEvent(s, br->join, 0));
 }
 
 }  // namespace skg
