@@ -361,13 +361,25 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
 // Permutation + (data-parallel shard) + transposed-incidence plan of one epoch
 // into plan slot `slot`. Depends only on the seed, the triples and the
 // negatives, so the next epoch's plan can be built while this one trains.
-void enqueue_plan(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s) {
-  PlanSlot& ps = ctx->slots[slot];
-  uint64_t* seed = ctx->seed_eff.p + slot;
+void copy_floats(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s);
+
+void gen_perm(skg_ctx* ctx, const EpochShape& es, const uint64_t* seed, int32_t* dst, cudaStream_t s) {
   if (es.shuffle)
-    device_shuffle(seed, ctx->M, ps.order.p, ctx->shuffle, s);
+    device_shuffle(seed, ctx->M, dst, ctx->shuffle, s);
   else
-    device_iota(ps.order.p, ctx->M, s);
+    device_iota(dst, ctx->M, s);
+}
+
+void build_plan_from_order(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s);
+
+void enqueue_plan(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s) {
+  gen_perm(ctx, es, ctx->seed_eff.p + slot, ctx->slots[slot].order.p, s);
+  build_plan_from_order(ctx, es, slot, s);
+}
+
+// The transposed-incidence plan of slot `slot` from the permutation in its order buffer.
+void build_plan_from_order(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s) {
+  PlanSlot& ps = ctx->slots[slot];
   if (ctx->shard) {  // this rank's forward pairs + the owned-column plan of the global batches
     shard_order_kernel<<<grid_for(es.Mg), 256, 0, s>>>(ps.order.p, es.B, es.S, es.rank, es.nb, es.i0_last, es.Mg,
                                                         ps.order_g.p);
@@ -588,6 +600,7 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
     for (auto& sl : ctx->slots) sl.order_g.ensure(es.Mg + 1);
     if (ctx->dp) ctx->dp_grad.ensure(ctx->N * ctx->de + ctx->R * ctx->dr + ctx->proj.n + ctx->normals.n + 2);
   }
+  for (auto& p : ctx->perm) p.ensure(ctx->M + 1);
   for (auto& sl : ctx->slots) {
     sl.order.ensure(ctx->M + 1);
     if (!ctx->shard) sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
@@ -631,7 +644,7 @@ std::string raw_key(const T&... v) {
 std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
   return raw_key(es.B, es.nb, es.shuffle, es.kind, ctx->M, ctx->tables.p, ctx->H.p, ctx->NH.p, ctx->quad.p,
                  ctx->slots[0].order.p,
-                 ctx->slots[1].order.p, ctx->res.p, ctx->ht_work.p, ctx->slots[0].plan.cap_entries,
+                 ctx->slots[1].order.p, ctx->perm[0].p, ctx->perm[1].p, ctx->res.p, ctx->ht_work.p, ctx->slots[0].plan.cap_entries,
                  ctx->slots[1].plan.cap_entries, ctx->shuffle.cap_n, es.world, es.rank, ctx->dp_grad.p,
                  ctx->slots[0].order_g.p, ctx->slots[1].order_g.p, ctx->proj.p, ctx->normals.p, margin,
                  // shapes baked into the captured launches (strides, relation offset, plan id space)
@@ -728,10 +741,18 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
   try {
     SKG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
     SKG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
-    enqueue_plan(ctx, es, nxt, ctx->side);
+    SKG_CUDA(cudaStreamWaitEvent(ctx->side2, ctx->fork_ev, 0));
+    // side: epoch + 1's plan from its permutation (shuffled during the previous epoch)
+    copy_floats(reinterpret_cast<const float*>(ctx->perm[nxt].p), reinterpret_cast<float*>(ctx->slots[nxt].order.p),
+                ctx->M, ctx->num_sms, ctx->side);
+    build_plan_from_order(ctx, es, nxt, ctx->side);
     SKG_CUDA(cudaEventRecord(ctx->join_ev, ctx->side));
+    // side2: epoch + 2's permutation (seed slot 2 + cur)
+    gen_perm(ctx, es, ctx->seed_eff.p + 2 + cur, ctx->perm[cur].p, ctx->side2);
+    SKG_CUDA(cudaEventRecord(ctx->join2_ev, ctx->side2));
     enqueue_batches(ctx, es, cur, ctx->stream, nullptr);
     SKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev, 0));
+    SKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join2_ev, 0));
   } catch (...) {
     cudaStreamEndCapture(ctx->stream, &g);
     if (g) cudaGraphDestroy(g);
@@ -759,6 +780,7 @@ void skg::drop_graphs(skg_ctx* ctx) {
     ctx->graphs[k] = nullptr;
     ctx->graph_keys[k].clear();
     ctx->slots[k].key.clear();
+    ctx->perm_key[k].clear();
   }
 }
 
@@ -816,7 +838,7 @@ struct StagedEpoch {
   int cur = 0, nxt = 1;
   int64_t eager = 0;
   int64_t epoch = 0;
-  std::string next_key;
+  std::string next_key, perm_key;
 };
 
 StagedEpoch stage_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc, int64_t epoch,
@@ -842,8 +864,19 @@ StagedEpoch stage_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_tra
   if (is_mult(cfg) && has_self_loops(ctx)) {
     train_until_degenerate(ctx, es, epoch, cur);  // always throws
   }
-  // Speculatively build epoch + 1's plan (same data and schedule) alongside.
-  set_slot_seed(ctx, nxt, epoch_seed(tc.seed, epoch + 1));
+  // Speculatively build epoch + 1's plan (same data and schedule) alongside,
+  // from its permutation (normally shuffled by the previous epoch's graph),
+  // and shuffle epoch + 2's permutation beside it.
+  const std::string pk1 = plan_key(ctx, es, tc, epoch + 1);
+  if (ctx->perm_key[nxt] != pk1) {
+    set_slot_seed(ctx, nxt, epoch_seed(tc.seed, epoch + 1));
+    const int64_t before = kernel_launches();
+    gen_perm(ctx, es, ctx->seed_eff.p + nxt, ctx->perm[nxt].p, ctx->stream);
+    sg.eager += kernel_launches() - before;
+    ctx->perm_key[nxt] = pk1;
+  }
+  set_slot_seed(ctx, 2 + cur, epoch_seed(tc.seed, epoch + 2));
+  ctx->perm_key[cur].clear();
   ctx->slots[nxt].key.clear();
   // Margin is baked into the forward launches, so it is part of the graph key.
   const std::string gk = graph_key(ctx, es, tc.margin);
@@ -852,7 +885,8 @@ StagedEpoch stage_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_tra
     capture_epoch_graph(ctx, es, cur);
     ctx->graph_keys[cur] = gk;
   }
-  sg.next_key = plan_key(ctx, es, tc, epoch + 1);
+  sg.next_key = pk1;
+  sg.perm_key = plan_key(ctx, es, tc, epoch + 2);
   return sg;
 }
 
@@ -863,6 +897,7 @@ void fire_epoch(skg_ctx* ctx, const StagedEpoch& sg) {
   ctx->last_launches = ctx->graph_launches_k[sg.cur] + sg.eager;
   ctx->last_slot = sg.cur;
   ctx->slots[sg.nxt].key = sg.next_key;
+  ctx->perm_key[sg.cur] = sg.perm_key;
   ctx->cur = sg.nxt;
 }
 
@@ -872,6 +907,7 @@ void complete_epoch(skg_ctx* ctx, const StagedEpoch& sg, skg_epoch_report* rep) 
     finish_epoch(ctx, es, sg.epoch, rep);
   } catch (...) {
     ctx->slots[sg.nxt].key.clear();  // a failed epoch leaves no reusable prefetch
+    ctx->perm_key[sg.cur].clear();
     throw;
   }
   float ms = 0.f;
@@ -1127,6 +1163,8 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaEventCreate(&ctx->ev1));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    SKG_CUDA(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->join2_ev, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->up, cudaStreamNonBlocking));
@@ -1137,9 +1175,9 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
     ctx->err_words.ensure(4);
     ctx->counter.ensure(1);
-    ctx->seed_eff.ensure(2);
+    ctx->seed_eff.ensure(4);
     ctx->lr_dev.ensure(2);
-    SKG_CUDA(cudaMallocHost(&ctx->h_seed, sizeof(uint64_t) * 2));
+    SKG_CUDA(cudaMallocHost(&ctx->h_seed, sizeof(uint64_t) * 4));
     SKG_CUDA(cudaMallocHost(&ctx->h_lr, sizeof(float) * 2));
     SKG_CUDA(cudaMallocHost(&ctx->h_err, sizeof(uint32_t) * 4));
     SKG_CUDA(cudaMallocHost(&ctx->h_spec, sizeof(uint32_t) * 4));
@@ -1168,6 +1206,8 @@ void skg_destroy(skg_ctx* ctx) {
   if (ctx->h_stamps) cudaFreeHost(ctx->h_stamps);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->side2) cudaStreamDestroy(ctx->side2);
+  if (ctx->join2_ev) cudaEventDestroy(ctx->join2_ev);
   if (ctx->aux_fork) cudaEventDestroy(ctx->aux_fork);
   if (ctx->aux_join) cudaEventDestroy(ctx->aux_join);
   if (ctx->up) {
@@ -1526,6 +1566,7 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   copy_floats(ctx->backup.p + op, ctx->proj.p, np, ctx->num_sms, ctx->stream);
   copy_floats(ctx->backup.p + on, ctx->normals.p, nn, ctx->num_sms, ctx->stream);
   for (auto& sl : ctx->slots) sl.key.clear();
+  for (auto& k : ctx->perm_key) k.clear();
   ctx->has_neg = false;
   if (bad_tri) {  // set_triples' error (incidence.hpp:26-29: entity check first)
     ctx->triples_valid = false;
@@ -2073,6 +2114,8 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const sk
     ctx->last_slot = ctx->cur;
     ctx->slots[0].key.clear();
     ctx->slots[1].key.clear();
+    ctx->perm_key[0].clear();
+    ctx->perm_key[1].clear();
     finish_epoch(ctx, es, epoch, rep);
     auto el = [&](size_t a, size_t b) {
       float ms = 0.f;

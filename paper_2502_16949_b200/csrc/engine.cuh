@@ -113,6 +113,13 @@ struct skg_ctx {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaStream_t aux = nullptr;  // per-batch side branch (TransH relation step beside the entity pass)
   cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
+  // Epoch permutations two epochs ahead: the graph of epoch e builds e + 1's
+  // plan from perm[nxt] (made during epoch e - 1) while a second side branch
+  // shuffles e + 2's order into perm[cur]; perm_key says which epoch each holds.
+  skg::DevBuf<int32_t> perm[2];
+  std::string perm_key[2];
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t join2_ev = nullptr;
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   std::string graph_keys[2];
   int64_t graph_launches_k[2] = {0, 0};
