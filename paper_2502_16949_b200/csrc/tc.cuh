@@ -48,6 +48,20 @@ __device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr, uint32_t sbo
   return d;
 }
 
+// MN-major SWIZZLE_128B_BASE32B descriptor (layout type 1; the only MN-major
+// tf32 layout): atoms of 4 K-rows x 128 B with 32-byte chunks XOR-swizzled
+// by (row & 3); LBO = stride between 32-element MN blocks, SBO = stride
+// between 4-row K groups (tools/umma_mn_probe.cu).
+__device__ __forceinline__ uint64_t make_desc_sw128_32b(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  d |= 1ull << 61;
+  return d;
+}
+
 // Instruction descriptor for kind::tf32 with an fp32 accumulator.
 __host__ __device__ constexpr uint32_t make_idesc_tf32(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4)                                   // D format F32

@@ -39,15 +39,22 @@ namespace {
 constexpr int kD = 128;
 constexpr int kRows = 128;
 constexpr int kPairs = 64;
-constexpr int kThreads = 384;
-constexpr int kMmaWarp = 8, kRowWarp = 10, kGatherWarp = 11;  // warp 9: ring loader
+#ifndef SKG_TR_GATHER_WARPS
+#define SKG_TR_GATHER_WARPS 4
+#endif
+constexpr int kGatherWarps = SKG_TR_GATHER_WARPS;  // one warp's cp.async stream cannot fill an SM's L2 bandwidth
+constexpr int kMmaWarp = 8, kRowWarp = 10, kGatherWarp = 11;  // warp 9: ring loader; gather warps 11 ..
+constexpr int kThreads = (kGatherWarp + kGatherWarps) * 32;
 
-// sU / sDZ: K-major SWIZZLE_128B (m = row, k = feature) in four 32-feature
-// column blocks of 128 rows x 128 B; 16-byte unit (r, c4) =
-// block * 1024 + r * 8 + ((c4 & 7) ^ (r & 7)). A row's 32 units land in
-// distinct bank groups per 128 B, so both the coalesced row gather (lane =
-// chunk) and the thread-per-row epilogue stores are conflict-free.
-__device__ __forceinline__ int tile_unit(int r, int c4) { return (c4 >> 3) * 1024 + r * 8 + ((c4 & 7) ^ (r & 7)); }
+// sU / sDZ: row tiles (m = row, feature) in four 32-feature column blocks of
+// 128 rows x 128 B, 32-byte chunks XOR-swizzled by (row & 3): the
+// SWIZZLE_128B_BASE32B layout, so GEMM3 reads both tiles in place as MN-major
+// operands (K = rows, MN = features; LBO = the 16 KB block stride, SBO = 512 B
+// per 4 rows — tools/umma_mn_probe.cu). 16-byte unit (r, c4) =
+// block * 1024 + r * 8 + (((c4 & 7) >> 1) ^ (r & 3)) * 2 + (c4 & 1).
+__device__ __forceinline__ int swz32(int r, int c4) { return ((((c4 & 7) >> 1) ^ (r & 3)) << 1) | (c4 & 1); }
+__device__ __forceinline__ int tile_unit(int r, int c4) { return (c4 >> 3) * 1024 + r * 8 + swz32(r, c4); }
+constexpr uint32_t kTileLBO = 1024 * 16, kSBO32 = 4 * 128;
 
 
 // Ring chunk of M_r: 128 (n) x 16 (k), hi then lo; unit (n, k4) = (n & 7) + (n >> 3) * 32 + k4 * 8.
@@ -62,16 +69,19 @@ constexpr int kRing = 3;
 #define SKG_APPLY_Y 32  // relation-parallel blocks x 32 slices of the 16 K-element proj block
 #endif
 
-// GEMM3 staging slot: 8 rows (K) of DZ^T and U^T, hi and lo; arrays [128][8]
-// with unit (i, k4) = (i & 7) + (i >> 3) * 18 + k4 * 9 (padded: the producers'
-// transposing stores hit 32 distinct banks).
+// GEMM3 (dM += DZ^T U, K = rows) in slots of 8 rows: the hi terms are the raw
+// sDZ / sU rows read in place (the tensor core truncates fp32 to tf32); only
+// lo = x - trunc(x) of DZ and U is staged, row-major in the same swizzle
+// (8 rows x 4 blocks of 128 B: LBO = 1 KB, SBO = 512 B), no transposition.
 constexpr int kG3Rows = 8;
-constexpr int kG3Units = 16 * 18;
-constexpr int kG3ArrFloats = kG3Units * 4;
-constexpr uint32_t kG3LBO = 9 * 16, kG3SBO = 18 * 16;
-constexpr int kG3Slots = 2;
+constexpr int kG3ArrFloats = kG3Rows * kD;
+constexpr uint32_t kG3LBO = kG3Rows * 128;
+#ifndef SKG_TR_G3_SLOTS
+#define SKG_TR_G3_SLOTS 4
+#endif
+constexpr int kG3Slots = SKG_TR_G3_SLOTS;
 constexpr int kG3PerTile = kRows / kG3Rows;
-__device__ __forceinline__ int g3_off(int i, int k) { return (((i & 7) + (i >> 3) * 18 + (k >> 2) * 9) << 2) + (k & 3); }
+__device__ __forceinline__ int g3_unit(int r, int c4) { return (c4 >> 3) * (kG3Rows * 8) + r * 8 + swz32(r, c4); }
 
 // TMEM columns: [0,128) U hi -> DZ hi and [128,256) U lo -> DZ lo (A operands
 // of GEMM1 / GEMM2 read straight from TMEM), [256,384) V, then dU (GEMM2
@@ -93,7 +103,7 @@ struct Smem {
   float U[kRows * kD];
   float DZ[kRows * kD];
   float ring[kRing][2 * kChunkFloats];
-  float g3[kG3Slots][4][kG3ArrFloats];  // DZ^T hi, DZ^T lo, U^T hi, U^T lo
+  float g3[kG3Slots][2][kG3ArrFloats];  // DZ lo, U lo (1 KB-aligned slots)
   int4 rows[2][kRows];                  // {head, tail, incidence row (-1: padding), 0}
   float rel[2][kD];
   int np[2];
@@ -103,7 +113,7 @@ struct Smem {
   uint64_t g_full, u_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty;
   uint64_t rows_full[2], rows_empty[2];
   uint64_t g3_full[kG3Slots], g3_empty[kG3Slots];
-  uint64_t stg[kRows / 8];  // row group s staged: its sU / sDZ rows may be refilled
+  uint64_t stg[kRows / 8];  // row group s consumed by GEMM3: its sU / sDZ rows may be refilled
   uint64_t ring_full[kRing], ring_empty[kRing];
   uint32_t tmem_base;
   int last;
@@ -127,6 +137,39 @@ __device__ __forceinline__ void st_global_v8(float* p, const uint32_t* v) {  // 
   asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
                "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
+}
+
+// lo = x - trunc(x) of slot s3's 8 rows of DZ and U into ring slot (it * 16 + s3) % kG3Slots;
+// thread t < 128: row t >> 4 of the slot, 16-byte units t & 15 and (t & 15) + 16.
+#ifndef SKG_TR_STAGE_STEP
+#define SKG_TR_STAGE_STEP 2
+#endif
+constexpr int kStageStep = SKG_TR_STAGE_STEP;  // 2: producers stage even slots, epilogue warps odd ones
+__device__ __forceinline__ void stage_slot(Smem& S, uint32_t it, int s3, int t) {
+  const uint32_t g3n = it * kG3PerTile + static_cast<uint32_t>(s3);
+  const int slot = static_cast<int>(g3n % kG3Slots);
+  if (g3n >= kG3Slots) tc::mbar_wait(&S.g3_empty[slot], ((g3n / kG3Slots) - 1) & 1);
+  const int rq = t >> 4, cq = t & 15;
+  const int row = s3 * kG3Rows + rq;
+  float* Alo = S.g3[slot][0];
+  float* Blo = S.g3[slot][1];
+#pragma unroll
+  for (int h2 = 0; h2 < 2; ++h2) {
+    const int c4 = cq + 16 * h2;
+    const float4 dz = *reinterpret_cast<const float4*>(S.DZ + 4 * tile_unit(row, c4));
+    const float4 u = *reinterpret_cast<const float4*>(S.U + 4 * tile_unit(row, c4));
+    const int o = 4 * g3_unit(rq, c4);
+    *reinterpret_cast<float4*>(Alo + o) = make_float4(tc::tf32_trunc_lo(dz.x), tc::tf32_trunc_lo(dz.y),
+                                                      tc::tf32_trunc_lo(dz.z), tc::tf32_trunc_lo(dz.w));
+    *reinterpret_cast<float4*>(Blo + o) = make_float4(tc::tf32_trunc_lo(u.x), tc::tf32_trunc_lo(u.y),
+                                                      tc::tf32_trunc_lo(u.z), tc::tf32_trunc_lo(u.w));
+  }
+  tc::fence_async_shared();
+  tc::mbar_arrive(&S.g3_full[slot]);
+}
+
+__device__ __forceinline__ float4 f4sel(int c, float4 a, float4 b) {  // c ? a : b
+  return make_float4(c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w);
 }
 
 __device__ __forceinline__ uint32_t idesc128() { return tc::make_idesc_tf32(128, 128, 0, 0); }
@@ -193,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
   if (tid == 0) {
-    tc::mbar_init(&S.g_full, 32);
+    tc::mbar_init(&S.g_full, 32 * kGatherWarps);
     tc::mbar_init(&S.u_full, 128);
     tc::mbar_init(&S.v_full, 1);
     tc::mbar_init(&S.dz_full, 128);
@@ -209,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&S.rows_full[i], 1);
       tc::mbar_init(&S.rows_empty[i], 128);
     }
-    for (int i = 0; i < kRows / 8; ++i) tc::mbar_init(&S.stg[i], 128);
+    for (int i = 0; i < kRows / 8; ++i) tc::mbar_init(&S.stg[i], 1);
     for (int i = 0; i < kRing; ++i) {
       tc::mbar_init(&S.ring_full[i], 1);
       tc::mbar_init(&S.ring_empty[i], 1);
@@ -312,8 +355,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           dz[q] = sc == 0.f ? 0.f : (L2 ? __fmul_rn(x, sc) : (x > 0.f ? sc : (x < 0.f ? -sc : 0.f)));
         }
 #pragma unroll
-        for (int q = 0; q < 32; q += 4)
-          *reinterpret_cast<float4*>(S.DZ + 4 * tile_unit(m, (c + q) >> 2)) = make_float4(dz[q], dz[q + 1], dz[q + 2], dz[q + 3]);
+        for (int q = 0; q < 32; q += 8) {  // unit pairs in swapped order on rows with bit 2 set (see the producers)
+          const int fl = (m >> 2) & 1;
+          const float4 a = make_float4(dz[q], dz[q + 1], dz[q + 2], dz[q + 3]);
+          const float4 b = make_float4(dz[q + 4], dz[q + 5], dz[q + 6], dz[q + 7]);
+          const int ua = tile_unit(m, (c + q) >> 2), ub = tile_unit(m, (c + q + 4) >> 2);
+          *reinterpret_cast<float4*>(S.DZ + 4 * (fl ? ub : ua)) = f4sel(fl, b, a);
+          *reinterpret_cast<float4*>(S.DZ + 4 * (fl ? ua : ub)) = f4sel(fl, a, b);
+        }
         float lo[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) lo[q] = tc::tf32_trunc_lo(dz[q]);
@@ -340,6 +389,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_arrive(&S.dz_full);
       if (m == 0) trace(it, 12);
       tc::named_sync(1, 128);
+      if (kStageStep == 2)  // the odd GEMM3 slots (sDZ rows of the other epilogue warps are written: named_sync above)
+        for (int s3 = 1; s3 < kG3PerTile; s3 += 2) stage_slot(S, it, s3, m);
       dr_acc = __fadd_rn(dr_acc, __fadd_rn(__fadd_rn(S.colsum[0][m], S.colsum[1][m]),
                                            __fadd_rn(S.colsum[2][m], S.colsum[3][m])));
       if (m == 0) lsum = __fadd_rn(lsum, __fadd_rn(S.tl[0], S.tl[1]));
@@ -399,7 +450,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int p = tid - 128;   // row p == TMEM lane p (warp quadrant = warp % 4)
     const int pw = warp - 4;
     const uint32_t lane_addr = static_cast<uint32_t>(pw * 32) << 16;
-    uint32_t g3n = 0;
     for (uint32_t it = 0; it < ntile; ++it) {
       const int buf = it & 1;
       tc::mbar_wait(&S.rows_full[buf], (it >> 1) & 1);
@@ -414,18 +464,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_after();
       }
       const bool ok = rows[p].z >= 0;
+      const int flip = (p >> 2) & 1;
 #pragma unroll 1
       for (int c = 0; c < kD; c += 16) {
         float hi[16], lo[16];
+        float4 uv[4];
 #pragma unroll
         for (int q = 0; q < 16; q += 4) {
-          float4* up = reinterpret_cast<float4*>(S.U + 4 * tile_unit(p, (c + q) >> 2));
+          // rows p and p + 4 share a swizzled 32-byte chunk: rows with bit 2 set
+          // visit the two 16-byte units of each chunk in swapped order, so the
+          // eight rows of a quarter-warp phase touch eight distinct units
+          const int j = (q >> 2) ^ flip;
+          float4* up = reinterpret_cast<float4*>(S.U + 4 * tile_unit(p, (c >> 2) + j));
           const float4 xh = *up;
-          const float4 xt = *reinterpret_cast<const float4*>(S.DZ + 4 * tile_unit(p, (c + q) >> 2));
+          const float4 xt = *reinterpret_cast<const float4*>(S.DZ + 4 * tile_unit(p, (c >> 2) + j));
           const float4 u = ok ? make_float4(__fsub_rn(xh.x, xt.x), __fsub_rn(xh.y, xt.y), __fsub_rn(xh.z, xt.z),
                                             __fsub_rn(xh.w, xt.w))
                               : make_float4(0.f, 0.f, 0.f, 0.f);
           *up = u;
+          uv[q >> 2] = u;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+          const float4 u = f4sel(flip, uv[(q >> 2) ^ 1], uv[q >> 2]);
           hi[q] = u.x, hi[q + 1] = u.y, hi[q + 2] = u.z, hi[q + 3] = u.w;
           lo[q] = tc::tf32_trunc_lo(u.x);
           lo[q + 1] = tc::tf32_trunc_lo(u.y);
@@ -439,52 +500,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::fence_before();
       tc::mbar_arrive(&S.u_full);
       if (p == 0) trace(it, 2);
-      // GEMM3 staging: DZ^T and U^T, 8 rows per slot, split hi (rna) / lo;
-      // each staged row group's sU / sDZ rows are refilled with the next
-      // tile's head / tail rows by the gather warp
+      // GEMM3 staging (even slots; the epilogue warps stage the odd ones)
       tc::mbar_wait(&S.dz_full, it & 1);
       if (p == 0) trace(it, 3);
-      const int kq = p & 7, ig = p >> 3;
-#pragma unroll 1
-      for (int s3 = 0; s3 < kG3PerTile; ++s3, ++g3n) {
-        const int slot = g3n % kG3Slots;
-        if (g3n >= kG3Slots) tc::mbar_wait(&S.g3_empty[slot], ((g3n / kG3Slots) - 1) & 1);
-        const int row = s3 * kG3Rows + kq;
-        float* Ahi = S.g3[slot][0];
-        float* Alo = S.g3[slot][1];
-        float* Bhi = S.g3[slot][2];
-        float* Blo = S.g3[slot][3];
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int c4 = ig + 16 * h2;
-          const float4 dz = *reinterpret_cast<const float4*>(S.DZ + 4 * tile_unit(row, c4));
-          const float4 u = *reinterpret_cast<const float4*>(S.U + 4 * tile_unit(row, c4));
-          const float dv[4] = {dz.x, dz.y, dz.z, dz.w}, uv[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int o = g3_off(4 * c4 + e, kq);
-            float hi, lo;
-            tc::split_tf32(dv[e], hi, lo);
-#ifndef SKG_TR_NO_HI_STAGE
-            Ahi[o] = hi;
-#endif
-            Alo[o] = lo;
-            tc::split_tf32(uv[e], hi, lo);
-#ifndef SKG_TR_NO_HI_STAGE
-            Bhi[o] = hi;
-#endif
-            Blo[o] = lo;
-          }
-        }
-        tc::fence_async_shared();
-        tc::mbar_arrive(&S.g3_full[slot]);
-        tc::mbar_arrive(&S.stg[s3]);
-      }
+      for (int s3 = 0; s3 < kG3PerTile; s3 += kStageStep) stage_slot(S, it, s3, p);
       if (p == 0) trace(it, 4);
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issue
     const uint32_t id = idesc128();
+    const uint32_t id3 = tc::make_idesc_tf32(128, 128, 1, 1);  // GEMM3: both operands MN-major
     uint32_t rn = 0, g3n = 0, nrun = 0;
     int run = -1;
     for (uint32_t it = 0; it < ntile; ++it) {
@@ -522,46 +547,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_wait(&S.dm_empty, (nrun - 1) & 1);
         tc::fence_after();
       }
-      // GEMM2 (dU = DZ M_r; DZ hi / lo from TMEM) interleaved with the
-      // GEMM3 slots: one GEMM2 chunk after every second slot keeps the tensor
-      // pipe busy while the producers refill the slot just released.
+      // GEMM3 over the 16 staged slots first: each slot's commit releases its
+      // row group of sU / sDZ to the next tile's gather, so the gather runs
+      // under GEMM2 (dU = DZ M_r; DZ hi / lo from TMEM), issued after it.
       tc::mbar_wait(&S.dz_full, it & 1);
       tc::fence_after();
       trace(it, 9);
+      auto gemm2_chunk = [&](int c) {
+        const int s = rn % kRing;
+        tc::mbar_wait(&S.ring_full[s], (rn / kRing) & 1);
+        tc::fence_after();
+        const uint32_t bh = tc::smem_u32(S.ring[s]), bl = bh + kChunkFloats * 4;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int ks = c * 2 + kk;
+          const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
+          const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
+          tc::mma_ts_elect(tbase + kColDU, tbase + kColHi + ks * 8, bhd, id, ks > 0 ? 1u : 0u);
+          tc::mma_ts_elect(tbase + kColDU, tbase + kColHi + ks * 8, bld, id, 1u);
+          tc::mma_ts_elect(tbase + kColDU, tbase + kColLo + ks * 8, bhd, id, 1u);
+        }
+        tc::commit_elect(&S.ring_empty[s]);
+        ++rn;
+      };
       for (int s3 = 0; s3 < kG3PerTile; ++s3, ++g3n) {
         const int slot = g3n % kG3Slots;
         tc::mbar_wait(&S.g3_full[slot], (g3n / kG3Slots) & 1);
         tc::fence_after();
         if (s3 == 0) trace(it, 7);
-        const uint32_t base = tc::smem_u32(S.g3[slot][0]);
-        const uint64_t ahi = tc::make_desc(base, kG3LBO, kG3SBO);
-        const uint64_t alo = tc::make_desc(base + kG3ArrFloats * 4, kG3LBO, kG3SBO);
-        const uint64_t bhi = tc::make_desc(base + 2 * kG3ArrFloats * 4, kG3LBO, kG3SBO);
-        const uint64_t blo = tc::make_desc(base + 3 * kG3ArrFloats * 4, kG3LBO, kG3SBO);
-        tc::mma_ss_elect(tbase + kColDM, ahi, bhi, id, (first_of_run && s3 == 0) ? 0u : 1u);
-        tc::mma_ss_elect(tbase + kColDM, ahi, blo, id, 1u);
-        tc::mma_ss_elect(tbase + kColDM, alo, bhi, id, 1u);
+        const uint32_t roff = static_cast<uint32_t>(s3 * kG3Rows * 128);  // the slot's rows in sDZ / sU
+        const uint64_t ahi = tc::make_desc_sw128_32b(tc::smem_u32(S.DZ) + roff, kTileLBO, kSBO32);
+        const uint64_t bhi = tc::make_desc_sw128_32b(tc::smem_u32(S.U) + roff, kTileLBO, kSBO32);
+        const uint64_t alo = tc::make_desc_sw128_32b(tc::smem_u32(S.g3[slot][0]), kG3LBO, kSBO32);
+        const uint64_t blo = tc::make_desc_sw128_32b(tc::smem_u32(S.g3[slot][1]), kG3LBO, kSBO32);
+        tc::mma_ss_elect(tbase + kColDM, ahi, bhi, id3, (first_of_run && s3 == 0) ? 0u : 1u);
+        tc::mma_ss_elect(tbase + kColDM, ahi, blo, id3, 1u);
+        tc::mma_ss_elect(tbase + kColDM, alo, bhi, id3, 1u);
         tc::commit_elect(&S.g3_empty[slot]);
+        tc::commit_elect(&S.stg[s3]);  // row group s3 of sU / sDZ read: the gather may refill it
         if (s3 == kG3PerTile - 1 && last_of_run) tc::commit_elect(&S.dm_full);
-        if (s3 & 1) {
-          const int c = s3 >> 1;
-          const int s = rn % kRing;
-          tc::mbar_wait(&S.ring_full[s], (rn / kRing) & 1);
-          tc::fence_after();
-          const uint32_t bh = tc::smem_u32(S.ring[s]), bl = bh + kChunkFloats * 4;
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const int ks = c * 2 + kk;
-            const uint64_t bhd = tc::make_desc(bh + kk * 256, kChLBO, kChSBO);
-            const uint64_t bld = tc::make_desc(bl + kk * 256, kChLBO, kChSBO);
-            tc::mma_ts_elect(tbase + kColDU, tbase + kColHi + ks * 8, bhd, id, ks > 0 ? 1u : 0u);
-            tc::mma_ts_elect(tbase + kColDU, tbase + kColHi + ks * 8, bld, id, 1u);
-            tc::mma_ts_elect(tbase + kColDU, tbase + kColLo + ks * 8, bhd, id, 1u);
-          }
-          tc::commit_elect(&S.ring_empty[s]);
-          ++rn;
-        }
+#ifndef SKG_TR_G2_AFTER
+        if (s3 & 1) gemm2_chunk(s3 >> 1);
+#endif
       }
+#ifdef SKG_TR_G2_AFTER
+      for (int c = 0; c < kChunksPerGemm; ++c) gemm2_chunk(c);
+#endif
       trace(it, 8);
       tc::commit_elect(&S.g2_done);
       trace(it, 10);
@@ -587,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #endif
     }
-  } else if (warp == kGatherWarp) {
+  } else if (warp >= kGatherWarp) {
     // ------------------------------------------------------------ row gather
     // 16-byte cp.async per lane (lane = chunk of a 512-byte row): head rows
     // into sU, tail rows into sDZ at tile_unit; one warp keeps a tile's 256
@@ -609,8 +640,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it > 0) tc::mbar_wait(&S.stg[kG3PerTile - 1], (it - 1) & 1);
 #endif
 #pragma unroll 1
-      for (int s3 = 0; s3 < kG3PerTile; ++s3) {
-        // tile it's rows go into the row groups tile it - 1 has finished staging
+      for (int s3 = warp - kGatherWarp; s3 < kG3PerTile; s3 += kGatherWarps) {
+        // tile it's rows go into the row groups GEMM3 of tile it - 1 has consumed
         if (it > 0) tc::mbar_wait(&S.stg[s3], (it - 1) & 1);
         gather8(rows, s3 * 8);
       }
