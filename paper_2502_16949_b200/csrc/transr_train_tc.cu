@@ -108,9 +108,10 @@ struct Smem {
   float rel[2][kD];
   int np[2];
   float rs[kRows];
+  float sc[kRows];  // per-row gradient scale of the current tile (pass 2 of the producers)
   float colsum[4][kD];
   float tl[2];
-  uint64_t g_full, u_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty;
+  uint64_t g_full, u_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty, sc_full;
   uint64_t rows_full[2], rows_empty[2];
   uint64_t g3_full[kG3Slots], g3_empty[kG3Slots];
   uint64_t stg[kRows / 8];  // row group s consumed by GEMM3: its sU / sDZ rows may be refilled
@@ -170,6 +171,102 @@ __device__ __forceinline__ void stage_slot(Smem& S, uint32_t it, int s3, int t) 
 
 __device__ __forceinline__ float4 f4sel(int c, float4 a, float4 b) {  // c ? a : b
   return make_float4(c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w);
+}
+
+// U = h - t in place for row p, columns [c0, c1), hi / lo -> TMEM lane p
+// (taddr carries the warp's lane quadrant). Rows p and p + 4 share a swizzled
+// 32-byte chunk: rows with bit 2 set visit the two 16-byte units of each chunk
+// in swapped order, so the eight rows of a quarter-warp phase touch eight
+// distinct units.
+#ifndef SKG_TR_USPLIT
+#define SKG_TR_USPLIT 64
+#endif
+constexpr int kUSplit = SKG_TR_USPLIT;  // producers: columns [0, kUSplit); gather warps: the rest
+__device__ __forceinline__ void compute_u(Smem& S, uint32_t taddr, int p, bool ok, int c0, int c1) {
+  const int flip = (p >> 2) & 1;
+#pragma unroll 1
+  for (int c = c0; c < c1; c += 16) {
+    float hi[16], lo[16];
+    float4 uv[4];
+#pragma unroll
+    for (int q = 0; q < 16; q += 4) {
+      const int j = (q >> 2) ^ flip;
+      float4* up = reinterpret_cast<float4*>(S.U + 4 * tile_unit(p, (c >> 2) + j));
+      const float4 xh = *up;
+      const float4 xt = *reinterpret_cast<const float4*>(S.DZ + 4 * tile_unit(p, (c >> 2) + j));
+      const float4 u = ok ? make_float4(__fsub_rn(xh.x, xt.x), __fsub_rn(xh.y, xt.y), __fsub_rn(xh.z, xt.z),
+                                        __fsub_rn(xh.w, xt.w))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      *up = u;
+      uv[q >> 2] = u;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; q += 4) {
+      const float4 u = f4sel(flip, uv[(q >> 2) ^ 1], uv[q >> 2]);
+      hi[q] = u.x, hi[q + 1] = u.y, hi[q + 2] = u.z, hi[q + 3] = u.w;
+      lo[q] = tc::tf32_trunc_lo(u.x);
+      lo[q + 1] = tc::tf32_trunc_lo(u.y);
+      lo[q + 2] = tc::tf32_trunc_lo(u.z);
+      lo[q + 3] = tc::tf32_trunc_lo(u.w);
+    }
+    tc::tmem_st16(taddr + kColHi + c, hi);
+    tc::tmem_st16(taddr + kColLo + c, lo);
+  }
+}
+
+// Pass 2 of the epilogue for row m, columns [c0, c1): DZ = dir(V + r) * sc
+// -> sDZ (raw = tf32 hi) and TMEM hi / lo, column sums of the warp's 32 rows
+// -> colsum[w][c]. Unit pairs in swapped order on rows with bit 2 set (see
+// compute_u).
+#ifndef SKG_TR_DZSPLIT
+#define SKG_TR_DZSPLIT 64
+#endif
+constexpr int kDzSplit = SKG_TR_DZSPLIT;  // epilogue warps: columns [0, kDzSplit); producers: the rest
+template <bool L2>
+__device__ __forceinline__ void dz_pass(Smem& S, uint32_t taddr, int m, int w, float sc, const float* relr, int c0,
+                                        int c1) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int c = c0; c < c1; c += 32) {
+    uint32_t r0[16], r1[16];
+    tc::tmem_ld16_nowait(taddr + kColV + c, r0);
+    tc::tmem_ld16_nowait(taddr + kColV + c + 16, r1);
+    tc::tmem_wait_ld();
+    float dz[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const float x = __fadd_rn(__uint_as_float(q < 16 ? r0[q] : r1[q - 16]), relr[c + q]);
+      dz[q] = sc == 0.f ? 0.f : (L2 ? __fmul_rn(x, sc) : (x > 0.f ? sc : (x < 0.f ? -sc : 0.f)));
+    }
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) {
+      const int fl = (m >> 2) & 1;
+      const float4 a = make_float4(dz[q], dz[q + 1], dz[q + 2], dz[q + 3]);
+      const float4 b = make_float4(dz[q + 4], dz[q + 5], dz[q + 6], dz[q + 7]);
+      const int ua = tile_unit(m, (c + q) >> 2), ub = tile_unit(m, (c + q + 4) >> 2);
+      *reinterpret_cast<float4*>(S.DZ + 4 * (fl ? ub : ua)) = f4sel(fl, b, a);
+      *reinterpret_cast<float4*>(S.DZ + 4 * (fl ? ua : ub)) = f4sel(fl, a, b);
+    }
+    float lo[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) lo[q] = tc::tf32_trunc_lo(dz[q]);
+    tc::tmem_st16(taddr + kColHi + c, dz);
+    tc::tmem_st16(taddr + kColHi + c + 16, dz + 16);
+    tc::tmem_st16(taddr + kColLo + c, lo);
+    tc::tmem_st16(taddr + kColLo + c + 16, lo + 16);
+    // transpose-reduce the 32 x 32 block: lane l ends with the column c + l sum
+#pragma unroll
+    for (int ww = 16; ww >= 1; ww >>= 1) {
+      const bool upper = (lane & ww) != 0;
+#pragma unroll
+      for (int q = 0; q < ww; ++q) {
+        const float send = upper ? dz[q] : dz[q + ww];
+        const float keep = upper ? dz[q + ww] : dz[q];
+        dz[q] = __fadd_rn(keep, __shfl_xor_sync(kFull, send, ww));
+      }
+    }
+    S.colsum[w][c + lane] = dz[0];
+  }
 }
 
 __device__ __forceinline__ uint32_t idesc128() { return tc::make_idesc_tf32(128, 128, 0, 0); }
@@ -237,9 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
   if (tid == 0) {
     tc::mbar_init(&S.g_full, 32 * kGatherWarps);
-    tc::mbar_init(&S.u_full, 128);
+    tc::mbar_init(&S.u_full, kUSplit < kD ? 256 : 128);
     tc::mbar_init(&S.v_full, 1);
-    tc::mbar_init(&S.dz_full, 128);
+    tc::mbar_init(&S.dz_full, kDzSplit < kD ? 256 : 128);
+    tc::mbar_init(&S.sc_full, 128);
     tc::mbar_init(&S.g2_done, 1);
     tc::mbar_init(&S.du_empty, 128);
     tc::mbar_init(&S.dm_full, 1);
@@ -341,55 +439,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) S.tl[warp] = v;
         }
       }
-      // pass 2: DZ (norm direction * up) -> sDZ (raw = tf32 hi), lo -> TMEM; column sums of DZ
-#pragma unroll 1
-      for (int c = 0; c < kD; c += 32) {
-        uint32_t r0[16], r1[16];
-        tc::tmem_ld16_nowait(tbase + lane_addr + kColV + c, r0);
-        tc::tmem_ld16_nowait(tbase + lane_addr + kColV + c + 16, r1);
-        tc::tmem_wait_ld();
-        float dz[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const float x = __fadd_rn(__uint_as_float(q < 16 ? r0[q] : r1[q - 16]), relr[c + q]);
-          dz[q] = sc == 0.f ? 0.f : (L2 ? __fmul_rn(x, sc) : (x > 0.f ? sc : (x < 0.f ? -sc : 0.f)));
-        }
-#pragma unroll
-        for (int q = 0; q < 32; q += 8) {  // unit pairs in swapped order on rows with bit 2 set (see the producers)
-          const int fl = (m >> 2) & 1;
-          const float4 a = make_float4(dz[q], dz[q + 1], dz[q + 2], dz[q + 3]);
-          const float4 b = make_float4(dz[q + 4], dz[q + 5], dz[q + 6], dz[q + 7]);
-          const int ua = tile_unit(m, (c + q) >> 2), ub = tile_unit(m, (c + q + 4) >> 2);
-          *reinterpret_cast<float4*>(S.DZ + 4 * (fl ? ub : ua)) = f4sel(fl, b, a);
-          *reinterpret_cast<float4*>(S.DZ + 4 * (fl ? ua : ub)) = f4sel(fl, a, b);
-        }
-        float lo[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) lo[q] = tc::tf32_trunc_lo(dz[q]);
-        tc::tmem_st16(tbase + lane_addr + kColHi + c, dz);
-        tc::tmem_st16(tbase + lane_addr + kColHi + c + 16, dz + 16);
-        tc::tmem_st16(tbase + lane_addr + kColLo + c, lo);
-        tc::tmem_st16(tbase + lane_addr + kColLo + c + 16, lo + 16);
-        // transpose-reduce the 32 x 32 block: lane l ends with the column c + l sum
-#pragma unroll
-        for (int w = 16; w >= 1; w >>= 1) {
-          const bool upper = (lane & w) != 0;
-#pragma unroll
-          for (int q = 0; q < w; ++q) {
-            const float send = upper ? dz[q] : dz[q + w];
-            const float keep = upper ? dz[q + w] : dz[q];
-            dz[q] = __fadd_rn(keep, __shfl_xor_sync(kFull, send, w));
-          }
-        }
-        S.colsum[warp][c + lane] = dz[0];
-      }
+      // pass 2 (columns [0, kDzSplit); the producer warps take the rest)
+      S.sc[m] = sc;
+      if (kDzSplit < kD) tc::mbar_arrive(&S.sc_full);
+      dz_pass<L2>(S, tbase + lane_addr, m, warp, sc, relr, 0, kDzSplit);
       tc::tmem_wait_st();
       tc::fence_before();
       tc::fence_async_shared();
       tc::mbar_arrive(&S.dz_full);
       if (m == 0) trace(it, 12);
-      tc::named_sync(1, 128);
-      if (kStageStep == 2)  // the odd GEMM3 slots (sDZ rows of the other epilogue warps are written: named_sync above)
+      tc::mbar_wait(&S.dz_full, it & 1);  // every DZ row and column (and column sum) is written
+      if (kStageStep == 2)  // the odd GEMM3 slots
         for (int s3 = 1; s3 < kG3PerTile; s3 += 2) stage_slot(S, it, s3, m);
       dr_acc = __fadd_rn(dr_acc, __fadd_rn(__fadd_rn(S.colsum[0][m], S.colsum[1][m]),
                                            __fadd_rn(S.colsum[2][m], S.colsum[3][m])));
@@ -463,43 +523,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_wait(&S.g2_done, (it - 1) & 1);
         tc::fence_after();
       }
-      const bool ok = rows[p].z >= 0;
-      const int flip = (p >> 2) & 1;
-#pragma unroll 1
-      for (int c = 0; c < kD; c += 16) {
-        float hi[16], lo[16];
-        float4 uv[4];
-#pragma unroll
-        for (int q = 0; q < 16; q += 4) {
-          // rows p and p + 4 share a swizzled 32-byte chunk: rows with bit 2 set
-          // visit the two 16-byte units of each chunk in swapped order, so the
-          // eight rows of a quarter-warp phase touch eight distinct units
-          const int j = (q >> 2) ^ flip;
-          float4* up = reinterpret_cast<float4*>(S.U + 4 * tile_unit(p, (c >> 2) + j));
-          const float4 xh = *up;
-          const float4 xt = *reinterpret_cast<const float4*>(S.DZ + 4 * tile_unit(p, (c >> 2) + j));
-          const float4 u = ok ? make_float4(__fsub_rn(xh.x, xt.x), __fsub_rn(xh.y, xt.y), __fsub_rn(xh.z, xt.z),
-                                            __fsub_rn(xh.w, xt.w))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-          *up = u;
-          uv[q >> 2] = u;
-        }
-#pragma unroll
-        for (int q = 0; q < 16; q += 4) {
-          const float4 u = f4sel(flip, uv[(q >> 2) ^ 1], uv[q >> 2]);
-          hi[q] = u.x, hi[q + 1] = u.y, hi[q + 2] = u.z, hi[q + 3] = u.w;
-          lo[q] = tc::tf32_trunc_lo(u.x);
-          lo[q + 1] = tc::tf32_trunc_lo(u.y);
-          lo[q + 2] = tc::tf32_trunc_lo(u.z);
-          lo[q + 3] = tc::tf32_trunc_lo(u.w);
-        }
-        tc::tmem_st16(tbase + lane_addr + kColHi + c, hi);
-        tc::tmem_st16(tbase + lane_addr + kColLo + c, lo);
-      }
+      if (p == 0) trace(it, 15);
+      compute_u(S, tbase + lane_addr, p, rows[p].z >= 0, 0, kUSplit);
       tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(&S.u_full);
       if (p == 0) trace(it, 2);
+      if (kDzSplit < kD) {  // pass 2 of the epilogue on columns [kDzSplit, kD) of this warp's TMEM lanes
+        tc::mbar_wait(&S.sc_full, it & 1);
+        tc::fence_after();
+        dz_pass<L2>(S, tbase + lane_addr, p, pw, S.sc[p], S.rel[buf], kDzSplit, kD);
+        tc::tmem_wait_st();
+        tc::fence_before();
+        tc::fence_async_shared();
+        tc::mbar_arrive(&S.dz_full);
+      }
       // GEMM3 staging (even slots; the epilogue warps stage the odd ones)
       tc::mbar_wait(&S.dz_full, it & 1);
       if (p == 0) trace(it, 3);
@@ -646,6 +684,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         gather8(rows, s3 * 8);
       }
       tc::cp_async_mbar_arrive(&S.g_full);
+      if (kUSplit < kD) {  // columns [kUSplit, kD) of U for the rows of this warp's TMEM lane quadrant
+        const int q4 = warp & 3;
+        const int row = q4 * 32 + lane;
+        tc::mbar_wait(&S.g_full, it & 1);
+        if (it > 0) {
+          tc::mbar_wait(&S.g2_done, (it - 1) & 1);
+          tc::fence_after();
+        }
+        compute_u(S, tbase + (static_cast<uint32_t>(q4 * 32) << 16), row, rows[row].z >= 0, kUSplit, kD);
+        tc::tmem_wait_st();
+        tc::fence_before();
+        tc::mbar_arrive(&S.u_full);
+      }
     }
   } else {
     // ------------------------------------------------------------ ring loader

@@ -15,7 +15,7 @@ import bench  # noqa: E402
 from paper_2502_16949_b200 import Engine, ModelConfig, TrainConfig  # noqa: E402
 
 EV = ["pro_start", "gathered", "u_full", "pro_dz", "g3_staged", "mma_u", "g1_issued", "g3_first", "g3_issued",
-      "g2_start", "g2_issued", "epi_v", "epi_dz", "epi_g2", "epi_drained"]
+      "g2_start", "g2_issued", "epi_v", "epi_dz", "epi_g2", "epi_drained", "pro_g2ok"]
 
 
 def main():
@@ -44,7 +44,7 @@ def main():
             e = tr[cta, it]
             if e[0] == 0 or e[14] == 0:
                 continue
-            rows.append(e[:15] - e[0])
+            rows.append(e[:16] - e[0])
     rows = np.array(rows)
     print(f"{len(rows)} traced tiles; offsets from pro_start (cycles), median:")
     for i, name in enumerate(EV):
