@@ -9,6 +9,11 @@
 #include <functional>
 #include <cstring>
 #include <sstream>
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "engine.cuh"
@@ -362,6 +367,8 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
 // into plan slot `slot`. Depends only on the seed, the triples and the
 // negatives, so the next epoch's plan can be built while this one trains.
 void copy_floats(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s);
+
+void destroy_host_narrow(skg::HostNarrow* h);
 
 void gen_perm(skg_ctx* ctx, const EpochShape& es, const uint64_t* seed, int32_t* dst, cudaStream_t s) {
   if (es.shuffle)
@@ -1224,6 +1231,9 @@ void skg_destroy(skg_ctx* ctx) {
   if (ctx->h_lr) cudaFreeHost(ctx->h_lr);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->h_spec) cudaFreeHost(ctx->h_spec);
+  destroy_host_narrow(ctx->narrow);
+  ctx->narrow = nullptr;
+  if (ctx->h_stage32) cudaFreeHost(ctx->h_stage32);
   if (ctx->h_loss) cudaFreeHost(ctx->h_loss);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1493,6 +1503,136 @@ void copy_floats(const float* src, float* dst, int64_t n, int num_sms, cudaStrea
   SKG_LAUNCH_CHECK();
 }
 
+// ---- host-narrowed deferred uploads
+// The caller's five int64 id arrays are narrowed to int32 by host threads in
+// kWaves waves (triples [w L, (w + 1) L), L = ceil(m / kWaves)), wave-major in a
+// pinned buffer: wave w holds its five arrays back to back. Each wave is
+// DMA'd as soon as every thread has finished it, so the copy of half the
+// bytes overlaps the narrowing of the next wave and the running epoch. The
+// threads also do set_triples' / set_negatives' range checks (first bad
+// index per category, like spec_check_kernel). SKG_SPEC_I64=1 keeps the int64 DMA.
+constexpr int kWaves = 4;
+}  // namespace
+
+struct skg::HostNarrow {
+  std::vector<std::thread> th;
+  std::mutex mu;
+  std::condition_variable cv;
+  uint64_t gen = 0;
+  bool stop = false;
+  int nt = 1;
+  // job
+  const int64_t* src[5] = {};
+  int32_t* dst = nullptr;
+  int64_t m = 0, L = 0, n_ent = 0, n_rel = 0;
+  std::atomic<int> wave_done[kWaves];
+  std::atomic<uint32_t> bad[3];
+  explicit HostNarrow(int n) : nt(n) {
+    for (auto& w : wave_done) w = 0;
+    for (int t = 0; t < nt; ++t) th.emplace_back([this, t] { loop(t); });
+  }
+  ~HostNarrow() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
+  }
+  void loop(int t) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu);
+        cv.wait(g, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+      }
+      work(t);
+    }
+  }
+  static void atomic_min(std::atomic<uint32_t>& a, uint32_t v) {
+    uint32_t cur = a.load(std::memory_order_relaxed);
+    while (v < cur && !a.compare_exchange_weak(cur, v, std::memory_order_relaxed)) {
+    }
+  }
+  void work(int t) {
+    for (int w = 0; w < kWaves; ++w) {
+      const int64_t a = std::min<int64_t>(m, w * L), b = std::min<int64_t>(m, a + L), lw = b - a;
+      const int64_t i0 = a + lw * t / nt, i1 = a + lw * (t + 1) / nt;
+      int32_t* base = dst + 5 * a;
+      for (int k = 0; k < 5; ++k) {
+        const int64_t* s = src[k];
+        int32_t* d = base + k * lw - a;
+        const int64_t lim = k == 1 ? n_rel : n_ent;
+        bool any = false;
+        for (int64_t i = i0; i < i1; ++i) {  // vectorizable: narrow and flag, the index search only on a miss
+          const int64_t v = s[i];
+          any |= static_cast<uint64_t>(v) >= static_cast<uint64_t>(lim);
+          d[i] = static_cast<int32_t>(v);
+        }
+        if (any)
+          for (int64_t i = i0; i < i1; ++i)
+            if (static_cast<uint64_t>(s[i]) >= static_cast<uint64_t>(lim)) {
+              atomic_min(bad[k == 1 ? 1 : (k <= 2 ? 0 : 2)], static_cast<uint32_t>(i));
+              break;
+            }
+      }
+      wave_done[w].fetch_add(1, std::memory_order_release);
+    }
+  }
+  void start(const int64_t* const* s, int32_t* d, int64_t mm, int64_t ne, int64_t nr) {
+    for (int k = 0; k < 5; ++k) src[k] = s[k];
+    dst = d;
+    m = mm;
+    L = (mm + kWaves - 1) / kWaves;
+    n_ent = ne;
+    n_rel = nr;
+    for (auto& w : wave_done) w.store(0, std::memory_order_relaxed);
+    for (auto& x : bad) x.store(0xFFFFFFFFu, std::memory_order_relaxed);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      ++gen;
+    }
+    cv.notify_all();
+  }
+  void wait_wave(int w) {
+    while (wave_done[w].load(std::memory_order_acquire) < nt) std::this_thread::yield();
+  }
+};
+
+namespace {
+
+void destroy_host_narrow(skg::HostNarrow* h) { delete h; }
+
+// Compare the narrowed (wave-major) ids with the device ids the epoch used.
+__global__ void spec_check32_kernel(const int32_t* __restrict__ st, int64_t m, int64_t L,
+                                    const int32_t* __restrict__ H, const int32_t* __restrict__ Rl,
+                                    const int32_t* __restrict__ T, const int32_t* __restrict__ NH,
+                                    const int32_t* __restrict__ NT, uint32_t* __restrict__ flags) {
+  bool diff = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = (i / L) * L, lw = min(L, m - a);
+    const int32_t* b = st + 5 * a + (i - a);
+    diff |= (__ldcs(b) != __ldg(H + i)) | (__ldcs(b + lw) != __ldg(Rl + i)) | (__ldcs(b + 2 * lw) != __ldg(T + i)) |
+            (__ldcs(b + 3 * lw) != __ldg(NH + i)) | (__ldcs(b + 4 * lw) != __ldg(NT + i));
+  }
+  if (__any_sync(kFull, diff) && (threadIdx.x & 31) == 0) atomicOr(flags + 3, 1u);
+}
+
+__global__ void adopt_staged32_kernel(const int32_t* __restrict__ st, int64_t m, int64_t L, int32_t* __restrict__ H,
+                                      int32_t* __restrict__ Rl, int32_t* __restrict__ T, int32_t* __restrict__ NH,
+                                      int32_t* __restrict__ NT) {
+  int32_t* dst[5] = {H, Rl, T, NH, NT};
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t a = (i / L) * L, lw = min(L, m - a);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) dst[k][i] = st[5 * a + k * lw + (i - a)];
+  }
+}
+
 // train_epoch with a deferred (pinned, identical-shape) upload pending: the
 // copy runs on the DMA engines while the epoch trains on the current device
 // ids; identical data (the common per-epoch re-upload) keeps the result.
@@ -1512,13 +1652,48 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   ctx->spec_flags.ensure(4);
   // the copy + check are enqueued right after the epoch graph is launched
   bool launched = false;
+  static const bool i64 = [] {
+    const char* v = std::getenv("SKG_SPEC_I64");
+    return v && v[0] == '1';
+  }();
+  const bool narrowed = !i64 && m > 0;
+  if (narrowed) {
+    if (!ctx->narrow) {
+      const unsigned hc = std::thread::hardware_concurrency();
+      ctx->narrow = new HostNarrow(static_cast<int>(std::max(1u, std::min(16u, hc > 2 ? hc - 1 : 1u))));
+    }
+    if (ctx->h_stage32_cap < 5 * m) {
+      if (ctx->h_stage32) cudaFreeHost(ctx->h_stage32);
+      ctx->h_stage32 = nullptr;
+      SKG_CUDA(cudaMallocHost(&ctx->h_stage32, sizeof(int32_t) * 5 * m));
+      ctx->h_stage32_cap = 5 * m;
+    }
+    ctx->stage_i32.ensure(5 * m + 1);
+  }
   const std::function<void()> upload = [&]() {
     SKG_CUDA(cudaMemsetAsync(ctx->spec_flags.p, 0xFF, sizeof(uint32_t) * 3, ctx->up));
     SKG_CUDA(cudaMemsetAsync(ctx->spec_flags.p + 3, 0, sizeof(uint32_t), ctx->up));
-    for (int k = 0; k < 5; ++k)
-      SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, src[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice, ctx->up));
-    spec_check_kernel<<<static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms)), 256, 0, ctx->up>>>(
-        ctx->stage_i64.p, m, ctx->tN, ctx->tR, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->spec_flags.p);
+    if (narrowed) {
+      HostNarrow& hn = *ctx->narrow;
+      hn.start(src, ctx->h_stage32, m, ctx->tN, ctx->tR);
+      for (int w = 0; w < kWaves; ++w) {
+        const int64_t a = std::min<int64_t>(m, w * hn.L), b = std::min<int64_t>(m, a + hn.L);
+        hn.wait_wave(w);
+        if (b > a)
+          SKG_CUDA(cudaMemcpyAsync(ctx->stage_i32.p + 5 * a, ctx->h_stage32 + 5 * a, sizeof(int32_t) * 5 * (b - a),
+                                   cudaMemcpyHostToDevice, ctx->up));
+      }
+      ctx->upload_bytes += static_cast<int64_t>(sizeof(int32_t)) * 5 * m;
+      spec_check32_kernel<<<static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms)), 256, 0,
+                            ctx->up>>>(ctx->stage_i32.p, m, hn.L, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p,
+                                       ctx->spec_flags.p);
+    } else {
+      for (int k = 0; k < 5; ++k)
+        SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, src[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice, ctx->up));
+      ctx->upload_bytes += static_cast<int64_t>(sizeof(int64_t)) * 5 * m;
+      spec_check_kernel<<<static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms)), 256, 0, ctx->up>>>(
+          ctx->stage_i64.p, m, ctx->tN, ctx->tR, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p, ctx->spec_flags.p);
+    }
     count_launch();
     SKG_LAUNCH_CHECK();
     SKG_CUDA(cudaEventRecord(ctx->up_ev, ctx->up));
@@ -1555,6 +1730,8 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
                  us(t2 - t1), us(t3 - t2), rep->t_backward_s * 1e6);
   }
   for (int k = 0; k < 4; ++k) f[k] = ctx->h_spec[k];
+  if (narrowed)  // range checks ran on the host threads
+    for (int k = 0; k < 3; ++k) f[k] = ctx->narrow->bad[k].load(std::memory_order_relaxed);
   const bool bad_tri = f[0] != 0xFFFFFFFFu || f[1] != 0xFFFFFFFFu, bad_neg = f[2] != 0xFFFFFFFFu;
   if (!bad_tri && !bad_neg && f[3] == 0) {  // identical re-upload: the speculative epoch stands
     ++ctx->spec_hits;
@@ -1577,8 +1754,12 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     throw ShapeError("triple " + std::to_string(f[1]) + ": relation id out of range");
   }
   // adopt the uploaded ids (data changed, or the negatives are invalid)
-  narrow_staged_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->stage_i64.p, m, ctx->H.p, ctx->Rl.p, ctx->T.p,
-                                                            ctx->NH.p, ctx->NT.p);
+  if (narrowed)
+    adopt_staged32_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->stage_i32.p, m, ctx->narrow->L, ctx->H.p,
+                                                                ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p);
+  else
+    narrow_staged_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->stage_i64.p, m, ctx->H.p, ctx->Rl.p, ctx->T.p,
+                                                              ctx->NH.p, ctx->NT.p);
   count_launch();
   SKG_LAUNCH_CHECK();
   ++ctx->data_version;
@@ -1611,6 +1792,12 @@ skg_status skg_set_deferred_uploads(skg_ctx* ctx, int32_t enable) {
 
 skg_status skg_set_phase_timers(skg_ctx* ctx, int32_t enable) {
   return guard(ctx, [&] { ctx->phase_timers = enable != 0; });
+}
+
+skg_status skg_upload_bytes(skg_ctx* ctx, int64_t* bytes) {
+  return guard(ctx, [&] {
+    if (bytes) *bytes = ctx->upload_bytes;
+  });
 }
 
 skg_status skg_upload_stats(skg_ctx* ctx, int64_t* hits, int64_t* misses) {

@@ -48,6 +48,8 @@ struct ShardState;  // row-sharded tables (shard.cu)
 
 // One epoch's permutation and transposed-incidence plan. Two slots let the
 // next epoch's plan be built on a side stream while the current one trains.
+struct HostNarrow;  // engine.cu
+
 struct PlanSlot {
   DevBuf<int32_t> order, order_g;
   EpochPlan plan;
@@ -148,6 +150,11 @@ struct skg_ctx {
   skg::DevBuf<float> backup;        // parameters before a speculative epoch
   skg::DevBuf<uint32_t> spec_flags; // first bad entity / relation / negative index, changed
   int64_t spec_hits = 0, spec_misses = 0;
+  int64_t upload_bytes = 0;             // bytes DMA'd by deferred uploads (skg_upload_bytes)
+  skg::HostNarrow* narrow = nullptr;    // host threads narrowing deferred int64 uploads to int32
+  int32_t* h_stage32 = nullptr;         // pinned: narrowed ids, wave-major
+  int64_t h_stage32_cap = 0;
+  skg::DevBuf<int32_t> stage_i32;       // device copy of h_stage32
   uint32_t* h_spec = nullptr;           // pinned: the check's flags
 
   // ---- data parallel

@@ -91,6 +91,7 @@ def load_library():
         "skg_set_deferred_uploads": [vp, i32],
         "skg_set_phase_timers": [vp, i32],
         "skg_upload_stats": [vp, vp, vp],
+        "skg_upload_bytes": [vp, vp],
         "skg_set_triples": [vp, i64, vp, vp, vp, i64, i64],
         "skg_set_negatives": [vp, i64, vp, vp],
         "skg_negative_sample": [vp, C.c_uint64, i32, vp, vp],
@@ -211,6 +212,12 @@ class Engine:
     def set_phase_timers(self, enable: bool):
         """PhaseTimer buckets in EpochReport (default on; see skge_b200.h)."""
         self._check(self.L.skg_set_phase_timers(self.h, int(bool(enable))))
+
+    def upload_bytes(self):
+        """Bytes DMA'd host -> device by deferred re-uploads so far (skg_upload_bytes)."""
+        b = C.c_int64()
+        self._check(self.L.skg_upload_bytes(self.h, C.byref(b)))
+        return b.value
 
     def upload_stats(self):
         """(hits, misses) of deferred re-uploads: identical data kept / rolled back and retrained."""
