@@ -14,7 +14,8 @@ cap() {  # name config kernel-regex skip
 }
 cap C1_fwd C1 hrt_forward 20
 cap C1_bwd C1 segment_backward 20
-cap C2_tile C2 transh_tile 10
+cap C2_tile C2 transh_pipe 10
+cap C2_fin C2 transh_rel_finalize 10
 cap C2_bwd C2 segment_backward 10
 cap C3_fwd C3 hrt_forward 12
 cap C3_bwd C3 segment_backward 12
@@ -26,6 +27,6 @@ cap C5_scatter C5 radix_scatter 8
 cap M1_fwd M1 mult_forward 20
 cap M1_bwd M1 segment_backward 20
 # summaries on the box (the .ncu-rep files stay there: gpurun_out merges are capped at 64 MiB)
-python tools/make_profiles.py --src gpurun_out/prof --out gpurun_out/profiles_new > gpurun_out/make_profiles.log 2>&1
+python tools/make_profiles.py --src gpurun_out/prof --round ${ROUND:-r02} --out gpurun_out/profiles_new > gpurun_out/make_profiles.log 2>&1
 rm -f gpurun_out/prof/*.ncu-rep
 echo done
