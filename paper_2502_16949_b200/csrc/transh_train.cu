@@ -210,13 +210,13 @@ __device__ __forceinline__ void warp_reduce_rows(float (&p)[kRowsPerWarp]) {
 
 // embedding.cpp:181-189 on one normal, by a warp (normals_renorm_kernel's order:
 // lane-strided squares, then the warp tree)
-__device__ __forceinline__ void renorm_normal(float* normals, int64_t r, int lane, uint32_t* err) {
-  float* row = normals + r * kD;
+__device__ __forceinline__ void renorm_normal(float* normals, int64_t r, int d, int lane, uint32_t* err) {
+  float* row = normals + r * d;
   float x[kD / 32];
   float ss = 0.f;
 #pragma unroll
   for (int q = 0; q < kD / 32; ++q) {
-    x[q] = row[lane + 32 * q];
+    x[q] = lane + 32 * q < d ? row[lane + 32 * q] : 0.f;
     ss = __fadd_rn(ss, __fmul_rn(x[q], x[q]));
   }
   const float nn = __fsqrt_rn(warp_sum_bcast(ss));
@@ -226,7 +226,8 @@ __device__ __forceinline__ void renorm_normal(float* normals, int64_t r, int lan
     return;
   }
 #pragma unroll
-  for (int q = 0; q < kD / 32; ++q) row[lane + 32 * q] = __fdiv_rn(x[q], nn);
+  for (int q = 0; q < kD / 32; ++q)
+    if (lane + 32 * q < d) row[lane + 32 * q] = __fdiv_rn(x[q], nn);
 }
 
 __device__ __forceinline__ uint32_t cta_of_tile(uint32_t t, uint32_t T, uint32_t G) {  // max j: range_start(j) <= t
@@ -242,7 +243,7 @@ __device__ __forceinline__ void th_stamp(bool on, int ev) {
   if (on && blockIdx.x < kThTrCtas && ev < kThTrEvents) stamp_now(&g_thtrace[blockIdx.x * kThTrEvents + ev]);
 }
 
-template <bool L2>
+template <bool L2, bool FULL>  // FULL: d == kD (compile-time row strides)
 __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
@@ -253,6 +254,18 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
   const uint32_t G = gridDim.x;
   const bool tr = g_thtrace_on == f.batch + 1;
   if (tid == 0) th_stamp(tr, 0);
+  const int d = FULL ? kD : f.de, d4 = d >> 2;  // row width (<= kD); staged rows are zero-padded to kD columns
+  if (d < kD && warp < kCompute) {  // the copies never write the padding: clear it once
+    for (int i = tid; i < kStages * 2 * kRows * (kD - d) / 4; i += kCompute * 32) {
+      const int c4 = d4 + i % (kD / 4 - d4), rr = i / (kD / 4 - d4);  // rr over stages x {H, T} x rows
+      const int st = rr / (2 * kRows), ht = (rr / kRows) & 1, row = rr % kRows;
+      reinterpret_cast<float4*>((ht ? S.Tl[st] : S.H[st]) + row * kStride)[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int i = tid; i < kStages * 2 * (kD - d); i += kCompute * 32) {
+      const int c = d + i % (kD - d), rr = i / (kD - d);
+      (rr & 1 ? S.meta[rr >> 1].dr : S.meta[rr >> 1].wr)[c] = 0.f;
+    }
+  }
   if (warp == kLoaderWarp) {
     if (alive) enumerate_rel_tiles(a, S.rt);
     __syncwarp();
@@ -348,8 +361,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
             M.first = S.rt.first[kq[c]];
             M.end = S.rt.first[kq[c] + 1];
           }
-          tc::cp_async16(M.wr + 4 * lane, f.normals + r * kD + 4 * lane);
-          tc::cp_async16(M.dr + 4 * lane, f.X + (f.N + r) * kD + 4 * lane);
+          if (lane < d4) {
+            tc::cp_async16(M.wr + 4 * lane, f.normals + r * d + 4 * lane);
+            tc::cp_async16(M.dr + 4 * lane, f.X + f.N * d + r * d + 4 * lane);
+          }
         }
         // rows: lane = 16-byte chunk of a 512-byte row
         float* Hs = S.H[s];
@@ -359,10 +374,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
           const int hp = __shfl_sync(kFull, pr[c].x, p), tp = __shfl_sync(kFull, pr[c].y, p);
           const int hn = __shfl_sync(kFull, ng[c].x, p), tn = __shfl_sync(kFull, ng[c].y, p);
           const int m = kRowsPerWarp * (p / kHalf) + p % kHalf;
-          tc::cp_async16(Hs + m * kStride + 4 * lane, f.X + static_cast<size_t>(hp) * kD + 4 * lane);
-          tc::cp_async16(Ts + m * kStride + 4 * lane, f.X + static_cast<size_t>(tp) * kD + 4 * lane);
-          tc::cp_async16(Hs + (m + kHalf) * kStride + 4 * lane, f.X + static_cast<size_t>(hn) * kD + 4 * lane);
-          tc::cp_async16(Ts + (m + kHalf) * kStride + 4 * lane, f.X + static_cast<size_t>(tn) * kD + 4 * lane);
+          if (lane < d4) {  // columns >= d stay zero (cleared once at kernel start)
+            tc::cp_async16(Hs + m * kStride + 4 * lane, f.X + static_cast<size_t>(hp) * d + 4 * lane);
+            tc::cp_async16(Ts + m * kStride + 4 * lane, f.X + static_cast<size_t>(tp) * d + 4 * lane);
+            tc::cp_async16(Hs + (m + kHalf) * kStride + 4 * lane, f.X + static_cast<size_t>(hn) * d + 4 * lane);
+            tc::cp_async16(Ts + (m + kHalf) * kStride + 4 * lane, f.X + static_cast<size_t>(tn) * d + 4 * lane);
+          }
         }
         tc::cp_async_mbar_arrive(&S.full[s]);
         __syncwarp();
@@ -503,7 +520,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
           const float dzw = __shfl_sync(kFull, part[0], kLanesPerRow * q);
           if (!((amask >> (kLanesPerRow * q)) & 1u)) continue;
           const int r2 = rz[q];
-          reinterpret_cast<float4*>(f.res_u + static_cast<size_t>(r2) * kD)[lane] = f4sub(dz[q], f4scale(dzw, w));
+          if (lane < d4)
+            reinterpret_cast<float4*>(f.res_u + static_cast<size_t>(r2) * d)[lane] = f4sub(dz[q], f4scale(dzw, w));
           acc_dz = f4add(acc_dz, dz[q]);
           acc_n = f4add(acc_n, f4add(f4scale(dzw, u[q]), f4scale(wu[q], dz[q])));
         }
@@ -573,6 +591,7 @@ __global__ void __launch_bounds__(2 * kD) transh_rel_finalize_kernel(const TArgs
     const int64_t r = a.info[4 + 3 * b];
     const uint32_t j0 = cta_of_tile(a.info[5 + 3 * b], T, G), j1 = cta_of_tile(a.info[6 + 3 * b] - 1, T, G);
     const int c = tid & (kD - 1), v = tid / kD;  // (column, vector)
+    const int d = f.de;
     const float* src = a.partial + static_cast<size_t>(v) * kD + c;
     float g = 0.f;
     uint32_t j = j0;
@@ -585,15 +604,19 @@ __global__ void __launch_bounds__(2 * kD) transh_rel_finalize_kernel(const TArgs
     }
     for (; j <= j1; ++j) g = __fadd_rn(g, __ldcg(src + static_cast<size_t>(j + b) * 2 * kD));
     if (a.nrm_sink) {  // data parallel: this rank's gradient rows (summed over ranks, then one dense step)
-      if (v == 0) a.rel[r * kD + c] = g;
-      else a.nrm_sink[r * kD + c] = -g;
+      if (c < d) {
+        if (v == 0) a.rel[r * d + c] = g;
+        else a.nrm_sink[r * d + c] = -g;
+      }
       return;
     }
     const float step = *a.lr;
-    float* p = v == 0 ? a.rel + r * kD + c : const_cast<float*>(f.normals) + r * kD + c;
-    *p = __fsub_rn(*p, __fmul_rn(step, v == 0 ? g : -g));  // grads.normals -= nrm (models.hpp:112)
+    if (c < d) {
+      float* p = v == 0 ? a.rel + r * d + c : const_cast<float*>(f.normals) + r * d + c;
+      *p = __fsub_rn(*p, __fmul_rn(step, v == 0 ? g : -g));  // grads.normals -= nrm (models.hpp:112)
+    }
     __syncthreads();
-    if (warp == 0) renorm_normal(const_cast<float*>(f.normals), r, lane, f.err);
+    if (warp == 0) renorm_normal(const_cast<float*>(f.normals), r, f.de, lane, f.err);
   }
   if (a.nrm_sink || static_cast<int64_t>(b) >= a.R || warp != 0) return;
   bool present = false;
@@ -601,12 +624,15 @@ __global__ void __launch_bounds__(2 * kD) transh_rel_finalize_kernel(const TArgs
     const uint32_t q = q0 + lane;
     present = __any_sync(kFull, q < nrel && a.info[4 + 3 * q] == b);
   }
-  if (!present) renorm_normal(const_cast<float*>(f.normals), b, lane, f.err);
+  if (!present) renorm_normal(const_cast<float*>(f.normals), b, f.de, lane, f.err);
 }
 
 }  // namespace
 
-bool transh_tiles_supported(int de, int dr, int64_t R) { return de == kD && dr == kD && R <= kMaxRelSeg; }
+// any width up to 128 in 16-byte chunks: rows are staged zero-padded to 128 columns
+bool transh_tiles_supported(int de, int dr, int64_t R) {
+  return de == dr && de >= 4 && de <= kD && de % 4 == 0 && R <= kMaxRelSeg;
+}
 
 int64_t transh_trace(int enable, unsigned long long* out, int64_t cap) {
   SKG_CUDA(cudaMemcpyToSymbol(g_thtrace_on, &enable, sizeof(int)));
@@ -626,8 +652,10 @@ int64_t transh_tiles_work_floats(int64_t rows, int64_t R) {
 
 void configure_transh_tiles_kernels() {
   const int smem = static_cast<int>(sizeof(PipeSmem));
-  SKG_CUDA(cudaFuncSetAttribute(transh_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  SKG_CUDA(cudaFuncSetAttribute(transh_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  SKG_CUDA(cudaFuncSetAttribute(transh_pipe_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  SKG_CUDA(cudaFuncSetAttribute(transh_pipe_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  SKG_CUDA(cudaFuncSetAttribute(transh_pipe_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  SKG_CUDA(cudaFuncSetAttribute(transh_pipe_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 }
 
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
@@ -654,8 +682,11 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   a.R = R;
   const size_t smem = sizeof(PipeSmem);
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, num_sms));  // persistent, one CTA per SM
-  if (l2) transh_pipe_kernel<true><<<grid, kPipeThreads, smem, s>>>(a);
-  else transh_pipe_kernel<false><<<grid, kPipeThreads, smem, s>>>(a);
+  const bool full = fa.de == kD;
+  if (l2 && full) transh_pipe_kernel<true, true><<<grid, kPipeThreads, smem, s>>>(a);
+  else if (l2) transh_pipe_kernel<true, false><<<grid, kPipeThreads, smem, s>>>(a);
+  else if (full) transh_pipe_kernel<false, true><<<grid, kPipeThreads, smem, s>>>(a);
+  else transh_pipe_kernel<false, false><<<grid, kPipeThreads, smem, s>>>(a);
   count_launch();
   SKG_LAUNCH_CHECK();
   if (mark) (*mark)();

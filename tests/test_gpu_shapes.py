@@ -81,17 +81,19 @@ def _delta_check(name, before, got, want, tol_frob, tol_rows):
     assert int(np.count_nonzero(stray)) <= 4, name
 
 
-@pytest.mark.parametrize("model,N,R,n_total,B", [("transh", 40943, 11, 96483, 16384),
-                                                 ("transr", 123182, 37, 1198932, 65536)])
-def test_ht_backward_deltas_at_config_shape(eng, orc32, model, N, R, n_total, B):
+@pytest.mark.parametrize("model,N,R,n_total,B,d", [("transh", 40943, 11, 96483, 16384, 128),
+                                                   ("transr", 123182, 37, 1198932, 65536, 128),
+                                                   ("transh", 40943, 11, 96483, 16384, 64)])
+def test_ht_backward_deltas_at_config_shape(eng, orc32, model, N, R, n_total, B, d):
     """One full C2 / C4 minibatch at lr 100: every table's delta matches the oracle's to
-    1e-3 (Frobenius, relative) and per row, so a missing or wrong backward term fails."""
+    1e-3 (Frobenius, relative) and per row, so a missing or wrong backward term fails.
+    (d = 64: the zero-padded TransH tiles.)"""
     h, r, t = (a[:B] for a in orc32.synthetic_train(N, R, n_total, 1))
-    st = orc32.init_store(model, N, R, 128, 128, 1)
+    st = orc32.init_store(model, N, R, d, d, 1)
     if model == "transr":  # off the identity, so the projection and its gradient matter
         st.proj += np.random.default_rng(2).uniform(-0.05, 0.05, st.proj.shape).astype(np.float32)
     before = st.copy()
-    cfg = ModelConfig.make(model, 128, 128, "l2")
+    cfg = ModelConfig.make(model, d, d, "l2")
     eng.store_upload(cfg, st.entity, st.relation, st.proj, st.normals)
     eng.set_triples(h, r, t, N, R)
     kw = dict(lr=100.0, margin=0.5, batch_size=B, seed=1)
