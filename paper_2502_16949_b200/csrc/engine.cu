@@ -159,7 +159,8 @@ void ensure_workspace(skg_ctx* ctx, int64_t rows, int kind) {
   const int64_t d = std::max(ctx->de, ctx->dr);
   ctx->res.ensure(rows * d * (is_mult_kind(kind) ? 3 : 1));  // multiplicative: 3 gradient planes
   // TransR tcgen05 training writes dU in tile-blocked slots (kTileSlotRows): up to R + 1 partial tiles more
-  const bool tile_rows = (kind == kTransR_L2 || kind == kTransR_L1) && ctx->de == 128;
+  const bool tile_rows = (kind == kTransR_L2 || kind == kTransR_L1) &&
+                         transr_train_tc_supported(static_cast<int>(ctx->de), static_cast<int>(ctx->dr));
   ctx->res_u.ensure(tile_rows ? std::max(rows * ctx->de, tile_rows_floats(rows, ctx->R)) : rows * ctx->de);
   ctx->scal.ensure(rows);
   ctx->scores.ensure(rows);

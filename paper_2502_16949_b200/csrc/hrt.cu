@@ -797,7 +797,7 @@ void launch_bwd_k(bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s) {
   const bool v4 = (a.d % 4) == 0;
   const bool narrow = v4 ? a.d <= 128 : a.d <= 32;
   if constexpr (KIND == kTileSlotRows) {
-    if (a.d != 128) throw CudaError("tile-blocked dU rows need d = 128");
+    if (a.d > 128 || a.d % kDuGroup != 0) throw CudaError("tile-blocked dU rows need d <= 128, a multiple of 16");
     if (sgd) segment_backward_staged_kernel<true, kTileSlotRows><<<grid, kThreads, 0, s>>>(a);
     else segment_backward_staged_kernel<false, kTileSlotRows><<<grid, kThreads, 0, s>>>(a);
   } else if (KIND == kPlainRows && v4 && narrow) {

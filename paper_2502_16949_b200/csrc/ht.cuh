@@ -92,7 +92,9 @@ int64_t transr_trace(int enable, unsigned long long* out, int64_t cap);  // debu
 void launch_transr_train_apply(const uint32_t* tile_total, const uint32_t* seg_tiles, const uint32_t* tile_seg,
                                const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
                                float* proj, float* rel, const float* lr, const uint32_t* err, float* mr, int64_t R,
-                               cudaStream_t s, int sink = 0);
+                               cudaStream_t s, int sink, int dr, int de);
+// d_e, d_r multiples of 16 up to 128 (the training kernel zero-pads its tiles)
+bool transr_train_tc_supported(int de, int dr);
 // always_prep: re-split M_r into the tf32 ring chunks before this batch (data parallel:
 // the dense step outside the kernel moved proj), otherwise only at batch 0
 void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val, const uint32_t* seg_start,

@@ -436,6 +436,13 @@ struct Work {
 
 int64_t max_tiles(int64_t rows, int64_t R) { return rows / kTilePairs + 2 * R + 2; }
 
+// dM partial of one (CTA, run) slot: the tcgen05 training kernel writes 128 x 128 (zero-padded
+// for narrower M_r), the FP32 tile kernel d_r x d_e.
+int64_t part_floats(int64_t de, int64_t dr) {
+  return transr_train_tc_supported(static_cast<int>(de), static_cast<int>(dr)) ? std::max<int64_t>(dr * de, 128 * 128)
+                                                                               : dr * de;
+}
+
 Work carve(float* work, int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
   Work w;
@@ -449,7 +456,7 @@ Work carve(float* work, int64_t rows, int64_t de, int64_t dr, int64_t R) {
   w.tile_total = w.tile_p0 + mt;
   w.seg_tiles = w.tile_total + 2;
   w.dm_part = rest + ((3 * mt + 2 * R + 8 + 31) / 32) * 32;  // 128 B aligned (float4 stores)
-  w.dr_part = w.dm_part + std::max<int64_t>(mt, transr_tc_slots(256, R)) * dr * de;
+  w.dr_part = w.dm_part + std::max<int64_t>(mt, transr_tc_slots(256, R)) * part_floats(de, dr);
   return w;
 }
 
@@ -521,7 +528,8 @@ int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R) {
   const int64_t mt = max_tiles(rows, R);
   const int64_t parts = std::max<int64_t>(mt, transr_tc_slots(256, R));  // tc path: (CTA, relation) runs
   return ((std::max(transr_tc_mr_floats(R), transr_train_tc_mr_floats(R)) + 31) / 32) * 32 +
-         ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + parts * dr * de + ((parts * dr + 31) / 32) * 32 + 64;
+         ((3 * mt + 2 * R + 8 + 31) / 32) * 32 + parts * part_floats(de, dr) +
+         ((parts * std::max<int64_t>(dr, 128) + 31) / 32) * 32 + 64;
 }
 
 void configure_transr_kernels() {
@@ -553,7 +561,7 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
   // gradients land in the sinks, and the engine applies one dense step
   float* proj_dst = sinks ? sinks->proj : const_cast<float*>(fa.proj);
   float* rel_dst = sinks ? sinks->rel : const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
-  if (transr_tc_supported(fa.de, fa.dr)) {
+  if (transr_train_tc_supported(fa.de, fa.dr)) {
     transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, 1,
                                                     w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err,
                                                     nullptr, 0, fa.stamp_start);
@@ -570,7 +578,7 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
     eb.d = fa.de;
     launch_segment_backward(kTileSlotRows, sinks == nullptr, eb, num_sms, s);
     launch_transr_train_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
-                              proj_dst, rel_dst, ba.lr, ba.err, w.mr_chunks, R, s, sinks != nullptr);
+                              proj_dst, rel_dst, ba.lr, ba.err, w.mr_chunks, R, s, sinks != nullptr, fa.dr, fa.de);
     if (mark) (*mark)();
     return;
   }

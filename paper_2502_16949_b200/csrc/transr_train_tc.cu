@@ -182,10 +182,11 @@ __device__ __forceinline__ float4 f4sel(int c, float4 a, float4 b) {  // c ? a :
 #define SKG_TR_USPLIT 64
 #endif
 constexpr int kUSplit = SKG_TR_USPLIT;  // producers: columns [0, kUSplit); gather warps: the rest
-__device__ __forceinline__ void compute_u(Smem& S, uint32_t taddr, int p, bool ok, int c0, int c1) {
+__device__ __forceinline__ void compute_u(Smem& S, uint32_t taddr, int p, bool ok_row, int c0, int c1, int de) {
   const int flip = (p >> 2) & 1;
 #pragma unroll 1
   for (int c = c0; c < c1; c += 16) {
+    const bool ok = ok_row && c < de;  // d_e is a multiple of 16: whole chunks are real or padding
     float hi[16], lo[16];
     float4 uv[4];
 #pragma unroll
@@ -296,7 +297,9 @@ __device__ __forceinline__ void chase_rows(const Args& a, uint32_t t, int lane, 
     const int kk = lane + 32 * q;
     pos[q] = kk < np ? static_cast<int>(__ldg(a.ent_val + e0 + p0 + kk) & 0x7fffffffu) : -1;
   }
-  const float4 rv = __ldg(reinterpret_cast<const float4*>(f.X + f.N * static_cast<int64_t>(kD) + r * kD) + lane);
+  const float4 rv = lane < (f.dr >> 2)  // d_r-wide relation row, zero-padded to kD
+                        ? __ldg(reinterpret_cast<const float4*>(f.X + f.N * static_cast<int64_t>(f.de) + r * f.dr) + lane)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int kk = lane + 32 * q;
@@ -332,6 +335,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto trace = [&](uint32_t it, int ev) { trace_ev(tr, it, ev); };
 
   if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
+  if (f.de < kD)  // row tiles narrower than 128: the gather never writes columns >= d_e, keep them zero
+    for (int i = tid; i < kRows * (kD - f.de) / 4; i += kThreads) {
+      const int r = i / ((kD - f.de) / 4), c4 = (f.de >> 2) + i % ((kD - f.de) / 4);
+      reinterpret_cast<float4*>(S.U)[tile_unit(r, c4)] = make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(S.DZ)[tile_unit(r, c4)] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   if (tid == 0) {
     tc::mbar_init(&S.g_full, 32 * kGatherWarps);
     tc::mbar_init(&S.u_full, kUSplit < kD ? 256 : 128);
@@ -524,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_after();
       }
       if (p == 0) trace(it, 15);
-      compute_u(S, tbase + lane_addr, p, rows[p].z >= 0, 0, kUSplit);
+      compute_u(S, tbase + lane_addr, p, rows[p].z >= 0, 0, kUSplit, f.de);
       tc::tmem_wait_st();
       tc::fence_before();
       tc::mbar_arrive(&S.u_full);
@@ -650,9 +659,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 4
       for (int k = lane; k < 4 * kRows; k += 32) {
         const int4 rw = S.rows[buf][k >> 2];
-        const float* row = f.X + static_cast<size_t>((k & 1) ? rw.y : rw.x) * kD + ((k >> 1) & 1) * 64;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 32));
+        const int hv = (k >> 1) & 1;
+        if (hv * 64 < f.de) {
+          const float* row = f.X + static_cast<size_t>((k & 1) ? rw.y : rw.x) * f.de + hv * 64;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+          if (hv * 64 + 32 < f.de) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 32));
+        }
       }
 #endif
     }
@@ -662,12 +674,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // into sU, tail rows into sDZ at tile_unit; one warp keeps a tile's 256
     // rows in flight without registers. (TMA tile::gather4 of 128-byte boxes
     // measured ~16 cycles per box row per SM here, too slow to hide.)
+    const int de = f.de, de4 = de >> 2;
     auto gather8 = [&](const int4* rows, int r0) {  // rows r0 .. r0 + 7, head and tail
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int4 rw = rows[r0 + q];
-        tc::cp_async16(S.U + 4 * tile_unit(r0 + q, lane), f.X + static_cast<size_t>(rw.x) * kD + 4 * lane);
-        tc::cp_async16(S.DZ + 4 * tile_unit(r0 + q, lane), f.X + static_cast<size_t>(rw.y) * kD + 4 * lane);
+        if (lane < de4) {  // d_e-wide rows; U's columns >= d_e are kept zero (compute_u)
+          tc::cp_async16(S.U + 4 * tile_unit(r0 + q, lane), f.X + static_cast<size_t>(rw.x) * de + 4 * lane);
+          tc::cp_async16(S.DZ + 4 * tile_unit(r0 + q, lane), f.X + static_cast<size_t>(rw.y) * de + 4 * lane);
+        }
       }
     };
     for (uint32_t it = 0; it < ntile; ++it) {
@@ -692,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mbar_wait(&S.g2_done, (it - 1) & 1);
           tc::fence_after();
         }
-        compute_u(S, tbase + (static_cast<uint32_t>(q4 * 32) << 16), row, rows[row].z >= 0, kUSplit, kD);
+        compute_u(S, tbase + (static_cast<uint32_t>(q4 * 32) << 16), row, rows[row].z >= 0, kUSplit, kD, f.de);
         tc::tmem_wait_st();
         tc::fence_before();
         tc::mbar_arrive(&S.u_full);
@@ -763,10 +778,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Per relation: both K-major operand views of M_r in 16-wide K chunks, split
 // hi (rna tf32) / lo, laid out exactly as the ring slots are read.
 //   layout 0 (GEMM1 B): n = output row i, k = j;  layout 1 (GEMM2 B): n = j, k = i.
-__global__ void transr_train_prep_kernel(const float* __restrict__ proj, float* __restrict__ out) {
+// M_r is d_r x d_e (models.hpp:23-29); entries outside it are zero, so the
+// padded GEMMs give zero V columns >= d_r and zero dU columns >= d_e.
+__global__ void transr_train_prep_kernel(const float* __restrict__ proj, float* __restrict__ out, int dr, int de) {
   const int r = blockIdx.x, lc = blockIdx.y;  // lc = layout * 8 + chunk
   const int layout = lc >> 3, k0 = (lc & 7) * kChunkK;
-  const float* M = proj + static_cast<int64_t>(r) * kD * kD;
+  const float* M = proj + static_cast<int64_t>(r) * dr * de;
   float* hi = out + r * kMrFloatsPerRel + static_cast<int64_t>(lc) * 2 * kChunkFloats;
   float* lo = hi + kChunkFloats;
   for (int i = threadIdx.x; i < kChunkFloats; i += blockDim.x) {
@@ -775,11 +792,11 @@ __global__ void transr_train_prep_kernel(const float* __restrict__ proj, float* 
     if (layout == 0) {  // M[n][k0 + kk]: 16 consecutive floats per row
       n = i >> 4;
       kk = i & 15;
-      x = M[n * kD + k0 + kk];
+      x = n < dr && k0 + kk < de ? M[n * de + k0 + kk] : 0.f;
     } else {            // M[k0 + kk][n]: coalesced along n
       kk = i >> 7;
       n = i & 127;
-      x = M[(k0 + kk) * kD + n];
+      x = k0 + kk < dr && n < de ? M[(k0 + kk) * de + n] : 0.f;
     }
     float h, l;
     tc::split_tf32(x, h, l);
@@ -799,7 +816,8 @@ __global__ void transr_train_apply_kernel(const uint32_t* __restrict__ tile_tota
                                           int64_t N, int G, const float* __restrict__ dm_part,
                                           const float* __restrict__ dr_part, float* __restrict__ proj,
                                           float* __restrict__ rel, const float* __restrict__ lr,
-                                          const uint32_t* __restrict__ err, float* __restrict__ mr, int sink) {
+                                          const uint32_t* __restrict__ err, float* __restrict__ mr, int sink, int dr,
+                                          int de) {
   if (err[0] != 0) return;
   const uint32_t k = blockIdx.x;
   if (k >= tile_total[1]) return;
@@ -846,7 +864,9 @@ __global__ void transr_train_apply_kernel(const uint32_t* __restrict__ tile_tota
       const size_t slot = static_cast<size_t>(jl[q]) + k;
       g = __fadd_rn(g, pm ? __ldcg(dm_part + slot * kD * kD + i) : __ldcg(dr_part + slot * kD + (i - kD * kD)));
     }
-    float* p = pm ? proj + r * kD * kD + i : rel + r * kD + (i - kD * kD);
+    const int a = i / kD, b = i - a * kD;  // M_r element (a, b), or relation column i - kD * kD
+    if (pm ? (a >= dr || b >= de) : (i - kD * kD >= dr)) continue;  // padding of a narrower M_r / relation row
+    float* p = pm ? proj + r * dr * de + a * de + b : rel + r * dr + (i - kD * kD);
     if (sink) {  // data parallel: this rank's gradient, one dense step after the all-reduce
       *p = g;
       continue;
@@ -854,7 +874,6 @@ __global__ void transr_train_apply_kernel(const uint32_t* __restrict__ tile_tota
     const float nv = __fsub_rn(*p, __fmul_rn(step, g));
     *p = nv;
     if (pm) {  // element (row a = output dim, col b = entity dim) of M_r into both ring layouts
-      const int a = i / kD, b = i - a * kD;
       float h, l;
       tc::split_tf32(nv, h, l);
       float* c0 = mrr + static_cast<int64_t>(b / kChunkK) * 2 * kChunkFloats;                   // layout 0: n = a, k = b
@@ -885,6 +904,11 @@ int64_t transr_trace(int enable, unsigned long long* out, int64_t cap) {
   return n;
 }
 
+// Training kernel widths: d_e, d_r multiples of 16 up to 128 (zero-padded tiles).
+bool transr_train_tc_supported(int de, int dr) {
+  return de >= 16 && dr >= 16 && de <= kD && dr <= kD && de % 16 == 0 && dr % 16 == 0;
+}
+
 void configure_transr_train_tc_kernels() {
   SKG_CUDA(cudaFuncSetAttribute(transr_train_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sizeof(Smem))));
@@ -899,7 +923,8 @@ void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val,
   // the split M_r chunks are refreshed by every batch's apply; the first batch
   // of an epoch re-splits from proj (the store may have been replaced)
   if (fa.batch == 0 || always_prep) {
-    transr_train_prep_kernel<<<dim3(static_cast<unsigned>(R), 2 * kChunksPerGemm), 256, 0, s>>>(fa.proj, mr);
+    transr_train_prep_kernel<<<dim3(static_cast<unsigned>(R), 2 * kChunksPerGemm), 256, 0, s>>>(fa.proj, mr, fa.dr,
+                                                                                                 fa.de);
     count_launch();
   }
   Args a{};
@@ -924,10 +949,10 @@ void launch_transr_train_tc(bool l2, const FwdArgs& fa, const uint32_t* ent_val,
 void launch_transr_train_apply(const uint32_t* tile_total, const uint32_t* seg_tiles, const uint32_t* tile_seg,
                                const uint32_t* seg_col, int64_t N, int G, const float* dm_part, const float* dr_part,
                                float* proj, float* rel, const float* lr, const uint32_t* err, float* mr, int64_t R,
-                               cudaStream_t s, int sink) {
+                               cudaStream_t s, int sink, int dr, int de) {
   transr_train_apply_kernel<<<dim3(static_cast<unsigned>(R), SKG_APPLY_Y), 256, 0, s>>>(tile_total, seg_tiles, tile_seg, seg_col,
                                                                               N, G, dm_part, dr_part, proj, rel, lr,
-                                                                              err, mr, sink);
+                                                                              err, mr, sink, dr, de);
   count_launch();
   SKG_LAUNCH_CHECK();
 }

@@ -84,7 +84,10 @@ def test_ht_score_backward(eng, orc32, model, norm, de, dr):
 @pytest.mark.parametrize("model,de,dr,batch", [("transh", 16, 16, 64), ("transr", 16, 12, 64), ("transh", 128, 128, 4096),
                                                 ("transr", 128, 128, 4096),
                                                 # relation-tile TransH kernel at widths below 128 (zero-padded tiles)
-                                                ("transh", 64, 64, 1024), ("transh", 100, 100, 2048)])
+                                                ("transh", 64, 64, 1024), ("transh", 100, 100, 2048),
+                                                # tcgen05 TransR step at other multiples of 16 (zero-padded tiles)
+                                                ("transr", 64, 32, 1024), ("transr", 32, 64, 1024),
+                                                ("transr", 112, 128, 2048)])
 def test_ht_fit_matches_oracle(eng, orc32, model, de, dr, batch):
     n, r, m = 3000, 11, 6000
     h, rel, t = orc32.synthetic_train(n, r, m, 3)

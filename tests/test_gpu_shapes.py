@@ -83,7 +83,8 @@ def _delta_check(name, before, got, want, tol_frob, tol_rows):
 
 @pytest.mark.parametrize("model,N,R,n_total,B,d", [("transh", 40943, 11, 96483, 16384, 128),
                                                    ("transr", 123182, 37, 1198932, 65536, 128),
-                                                   ("transh", 40943, 11, 96483, 16384, 64)])
+                                                   ("transh", 40943, 11, 96483, 16384, 64),
+                                                   ("transr", 123182, 37, 1198932, 65536, 64)])
 def test_ht_backward_deltas_at_config_shape(eng, orc32, model, N, R, n_total, B, d):
     """One full C2 / C4 minibatch at lr 100: every table's delta matches the oracle's to
     1e-3 (Frobenius, relative) and per row, so a missing or wrong backward term fails.
