@@ -428,6 +428,18 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
   const int64_t n_proj = ctx->proj.n, n_norm = ctx->normals.n;
   const int64_t n_sink = n_params + (ht ? n_proj + n_norm : 0);
   const int64_t nb_run = es.nb_run >= 0 ? es.nb_run : es.nb;
+  // A speculative epoch (deferred re-upload) snapshots the parameters on the
+  // upload stream while batch 0's forward already runs: batch 0's first
+  // parameter write waits for that copy (an external event node in the
+  // graph; a no-op when no snapshot was recorded).
+  bool snap_waited = false;
+  const std::function<void()> wait_snapshot = [&]() {
+    if (snap_waited) return;
+    snap_waited = true;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SKG_CUDA(cudaStreamIsCapturing(s, &cs));
+    SKG_CUDA(cudaStreamWaitEvent(s, ctx->snap_ev, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+  };
   for (int64_t b = 0; b < nb_run; ++b) {
     const int64_t lo = b * es.B;
     const int Bb = static_cast<int>(std::min(es.B, ctx->M - lo));
@@ -558,16 +570,24 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
       ba.plane_rows = 2 * es.B;
       launch_mult_forward(es.kind, true, fa, ctx->num_sms, s);
       mark();
+      if (b == 0) wait_snapshot();
       launch_segment_backward(kMultRows, true, ba, ctx->num_sms, s);
       mark();
     } else if (!ht) {
       launch_hrt_forward(es.kind, true, fa, ctx->num_sms, s);
       mark();
+      if (b == 0) wait_snapshot();
       launch_segment_backward(es.kind, true, ba, ctx->num_sms, s);
       mark();
     } else {
       const Branch br{ctx->aux, ctx->aux_fork, ctx->aux_join};
-      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, markp, ctx->R, nullptr, &br);
+      // the ht step calls its mark after the forward kernels (which write no parameters)
+      const std::function<void()> mark0 = [&]() {
+        if (markp) (*markp)();
+        wait_snapshot();
+      };
+      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, b == 0 ? &mark0 : markp, ctx->R, nullptr, &br);
+      if (b == 0) wait_snapshot();  // (if the step had no mark call)
     }
   }
   if (dp) dp_allreduce_sum(ctx, ctx->batch_loss.p, es.nb, s);  // shard losses -> global batch losses
@@ -1172,6 +1192,8 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->snap_ev, cudaEventDisableTiming));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->fork_up_ev, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->join2_ev, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming));
@@ -1215,6 +1237,8 @@ void skg_destroy(skg_ctx* ctx) {
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
+  if (ctx->snap_ev) cudaEventDestroy(ctx->snap_ev);
+  if (ctx->fork_up_ev) cudaEventDestroy(ctx->fork_up_ev);
   if (ctx->join2_ev) cudaEventDestroy(ctx->join2_ev);
   if (ctx->aux_fork) cudaEventDestroy(ctx->aux_fork);
   if (ctx->aux_join) cudaEventDestroy(ctx->aux_join);
@@ -1710,9 +1734,14 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   ctx->backup.ensure(nt + np + nn + 4);
   const int64_t ob = 0, op = (nt + 3) / 4 * 4, on = op + (np + 3) / 4 * 4;  // 16-byte aligned sections
   ctx->backup.ensure(on + nn + 4);
-  copy_floats(ctx->tables.p, ctx->backup.p + ob, nt, ctx->num_sms, ctx->stream);
-  copy_floats(ctx->proj.p, ctx->backup.p + op, np, ctx->num_sms, ctx->stream);
-  copy_floats(ctx->normals.p, ctx->backup.p + on, nn, ctx->num_sms, ctx->stream);
+  // snapshot on the upload stream: the epoch graph starts alongside and its
+  // batch 0 waits for snap_ev before writing any parameter
+  SKG_CUDA(cudaEventRecord(ctx->fork_up_ev, ctx->stream));
+  SKG_CUDA(cudaStreamWaitEvent(ctx->up, ctx->fork_up_ev, 0));
+  copy_floats(ctx->tables.p, ctx->backup.p + ob, nt, ctx->num_sms, ctx->up);
+  copy_floats(ctx->proj.p, ctx->backup.p + op, np, ctx->num_sms, ctx->up);
+  copy_floats(ctx->normals.p, ctx->backup.p + on, nn, ctx->num_sms, ctx->up);
+  SKG_CUDA(cudaEventRecord(ctx->snap_ev, ctx->up));
   const auto t1 = clk::now();
   std::exception_ptr failed;
   try {

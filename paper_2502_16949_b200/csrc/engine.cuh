@@ -122,6 +122,8 @@ struct skg_ctx {
   std::string perm_key[2];
   cudaStream_t side2 = nullptr;
   cudaEvent_t join2_ev = nullptr;
+  cudaEvent_t snap_ev = nullptr;     // speculative epoch: parameter snapshot done (waited by batch 0's first write)
+  cudaEvent_t fork_up_ev = nullptr;
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   std::string graph_keys[2];
   int64_t graph_launches_k[2] = {0, 0};
