@@ -2604,6 +2604,14 @@ extern "C" int64_t skg_debug_transr_trace(int32_t enable, unsigned long long* ou
   }
 }
 
+extern "C" int64_t skg_debug_bwd_trace(int32_t enable, unsigned long long* out, uint32_t* info, int64_t cap) {
+  try {
+    return skg::bwd_trace(enable, out, info, cap);
+  } catch (...) {
+    return -1;
+  }
+}
+
 extern "C" int64_t skg_debug_transh_trace(int32_t enable, unsigned long long* out, int64_t cap) {
   try {
     return transh_trace(enable, out, cap);

@@ -28,6 +28,7 @@
 #include "plan.cuh"
 #include "kernels.cuh"
 #include "primitives.cuh"
+#include "tc.cuh"
 
 namespace skg {
 
@@ -658,6 +659,13 @@ __global__ void __launch_bounds__(kThreads) segment_backward_staged_kernel(const
 // One warp per column segment; CH vector chunks per lane per pass (CH = 1
 // covers d <= 128 with float4 lanes). Up to KB residual rows are in flight
 // per round; the adds stay in the segment's entry order.
+// Debug: per-warp start / end stamps (globaltimer) and segment mix of one
+// chosen minibatch, off unless enabled through skg_debug_bwd_trace.
+constexpr int kBwTrWarps = 148 * 64;
+__device__ unsigned long long g_bwtrace[kBwTrWarps * 2];
+__device__ uint32_t g_bwtrace_info[kBwTrWarps];  // relation segments << 16 | entries
+__device__ int g_bwtrace_on;
+
 template <int KIND, bool SGD, int VEC, int CH, int KB = SKG_BWD_KB>
 __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArgs a) {
   using V = typename VecT<VEC>::T;
@@ -665,11 +673,16 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nw = gridDim.x * (blockDim.x >> 5);
+  const bool trc = g_bwtrace_on == a.batch + 1 && gw < kBwTrWarps;
+  uint32_t tr_info = 0;
+  if (trc && lane == 0) stamp_now(&g_bwtrace[2 * gw]);
   const uint32_t s0 = a.seg_base[a.batch], s1 = a.seg_base[a.batch + 1];
   const int dv = a.d / VEC;
   const V* RV = reinterpret_cast<const V*>(a.res);
   for (uint32_t s = s0 + gw; s < s1; s += nw) {
     const uint32_t col = a.seg_col[s];
+    if (trc) tr_info += (col >= static_cast<uint32_t>(a.N) && col != kDummyCol ? (1u << 16) : 0u) +
+                        (col != kDummyCol ? a.seg_start[s + 1] - a.seg_start[s] : 0u);
     if (col == kDummyCol || (a.entity_only && col >= static_cast<uint32_t>(a.N))) continue;
     const uint32_t e0 = a.seg_start[s], e1 = a.seg_start[s + 1];
     V* P = reinterpret_cast<V*>(a.X) + static_cast<size_t>(col) * dv;
@@ -741,7 +754,12 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
       }
     }
   }
+  if (trc && lane == 0) {
+    stamp_now(&g_bwtrace[2 * gw + 1]);
+    g_bwtrace_info[gw] = tr_info;
+  }
 }
+
 
 template <int KIND, bool TRAIN, int VEC>
 void launch_fwd_t(const FwdArgs& a, int num_sms, cudaStream_t s) {
@@ -791,35 +809,52 @@ void launch_fwd_k(bool train, const FwdArgs& a, int num_sms, cudaStream_t s) {
   }
 }
 
+// Grid of a grid-stride backward kernel. The warp-per-segment kernel keeps 8
+// blocks per SM: about two waves, and the second wave's blocks take over SMs
+// as first-wave blocks finish, which balances the uneven segments better than
+// a resident grid (measured: C1 23.0 vs 26.7 us, C5 313 vs 516 us). The staged
+// ht entity pass (mostly one-entry segments) runs every block at once
+// (C2 17.9 -> 16.5 us).
+template <class K>
+int resident_grid(K kernel, int num_sms) {
+  int per_sm = 0;
+  SKG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
+  return num_sms * (per_sm > 0 ? per_sm : 1);
+}
+
+template <class K>
+void run_bwd(K kernel, const BwdArgs& a, int num_sms, cudaStream_t s, bool resident = false) {
+  kernel<<<resident ? resident_grid(kernel, num_sms) : num_sms * 8, kThreads, 0, s>>>(a);
+}
+
 template <int KIND>
 void launch_bwd_k(bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s) {
-  const int grid = num_sms * 8;
   const bool v4 = (a.d % 4) == 0;
   const bool narrow = v4 ? a.d <= 128 : a.d <= 32;
   if constexpr (KIND == kTileSlotRows) {
     if (a.d > 128 || a.d % kDuGroup != 0) throw CudaError("tile-blocked dU rows need d <= 128, a multiple of 16");
-    if (sgd) segment_backward_staged_kernel<true, kTileSlotRows><<<grid, kThreads, 0, s>>>(a);
-    else segment_backward_staged_kernel<false, kTileSlotRows><<<grid, kThreads, 0, s>>>(a);
+    if (sgd) run_bwd(segment_backward_staged_kernel<true, kTileSlotRows>, a, num_sms, s, true);
+    else run_bwd(segment_backward_staged_kernel<false, kTileSlotRows>, a, num_sms, s, true);
   } else if (KIND == kPlainRows && v4 && narrow) {
-    if (sgd) segment_backward_staged_kernel<true><<<grid, kThreads, 0, s>>>(a);
-    else segment_backward_staged_kernel<false><<<grid, kThreads, 0, s>>>(a);
+    if (sgd) run_bwd(segment_backward_staged_kernel<true>, a, num_sms, s, true);
+    else run_bwd(segment_backward_staged_kernel<false>, a, num_sms, s, true);
   } else if (sgd) {
     if (v4) {
-      if (narrow) segment_backward_kernel<KIND, true, 4, 1><<<grid, kThreads, 0, s>>>(a);
+      if (narrow) run_bwd(segment_backward_kernel<KIND, true, 4, 1>, a, num_sms, s);
       else if (KIND == kTorusE_L2 || KIND == kTorusE_L1)  // L2-resident wide rows: 8 in flight (C3 -9%)
-        segment_backward_kernel<KIND, true, 4, 2, 8><<<grid, kThreads, 0, s>>>(a);
-      else segment_backward_kernel<KIND, true, 4, 2><<<grid, kThreads, 0, s>>>(a);
+        run_bwd(segment_backward_kernel<KIND, true, 4, 2, 8>, a, num_sms, s);
+      else run_bwd(segment_backward_kernel<KIND, true, 4, 2>, a, num_sms, s);
     } else {
-      if (narrow) segment_backward_kernel<KIND, true, 1, 1><<<grid, kThreads, 0, s>>>(a);
-      else segment_backward_kernel<KIND, true, 1, 2><<<grid, kThreads, 0, s>>>(a);
+      if (narrow) run_bwd(segment_backward_kernel<KIND, true, 1, 1>, a, num_sms, s);
+      else run_bwd(segment_backward_kernel<KIND, true, 1, 2>, a, num_sms, s);
     }
   } else {
     if (v4) {
-      if (narrow) segment_backward_kernel<KIND, false, 4, 1><<<grid, kThreads, 0, s>>>(a);
-      else segment_backward_kernel<KIND, false, 4, 2><<<grid, kThreads, 0, s>>>(a);
+      if (narrow) run_bwd(segment_backward_kernel<KIND, false, 4, 1>, a, num_sms, s);
+      else run_bwd(segment_backward_kernel<KIND, false, 4, 2>, a, num_sms, s);
     } else {
-      if (narrow) segment_backward_kernel<KIND, false, 1, 1><<<grid, kThreads, 0, s>>>(a);
-      else segment_backward_kernel<KIND, false, 1, 2><<<grid, kThreads, 0, s>>>(a);
+      if (narrow) run_bwd(segment_backward_kernel<KIND, false, 1, 1>, a, num_sms, s);
+      else run_bwd(segment_backward_kernel<KIND, false, 1, 2>, a, num_sms, s);
     }
   }
   count_launch();
@@ -853,6 +888,21 @@ void configure_kind() {
 
 // Opt every staged-tile kernel into > 48 KB dynamic shared memory. Called once
 // per context at creation, outside any stream capture.
+int64_t bwd_trace(int enable, unsigned long long* out, uint32_t* info, int64_t cap) {
+  SKG_CUDA(cudaMemcpyToSymbol(g_bwtrace_on, &enable, sizeof(int)));
+  if (enable) {
+    static const unsigned long long z[kBwTrWarps * 2] = {};
+    static const uint32_t zi[kBwTrWarps] = {};
+    SKG_CUDA(cudaMemcpyToSymbol(g_bwtrace, z, sizeof(z)));
+    SKG_CUDA(cudaMemcpyToSymbol(g_bwtrace_info, zi, sizeof(zi)));
+  }
+  if (out && cap >= kBwTrWarps) {
+    SKG_CUDA(cudaMemcpyFromSymbol(out, g_bwtrace, sizeof(unsigned long long) * 2 * kBwTrWarps));
+    SKG_CUDA(cudaMemcpyFromSymbol(info, g_bwtrace_info, sizeof(uint32_t) * kBwTrWarps));
+  }
+  return kBwTrWarps;
+}
+
 void configure_hrt_kernels() {
   configure_kind<kTransE_L2>();
   configure_kind<kTransE_L1>();

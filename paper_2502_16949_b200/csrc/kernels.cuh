@@ -112,6 +112,7 @@ struct BwdArgs {
 };
 
 void configure_hrt_kernels();
+int64_t bwd_trace(int enable, unsigned long long* out, uint32_t* info, int64_t cap);  // debug
 void configure_ht_kernels();
 void launch_hrt_forward(int kind, bool train, const FwdArgs& a, int num_sms, cudaStream_t s);
 void launch_segment_backward(int kind, bool sgd, const BwdArgs& a, int num_sms, cudaStream_t s);
