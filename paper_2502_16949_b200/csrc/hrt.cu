@@ -673,16 +673,20 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nw = gridDim.x * (blockDim.x >> 5);
+#ifdef SKG_BWD_TRACE  // debug build only: the stamps cost registers (C5: 80 -> 87, one block per SM less)
   const bool trc = g_bwtrace_on == a.batch + 1 && gw < kBwTrWarps;
   uint32_t tr_info = 0;
   if (trc && lane == 0) stamp_now(&g_bwtrace[2 * gw]);
+#endif
   const uint32_t s0 = a.seg_base[a.batch], s1 = a.seg_base[a.batch + 1];
   const int dv = a.d / VEC;
   const V* RV = reinterpret_cast<const V*>(a.res);
   for (uint32_t s = s0 + gw; s < s1; s += nw) {
     const uint32_t col = a.seg_col[s];
+#ifdef SKG_BWD_TRACE
     if (trc) tr_info += (col >= static_cast<uint32_t>(a.N) && col != kDummyCol ? (1u << 16) : 0u) +
                         (col != kDummyCol ? a.seg_start[s + 1] - a.seg_start[s] : 0u);
+#endif
     if (col == kDummyCol || (a.entity_only && col >= static_cast<uint32_t>(a.N))) continue;
     const uint32_t e0 = a.seg_start[s], e1 = a.seg_start[s + 1];
     V* P = reinterpret_cast<V*>(a.X) + static_cast<size_t>(col) * dv;
@@ -754,10 +758,12 @@ __global__ void __launch_bounds__(kThreads) segment_backward_kernel(const BwdArg
       }
     }
   }
+#ifdef SKG_BWD_TRACE
   if (trc && lane == 0) {
     stamp_now(&g_bwtrace[2 * gw + 1]);
     g_bwtrace_info[gw] = tr_info;
   }
+#endif
 }
 
 

@@ -1,4 +1,5 @@
-"""Per-warp timeline of the segment backward (bench config, one minibatch): when warps
+"""Per-warp timeline of the segment backward (bench config, one minibatch; needs a build with
+-DSKG_BWD_TRACE, e.g. tools/build_variants.sh trace -DSKG_BWD_TRACE): when warps
 that handled relation segments finish vs the others. Debug tool: python tools/bwd_trace.py C1"""
 import ctypes
 import os
