@@ -380,6 +380,31 @@ void gen_perm(skg_ctx* ctx, const EpochShape& es, const uint64_t* seed, int32_t*
 
 void build_plan_from_order(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s);
 
+ThTilePlan th_plan_of(const skg_ctx* ctx, const EpochShape& es, PlanSlot& ps) {
+  ThTilePlan tp;
+  if (!ps.th_on) return tp;
+  tp.meta = ps.th_meta.p;
+  tp.rows = ps.th_rows.p;
+  tp.pos = ps.th_pos.p;
+  tp.info = ps.th_info.p;
+  tp.B = es.B;
+  (void)ctx;
+  return tp;
+}
+
+void transh_tile_plan_for(skg_ctx* ctx, const EpochShape& es, PlanSlot& ps, cudaStream_t s) {
+  FwdArgs fa{};
+  fa.pair_ht = ps.plan.pair_ht;
+  fa.N = ctx->N;
+  BwdArgs ba{};
+  ba.ent_val = ps.plan.sorted_val;
+  ba.seg_start = ps.plan.seg_start;
+  ba.seg_col = ps.plan.seg_col;
+  ba.seg_base = ps.plan.seg_base;
+  ba.N = ctx->N;
+  transh_tile_plan(fa, ba, es.B, es.nb, ctx->M, ctx->R, th_plan_of(ctx, es, ps), s);
+}
+
 void enqueue_plan(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s) {
   gen_perm(ctx, es, ctx->seed_eff.p + slot, ctx->slots[slot].order.p, s);
   build_plan_from_order(ctx, es, slot, s);
@@ -404,6 +429,7 @@ void build_plan_from_order(skg_ctx* ctx, const EpochShape& es, int slot, cudaStr
     build_epoch_plan(ps.order_g.p, ctx->quad.p, ctx->Rl.p, es.Mg, es.S, ctx->N, ctx->R, ps.plan, s);
   } else {
     build_epoch_plan(ps.order.p, ctx->quad.p, ctx->Rl.p, ctx->M, es.B, ctx->N, ctx->R, ps.plan, s);
+    if (ps.th_on) transh_tile_plan_for(ctx, es, ps, s);
   }
 }
 
@@ -586,7 +612,9 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
         if (markp) (*markp)();
         wait_snapshot();
       };
-      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, b == 0 ? &mark0 : markp, ctx->R, nullptr, &br);
+      const ThTilePlan tp = th_plan_of(ctx, es, ps);
+      ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, b == 0 ? &mark0 : markp, ctx->R, nullptr, &br,
+                     tp.meta ? &tp : nullptr);
       if (b == 0) wait_snapshot();  // (if the step had no mark call)
     }
   }
@@ -629,9 +657,21 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
     if (ctx->dp) ctx->dp_grad.ensure(ctx->N * ctx->de + ctx->R * ctx->dr + ctx->proj.n + ctx->normals.n + 2);
   }
   for (auto& p : ctx->perm) p.ensure(ctx->M + 1);
+  // TransH relation tiles precomputed with the plan (single device, tile kernel, bounded size)
+  const int64_t th_mt = transh_tile_plan_tiles(es.B, ctx->R);
+  const bool th_on = (es.kind == kTransH_L2 || es.kind == kTransH_L1) && !ctx->dp && !ctx->shard &&
+                     transh_tiles_supported(static_cast<int>(ctx->de), static_cast<int>(ctx->dr), ctx->R) &&
+                     es.nb * th_mt * 656 <= (512ll << 20) && std::getenv("SKG_TH_NO_PLAN") == nullptr;
   for (auto& sl : ctx->slots) {
     sl.order.ensure(ctx->M + 1);
     if (!ctx->shard) sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
+    sl.th_on = th_on;
+    if (th_on) {
+      sl.th_meta.ensure(es.nb * th_mt);
+      sl.th_rows.ensure(es.nb * th_mt * 32);
+      sl.th_pos.ensure(es.nb * th_mt * 32);
+      sl.th_info.ensure(es.nb * (4 + 3 * ctx->R));
+    }
   }
   ctx->shuffle.reserve(ctx->M);
   if (ctx->quad_version != ctx->data_version || ctx->quad.n < ctx->M + 1) {  // packed ids for the plan
@@ -677,14 +717,16 @@ std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
                  ctx->slots[0].order_g.p, ctx->slots[1].order_g.p, ctx->proj.p, ctx->normals.p, margin,
                  // shapes baked into the captured launches (strides, relation offset, plan id space)
                  ctx->N, ctx->R, ctx->de, ctx->dr, ctx->cfg.dim_entity, ctx->proj.n, ctx->normals.n, dp_comm_tag(ctx),
-                 ctx->phase_timers, ctx->stamps.p, ctx->shard, shard_tag(ctx));
+                 ctx->phase_timers, ctx->stamps.p, ctx->shard, shard_tag(ctx), ctx->slots[0].th_meta.p,
+                 ctx->slots[1].th_meta.p, ctx->slots[0].th_rows.p, ctx->slots[1].th_rows.p, ctx->slots[0].th_pos.p,
+                 ctx->slots[1].th_pos.p, ctx->slots[0].th_info.p, ctx->slots[1].th_info.p, ctx->slots[0].th_on);
 }
 
 // Identity of an epoch plan: everything it depends on.
 std::string plan_key(skg_ctx* ctx, const EpochShape& es, const skg_train_config& tc, int64_t epoch) {
   const uint64_t seed = es.shuffle ? tc.seed : 0;
   return raw_key(epoch, seed, es.shuffle, es.B, ctx->M, ctx->data_version, es.world, es.rank, ctx->H.p, ctx->NH.p,
-                 ctx->N, ctx->R, dp_comm_tag(ctx));
+                 ctx->N, ctx->R, dp_comm_tag(ctx), ctx->slots[0].th_on);  // th_on: the plan carries TransH tiles
 }
 
 void finish_epoch(skg_ctx* ctx, const EpochShape& es, int64_t epoch, skg_epoch_report* rep) {

@@ -53,6 +53,11 @@ struct HostNarrow;  // engine.cu
 struct PlanSlot {
   DevBuf<int32_t> order, order_g;
   EpochPlan plan;
+  // TransH relation tiles of every batch (transh_tile_plan), built with the plan
+  DevBuf<int4> th_meta, th_rows;
+  DevBuf<int32_t> th_pos;
+  DevBuf<uint32_t> th_info;
+  bool th_on = false;
   std::string key;  // which (epoch, seed, data version, shape) the slot holds
 };
 

@@ -505,7 +505,8 @@ void configure_ht_kernels() {
 }
 
 void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                    const std::function<void()>* mark, int64_t R, const HtSinks* sinks, const Branch* br) {
+                    const std::function<void()>* mark, int64_t R, const HtSinks* sinks, const Branch* br,
+                    const ThTilePlan* tp) {
   if (kind == kTransR_L2 || kind == kTransR_L1) {
     transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R, sinks);
     return;
@@ -513,7 +514,7 @@ void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work,
   float* normals = const_cast<float*>(fa.normals);
   if (transh_tiles_supported(fa.de, fa.dr, R)) {  // relation-tiled path (transh_train.cu)
     // the tile kernel renormalizes the normals itself (data parallel: after the dense step)
-    transh_tiles_train_batch(kind == kTransH_L2, fa, ba, work, R, num_sms, s, mark, sinks, br);
+    transh_tiles_train_batch(kind == kTransH_L2, fa, ba, work, R, num_sms, s, mark, sinks, br, tp);
     if (mark) (*mark)();
     return;
   }

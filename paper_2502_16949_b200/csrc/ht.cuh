@@ -27,6 +27,19 @@ struct Branch {
   cudaEvent_t fork, join;
 };
 
+// TransH relation tiles of every minibatch, precomputed on the plan branch
+// (transh_tile_plan): per batch mt = transh_tile_plan_tiles(B, R) tile records.
+struct ThTilePlan {
+  int4* meta = nullptr;    // [nb][mt] {run, relation, pairs, 0}
+  int4* rows = nullptr;    // [nb][mt][32] {h, t, neg h, neg t}
+  int32_t* pos = nullptr;  // [nb][mt][32]
+  uint32_t* info = nullptr;  // [nb][4 + 3R]
+  int64_t B = 0;           // batch size the records were built for
+};
+int64_t transh_tile_plan_tiles(int64_t B, int64_t R);
+void transh_tile_plan(const FwdArgs& fa, const BwdArgs& ba, int64_t B, int64_t nb, int64_t M, int64_t R,
+                      const ThTilePlan& tp, cudaStream_t s);
+
 // embedding.cpp:181-189 on the TransH normals (after a data-parallel dense step)
 void launch_normals_renorm(float* normals, int64_t R, int d, uint32_t* err, cudaStream_t s);
 // Floats of per-batch scratch the ht kernels need for `rows` rows.
@@ -38,7 +51,7 @@ int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R
 // the backward for per-phase profiling.
 void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                     const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr,
-                    const Branch* br = nullptr);
+                    const Branch* br = nullptr, const ThTilePlan* tp = nullptr);
 // score_batch for ht models (res = v, res_u = u, scores). `ba` carries the
 // batch's plan (TransR groups rows by relation through it).
 void ht_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s, int64_t R);
@@ -58,7 +71,7 @@ int64_t transh_tiles_work_floats(int64_t rows, int64_t R);
 int64_t transh_trace(int enable, unsigned long long* out, int64_t cap);  // debug: phase timestamps
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
                               cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks = nullptr,
-                              const Branch* br = nullptr);
+                              const Branch* br = nullptr, const ThTilePlan* tp = nullptr);
 
 // TransR (transr.cu)
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R);

@@ -62,6 +62,10 @@ struct TArgs {
   const float* lr;
   float* nrm_sink;            // data parallel: normals gradient sink (null: SGD in place)
   int64_t R;
+  // the epoch plan's precomputed tiles of this batch (transh_tile_plan), or null: chase them here
+  const int4* tp_meta;   // per tile {relation run k, relation r, pairs np, 0}
+  const int4* tp_rows;   // per tile x pair {h, t, neg h, neg t}
+  const int32_t* tp_pos; // per tile x pair: batch position (-1: padding)
 };
 
 __device__ __forceinline__ float4 f4sub(float4 a, float4 b) {
@@ -167,7 +171,6 @@ struct PipeMeta {
   int4 rows[kRows];  // warp-major: rows 8w..8w+3 = pos of pairs 4w..4w+3, 8w+4.. = their negatives
   float wr[kD], dr[kD];  // w_r and d_r rows (copied with the stage)
   int k, r, np;
-  uint32_t first, end;  // relation k's tile range [first, end)
 };
 struct PipeSmem {
   float H[kStages][kRows * kStride];  // head rows (v overwrites them)
@@ -266,7 +269,20 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
       (rr & 1 ? S.meta[rr >> 1].dr : S.meta[rr >> 1].wr)[c] = 0.f;
     }
   }
-  if (warp == kLoaderWarp) {
+  if (warp == kLoaderWarp && a.tp_meta) {  // tiles precomputed by the plan (a.info is the plan's)
+    if (lane == 0) {
+      const uint32_t T = alive ? a.info[1] : 0u;
+      const uint32_t t0 = range_start(blockIdx.x, T, G), t1 = range_start(blockIdx.x + 1, T, G);
+      S.T = T;
+      S.t0 = t0;
+      S.ntile = t1 - t0;
+      for (int i = 0; i < kStages; ++i) {
+        tc::mbar_init(&S.full[i], 32 * kLoaders + 1);
+        tc::mbar_init(&S.empty[i], kCompute);
+      }
+      tc::fence_barrier_init();
+    }
+  } else if (warp == kLoaderWarp) {
     if (alive) enumerate_rel_tiles(a, S.rt);
     __syncwarp();
     if (blockIdx.x == 0 && alive)
@@ -309,8 +325,30 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
     for (uint32_t g = 0; g < ntile; g += kChase) {
       int pos[kChase], np[kChase];
       uint32_t kq[kChase];
+      int rr_[kChase];
+      int4 pr_[kChase];
+      if (a.tp_meta) {  // the plan's tile records: one load per pair, no chase
+#pragma unroll
+        for (int c = 0; c < kChase; ++c) {
+          pos[c] = -1;
+          np[c] = 0;
+          kq[c] = 0;
+          rr_[c] = 0;
+          pr_[c] = make_int4(0, 0, 0, 0);
+          if (g + c < ntile) {
+            const uint32_t t = t0 + g + c;
+            const int4 mt = __ldg(a.tp_meta + t);
+            kq[c] = static_cast<uint32_t>(mt.x);
+            rr_[c] = mt.y;
+            np[c] = mt.z;
+            pos[c] = __ldg(a.tp_pos + static_cast<size_t>(t) * kPairs + lane);
+            pr_[c] = __ldg(a.tp_rows + static_cast<size_t>(t) * kPairs + lane);
+          }
+        }
+      }
 #pragma unroll
       for (int c = 0; c < kChase; ++c) {
+        if (a.tp_meta) break;
         pos[c] = -1;
         np[c] = 0;
         kq[c] = 0;
@@ -329,7 +367,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
       for (int c = 0; c < kChase; ++c) {
         pr[c] = make_int4(0, 0, -1, 0);
         ng[c] = make_int4(0, 0, -1, 0);
-        if (pos[c] >= 0) {
+        if (pos[c] >= 0 && a.tp_meta) {
+          pr[c] = make_int4(pr_[c].x, pr_[c].y, pos[c], 0);
+          ng[c] = make_int4(pr_[c].z, pr_[c].w, pos[c] + f.B, 0);
+        } else if (pos[c] >= 0) {
           int h, tt, nh, nt;
           if (f.pair_ht) {
             const int4 x = __ldg(f.pair_ht + pos[c]);
@@ -353,13 +394,11 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
           const int mp = kRowsPerWarp * (lane / kHalf) + lane % kHalf;  // warp-major slot of pair `lane`
           M.rows[mp] = pr[c];
           M.rows[mp + kHalf] = ng[c];
-          const int64_t r = static_cast<int64_t>(__ldg(a.seg_col + S.rt.seg[kq[c]])) - f.N;
+          const int64_t r = a.tp_meta ? rr_[c] : static_cast<int64_t>(__ldg(a.seg_col + S.rt.seg[kq[c]])) - f.N;
           if (lane == 0) {
             M.k = static_cast<int>(kq[c]);
             M.r = static_cast<int>(r);
             M.np = np[c];
-            M.first = S.rt.first[kq[c]];
-            M.end = S.rt.first[kq[c] + 1];
           }
           if (lane < d4) {
             tc::cp_async16(M.wr + 4 * lane, f.normals + r * d + 4 * lane);
@@ -627,6 +666,58 @@ __global__ void __launch_bounds__(2 * kD) transh_rel_finalize_kernel(const TArgs
   if (!present) renorm_normal(const_cast<float*>(f.normals), b, f.de, lane, f.err);
 }
 
+// Per minibatch b of the epoch plan (one block each, on the plan branch):
+// the batch's relation tiles as the forward walks them -- per tile {run k,
+// relation r, pairs}, per pair its ids and batch position -- and the run table
+// transh_rel_finalize_kernel reads ({runs, tiles, 0, 0, then r, first, end per
+// run}). The forward then loads each tile's records directly instead of
+// chasing seg_start -> ent_val -> pair record at the start of every batch.
+__global__ void __launch_bounds__(256) transh_tile_plan_kernel(TArgs a, int64_t B_full, int64_t nb, int64_t M,
+                                                               int64_t mt, int4* meta, int4* rows, int32_t* pos,
+                                                               uint32_t* info) {
+  __shared__ RelTiles rt;
+  const int64_t b = blockIdx.x;  // batch; blockIdx.y: slice of its tiles
+  if (b >= nb) return;
+  a.batch = static_cast<int>(b);
+  const int tid = threadIdx.x;
+  if (tid < 32) enumerate_rel_tiles(a, rt);
+  __syncthreads();
+  const uint32_t T = static_cast<uint32_t>(min(static_cast<int64_t>(rt.first[rt.nrel]), mt));
+  const int64_t lo = b * B_full, Bb = min(B_full, M - lo);
+  const int4* pair_ht = a.f.pair_ht + lo;
+  uint32_t* inf = info + b * (4 + 3 * a.R);
+  int4* mb = meta + b * mt;
+  int4* rb = rows + b * mt * kPairs;
+  int32_t* pb = pos + b * mt * kPairs;
+  if (blockIdx.y == 0) {
+    for (uint32_t q = tid; q < rt.nrel; q += blockDim.x) {
+      inf[4 + 3 * q] = static_cast<uint32_t>(__ldg(a.seg_col + rt.seg[q]) - static_cast<uint32_t>(a.f.N));
+      inf[5 + 3 * q] = rt.first[q];
+      inf[6 + 3 * q] = rt.first[q + 1];
+    }
+    if (tid == 0) {
+      inf[0] = rt.nrel;
+      inf[1] = T;
+    }
+  }
+  for (uint32_t i = blockIdx.y * blockDim.x + tid; i < T * kPairs; i += gridDim.y * blockDim.x) {
+    const uint32_t t = i / kPairs, p = i % kPairs;
+    const uint32_t kq = rel_of_tile(rt, t);
+    const uint32_t sq = rt.seg[kq], pq = (t - rt.first[kq]) * kPairs;
+    const uint32_t e0 = __ldg(a.seg_start + sq), len = __ldg(a.seg_start + sq + 1) - e0;
+    const int np = static_cast<int>(min(static_cast<uint32_t>(kPairs), len / 2 - pq));
+    int ps = -1;
+    int4 q4 = make_int4(0, 0, 0, 0);
+    if (static_cast<int>(p) < np) {
+      ps = static_cast<int>(__ldg(a.ent_val + e0 + pq + p) & 0x7fffffffu);
+      if (ps < Bb) q4 = __ldg(pair_ht + ps);
+    }
+    rb[i] = q4;
+    pb[i] = ps;
+    if (p == 0) mb[t] = make_int4(static_cast<int>(kq), static_cast<int>(__ldg(a.seg_col + sq) - static_cast<uint32_t>(a.f.N)), np, 0);
+  }
+}
+
 }  // namespace
 
 // any width up to 128 in 16-byte chunks: rows are staged zero-padded to 128 columns
@@ -645,6 +736,26 @@ int64_t transh_trace(int enable, unsigned long long* out, int64_t cap) {
   return n;
 }
 
+int64_t transh_tile_plan_tiles(int64_t B, int64_t R) { return relation_max_tiles(2 * B, R); }
+
+void transh_tile_plan(const FwdArgs& fa, const BwdArgs& ba, int64_t B, int64_t nb, int64_t M, int64_t R,
+                      const ThTilePlan& tp, cudaStream_t s) {
+  TArgs a{};
+  a.f = fa;
+  a.ent_val = ba.ent_val;
+  a.seg_start = ba.seg_start;
+  a.seg_col = ba.seg_col;
+  a.seg_base = ba.seg_base;
+  a.R = R;
+  const int64_t mt = transh_tile_plan_tiles(B, R);
+  // (batch, slice) blocks: the records' dependent loads spread over the SMs
+  const unsigned slices = static_cast<unsigned>(std::min<int64_t>(64, std::max<int64_t>(1, mt * kPairs / 2048)));
+  transh_tile_plan_kernel<<<dim3(static_cast<unsigned>(nb), slices), 256, 0, s>>>(a, B, nb, M, mt, tp.meta, tp.rows,
+                                                                                   tp.pos, tp.info);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
 int64_t transh_tiles_work_floats(int64_t rows, int64_t R) {
   const int64_t mt = relation_max_tiles(rows, R);
   return (mt + R + 1) * 2 * kD + 3 * R + 64;  // run info, then (CTA, relation run) slots b + k, b < grid <= mt
@@ -660,7 +771,7 @@ void configure_transh_tiles_kernels() {
 
 void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, float* work, int64_t R, int num_sms,
                               cudaStream_t s, const std::function<void()>* mark, const HtSinks* sinks,
-                              const Branch* br) {
+                              const Branch* br, const ThTilePlan* tp) {
   const int64_t mt = relation_max_tiles(2 * static_cast<int64_t>(fa.B), R);
   // run info leads the workspace (a fixed address for every batch size), the
   // float4 run partials follow
@@ -680,6 +791,14 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
   a.lr = ba.lr;
   a.nrm_sink = sinks ? sinks->normals : nullptr;
   a.R = R;
+  if (tp && tp->meta) {  // this batch's slice of the plan's tile records
+    const int64_t mtp = transh_tile_plan_tiles(tp->B, R);
+    a.tp_meta = tp->meta + ba.batch * mtp;
+    a.tp_rows = tp->rows + ba.batch * mtp * kPairs;
+    a.tp_pos = tp->pos + ba.batch * mtp * kPairs;
+    a.info = tp->info + ba.batch * (4 + 3 * R);
+    a.mt = mtp;
+  }
   const size_t smem = sizeof(PipeSmem);
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(mt, num_sms));  // persistent, one CTA per SM
   const bool full = fa.de == kD;
