@@ -475,3 +475,42 @@ def _deferred_body(eng, orc32, cfg, tc_e, tc_o, st, P, h, rel, t, nh, nt, n, r):
     gh, gt = eng.negative_sample(11)
     oh, ot = orc32.negative_sample(h, rel, t, n, r, 11)
     assert np.array_equal(gh, oh) and np.array_equal(gt, ot)
+
+
+def test_deferred_reupload_large_narrowing(eng, orc32):
+    """Host-narrowed deferred uploads at a size that spreads the five id arrays over
+    every narrowing thread and all four DMA waves: an identical re-upload keeps the
+    speculative epoch (hit), one changed negative id in the last wave is detected
+    (miss) and retrained; tables stay bitwise the oracle's."""
+    n, r, d = 20000, 60, 8
+    h, rel, t = orc32.synthetic_train(n, r, 220000, 11)
+    m = len(h)
+    st = orc32.init_store("transe", n, r, d, d, 11)
+    cfg = ModelConfig.make("transe", d, d, "l2")
+    tc_e = TrainConfig.make(batch_size=8192, seed=4, lr=0.05)
+    tc_o = orc32.train_config(batch_size=8192, seed=4, lr=0.05)
+    nh, nt = orc32.negative_sample(h, rel, t, n, r, 2)
+    P = [_pinned(x) for x in (h, rel, t, nh, nt)]
+    eng.store_upload(cfg, st.entity, st.relation)
+    eng.set_triples(*P[:3], n, r)
+    eng.set_negatives(*P[3:])
+    eng.train_epoch(cfg, tc_e, 0, 0.05)
+    orc32.train_epoch("transe", st, (h, rel, t), (nh, nt), tc_o, 0, 0.05)
+    eng.set_deferred_uploads(True)
+    try:
+        hits0, miss0 = eng.upload_stats()
+        bytes0 = eng.upload_bytes()
+        for ep in (1, 2):
+            if ep == 2:
+                P[4][m - 3] = (P[4][m - 3] + 1) % n  # last wave, last array
+            eng.set_triples(*P[:3], n, r)
+            eng.set_negatives(*P[3:])
+            eng.train_epoch(cfg, tc_e, ep, 0.05)
+            orc32.train_epoch("transe", st, (h, rel, t), (np.asarray(P[3]), np.asarray(P[4])), tc_o, ep, 0.05)
+            ge, gr, _, _ = eng.store_download()
+            assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation), ep
+        hits1, miss1 = eng.upload_stats()
+        assert (hits1 - hits0, miss1 - miss0) == (1, 1)
+        assert eng.upload_bytes() - bytes0 == 2 * 5 * m * 4  # int32 on the wire
+    finally:
+        eng.set_deferred_uploads(False)
