@@ -508,7 +508,7 @@ void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work,
                     const std::function<void()>* mark, int64_t R, const HtSinks* sinks, const Branch* br,
                     const ThTilePlan* tp) {
   if (kind == kTransR_L2 || kind == kTransR_L1) {
-    transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R, sinks);
+    transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R, sinks, br);
     return;
   }
   float* normals = const_cast<float*>(fa.normals);

@@ -77,7 +77,8 @@ void transh_tiles_train_batch(bool l2, const FwdArgs& fa, const BwdArgs& ba, flo
 int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R);
 void configure_transr_kernels();
 void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                        const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr);
+                        const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr,
+                        const Branch* br = nullptr);
 void transr_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                   int64_t R);
 void transr_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj, int num_sms,

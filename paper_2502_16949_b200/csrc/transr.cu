@@ -555,7 +555,7 @@ void run_tc(int kind, int mode, const FwdArgs& fa, const BwdArgs& ba, const Work
 }  // namespace
 
 void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                        const std::function<void()>* mark, int64_t R, const HtSinks* sinks) {
+                        const std::function<void()>* mark, int64_t R, const HtSinks* sinks, const Branch* br) {
   const Work w = carve(work, 2 * static_cast<int64_t>(fa.B), fa.de, fa.dr, R);
   // data parallel (sinks): entity rows accumulate into ba.X, proj / relation
   // gradients land in the sinks, and the engine applies one dense step
@@ -573,12 +573,22 @@ void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* w
                            w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, w.mr_chunks, R, num_sms, s,
                            sinks != nullptr);
     if (mark) (*mark)();
+    // relation side (M_r and relation rows) on a forked branch beside the entity segment pass:
+    // disjoint parameters, both read only the projection kernel's outputs
+    cudaStream_t as = s;
+    if (br) {
+      SKG_CUDA(cudaEventRecord(br->fork, s));
+      SKG_CUDA(cudaStreamWaitEvent(br->aux, br->fork, 0));
+      as = br->aux;
+    }
+    launch_transr_train_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
+                              proj_dst, rel_dst, ba.lr, ba.err, w.mr_chunks, R, as, sinks != nullptr, fa.dr, fa.de);
+    if (br) SKG_CUDA(cudaEventRecord(br->join, br->aux));
     BwdArgs eb = ba;
     eb.entity_only = 1;
     eb.d = fa.de;
     launch_segment_backward(kTileSlotRows, sinks == nullptr, eb, num_sms, s);
-    launch_transr_train_apply(w.tile_total, w.seg_tiles, w.tile_seg, ba.seg_col, ba.N, num_sms, w.dm_part, w.dr_part,
-                              proj_dst, rel_dst, ba.lr, ba.err, w.mr_chunks, R, s, sinks != nullptr, fa.dr, fa.de);
+    if (br) SKG_CUDA(cudaStreamWaitEvent(s, br->join, 0));
     if (mark) (*mark)();
     return;
   }
