@@ -392,6 +392,17 @@ ThTilePlan th_plan_of(const skg_ctx* ctx, const EpochShape& es, PlanSlot& ps) {
   return tp;
 }
 
+TrTilePlan tr_plan_of(const EpochShape& es, PlanSlot& ps) {
+  TrTilePlan tp;
+  if (!ps.tr_on) return tp;
+  tp.tile_seg = ps.tr_seg.p;
+  tp.tile_p0 = ps.tr_p0.p;
+  tp.tile_total = ps.tr_total.p;
+  tp.seg_tiles = ps.tr_segtiles.p;
+  tp.B = es.B;
+  return tp;
+}
+
 void transh_tile_plan_for(skg_ctx* ctx, const EpochShape& es, PlanSlot& ps, cudaStream_t s) {
   FwdArgs fa{};
   fa.pair_ht = ps.plan.pair_ht;
@@ -430,6 +441,14 @@ void build_plan_from_order(skg_ctx* ctx, const EpochShape& es, int slot, cudaStr
   } else {
     build_epoch_plan(ps.order.p, ctx->quad.p, ctx->Rl.p, ctx->M, es.B, ctx->N, ctx->R, ps.plan, s);
     if (ps.th_on) transh_tile_plan_for(ctx, es, ps, s);
+    if (ps.tr_on) {
+      BwdArgs ba{};
+      ba.seg_start = ps.plan.seg_start;
+      ba.seg_col = ps.plan.seg_col;
+      ba.seg_base = ps.plan.seg_base;
+      ba.N = ctx->N;
+      transr_tile_plan(ba, es.B, es.nb, ctx->R, tr_plan_of(es, ps), s);
+    }
   }
 }
 
@@ -613,8 +632,9 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
         wait_snapshot();
       };
       const ThTilePlan tp = th_plan_of(ctx, es, ps);
+      const TrTilePlan trp = tr_plan_of(es, ps);
       ht_train_batch(es.kind, fa, ba, ctx->ht_work.p, ctx->num_sms, s, b == 0 ? &mark0 : markp, ctx->R, nullptr, &br,
-                     tp.meta ? &tp : nullptr);
+                     tp.meta ? &tp : nullptr, trp.tile_seg ? &trp : nullptr);
       if (b == 0) wait_snapshot();  // (if the step had no mark call)
     }
   }
@@ -662,10 +682,22 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
   const bool th_on = (es.kind == kTransH_L2 || es.kind == kTransH_L1) && !ctx->dp && !ctx->shard &&
                      transh_tiles_supported(static_cast<int>(ctx->de), static_cast<int>(ctx->dr), ctx->R) &&
                      es.nb * th_mt * 656 <= (512ll << 20) && std::getenv("SKG_TH_NO_PLAN") == nullptr;
+  // TransR relation tiles precomputed with the plan (single device, tcgen05 step)
+  const bool tr_on = (es.kind == kTransR_L2 || es.kind == kTransR_L1) && !ctx->dp && !ctx->shard &&
+                     transr_train_tc_supported(static_cast<int>(ctx->de), static_cast<int>(ctx->dr)) &&
+                     std::getenv("SKG_TR_NO_PLAN") == nullptr;
   for (auto& sl : ctx->slots) {
     sl.order.ensure(ctx->M + 1);
     if (!ctx->shard) sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
     sl.th_on = th_on;
+    sl.tr_on = tr_on;
+    if (tr_on) {
+      const int64_t mtr = relation_max_tiles(2 * es.B, ctx->R);
+      sl.tr_seg.ensure(es.nb * mtr);
+      sl.tr_p0.ensure(es.nb * mtr);
+      sl.tr_total.ensure(2 * es.nb);
+      sl.tr_segtiles.ensure(es.nb * (ctx->R + 2));
+    }
     if (th_on) {
       sl.th_meta.ensure(es.nb * th_mt);
       sl.th_rows.ensure(es.nb * th_mt * 32);
@@ -719,14 +751,18 @@ std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
                  ctx->N, ctx->R, ctx->de, ctx->dr, ctx->cfg.dim_entity, ctx->proj.n, ctx->normals.n, dp_comm_tag(ctx),
                  ctx->phase_timers, ctx->stamps.p, ctx->shard, shard_tag(ctx), ctx->slots[0].th_meta.p,
                  ctx->slots[1].th_meta.p, ctx->slots[0].th_rows.p, ctx->slots[1].th_rows.p, ctx->slots[0].th_pos.p,
-                 ctx->slots[1].th_pos.p, ctx->slots[0].th_info.p, ctx->slots[1].th_info.p, ctx->slots[0].th_on);
+                 ctx->slots[1].th_pos.p, ctx->slots[0].th_info.p, ctx->slots[1].th_info.p, ctx->slots[0].th_on,
+                 ctx->slots[0].tr_seg.p, ctx->slots[1].tr_seg.p, ctx->slots[0].tr_p0.p, ctx->slots[1].tr_p0.p,
+                 ctx->slots[0].tr_total.p, ctx->slots[1].tr_total.p, ctx->slots[0].tr_segtiles.p,
+                 ctx->slots[1].tr_segtiles.p, ctx->slots[0].tr_on);
 }
 
 // Identity of an epoch plan: everything it depends on.
 std::string plan_key(skg_ctx* ctx, const EpochShape& es, const skg_train_config& tc, int64_t epoch) {
   const uint64_t seed = es.shuffle ? tc.seed : 0;
   return raw_key(epoch, seed, es.shuffle, es.B, ctx->M, ctx->data_version, es.world, es.rank, ctx->H.p, ctx->NH.p,
-                 ctx->N, ctx->R, dp_comm_tag(ctx), ctx->slots[0].th_on);  // th_on: the plan carries TransH tiles
+                 ctx->N, ctx->R, dp_comm_tag(ctx), ctx->slots[0].th_on,  // the plan carries TransH / TransR tiles
+                 ctx->slots[0].tr_on);
 }
 
 void finish_epoch(skg_ctx* ctx, const EpochShape& es, int64_t epoch, skg_epoch_report* rep) {

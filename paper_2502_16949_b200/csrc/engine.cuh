@@ -58,6 +58,9 @@ struct PlanSlot {
   DevBuf<int32_t> th_pos;
   DevBuf<uint32_t> th_info;
   bool th_on = false;
+  // TransR relation tiles of every batch (transr_tile_plan)
+  DevBuf<uint32_t> tr_seg, tr_p0, tr_total, tr_segtiles;
+  bool tr_on = false;
   std::string key;  // which (epoch, seed, data version, shape) the slot holds
 };
 

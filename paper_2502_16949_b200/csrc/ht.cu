@@ -506,9 +506,9 @@ void configure_ht_kernels() {
 
 void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                     const std::function<void()>* mark, int64_t R, const HtSinks* sinks, const Branch* br,
-                    const ThTilePlan* tp) {
+                    const ThTilePlan* tp, const TrTilePlan* trp) {
   if (kind == kTransR_L2 || kind == kTransR_L1) {
-    transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R, sinks, br);
+    transr_train_batch(kind, fa, ba, work, num_sms, s, mark, R, sinks, br, trp);
     return;
   }
   float* normals = const_cast<float*>(fa.normals);

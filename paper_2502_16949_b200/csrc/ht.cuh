@@ -37,6 +37,14 @@ struct ThTilePlan {
   int64_t B = 0;           // batch size the records were built for
 };
 int64_t transh_tile_plan_tiles(int64_t B, int64_t R);
+// TransR relation tiles of every minibatch (transr_tile_plan): per batch b,
+// tile_seg / tile_p0 at b * relation_max_tiles(2B, R), tile_total at 2b,
+// seg_tiles at b (R + 2).
+struct TrTilePlan {
+  uint32_t *tile_seg = nullptr, *tile_p0 = nullptr, *tile_total = nullptr, *seg_tiles = nullptr;
+  int64_t B = 0;
+};
+void transr_tile_plan(const BwdArgs& ba, int64_t B, int64_t nb, int64_t R, const TrTilePlan& tp, cudaStream_t s);
 void transh_tile_plan(const FwdArgs& fa, const BwdArgs& ba, int64_t B, int64_t nb, int64_t M, int64_t R,
                       const ThTilePlan& tp, cudaStream_t s);
 
@@ -51,7 +59,7 @@ int64_t ht_work_floats(int kind, int64_t rows, int64_t de, int64_t dr, int64_t R
 // the backward for per-phase profiling.
 void ht_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                     const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr,
-                    const Branch* br = nullptr, const ThTilePlan* tp = nullptr);
+                    const Branch* br = nullptr, const ThTilePlan* tp = nullptr, const TrTilePlan* trp = nullptr);
 // score_batch for ht models (res = v, res_u = u, scores). `ba` carries the
 // batch's plan (TransR groups rows by relation through it).
 void ht_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s, int64_t R);
@@ -78,7 +86,7 @@ int64_t transr_work_floats(int64_t rows, int64_t de, int64_t dr, int64_t R);
 void configure_transr_kernels();
 void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                         const std::function<void()>* mark, int64_t R, const HtSinks* sinks = nullptr,
-                        const Branch* br = nullptr);
+                        const Branch* br = nullptr, const TrTilePlan* tp = nullptr);
 void transr_score(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
                   int64_t R);
 void transr_score_backward(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, float* g_proj, int num_sms,

@@ -57,14 +57,12 @@ struct TrArgs {
 // Thread per segment, block scan of the tile counts, then every thread
 // writes its own segment's tiles.
 constexpr int kTilesThreads = 1024;
-__global__ void __launch_bounds__(kTilesThreads) transr_tiles_kernel(
-    const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ seg_col, const uint32_t* __restrict__ seg_base,
-    int batch, int64_t N, int paired, uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_p0,
-    uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles, const uint32_t* __restrict__ err,
-    uint32_t* __restrict__ zero = nullptr, int nzero = 0, unsigned long long* stamp = nullptr) {
+__device__ __forceinline__ void tiles_body(const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ seg_col,
+                                           const uint32_t* __restrict__ seg_base, int batch, int64_t N, int paired,
+                                           uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_p0,
+                                           uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles,
+                                           const uint32_t* __restrict__ err) {
   __shared__ uint32_t wsum[kTilesThreads / 32];
-  if (stamp && threadIdx.x == 0) stamp_now(stamp);
-  for (int i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0u;  // per-relation tickets of the next kernel
   __shared__ uint32_t carry_t, nrel;
   __shared__ int stop;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -73,7 +71,7 @@ __global__ void __launch_bounds__(kTilesThreads) transr_tiles_kernel(
   if (tid == 0) {
     carry_t = 0;
     nrel = 0;
-    stop = err[0] != 0;
+    stop = err ? err[0] != 0 : 0;
   }
   __syncthreads();
   for (uint32_t base = s0; base < s1 && !stop; base += kTilesThreads) {
@@ -127,6 +125,27 @@ __global__ void __launch_bounds__(kTilesThreads) transr_tiles_kernel(
     tile_total[0] = carry_t;
     tile_total[1] = nrel;
   }
+}
+
+__global__ void __launch_bounds__(kTilesThreads) transr_tiles_kernel(
+    const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ seg_col, const uint32_t* __restrict__ seg_base,
+    int batch, int64_t N, int paired, uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_p0,
+    uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles, const uint32_t* __restrict__ err,
+    uint32_t* __restrict__ zero = nullptr, int nzero = 0, unsigned long long* stamp = nullptr) {
+  if (stamp && threadIdx.x == 0) stamp_now(stamp);
+  for (int i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0u;  // per-relation tickets of the next kernel
+  tiles_body(seg_start, seg_col, seg_base, batch, N, paired, tile_seg, tile_p0, tile_total, seg_tiles, err);
+}
+
+// Every minibatch's relation tiles of an epoch plan at once (block b = batch b),
+// on the plan branch: the training step then starts with its projection kernel.
+__global__ void __launch_bounds__(kTilesThreads) transr_tiles_plan_kernel(
+    const uint32_t* __restrict__ seg_start, const uint32_t* __restrict__ seg_col, const uint32_t* __restrict__ seg_base,
+    int64_t N, int64_t mt, int64_t R, uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_p0,
+    uint32_t* __restrict__ tile_total, uint32_t* __restrict__ seg_tiles) {
+  const int64_t b = blockIdx.x;
+  tiles_body(seg_start, seg_col, seg_base, static_cast<int>(b), N, 1, tile_seg + b * mt, tile_p0 + b * mt,
+             tile_total + 2 * b, seg_tiles + b * (R + 2), nullptr);
 }
 
 template <bool L2, int MODE>
@@ -516,6 +535,14 @@ void configure_one() {
 
 int64_t relation_max_tiles(int64_t rows, int64_t R) { return max_tiles(rows, R); }
 
+void transr_tile_plan(const BwdArgs& ba, int64_t B, int64_t nb, int64_t R, const TrTilePlan& tp, cudaStream_t s) {
+  transr_tiles_plan_kernel<<<static_cast<unsigned>(nb), kTilesThreads, 0, s>>>(
+      ba.seg_start, ba.seg_col, ba.seg_base, ba.N, max_tiles(2 * B, R), R, tp.tile_seg, tp.tile_p0, tp.tile_total,
+      tp.seg_tiles);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
 void launch_relation_tiles(const BwdArgs& ba, int paired, uint32_t* tile_seg, uint32_t* tile_p0, uint32_t* tile_total,
                            uint32_t* seg_tiles, cudaStream_t s, uint32_t* zero, int nzero) {
   transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, paired,
@@ -555,20 +582,29 @@ void run_tc(int kind, int mode, const FwdArgs& fa, const BwdArgs& ba, const Work
 }  // namespace
 
 void transr_train_batch(int kind, const FwdArgs& fa, const BwdArgs& ba, float* work, int num_sms, cudaStream_t s,
-                        const std::function<void()>* mark, int64_t R, const HtSinks* sinks, const Branch* br) {
-  const Work w = carve(work, 2 * static_cast<int64_t>(fa.B), fa.de, fa.dr, R);
+                        const std::function<void()>* mark, int64_t R, const HtSinks* sinks, const Branch* br,
+                        const TrTilePlan* tp) {
+  Work w = carve(work, 2 * static_cast<int64_t>(fa.B), fa.de, fa.dr, R);
   // data parallel (sinks): entity rows accumulate into ba.X, proj / relation
   // gradients land in the sinks, and the engine applies one dense step
   float* proj_dst = sinks ? sinks->proj : const_cast<float*>(fa.proj);
   float* rel_dst = sinks ? sinks->rel : const_cast<float*>(fa.X) + fa.N * static_cast<int64_t>(fa.de);
   if (transr_train_tc_supported(fa.de, fa.dr)) {
-    transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, 1,
-                                                    w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err,
-                                                    nullptr, 0, fa.stamp_start);
-    count_launch();
-    SKG_LAUNCH_CHECK();
     FwdArgs fa_tc = fa;
-    fa_tc.stamp_start = nullptr;  // stamped by the tiles kernel, the batch's first launch
+    if (tp && tp->tile_seg) {  // tiles from the epoch plan: this batch's slice
+      const int64_t mtp = max_tiles(2 * tp->B, R);
+      w.tile_seg = tp->tile_seg + ba.batch * mtp;
+      w.tile_p0 = tp->tile_p0 + ba.batch * mtp;
+      w.tile_total = tp->tile_total + 2 * static_cast<int64_t>(ba.batch);
+      w.seg_tiles = tp->seg_tiles + ba.batch * (R + 2);
+    } else {
+      transr_tiles_kernel<<<1, kTilesThreads, 0, s>>>(ba.seg_start, ba.seg_col, ba.seg_base, ba.batch, ba.N, 1,
+                                                      w.tile_seg, w.tile_p0, w.tile_total, w.seg_tiles, ba.err,
+                                                      nullptr, 0, fa.stamp_start);
+      count_launch();
+      SKG_LAUNCH_CHECK();
+      fa_tc.stamp_start = nullptr;  // stamped by the tiles kernel, the batch's first launch
+    }
     launch_transr_train_tc(kind == kTransR_L2, fa_tc, ba.ent_val, ba.seg_start, ba.seg_col, w.tile_seg, w.tile_p0,
                            w.tile_total, w.seg_tiles, w.dm_part, w.dr_part, w.mr_chunks, R, num_sms, s,
                            sinks != nullptr);

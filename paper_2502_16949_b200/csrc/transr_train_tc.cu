@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool alive = f.err[0] == 0;
   const bool tr = g_trace_on == f.batch + 1;  // trace one chosen minibatch
+  if (f.stamp_start && blockIdx.x == 0 && tid == 0) stamp_now(f.stamp_start);  // the batch's first kernel (tiles planned)
   auto trace = [&](uint32_t it, int ev) { trace_ev(tr, it, ev); };
 
   if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
