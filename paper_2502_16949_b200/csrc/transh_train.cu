@@ -162,7 +162,7 @@ constexpr int kLoaders = SKG_TRANSH_LOADERS;   // copy warps (one warp's cp.asyn
 constexpr int kPipeThreads = (kCompute + kLoaders) * 32;
 constexpr int kLoaderWarp = kCompute;          // first loader: enumerates the tiles, writes the stage metadata
 #ifndef SKG_TH_STAGES
-#define SKG_TH_STAGES 3
+#define SKG_TH_STAGES 2  // 2: the ring leaves shared memory for plan-branch blocks on the same SM (CTAs start together)
 #endif
 constexpr int kStages = SKG_TH_STAGES;
 static_assert(kPairs % kLoaders == 0, "loaders split a tile's pairs evenly");
