@@ -334,6 +334,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool tr = g_trace_on == f.batch + 1;  // trace one chosen minibatch
   if (f.stamp_start && blockIdx.x == 0 && tid == 0) stamp_now(f.stamp_start);  // the batch's first kernel (tiles planned)
   auto trace = [&](uint32_t it, int ev) { trace_ev(tr, it, ev); };
+  if (tr && tid == 0 && blockIdx.x < kTrCtas) {  // CTA start (globaltimer, comparable across SMs) in the last slot
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    g_trace[(blockIdx.x * kTrTiles + kTrTiles - 1) * kTrEvents + kTrEvents - 1] = g;
+  }
 
   if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
   if (f.de < kD)  // row tiles narrower than 128: the gather never writes columns >= d_e, keep them zero

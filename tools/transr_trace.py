@@ -33,7 +33,8 @@ def main():
     L.skg_debug_transr_trace.restype = ctypes.c_int64
     L.skg_debug_transr_trace.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64]
     eng.train_epoch(cfg, tcfg, 0, bench.LR)  # warm (graph capture)
-    n = L.skg_debug_transr_trace(1, None, 0)  # trace batch 0
+    tb = int(os.environ.get("TR_TRACE_BATCH", "0"))
+    n = L.skg_debug_transr_trace(tb + 1, None, 0)  # trace batch tb
     eng.train_epoch(cfg, tcfg, 1, bench.LR)
     buf = np.zeros(n, np.uint64)
     L.skg_debug_transr_trace(0, buf.ctypes.data, n)
@@ -54,6 +55,11 @@ def main():
         s = [tr[cta, it, 0] for it in range(16) if tr[cta, it, 0] and tr[cta, it, 14]]
         per += list(np.diff(s))
     print("tile period (median cycles):", int(np.median(per)) if per else None)
+    st = tr[:148, 15, 15]
+    st = st[st > 0]
+    if len(st):
+        d = (st - st.min()) / 1e3
+        print(f"CTA start (globaltimer): median {np.median(d):.2f} us, p90 {np.percentile(d, 90):.2f}, max {d.max():.2f}")
 
 
 if __name__ == "__main__":
