@@ -111,7 +111,8 @@ struct Smem {
   float sc[kRows];  // per-row gradient scale of the current tile (pass 2 of the producers)
   float colsum[4][kD];
   float tl[2];
-  uint64_t g_full, u_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty, sc_full;
+  uint64_t g_full, v_full, dz_full, g2_done, du_empty, dm_full, dm_empty, sc_full;
+  uint64_t u_q[4];  // U columns [32 q, 32 q + 32) in TMEM: GEMM1 starts on the first K quarter
   uint64_t rows_full[2], rows_empty[2];
   uint64_t g3_full[kG3Slots], g3_empty[kG3Slots];
   uint64_t stg[kRows / 8];  // row group s consumed by GEMM3: its sU / sDZ rows may be refilled
@@ -178,10 +179,6 @@ __device__ __forceinline__ float4 f4sel(int c, float4 a, float4 b) {  // c ? a :
 // 32-byte chunk: rows with bit 2 set visit the two 16-byte units of each chunk
 // in swapped order, so the eight rows of a quarter-warp phase touch eight
 // distinct units.
-#ifndef SKG_TR_USPLIT
-#define SKG_TR_USPLIT 64
-#endif
-constexpr int kUSplit = SKG_TR_USPLIT;  // producers: columns [0, kUSplit); gather warps: the rest
 __device__ __forceinline__ void compute_u(Smem& S, uint32_t taddr, int p, bool ok_row, int c0, int c1, int de) {
   const int flip = (p >> 2) & 1;
 #pragma unroll 1
@@ -349,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   if (tid == 0) {
     tc::mbar_init(&S.g_full, 32 * kGatherWarps);
-    tc::mbar_init(&S.u_full, kUSplit < kD ? 256 : 128);
+    for (int q = 0; q < 4; ++q) tc::mbar_init(&S.u_q[q], 256);
     tc::mbar_init(&S.v_full, 1);
     tc::mbar_init(&S.dz_full, kDzSplit < kD ? 256 : 128);
     tc::mbar_init(&S.sc_full, 128);
@@ -402,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool last_of_run = (t + 1 == t1) || (a.seg_tiles[k + 1] <= t + 1);
       const int buf = it & 1;
       tc::mbar_wait(&S.rows_full[buf], (it >> 1) & 1);  // tile metadata (rows, rel, np)
-      tc::mbar_wait(&S.u_full, it & 1);
+      tc::mbar_wait(&S.u_q[3], it & 1);
       tc::mbar_wait(&S.v_full, it & 1);
       tc::fence_after();
       if (m == 0) trace(it, 11);
@@ -539,10 +536,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_after();
       }
       if (p == 0) trace(it, 15);
-      compute_u(S, tbase + lane_addr, p, rows[p].z >= 0, 0, kUSplit, f.de);
-      tc::tmem_wait_st();
-      tc::fence_before();
-      tc::mbar_arrive(&S.u_full);
+      // U by K quarters (this group: columns [32 q, 32 q + 16), the gather warps the other
+      // 16), each quarter released to GEMM1 as soon as it is in TMEM
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        compute_u(S, tbase + lane_addr, p, rows[p].z >= 0, 32 * q, 32 * q + 16, f.de);
+        tc::tmem_wait_st();
+        tc::fence_before();
+        tc::mbar_arrive(&S.u_q[q]);
+      }
       if (p == 0) trace(it, 2);
       if (kDzSplit < kD) {  // pass 2 of the epilogue on columns [kDzSplit, kD) of this warp's TMEM lanes
         tc::mbar_wait(&S.sc_full, it & 1);
@@ -572,12 +574,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (run >= 0 && first_of_run) ++nrun;
       run = k;
       const bool last_of_run = (t + 1 == t1) || (a.seg_tiles[k + 1] <= t + 1);
-      tc::mbar_wait(&S.u_full, it & 1);
       if (it > 0) tc::mbar_wait(&S.du_empty, (it - 1) & 1);  // V shares columns with the drained dU
+      tc::mbar_wait(&S.u_q[0], it & 1);
       tc::fence_after();
       trace(it, 5);
-      // GEMM1: V = U M_r^T
+      // GEMM1: V = U M_r^T, K quarter by K quarter as U's columns land in TMEM
       for (int c = 0; c < kChunksPerGemm; ++c, ++rn) {
+        if (c > 0 && (c & 1) == 0) {
+          tc::mbar_wait(&S.u_q[c >> 1], it & 1);
+          tc::fence_after();
+        }
         const int s = rn % kRing;
         tc::mbar_wait(&S.ring_full[s], (rn / kRing) & 1);
         tc::fence_after();
@@ -705,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         gather8(rows, s3 * 8);
       }
       tc::cp_async_mbar_arrive(&S.g_full);
-      if (kUSplit < kD) {  // columns [kUSplit, kD) of U for the rows of this warp's TMEM lane quadrant
+      {  // columns [32 q + 16, 32 q + 32) of U for the rows of this warp's TMEM lane quadrant
         const int q4 = warp & 3;
         const int row = q4 * 32 + lane;
         tc::mbar_wait(&S.g_full, it & 1);
@@ -713,10 +719,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mbar_wait(&S.g2_done, (it - 1) & 1);
           tc::fence_after();
         }
-        compute_u(S, tbase + (static_cast<uint32_t>(q4 * 32) << 16), row, rows[row].z >= 0, kUSplit, kD, f.de);
-        tc::tmem_wait_st();
-        tc::fence_before();
-        tc::mbar_arrive(&S.u_full);
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          compute_u(S, tbase + (static_cast<uint32_t>(q4 * 32) << 16), row, rows[row].z >= 0, 32 * q + 16,
+                    32 * q + 32, f.de);
+          tc::tmem_wait_st();
+          tc::fence_before();
+          tc::mbar_arrive(&S.u_q[q]);
+        }
       }
     }
   } else {
