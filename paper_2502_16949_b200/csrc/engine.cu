@@ -355,7 +355,10 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
     if (!ev) return;
     cudaEvent_t e;
     SKG_CUDA(cudaEventCreate(&e));
-    SKG_CUDA(cudaEventRecord(e, s));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SKG_CUDA(cudaStreamIsCapturing(s, &cs));
+    // under capture: an event record node of the graph
+    SKG_CUDA(cudaEventRecordWithFlags(e, s, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
     ev->push_back(e);
   };
   mark();
@@ -2405,7 +2408,34 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const sk
     set_slot_seed(ctx, ctx->cur, epoch_seed(tc->seed, epoch));
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));
     std::vector<cudaEvent_t> ev;
-    enqueue_epoch(ctx, es, &ev);  // eager, no overlap: every launch is bracketed
+    // The plan, then every batch, each phase bracketed by event record nodes, in
+    // one captured graph: the phase times are the kernels' own, without the host
+    // launch gaps an eagerly enqueued epoch leaves between them (no overlap).
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t gx = nullptr;
+    SKG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_epoch(ctx, es, &ev);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      for (auto x : ev) cudaEventDestroy(x);
+      throw;
+    }
+    SKG_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    struct Cleanup {  // graph, its instance and the events, on every exit
+      cudaGraph_t& g;
+      cudaGraphExec_t& gx;
+      std::vector<cudaEvent_t>& ev;
+      ~Cleanup() {
+        if (gx) cudaGraphExecDestroy(gx);
+        if (g) cudaGraphDestroy(g);
+        for (auto x : ev) cudaEventDestroy(x);
+      }
+    } cleanup{g, gx, ev};
+    apply_l2_policy(ctx, g);
+    SKG_CUDA(cudaGraphInstantiate(&gx, g, 0));
+    SKG_CUDA(cudaGraphLaunch(gx, ctx->stream));
     ctx->last_slot = ctx->cur;
     ctx->slots[0].key.clear();
     ctx->slots[1].key.clear();
@@ -2430,7 +2460,6 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const sk
     rep->t_forward_s = f * 1e-3;
     rep->t_backward_s = b * 1e-3;
     rep->t_step_s = 0.0;
-    for (auto e : ev) cudaEventDestroy(e);
   });
 }
 
