@@ -391,6 +391,7 @@ def main():
 
     # ---- roofline of the dominant kernel (profiled epoch, per-launch events)
     rep, fwd_ms, bwd_ms, plan_ms = eng.profile_epoch(mcfg, tc, 200, LR)
+    shuffle_ms = eng.profile_shuffle_ms()
     fwd_b, bwd_b = algorithmic_bytes(cfg, eng, nb, world)
     peak, peak_kind = peaks()
     # Random-row gather peak over a table of this config's size (L2-resident for C1-C4): the
@@ -442,13 +443,13 @@ def main():
                           "unit": "TFLOP/s", "frac": tensor["achieved"] / tensor["peak"], "traffic": traffic,
                           "peak_source": tensor["peak_source"], "hbm_gbs": ach, "hbm_frac": ach / peak,
                           "forward_gbs": fwd_gbs, "backward_gbs": bwd_gbs, "fwd_ms_per_batch": fwd_ms,
-                          "bwd_ms_per_batch": bwd_ms, "plan_ms_per_epoch": plan_ms,
+                          "bwd_ms_per_batch": bwd_ms, "plan_ms_per_epoch": plan_ms, "shuffle_ms_per_epoch": shuffle_ms,
                           "note": "algorithmic fp32 FLOPs of the three projections; 3xTF32 issues 3 tf32 MMAs each"}
                          if tensor else
                          {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                           "frac": ach / peak, "traffic": traffic, "peak_source": peak_kind,
                           "forward_gbs": fwd_gbs, "backward_gbs": bwd_gbs, "fwd_ms_per_batch": fwd_ms,
-                          "bwd_ms_per_batch": bwd_ms, "plan_ms_per_epoch": plan_ms,
+                          "bwd_ms_per_batch": bwd_ms, "plan_ms_per_epoch": plan_ms, "shuffle_ms_per_epoch": shuffle_ms,
                           "gather_peak_gbs": gather_peak, "gather_frac": ach / gather_peak,
                           "gather_peak_source": f"skg_measure_gather: random {row_floats * 4}-byte rows of a "
                                                 f"{table_bytes / 2**20:.1f} MiB table (L2-resident below ~100 MiB)",

@@ -231,12 +231,15 @@ skg_status skg_train_epoch(skg_ctx* ctx, const skg_model_config* cfg, const skg_
  * optional entity renorm. reports has room for tc->epochs entries. */
 skg_status skg_fit(skg_ctx* ctx, const skg_model_config* cfg, const skg_train_config* tc,
                    skg_epoch_report* reports);
-/* Per-phase device timing of one epoch without the graph: kernel events
- * bracket every forward / backward launch (measurement hook for bench.py). */
+/* Per-phase device timing of one epoch, phases in sequence (no overlap): the
+ * epoch is captured into a graph whose event record nodes bracket the shuffle,
+ * the incidence plan and every forward / backward (measurement hook for
+ * bench.py). plan_ms excludes the shuffle; skg_profile_shuffle_ms reports it. */
 skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg,
                              const skg_train_config* tc, int64_t epoch, float lr,
                              skg_epoch_report* report, double* fwd_ms_per_batch,
                              double* bwd_ms_per_batch, double* plan_ms);
+skg_status skg_profile_shuffle_ms(skg_ctx* ctx, double* shuffle_ms);
 /* Phase buckets of the epoch report, default on. Off: t_forward_s = 0 and
  * t_backward_s = the whole epoch's device time (no event nodes in the graph). */
 skg_status skg_set_phase_timers(skg_ctx* ctx, int32_t enable);

@@ -349,6 +349,9 @@ void enqueue_shard_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStr
   shard_barrier(ctx, s);  // every rank has read the shard losses before any rank clears them
 }
 
+void gen_perm(skg_ctx* ctx, const EpochShape& es, const uint64_t* seed, int32_t* dst, cudaStream_t s);
+void build_plan_from_order(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t s);
+
 void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>* ev) {
   cudaStream_t s = ctx->stream;
   std::function<void()> mark = [&]() {
@@ -362,7 +365,9 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
     ev->push_back(e);
   };
   mark();
-  enqueue_plan(ctx, es, ctx->cur, s);
+  gen_perm(ctx, es, ctx->seed_eff.p + ctx->cur, ctx->slots[ctx->cur].order.p, s);  // the shuffle ...
+  mark();
+  build_plan_from_order(ctx, es, ctx->cur, s);  // ... and the incidence plan, timed apart
   mark();
   enqueue_batches(ctx, es, ctx->cur, s, ev ? &mark : nullptr);
 }
@@ -1905,6 +1910,12 @@ skg_status skg_set_phase_timers(skg_ctx* ctx, int32_t enable) {
   return guard(ctx, [&] { ctx->phase_timers = enable != 0; });
 }
 
+skg_status skg_profile_shuffle_ms(skg_ctx* ctx, double* shuffle_ms) {
+  return guard(ctx, [&] {
+    if (shuffle_ms) *shuffle_ms = ctx->last_shuffle_ms;
+  });
+}
+
 skg_status skg_upload_bytes(skg_ctx* ctx, int64_t* bytes) {
   return guard(ctx, [&] {
     if (bytes) *bytes = ctx->upload_bytes;
@@ -2447,11 +2458,12 @@ skg_status skg_profile_epoch(skg_ctx* ctx, const skg_model_config* cfg, const sk
       SKG_CUDA(cudaEventElapsedTime(&ms, ev[a], ev[b]));
       return static_cast<double>(ms);
     };
-    *plan_ms = el(0, 1);
+    ctx->last_shuffle_ms = el(0, 1);  // the epoch's permutation (two epochs ahead in the graphs)
+    *plan_ms = el(1, 2);              // the transposed-incidence plan of the epoch
     double f = 0, b = 0;
-    const size_t per = (ev.size() - 2) / es.nb;  // marks per batch
+    const size_t per = (ev.size() - 3) / es.nb;  // marks per batch
     for (int64_t k = 0; k < es.nb; ++k) {
-      const size_t s0 = 1 + k * per;
+      const size_t s0 = 2 + k * per;
       f += el(s0, s0 + 1);
       b += el(s0 + 1, s0 + per);
     }

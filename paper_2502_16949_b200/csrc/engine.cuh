@@ -161,6 +161,7 @@ struct skg_ctx {
   skg::DevBuf<uint32_t> spec_flags; // first bad entity / relation / negative index, changed
   int64_t spec_hits = 0, spec_misses = 0;
   int64_t upload_bytes = 0;             // bytes DMA'd by deferred uploads (skg_upload_bytes)
+  double last_shuffle_ms = 0.0;         // shuffle part of the last skg_profile_epoch
   skg::HostNarrow* narrow = nullptr;    // host threads narrowing deferred int64 uploads to int32
   int32_t* h_stage32 = nullptr;         // pinned: narrowed ids, wave-major
   int64_t h_stage32_cap = 0;

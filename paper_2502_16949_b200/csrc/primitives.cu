@@ -364,9 +364,16 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* 
 }
 
 void SortPlan::reserve(int64_t n) {
-  // segmented sorts pad the last segment with empty blocks: at most 2x blocks
-  const int64_t bi = static_cast<int64_t>(kSortWarps) * 32 * sort_chunks(n);
-  const int64_t nblk = 2 * ((n + bi - 1) / bi);
+  // segmented sorts pad the last segment with empty blocks: at most 2x blocks.
+  // The block count is not monotone in n (a longer sort uses longer chunks), so
+  // size for every n' <= n: the largest n' of each chunk length up to n's.
+  int64_t nblk = 0;
+  const int top = sort_chunks(n);
+  for (int ch = 1; ch <= top; ch <<= 1) {
+    const int64_t bi = static_cast<int64_t>(kSortWarps) * 32 * ch;
+    const int64_t m = ch == top ? n : std::min<int64_t>(n, (2 * 148 + 1) * bi - 1);
+    nblk = std::max<int64_t>(nblk, 2 * ((m + bi - 1) / bi));
+  }
   const int64_t need = nblk * (1 << kMaxBits);
   if (need > counts_cap) {
     if (counts) cudaFree(counts);

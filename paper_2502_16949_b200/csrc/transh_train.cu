@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
   const bool tr = g_thtrace_on == f.batch + 1;
   if (tid == 0) th_stamp(tr, 0);
   const int d = FULL ? kD : f.de, d4 = d >> 2;  // row width (<= kD); staged rows are zero-padded to kD columns
-  if (d < kD && warp < kCompute) {  // the copies never write the padding: clear it once
+  if constexpr (!FULL) if (d < kD && warp < kCompute) {  // the copies never write the padding: clear it once
     for (int i = tid; i < kStages * 2 * kRows * (kD - d) / 4; i += kCompute * 32) {
       const int c4 = d4 + i % (kD / 4 - d4), rr = i / (kD / 4 - d4);  // rr over stages x {H, T} x rows
       const int st = rr / (2 * kRows), ht = (rr / kRows) & 1, row = rr % kRows;
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
   }
   __syncthreads();
   if (tid == 0) th_stamp(tr, 1);
-  const uint32_t ntile = S.ntile, t0 = S.t0, T = S.T;
+  const uint32_t ntile = S.ntile, t0 = S.t0;
   uint32_t pend = 0;
 
   if (warp >= kLoaderWarp) {

@@ -107,6 +107,7 @@ def load_library():
         "skg_train_epoch": [vp, vp, vp, i64, f32, vp],
         "skg_fit": [vp, vp, vp, vp],
         "skg_profile_epoch": [vp, vp, vp, i64, f32, vp, vp, vp, vp],
+        "skg_profile_shuffle_ms": [vp, vp],
         "skg_nccl_unique_id": [vp],
         "skg_dp_init": [vp, vp, C.c_int, C.c_int],
         "skg_generate_synthetic": [i64, i64, i64, C.c_uint64, vp, vp, vp],
@@ -342,6 +343,12 @@ class Engine:
         self._check(self.L.skg_profile_epoch(self.h, C.byref(cfg), C.byref(tc), epoch, lr, C.byref(rep),
                                              C.byref(f), C.byref(b), C.byref(p)))
         return rep, f.value, b.value, p.value
+
+    def profile_shuffle_ms(self) -> float:
+        """Shuffle (epoch permutation) time of the last profile_epoch, ms."""
+        v = C.c_double()
+        self._check(self.L.skg_profile_shuffle_ms(self.h, C.byref(v)))
+        return v.value
 
     def synchronize(self):
         self._check(self.L.skg_synchronize(self.h))
