@@ -51,6 +51,16 @@ __device__ __forceinline__ void stamp_now(unsigned long long* p) {
   *p = t;
 }
 
+// Last-block ticket: a gpu-scope acq_rel add publishes this block's partial
+// (written before the add, or by its threads before a barrier) and, in the
+// block that draws the last ticket, makes every other block's partial visible
+// -- without the two full fences of __threadfence + atomicAdd.
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* counter) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.402823466e38f; }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

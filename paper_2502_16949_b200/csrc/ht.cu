@@ -85,12 +85,10 @@ __device__ void finalize_loss(const FwdArgs& a, float lsum, float* warp_loss) {
     float b = 0.f;
     for (int w = 0; w < nwarps; ++w) b = __fadd_rn(b, warp_loss[w]);
     a.block_partial[blockIdx.x] = b;
-    __threadfence();
-    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+    last = ticket_acq_rel(a.counter) == gridDim.x - 1;
   }
   __syncthreads();
   if (last && warp == 0) {
-    __threadfence();
     float acc = 0.f;
     for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, a.block_partial[b]);
 #pragma unroll
@@ -99,7 +97,7 @@ __device__ void finalize_loss(const FwdArgs& a, float lsum, float* warp_loss) {
       const float loss = __fdiv_rn(acc, static_cast<float>(a.B));
       a.batch_loss[a.batch] = loss;
       if (a.stamp_end) stamp_now(a.stamp_end);
-      const uint32_t pflags = atomicOr(&a.err[3], 0u);
+      const uint32_t pflags = *reinterpret_cast<volatile uint32_t*>(&a.err[3]);
       if (nonfinite(loss)) {
         a.err[1] = a.batch;
         atomicCAS(&a.err[0], 0u, static_cast<uint32_t>(kErrLossNonFinite));

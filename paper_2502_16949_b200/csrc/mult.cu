@@ -345,12 +345,10 @@ __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a)
     float b = 0.f;
     for (int w = 0; w < nwarps; ++w) b = __fadd_rn(b, warp_loss[w]);
     a.block_partial[blockIdx.x] = b;
-    __threadfence();
-    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+    last = ticket_acq_rel(a.counter) == gridDim.x - 1;
   }
   __syncthreads();
   if (last && warp == 0) {
-    __threadfence();
     float acc = 0.f;
     for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, a.block_partial[b]);
 #pragma unroll
@@ -359,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a)
       const float loss = __fdiv_rn(acc, a.loss_div > 0.f ? a.loss_div : static_cast<float>(a.B));
       a.batch_loss[a.batch] = loss;
       if (a.stamp_end) stamp_now(a.stamp_end);
-      const uint32_t pflags = atomicOr(&a.err[3], 0u);
+      const uint32_t pflags = *reinterpret_cast<volatile uint32_t*>(&a.err[3]);
       if (!(fabsf(loss) <= 3.402823466e38f)) {
         a.err[1] = a.batch;
         atomicCAS(&a.err[0], 0u, static_cast<uint32_t>(kErrLossNonFinite));

@@ -585,12 +585,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
     float lsum = 0.f;
     for (int q = 0; q < kCompute; ++q) lsum = __fadd_rn(lsum, S.wl[q]);
     f.block_partial[blockIdx.x] = lsum;
-    __threadfence();
-    S.last_cta = atomicAdd(f.counter, 1u) == gridDim.x - 1;
+    S.last_cta = ticket_acq_rel(f.counter) == gridDim.x - 1;
   }
   __syncthreads();
   if (S.last_cta && warp == 0) {
-    __threadfence();
     float acc = 0.f;
     for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, f.block_partial[b]);
 #pragma unroll
@@ -599,7 +597,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) transh_pipe_kernel(const TArg
       const float loss = __fdiv_rn(acc, f.loss_div > 0.f ? f.loss_div : static_cast<float>(f.B));
       f.batch_loss[f.batch] = loss;
       if (f.stamp_end) stamp_now(f.stamp_end);
-      const uint32_t pflags = atomicOr(&f.err[3], 0u);
+      const uint32_t pflags = *reinterpret_cast<volatile uint32_t*>(&f.err[3]);
       if (nonfinite(loss)) {
         f.err[1] = f.batch;
         atomicCAS(&f.err[0], 0u, static_cast<uint32_t>(kErrLossNonFinite));

@@ -458,12 +458,10 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
   __shared__ bool last;
   if (tid == 0) {
     f.block_partial[blockIdx.x] = lsum;
-    __threadfence();
-    last = atomicAdd(f.counter, 1u) == gridDim.x - 1;
+    last = ticket_acq_rel(f.counter) == gridDim.x - 1;
   }
   __syncthreads();
   if (last && warp == 0) {
-    __threadfence();
     float acc = 0.f;
     for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, f.block_partial[b]);
 #pragma unroll
@@ -472,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) transr_tc_kernel(const TcArgs a) 
       const float loss = __fdiv_rn(acc, static_cast<float>(f.B));
       f.batch_loss[f.batch] = loss;
       if (f.stamp_end) stamp_now(f.stamp_end);
-      const uint32_t pflags = atomicOr(&f.err[3], 0u);
+      const uint32_t pflags = *reinterpret_cast<volatile uint32_t*>(&f.err[3]);
       if (nonfinite(loss)) {
         f.err[1] = f.batch;
         atomicCAS(&f.err[0], 0u, static_cast<uint32_t>(kErrLossNonFinite));

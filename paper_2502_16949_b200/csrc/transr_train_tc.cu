@@ -320,6 +320,16 @@ __device__ __forceinline__ void chase_rows(const Args& a, uint32_t t, int lane, 
   if (lane == 0) *np_out = np;
 }
 
+// CTAs that take tiles: the fewest giving the same longest range as all G, so
+// the spare SMs stay free for the graph's side branches (a persistent CTA that
+// finds its SM held by a long plan-branch block would start late and hold up
+// the batch). Training kernel and apply agree on it, both from T.
+__device__ __forceinline__ uint32_t working_ctas(uint32_t T, uint32_t G) {
+  if (T == 0) return G;
+  const uint32_t per = (T + G - 1) / G;
+  return (T + per - 1) / per;
+}
+
 template <bool L2>
 __global__ void __launch_bounds__(kThreads, 1)
     transr_train_tc_kernel(const Args a) {
@@ -331,11 +341,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool tr = g_trace_on == f.batch + 1;  // trace one chosen minibatch
   if (f.stamp_start && blockIdx.x == 0 && tid == 0) stamp_now(f.stamp_start);  // the batch's first kernel (tiles planned)
   auto trace = [&](uint32_t it, int ev) { trace_ev(tr, it, ev); };
-  if (tr && tid == 0 && blockIdx.x < kTrCtas) {  // CTA start (globaltimer, comparable across SMs) in the last slot
-    unsigned long long g;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-    g_trace[(blockIdx.x * kTrTiles + kTrTiles - 1) * kTrEvents + kTrEvents - 1] = g;
-  }
+  // globaltimer stamps (comparable across SMs) in the last tile slot: 15 CTA start,
+  // 14 first tile's rows seen by the producers, 13 loops done, 12 loss written
+  auto gtrace = [&](int ev) {
+    if (tr && blockIdx.x < kTrCtas) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      g_trace[(blockIdx.x * kTrTiles + kTrTiles - 1) * kTrEvents + ev] = g;
+    }
+  };
+  if (tid == 0) gtrace(15);
 
   if (warp == 0) tc::tmem_alloc(&S.tmem_base, 512);
   if (f.de < kD)  // row tiles narrower than 128: the gather never writes columns >= d_e, keep them zero
@@ -376,9 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((tc::smem_u32(S.U) & 1023u) != 0) __trap();  // SWIZZLE_128B atoms need 1 KB alignment
 
   const uint32_t T = alive ? a.tile_total[0] : 0u;
-  const uint32_t G = gridDim.x;
-  const uint32_t t0 = static_cast<uint32_t>((static_cast<uint64_t>(T) * blockIdx.x) / G);
-  const uint32_t t1 = static_cast<uint32_t>((static_cast<uint64_t>(T) * (blockIdx.x + 1)) / G);
+  const uint32_t G = working_ctas(T, gridDim.x);
+  const uint32_t b = blockIdx.x < G ? blockIdx.x : G;  // CTAs past G take no tile
+  const uint32_t t0 = static_cast<uint32_t>((static_cast<uint64_t>(T) * b) / G);
+  const uint32_t t1 = blockIdx.x < G ? static_cast<uint32_t>((static_cast<uint64_t>(T) * (b + 1)) / G) : t0;
   const uint32_t ntile = t1 - t0;
 
   float lsum = 0.f;
@@ -526,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int buf = it & 1;
       tc::mbar_wait(&S.rows_full[buf], (it >> 1) & 1);
       if (p == 0) trace(it, 0);
+      if (p == 0 && it == 0) gtrace(14);
       const int4* rows = S.rows[buf];
       tc::mbar_wait(&S.g_full, it & 1);  // head rows in sU, tail rows in sDZ
       if (p == 0) trace(it, 1);
@@ -752,6 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- teardown, loss: one partial per CTA, the last CTA finalizes (tile order)
   tc::fence_before();
   __syncthreads();
+  if (tid == 0) gtrace(13);
   if (warp == 0) tc::tmem_dealloc(tbase, 512);
   if (warp < 4) {
     pend = __reduce_or_sync(kFull, pend);
@@ -763,12 +781,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (!alive) return;
   if (tid == 0) {
     f.block_partial[blockIdx.x] = lsum;
-    __threadfence();
-    S.last = atomicAdd(f.counter, 1u) == gridDim.x - 1;
+    S.last = ticket_acq_rel(f.counter) == gridDim.x - 1;
   }
   __syncthreads();
   if (S.last && warp == 0) {
-    __threadfence();
     float acc = 0.f;
     for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) acc = __fadd_rn(acc, f.block_partial[b]);
 #pragma unroll
@@ -777,7 +793,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float loss = __fdiv_rn(acc, f.loss_div > 0.f ? f.loss_div : static_cast<float>(f.B));
       f.batch_loss[f.batch] = loss;
       if (f.stamp_end) stamp_now(f.stamp_end);
-      const uint32_t pflags = atomicOr(&f.err[3], 0u);
+      gtrace(12);
+      const uint32_t pflags = *reinterpret_cast<volatile uint32_t*>(&f.err[3]);
       if (nonfinite(loss)) {
         f.err[1] = f.batch;
         atomicCAS(&f.err[0], 0u, static_cast<uint32_t>(kErrLossNonFinite));
@@ -838,6 +855,7 @@ __global__ void transr_train_apply_kernel(const uint32_t* __restrict__ tile_tota
   const uint32_t k = blockIdx.x;
   if (k >= tile_total[1]) return;
   const uint32_t T = tile_total[0];
+  G = static_cast<int>(working_ctas(T, static_cast<uint32_t>(G)));
   const uint32_t lo = seg_tiles[k], hi = seg_tiles[k + 1];
   if (hi <= lo) return;
   const int64_t r = static_cast<int64_t>(seg_col[tile_seg[lo]]) - N;
