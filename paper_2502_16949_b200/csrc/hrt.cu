@@ -134,15 +134,21 @@ __device__ __forceinline__ float warp_reduce16(const float* rows, int S, int d, 
   const int r = lane >> 1, hb = lane & 1;
   const float* v = rows + r * S + 2 * hb;
   float sa = 0.f, sb = 0.f;
-  bool nf = false;
 #pragma unroll 8
   for (int j = 0; j < d; j += 4) {
     const float2 x = *reinterpret_cast<const float2*>(v + j);
-    nf |= !(fabsf(x.x) <= 3.402823466e38f) | !(fabsf(x.y) <= 3.402823466e38f);
     sa = __fadd_rn(sa, term_of(KIND, x.x));
     sb = __fadd_rn(sb, term_of(KIND, x.y));
   }
   const float pair = __fadd_rn(sa, sb);                // s0 + s1 (h = 0) or s2 + s3 (h = 1)
+  // Terms are >= 0 or NaN, so a finite sum proves every element finite; only a
+  // non-finite sum (a non-finite element, or overflow) rescans its elements.
+  bool nf = false;
+  if (!(fabsf(pair) <= 3.402823466e38f))
+    for (int j = 0; j < d; j += 4) {
+      const float2 x = *reinterpret_cast<const float2*>(v + j);
+      nf |= !(fabsf(x.x) <= 3.402823466e38f) | !(fabsf(x.y) <= 3.402823466e38f);
+    }
   const float tot = __fadd_rn(pair, __shfl_down_sync(kFull, pair, 1));  // on h == 0 lanes
   const unsigned nfm = __ballot_sync(kFull, nf);
   bad = ((nfm >> (2 * (lane & 15))) & 3u) != 0u;
@@ -157,13 +163,11 @@ __device__ __forceinline__ float warp_reduce8(const float* rows, int S, int d, i
   const int r = lane >> 2, k = lane & 3;
   const float* v = rows + r * S + k;
   float sacc = 0.f;
-  bool nf = false;
 #pragma unroll 8
-  for (int j = 0; j < d; j += 4) {
-    const float x = v[j];
-    nf |= !(fabsf(x) <= 3.402823466e38f);
-    sacc = __fadd_rn(sacc, term_of(KIND, x));
-  }
+  for (int j = 0; j < d; j += 4) sacc = __fadd_rn(sacc, term_of(KIND, v[j]));
+  bool nf = false;  // a finite sum proves every element finite (see warp_reduce16)
+  if (!(fabsf(sacc) <= 3.402823466e38f))
+    for (int j = 0; j < d; j += 4) nf |= !(fabsf(v[j]) <= 3.402823466e38f);
   const float s1 = __shfl_down_sync(kFull, sacc, 1), s2 = __shfl_down_sync(kFull, sacc, 2),
               s3 = __shfl_down_sync(kFull, sacc, 3);
   const float tot = __fadd_rn(__fadd_rn(sacc, s1), __fadd_rn(s2, s3));  // on k == 0 lanes
@@ -423,6 +427,18 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
     }
     // ---- residual rows of active pairs (all rows in SCORE mode) to HBM
     const unsigned wmask = __ballot_sync(kFull, TRAIN ? (sc != 0.f) : (lane < 16 && valid)) & vmask;
+    if (TRAIN && VEC == 4 && d <= 128) {  // one 16-byte chunk per lane per row; row ids from the tile index
+      const int d4 = d >> 2;
+      const size_t base = static_cast<size_t>(tile) * TP;
+      for (unsigned m = wmask; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const size_t r2 = base + (j & (TP - 1)) + (j >= TP ? static_cast<size_t>(a.B) : 0u);
+        if (lane < d4)
+          reinterpret_cast<float4*>(a.res + r2 * d)[lane] = *reinterpret_cast<const float4*>(rows + j * S + 4 * lane);
+      }
+      __syncwarp();
+      continue;
+    }
     for (unsigned m = wmask; m; m &= m - 1) {
       const int j = __ffs(m) - 1;
       const int r2 = __shfl_sync(kFull, row2, j);  // uniform: every lane executes

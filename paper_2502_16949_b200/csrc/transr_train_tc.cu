@@ -424,7 +424,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row2 = S.rows[buf][m].z;
       // pass 1: v = V + r, reference-order squared_sum / abs_sum (norms.hpp:19-55)
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      bool bad = false;
 #pragma unroll 1
       for (int c = 0; c < kD; c += 32) {
         uint32_t r0[16], r1[16];
@@ -434,18 +433,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int q = 0; q < 32; q += 4) {
           const uint32_t* rr = q < 16 ? r0 + q : r1 + (q - 16);
-          const float x0 = __fadd_rn(__uint_as_float(rr[0]), relr[c + q]);
-          const float x1 = __fadd_rn(__uint_as_float(rr[1]), relr[c + q + 1]);
-          const float x2 = __fadd_rn(__uint_as_float(rr[2]), relr[c + q + 2]);
-          const float x3 = __fadd_rn(__uint_as_float(rr[3]), relr[c + q + 3]);
-          bad |= nonfinite(x0) | nonfinite(x1) | nonfinite(x2) | nonfinite(x3);
-          s0 = __fadd_rn(s0, norm_term<L2>(x0));
-          s1 = __fadd_rn(s1, norm_term<L2>(x1));
-          s2 = __fadd_rn(s2, norm_term<L2>(x2));
-          s3 = __fadd_rn(s3, norm_term<L2>(x3));
+          s0 = __fadd_rn(s0, norm_term<L2>(__fadd_rn(__uint_as_float(rr[0]), relr[c + q])));
+          s1 = __fadd_rn(s1, norm_term<L2>(__fadd_rn(__uint_as_float(rr[1]), relr[c + q + 1])));
+          s2 = __fadd_rn(s2, norm_term<L2>(__fadd_rn(__uint_as_float(rr[2]), relr[c + q + 2])));
+          s3 = __fadd_rn(s3, norm_term<L2>(__fadd_rn(__uint_as_float(rr[3]), relr[c + q + 3])));
         }
       }
       const float ssum = __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
+      // terms are >= 0 or NaN: a finite sum proves every element of v finite;
+      // otherwise the warp rescans V (tcgen05.ld is warp-collective)
+      bool bad = false;
+      if (__any_sync(kFull, nonfinite(ssum))) {
+#pragma unroll 1
+        for (int c = 0; c < kD; c += 16) {
+          uint32_t r0[16];
+          tc::tmem_ld16_nowait(tbase + lane_addr + kColV + c, r0);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) bad |= nonfinite(__fadd_rn(__uint_as_float(r0[q]), relr[c + q]));
+        }
+      }
       S.rs[m] = L2 ? __fsqrt_rn(ssum) : ssum;
       if (bad && row2 >= 0) pend |= kPendEntity;
       tc::named_sync(1, 128);
