@@ -88,9 +88,11 @@ __device__ float ref_reduce(const float* v, int n, bool& bad) {
     s = 0.f;
     for (int j = 0; j < n; ++j) {
       const float x = v[j];
-      nf |= !(fabsf(x) <= 3.402823466e38f);
       s = __fadd_rn(s, KIND == kTorusE_L2 ? __fmul_rn(x, x) : fabsf(x));
     }
+    // terms are >= 0 or NaN: a finite sum proves every element finite
+    if (!(fabsf(s) <= 3.402823466e38f))
+      for (int j = 0; j < n; ++j) nf |= !(fabsf(v[j]) <= 3.402823466e38f);
   } else if (n < 8) {
     s = 0.f;
     for (int j = 0; j < n; ++j) {
@@ -427,14 +429,15 @@ __global__ void __launch_bounds__(kThreads, MINB) hrt_forward_kernel(const FwdAr
     }
     // ---- residual rows of active pairs (all rows in SCORE mode) to HBM
     const unsigned wmask = __ballot_sync(kFull, TRAIN ? (sc != 0.f) : (lane < 16 && valid)) & vmask;
-    if (TRAIN && VEC == 4 && d <= 128) {  // one 16-byte chunk per lane per row; row ids from the tile index
-      const int d4 = d >> 2;
-      const size_t base = static_cast<size_t>(tile) * TP;
-      for (unsigned m = wmask; m; m &= m - 1) {
-        const int j = __ffs(m) - 1;
-        const size_t r2 = base + (j & (TP - 1)) + (j >= TP ? static_cast<size_t>(a.B) : 0u);
-        if (lane < d4)
-          reinterpret_cast<float4*>(a.res + r2 * d)[lane] = *reinterpret_cast<const float4*>(rows + j * S + 4 * lane);
+    if (TRAIN && VEC == 4 && d <= 128) {  // one 16-byte chunk per lane per row; row k of the tile is
+      const int d4 = d >> 2;              // pair tile * TP + k (positive) or B + that (negative)
+      float4* pos = reinterpret_cast<float4*>(a.res) + static_cast<size_t>(tile) * TP * d4 + lane;
+      float4* neg = pos + static_cast<size_t>(a.B) * d4;
+      if (lane < d4) {
+#pragma unroll
+        for (int q = 0; q < RW; ++q)
+          if ((wmask >> q) & 1u)
+            (q < TP ? pos : neg)[(q & (TP - 1)) * d4] = *reinterpret_cast<const float4*>(rows + q * S + 4 * lane);
       }
       __syncwarp();
       continue;
