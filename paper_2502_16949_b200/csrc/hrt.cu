@@ -832,12 +832,14 @@ void launch_fwd_k(bool train, const FwdArgs& a, int num_sms, cudaStream_t s) {
   }
 }
 
-// Grid of a grid-stride backward kernel. The warp-per-segment kernel keeps 8
-// blocks per SM: about two waves, and the second wave's blocks take over SMs
-// as first-wave blocks finish, which balances the uneven segments better than
-// a resident grid (measured: C1 23.0 vs 26.7 us, C5 313 vs 516 us). The staged
-// ht entity pass (mostly one-entry segments) runs every block at once
-// (C2 17.9 -> 16.5 us).
+// Grid of a grid-stride backward kernel. The warp-per-segment kernel launches
+// 64 warps per SM in 128-thread blocks: about two waves, and the second wave's
+// blocks take over SMs as first-wave blocks finish, which balances the uneven
+// segments better than a resident grid (measured: C1 23.0 vs 26.7 us, C5 313
+// vs 516 us); 4-warp blocks hand SMs over sooner than 8-warp ones (epoch C3
+// 0.754 -> 0.732 ms, C1 0.653 -> 0.647, M1-M3 -0.7 %; SKG_BWD_TPB=256 restores).
+// The staged ht entity pass (mostly one-entry segments) runs every block at
+// once (C2 17.9 -> 16.5 us).
 template <class K>
 int resident_grid(K kernel, int num_sms) {
   int per_sm = 0;
@@ -845,9 +847,23 @@ int resident_grid(K kernel, int num_sms) {
   return num_sms * (per_sm > 0 ? per_sm : 1);
 }
 
+inline int bwd_tpb() {
+  static const int v = [] {
+    const char* e = std::getenv("SKG_BWD_TPB");
+    const int t = e ? std::atoi(e) : 128;
+    return (t == 64 || t == 128 || t == 256) ? t : kThreads;
+  }();
+  return v;
+}
+
 template <class K>
 void run_bwd(K kernel, const BwdArgs& a, int num_sms, cudaStream_t s, bool resident = false) {
-  kernel<<<resident ? resident_grid(kernel, num_sms) : num_sms * 8, kThreads, 0, s>>>(a);
+  if (resident) {
+    kernel<<<resident_grid(kernel, num_sms), kThreads, 0, s>>>(a);
+    return;
+  }
+  const int tpb = bwd_tpb();
+  kernel<<<num_sms * 8 * (kThreads / tpb), tpb, 0, s>>>(a);
 }
 
 template <int KIND>
