@@ -1049,10 +1049,22 @@ void complete_epoch(skg_ctx* ctx, const StagedEpoch& sg, skg_epoch_report* rep) 
 void train_epoch_impl(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_config& tc,
                       int64_t epoch, float lr, skg_epoch_report* rep,
                       const std::function<void()>* after_launch = nullptr) {
+  static const bool dbg = std::getenv("SKG_EPOCH_DEBUG") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   const StagedEpoch sg = stage_epoch(ctx, cfg, tc, epoch, lr);
+  const auto t1 = clk::now();
   fire_epoch(ctx, sg);
+  const auto t2 = clk::now();
   if (after_launch) (*after_launch)();
+  const auto t3 = clk::now();
   complete_epoch(ctx, sg, rep);
+  if (dbg) {
+    const auto t4 = clk::now();
+    auto us = [](clk::duration d) { return std::chrono::duration<double, std::micro>(d).count(); };
+    std::fprintf(stderr, "epoch: stage %.1f us, launch %.1f us, after-launch %.1f us, complete %.1f us (graph %.1f us)\n",
+                 us(t1 - t0), us(t2 - t1), us(t3 - t2), us(t4 - t3), ctx->last_epoch_ms * 1e3);
+  }
 }
 
 void negative_sample_impl(skg_ctx* ctx, uint64_t seed, bool avoid) {  // training.cpp:51-71
