@@ -9,6 +9,7 @@ exception kind (ShapeError, ConfigError, TrainingError, ...).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 
 import numpy as np
@@ -139,8 +140,28 @@ def load_library():
     return L
 
 
+_PTRS = {}  # id(array) -> (weakref, c_void_p): per-step re-uploads pass the same arrays
+
+
+class _Arg:
+    """A pointer argument that keeps its array alive for the duration of the call."""
+    __slots__ = ("_as_parameter_", "a")
+
+    def __init__(self, ptr, a):
+        self._as_parameter_ = ptr
+        self.a = a
+
+
 def _p(a):
-    return None if a is None else a.ctypes.data_as(C.c_void_p)
+    if a is None:
+        return None
+    hit = _PTRS.get(id(a))
+    if hit is None or hit[0]() is not a:
+        if len(_PTRS) > 64:
+            _PTRS.clear()
+        hit = (weakref.ref(a), C.c_void_p(a.ctypes.data))
+        _PTRS[id(a)] = hit
+    return _Arg(hit[1], a)
 
 
 def _i64(a):
