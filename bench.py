@@ -141,6 +141,20 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "NVML, 1 ms polling"}
 
 
+def pcie_link(device):
+    """PCIe link generation / width (current and max) from NVML, to diagnose slow host copies."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        return {"gen": pynvml.nvmlDeviceGetCurrPcieLinkGeneration(h),
+                "width": pynvml.nvmlDeviceGetCurrPcieLinkWidth(h),
+                "max_gen": pynvml.nvmlDeviceGetMaxPcieLinkGeneration(h),
+                "max_width": pynvml.nvmlDeviceGetMaxPcieLinkWidth(h)}
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)[:80]}
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -362,6 +376,8 @@ def main():
     e2e_steps = max(30, min(args.steps, 100))
     e2e_epoch0 = args.warmup + args.steps + 1  # the training run continues: consecutive epochs
     host_set_s = call_s = graph_s = 0.0
+    link = pcie_link(local)
+    step_ms = []
     t0 = time.perf_counter()
     for k in range(e2e_steps):
         ta = time.perf_counter()
@@ -372,6 +388,7 @@ def main():
         tcall = time.perf_counter()
         host_set_s += tb - ta
         call_s += tcall - tb
+        step_ms.append((tcall - ta) * 1e3)
         graph_s += rep.t_forward_s + rep.t_backward_s + rep.t_step_s
     e2e_s = allreduce_max(time.perf_counter() - t0, world)
     e2e = M * e2e_steps / e2e_s
@@ -383,9 +400,11 @@ def main():
                  "graph_device_ms": graph_s / e2e_steps * 1e3,
                  "note": "train_epoch_call = graph launch + the overlapped H2D copy and on-device check of the "
                          "re-uploaded ids + the epoch; graph_device = the epoch graph's own device time",
-                 "spec_hits": hits1 - hits0, "spec_misses": miss1 - miss0, "steps": e2e_steps}
+                 "spec_hits": hits1 - hits0, "spec_misses": miss1 - miss0, "steps": e2e_steps,
+                 "step_ms_median": statistics.median(step_ms), "step_ms_max": max(step_ms),
+                 "pcie_link": link}
     # bytes actually copied per step: the deferred re-upload narrows the five int64 id arrays to
-    # int32 on host threads before the DMA (int64 arrays of the API; SKG_SPEC_I64=1: int64 DMA)
+    # uint16 / int32 on host threads before the DMA (int64 arrays of the API; SKG_SPEC_I64=1: int64 DMA)
     h2d = (bytes1 - bytes0) // e2e_steps if bytes1 > bytes0 else 5 * M * 8
     d2h = nb * 4 + 16 + 8 * 2
 
@@ -435,9 +454,9 @@ def main():
             "wall_s": round(wall, 4), "final_loss": losses[-1], "parallel_layout": layout,
             "e2e": {"value": e2e, "unit": "triplets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "skg_set_triples + skg_set_negatives (pinned int64) + skg_train_epoch; the identical-shape "
-                            "pinned re-upload is range-checked and narrowed to int32 by host threads, copied by "
-                            "DMA in waves and verified on device while the epoch trains (rolled back and "
-                            "retrained if it differs)",
+                            "pinned re-upload is range-checked and narrowed by host threads (uint16 when every "
+                            "table has <= 65536 rows, else int32), copied by DMA in waves and verified on device "
+                            "while the epoch trains (rolled back and retrained if it differs)",
                     "breakdown": e2e_split},
             "roofline": ({"bound": "tensor", "kernel": dom, "achieved": tensor["achieved"], "peak": tensor["peak"],
                           "unit": "TFLOP/s", "frac": tensor["achieved"] / tensor["peak"], "traffic": traffic,

@@ -143,8 +143,8 @@ skg_status skg_set_deferred_uploads(skg_ctx* ctx, int32_t enable); /* default 0 
 /* Deferred re-uploads so far: kept (identical data) / rolled back + retrained. */
 skg_status skg_upload_stats(skg_ctx* ctx, int64_t* hits, int64_t* misses);
 /* Bytes copied host -> device by deferred re-uploads so far: the five id arrays
- * narrowed to int32 by host threads (range-checked on the way), or int64 with
- * SKG_SPEC_I64=1. */
+ * narrowed by host threads (range-checked on the way) to uint16 when every
+ * table has at most 65536 rows, else to int32; int64 with SKG_SPEC_I64=1. */
 skg_status skg_upload_bytes(skg_ctx* ctx, int64_t* bytes);
 skg_status skg_set_triples(skg_ctx* ctx, int64_t m, const int64_t* heads, const int64_t* relations,
                            const int64_t* tails, int64_t num_entities, int64_t num_relations);

@@ -773,11 +773,31 @@ std::string plan_key(skg_ctx* ctx, const EpochShape& es, const skg_train_config&
                  ctx->slots[0].tr_on);
 }
 
+// The epoch's results (batch losses, error words, the speculative upload
+// check's flags) written by one kernel into the pinned host buffers, which
+// are device-addressable under UVA: one node after the epoch instead of up to
+// three D2H copies, each a separate DMA round trip on the critical path.
+__global__ void publish_kernel(const float* __restrict__ loss, int64_t nb, float* h_loss,
+                               const uint32_t* __restrict__ err, uint32_t* h_err,
+                               const uint32_t* __restrict__ spec, uint32_t* h_spec) {
+  const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (int64_t i = i0; i < nb; i += static_cast<int64_t>(gridDim.x) * blockDim.x) h_loss[i] = loss[i];
+  if (i0 < 4) {
+    h_err[i0] = err[i0];
+    if (spec) h_spec[i0] = spec[i0];
+  }
+}
+
 void finish_epoch(skg_ctx* ctx, const EpochShape& es, int64_t epoch, skg_epoch_report* rep) {
-  SKG_CUDA(cudaMemcpyAsync(ctx->h_loss, ctx->batch_loss.p, sizeof(float) * es.nb, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-  SKG_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->err_words.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost,
-                           ctx->stream));
+  {
+    const uint32_t* spec = ctx->pub_spec;
+    ctx->pub_spec = nullptr;
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((es.nb + 255) / 256, 64)));
+    publish_kernel<<<grid, 256, 0, ctx->stream>>>(ctx->batch_loss.p, es.nb, ctx->h_loss, ctx->err_words.p,
+                                                  ctx->h_err, spec, ctx->h_spec);
+    count_launch();
+    SKG_LAUNCH_CHECK();
+  }
   if (ctx->phase_timers)
     SKG_CUDA(cudaMemcpyAsync(ctx->h_stamps, ctx->stamps.p, sizeof(unsigned long long) * 2 * es.nb,
                              cudaMemcpyDeviceToHost, ctx->stream));
@@ -798,6 +818,37 @@ void set_epoch_params(skg_ctx* ctx, const skg_train_config& tc, float lr) {
   ctx->h_lr[0] = lr;
   ctx->h_lr[1] = tc.margin;
   SKG_CUDA(cudaMemcpyAsync(ctx->lr_dev.p, ctx->h_lr, sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+}
+
+// First node of every epoch graph: this epoch's lr and the seed of the
+// permutation the graph shuffles (arguments replaced in the instantiated graph
+// before each launch, see set_graph_params).
+struct EpochParams {
+  float* lr_dev;
+  uint64_t* seed_dst;
+  float lr;
+  uint64_t seed;
+};
+__global__ void epoch_params_kernel(EpochParams p) {
+  *p.lr_dev = p.lr;
+  *p.seed_dst = p.seed;
+}
+
+EpochParams epoch_params_of(skg_ctx* ctx, int cur) {
+  return EpochParams{ctx->lr_dev.p, ctx->seed_eff.p + 2 + cur, ctx->h_lr[0], ctx->h_seed[2 + cur]};
+}
+
+void set_graph_params(skg_ctx* ctx, int cur) {
+  EpochParams ep = epoch_params_of(ctx, cur);
+  void* args[1] = {&ep};
+  cudaKernelNodeParams kp{};
+  kp.func = reinterpret_cast<void*>(epoch_params_kernel);
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(1);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  SKG_CUDA(cudaGraphExecKernelNodeSetParams(ctx->graphs[cur], ctx->param_node[cur], &kp));
 }
 
 void set_slot_seed(skg_ctx* ctx, int slot, uint64_t seed_eff) {
@@ -853,6 +904,9 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
   cudaGraph_t g = nullptr;
   SKG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   try {
+    epoch_params_kernel<<<1, 1, 0, ctx->stream>>>(epoch_params_of(ctx, cur));
+    count_launch();
+    SKG_LAUNCH_CHECK();
     SKG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
     SKG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
     SKG_CUDA(cudaStreamWaitEvent(ctx->side2, ctx->fork_ev, 0));
@@ -881,8 +935,30 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
   }
   if (ctx->graphs[cur]) cudaGraphExecDestroy(ctx->graphs[cur]);
   ctx->graphs[cur] = nullptr;
-  SKG_CUDA(cudaGraphInstantiate(&ctx->graphs[cur], g, 0));
-  SKG_CUDA(cudaGraphDestroy(g));
+  if (ctx->graph_src[cur]) cudaGraphDestroy(ctx->graph_src[cur]);
+  ctx->graph_src[cur] = nullptr;
+  ctx->param_node[cur] = nullptr;
+  try {
+    size_t n = 0;
+    SKG_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    SKG_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType t;
+      SKG_CUDA(cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp{};
+      SKG_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+      if (kp.func == reinterpret_cast<void*>(epoch_params_kernel)) ctx->param_node[cur] = nd;
+    }
+    if (!ctx->param_node[cur]) throw CudaError("epoch graph: parameter node not found");
+    SKG_CUDA(cudaGraphInstantiate(&ctx->graphs[cur], g, 0));
+  } catch (...) {
+    cudaGraphDestroy(g);
+    ctx->param_node[cur] = nullptr;
+    throw;
+  }
+  ctx->graph_src[cur] = g;  // owns param_node[cur]
   ctx->graph_launches_k[cur] = kernel_launches() - before;
 }
 
@@ -892,6 +968,9 @@ void skg::drop_graphs(skg_ctx* ctx) {
   for (int k = 0; k < 2; ++k) {
     if (ctx->graphs[k]) cudaGraphExecDestroy(ctx->graphs[k]);
     ctx->graphs[k] = nullptr;
+    if (ctx->graph_src[k]) cudaGraphDestroy(ctx->graph_src[k]);
+    ctx->graph_src[k] = nullptr;
+    ctx->param_node[k] = nullptr;
     ctx->graph_keys[k].clear();
     ctx->slots[k].key.clear();
     ctx->perm_key[k].clear();
@@ -961,7 +1040,10 @@ StagedEpoch stage_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_tra
   EpochShape& es = sg.es;
   sg.epoch = epoch;
   prepare_epoch(ctx, cfg, tc, es);
-  set_epoch_params(ctx, tc, lr);
+  // lr (and margin, baked in at capture) on the host side only: the graph's
+  // parameter node writes lr to the device (set_graph_params)
+  ctx->h_lr[0] = lr;
+  ctx->h_lr[1] = tc.margin;
   const int cur = ctx->cur, nxt = 1 - cur;
   sg.cur = cur;
   sg.nxt = nxt;
@@ -976,6 +1058,7 @@ StagedEpoch stage_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_tra
     ctx->slots[cur].key = pk;
   }
   if (is_mult(cfg) && has_self_loops(ctx)) {
+    set_epoch_params(ctx, tc, lr);                // eager batches read lr from the device
     train_until_degenerate(ctx, es, epoch, cur);  // always throws
   }
   // Speculatively build epoch + 1's plan (same data and schedule) alongside,
@@ -989,7 +1072,7 @@ StagedEpoch stage_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_tra
     sg.eager += kernel_launches() - before;
     ctx->perm_key[nxt] = pk1;
   }
-  set_slot_seed(ctx, 2 + cur, epoch_seed(tc.seed, epoch + 2));
+  ctx->h_seed[2 + cur] = epoch_seed(tc.seed, epoch + 2);  // written by the graph's parameter node
   ctx->perm_key[cur].clear();
   ctx->slots[nxt].key.clear();
   // Margin is baked into the forward launches, so it is part of the graph key.
@@ -998,6 +1081,8 @@ StagedEpoch stage_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_tra
     SKG_CUDA(cudaStreamSynchronize(ctx->stream));  // margin in h_lr[1] is read at capture
     capture_epoch_graph(ctx, es, cur);
     ctx->graph_keys[cur] = gk;
+  } else {
+    set_graph_params(ctx, cur);
   }
   sg.next_key = pk1;
   sg.perm_key = plan_key(ctx, es, tc, epoch + 2);
@@ -1646,7 +1731,8 @@ struct skg::HostNarrow {
   int nt = 1;
   // job
   const int64_t* src[5] = {};
-  int32_t* dst = nullptr;
+  void* dst = nullptr;
+  bool w16 = false;  // ids fit 16 bits (every table <= 65536 rows): uint16 wire format
   int64_t m = 0, L = 0, n_ent = 0, n_rel = 0;
   std::atomic<int> wave_done[kWaves];
   std::atomic<uint32_t> bad[3];
@@ -1680,19 +1766,26 @@ struct skg::HostNarrow {
     }
   }
   void work(int t) {
+    if (w16)
+      work_t<uint16_t>(t);
+    else
+      work_t<int32_t>(t);
+  }
+  template <typename D>
+  void work_t(int t) {
     for (int w = 0; w < kWaves; ++w) {
       const int64_t a = std::min<int64_t>(m, w * L), b = std::min<int64_t>(m, a + L), lw = b - a;
       const int64_t i0 = a + lw * t / nt, i1 = a + lw * (t + 1) / nt;
-      int32_t* base = dst + 5 * a;
+      D* base = static_cast<D*>(dst) + 5 * a;
       for (int k = 0; k < 5; ++k) {
         const int64_t* s = src[k];
-        int32_t* d = base + k * lw - a;
+        D* d = base + k * lw - a;
         const int64_t lim = k == 1 ? n_rel : n_ent;
         bool any = false;
         for (int64_t i = i0; i < i1; ++i) {  // vectorizable: narrow and flag, the index search only on a miss
           const int64_t v = s[i];
           any |= static_cast<uint64_t>(v) >= static_cast<uint64_t>(lim);
-          d[i] = static_cast<int32_t>(v);
+          d[i] = static_cast<D>(v);
         }
         if (any)
           for (int64_t i = i0; i < i1; ++i)
@@ -1704,9 +1797,10 @@ struct skg::HostNarrow {
       wave_done[w].fetch_add(1, std::memory_order_release);
     }
   }
-  void start(const int64_t* const* s, int32_t* d, int64_t mm, int64_t ne, int64_t nr) {
+  void start(const int64_t* const* s, void* d, bool narrow16, int64_t mm, int64_t ne, int64_t nr) {
     for (int k = 0; k < 5; ++k) src[k] = s[k];
     dst = d;
+    w16 = narrow16;
     m = mm;
     L = (mm + kWaves - 1) / kWaves;
     n_ent = ne;
@@ -1729,7 +1823,8 @@ namespace {
 void destroy_host_narrow(skg::HostNarrow* h) { delete h; }
 
 // Compare the narrowed (wave-major) ids with the device ids the epoch used.
-__global__ void spec_check32_kernel(const int32_t* __restrict__ st, int64_t m, int64_t L,
+template <typename S>
+__global__ void spec_check32_kernel(const S* __restrict__ st, int64_t m, int64_t L,
                                     const int32_t* __restrict__ H, const int32_t* __restrict__ Rl,
                                     const int32_t* __restrict__ T, const int32_t* __restrict__ NH,
                                     const int32_t* __restrict__ NT, uint32_t* __restrict__ flags) {
@@ -1737,14 +1832,17 @@ __global__ void spec_check32_kernel(const int32_t* __restrict__ st, int64_t m, i
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t a = (i / L) * L, lw = min(L, m - a);
-    const int32_t* b = st + 5 * a + (i - a);
-    diff |= (__ldcs(b) != __ldg(H + i)) | (__ldcs(b + lw) != __ldg(Rl + i)) | (__ldcs(b + 2 * lw) != __ldg(T + i)) |
-            (__ldcs(b + 3 * lw) != __ldg(NH + i)) | (__ldcs(b + 4 * lw) != __ldg(NT + i));
+    const S* b = st + 5 * a + (i - a);
+    diff |= (static_cast<int32_t>(__ldcs(b)) != __ldg(H + i)) | (static_cast<int32_t>(__ldcs(b + lw)) != __ldg(Rl + i)) |
+            (static_cast<int32_t>(__ldcs(b + 2 * lw)) != __ldg(T + i)) |
+            (static_cast<int32_t>(__ldcs(b + 3 * lw)) != __ldg(NH + i)) |
+            (static_cast<int32_t>(__ldcs(b + 4 * lw)) != __ldg(NT + i));
   }
   if (__any_sync(kFull, diff) && (threadIdx.x & 31) == 0) atomicOr(flags + 3, 1u);
 }
 
-__global__ void adopt_staged32_kernel(const int32_t* __restrict__ st, int64_t m, int64_t L, int32_t* __restrict__ H,
+template <typename S>
+__global__ void adopt_staged32_kernel(const S* __restrict__ st, int64_t m, int64_t L, int32_t* __restrict__ H,
                                       int32_t* __restrict__ Rl, int32_t* __restrict__ T, int32_t* __restrict__ NH,
                                       int32_t* __restrict__ NT) {
   int32_t* dst[5] = {H, Rl, T, NH, NT};
@@ -1752,7 +1850,7 @@ __global__ void adopt_staged32_kernel(const int32_t* __restrict__ st, int64_t m,
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t a = (i / L) * L, lw = min(L, m - a);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) dst[k][i] = st[5 * a + k * lw + (i - a)];
+    for (int k = 0; k < 5; ++k) dst[k][i] = static_cast<int32_t>(st[5 * a + k * lw + (i - a)]);
   }
 }
 
@@ -1780,10 +1878,23 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     return v && v[0] == '1';
   }();
   const bool narrowed = !i64 && m > 0;
+  // wire format of the narrowed ids: uint16 when every id fits (C1-C3 tables),
+  // else int32 (range-checked on the host either way)
+  static const bool no16 = [] {
+    const char* v = std::getenv("SKG_SPEC_NO16");
+    return v && v[0] == '1';
+  }();
+  const bool w16 = narrowed && !no16 && ctx->tN <= 65536 && ctx->tR <= 65536;
+  const int64_t wsz = w16 ? 2 : 4;
   if (narrowed) {
     if (!ctx->narrow) {
+      // at most half the host's cores: a wave waits for its slowest thread, and
+      // with every core busy one preempted thread costs a scheduler timeslice
+      // (measured: 15 threads on 16 cores gave 1.1-1.4 ms step outliers, 8 none)
       const unsigned hc = std::thread::hardware_concurrency();
-      ctx->narrow = new HostNarrow(static_cast<int>(std::max(1u, std::min(16u, hc > 2 ? hc - 1 : 1u))));
+      int nt = static_cast<int>(std::max(1u, std::min(8u, hc / 2)));
+      if (const char* e = std::getenv("SKG_NARROW_THREADS")) nt = std::max(1, std::atoi(e));
+      ctx->narrow = new HostNarrow(nt);
     }
     if (ctx->h_stage32_cap < 5 * m) {
       if (ctx->h_stage32) cudaFreeHost(ctx->h_stage32);
@@ -1793,23 +1904,35 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     }
     ctx->stage_i32.ensure(5 * m + 1);
   }
+  bool in_epoch = true;
+  // until the flags are read back, the check counts as a miss (changed data:
+  // roll back and adopt), never as a stale hit
+  ctx->h_spec[0] = ctx->h_spec[1] = ctx->h_spec[2] = 0xFFFFFFFFu;
+  ctx->h_spec[3] = 1u;
   const std::function<void()> upload = [&]() {
     SKG_CUDA(cudaMemsetAsync(ctx->spec_flags.p, 0xFF, sizeof(uint32_t) * 3, ctx->up));
     SKG_CUDA(cudaMemsetAsync(ctx->spec_flags.p + 3, 0, sizeof(uint32_t), ctx->up));
     if (narrowed) {
       HostNarrow& hn = *ctx->narrow;
-      hn.start(src, ctx->h_stage32, m, ctx->tN, ctx->tR);
+      hn.start(src, ctx->h_stage32, w16, m, ctx->tN, ctx->tR);
+      char* hst = reinterpret_cast<char*>(ctx->h_stage32);
+      char* dst = reinterpret_cast<char*>(ctx->stage_i32.p);
       for (int w = 0; w < kWaves; ++w) {
         const int64_t a = std::min<int64_t>(m, w * hn.L), b = std::min<int64_t>(m, a + hn.L);
         hn.wait_wave(w);
         if (b > a)
-          SKG_CUDA(cudaMemcpyAsync(ctx->stage_i32.p + 5 * a, ctx->h_stage32 + 5 * a, sizeof(int32_t) * 5 * (b - a),
-                                   cudaMemcpyHostToDevice, ctx->up));
+          SKG_CUDA(cudaMemcpyAsync(dst + wsz * 5 * a, hst + wsz * 5 * a, wsz * 5 * (b - a), cudaMemcpyHostToDevice,
+                                   ctx->up));
       }
-      ctx->upload_bytes += static_cast<int64_t>(sizeof(int32_t)) * 5 * m;
-      spec_check32_kernel<<<static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms)), 256, 0,
-                            ctx->up>>>(ctx->stage_i32.p, m, hn.L, ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p,
-                                       ctx->spec_flags.p);
+      ctx->upload_bytes += wsz * 5 * m;
+      const unsigned g = static_cast<unsigned>(std::min<int64_t>(grid_for(m), 2LL * ctx->num_sms));
+      if (w16)
+        spec_check32_kernel<<<g, 256, 0, ctx->up>>>(reinterpret_cast<const uint16_t*>(ctx->stage_i32.p), m, hn.L,
+                                                    ctx->H.p, ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p,
+                                                    ctx->spec_flags.p);
+      else
+        spec_check32_kernel<<<g, 256, 0, ctx->up>>>(ctx->stage_i32.p, m, hn.L, ctx->H.p, ctx->Rl.p, ctx->T.p,
+                                                    ctx->NH.p, ctx->NT.p, ctx->spec_flags.p);
     } else {
       for (int k = 0; k < 5; ++k)
         SKG_CUDA(cudaMemcpyAsync(ctx->stage_i64.p + k * m, src[k], sizeof(int64_t) * m, cudaMemcpyHostToDevice, ctx->up));
@@ -1823,8 +1946,11 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     // the epoch's own final sync also covers the check: its flags are read
     // back on the main stream after the upload's event
     SKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->up_ev, 0));
-    SKG_CUDA(cudaMemcpyAsync(ctx->h_spec, ctx->spec_flags.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost,
-                             ctx->stream));
+    if (in_epoch)  // finish_epoch's publish kernel copies the flags with the losses
+      ctx->pub_spec = ctx->spec_flags.p;
+    else
+      SKG_CUDA(cudaMemcpyAsync(ctx->h_spec, ctx->spec_flags.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost,
+                               ctx->stream));
     launched = true;
   };
   // parameters the epoch mutates: [entity; relation], proj, normals
@@ -1847,6 +1973,8 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   } catch (...) {
     failed = std::current_exception();
   }
+  ctx->pub_spec = nullptr;
+  in_epoch = false;
   if (!launched) upload();  // the epoch failed before its launch: still check the upload
   const auto t2 = clk::now();
   SKG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1882,7 +2010,11 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     throw ShapeError("triple " + std::to_string(f[1]) + ": relation id out of range");
   }
   // adopt the uploaded ids (data changed, or the negatives are invalid)
-  if (narrowed)
+  if (narrowed && w16)
+    adopt_staged32_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(reinterpret_cast<const uint16_t*>(ctx->stage_i32.p),
+                                                                m, ctx->narrow->L, ctx->H.p, ctx->Rl.p, ctx->T.p,
+                                                                ctx->NH.p, ctx->NT.p);
+  else if (narrowed)
     adopt_staged32_kernel<<<grid_for(m), 256, 0, ctx->stream>>>(ctx->stage_i32.p, m, ctx->narrow->L, ctx->H.p,
                                                                 ctx->Rl.p, ctx->T.p, ctx->NH.p, ctx->NT.p);
   else

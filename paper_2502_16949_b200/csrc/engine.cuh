@@ -134,6 +134,16 @@ struct skg_ctx {
   cudaEvent_t fork_up_ev = nullptr;
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   std::string graph_keys[2];
+  // The epoch graph's first node writes this epoch's lr and the seed of the
+  // permutation it shuffles (epoch + 2) to the device; its kernel arguments
+  // are updated in the instantiated graph before each launch (no H2D copies
+  // ahead of the graph). graph_src keeps the captured graph the node belongs to.
+  cudaGraph_t graph_src[2] = {nullptr, nullptr};
+  cudaGraphNode_t param_node[2] = {nullptr, nullptr};
+  // finish_epoch: one kernel writes the batch losses, the error words and (in
+  // a speculative epoch) the upload check's flags straight into the pinned
+  // host buffers (mapped under UVA) instead of three D2H copies.
+  const uint32_t* pub_spec = nullptr;
   int64_t graph_launches_k[2] = {0, 0};
   int64_t last_launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

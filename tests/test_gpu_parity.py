@@ -477,12 +477,14 @@ def _deferred_body(eng, orc32, cfg, tc_e, tc_o, st, P, h, rel, t, nh, nt, n, r):
     assert np.array_equal(gh, oh) and np.array_equal(gt, ot)
 
 
-def test_deferred_reupload_large_narrowing(eng, orc32):
+@pytest.mark.parametrize("n,wire", [(20000, 2), (70000, 4)])
+def test_deferred_reupload_large_narrowing(eng, orc32, n, wire):
     """Host-narrowed deferred uploads at a size that spreads the five id arrays over
     every narrowing thread and all four DMA waves: an identical re-upload keeps the
     speculative epoch (hit), one changed negative id in the last wave is detected
-    (miss) and retrained; tables stay bitwise the oracle's."""
-    n, r, d = 20000, 60, 8
+    (miss) and retrained; tables stay bitwise the oracle's. Ids travel as uint16
+    when every table has at most 65536 rows, else as int32."""
+    r, d = 60, 8
     h, rel, t = orc32.synthetic_train(n, r, 220000, 11)
     m = len(h)
     st = orc32.init_store("transe", n, r, d, d, 11)
@@ -511,6 +513,6 @@ def test_deferred_reupload_large_narrowing(eng, orc32):
             assert np.array_equal(ge, st.entity) and np.array_equal(gr, st.relation), ep
         hits1, miss1 = eng.upload_stats()
         assert (hits1 - hits0, miss1 - miss0) == (1, 1)
-        assert eng.upload_bytes() - bytes0 == 2 * 5 * m * 4  # int32 on the wire
+        assert eng.upload_bytes() - bytes0 == 2 * 5 * m * wire  # uint16 / int32 on the wire
     finally:
         eng.set_deferred_uploads(False)
