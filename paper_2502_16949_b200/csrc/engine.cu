@@ -685,15 +685,17 @@ void prepare_epoch(skg_ctx* ctx, const skg_model_config& cfg, const skg_train_co
     if (ctx->dp) ctx->dp_grad.ensure(ctx->N * ctx->de + ctx->R * ctx->dr + ctx->proj.n + ctx->normals.n + 2);
   }
   for (auto& p : ctx->perm) p.ensure(ctx->M + 1);
+  static const bool th_no_plan = std::getenv("SKG_TH_NO_PLAN") != nullptr;
+  static const bool tr_no_plan = std::getenv("SKG_TR_NO_PLAN") != nullptr;
   // TransH relation tiles precomputed with the plan (single device, tile kernel, bounded size)
   const int64_t th_mt = transh_tile_plan_tiles(es.B, ctx->R);
   const bool th_on = (es.kind == kTransH_L2 || es.kind == kTransH_L1) && !ctx->dp && !ctx->shard &&
                      transh_tiles_supported(static_cast<int>(ctx->de), static_cast<int>(ctx->dr), ctx->R) &&
-                     es.nb * th_mt * 656 <= (512ll << 20) && std::getenv("SKG_TH_NO_PLAN") == nullptr;
+                     es.nb * th_mt * 656 <= (512ll << 20) && !th_no_plan;
   // TransR relation tiles precomputed with the plan (single device, tcgen05 step)
   const bool tr_on = (es.kind == kTransR_L2 || es.kind == kTransR_L1) && !ctx->dp && !ctx->shard &&
                      transr_train_tc_supported(static_cast<int>(ctx->de), static_cast<int>(ctx->dr)) &&
-                     std::getenv("SKG_TR_NO_PLAN") == nullptr;
+                     !tr_no_plan;
   for (auto& sl : ctx->slots) {
     sl.order.ensure(ctx->M + 1);
     if (!ctx->shard) sl.plan.reserve(6 * (ctx->dp ? es.Mg : ctx->M) + 6, es.nb);
