@@ -1705,6 +1705,49 @@ __global__ void copy_kernel(const float* __restrict__ src, float* __restrict__ d
   for (int64_t i = done + tid; i < n; i += stride) dst[i] = src[i];
 }
 
+// Up to three float copies in one launch (blockIdx.y = segment): the
+// speculative epoch's parameter snapshot / restore of tables, proj, normals.
+struct CopySegs {
+  const float* src[3];
+  float* dst[3];
+  int64_t n[3];
+};
+__global__ void copy_segs_kernel(const CopySegs c) {
+  const int k = blockIdx.y;
+  const float* __restrict__ src = c.src[k];
+  float* __restrict__ dst = c.dst[k];
+  const int64_t n = c.n[k], n4 = n >> 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    for (int64_t i = tid; i < n4; i += stride)
+      reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+    done = 4 * n4;
+  }
+  for (int64_t i = done + tid; i < n; i += stride) dst[i] = src[i];
+}
+
+void copy_float_segs(const float* const* src, float* const* dst, const int64_t* n, int num_sms, cudaStream_t s) {
+  CopySegs c{};
+  int k = 0;
+  int64_t most = 0;
+  for (int i = 0; i < 3; ++i)
+    if (n[i] > 0) {
+      c.src[k] = src[i];
+      c.dst[k] = dst[i];
+      c.n[k] = n[i];
+      most = std::max(most, n[i]);
+      ++k;
+    }
+  if (k == 0) return;
+  const int64_t blocks = std::min<int64_t>((most / 4 + 255) / 256 + 1, 8LL * num_sms);
+  copy_segs_kernel<<<dim3(static_cast<unsigned>(blocks), k), 256, 0, s>>>(c);
+  count_launch();
+  SKG_LAUNCH_CHECK();
+}
+
 void copy_floats(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = std::min<int64_t>((n / 4 + 255) / 256 + 1, 8LL * num_sms);
@@ -1964,9 +2007,12 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   // batch 0 waits for snap_ev before writing any parameter
   SKG_CUDA(cudaEventRecord(ctx->fork_up_ev, ctx->stream));
   SKG_CUDA(cudaStreamWaitEvent(ctx->up, ctx->fork_up_ev, 0));
-  copy_floats(ctx->tables.p, ctx->backup.p + ob, nt, ctx->num_sms, ctx->up);
-  copy_floats(ctx->proj.p, ctx->backup.p + op, np, ctx->num_sms, ctx->up);
-  copy_floats(ctx->normals.p, ctx->backup.p + on, nn, ctx->num_sms, ctx->up);
+  const float* live[3] = {ctx->tables.p, ctx->proj.p, ctx->normals.p};
+  float* live_w[3] = {ctx->tables.p, ctx->proj.p, ctx->normals.p};
+  const float* saved[3] = {ctx->backup.p + ob, ctx->backup.p + op, ctx->backup.p + on};
+  float* saved_w[3] = {ctx->backup.p + ob, ctx->backup.p + op, ctx->backup.p + on};
+  const int64_t lens[3] = {nt, np, nn};
+  copy_float_segs(live, saved_w, lens, ctx->num_sms, ctx->up);
   SKG_CUDA(cudaEventRecord(ctx->snap_ev, ctx->up));
   const auto t1 = clk::now();
   std::exception_ptr failed;
@@ -1997,9 +2043,7 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     return;
   }
   ++ctx->spec_misses;
-  copy_floats(ctx->backup.p + ob, ctx->tables.p, nt, ctx->num_sms, ctx->stream);
-  copy_floats(ctx->backup.p + op, ctx->proj.p, np, ctx->num_sms, ctx->stream);
-  copy_floats(ctx->backup.p + on, ctx->normals.p, nn, ctx->num_sms, ctx->stream);
+  copy_float_segs(saved, live_w, lens, ctx->num_sms, ctx->stream);
   for (auto& sl : ctx->slots) sl.key.clear();
   for (auto& k : ctx->perm_key) k.clear();
   ctx->has_neg = false;
