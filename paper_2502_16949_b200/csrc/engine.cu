@@ -376,6 +376,7 @@ void enqueue_epoch(skg_ctx* ctx, const EpochShape& es, std::vector<cudaEvent_t>*
 // into plan slot `slot`. Depends only on the seed, the triples and the
 // negatives, so the next epoch's plan can be built while this one trains.
 void copy_floats(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s);
+void snapshot_params(skg_ctx* ctx, bool restore, cudaStream_t s);
 
 void destroy_host_narrow(skg::HostNarrow* h);
 
@@ -491,7 +492,12 @@ void enqueue_batches(skg_ctx* ctx, const EpochShape& es, int slot, cudaStream_t 
     snap_waited = true;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     SKG_CUDA(cudaStreamIsCapturing(s, &cs));
-    SKG_CUDA(cudaStreamWaitEvent(s, ctx->snap_ev, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+    // in a speculative graph the snapshot branch is part of this capture (an edge), otherwise an
+    // external wait on the last record (a snapshot enqueued before the launch, or none)
+    if (cs == cudaStreamCaptureStatusActive && ctx->spec_graph)
+      SKG_CUDA(cudaStreamWaitEvent(s, ctx->snap_cap_ev, 0));
+    else
+      SKG_CUDA(cudaStreamWaitEvent(s, ctx->snap_ev, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
   };
   for (int64_t b = 0; b < nb_run; ++b) {
     const int64_t lo = b * es.B;
@@ -764,7 +770,7 @@ std::string graph_key(skg_ctx* ctx, const EpochShape& es, float margin) {
                  ctx->slots[1].th_pos.p, ctx->slots[0].th_info.p, ctx->slots[1].th_info.p, ctx->slots[0].th_on,
                  ctx->slots[0].tr_seg.p, ctx->slots[1].tr_seg.p, ctx->slots[0].tr_p0.p, ctx->slots[1].tr_p0.p,
                  ctx->slots[0].tr_total.p, ctx->slots[1].tr_total.p, ctx->slots[0].tr_segtiles.p,
-                 ctx->slots[1].tr_segtiles.p, ctx->slots[0].tr_on);
+                 ctx->slots[1].tr_segtiles.p, ctx->slots[0].tr_on, ctx->spec_graph, ctx->backup.p);
 }
 
 // Identity of an epoch plan: everything it depends on.
@@ -909,6 +915,12 @@ void capture_epoch_graph(skg_ctx* ctx, const EpochShape& es, int cur) {
     epoch_params_kernel<<<1, 1, 0, ctx->stream>>>(epoch_params_of(ctx, cur));
     count_launch();
     SKG_LAUNCH_CHECK();
+    if (ctx->spec_graph) {  // speculative epoch: parameter snapshot on a branch (joined at batch 0's first write)
+      SKG_CUDA(cudaEventRecord(ctx->fork_up_ev, ctx->stream));
+      SKG_CUDA(cudaStreamWaitEvent(ctx->up, ctx->fork_up_ev, 0));
+      snapshot_params(ctx, false, ctx->up);
+      SKG_CUDA(cudaEventRecord(ctx->snap_cap_ev, ctx->up));
+    }
     SKG_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
     SKG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
     SKG_CUDA(cudaStreamWaitEvent(ctx->side2, ctx->fork_ev, 0));
@@ -1378,6 +1390,7 @@ skg_status skg_create(int device, skg_ctx** out) {
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
     SKG_CUDA(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->snap_ev, cudaEventDisableTiming));
+    SKG_CUDA(cudaEventCreateWithFlags(&ctx->snap_cap_ev, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->fork_up_ev, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->join2_ev, cudaEventDisableTiming));
     SKG_CUDA(cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
@@ -1423,6 +1436,7 @@ void skg_destroy(skg_ctx* ctx) {
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
   if (ctx->snap_ev) cudaEventDestroy(ctx->snap_ev);
+  if (ctx->snap_cap_ev) cudaEventDestroy(ctx->snap_cap_ev);
   if (ctx->fork_up_ev) cudaEventDestroy(ctx->fork_up_ev);
   if (ctx->join2_ev) cudaEventDestroy(ctx->join2_ev);
   if (ctx->aux_fork) cudaEventDestroy(ctx->aux_fork);
@@ -1748,6 +1762,21 @@ void copy_float_segs(const float* const* src, float* const* dst, const int64_t* 
   SKG_LAUNCH_CHECK();
 }
 
+// The parameters a speculative epoch mutates ([entity; relation], proj,
+// normals) to / from ctx->backup (16-byte aligned sections).
+void snapshot_params(skg_ctx* ctx, bool restore, cudaStream_t s) {
+  const int64_t nt = ctx->tables.n, np = ctx->proj.n, nn = ctx->normals.n;
+  const int64_t op = (nt + 3) / 4 * 4, on = op + (np + 3) / 4 * 4;
+  ctx->backup.ensure(on + nn + 4);
+  float* live[3] = {ctx->tables.p, ctx->proj.p, ctx->normals.p};
+  float* saved[3] = {ctx->backup.p, ctx->backup.p + op, ctx->backup.p + on};
+  const int64_t lens[3] = {nt, np, nn};
+  if (restore)
+    copy_float_segs(saved, live, lens, ctx->num_sms, s);
+  else
+    copy_float_segs(live, saved, lens, ctx->num_sms, s);
+}
+
 void copy_floats(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = std::min<int64_t>((n / 4 + 255) / 256 + 1, 8LL * num_sms);
@@ -1998,22 +2027,23 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
                                ctx->stream));
     launched = true;
   };
-  // parameters the epoch mutates: [entity; relation], proj, normals
-  const int64_t nt = ctx->tables.n, np = ctx->proj.n, nn = ctx->normals.n;
-  ctx->backup.ensure(nt + np + nn + 4);
-  const int64_t ob = 0, op = (nt + 3) / 4 * 4, on = op + (np + 3) / 4 * 4;  // 16-byte aligned sections
-  ctx->backup.ensure(on + nn + 4);
-  // snapshot on the upload stream: the epoch graph starts alongside and its
-  // batch 0 waits for snap_ev before writing any parameter
-  SKG_CUDA(cudaEventRecord(ctx->fork_up_ev, ctx->stream));
-  SKG_CUDA(cudaStreamWaitEvent(ctx->up, ctx->fork_up_ev, 0));
-  const float* live[3] = {ctx->tables.p, ctx->proj.p, ctx->normals.p};
-  float* live_w[3] = {ctx->tables.p, ctx->proj.p, ctx->normals.p};
-  const float* saved[3] = {ctx->backup.p + ob, ctx->backup.p + op, ctx->backup.p + on};
-  float* saved_w[3] = {ctx->backup.p + ob, ctx->backup.p + op, ctx->backup.p + on};
-  const int64_t lens[3] = {nt, np, nn};
-  copy_float_segs(live, saved_w, lens, ctx->num_sms, ctx->up);
-  SKG_CUDA(cudaEventRecord(ctx->snap_ev, ctx->up));
+  // Parameter snapshot: a branch of the epoch graph itself (spec_graph: no
+  // launches ahead of the graph), taken at the graph's start; batch 0 waits
+  // for it before writing any parameter. Sharded contexts and the
+  // multiplicative models (whose degenerate-batch path trains eagerly before
+  // any graph launch, then throws) snapshot ahead of the launch.
+  {
+    const int64_t nt = ctx->tables.n, np = ctx->proj.n, nn = ctx->normals.n;  // backup sized before any capture
+    ctx->backup.ensure((nt + 3) / 4 * 4 + (np + 3) / 4 * 4 + nn + 4);
+  }
+  const bool in_graph_snapshot = ctx->shard == nullptr && !is_mult(cfg);
+  ctx->spec_graph = in_graph_snapshot;
+  if (!in_graph_snapshot) {
+    SKG_CUDA(cudaEventRecord(ctx->fork_up_ev, ctx->stream));
+    SKG_CUDA(cudaStreamWaitEvent(ctx->up, ctx->fork_up_ev, 0));
+    snapshot_params(ctx, false, ctx->up);
+    SKG_CUDA(cudaEventRecord(ctx->snap_ev, ctx->up));
+  }
   const auto t1 = clk::now();
   std::exception_ptr failed;
   try {
@@ -2021,6 +2051,9 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
   } catch (...) {
     failed = std::current_exception();
   }
+  ctx->spec_graph = false;
+  // an in-graph snapshot exists iff the graph ran, i.e. the upload was enqueued after its launch
+  const bool snapshot_taken = !in_graph_snapshot || launched;
   ctx->pub_spec = nullptr;
   in_epoch = false;
   if (!launched) upload();  // the epoch failed before its launch: still check the upload
@@ -2043,7 +2076,7 @@ void train_epoch_speculative(skg_ctx* ctx, const skg_model_config& cfg, const sk
     return;
   }
   ++ctx->spec_misses;
-  copy_float_segs(saved, live_w, lens, ctx->num_sms, ctx->stream);
+  if (snapshot_taken) snapshot_params(ctx, true, ctx->stream);  // else the epoch never ran: nothing to undo
   for (auto& sl : ctx->slots) sl.key.clear();
   for (auto& k : ctx->perm_key) k.clear();
   ctx->has_neg = false;

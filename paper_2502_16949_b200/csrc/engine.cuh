@@ -131,6 +131,7 @@ struct skg_ctx {
   cudaStream_t side2 = nullptr;
   cudaEvent_t join2_ev = nullptr;
   cudaEvent_t snap_ev = nullptr;     // speculative epoch: parameter snapshot done (waited by batch 0's first write)
+  cudaEvent_t snap_cap_ev = nullptr; // the same inside a speculative graph (an event used in a capture stays there)
   cudaEvent_t fork_up_ev = nullptr;
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   std::string graph_keys[2];
@@ -144,6 +145,9 @@ struct skg_ctx {
   // a speculative epoch) the upload check's flags straight into the pinned
   // host buffers (mapped under UVA) instead of three D2H copies.
   const uint32_t* pub_spec = nullptr;
+  // A speculative epoch's graph snapshots the parameters itself (a branch at
+  // the graph's start, batch 0's first parameter write waits for it).
+  bool spec_graph = false;
   int64_t graph_launches_k[2] = {0, 0};
   int64_t last_launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
