@@ -477,7 +477,7 @@ def _deferred_body(eng, orc32, cfg, tc_e, tc_o, st, P, h, rel, t, nh, nt, n, r):
     assert np.array_equal(gh, oh) and np.array_equal(gt, ot)
 
 
-@pytest.mark.parametrize("n,wire", [(20000, 2), (70000, 4)])
+@pytest.mark.parametrize("n,wire", [(20000, 2), (65536, 2), (65537, 4), (70000, 4)])
 def test_deferred_reupload_large_narrowing(eng, orc32, n, wire):
     """Host-narrowed deferred uploads at a size that spreads the five id arrays over
     every narrowing thread and all four DMA waves: an identical re-upload keeps the
@@ -492,6 +492,7 @@ def test_deferred_reupload_large_narrowing(eng, orc32, n, wire):
     tc_e = TrainConfig.make(batch_size=8192, seed=4, lr=0.05)
     tc_o = orc32.train_config(batch_size=8192, seed=4, lr=0.05)
     nh, nt = orc32.negative_sample(h, rel, t, n, r, 2)
+    nh[m // 2] = n - 1  # the largest id the wire format must carry (65535 at n = 65536)
     P = [_pinned(x) for x in (h, rel, t, nh, nt)]
     eng.store_upload(cfg, st.entity, st.relation)
     eng.set_triples(*P[:3], n, r)
