@@ -114,6 +114,11 @@ struct Chunk {
 // shared memory so that lane j then sums row j in the reference's order.
 template <int KIND, bool TRAIN, int VEC>
 __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a) {
+#ifdef SKG_MULT_NOPAIR
+  constexpr bool kPairRounds = false;
+#else
+  constexpr bool kPairRounds = TRAIN;
+#endif
   using U = Unit<KIND>;
   using T = typename U::T;
   extern __shared__ float smem[];
@@ -165,12 +170,15 @@ __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a)
     bool badrow = false;  // lane j: a non-finite term in row j (gradient would be non-finite)
 #pragma unroll 1
     for (int j0 = 0; j0 < 16; j0 += 4) {
-      int hj[4], tj[4], rj[4];
+      // a round's four rows: TRAIN, two (pos, neg) pairs {p, p + 8, p + 1, p + 9}
+      // (a pair shares its relation row: loaded once); SCORE, rows j0 .. j0 + 3
+      int rowq[4], hj[4], tj[4], rj[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        hj[q] = __shfl_sync(kFull, h, j0 + q);
-        tj[q] = __shfl_sync(kFull, t, j0 + q);
-        rj[q] = __shfl_sync(kFull, r, j0 + q);
+        rowq[q] = kPairRounds ? (j0 >> 1) + (q >> 1) + (q & 1) * 8 : j0 + q;
+        hj[q] = __shfl_sync(kFull, h, rowq[q]);
+        tj[q] = __shfl_sync(kFull, t, rowq[q]);
+        rj[q] = __shfl_sync(kFull, r, rowq[q]);
       }
       bool nf[4] = {false, false, false, false};
       if constexpr (VEC == 4) {
@@ -181,20 +189,21 @@ __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a)
           float4 xh[4], xt[4], xr[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (!((vmask >> (j0 + q)) & 1u)) continue;
+            if (!((vmask >> rowq[q]) & 1u)) continue;
             xh[q] = __ldg(X4 + static_cast<size_t>(hj[q]) * W4 + c);
             xt[q] = __ldg(X4 + static_cast<size_t>(tj[q]) * W4 + c);
-            xr[q] = __ldg(X4 + static_cast<size_t>(N + rj[q]) * W4 + c);
+            if (!kPairRounds || (q & 1) == 0) xr[q] = __ldg(X4 + static_cast<size_t>(N + rj[q]) * W4 + c);
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (!((vmask >> (j0 + q)) & 1u)) continue;
+            if (!((vmask >> rowq[q]) & 1u)) continue;
+            const float4 xrq = (kPairRounds && (q & 1)) ? xr[q - 1] : xr[q];
 #pragma unroll
             for (int k = 0; k < CK::NU; ++k) {
-              const T h1 = CK::get(xh[q], k), t1 = CK::get(xt[q], k), r1 = CK::get(xr[q], k);
+              const T h1 = CK::get(xh[q], k), t1 = CK::get(xt[q], k), r1 = CK::get(xrq, k);
               const float v = U::term(h1, t1, r1, tj[q] < hj[q]);
               nf[q] |= !finite_f(v) || !fin(h1) || !fin(t1) || !fin(r1);
-              rows[(j0 + q) * S + c * CK::NU + k] = v;
+              rows[rowq[q] * S + c * CK::NU + k] = v;
             }
           }
         }
@@ -203,24 +212,24 @@ __global__ void __launch_bounds__(kThreads) mult_forward_kernel(const FwdArgs a)
           T xh[4], xt[4], xr[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (!((vmask >> (j0 + q)) & 1u)) continue;
+            if (!((vmask >> rowq[q]) & 1u)) continue;
             xh[q] = U::load(a.X, hj[q], W, c);
             xt[q] = U::load(a.X, tj[q], W, c);
             xr[q] = U::load(a.X, N + rj[q], W, c);
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            if (!((vmask >> (j0 + q)) & 1u)) continue;
+            if (!((vmask >> rowq[q]) & 1u)) continue;
             const float v = U::term(xh[q], xt[q], xr[q], tj[q] < hj[q]);
             nf[q] |= !finite_f(v) || !fin(xh[q]) || !fin(xt[q]) || !fin(xr[q]);
-            rows[(j0 + q) * S + c] = v;
+            rows[rowq[q] * S + c] = v;
           }
         }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const bool any = __any_sync(kFull, nf[q]);
-        if (lane == j0 + q) badrow = any;
+        if (lane == rowq[q]) badrow = any;
       }
     }
     __syncwarp();
